@@ -1,0 +1,145 @@
+/*
+ * frw_gpu.h -- C ABI of the B200-native FRW / MicroWalk hot path
+ * (libfrwgpu.so, sm_100a).  Plain C: POD in and out, int status codes,
+ * no exceptions, no torch types.  The C++ host layer
+ * (paper_2507_09730_b200/csrc/host, the `frwcap` API mirror) and the ctypes
+ * tests call these entry points; INTEGRATION.md shows the binding a
+ * maintainer of the reference would add.
+ *
+ * The reference (/root/reference/proj) has no C ABI: its boundary is the C++
+ * API in proj/include/frwcap/*.hpp and the pybind11 module _core
+ * (bindings/py_module.cpp).  Each entry point below names the reference
+ * interface it replaces.
+ *
+ * Ownership: one context per device; calls on one context are serialized
+ * by the caller.  Device buffers are owned by the context; host buffers by
+ * the caller.  Functions suffixed _dev take device pointers and run
+ * asynchronously on the context stream; the others take host pointers and
+ * return after the results are copied back.
+ */
+#ifndef FRW_GPU_H
+#define FRW_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct frw_ctx frw_ctx;
+
+/* Status codes; the C++ host maps them back to the reference exception
+ * types (SURVEY.md §8(b) "Error conventions"). */
+enum {
+  FRW_OK = 0,
+  FRW_EINVAL = -1,    /* std::invalid_argument                           */
+  FRW_ECUDA = -2,     /* CUDA runtime failure                            */
+  FRW_ESTEPCAP = -3,  /* std::runtime_error: step cap exceeded           */
+                      /*   (microwalk.cpp:81, :153-155)                  */
+  FRW_EENGULFED = -4, /* EngulfedStart (microwalk.hpp:31-33)             */
+  FRW_ESOLVE = -5,    /* SolveError (sgf.hpp:104-109)                    */
+  FRW_ENOMEM = -6,
+  FRW_EMISS = -7      /* stratified-SGF table miss (handled by the host) */
+};
+
+/* Random streams.  SPLITMIX_PARITY replays the reference stream of each
+ * transit/walk bit for bit (rng.hpp:12-40, SplitMix64(seed, stream));
+ * PHILOX is the production generator, Philox4x32-10 keyed by seed with
+ * counter (transit or walk id, step). */
+enum { FRW_RNG_SPLITMIX_PARITY = 0, FRW_RNG_PHILOX = 1 };
+
+/* ---- context ------------------------------------------------------------ */
+int frw_ctx_create(int device, frw_ctx **out);
+void frw_ctx_destroy(frw_ctx *ctx);
+const char *frw_last_error(const frw_ctx *ctx);
+/* device properties the bench reports (SM count, clock kHz) */
+int frw_device_info(const frw_ctx *ctx, int *sm_count, int *sm_clock_khz,
+                    char *name, int name_len);
+/* optional: run on an existing cudaStream_t (e.g. torch's current stream) */
+int frw_set_stream(frw_ctx *ctx, void *cuda_stream);
+int frw_synchronize(frw_ctx *ctx);
+
+/* ---- single transition cube (configs C1/C2) ----------------------------- */
+/* Replaces constructing a DielectricGrid (geometry.hpp:151-172) for
+ * microwalk_transit(const DielectricGrid&, ...) (microwalk.hpp:77-79).
+ * eps: n^3 relative permittivities, x fastest (idx = (k*n+j)*n+i);
+ * mask: n^3 conductor ids (-1 free) or NULL.  The cube is centred at
+ * (cx,cy,cz) with the given half width.  The upload compiles the grid into
+ * the device stencil table (one 16-bit record id per node plus a table of
+ * distinct step records). */
+int frw_upload_grid(frw_ctx *ctx, int n, const double *eps,
+                    const int32_t *mask, double cx, double cy, double cz,
+                    double half_width);
+
+/* Host-only compilation of a cube into the stencil table (no device calls;
+ * used by the CPU tests to check the threshold construction).  Pass NULL
+ * buffers to query *records first; map has n^3 entries, rec 6*records,
+ * rec_lo 5*records. */
+int frw_grid_compile(int n, const double *eps, const int32_t *mask,
+                     uint16_t *map, uint32_t *rec, uint32_t *rec_lo,
+                     int *records);
+
+/* Upload statistics: distinct step records, bytes staged per CTA in shared
+ * memory, whether the table is shared-memory resident. */
+int frw_grid_info(const frw_ctx *ctx, int *records, int *smem_bytes,
+                  int *smem_resident);
+
+typedef struct {
+  int rng_mode;          /* FRW_RNG_*                                     */
+  uint64_t seed;
+  uint64_t stream_begin; /* transit t uses stream stream_begin + t         */
+  int64_t count;         /* number of transits                             */
+  int32_t step_cap;      /* 0: 1000*n^2, like microwalk.cpp:81             */
+  int32_t blocks;        /* 0: one persistent CTA per SM                   */
+} frw_mw_params;
+
+/* Outputs.  panels/steps/cond are per transit (may be NULL): panel is the
+ * surface panel (surface_panel_of, sgf.cpp:13-30) or -1 for a conductor
+ * exit (cond then holds the conductor id).  hist has 6n^2 bins counting
+ * surface exits.  step_sum/step_sumsq are exact integer moments of the
+ * step count; cond_exits counts conductor exits. */
+typedef struct {
+  int32_t *panels;
+  int32_t *steps;
+  int32_t *cond;
+  uint64_t *hist;
+  uint64_t *step_sum;   /* [1] */
+  uint64_t *step_sumsq; /* [1] */
+  uint64_t *cond_exits; /* [1] */
+} frw_mw_out;
+
+/* Host-pointer batch: runs `count` transits of the uploaded cube
+ * (microwalk_transit, microwalk.cpp:188-197, batched) and copies the
+ * requested outputs back.  hist/moments are overwritten, not accumulated. */
+int frw_microwalk_batch(frw_ctx *ctx, const frw_mw_params *p,
+                        const frw_mw_out *host_out);
+/* Device-pointer batch, asynchronous on the context stream.  hist and the
+ * moments are ACCUMULATED into (zero them first to overwrite). */
+int frw_microwalk_batch_dev(frw_ctx *ctx, const frw_mw_params *p,
+                            const frw_mw_out *dev_out);
+/* the error flag of the last _dev launch (FRW_OK or FRW_ESTEPCAP);
+ * synchronizes the context stream */
+int frw_microwalk_check(frw_ctx *ctx);
+
+/* Events on the context stream for device timing of _dev launches:
+ * elapsed ms between frw_event_record(ctx, 0) and frw_event_record(ctx, 1). */
+int frw_event_record(frw_ctx *ctx, int which);
+int frw_event_elapsed_ms(frw_ctx *ctx, float *ms);
+
+/* Device memory helpers for callers without their own allocator. */
+int frw_dev_alloc(frw_ctx *ctx, size_t bytes, void **ptr);
+int frw_dev_free(frw_ctx *ctx, void *ptr);
+int frw_dev_memset(frw_ctx *ctx, void *ptr, int value, size_t bytes);
+int frw_memcpy_h2d(frw_ctx *ctx, void *dst, const void *src, size_t bytes);
+int frw_memcpy_d2h(frw_ctx *ctx, void *dst, const void *src, size_t bytes);
+
+/* Shared-memory bandwidth probe used as the on-chip roofline denominator:
+ * every SM streams `iters` 128-bit conflict-free LDS per thread; returns
+ * bytes/s measured with device events. */
+int frw_smem_bandwidth_probe(frw_ctx *ctx, int iters, double *bytes_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRW_GPU_H */

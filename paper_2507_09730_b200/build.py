@@ -1,0 +1,89 @@
+"""In-tree build of the native libraries (nvcc/g++, no JIT cache).
+
+* lib/libfrwgpu.so  -- CUDA kernels for sm_100a + the C ABI (include/frw_gpu.h)
+* _core*.so         -- pybind11 module: the C++ `frwcap` API mirror over the
+                       C ABI (bindings/py_module.cpp of the reference)
+The oracle (test infrastructure) is built by oracle/Makefile.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+import sysconfig
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "lib")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_INC = "/usr/local/cuda/include"
+CUDA_LIB = "/usr/local/cuda/lib64"
+
+
+def _run(cmd):
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build_gpu_lib(force=False):
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "libfrwgpu.so")
+    cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    deps = cu + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) \
+        + [os.path.join(ROOT, "include", "frw_gpu.h")]
+    if force or _stale(out, deps):
+        _run([NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
+              "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
+              "-o", out, *cu])
+    return out
+
+
+def build_core(force=False):
+    """pybind11 `_core` (host C++ engine) linked against libfrwgpu.so."""
+    host = sorted(glob.glob(os.path.join(CSRC, "host", "*.cpp")))
+    if not host:
+        return None
+    import pybind11
+    suffix = sysconfig.get_config_var("EXT_SUFFIX")
+    out = os.path.join(PKG, "_core" + suffix)
+    deps = host + glob.glob(os.path.join(CSRC, "host", "*.hpp")) + \
+        glob.glob(os.path.join(CSRC, "host", "frwcap", "*.hpp")) + \
+        [os.path.join(ROOT, "include", "frw_gpu.h"), os.path.join(LIB, "libfrwgpu.so")]
+    if force or _stale(out, deps):
+        json_inc = os.path.join(sysconfig.get_paths()["purelib"],
+                                "include/cudnn_frontend/thirdparty/nlohmann")
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-ffp-contract=off",
+              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(CSRC, "host"),
+              "-I", pybind11.get_include(), "-I", sysconfig.get_paths()["include"],
+              "-I", json_inc, "-I", CUDA_INC, "-o", out, *host,
+              "-L", LIB, "-lfrwgpu", "-Wl,-rpath,$ORIGIN/lib", "-lpthread"])
+    return out
+
+
+def build_oracle(with_ref=None):
+    tgts = ["all"]
+    if with_ref is None:
+        with_ref = os.path.isdir("/root/reference/proj")
+    if with_ref:
+        tgts.append("ref")
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), *tgts])
+
+
+def build_all(force=False):
+    build_gpu_lib(force)
+    build_core(force)
+    build_oracle()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

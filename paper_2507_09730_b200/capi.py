@@ -1,0 +1,230 @@
+"""ctypes binding of the C ABI in include/frw_gpu.h (libfrwgpu.so).
+
+This is the reference-facing plugin boundary for the single-cube MicroWalk
+path (configs C1/C2) as a Python caller sees it; the walk engine is reached
+through the C++ `frwcap` mirror (`paper_2507_09730_b200.frwcap`).  There is
+no CPU fallback: if the CUDA library is missing or no device is present the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libfrwgpu.so")
+
+FRW_OK, FRW_EINVAL, FRW_ECUDA, FRW_ESTEPCAP, FRW_EENGULFED, FRW_ESOLVE = 0, -1, -2, -3, -4, -5
+FRW_ENOMEM, FRW_EMISS = -6, -7
+RNG_SPLITMIX_PARITY, RNG_PHILOX = 0, 1
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_up = C.POINTER(C.c_uint64)
+
+
+class FrwError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class StepCapExceeded(FrwError):
+    pass
+
+
+class EngulfedStart(FrwError):
+    pass
+
+
+class MwParams(C.Structure):
+    _fields_ = [("rng_mode", C.c_int), ("seed", C.c_uint64), ("stream_begin", C.c_uint64),
+                ("count", C.c_int64), ("step_cap", C.c_int32), ("blocks", C.c_int32)]
+
+
+class MwOut(C.Structure):
+    _fields_ = [("panels", C.c_void_p), ("steps", C.c_void_p), ("cond", C.c_void_p),
+                ("hist", C.c_void_p), ("step_sum", C.c_void_p), ("step_sumsq", C.c_void_p),
+                ("cond_exits", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfrwgpu.so (built by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                              "g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.frw_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.frw_ctx_destroy.argtypes = [C.c_void_p]
+        L.frw_last_error.restype = C.c_char_p
+        L.frw_last_error.argtypes = [C.c_void_p]
+        L.frw_device_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.c_char_p, C.c_int]
+        L.frw_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+        L.frw_synchronize.argtypes = [C.c_void_p]
+        L.frw_upload_grid.argtypes = [C.c_void_p, C.c_int, _dp, _ip, C.c_double, C.c_double,
+                                      C.c_double, C.c_double]
+        L.frw_grid_compile.argtypes = [C.c_int, _dp, _ip, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.POINTER(C.c_int)]
+        L.frw_grid_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int)]
+        L.frw_microwalk_batch.argtypes = [C.c_void_p, C.POINTER(MwParams), C.POINTER(MwOut)]
+        L.frw_microwalk_batch_dev.argtypes = [C.c_void_p, C.POINTER(MwParams), C.POINTER(MwOut)]
+        L.frw_microwalk_check.argtypes = [C.c_void_p]
+        L.frw_event_record.argtypes = [C.c_void_p, C.c_int]
+        L.frw_event_elapsed_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+        L.frw_dev_alloc.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
+        L.frw_dev_free.argtypes = [C.c_void_p, C.c_void_p]
+        L.frw_dev_memset.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_size_t]
+        L.frw_memcpy_h2d.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
+        L.frw_memcpy_d2h.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
+        L.frw_smem_bandwidth_probe.argtypes = [C.c_void_p, C.c_int, _dp]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def grid_compile(eps, mask=None):
+    """Host-only stencil-table compilation (no GPU needed)."""
+    L = lib()
+    eps = np.ascontiguousarray(eps, np.float64)
+    n = int(round(len(eps) ** (1 / 3)))
+    m = None if mask is None else np.ascontiguousarray(mask, np.int32)
+    R = C.c_int()
+    rc = L.frw_grid_compile(n, eps.ctypes.data_as(_dp), None if m is None else m.ctypes.data_as(_ip),
+                            None, None, None, C.byref(R))
+    if rc:
+        raise FrwError(rc, "grid_compile failed")
+    mp = np.empty(n ** 3, np.uint16)
+    rec = np.empty((R.value, 6), np.uint32)
+    lo = np.empty((R.value, 5), np.uint32)
+    L.frw_grid_compile(n, eps.ctypes.data_as(_dp), None if m is None else m.ctypes.data_as(_ip),
+                       _p(mp), _p(rec), _p(lo), C.byref(R))
+    return mp, rec, lo
+
+
+class Context:
+    """One device context (frw_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.L = lib()
+        h = C.c_void_p()
+        rc = self.L.frw_ctx_create(device, C.byref(h))
+        if rc:
+            raise FrwError(rc, f"frw_ctx_create({device}) failed (is a CUDA device present?)")
+        self.h = h
+        self.n = None
+        sm, clk = C.c_int(), C.c_int()
+        name = C.create_string_buffer(256)
+        self.L.frw_device_info(self.h, C.byref(sm), C.byref(clk), name, 256)
+        self.sm_count, self.sm_clock_khz, self.name = sm.value, clk.value, name.value.decode()
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.frw_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc == 0:
+            return
+        msg = self.L.frw_last_error(self.h).decode()
+        if rc == FRW_ESTEPCAP:
+            raise StepCapExceeded(rc, msg)
+        if rc == FRW_EENGULFED:
+            raise EngulfedStart(rc, msg)
+        if rc == FRW_EINVAL:
+            raise ValueError(msg)
+        raise FrwError(rc, msg)
+
+    # -- single cube ------------------------------------------------------
+    def upload_grid(self, eps, center=(0.0, 0.0, 0.0), half_width=None, mask=None):
+        eps = np.ascontiguousarray(eps, np.float64)
+        n = int(round(len(eps) ** (1 / 3)))
+        if n ** 3 != len(eps):
+            raise ValueError("eps must hold n^3 values")
+        m = None if mask is None else np.ascontiguousarray(mask, np.int32)
+        hw = n / 2.0 if half_width is None else float(half_width)
+        self._check(self.L.frw_upload_grid(self.h, n, eps.ctypes.data_as(_dp),
+                                           None if m is None else m.ctypes.data_as(_ip),
+                                           float(center[0]), float(center[1]),
+                                           float(center[2]), hw))
+        self.n = n
+
+    def grid_info(self):
+        r, b, s = C.c_int(), C.c_int(), C.c_int()
+        self._check(self.L.frw_grid_info(self.h, C.byref(r), C.byref(b), C.byref(s)))
+        return dict(records=r.value, smem_bytes=b.value, smem_resident=bool(s.value))
+
+    def microwalk_batch(self, count, seed=1, stream_begin=0, rng=RNG_PHILOX, step_cap=0,
+                        per_transit=False, blocks=0):
+        """Host-buffer batch (frw_microwalk_batch)."""
+        n = self.n
+        hist = np.zeros(6 * n * n, np.uint64)
+        s1, s2, cx = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        panel = steps = cond = None
+        if per_transit:
+            panel = np.empty(count, np.int32)
+            steps = np.empty(count, np.int32)
+            cond = np.empty(count, np.int32)
+        p = MwParams(rng, seed, stream_begin, count, step_cap, blocks)
+        o = MwOut(_p(panel), _p(steps), _p(cond), _p(hist), C.cast(C.byref(s1), C.c_void_p),
+                  C.cast(C.byref(s2), C.c_void_p), C.cast(C.byref(cx), C.c_void_p))
+        self._check(self.L.frw_microwalk_batch(self.h, C.byref(p), C.byref(o)))
+        return dict(hist=hist, step_sum=s1.value, step_sumsq=s2.value, cond_exits=cx.value,
+                    panel=panel, steps=steps, cond=cond)
+
+    # device-resident interface (bench value path) -------------------------
+    def alloc(self, nbytes):
+        ptr = C.c_void_p()
+        self._check(self.L.frw_dev_alloc(self.h, nbytes, C.byref(ptr)))
+        return ptr.value
+
+    def free(self, ptr):
+        self._check(self.L.frw_dev_free(self.h, C.c_void_p(ptr)))
+
+    def memset(self, ptr, nbytes):
+        self._check(self.L.frw_dev_memset(self.h, C.c_void_p(ptr), 0, nbytes))
+
+    def d2h(self, dst: np.ndarray, src_ptr):
+        self._check(self.L.frw_memcpy_d2h(self.h, _p(dst), C.c_void_p(src_ptr), dst.nbytes))
+
+    def microwalk_batch_dev(self, count, hist_ptr, mom_ptr, seed=1, stream_begin=0,
+                            rng=RNG_PHILOX, step_cap=0, blocks=0):
+        p = MwParams(rng, seed, stream_begin, count, step_cap, blocks)
+        o = MwOut(None, None, None, hist_ptr, mom_ptr, mom_ptr + 8, mom_ptr + 16)
+        self._check(self.L.frw_microwalk_batch_dev(self.h, C.byref(p), C.byref(o)))
+
+    def check(self):
+        self._check(self.L.frw_microwalk_check(self.h))
+
+    def synchronize(self):
+        self._check(self.L.frw_synchronize(self.h))
+
+    def event_record(self, which):
+        self._check(self.L.frw_event_record(self.h, which))
+
+    def elapsed_ms(self):
+        ms = C.c_float()
+        self._check(self.L.frw_event_elapsed_ms(self.h, C.byref(ms)))
+        return ms.value
+
+    def smem_bandwidth(self, iters=4096):
+        out = C.c_double()
+        self._check(self.L.frw_smem_bandwidth_probe(self.h, iters, C.byref(out)))
+        return out.value

@@ -1,0 +1,64 @@
+// frw_internal.h -- context state shared by the libfrwgpu.so translation
+// units (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "frw_gpu.h"
+
+namespace frw {
+
+// Compiled single-cube stencil table (see mw_grid.cu).
+struct GridTable {
+  int n = 0;
+  int records = 0;
+  int start_idx = 0;
+  bool start_is_conductor = false;
+  double center[3] = {0, 0, 0};
+  double half_width = 0;
+  uint16_t* d_map = nullptr;      // [n^3] node -> record
+  uint32_t* d_rec = nullptr;      // [R][6] T_hi[5], exit codes
+  uint32_t* d_rec_lo = nullptr;   // [R][5] low 21 bits of the thresholds
+  int32_t* d_mask = nullptr;      // [n^3] conductor ids or null
+  size_t map_bytes = 0, rec_bytes = 0;  // padded to 16 B
+};
+
+}  // namespace frw
+
+struct frw_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int sm_count = 0;
+  int sm_clock_khz = 0;
+  int max_smem_optin = 0;
+  char name[256] = {0};
+
+  frw::GridTable grid;
+
+  // scratch for launches
+  unsigned long long* d_ctr = nullptr;  // transit counter
+  int* d_err = nullptr;                 // error flag
+  // host-batch staging
+  uint64_t* d_hist = nullptr;
+  size_t hist_cap = 0;
+  uint64_t* d_mom = nullptr;            // [3]
+  int32_t* d_tr = nullptr;              // per-transit outputs (3 arrays)
+  size_t tr_cap = 0;
+};
+
+#define FRW_CUDA(ctx, call)                                         \
+  do {                                                              \
+    cudaError_t e_ = (call);                                        \
+    if (e_ != cudaSuccess) {                                        \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      return FRW_ECUDA;                                             \
+    }                                                               \
+  } while (0)
+
+int frw_fail(frw_ctx* ctx, int code, const std::string& msg);
