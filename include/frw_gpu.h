@@ -74,11 +74,14 @@ int frw_upload_grid(frw_ctx *ctx, int n, const double *eps,
 
 /* Host-only compilation of a cube into the stencil table (no device calls;
  * used by the CPU tests to check the threshold construction).  Pass NULL
- * buffers to query *records first; map has n^3 entries, rec 6*records,
- * rec_lo 5*records. */
+ * buffers to query *records first; map has n^3 entries, rec `records`
+ * packed words (five 10-bit threshold lanes at bits 11d, exit bits 55..60),
+ * full 5*records exact 53-bit thresholds. */
 int frw_grid_compile(int n, const double *eps, const int32_t *mask,
-                     uint16_t *map, uint32_t *rec, uint32_t *rec_lo,
+                     uint16_t *map, uint64_t *rec, uint64_t *full,
                      int *records);
+/* bytes the last frw_upload_grid copied host->device */
+int frw_grid_h2d_bytes(const frw_ctx *ctx, uint64_t *bytes);
 
 /* Upload statistics: distinct step records, bytes staged per CTA in shared
  * memory, whether the table is shared-memory resident. */

@@ -75,6 +75,7 @@ def lib():
                                        C.POINTER(C.c_int)]
         L.frw_grid_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                     C.POINTER(C.c_int)]
+        L.frw_grid_h2d_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
         L.frw_microwalk_batch.argtypes = [C.c_void_p, C.POINTER(MwParams), C.POINTER(MwOut)]
         L.frw_microwalk_batch_dev.argtypes = [C.c_void_p, C.POINTER(MwParams), C.POINTER(MwOut)]
         L.frw_microwalk_check.argtypes = [C.c_void_p]
@@ -106,11 +107,11 @@ def grid_compile(eps, mask=None):
     if rc:
         raise FrwError(rc, "grid_compile failed")
     mp = np.empty(n ** 3, np.uint16)
-    rec = np.empty((R.value, 6), np.uint32)
-    lo = np.empty((R.value, 5), np.uint32)
+    rec = np.empty(R.value, np.uint64)
+    full = np.empty((R.value, 5), np.uint64)
     L.frw_grid_compile(n, eps.ctypes.data_as(_dp), None if m is None else m.ctypes.data_as(_ip),
-                       _p(mp), _p(rec), _p(lo), C.byref(R))
-    return mp, rec, lo
+                       _p(mp), _p(rec), _p(full), C.byref(R))
+    return mp, rec, full
 
 
 class Context:
@@ -169,7 +170,10 @@ class Context:
     def grid_info(self):
         r, b, s = C.c_int(), C.c_int(), C.c_int()
         self._check(self.L.frw_grid_info(self.h, C.byref(r), C.byref(b), C.byref(s)))
-        return dict(records=r.value, smem_bytes=b.value, smem_resident=bool(s.value))
+        h2d = C.c_uint64()
+        self._check(self.L.frw_grid_h2d_bytes(self.h, C.byref(h2d)))
+        return dict(records=r.value, smem_bytes=b.value, smem_resident=bool(s.value),
+                    h2d_bytes=h2d.value)
 
     def microwalk_batch(self, count, seed=1, stream_begin=0, rng=RNG_PHILOX, step_cap=0,
                         per_transit=False, blocks=0):

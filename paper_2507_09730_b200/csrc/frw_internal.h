@@ -20,8 +20,9 @@ struct GridTable {
   double center[3] = {0, 0, 0};
   double half_width = 0;
   uint16_t* d_map = nullptr;      // [n^3] node -> record
-  uint32_t* d_rec = nullptr;      // [R][6] T_hi[5], exit codes
-  uint32_t* d_rec_lo = nullptr;   // [R][5] low 21 bits of the thresholds
+  uint64_t* d_rec = nullptr;      // [R] packed SWAR record
+  uint64_t* d_full = nullptr;     // [R][5] exact 53-bit thresholds
+  uint64_t h2d_bytes = 0;         // bytes copied by the last upload
   int32_t* d_mask = nullptr;      // [n^3] conductor ids or null
   size_t map_bytes = 0, rec_bytes = 0;  // padded to 16 B
 };

@@ -6,24 +6,28 @@
 //
 // B200 design:
 //  * The cube is compiled once into a stencil table: every node gets a
-//    16-bit id of its distinct "step record" (the six alphas of Eq. 5 are a
-//    function of the node's and its neighbours' permittivities, so a
-//    C2-sized cube has ~3k distinct records for 69k nodes).  A record holds
-//    the five direction thresholds in the integer domain of the 53-bit
-//    uniform: x >= X_d  <=>  fl(x*2^-53*sum) >= acc_d, where acc_d are the
-//    reference's in-order partial sums (microwalk.cpp:105-121).  Comparing
-//    integers against X_d therefore reproduces the reference's f64 scan bit
-//    for bit, with no division and no FP64 on the step path.
-//  * The node map (2 B/node) and the record table (24 B/record: the high
-//    32 bits of each threshold + the exit codes) are staged into shared
-//    memory with one cp.async.bulk per chunk (TMA bulk engine, mbarrier
-//    completion).  The low 21 threshold bits stay in global memory and are
-//    read only on a high-word tie (probability ~5e-10 per step).
+//    16-bit id of its distinct "step record" (the six alphas of Eq. 5 depend
+//    only on the node's and its neighbours' permittivities, so the C2 cube
+//    has ~3k distinct records for 69k nodes).  A record carries the five
+//    direction thresholds in the integer domain of the 53-bit uniform:
+//    x >= X_d  <=>  fl(x*2^-53*sum) >= acc_d, with acc_d the reference's
+//    in-order partial sums (microwalk.cpp:105-121).  Integer comparisons
+//    against X_d reproduce the reference's f64 scan bit for bit, with no
+//    division and no FP64 on the step path.
+//  * On chip a record is ONE 64-bit word: the top 10 bits of the five
+//    thresholds in 11-bit SWAR lanes (guard bit per lane) plus six exit bits.
+//    The step compares the top 10 bits of x against all five lanes with two
+//    64-bit subtractions; only on a 10-bit tie (~0.5% of steps) does a lane
+//    fetch the exact 53-bit thresholds from global memory (L1/L2 resident).
+//  * Node map (2 B/node) + packed records (8 B/record) are staged into shared
+//    memory with cp.async.bulk (TMA bulk-copy engine, mbarrier completion):
+//    162 KB for C2, so every step costs one LDS.U16 + one LDS.64 + one LDS.32
+//    (stride table, broadcast) instead of 7 conflicted loads.
 //  * Persistent CTAs, one walker per thread, refilled from a global transit
 //    counter; lanes step in phase-aligned super-steps of 4 so Philox blocks
-//    and exit bookkeeping are warp-uniform (the "compaction/re-binning" of
-//    live walkers: a lane whose transit ends is re-armed with the next
-//    transit at the next super-step boundary instead of idling).
+//    and exit bookkeeping are warp-uniform (the re-binning of live walkers: a
+//    lane whose transit ends is re-armed with the next transit at the next
+//    super-step boundary instead of idling).
 //  * Histogram (RED.64 to global), exact u64 step moments and optional
 //    per-transit records are fused into the exit path.
 #include <cuda_runtime.h>
@@ -44,6 +48,12 @@ constexpr int kThreads = 1024;
 constexpr int kDirAxis[6] = {0, 0, 1, 1, 2, 2};
 constexpr int kDirSign[6] = {-1, +1, -1, +1, -1, +1};
 
+// SWAR layout of a packed record
+constexpr int kLane = 11;                          // 10-bit threshold + guard
+constexpr uint64_t kOnes = 0x0000100200400801ull;  // 1 in each of the 5 lanes
+constexpr uint64_t kGuard = kOnes << 10;           // guard bit of each lane
+constexpr int kExitShift = 55;                     // six exit bits 55..60
+
 // ---------------------------------------------------------------------------
 // host: compile the grid into node map + step records
 
@@ -57,10 +67,11 @@ struct KeyHash {
   }
 };
 
-// smallest x in [0, 2^53] with fl(x * sum) >= acc * 2^53 (2^53 if none)
+// smallest x in [0, 2^53] with fl(x * sum) >= acc * 2^53 (2^53 if none);
+// fl(x*sum) is monotone in x, so "x >= X" <=> "not (target < acc)"
 uint64_t threshold_of(double acc, double sum) {
   const double target = std::ldexp(acc, 53);
-  uint64_t lo = 0, hi = 1ull << 53;  // invariant: answer in [lo, hi]
+  uint64_t lo = 0, hi = 1ull << 53;
   while (lo < hi) {
     const uint64_t mid = lo + (hi - lo) / 2;
     if (static_cast<double>(mid) * sum >= target)
@@ -73,8 +84,8 @@ uint64_t threshold_of(double acc, double sum) {
 
 struct Compiled {
   std::vector<uint16_t> map;
-  std::vector<uint32_t> rec;     // [R][6]
-  std::vector<uint32_t> rec_lo;  // [R][5]
+  std::vector<uint64_t> rec;   // [R] packed
+  std::vector<uint64_t> full;  // [R][5] exact thresholds X_d
 };
 
 int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
@@ -128,16 +139,15 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
           if (r > 0xFFFF)
             return frw_fail(ctx, FRW_EINVAL, "more than 65536 distinct stencil records");
           it = rec_of.emplace(key, r).first;
-          // microwalk.cpp:91-109: alphas and their in-order sum
+          // microwalk.cpp:91-109: alphas (1 on absorbing faces) and their
+          // in-order partial sums
           double acc[6], sum = 0;
-          uint32_t flags = 0;
+          uint64_t packed = 0;
           const double ev = self_cond ? 1.0 : pal[node_pal[v]];
           for (int d = 0; d < 6; ++d) {
             double a = 1.0;
-            if (code[d] == kSurface)
-              flags |= 1u << (2 * d);
-            else if (code[d] == kCond)
-              flags |= 2u << (2 * d);
+            if (code[d] == kSurface || code[d] == kCond)
+              packed |= 1ull << (kExitShift + d);
             else {
               const double en = pal[code[d]];
               a = en / (en + ev);
@@ -147,15 +157,13 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
           }
           for (int d = 0; d < 5; ++d) {
             const uint64_t X = threshold_of(acc[d], sum);
-            if (X >= (1ull << 53)) {  // never reached: x < 2^53 always
-              out.rec.push_back(0xFFFFFFFFu);
-              out.rec_lo.push_back(1u << 21);
-            } else {
-              out.rec.push_back(static_cast<uint32_t>(X >> 21));
-              out.rec_lo.push_back(static_cast<uint32_t>(X & 0x1FFFFFu));
-            }
+            out.full.push_back(X);
+            // X = 2^53 (never reached) clamps to 1023: every x with top bits
+            // 1023 then ties and the exact fallback decides
+            const uint64_t t10 = std::min<uint64_t>(X >> 43, 1023);
+            packed |= t10 << (kLane * d);
           }
-          out.rec.push_back(flags);
+          out.rec.push_back(packed);
         }
         out.map[v] = static_cast<uint16_t>(it->second);
       }
@@ -167,15 +175,15 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
 
 struct DevGrid {
   const uint16_t* map;
-  const uint32_t* rec;
-  const uint32_t* rec_lo;
+  const uint64_t* rec;
+  const uint64_t* full;
   const int32_t* mask;
   int n;
   int nn;
   int start_idx;
-  uint32_t start_pk;
-  uint32_t map_bytes;  // padded
-  uint32_t rec_bytes;  // padded
+  uint32_t map_bytes;  // padded to 16
+  uint32_t rec_bytes;  // padded to 16
+  float inv_n, inv_nn;
 };
 
 struct DevParams {
@@ -189,16 +197,38 @@ struct DevParams {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// shared-window address materialized once into a register (keeps ptxas
+// from re-deriving it from SR_CgaCtaId inside the step loop)
+__device__ __forceinline__ uint32_t smem_base(const void* p) {
+  uint32_t a;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }"
+               : "=r"(a)
+               : "l"(p));
+  return a;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 
 // Stage [src, src+bytes) into shared memory with the bulk-copy engine.
-__device__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
-                           uint64_t* bar) {
+__device__ void bulk_stage(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = smem_u32(bar);
   if (threadIdx.x == 0) {
-    const uint32_t b = smem_u32(bar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
-                 "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
                  : "memory");
     constexpr uint32_t kChunk = 32768;
     for (uint32_t off = 0; off < bytes; off += kChunk) {
@@ -211,7 +241,6 @@ __device__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
     }
   }
   __syncthreads();
-  const uint32_t b = smem_u32(bar);
   uint32_t done = 0;
   while (!done) {
     asm volatile(
@@ -223,25 +252,15 @@ __device__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
   }
 }
 
-// count of thresholds d in 0..4 with x >= X_d, x = (xhi << 21) | xlo;
-// the low word (global) is consulted only on a high-word tie
-template <class LoFn>
-__device__ __forceinline__ int step_dir(uint32_t xhi, const uint32_t* r,
-                                        const uint32_t* rec_lo_row,
-                                        LoFn&& get_lo) {
-  const uint32_t t0 = r[0], t1 = r[1], t2 = r[2], t3 = r[3], t4 = r[4];
-  int dir = (xhi > t0) + (xhi > t1) + (xhi > t2) + (xhi > t3) + (xhi > t4);
-  const bool tie = (xhi == t0) | (xhi == t1) | (xhi == t2) | (xhi == t3) |
-                   (xhi == t4);
-  if (__builtin_expect(tie, 0)) {
-    const uint32_t xlo = get_lo();
-    const uint32_t th[5] = {t0, t1, t2, t3, t4};
-    dir = 0;
-#pragma unroll
-    for (int d = 0; d < 5; ++d)
-      dir += (xhi > th[d]) || (xhi == th[d] && xlo >= __ldg(rec_lo_row + d));
-  }
-  return dir;
+// q = v / d for 0 <= v < 2^24 via a float reciprocal and one correction
+__device__ __forceinline__ int fdiv(int v, int d, float inv) {
+  int q = __float2int_rz(static_cast<float>(v) * inv);
+  const int r = v - q * d;
+  if (r < 0)
+    --q;
+  else if (r >= d)
+    ++q;
+  return q;
 }
 
 template <int RNG, bool SMEM>
@@ -252,21 +271,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                    unsigned long long* m_sq, unsigned long long* m_cx) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
-  __shared__ int2 stride[6];  // {node index stride, packed-coordinate stride}
+  __shared__ int stride[6];
 
-  const uint16_t* map = g.map;
-  const uint32_t* rec = g.rec;
-  if (SMEM) {
-    bulk_stage(smem, g.map, g.map_bytes + g.rec_bytes, &bar);
-    map = reinterpret_cast<const uint16_t*>(smem);
-    rec = reinterpret_cast<const uint32_t*>(smem + g.map_bytes);
-  }
+  if (SMEM) bulk_stage(smem, g.map, g.map_bytes + g.rec_bytes, &bar);
   if (threadIdx.x < 6) {
-    const int d = threadIdx.x, ax = d >> 1, s = (d & 1) ? 1 : -1;
-    stride[d] = make_int2(s * (ax == 0 ? 1 : ax == 1 ? g.n : g.nn),
-                          s * (1 << (10 * ax)));
+    const int d = threadIdx.x, ax = d >> 1;
+    stride[d] = ((d & 1) ? 1 : -1) * (ax == 0 ? 1 : ax == 1 ? g.n : g.nn);
   }
   __syncthreads();
+  const uint32_t s_map = smem_base(smem);
+  const uint32_t s_rec = s_map + g.map_bytes;
+  const uint32_t s_str = smem_base(stride);
 
   const int n = g.n;
   const int cap = p.step_cap;
@@ -276,13 +291,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   long long t_next = static_cast<long long>(atomicAdd(ctr, 1ull));
   bool live = t < p.count;
   int idx = g.start_idx;
-  uint32_t pk = g.start_pk;
   int steps = 0;
-  uint64_t sm = 0;     // parity: SplitMix64 state
-  uint32_t blk = 0;    // philox: 4-step block index within the transit
+  uint64_t sm = 0;   // parity: SplitMix64 state
+  uint32_t blk = 0;  // philox: 4-step block index within the transit
   if (RNG == FRW_RNG_SPLITMIX_PARITY && live)
     sm = sm64_stream_from_mixed(p.mixed_seed, p.stream_begin + t);
-
   const uint32_t k0 = static_cast<uint32_t>(p.seed);
   const uint32_t k1 = static_cast<uint32_t>(p.seed >> 32);
 
@@ -292,59 +305,98 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (RNG == FRW_RNG_PHILOX) {
       const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
       const U32x4 o = philox4x32_10(
-          {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32), blk, 0u},
-          k0, k1);
-      w[0] = o.x; w[1] = o.y; w[2] = o.z; w[3] = o.w;
+          {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32), blk, 0u}, k0, k1);
+      w[0] = o.x;
+      w[1] = o.y;
+      w[2] = o.z;
+      w[3] = o.w;
     }
-    int code = 0, xdir = 0;
+    bool exited = false;
+    int xdir = 0;
+    // The four steps run unconditionally (predicated state updates, no
+    // per-step branch); a lane that has exited, or reached the cap, keeps
+    // re-reading its last node without consuming randomness.
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (live && code == 0 && steps < cap) {
-        ++steps;
-        uint32_t xhi;
-        uint64_t z = 0;
+      const bool act = live && !exited && steps < cap;
+      uint64_t z = 0;
+      uint32_t x10;
+      if (RNG == FRW_RNG_SPLITMIX_PARITY) {
+        const uint64_t s1 = sm + kGamma;  // SplitMix64::next (rng.hpp:19-22)
+        z = sm64_mix(s1);
+        sm = act ? s1 : sm;
+        x10 = static_cast<uint32_t>(z >> 54);  // top 10 bits of x = z >> 11
+      } else {
+        x10 = w[u] >> 22;
+      }
+      steps += act;
+      const uint32_t r = SMEM ? lds_u16(s_map + 2u * idx) : __ldg(g.map + idx);
+      const uint64_t rc = SMEM ? lds_u64(s_rec + 8u * r) : __ldg(g.rec + r);
+      // SWAR: lane d of (x|guard) - T keeps its guard iff x10 >= T_d;
+      // subtracting one more per lane tests x10 > T_d
+      const uint64_t d0 = static_cast<uint64_t>(x10) * kOnes + kGuard - rc;
+      const uint64_t ge = d0 & kGuard;
+      const uint64_t gt = (d0 - kOnes) & kGuard;
+      int dir = __popcll(gt);
+      if (__builtin_expect(act && ge != gt, 0)) {
+        // 10-bit tie: exact comparison against the 53-bit thresholds
+        const uint64_t* f = g.full + 5 * r;
         if (RNG == FRW_RNG_SPLITMIX_PARITY) {
-          z = sm64_next(sm);
-          xhi = static_cast<uint32_t>(z >> 32);
+          const uint64_t x53 = z >> 11;
+          dir = 0;
+#pragma unroll
+          for (int d = 0; d < 5; ++d) dir += x53 >= __ldg(f + d);
         } else {
-          xhi = w[u];
-        }
-        const uint32_t r = map[idx];
-        const uint32_t* rr = rec + 6 * r;
-        const int dir = step_dir(xhi, rr, g.rec_lo + 5 * r, [&]() -> uint32_t {
-          if (RNG == FRW_RNG_SPLITMIX_PARITY)
-            return static_cast<uint32_t>(z >> 11) & 0x1FFFFFu;
-          const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
-          return philox4x32_10({static_cast<uint32_t>(id),
-                                static_cast<uint32_t>(id >> 32),
-                                static_cast<uint32_t>(steps), 1u},
-                               k0, k1).x >> 11;
-        });
-        const int c = (rr[5] >> (2 * dir)) & 3;
-        if (c) {
-          code = c;
-          xdir = dir;
-        } else {
-          const int2 s = stride[dir];
-          idx += s.x;
-          pk += s.y;
+          // the 32-bit word is the top of x; its low 21 bits are drawn
+          // from the (id, step, 1) counter only on a further tie
+          const uint32_t xh = w[u];
+          dir = 0;
+          bool tie32 = false;
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            const uint32_t th = static_cast<uint32_t>(__ldg(f + d) >> 21);
+            dir += xh > th;
+            tie32 |= xh == th;
+          }
+          if (tie32) {
+            const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
+            const uint32_t lo = philox4x32_10({static_cast<uint32_t>(id),
+                                               static_cast<uint32_t>(id >> 32),
+                                               static_cast<uint32_t>(steps), 1u},
+                                              k0, k1).x >> 11;
+            const uint64_t x53 = (static_cast<uint64_t>(xh) << 21) | lo;
+            dir = 0;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) dir += x53 >= __ldg(f + d);
+          }
         }
       }
+      const bool ex = (static_cast<uint32_t>(rc >> 32) >> (kExitShift - 32 + dir)) & 1;
+      const int s = SMEM ? lds_s32(s_str + 4u * dir) : stride[dir];
+      xdir = (act && ex) ? dir : xdir;
+      idx += (act && !ex) ? s : 0;
+      exited |= act && ex;
     }
     ++blk;
     // ---- exit bookkeeping, batched once per super-step -------------------
-    if (live && (code != 0 || steps >= cap)) {
+    if (live && (exited || steps >= cap)) {
       int32_t panel = -1, cid = -1;
-      if (code == 1) {
-        const int i = pk & 1023, j = (pk >> 10) & 1023, k = pk >> 20;
+      if (exited) {
+        const int k = fdiv(idx, g.nn, g.inv_nn);
+        const int rem = idx - k * g.nn;
+        const int j = fdiv(rem, n, g.inv_n);
+        const int i = rem - j * n;
         const int ax = xdir >> 1;
-        const int uu = ax == 0 ? j : i;
-        const int vv = ax == 2 ? j : k;
-        panel = (xdir * n + vv) * n + uu;  // sgf.hpp:34-36, sgf.cpp:13-30
-        atomicAdd(hist + panel, 1ull);
-      } else if (code == 2) {
-        cid = g.mask[idx + stride[xdir].x];
-        ++cexit;
+        const int c = ax == 0 ? i : ax == 1 ? j : k;
+        if ((xdir & 1) ? c == n - 1 : c == 0) {  // left the lattice: surface
+          const int uu = ax == 0 ? j : i;
+          const int vv = ax == 2 ? j : k;
+          panel = (xdir * n + vv) * n + uu;  // sgf.hpp:34-36, sgf.cpp:13-30
+          atomicAdd(hist + panel, 1ull);
+        } else {  // absorbed by a conductor voxel (masked lattices)
+          cid = g.mask[idx + stride[xdir]];
+          ++cexit;
+        }
       } else {
         atomicExch(err, FRW_ESTEPCAP);  // microwalk.cpp:153-155
       }
@@ -359,7 +411,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (live) {
         t_next = static_cast<long long>(atomicAdd(ctr, 1ull));
         idx = g.start_idx;
-        pk = g.start_pk;
         steps = 0;
         blk = 0;
         if (RNG == FRW_RNG_SPLITMIX_PARITY)
@@ -367,7 +418,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  // exact moments: warp reduce then one atomic per warp
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ssum += __shfl_xor_sync(0xFFFFFFFFu, ssum, o);
@@ -382,12 +432,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int RNG, bool SMEM>
-int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o) {
+int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned long long* ms,
+           unsigned long long* mq, unsigned long long* mc) {
   const GridTable& G = ctx->grid;
-  DevGrid g{G.d_map, G.d_rec, G.d_rec_lo, G.d_mask, G.n, G.n * G.n, G.start_idx,
-            0, static_cast<uint32_t>(G.map_bytes), static_cast<uint32_t>(G.rec_bytes)};
-  const int c = (G.n - 1) / 2;
-  g.start_pk = static_cast<uint32_t>(c | (c << 10) | (c << 20));
+  DevGrid g{G.d_map, G.d_rec, G.d_full, G.d_mask, G.n, G.n * G.n, G.start_idx,
+            static_cast<uint32_t>(G.map_bytes), static_cast<uint32_t>(G.rec_bytes),
+            1.0f / G.n, 1.0f / (G.n * G.n)};
   DevParams dp{p->seed, sm64_mix(p->seed), p->stream_begin, p->count,
                p->step_cap > 0 ? p->step_cap : 1000 * G.n * G.n};
   const size_t smem = SMEM ? G.map_bytes + G.rec_bytes : 0;
@@ -399,10 +449,7 @@ int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o) {
   const int blocks = p->blocks > 0 ? p->blocks : ctx->sm_count;
   kern<<<blocks, kThreads, smem, ctx->stream>>>(
       g, dp, ctx->d_ctr, ctx->d_err, o->panels, o->steps, o->cond,
-      reinterpret_cast<unsigned long long*>(o->hist),
-      reinterpret_cast<unsigned long long*>(o->step_sum ? o->step_sum : ctx->d_mom),
-      reinterpret_cast<unsigned long long*>(o->step_sumsq ? o->step_sumsq : ctx->d_mom + 1),
-      reinterpret_cast<unsigned long long*>(o->cond_exits ? o->cond_exits : ctx->d_mom + 2));
+      reinterpret_cast<unsigned long long*>(o->hist), ms, mq, mc);
   FRW_CUDA(ctx, cudaGetLastError());
   return FRW_OK;
 }
@@ -414,8 +461,8 @@ using namespace frw;
 
 extern "C" {
 
-int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
-                    double cx, double cy, double cz, double half_width) {
+int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask, double cx,
+                    double cy, double cz, double half_width) {
   if (!ctx) return FRW_EINVAL;
   if (n < 1 || n > 1000 || !eps)
     return frw_fail(ctx, FRW_EINVAL, "upload_grid: need 1 <= n <= 1000 and eps");
@@ -425,11 +472,11 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   GridTable& G = ctx->grid;
   cudaFree(G.d_map);  // also releases d_rec (same allocation)
-  cudaFree(G.d_rec_lo);
+  cudaFree(G.d_full);
   cudaFree(G.d_mask);
   G = GridTable{};
   G.n = n;
-  G.records = static_cast<int>(cg.rec.size() / 6);
+  G.records = static_cast<int>(cg.rec.size());
   const int c = (n - 1) / 2;  // start_node, sgf.hpp:58-61
   G.start_idx = (c * n + c) * n + c;
   G.start_is_conductor = mask && mask[G.start_idx] >= 0;
@@ -438,40 +485,41 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   G.center[2] = cz;
   G.half_width = half_width;
   G.map_bytes = (cg.map.size() * 2 + 15) / 16 * 16;
-  G.rec_bytes = (cg.rec.size() * 4 + 15) / 16 * 16;
-  // one allocation: map then records, so one bulk stage covers both
+  G.rec_bytes = (cg.rec.size() * 8 + 15) / 16 * 16;
+  // one allocation: map then packed records, so one bulk stage covers both
   char* blob = nullptr;
   FRW_CUDA(ctx, cudaMalloc(&blob, G.map_bytes + G.rec_bytes));
   G.d_map = reinterpret_cast<uint16_t*>(blob);
-  G.d_rec = reinterpret_cast<uint32_t*>(blob + G.map_bytes);
+  G.d_rec = reinterpret_cast<uint64_t*>(blob + G.map_bytes);
   FRW_CUDA(ctx, cudaMemcpyAsync(G.d_map, cg.map.data(), cg.map.size() * 2,
                                 cudaMemcpyHostToDevice, ctx->stream));
-  FRW_CUDA(ctx, cudaMemcpyAsync(G.d_rec, cg.rec.data(), cg.rec.size() * 4,
+  FRW_CUDA(ctx, cudaMemcpyAsync(G.d_rec, cg.rec.data(), cg.rec.size() * 8,
                                 cudaMemcpyHostToDevice, ctx->stream));
-  FRW_CUDA(ctx, cudaMalloc(&G.d_rec_lo, cg.rec_lo.size() * 4));
-  FRW_CUDA(ctx, cudaMemcpyAsync(G.d_rec_lo, cg.rec_lo.data(), cg.rec_lo.size() * 4,
+  FRW_CUDA(ctx, cudaMalloc(&G.d_full, cg.full.size() * 8));
+  FRW_CUDA(ctx, cudaMemcpyAsync(G.d_full, cg.full.data(), cg.full.size() * 8,
                                 cudaMemcpyHostToDevice, ctx->stream));
+  G.h2d_bytes = cg.map.size() * 2 + cg.rec.size() * 8 + cg.full.size() * 8;
   if (mask) {
     const size_t nodes = static_cast<size_t>(n) * n * n;
     FRW_CUDA(ctx, cudaMalloc(&G.d_mask, nodes * 4));
     FRW_CUDA(ctx, cudaMemcpyAsync(G.d_mask, mask, nodes * 4, cudaMemcpyHostToDevice,
                                   ctx->stream));
+    G.h2d_bytes += nodes * 4;
   }
   FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  // the d_map blob is freed through d_map (cudaFree on the base pointer)
   return FRW_OK;
 }
 
 int frw_grid_compile(int n, const double* eps, const int32_t* mask, uint16_t* map,
-                     uint32_t* rec, uint32_t* rec_lo, int* records) {
+                     uint64_t* rec, uint64_t* full, int* records) {
   if (n < 1 || n > 1000 || !eps || !records) return FRW_EINVAL;
   frw_ctx tmp;
   Compiled cg;
   if (int rc = compile_grid(&tmp, n, eps, mask, cg)) return rc;
-  *records = static_cast<int>(cg.rec.size() / 6);
+  *records = static_cast<int>(cg.rec.size());
   if (map) std::memcpy(map, cg.map.data(), cg.map.size() * 2);
-  if (rec) std::memcpy(rec, cg.rec.data(), cg.rec.size() * 4);
-  if (rec_lo) std::memcpy(rec_lo, cg.rec_lo.data(), cg.rec_lo.size() * 4);
+  if (rec) std::memcpy(rec, cg.rec.data(), cg.rec.size() * 8);
+  if (full) std::memcpy(full, cg.full.data(), cg.full.size() * 8);
   return FRW_OK;
 }
 
@@ -481,8 +529,13 @@ int frw_grid_info(const frw_ctx* ctx, int* records, int* smem_bytes, int* smem_r
   const size_t bytes = G.map_bytes + G.rec_bytes;
   if (records) *records = G.records;
   if (smem_bytes) *smem_bytes = static_cast<int>(bytes);
-  if (smem_resident)
-    *smem_resident = bytes + 1024 <= static_cast<size_t>(ctx->max_smem_optin);
+  if (smem_resident) *smem_resident = bytes + 1024 <= static_cast<size_t>(ctx->max_smem_optin);
+  return FRW_OK;
+}
+
+int frw_grid_h2d_bytes(const frw_ctx* ctx, uint64_t* bytes) {
+  if (!ctx || !bytes) return FRW_EINVAL;
+  *bytes = ctx->grid.h2d_bytes;
   return FRW_OK;
 }
 
@@ -498,12 +551,15 @@ int frw_microwalk_batch_dev(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_o
     return frw_fail(ctx, FRW_EINVAL, "microwalk_batch: unknown rng mode");
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   if (p->count == 0) return FRW_OK;
+  auto* ms = reinterpret_cast<unsigned long long*>(o->step_sum ? o->step_sum : ctx->d_mom);
+  auto* mq = reinterpret_cast<unsigned long long*>(o->step_sumsq ? o->step_sumsq : ctx->d_mom + 1);
+  auto* mc = reinterpret_cast<unsigned long long*>(o->cond_exits ? o->cond_exits : ctx->d_mom + 2);
   const bool smem = G.map_bytes + G.rec_bytes + 1024 <= static_cast<size_t>(ctx->max_smem_optin);
   if (p->rng_mode == FRW_RNG_SPLITMIX_PARITY)
-    return smem ? launch<FRW_RNG_SPLITMIX_PARITY, true>(ctx, p, o)
-                : launch<FRW_RNG_SPLITMIX_PARITY, false>(ctx, p, o);
-  return smem ? launch<FRW_RNG_PHILOX, true>(ctx, p, o)
-              : launch<FRW_RNG_PHILOX, false>(ctx, p, o);
+    return smem ? launch<FRW_RNG_SPLITMIX_PARITY, true>(ctx, p, o, ms, mq, mc)
+                : launch<FRW_RNG_SPLITMIX_PARITY, false>(ctx, p, o, ms, mq, mc);
+  return smem ? launch<FRW_RNG_PHILOX, true>(ctx, p, o, ms, mq, mc)
+              : launch<FRW_RNG_PHILOX, false>(ctx, p, o, ms, mq, mc);
 }
 
 int frw_microwalk_check(frw_ctx* ctx) {

@@ -1,0 +1,122 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the
+header declares, and the stencil-table compilation reproduces the
+reference's f64 direction scan bit for bit (emulated on the host)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2507_09730_b200 import capi
+from paper_2507_09730_b200.workloads import c1_grid, c2_grid, random_voxel_grid
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared(header):
+    txt = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(r"\b(frw_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = capi.lib()
+    names = _declared("frw_gpu.h")
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+
+
+def test_no_cpu_fallback_without_device():
+    # on a CPU-only host the context must fail loudly, never emulate
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(capi.FrwError):
+        capi.Context(0)
+
+
+M64 = (1 << 64) - 1
+
+
+def _emulate(oracle, eps, seed, count, mask=None):
+    """Host replay of the kernel's table-driven step (mw_grid.cu)."""
+    n = round(len(eps) ** (1 / 3))
+    mp, rec, full = capi.grid_compile(eps, mask)
+    strides = [-1, 1, -n, n, -n * n, n * n]
+    ones, guard = 0x0000100200400801, 0x0000100200400801 << 10
+    c = (n - 1) // 2
+    out, ties = [], 0
+    for t in range(count):
+        st = oracle.stream_state(seed, t)
+        idx = (c * n + c) * n + c
+        node = [c, c, c]
+        steps = 0
+        while True:
+            steps += 1
+            st = (st + 0x9E3779B97F4A7C15) & M64
+            z = int(oracle.lib.frwo_mix(st))
+            r = int(mp[idx])
+            rc = int(rec[r])
+            xg = (z >> 54) * ones + guard                     # SWAR lanes
+            ge = ((xg - rc) & M64) & guard
+            gt = ((xg - rc - ones) & M64) & guard
+            d = bin(gt).count("1")
+            if ge != gt:                                      # 10-bit tie
+                ties += 1
+                d = sum((z >> 11) >= int(full[r, q]) for q in range(5))
+            if (rc >> (55 + d)) & 1:
+                ax = d >> 1
+                i, j, k = node
+                cc = node[ax]
+                if (cc == n - 1) if d & 1 else (cc == 0):
+                    u = j if ax == 0 else i
+                    v = j if ax == 2 else k
+                    out.append(((d * n + v) * n + u, steps))
+                else:
+                    out.append((-1, steps))
+                break
+            idx += strides[d]
+            node[d >> 1] += 1 if d & 1 else -1
+    return np.array(out)
+
+
+@pytest.mark.parametrize("which", ["c1", "c2", "rv3", "rv6"])
+def test_threshold_tables_replay_reference_bit_exact(oracle, which):
+    eps = {"c1": c1_grid(1)[0], "c2": c2_grid(1)[0], "rv3": random_voxel_grid(3, 5),
+           "rv6": random_voxel_grid(6, 12)}[which]
+    n = round(len(eps) ** (1 / 3))
+    cnt = 40 if n > 30 else 300
+    e = _emulate(oracle, eps, 3, cnt)
+    w = oracle.microwalk_grid(eps, np.zeros(3), n / 2.0, 3, 0, cnt)
+    assert np.array_equal(e[:, 0], w["panel"]) and np.array_equal(e[:, 1], w["steps"])
+
+
+def test_threshold_tables_masked(oracle):
+    from tests.golden.make_golden import staircase_scene
+    eps, mask = oracle.build_grid(staircase_scene(), [-10.0, 0, 0], 10.0, 5, mask=True)
+    # the emulator assumes a unit cube; panels/steps do not depend on geometry
+    e = _emulate(oracle, eps, 64, 300, mask)
+    w = oracle.microwalk_grid(eps, np.array([-10.0, 0, 0]), 10.0, 64, 0, 300, mask=mask)
+    assert np.array_equal(e[:, 0], w["panel"]) and np.array_equal(e[:, 1], w["steps"])
+
+
+def test_record_counts_fit_shared_memory():
+    for eps in (c1_grid(1)[0], c2_grid(1)[0]):
+        n = round(len(eps) ** (1 / 3))
+        _, rec, _ = capi.grid_compile(eps)
+        smem = (2 * n ** 3 + 15) // 16 * 16 + (8 * rec.shape[0] + 15) // 16 * 16
+        assert smem <= 227 * 1024
+
+
+def test_packed_thresholds_are_monotone_prefixes():
+    """lane d holds the top 10 bits of X_d; X_d is non-decreasing in d"""
+    _, rec, full = capi.grid_compile(c2_grid(1)[0])
+    assert (np.diff(full.astype(np.float64), axis=1) >= 0).all()
+    lanes = np.stack([(rec >> np.uint64(11 * d)) & np.uint64(1023) for d in range(5)], axis=1)
+    assert np.array_equal(lanes, np.minimum(full >> np.uint64(43), np.uint64(1023)))
+
+
+def test_invalid_grid_rejected():
+    with pytest.raises(capi.FrwError):
+        capi.grid_compile(np.array([1.0, -2.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0]))
