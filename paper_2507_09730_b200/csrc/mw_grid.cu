@@ -161,7 +161,9 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
             // X = 2^53 (never reached) clamps to 1023: every x with top bits
             // 1023 then ties and the exact fallback decides
             const uint64_t t10 = std::min<uint64_t>(X >> 43, 1023);
-            packed |= t10 << (kLane * d);
+            // stored pre-negated: lane = 1023 - T_d, so x10*ones + record
+            // carries into the lane's guard bit exactly when x10 > T_d
+            packed |= (1023 - t10) << (kLane * d);
           }
           out.rec.push_back(packed);
         }
@@ -332,13 +334,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       steps += act;
       const uint32_t r = SMEM ? lds_u16(s_map + 2u * idx) : __ldg(g.map + idx);
       const uint64_t rc = SMEM ? lds_u64(s_rec + 8u * r) : __ldg(g.rec + r);
-      // SWAR: lane d of (x|guard) - T keeps its guard iff x10 >= T_d;
-      // subtracting one more per lane tests x10 > T_d
-      const uint64_t d0 = static_cast<uint64_t>(x10) * kOnes + kGuard - rc;
-      const uint64_t ge = d0 & kGuard;
-      const uint64_t gt = (d0 - kOnes) & kGuard;
-      int dir = __popcll(gt);
-      if (__builtin_expect(act && ge != gt, 0)) {
+      // SWAR: lane d of x10*ones + rec = x10 + 1023 - T_d reaches its guard
+      // bit iff x10 > T_d; the guard bits (10,21 | 32,43,54) of the low and
+      // high words are disjoint, so one POPC of their OR counts them.  A lane
+      // whose low 10 bits are all ones has x10 == T_d: a tie.
+      const uint64_t d1 = static_cast<uint64_t>(x10) * kOnes + rc;
+      const uint32_t lo = static_cast<uint32_t>(d1), hi = static_cast<uint32_t>(d1 >> 32);
+      int dir = __popc((lo & static_cast<uint32_t>(kGuard)) |
+                       (hi & static_cast<uint32_t>(kGuard >> 32)));
+      const uint64_t d2 = d1 + kOnes;
+      const bool tie = ((d2 ^ d1) & kGuard) != 0;
+      if (__builtin_expect(__any_sync(0xFFFFFFFFu, act && tie), 0) && act && tie) {
         // 10-bit tie: exact comparison against the 53-bit thresholds
         const uint64_t* f = g.full + 5 * r;
         if (RNG == FRW_RNG_SPLITMIX_PARITY) {
@@ -371,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      const bool ex = (static_cast<uint32_t>(rc >> 32) >> (kExitShift - 32 + dir)) & 1;
+      const bool ex = ((static_cast<uint32_t>(rc >> 32) >> dir) & (1u << (kExitShift - 32))) != 0;
       const int s = SMEM ? lds_s32(s_str + 4u * dir) : stride[dir];
       xdir = (act && ex) ? dir : xdir;
       idx += (act && !ex) ? s : 0;

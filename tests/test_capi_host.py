@@ -58,11 +58,10 @@ def _emulate(oracle, eps, seed, count, mask=None):
             z = int(oracle.lib.frwo_mix(st))
             r = int(mp[idx])
             rc = int(rec[r])
-            xg = (z >> 54) * ones + guard                     # SWAR lanes
-            ge = ((xg - rc) & M64) & guard
-            gt = ((xg - rc - ones) & M64) & guard
+            d1 = ((z >> 54) * ones + rc) & M64               # SWAR lanes
+            gt = d1 & guard                                   # x10 > T_d
             d = bin(gt).count("1")
-            if ge != gt:                                      # 10-bit tie
+            if (((d1 + ones) ^ d1) & guard) != 0:             # 10-bit tie
                 ties += 1
                 d = sum((z >> 11) >= int(full[r, q]) for q in range(5))
             if (rc >> (55 + d)) & 1:
@@ -110,11 +109,11 @@ def test_record_counts_fit_shared_memory():
 
 
 def test_packed_thresholds_are_monotone_prefixes():
-    """lane d holds the top 10 bits of X_d; X_d is non-decreasing in d"""
+    """lane d holds 1023 minus the top 10 bits of X_d; X_d is non-decreasing"""
     _, rec, full = capi.grid_compile(c2_grid(1)[0])
     assert (np.diff(full.astype(np.float64), axis=1) >= 0).all()
-    lanes = np.stack([(rec >> np.uint64(11 * d)) & np.uint64(1023) for d in range(5)], axis=1)
-    assert np.array_equal(lanes, np.minimum(full >> np.uint64(43), np.uint64(1023)))
+    lanes = np.stack([(rec >> np.uint64(11 * d)) & np.uint64(2047) for d in range(5)], axis=1)
+    assert np.array_equal(lanes, 1023 - np.minimum(full >> np.uint64(43), np.uint64(1023)))
 
 
 def test_invalid_grid_rejected():
