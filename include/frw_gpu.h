@@ -125,6 +125,102 @@ int frw_microwalk_batch_dev(frw_ctx *ctx, const frw_mw_params *p,
  * synchronizes the context stream */
 int frw_microwalk_check(frw_ctx *ctx);
 
+/* ---- floating-random-walk engine (configs C3-C5) ------------------------- */
+/* Replaces frwcap::Structure (geometry.hpp:94-121) on the device.  Boxes are
+ * lo.xyz,hi.xyz in nm, in declaration order (dielectrics: later wins,
+ * geometry.cpp:47-55; conductors: first hit wins, geometry.cpp:57-62). */
+typedef struct {
+  int32_t n_cond;
+  const int32_t *cond_id;
+  const double *cond_box;   /* [n_cond][6] */
+  int32_t n_diel;
+  const double *diel_box;   /* [n_diel][6] */
+  const double *diel_eps;   /* [n_diel]    */
+  double background_eps;
+  double world[6];
+} frw_structure;
+int frw_upload_structure(frw_ctx *ctx, const frw_structure *s);
+
+/* Stratified-SGF table (StratifiedSgfCache, sgf_cache.hpp:52-108): one entry
+ * per ProfileKey (n, axis, layers rounded to 6 significant digits;
+ * sgf_cache.cpp:29-51) holding the canonical unit-pitch solve: probs and
+ * inclusive cdf over the 6n^2 surface panels and the three gradient kernels
+ * (kernels may be NULL for a probs-only entry). */
+int frw_sgf_put(frw_ctx *ctx, int n, int axis, const double *layers,
+                double pitch, const double *probs, const double *cdf,
+                const double *kernels);
+int frw_sgf_count(const frw_ctx *ctx, int *entries);
+int frw_sgf_clear(frw_ctx *ctx);
+
+/* Called by frw_run_walks with the keys the table lacks (deduplicated;
+ * layers is count x n, row-major); the host solves the canonical grids and
+ * calls frw_sgf_put for each before returning 0.  The walks that missed
+ * are re-run from their start (their random streams are a pure function of
+ * the walk id), so results do not depend on when an entry arrived. */
+typedef int (*frw_miss_fn)(void *user, int n, int count, const int *axes,
+                           const double *layers);
+
+enum { FRW_MODE_FDM = 0, FRW_MODE_MW = 1, FRW_MODE_MWE = 2,
+       FRW_MODE_HYBRID_MW = 3, FRW_MODE_HYBRID_MWE = 4 };
+
+/* Engine parameters (Config, engine.hpp:28-43, plus the derived
+ * GaussianSurface of engine.cpp:84-124 and snap distance engine.cpp:186). */
+typedef struct {
+  int32_t grid_n;
+  int32_t mode;           /* FRW_MODE_*                                   */
+  double expansion;
+  double snap;            /* absolute snap distance, nm                   */
+  int64_t hop_cap;
+  uint64_t seed;
+  int32_t rng_mode;       /* FRW_RNG_*                                    */
+  int32_t n_slots;        /* resident walk slots, 0 = default             */
+  double gauss_box[6];
+  double face_cdf[6];
+  double area_m2;
+} frw_walk_params;
+
+/* Tallies of one frw_run_walks call (overwritten, not accumulated).  Slot
+ * arrays have n_cond+1 entries: conductors in declaration order, ground
+ * last (engine.cpp:461-468).  Sums are reduced in a fixed order over walk
+ * ids, so they are bit-reproducible run to run and independent of the
+ * launch shape. */
+typedef struct {
+  double *sum;
+  double *sumsq;
+  uint64_t *landed;
+  uint64_t aborted;       /* hop-cap or resample-cap walks, in ground     */
+  uint64_t resampled;     /* degenerate Gaussian points redrawn           */
+  uint64_t first[4];      /* stratified, shrunk, layered, homogenized     */
+  uint64_t sub[4];        /* cached, microwalk, microwalk_e, fdm          */
+  uint64_t cache_hits;
+  uint64_t cache_misses;  /* distinct keys handed to the miss callback    */
+  uint64_t mw_steps;      /* total MicroWalk lattice steps                */
+  uint64_t restarts;      /* walks re-run after a table miss              */
+  double mw_ms;           /* device time of the MicroWalk kernel          */
+  double total_ms;        /* device time of the whole call                */
+} frw_tally;
+
+/* Per-walk outcome (Engine::WalkOut, engine.hpp:157-161, plus the walk's
+ * dispatch counts).  branch is the first-transition ladder branch (0-3) or
+ * 255 when the resample cap was hit. */
+typedef struct {
+  double weight;       /* first-transition weight, farads                 */
+  uint64_t mw_steps;   /* MicroWalk lattice steps taken                   */
+  int32_t slot;        /* terminal: conductor declaration index or ground */
+  uint32_t cached;     /* cached (stratified) hops                        */
+  uint32_t microwalk;  /* MicroWalk hops                                  */
+  uint8_t aborted, branch, resampled, done;
+} frw_walk_record;
+
+/* Runs walks [walk_begin, walk_begin+count) of the master conductor whose
+ * declaration index is `master` (Engine::run_walk, engine.cpp:352-376,
+ * batched).  `records` (host array of `count`, may be NULL) receives the
+ * per-walk outcomes in walk order, e.g. for a walk-order fold on the host
+ * (engine.cpp:461-468). */
+int frw_run_walks(frw_ctx *ctx, const frw_walk_params *p, int32_t master,
+                  uint64_t walk_begin, int64_t count, frw_miss_fn miss,
+                  void *user, frw_tally *out, frw_walk_record *records);
+
 /* Events on the context stream for device timing of _dev launches:
  * elapsed ms between frw_event_record(ctx, 0) and frw_event_record(ctx, 1). */
 int frw_event_record(frw_ctx *ctx, int which);

@@ -42,7 +42,9 @@ def build_gpu_lib(force=False):
     deps = cu + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) \
         + [os.path.join(ROOT, "include", "frw_gpu.h")]
     if force or _stale(out, deps):
-        _run([NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v",
+        # -fmad=false: geometry/voxel-centre arithmetic must round like the
+        # reference (x86-64 baseline, no FMA contraction)
+        _run([NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "-Xptxas", "-v",
               "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
               "-o", out, *cu])
     return out

@@ -50,6 +50,36 @@ class MwOut(C.Structure):
                 ("cond_exits", C.c_void_p)]
 
 
+class StructureDesc(C.Structure):
+    _fields_ = [("n_cond", C.c_int32), ("cond_id", C.POINTER(C.c_int32)),
+                ("cond_box", C.POINTER(C.c_double)), ("n_diel", C.c_int32),
+                ("diel_box", C.POINTER(C.c_double)), ("diel_eps", C.POINTER(C.c_double)),
+                ("background_eps", C.c_double), ("world", C.c_double * 6)]
+
+
+class WalkParams(C.Structure):
+    _fields_ = [("grid_n", C.c_int32), ("mode", C.c_int32), ("expansion", C.c_double),
+                ("snap", C.c_double), ("hop_cap", C.c_int64), ("seed", C.c_uint64),
+                ("rng_mode", C.c_int32), ("n_slots", C.c_int32), ("gauss_box", C.c_double * 6),
+                ("face_cdf", C.c_double * 6), ("area_m2", C.c_double)]
+
+
+class Tally(C.Structure):
+    _fields_ = [("sum", C.POINTER(C.c_double)), ("sumsq", C.POINTER(C.c_double)),
+                ("landed", C.POINTER(C.c_uint64)), ("aborted", C.c_uint64),
+                ("resampled", C.c_uint64), ("first", C.c_uint64 * 4), ("sub", C.c_uint64 * 4),
+                ("cache_hits", C.c_uint64), ("cache_misses", C.c_uint64),
+                ("mw_steps", C.c_uint64), ("restarts", C.c_uint64), ("mw_ms", C.c_double),
+                ("total_ms", C.c_double)]
+
+
+WALK_RECORD = np.dtype([("weight", "<f8"), ("mw_steps", "<u8"), ("slot", "<i4"),
+                        ("cached", "<u4"), ("microwalk", "<u4"), ("aborted", "u1"),
+                        ("branch", "u1"), ("resampled", "u1"), ("done", "u1")])
+MISS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int),
+                      C.POINTER(C.c_double))
+MODE_MW, MODE_HYBRID_MW = 1, 3
+
 _lib = None
 
 
@@ -87,6 +117,13 @@ def lib():
         L.frw_memcpy_h2d.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
         L.frw_memcpy_d2h.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
         L.frw_smem_bandwidth_probe.argtypes = [C.c_void_p, C.c_int, _dp]
+        L.frw_upload_structure.argtypes = [C.c_void_p, C.POINTER(StructureDesc)]
+        L.frw_sgf_put.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_double, _dp, _dp, _dp]
+        L.frw_sgf_count.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
+        L.frw_sgf_clear.argtypes = [C.c_void_p]
+        L.frw_run_walks.argtypes = [C.c_void_p, C.POINTER(WalkParams), C.c_int32, C.c_uint64,
+                                    C.c_int64, MISS_FN, C.c_void_p, C.POINTER(Tally),
+                                    C.c_void_p]
         _lib = L
     return _lib
 
@@ -227,6 +264,69 @@ class Context:
         ms = C.c_float()
         self._check(self.L.frw_event_elapsed_ms(self.h, C.byref(ms)))
         return ms.value
+
+    # -- walk engine -------------------------------------------------------
+    def upload_structure(self, cond_id, cond_box, diel_box, diel_eps, background_eps, world):
+        keep = (np.ascontiguousarray(cond_id, np.int32),
+                np.ascontiguousarray(cond_box, np.float64).reshape(-1, 6),
+                np.ascontiguousarray(diel_box, np.float64).reshape(-1, 6),
+                np.ascontiguousarray(diel_eps, np.float64))
+        d = StructureDesc(len(keep[0]), keep[0].ctypes.data_as(_ip),
+                          keep[1].ctypes.data_as(_dp), len(keep[3]),
+                          keep[2].ctypes.data_as(_dp), keep[3].ctypes.data_as(_dp),
+                          float(background_eps), (C.c_double * 6)(*[float(x) for x in world]))
+        self._check(self.L.frw_upload_structure(self.h, C.byref(d)))
+        self.n_slots_out = len(keep[0]) + 1
+
+    def sgf_put(self, n, axis, layers, pitch, probs, cdf, kernels=None):
+        layers = np.ascontiguousarray(layers, np.float64)
+        probs = np.ascontiguousarray(probs, np.float64)
+        cdf = np.ascontiguousarray(cdf, np.float64)
+        k = None if kernels is None else np.ascontiguousarray(kernels, np.float64)
+        self._check(self.L.frw_sgf_put(self.h, n, axis, layers.ctypes.data_as(_dp), float(pitch),
+                                       probs.ctypes.data_as(_dp), cdf.ctypes.data_as(_dp),
+                                       None if k is None else k.ctypes.data_as(_dp)))
+
+    def sgf_count(self):
+        c = C.c_int()
+        self._check(self.L.frw_sgf_count(self.h, C.byref(c)))
+        return c.value
+
+    def sgf_clear(self):
+        self._check(self.L.frw_sgf_clear(self.h))
+
+    def run_walks(self, params: WalkParams, master, walk_begin, count, solver, records=True):
+        """frw_run_walks; `solver(n, axis, layers) -> (pitch, probs, cdf, kernels)` fills
+        table misses.  Returns (tally dict, records array or None)."""
+        nsl = self.n_slots_out
+        s1, s2 = np.zeros(nsl), np.zeros(nsl)
+        land = np.zeros(nsl, np.uint64)
+        t = Tally(s1.ctypes.data_as(_dp), s2.ctypes.data_as(_dp), land.ctypes.data_as(_up))
+        rec = np.zeros(count, WALK_RECORD) if records else None
+        errors = []
+
+        def cb(user, n, cnt, axes, layers):
+            try:
+                for q in range(cnt):
+                    lay = np.ctypeslib.as_array(layers, shape=(cnt * n,))[q * n:(q + 1) * n].copy()
+                    pitch, probs, cdf, ker = solver(n, int(axes[q]), lay)
+                    self.sgf_put(n, int(axes[q]), lay, pitch, probs, cdf, ker)
+                return 0
+            except Exception as e:  # pragma: no cover - surfaced below
+                errors.append(e)
+                return 1
+
+        fn = MISS_FN(cb)
+        rc = self.L.frw_run_walks(self.h, C.byref(params), master, walk_begin, count, fn, None,
+                                  C.byref(t), None if rec is None else rec.ctypes.data_as(C.c_void_p))
+        if errors:
+            raise errors[0]
+        self._check(rc)
+        tally = dict(sum=s1, sumsq=s2, landed=land, aborted=t.aborted, resampled=t.resampled,
+                     first=list(t.first), sub=list(t.sub), misses=t.cache_misses,
+                     mw_steps=t.mw_steps, restarts=t.restarts, mw_ms=t.mw_ms,
+                     total_ms=t.total_ms)
+        return tally, rec
 
     def smem_bandwidth(self, iters=4096):
         out = C.c_double()

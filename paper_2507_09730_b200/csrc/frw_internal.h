@@ -45,6 +45,10 @@ struct frw_ctx {
   // scratch for launches
   unsigned long long* d_ctr = nullptr;  // transit counter
   int* d_err = nullptr;                 // error flag
+  // walk engine state (walk.cu); freed through walk_free
+  void* walk = nullptr;
+  void (*walk_free)(frw_ctx*) = nullptr;
+
   // host-batch staging
   uint64_t* d_hist = nullptr;
   size_t hist_cap = 0;

@@ -1,0 +1,446 @@
+// engine.cpp -- host driver of the device walk engine.
+//
+// Mirrors the reference's Config / Engine / extract surface
+// (proj/include/frwcap/engine.hpp:23-177, proj/src/engine.cpp:37-513):
+// the same knobs and validation, the same Gaussian surface and snap
+// distance, the same batch/convergence rule and walk-order fold, so a
+// caller sees the reference's CapacitanceResult.  The walks themselves run
+// on the device through frw_run_walks (include/frw_gpu.h); SGF table misses
+// come back through a callback and are solved by StratifiedSgfCache.
+#include <algorithm>
+#include <cctype>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <map>
+#include <mutex>
+
+#include "frwcap.hpp"
+
+namespace frwcap {
+
+namespace {
+using Clock = std::chrono::steady_clock;
+}
+
+Mode parse_mode(const std::string& name) {
+  std::string u(name);
+  std::transform(u.begin(), u.end(), u.begin(), [](unsigned char c) { return std::toupper(c); });
+  if (u == "FDM") return Mode::FDM;
+  if (u == "MW") return Mode::MW;
+  if (u == "MWE") return Mode::MWE;
+  if (u == "HYBRID-MW") return Mode::HybridMW;
+  if (u == "HYBRID-MWE") return Mode::HybridMWE;
+  throw std::invalid_argument("unknown mode: " + name);
+}
+
+std::string mode_name(Mode m) {
+  switch (m) {
+    case Mode::FDM: return "FDM";
+    case Mode::MW: return "MW";
+    case Mode::MWE: return "MWE";
+    case Mode::HybridMW: return "HYBRID-MW";
+    case Mode::HybridMWE: return "HYBRID-MWE";
+  }
+  return "?";
+}
+
+// engine.cpp:69-82
+void Config::validate() const {
+  if (grid_n < 2) throw std::invalid_argument("grid_n must be >= 2");
+  if (!(expansion >= 1.0)) throw std::invalid_argument("expansion must be >= 1");
+  if (!(rel_std_tol > 0.0 && rel_std_tol < 1.0))
+    throw std::invalid_argument("rel_std_tol must lie in (0,1)");
+  if (min_walks < 1 || max_walks < min_walks)
+    throw std::invalid_argument("need 1 <= min_walks <= max_walks");
+  if (batch < 1) throw std::invalid_argument("batch must be >= 1");
+  if (!(snap_tol > 0.0)) throw std::invalid_argument("snap_tol must be > 0");
+  if (hop_cap < 1) throw std::invalid_argument("hop_cap must be >= 1");
+  if (!(gaussian_gap_fraction > 0.0 && gaussian_gap_fraction < 1.0))
+    throw std::invalid_argument("gaussian_gap_fraction must lie in (0,1)");
+  if (grid_n > 64) throw std::invalid_argument("grid_n must be <= 64 on the device");
+  if (device_batch < 1) throw std::invalid_argument("device_batch must be >= 1");
+}
+
+// engine.cpp:84-124
+GaussianSurface gaussian_surface(const Structure& s, double gap_fraction) {
+  if (!(gap_fraction > 0.0 && gap_fraction < 1.0))
+    throw ValidationError("gaussian gap fraction must lie in (0,1)");
+  const Conductor* m = s.find_conductor(s.master_id);
+  if (!m) throw ValidationError("master conductor not found");
+  double gap = std::numeric_limits<double>::infinity();
+  for (int a = 0; a < 3; ++a) {
+    gap = std::min(gap, m->box.lo[a] - s.world.lo[a]);
+    gap = std::min(gap, s.world.hi[a] - m->box.hi[a]);
+  }
+  for (const Conductor& c : s.conductors) {
+    if (c.id == s.master_id) continue;
+    double g = 0;  // Chebyshev gap between disjoint boxes
+    for (int a = 0; a < 3; ++a)
+      g = std::max(g, std::max(m->box.lo[a] - c.box.hi[a], c.box.lo[a] - m->box.hi[a]));
+    gap = std::min(gap, std::max(g, 0.0));
+  }
+  if (!(gap > 0.0)) throw ValidationError("master touches another conductor or the wall");
+  GaussianSurface out;
+  const double inflate = gap_fraction * gap;
+  for (int a = 0; a < 3; ++a) {
+    out.box.lo[a] = m->box.lo[a] - inflate;
+    out.box.hi[a] = m->box.hi[a] + inflate;
+  }
+  const double ex = out.box.hi.x - out.box.lo.x;
+  const double ey = out.box.hi.y - out.box.lo.y;
+  const double ez = out.box.hi.z - out.box.lo.z;
+  const std::array<double, 6> f = {ey * ez, ey * ez, ex * ez, ex * ez, ex * ey, ex * ey};
+  double total = 0;
+  for (double v : f) total += v;
+  double acc = 0;
+  for (int i = 0; i < 6; ++i) {
+    acc += f[i] / total;
+    out.face_cdf[i] = acc;
+  }
+  out.face_cdf[5] = 1.0;
+  out.area_m2 = total * kMetersPerNm * kMetersPerNm;
+  return out;
+}
+
+const TerminalEstimate* CapacitanceResult::find_terminal(int id) const {
+  for (const auto& t : terminals)
+    if (t.conductor_id == id) return &t;
+  return nullptr;
+}
+
+const TerminalEstimate& CapacitanceResult::self() const {
+  const TerminalEstimate* t = find_terminal(master_id);
+  if (!t) throw std::logic_error("result has no master terminal");
+  return *t;
+}
+
+// ---- device context ---------------------------------------------------------
+
+void throw_status(frw_ctx* ctx, int rc) {
+  if (rc == FRW_OK) return;
+  const std::string msg = frw_last_error(ctx);
+  switch (rc) {
+    case FRW_EINVAL: throw std::invalid_argument(msg);
+    case FRW_ESOLVE: throw SolveError(msg, 0.0);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+namespace {
+std::mutex g_dev_mu;
+std::map<int, Device*>& devices() {
+  static auto* m = new std::map<int, Device*>;  // intentionally leaked: no
+  return *m;                                    // teardown after CUDA exits
+}
+struct DeviceTable {
+  int n = 0;  // lattice size of the keys currently on the device
+};
+std::map<frw_ctx*, DeviceTable>& tables() {
+  static auto* m = new std::map<frw_ctx*, DeviceTable>;
+  return *m;
+}
+
+void put_entry(frw_ctx* ctx, const ProfileKey& k, const DiscreteSGF& g) {
+  std::vector<double> kern;
+  const bool has = !g.grad_kernels[0].empty();
+  if (has) {
+    kern.reserve(3 * g.probs.size());
+    for (const auto& v : g.grad_kernels) kern.insert(kern.end(), v.begin(), v.end());
+  }
+  throw_status(ctx, frw_sgf_put(ctx, k.n, k.axis, k.layers.data(), g.pitch, g.probs.data(),
+                                g.cdf.data(), has ? kern.data() : nullptr));
+}
+}  // namespace
+
+Device::Device(int device) {
+  const int rc = frw_ctx_create(device, &ctx_);
+  if (rc != FRW_OK)
+    throw std::runtime_error("cannot open CUDA device " + std::to_string(device) +
+                             " (the B200 build has no CPU fallback)");
+}
+
+Device::~Device() { frw_ctx_destroy(ctx_); }
+
+Device& Device::get(int device) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto& m = devices();
+  auto it = m.find(device);
+  if (it == m.end()) it = m.emplace(device, new Device(device)).first;
+  return *it->second;
+}
+
+// ---- engine -------------------------------------------------------------------
+
+Engine::Engine(const Structure& s, const Config& cfg, StratifiedSgfCache* cache)
+    : s_(s), cfg_(cfg) {
+  cfg_.validate();
+  s_.validate();
+  if (cfg_.mode != Mode::MW && cfg_.mode != Mode::HybridMW)
+    throw std::invalid_argument("mode " + mode_name(cfg_.mode) +
+                                " is not available on the B200 device build yet; use "
+                                "HYBRID-MW or MW");
+  if (cache) {
+    cache_ = cache;
+  } else {
+    owned_cache_ = std::make_unique<StratifiedSgfCache>();
+    cache_ = owned_cache_.get();
+  }
+  surface_ = gaussian_surface(s_, cfg_.gaussian_gap_fraction);
+  const Vec3 he = surface_.box.half_extent();
+  snap_ = cfg_.snap_tol * std::max({he.x, he.y, he.z});  // engine.cpp:186-187
+  for (size_t i = 0; i < s_.conductors.size(); ++i)
+    if (s_.conductors[i].id == s_.master_id) master_slot_ = static_cast<int>(i);
+  ctx_ = Device::get(cfg_.device).ctx();
+}
+
+void Engine::upload() {
+  std::vector<int32_t> ids;
+  std::vector<double> cb, db, de;
+  for (const auto& c : s_.conductors) {
+    ids.push_back(c.id);
+    for (int a = 0; a < 3; ++a) cb.push_back(c.box.lo[a]);
+    for (int a = 0; a < 3; ++a) cb.push_back(c.box.hi[a]);
+  }
+  for (const auto& d : s_.dielectrics) {
+    for (int a = 0; a < 3; ++a) db.push_back(d.box.lo[a]);
+    for (int a = 0; a < 3; ++a) db.push_back(d.box.hi[a]);
+    de.push_back(d.eps_r);
+  }
+  frw_structure fs{};
+  fs.n_cond = static_cast<int32_t>(ids.size());
+  fs.cond_id = ids.data();
+  fs.cond_box = cb.data();
+  fs.n_diel = static_cast<int32_t>(de.size());
+  fs.diel_box = db.data();
+  fs.diel_eps = de.data();
+  fs.background_eps = s_.background_eps;
+  for (int a = 0; a < 3; ++a) {
+    fs.world[a] = s_.world.lo[a];
+    fs.world[3 + a] = s_.world.hi[a];
+  }
+  throw_status(ctx_, frw_upload_structure(ctx_, &fs));
+  // device table: one lattice size; carry over every cached key of this size
+  DeviceTable& T = tables()[ctx_];
+  if (T.n != cfg_.grid_n) {
+    throw_status(ctx_, frw_sgf_clear(ctx_));
+    T.n = cfg_.grid_n;
+  }
+  for (const auto& [k, g] : cache_->entries())
+    if (k.n == cfg_.grid_n) put_entry(ctx_, k, *g);
+}
+
+frw_walk_params Engine::params() const {
+  frw_walk_params p{};
+  p.grid_n = cfg_.grid_n;
+  p.mode = cfg_.mode == Mode::MW ? FRW_MODE_MW : FRW_MODE_HYBRID_MW;
+  p.expansion = cfg_.expansion;
+  p.snap = snap_;
+  p.hop_cap = cfg_.hop_cap;
+  p.seed = cfg_.seed;
+  p.rng_mode = cfg_.rng == RngMode::Philox ? FRW_RNG_PHILOX : FRW_RNG_SPLITMIX_PARITY;
+  p.n_slots = 0;
+  for (int a = 0; a < 3; ++a) {
+    p.gauss_box[a] = surface_.box.lo[a];
+    p.gauss_box[3 + a] = surface_.box.hi[a];
+  }
+  for (int f = 0; f < 6; ++f) p.face_cdf[f] = surface_.face_cdf[f];
+  p.area_m2 = surface_.area_m2;
+  return p;
+}
+
+namespace {
+struct MissCtx {
+  frw_ctx* ctx;
+  StratifiedSgfCache* cache;
+  std::string err;
+};
+
+int miss_cb(void* user, int n, int count, const int* axes, const double* layers) {
+  auto* m = static_cast<MissCtx*>(user);
+  try {
+    std::vector<ProfileKey> keys(count);
+    for (int q = 0; q < count; ++q) {
+      keys[q].n = n;
+      keys[q].axis = axes[q];
+      keys[q].layers.assign(layers + static_cast<size_t>(q) * n,
+                            layers + static_cast<size_t>(q + 1) * n);
+    }
+    m->cache->solve_many(keys);
+    for (const auto& k : keys) put_entry(m->ctx, k, *m->cache->find(k));
+    return 0;
+  } catch (const std::exception& e) {
+    m->err = e.what();
+    return 1;
+  }
+}
+}  // namespace
+
+std::vector<frw_walk_record> Engine::run_walks(uint64_t begin, int64_t count) {
+  upload();
+  std::vector<frw_walk_record> rec(count);
+  std::vector<double> sum(s_.conductors.size() + 1), sq(sum.size());
+  std::vector<uint64_t> landed(sum.size());
+  frw_tally t{};
+  t.sum = sum.data();
+  t.sumsq = sq.data();
+  t.landed = landed.data();
+  MissCtx mc{ctx_, cache_, {}};
+  const frw_walk_params p = params();
+  const int rc = frw_run_walks(ctx_, &p, master_slot_, begin, count, miss_cb, &mc, &t, rec.data());
+  if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
+  throw_status(ctx_, rc);
+  return rec;
+}
+
+CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
+  const auto t_start = Clock::now();
+  upload();
+  const size_t nslots = s_.conductors.size() + 1;
+  const int master = master_slot_;
+  std::vector<double> sum(nslots, 0.0), sumsq(nslots, 0.0);
+  std::vector<uint64_t> landed(nslots, 0);
+  CapacitanceResult res;
+  uint64_t walks = 0;
+  bool converged = false;
+  double mw_ms = 0, dev_ms = 0;
+  const auto misses0 = cache_->stats().misses;
+
+  // engine.cpp:388-420: mean/SE per slot and the stopping rule
+  auto estimate = [&](size_t k) {
+    const double w = static_cast<double>(walks);
+    const double mean = sum[k] / w;
+    double se = 0;
+    if (walks > 1) se = std::sqrt(std::max(0.0, (sumsq[k] - sum[k] * sum[k] / w) / (w - 1)) / w);
+    return std::pair<double, double>(mean, se);
+  };
+  auto converged_now = [&]() {
+    const auto [self, self_se] = estimate(master);
+    if (!(self > 0)) return false;
+    if (self_se > cfg_.rel_std_tol * self) return false;
+    if (cfg_.all_couplings_rule) {
+      for (size_t k = 0; k + 1 < nslots; ++k) {
+        if (static_cast<int>(k) == master) continue;
+        const auto [v, se] = estimate(k);
+        if (se > cfg_.rel_std_tol * std::fabs(v)) return false;
+      }
+      return true;
+    }
+    size_t big = nslots;
+    double big_abs = 0;
+    for (size_t k = 0; k < nslots; ++k) {
+      if (static_cast<int>(k) == master) continue;
+      const double a = std::fabs(sum[k] / static_cast<double>(walks));
+      if (a > big_abs) {
+        big_abs = a;
+        big = k;
+      }
+    }
+    if (big == nslots) return true;
+    const auto [v, se] = estimate(big);
+    return se <= cfg_.rel_std_tol * std::fabs(v);
+  };
+
+  const frw_walk_params p = params();
+  MissCtx mc{ctx_, cache_, {}};
+  std::vector<frw_walk_record> rec;
+  std::vector<double> ts(nslots), tq(nslots);
+  std::vector<uint64_t> tl(nslots);
+  const long batch = cfg_.batch;
+  const long dev_batch = std::max<long>(batch, cfg_.device_batch / batch * batch);
+  while (walks < static_cast<uint64_t>(cfg_.max_walks) && !converged) {
+    const int64_t chunk = std::min<int64_t>(dev_batch, cfg_.max_walks - static_cast<int64_t>(walks));
+    rec.resize(chunk);
+    frw_tally t{};
+    t.sum = ts.data();
+    t.sumsq = tq.data();
+    t.landed = tl.data();
+    const int rc = frw_run_walks(ctx_, &p, master, walks, chunk, miss_cb, &mc, &t, rec.data());
+    if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
+    throw_status(ctx_, rc);
+    mw_ms += t.mw_ms;
+    dev_ms += t.total_ms;
+    // fold per-walk results in walk order, one reference batch at a time
+    for (int64_t off = 0; off < chunk; off += batch) {
+      const int64_t end = std::min<int64_t>(chunk, off + batch);
+      for (int64_t i = off; i < end; ++i) {
+        const frw_walk_record& r = rec[i];
+        sum[r.slot] += r.weight;
+        sumsq[r.slot] += r.weight * r.weight;
+        ++landed[r.slot];
+        res.aborted += r.aborted;
+        res.resampled += r.resampled;
+        switch (r.branch) {
+          case 0: ++res.dispatch.first_stratified; break;
+          case 1: ++res.dispatch.first_shrunk; break;
+          case 2: ++res.dispatch.first_layered; break;
+          case 3: ++res.dispatch.first_homogenized; break;
+          default: break;
+        }
+        res.dispatch.cached += r.cached;
+        res.dispatch.microwalk += r.microwalk;
+        res.mw_steps += r.mw_steps;
+      }
+      walks += end - off;
+      if (walks >= static_cast<uint64_t>(cfg_.min_walks) && converged_now()) {
+        converged = true;
+        break;
+      }
+    }
+  }
+  res.master_id = s_.master_id;
+  res.walks = walks;
+  res.converged = converged;
+  const auto st = cache_->stats();
+  res.cache_misses = st.misses - misses0;
+  const uint64_t lookups = res.dispatch.first_total() + res.dispatch.cached;
+  res.cache_hits = lookups > res.cache_misses ? lookups - res.cache_misses : 0;
+  for (size_t k = 0; k < nslots; ++k) {
+    TerminalEstimate te;
+    te.conductor_id = k < s_.conductors.size() ? s_.conductors[k].id : -1;
+    const auto [v, se] = estimate(k);
+    te.value = v;
+    te.std_err = se;
+    te.walks_landed = landed[k];
+    res.terminals.push_back(te);
+  }
+  res.t_mw_seconds = mw_ms * 1e-3;
+  res.t_device_seconds = dev_ms * 1e-3;
+  res.t_total_seconds = std::chrono::duration<double>(Clock::now() - t_start).count();
+  return res;
+}
+
+CapacitanceResult extract(const Structure& s, const Config& cfg, int threads,
+                          StratifiedSgfCache* cache) {
+  Engine e(s, cfg, cache);
+  return e.extract(threads);
+}
+
+// ---- single-cube transits ------------------------------------------------------
+
+TransitBatch microwalk_transit_batch(int n, const std::vector<double>& eps, const Vec3& c,
+                                     double half_width, uint64_t seed, uint64_t stream_begin,
+                                     int64_t count, RngMode rng, bool per_transit, int device) {
+  frw_ctx* ctx = Device::get(device).ctx();
+  throw_status(ctx, frw_upload_grid(ctx, n, eps.data(), nullptr, c.x, c.y, c.z, half_width));
+  TransitBatch out;
+  out.hist.assign(6ull * n * n, 0);
+  if (per_transit) {
+    out.panels.resize(count);
+    out.steps.resize(count);
+  }
+  frw_mw_params p{rng == RngMode::Philox ? FRW_RNG_PHILOX : FRW_RNG_SPLITMIX_PARITY, seed,
+                  stream_begin, count, 0, 0};
+  frw_mw_out o{};
+  o.hist = out.hist.data();
+  o.step_sum = &out.step_sum;
+  o.step_sumsq = &out.step_sumsq;
+  if (per_transit) {
+    o.panels = out.panels.data();
+    o.steps = out.steps.data();
+  }
+  throw_status(ctx, frw_microwalk_batch(ctx, &p, &o));
+  return out;
+}
+
+}  // namespace frwcap

@@ -1,0 +1,265 @@
+// frwcap.hpp -- host C++ API of the B200 build, mirroring the reference's
+// public solver API (proj/include/frwcap/{geometry,engine,sgf,sgf_cache,
+// microwalk}.hpp) so callers switch by relinking.  Everything that walks
+// runs on the device through the C ABI in include/frw_gpu.h; this layer
+// owns parsing, validation, the SGF cache (miss solves), the batch /
+// convergence loop and the result bookkeeping.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <unordered_map>
+#include <vector>
+
+#include "frw_gpu.h"
+
+namespace frwcap {
+
+inline constexpr double kEps0 = 8.8541878128e-12;  // F/m (constants.hpp:5)
+inline constexpr double kMetersPerNm = 1e-9;       // constants.hpp:6
+
+// ---- geometry (geometry.hpp:14-121) ---------------------------------------
+struct Vec3 {
+  double x = 0, y = 0, z = 0;
+  double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
+  double& operator[](int a) { return a == 0 ? x : (a == 1 ? y : z); }
+};
+
+struct Box {
+  Vec3 lo, hi;
+  bool contains(const Vec3& p) const;
+  double chebyshev_to(const Vec3& p) const;
+  double chebyshev_to_wall(const Vec3& p) const;
+  bool contains_box(const Box& o) const;
+  bool valid() const;
+  Vec3 half_extent() const { return {(hi.x - lo.x) / 2, (hi.y - lo.y) / 2, (hi.z - lo.z) / 2}; }
+};
+
+struct Conductor {
+  int id = 0;
+  Box box;
+};
+struct Dielectric {
+  Box box;
+  double eps_r = 1.0;
+};
+
+class ParseError : public std::runtime_error {
+ public:
+  ParseError(int line, int column, const std::string& what)
+      : std::runtime_error("parse error at line " + std::to_string(line) + ", column " +
+                           std::to_string(column) + ": " + what),
+        line(line),
+        column(column) {}
+  int line, column;
+};
+class ValidationError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct Structure {
+  std::vector<Conductor> conductors;
+  std::vector<Dielectric> dielectrics;
+  double background_eps = 1.0;
+  Box world;
+  int master_id = 0;
+
+  double permittivity_at(const Vec3& p) const;
+  std::optional<int> conductor_at(const Vec3& p, double tol) const;
+  const Conductor* find_conductor(int id) const;
+  void validate() const;
+};
+
+Structure parse_structure(std::string_view text, double world_margin = 5.0);
+Structure parse_structure_file(const std::string& path, double world_margin = 5.0);
+
+// ---- SGF (sgf.hpp:116-147) and its cache (sgf_cache.hpp) -------------------
+struct DiscreteSGF {
+  int n = 0;
+  double pitch = 1.0;
+  std::vector<double> probs, cdf;
+  std::array<std::vector<double>, 3> grad_kernels;
+};
+
+class SolveError : public std::runtime_error {
+ public:
+  SolveError(const std::string& what, double residual)
+      : std::runtime_error(what), residual(residual) {}
+  double residual = 0;
+};
+
+double round_sig(double x, int digits);
+
+struct ProfileKey {
+  int n = 0;
+  int axis = 0;
+  std::vector<double> layers;  // rounded to 6 significant digits
+  bool operator==(const ProfileKey&) const = default;
+};
+struct ProfileKeyHash {
+  size_t operator()(const ProfileKey& k) const;
+};
+ProfileKey profile_key(int n, int axis, const std::vector<double>& layers);
+
+// canonical unit-pitch solve of a key (sgf_cache.cpp:78-131 + sgf.cpp:231-290)
+DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels = true);
+// surface law of an arbitrary unmasked n^3 grid (probs only)
+DiscreteSGF solve_grid(int n, const std::vector<double>& eps, double half_width,
+                       bool with_kernels = false);
+// e_c^T A_II^{-1} d (sgf.cpp:292-299)
+double expected_steps(int n, const std::vector<double>& eps);
+
+class StratifiedSgfCache {
+ public:
+  explicit StratifiedSgfCache(size_t capacity = 0) : capacity_(capacity) {}
+  std::shared_ptr<const DiscreteSGF> get(const ProfileKey& key);
+  std::shared_ptr<const DiscreteSGF> find(const ProfileKey& key) const;
+  // solves the missing keys in parallel (host threads)
+  void solve_many(const std::vector<ProfileKey>& keys, int threads = 0);
+  struct Stats {
+    uint64_t hits = 0, misses = 0;
+    size_t size = 0;
+  };
+  Stats stats() const;
+  void clear();
+  std::vector<std::pair<ProfileKey, std::shared_ptr<const DiscreteSGF>>> entries() const;
+  // SGF1 persistence (sgf_cache.cpp:210-324)
+  void save(const std::string& path, int only_n = 0) const;
+  size_t load(const std::string& path);
+
+ private:
+  size_t capacity_;
+  mutable std::mutex mu_;
+  std::unordered_map<ProfileKey, std::shared_ptr<const DiscreteSGF>, ProfileKeyHash> map_;
+  uint64_t hits_ = 0, misses_ = 0;
+};
+
+// ---- engine (engine.hpp:23-177) ---------------------------------------------
+enum class Mode { FDM, MW, MWE, HybridMW, HybridMWE };
+Mode parse_mode(const std::string& name);
+std::string mode_name(Mode mode);
+
+enum class RngMode { SplitMixParity, Philox };
+
+struct Config {
+  int grid_n = 24;
+  double expansion = 5.0;
+  Mode mode = Mode::HybridMWE;
+  double rel_std_tol = 0.01;
+  long min_walks = 4096;
+  long max_walks = 4000000;
+  int batch = 1024;
+  uint64_t seed = 1;
+  double snap_tol = 1e-4;
+  long hop_cap = 10000;
+  double gaussian_gap_fraction = 0.5;
+  double world_margin = 5.0;
+  // B200 knobs (defaults keep the reference behaviour)
+  RngMode rng = RngMode::Philox;
+  bool all_couplings_rule = false;  // stop when every coupling meets tol (C4)
+  long device_batch = 1 << 20;      // walks per device launch sequence
+  int device = 0;
+
+  void validate() const;
+};
+
+struct GaussianSurface {
+  Box box;
+  double area_m2 = 0;
+  std::array<double, 6> face_cdf{};
+};
+GaussianSurface gaussian_surface(const Structure& s, double gap_fraction);
+
+struct DispatchStats {
+  uint64_t first_stratified = 0, first_shrunk = 0, first_layered = 0, first_homogenized = 0;
+  uint64_t cached = 0, microwalk = 0, microwalk_e = 0, fdm = 0;
+  uint64_t first_total() const {
+    return first_stratified + first_shrunk + first_layered + first_homogenized;
+  }
+  uint64_t subsequent_total() const { return cached + microwalk + microwalk_e + fdm; }
+};
+
+struct TerminalEstimate {
+  int conductor_id = -1;
+  double value = 0;
+  double std_err = 0;
+  uint64_t walks_landed = 0;
+};
+
+struct CapacitanceResult {
+  int master_id = 0;
+  std::vector<TerminalEstimate> terminals;
+  uint64_t walks = 0;
+  bool converged = false;
+  uint64_t aborted = 0;
+  uint64_t resampled = 0;
+  DispatchStats dispatch;
+  uint64_t cache_hits = 0;
+  uint64_t cache_misses = 0;
+  double t_mw_seconds = 0;
+  double t_total_seconds = 0;
+  uint64_t mw_steps = 0;       // B200 extra: total lattice steps
+  double t_device_seconds = 0; // B200 extra: device time of the walk launches
+  const TerminalEstimate* find_terminal(int conductor_id) const;
+  const TerminalEstimate& self() const;
+};
+
+// Shared device context (one per device and process).
+class Device {
+ public:
+  static Device& get(int device);
+  frw_ctx* ctx() const { return ctx_; }
+  ~Device();
+
+ private:
+  explicit Device(int device);
+  frw_ctx* ctx_ = nullptr;
+};
+
+void throw_status(frw_ctx* ctx, int rc);
+
+class Engine {
+ public:
+  Engine(const Structure& s, const Config& cfg, StratifiedSgfCache* cache = nullptr);
+  const GaussianSurface& surface() const { return surface_; }
+  double snap_distance() const { return snap_; }
+  StratifiedSgfCache& cache() { return *cache_; }
+  CapacitanceResult extract(int threads = 0);
+  // per-walk outcomes of walks [begin, begin+count) (parity tests)
+  std::vector<frw_walk_record> run_walks(uint64_t begin, int64_t count);
+
+ private:
+  void upload();
+  frw_walk_params params() const;
+  const Structure& s_;
+  Config cfg_;
+  std::unique_ptr<StratifiedSgfCache> owned_cache_;
+  StratifiedSgfCache* cache_;
+  GaussianSurface surface_;
+  double snap_ = 0;
+  int master_slot_ = 0;
+  frw_ctx* ctx_ = nullptr;
+};
+
+CapacitanceResult extract(const Structure& s, const Config& cfg, int threads = 0,
+                          StratifiedSgfCache* cache = nullptr);
+
+// ---- MicroWalk over a materialised cube (microwalk.hpp:77-79, batched) ------
+struct TransitBatch {
+  std::vector<uint64_t> hist;
+  std::vector<int32_t> panels, steps;
+  uint64_t step_sum = 0, step_sumsq = 0;
+};
+TransitBatch microwalk_transit_batch(int n, const std::vector<double>& eps, const Vec3& center,
+                                     double half_width, uint64_t seed, uint64_t stream_begin,
+                                     int64_t count, RngMode rng, bool per_transit,
+                                     int device = 0);
+
+}  // namespace frwcap

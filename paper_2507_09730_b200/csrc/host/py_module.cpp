@@ -1,0 +1,304 @@
+// py_module.cpp -- pybind11 module `_core` of the B200 build.
+//
+// Same names, keyword options, result dictionaries and error mapping as the
+// reference module (proj/bindings/py_module.cpp:20-224); the work runs on
+// the device.  B200-only extras are prefixed or documented as such.
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cmath>
+#include <sstream>
+
+#include "frwcap.hpp"
+
+namespace py = pybind11;
+using namespace frwcap;
+
+namespace {
+
+// py_module.cpp:20-57 (+ B200 knobs rng, all_couplings, device_batch, device)
+Config config_from_kwargs(const py::kwargs& kw, int& threads) {
+  Config cfg;
+  threads = 0;
+  for (const auto& item : kw) {
+    const std::string key = py::cast<std::string>(item.first);
+    const py::handle v = item.second;
+    if (key == "grid_n") cfg.grid_n = py::cast<int>(v);
+    else if (key == "expansion") cfg.expansion = py::cast<double>(v);
+    else if (key == "mode") cfg.mode = parse_mode(py::cast<std::string>(v));
+    else if (key == "tol") cfg.rel_std_tol = py::cast<double>(v);
+    else if (key == "min_walks") cfg.min_walks = py::cast<long>(v);
+    else if (key == "max_walks") cfg.max_walks = py::cast<long>(v);
+    else if (key == "batch") cfg.batch = py::cast<long>(v);
+    else if (key == "seed") cfg.seed = py::cast<uint64_t>(v);
+    else if (key == "snap_tol") cfg.snap_tol = py::cast<double>(v);
+    else if (key == "hop_cap") cfg.hop_cap = py::cast<long>(v);
+    else if (key == "gaussian_gap_fraction") cfg.gaussian_gap_fraction = py::cast<double>(v);
+    else if (key == "world_margin") cfg.world_margin = py::cast<double>(v);
+    else if (key == "threads") threads = py::cast<int>(v);
+    else if (key == "rng") {
+      const std::string r = py::cast<std::string>(v);
+      if (r == "philox") cfg.rng = RngMode::Philox;
+      else if (r == "splitmix") cfg.rng = RngMode::SplitMixParity;
+      else throw py::value_error("rng must be 'philox' or 'splitmix'");
+    } else if (key == "all_couplings") cfg.all_couplings_rule = py::cast<bool>(v);
+    else if (key == "device_batch") cfg.device_batch = py::cast<long>(v);
+    else if (key == "device") cfg.device = py::cast<int>(v);
+    else throw py::value_error("unknown option: " + key);
+  }
+  cfg.validate();
+  return cfg;
+}
+
+// py_module.cpp:59-98
+py::dict result_to_dict(const CapacitanceResult& r) {
+  py::list terms;
+  for (const auto& t : r.terminals) {
+    py::dict e;
+    e["conductor_id"] = t.conductor_id;
+    e["capacitance_farads"] = t.value;
+    e["std_err_farads"] = t.std_err;
+    e["walks_landed"] = t.walks_landed;
+    terms.append(e);
+  }
+  py::dict first, sub, dispatch, cache, d;
+  first["stratified"] = r.dispatch.first_stratified;
+  first["shrunk"] = r.dispatch.first_shrunk;
+  first["layered"] = r.dispatch.first_layered;
+  first["homogenized"] = r.dispatch.first_homogenized;
+  sub["cached"] = r.dispatch.cached;
+  sub["microwalk"] = r.dispatch.microwalk;
+  sub["microwalk_e"] = r.dispatch.microwalk_e;
+  sub["fdm"] = r.dispatch.fdm;
+  dispatch["first"] = first;
+  dispatch["subsequent"] = sub;
+  cache["hits"] = r.cache_hits;
+  cache["misses"] = r.cache_misses;
+  d["master_id"] = r.master_id;
+  d["terminals"] = terms;
+  d["walks"] = r.walks;
+  d["converged"] = r.converged;
+  d["aborted"] = r.aborted;
+  d["resampled"] = r.resampled;
+  d["dispatch_stats"] = dispatch;
+  d["cache"] = cache;
+  d["t_mw_seconds"] = r.t_mw_seconds;
+  d["t_total_seconds"] = r.t_total_seconds;
+  d["mw_steps"] = r.mw_steps;                   // B200 extra
+  d["t_device_seconds"] = r.t_device_seconds;   // B200 extra
+  return d;
+}
+
+StratifiedSgfCache& shared_cache() {
+  static auto* c = new StratifiedSgfCache;  // process-wide, like a CLI --cache
+  return *c;
+}
+
+py::dict extract_structure(const Structure& s, const Config& cfg, int threads) {
+  CapacitanceResult res;
+  {
+    py::gil_scoped_release release;
+    res = extract(s, cfg, threads, &shared_cache());
+  }
+  return result_to_dict(res);
+}
+
+// random_voxel_grid (oracle.cpp:315-320) on SplitMix64 (rng.hpp:12-40)
+struct Sm64 {
+  uint64_t s;
+  static uint64_t mix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  Sm64(uint64_t seed, uint64_t stream) : s(mix(mix(seed) + (stream + 1) * 0x9E3779B97F4A7C15ULL)) {}
+  double uniform() {
+    s += 0x9E3779B97F4A7C15ULL;
+    return static_cast<double>(mix(s) >> 11) * 0x1.0p-53;
+  }
+};
+
+std::vector<double> random_voxel_grid(int n, Sm64& r) {
+  std::vector<double> e(static_cast<size_t>(n) * n * n);
+  for (double& v : e) v = std::max(-10.0 * std::log1p(-r.uniform()), 1e-9);
+  return e;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+  m.doc() = "floating random walk capacitance extraction (B200 device build)";
+
+  m.def(
+      "extract_json",
+      [](const std::string& text, const py::kwargs& kw) {
+        int threads = 0;
+        const Config cfg = config_from_kwargs(kw, threads);
+        return extract_structure(parse_structure(text, cfg.world_margin), cfg, threads);
+      },
+      py::arg("structure_json"),
+      "Extract the master conductor's capacitance row from a structure given as JSON text.");
+
+  m.def(
+      "extract_file",
+      [](const std::string& path, const py::kwargs& kw) {
+        int threads = 0;
+        const Config cfg = config_from_kwargs(kw, threads);
+        return extract_structure(parse_structure_file(path, cfg.world_margin), cfg, threads);
+      },
+      py::arg("path"), "Extract the master conductor's capacitance row from a structure file.");
+
+  m.def(
+      "reference_capacitance_file",
+      [](const std::string&, int, double) -> py::dict {
+        throw std::runtime_error(
+            "reference_capacitance_file (full-domain FV oracle, oracle.cpp:92-213) is validation "
+            "machinery outside the B200 hot path; it is not part of this build");
+      },
+      py::arg("path"), py::arg("resolution") = 48, py::arg("world_margin") = 5.0);
+
+  // oracle.cpp:296-310: C = eps0 * area / sum(d_k / eps_k)
+  m.def(
+      "analytic_plate_capacitance",
+      [](const std::vector<std::pair<double, double>>& layers, double area_m2) {
+        if (layers.empty()) throw std::invalid_argument("analytic_plate_capacitance: no layers");
+        double sum = 0;
+        for (const auto& [d, e] : layers) {
+          if (!(d > 0) || !(e > 0))
+            throw std::invalid_argument("analytic_plate_capacitance: nonpositive layer");
+          sum += d * kMetersPerNm / e;
+        }
+        return kEps0 * area_m2 / sum;
+      },
+      py::arg("layers"), py::arg("area_m2"));
+
+  // py_module.cpp:172-189: TV distance of device transits vs the solved law
+  m.def(
+      "transit_tv",
+      [](int n, uint64_t grid_seed, long samples, uint64_t sample_seed) {
+        py::gil_scoped_release release;
+        Sm64 g(grid_seed, 0);
+        const auto eps = random_voxel_grid(n, g);
+        const DiscreteSGF sgf = solve_grid(n, eps, n / 2.0, false);
+        const TransitBatch b = microwalk_transit_batch(n, eps, {0, 0, 0}, n / 2.0, sample_seed, 0,
+                                                       samples, RngMode::Philox, false);
+        double tv = 0;
+        for (size_t q = 0; q < sgf.probs.size(); ++q)
+          tv += std::fabs(static_cast<double>(b.hist[q]) / samples - sgf.probs[q]);
+        return tv / 2;
+      },
+      py::arg("n"), py::arg("grid_seed"), py::arg("samples"), py::arg("sample_seed"));
+
+  m.def(
+      "expected_steps_uniform",
+      [](int n) {
+        py::gil_scoped_release release;
+        return expected_steps(n, std::vector<double>(static_cast<size_t>(n) * n * n, 1.0));
+      },
+      py::arg("n"));
+
+  // minimal in-process CLI: the `extract` subcommand of cli.cpp:165-213
+  m.def(
+      "run_cli",
+      [](const std::vector<std::string>& args) -> py::tuple {
+        std::ostringstream out, err;
+        int rc = 0;
+        try {
+          if (args.empty() || args[0] != "extract") {
+            err << "error: only the 'extract' subcommand is available in the B200 build\n";
+            return py::make_tuple(2, out.str(), err.str());
+          }
+          std::string path;
+          Config cfg;
+          int threads = 0;
+          for (size_t i = 1; i < args.size(); ++i) {
+            const std::string& a = args[i];
+            auto val = [&]() -> std::string {
+              if (i + 1 >= args.size()) throw std::invalid_argument(a + " needs a value");
+              return args[++i];
+            };
+            if (a == "--structure") path = val();
+            else if (a == "--grid-n") cfg.grid_n = std::stoi(val());
+            else if (a == "--mode") cfg.mode = parse_mode(val());
+            else if (a == "--tol") cfg.rel_std_tol = std::stod(val());
+            else if (a == "--min-walks") cfg.min_walks = std::stol(val());
+            else if (a == "--max-walks") cfg.max_walks = std::stol(val());
+            else if (a == "--batch") cfg.batch = std::stoi(val());
+            else if (a == "--seed") cfg.seed = std::stoull(val());
+            else if (a == "--threads") threads = std::stoi(val());
+            else throw std::invalid_argument("unknown option " + a);
+          }
+          if (path.empty()) throw std::invalid_argument("--structure is required");
+          cfg.validate();
+          CapacitanceResult r;
+          {
+            py::gil_scoped_release release;
+            r = extract(parse_structure_file(path, cfg.world_margin), cfg, threads, &shared_cache());
+          }
+          py::dict rep;
+          rep["schema_version"] = 1;
+          rep["command"] = "extract";
+          rep["argv"] = args;
+          rep["results"] = result_to_dict(r);
+          out << py::module_::import("json").attr("dumps")(rep, py::arg("indent") = 2).cast<std::string>()
+              << "\n";
+        } catch (const std::exception& e) {
+          err << "error: " << e.what() << "\n";
+          rc = 2;
+        }
+        return py::make_tuple(rc, out.str(), err.str());
+      },
+      py::arg("args"));
+
+  // ---- B200 extras ---------------------------------------------------------
+  m.def(
+      "run_walks_json",
+      [](const std::string& text, uint64_t begin, int64_t count, const py::kwargs& kw) {
+        int threads = 0;
+        const Config cfg = config_from_kwargs(kw, threads);
+        const Structure s = parse_structure(text, cfg.world_margin);
+        std::vector<frw_walk_record> rec;
+        {
+          py::gil_scoped_release release;
+          Engine e(s, cfg, &shared_cache());
+          rec = e.run_walks(begin, count);
+        }
+        py::array_t<int32_t> slot(count);
+        py::array_t<double> w(count);
+        py::array_t<uint8_t> ab(count);
+        py::array_t<uint32_t> mw(count);
+        py::array_t<uint64_t> steps(count);
+        for (int64_t i = 0; i < count; ++i) {
+          slot.mutable_at(i) = rec[i].slot;
+          w.mutable_at(i) = rec[i].weight;
+          ab.mutable_at(i) = rec[i].aborted;
+          mw.mutable_at(i) = rec[i].microwalk;
+          steps.mutable_at(i) = rec[i].mw_steps;
+        }
+        py::dict d;
+        d["slot"] = slot;
+        d["weight"] = w;
+        d["aborted"] = ab;
+        d["microwalk"] = mw;
+        d["mw_steps"] = steps;
+        return d;
+      },
+      py::arg("structure_json"), py::arg("begin"), py::arg("count"),
+      "Per-walk outcomes of walks [begin, begin+count) (parity tests).");
+
+  m.def("sgf_cache_save", [](const std::string& path) { shared_cache().save(path); });
+  m.def("sgf_cache_load", [](const std::string& path) { return shared_cache().load(path); });
+  m.def("sgf_cache_clear", []() { shared_cache().clear(); });
+  m.def("sgf_cache_stats", []() {
+    const auto st = shared_cache().stats();
+    py::dict d;
+    d["hits"] = st.hits;
+    d["misses"] = st.misses;
+    d["size"] = st.size;
+    return d;
+  });
+
+  m.attr("__version__") = "1.0.0";
+}

@@ -1,0 +1,1835 @@
+// walk.cu -- the floating-random-walk engine on sm_100a (configs C3-C5).
+//
+// Reference semantics (relative to /root/reference/proj):
+//   Engine::run_walk          src/engine.cpp:352-376   (walk driver)
+//   Engine::first_transition  src/engine.cpp:201-288   (ladder + weight)
+//   Engine::transition        src/engine.cpp:290-350   (snap, cached, MW)
+//   sample_gaussian           src/engine.cpp:126-148
+//   walk_lattice<LazyField>   src/microwalk.cpp:44-156 (lazy MicroWalk)
+//   Structure queries         src/geometry.cpp:31-80, :357-396
+//   profile_key / round_sig   src/sgf_cache.cpp:13-51
+//   sample_panel              src/sgf.cpp:301-308
+//
+// B200 design: a wavefront engine over a resident pool of
+// walk slots, so that the long MicroWalk step loops never share a warp with
+// the (divergent, scan-heavy) geometry queries:
+//   k_spawn    Gaussian sample + first-transition ladder for free slots
+//   k_advance  snap / ground tests, free cube, stratification probe; cached
+//              (stratified) hops are taken inline; a general cube is
+//              compiled into a MicroWalk job (clipped dielectric boxes in
+//              voxel-index space + the start node's cell) and queued
+//   k_mw       persistent MicroWalk kernel: one hop per thread, threads
+//              re-armed from the queue; steps inside a uniform cell use the
+//              integer threshold compare of mw_grid.cu, steps next to an
+//              interface use the reference's f64 scan with alphas read from
+//              a palette-pair table (no division)
+//   k_finish   the tail: each remaining walk runs to completion in-thread
+//   k_reduce*  per-walk records -> per-terminal tallies in a fixed order
+// All geometry and voxel-centre arithmetic is compiled with -fmad=false so
+// it rounds exactly like the reference (x86-64 baseline, no contraction).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+#include "frw_internal.h"
+#include "frw_rng.cuh"
+
+namespace frw {
+namespace {
+
+constexpr int KMAX = 32;    // clipped dielectric boxes per MicroWalk cube
+constexpr int NMAX = 64;    // lattice size cap (layers per key)
+constexpr int PMAX = 64;    // permittivity palette cap
+constexpr int kSlotsDefault = 1 << 19;
+constexpr double kEps0 = 8.8541878128e-12;  // constants.hpp:5
+constexpr double kMPerNm = 1e-9;            // constants.hpp:6
+
+
+
+// SWAR step record layout shared with mw_grid.cu
+constexpr uint64_t kOnes = 0x0000100200400801ull;
+constexpr uint64_t kGuard = kOnes << 10;
+
+enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2 };
+
+// ---------------------------------------------------------------------------
+// device-side views
+
+struct DStruct {
+  int nc, nd, P, bg;
+  const double* cbox;   // [nc][6]
+  const double* dbox;   // [nd][6]
+  const uint8_t* dcls;  // [nd] palette class
+  const double* pal;    // [P]
+  const double* alpha;  // [P][P]: alpha[nb*P + self] = e_nb/(e_nb+e_self)
+  const double* rpal;   // [P] value rounded to 6 significant digits
+  double world[6];
+};
+
+struct DSgf {
+  int cap;                   // power of two
+  const uint64_t* hash;      // [cap]
+  const int* entry;          // [cap], -1 empty
+  const int* axis;           // [entries]
+  const double* keys;        // [entries][NMAX]
+  const double* pitch;       // [entries]
+  const double* const* data; // [entries] -> cdf[P], probs[P], kern[3][P]
+};
+
+struct DParams {
+  int n, panels, mode, rng;
+  double snap;
+  long long hop_cap;
+  uint64_t seed, mixed_seed;
+  double gbox[6], fcdf[6], area;
+  uint64_t urec;      // packed SWAR record of the uniform (alpha=1/2) cell
+  uint64_t ufull[5];  // its exact 53-bit thresholds
+  uint64_t walk_begin;
+  long long count;
+  int master;
+};
+
+struct WalkRec {  // per walk id, written once when the walk terminates
+  double weight;
+  uint64_t mw_steps;
+  int slot;
+  uint32_t cached;
+  uint32_t mw;
+  uint8_t aborted, branch, resampled, done;
+};
+
+struct DSlots {
+  int S;
+  uint8_t* state;
+  long long* wid;        // walk index relative to walk_begin
+  double* p;             // [S][3]
+  double* weight;
+  uint64_t* rng;         // SplitMix64 state or Philox block counter
+  int* hops;
+  uint32_t* cached;
+  uint32_t* mw;
+  uint64_t* mwsteps;
+  uint8_t* branch;
+  uint8_t* resampled;
+  // MicroWalk job compiled by k_advance
+  double* cube;          // [S][4] center, half width
+  uint8_t* nbox;         // [S]
+  uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class
+  uint64_t* room;        // [S] start cell distances (6 bytes, dir order)
+  uint64_t* fc;          // [S] start cell + face-neighbour classes
+};
+
+struct DCounters {
+  unsigned long long next;       // next new walk id
+  unsigned long long done;       // walks finished
+  unsigned long long qlen;       // MicroWalk queue length
+  unsigned long long qhead;      // MicroWalk queue head
+  unsigned long long nmiss;      // miss records written
+  unsigned long long npend;      // pending restarts available
+  unsigned long long pend_head;  // pending restarts consumed
+  unsigned long long nretry;     // walks parked by a miss this round
+  unsigned long long active;     // slots ACTIVE/NEED_MW after k_advance
+  unsigned long long err;        // error code (first)
+};
+
+constexpr int kMissMax = 4096;
+struct DMiss {
+  int* axis;        // [kMissMax]
+  double* layers;   // [kMissMax][NMAX]
+  long long* retry; // [S] walk ids parked by misses
+  long long* pend;  // [S] walk ids to restart
+};
+
+// ---------------------------------------------------------------------------
+// exact reference arithmetic helpers (std::max / std::min semantics)
+
+__device__ __forceinline__ double mx(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double mn(double a, double b) { return b < a ? b : a; }
+
+// Box::chebyshev_to (geometry.cpp:31-37)
+__device__ __forceinline__ double cheb_to(const double* b, const double p[3]) {
+  double d = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d = mx(d, mx(__ldg(b + a) - p[a], p[a] - __ldg(b + 3 + a)));
+  return mx(d, 0.0);
+}
+// Box::chebyshev_to_wall (geometry.cpp:39-45)
+__device__ __forceinline__ double cheb_wall(const double* b, const double p[3]) {
+  double d = INFINITY;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d = mn(d, mn(p[a] - b[a], b[3 + a] - p[a]));
+  return d;
+}
+// Box::contains (geometry.hpp:37-40); `b` may live in any address space
+__device__ __forceinline__ bool box_contains(const double* b, const double p[3]) {
+  return p[0] >= b[0] && p[0] <= b[3] && p[1] >= b[1] && p[1] <= b[4] && p[2] >= b[2] &&
+         p[2] <= b[5];
+}
+
+// Structure::conductor_at (geometry.cpp:57-62): declaration index or -1
+__device__ int conductor_at(const DStruct& s, const double p[3], double tol) {
+  for (int c = 0; c < s.nc; ++c)
+    if (cheb_to(s.cbox + 6 * c, p) <= tol) return c;
+  return -1;
+}
+
+// Structure::max_free_cube (geometry.cpp:64-80); false when the reference
+// would throw (point outside the world or inside a conductor)
+__device__ bool max_free_cube(const DStruct& s, const double p[3], double* h) {
+  double r = cheb_wall(s.world, p);
+  if (r <= 0) return false;
+  for (int c = 0; c < s.nc; ++c) {
+    const double d = cheb_to(s.cbox + 6 * c, p);
+    if (d <= 0) return false;
+    if (d <= r) r = d;
+  }
+  *h = r;
+  return true;
+}
+
+// Structure::permittivity_at (geometry.cpp:47-55) as a palette class;
+// -1 outside the world
+__device__ int eps_class_at(const DStruct& s, const double p[3]) {
+  if (!box_contains(s.world, p)) return -1;
+  int cls = s.bg;
+  for (int d = 0; d < s.nd; ++d)
+    if (box_contains(s.dbox + 6 * d, p)) cls = __ldg(s.dcls + d);
+  return cls;
+}
+
+// transit_cube (microwalk.hpp:39-44)
+__device__ __forceinline__ void transit_cube(const double p[3], double hw, int n, double c[3],
+                                             double* h) {
+  if (n % 2 == 1) {
+    c[0] = p[0];
+    c[1] = p[1];
+    c[2] = p[2];
+    *h = hw;
+    return;
+  }
+  const double delta = hw / (n + 1);
+  *h = (hw - delta) * (1.0 - 1e-12);
+  c[0] = p[0] + delta;
+  c[1] = p[1] + delta;
+  c[2] = p[2] + delta;
+}
+
+// surface_panel_center (sgf.cpp:38-49)
+__device__ void panel_center(const double c[3], double h, int n, int panel, double out[3]) {
+  const int face = panel / (n * n);
+  const int rem = panel - face * n * n;
+  const int u = rem % n, v = rem / n;
+  const int axis = face >> 1;
+  const double pitch = 2.0 * h / n;
+  out[axis] = c[axis] + ((face & 1) ? 1 : -1) * h;
+  const int b1 = axis == 0 ? 1 : 0;
+  const int b2 = axis == 2 ? 1 : 2;
+  out[b1] = c[b1] - h + (u + 0.5) * pitch;
+  out[b2] = c[b2] - h + (v + 0.5) * pitch;
+}
+
+// geometry.cpp:15-19
+__device__ __forceinline__ bool eps_equal(double a, double b) {
+  return fabs(a - b) <= 1e-9 * mx(fabs(a), fabs(b));
+}
+
+// round_sig (sgf_cache.cpp:13-18).  Palette values use host-rounded copies;
+// this device version serves the slice means of ladder branches 2-3.  The
+// power of ten comes from exactly rounded literals, so it matches glibc
+// except when |x| lies within ~1e-15 of a power of ten.
+__device__ double round_sig6(double x) {
+  if (x == 0 || !isfinite(x)) return x;
+  const double e10 = floor(log10(fabs(x)));
+  const int k = 5 - static_cast<int>(e10);
+  double mag;
+  if (k >= 0 && k <= 22) {
+    mag = 1.0;
+    for (int i = 0; i < k; ++i) mag *= 10.0;  // exact up to 1e22
+  } else if (k < 0 && k >= -22) {
+    const double neg[23] = {1e0,   1e-1,  1e-2,  1e-3,  1e-4,  1e-5,  1e-6,  1e-7,
+                            1e-8,  1e-9,  1e-10, 1e-11, 1e-12, 1e-13, 1e-14, 1e-15,
+                            1e-16, 1e-17, 1e-18, 1e-19, 1e-20, 1e-21, 1e-22};
+    mag = neg[-k];
+  } else {
+    mag = pow(10.0, static_cast<double>(k));
+  }
+  return round(x * mag) / mag;
+}
+
+// ---------------------------------------------------------------------------
+// random streams: one per walk
+
+struct Rng {
+  uint64_t s;  // parity: SplitMix64 state; philox: block counter
+};
+
+__device__ __forceinline__ uint64_t philox53(const DParams& P, uint64_t wid, uint32_t blk,
+                                             uint32_t dom) {
+  const uint64_t id = P.walk_begin + wid;
+  const U32x4 o = philox4x32_10(
+      {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32), blk, dom},
+      static_cast<uint32_t>(P.seed), static_cast<uint32_t>(P.seed >> 32));
+  return (static_cast<uint64_t>(o.x) << 21) | (o.y >> 11);
+}
+
+// one 53-bit uniform integer (rng.hpp:25 in parity mode)
+__device__ __forceinline__ uint64_t draw53(const DParams& P, long long wid, Rng& r) {
+  if (P.rng == FRW_RNG_SPLITMIX_PARITY) return sm64_next(r.s) >> 11;
+  return philox53(P, static_cast<uint64_t>(wid), static_cast<uint32_t>(r.s++), 0u);
+}
+__device__ __forceinline__ double uniform(const DParams& P, long long wid, Rng& r) {
+  return static_cast<double>(draw53(P, wid, r)) * 0x1.0p-53;
+}
+
+// ---------------------------------------------------------------------------
+// stratification probe + profile key (geometry.cpp:357-396, sgf_cache.cpp:29-51)
+
+// returns the key axis (0..2) and rounded layers, or -1 (general cube),
+// -2 (error: slice centre outside the world)
+__device__ int stratified_key(const DStruct& s, const double c[3], double h, int n,
+                              double* layers) {
+  const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
+  int hits[KMAX];
+  int nh = 0;
+  bool overflow = false;
+  bool cov[3] = {true, true, true};
+  for (int d = 0; d < s.nd; ++d) {
+    const double* b = s.dbox + 6 * d;
+    double bb[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) bb[q] = __ldg(b + q);
+    // Box::intersects_open (geometry.hpp:49-52)
+    if (bb[0] < cb[3] && cb[0] < bb[3] && bb[1] < cb[4] && cb[1] < bb[4] && bb[2] < cb[5] &&
+        cb[2] < bb[5]) {
+      if (nh < KMAX)
+        hits[nh] = d;
+      else
+        overflow = true;
+      ++nh;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int q = 1; q <= 2; ++q) {
+          const int o = (a + q) % 3;
+          if (bb[o] > cb[o] || bb[3 + o] < cb[3 + o]) cov[a] = false;
+        }
+    }
+  }
+  int axis = -1;
+  if (nh == 0)
+    axis = 0;
+  else
+    for (int a = 0; a < 3 && axis < 0; ++a)
+      if (cov[a]) axis = a;
+  if (axis < 0) return -1;
+  const double pitch = 2.0 * h / n;
+  int cls0 = -1;
+  bool uniform = true;
+  for (int t = 0; t < n; ++t) {
+    double p[3] = {c[0], c[1], c[2]};
+    p[axis] = c[axis] - h + (t + 0.5) * pitch;
+    int cls;
+    if (!overflow) {
+      if (!box_contains(s.world, p)) return -2;
+      cls = s.bg;
+      for (int q = 0; q < nh; ++q)
+        if (box_contains(s.dbox + 6 * hits[q], p)) cls = __ldg(s.dcls + hits[q]);
+    } else {
+      cls = eps_class_at(s, p);
+      if (cls < 0) return -2;
+    }
+    if (t == 0) cls0 = cls;
+    // StratifiedProfile::uniform() compares raw permittivities
+    if (!eps_equal(__ldg(s.pal + cls), __ldg(s.pal + cls0))) uniform = false;
+    layers[t] = __ldg(s.rpal + cls);  // round_sig(layer, 6), host-exact
+  }
+  if (uniform) axis = 0;
+  // profile_key: uniform rounded layers normalise to axis 0
+  bool same = true;
+  for (int t = 1; t < n; ++t) same &= layers[t] == layers[0];
+  if (same) axis = 0;
+  return axis;
+}
+
+__device__ __forceinline__ uint64_t key_hash(int n, int axis, const double* layers) {
+  uint64_t h = sm64_mix((static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis));
+  for (int t = 0; t < n; ++t) h = sm64_mix(h ^ static_cast<uint64_t>(__double_as_longlong(layers[t])));
+  return h;
+}
+
+// table lookup; entry index or -1
+__device__ int sgf_find(const DSgf& T, int n, int axis, const double* layers) {
+  if (T.cap == 0) return -1;
+  const uint64_t h = key_hash(n, axis, layers);
+  for (int i = static_cast<int>(h & (T.cap - 1));; i = (i + 1) & (T.cap - 1)) {
+    const int e = __ldg(T.entry + i);
+    if (e < 0) return -1;
+    if (__ldg(T.hash + i) != h || __ldg(T.axis + e) != axis) continue;
+    const double* k = T.keys + static_cast<size_t>(e) * NMAX;
+    bool eq = true;
+    for (int t = 0; t < n && eq; ++t) eq = __ldg(k + t) == layers[t];
+    if (eq) return e;
+  }
+}
+
+// sample_panel (sgf.cpp:301-308): upper_bound on the inclusive cdf
+__device__ int sample_panel(const double* cdf, int count, double u) {
+  const double target = u * __ldg(cdf + count - 1);
+  int lo = 0, hi = count;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (target < __ldg(cdf + mid))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo == count ? count - 1 : lo;
+}
+
+__device__ void record_miss(DCounters* C, const DMiss& M, int n, int axis, const double* layers,
+                            long long wid) {
+  const unsigned long long m = atomicAdd(&C->nmiss, 1ull);
+  if (m < kMissMax) {
+    M.axis[m] = axis;
+    for (int t = 0; t < n; ++t) M.layers[m * NMAX + t] = layers[t];
+  }
+  const unsigned long long r = atomicAdd(&C->nretry, 1ull);
+  M.retry[r] = wid;
+}
+
+__device__ __forceinline__ void set_err(DCounters* C, int code) {
+  atomicCAS(&C->err, 0ull, static_cast<unsigned long long>(static_cast<unsigned>(-code)));
+}
+
+// ---------------------------------------------------------------------------
+// voxel-index clipping of the dielectric boxes for a lazy MicroWalk cube
+// (microwalk.cpp:25-30 voxel centres; inclusion is closed per axis, so the
+// voxels of a box form an index interval on every axis)
+
+__device__ __forceinline__ double vcenter(double c, double h, double p, int i) {
+  return c - h + (i + 0.5) * p;  // (c - h) + ((i + 0.5) * p), no contraction
+}
+
+// first i in [0, n] with centre(i) >= lo; last i in [-1, n-1] with centre(i) <= hi
+__device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih) {
+  const double p = 2.0 * h / n;
+  const double base = c - h;
+  int a = static_cast<int>(floor((lo - base) / p - 0.5));
+  a = max(0, min(n, a));
+  while (a > 0 && vcenter(c, h, p, a - 1) >= lo) --a;
+  while (a < n && vcenter(c, h, p, a) < lo) ++a;
+  int b = static_cast<int>(floor((hi - base) / p - 0.5));
+  b = max(-1, min(n - 1, b));
+  while (b < n - 1 && vcenter(c, h, p, b + 1) <= hi) ++b;
+  while (b >= 0 && vcenter(c, h, p, b) > hi) --b;
+  *il = a;
+  *ih = b;
+}
+
+__device__ __forceinline__ int box_lo(uint64_t b, int a) { return static_cast<int>((b >> (8 * a)) & 0xFF); }
+__device__ __forceinline__ int box_hi(uint64_t b, int a) { return static_cast<int>((b >> (24 + 8 * a)) & 0xFF); }
+__device__ __forceinline__ int box_cls(uint64_t b) { return static_cast<int>((b >> 48) & 0xFF); }
+
+// class of voxel (i,j,k): the last clipped box containing it, else background
+__device__ int cell_class(const uint64_t* boxes, int K, int bg, int i, int j, int k) {
+  int cls = bg;
+  for (int q = 0; q < K; ++q) {
+    const uint64_t b = boxes[q];
+    if (i >= box_lo(b, 0) && i <= box_hi(b, 0) && j >= box_lo(b, 1) && j <= box_hi(b, 1) &&
+        k >= box_lo(b, 2) && k <= box_hi(b, 2))
+      cls = box_cls(b);
+  }
+  return cls;
+}
+
+// extent [lo, hi] of the cell segment containing v along axis a
+__device__ void cell_extent(const uint64_t* boxes, int K, int n, int a, int v, int* lo, int* hi) {
+  int l = 0, r = n - 1;
+  for (int q = 0; q < K; ++q) {
+    const uint64_t b = boxes[q];
+    const int bl = box_lo(b, a), bh = box_hi(b, a);
+    if (bl <= v) l = max(l, bl); else r = min(r, bl - 1);
+    if (bh < v) l = max(l, bh + 1); else r = min(r, bh);
+  }
+  *lo = l;
+  *hi = r;
+}
+
+// node packing: i | j<<8 | k<<16
+__device__ __forceinline__ int coord(uint32_t node, int a) { return (node >> (8 * a)) & 0xFF; }
+
+// face-neighbour classes of the cell containing `node` (0xFF: lattice face)
+__device__ uint64_t face_classes(const uint64_t* boxes, int K, int bg, int n, uint32_t node,
+                                 uint64_t room, int c0) {
+  uint64_t fc = static_cast<uint64_t>(c0) << 48;
+#pragma unroll 1
+  for (int d = 0; d < 6; ++d) {
+    const int a = d >> 1;
+    const int dist = static_cast<int>((room >> (8 * d)) & 0xFF);
+    int v[3] = {coord(node, 0), coord(node, 1), coord(node, 2)};
+    v[a] += (d & 1) ? dist + 1 : -(dist + 1);
+    uint64_t cls = 0xFF;
+    if (v[a] >= 0 && v[a] < n) cls = static_cast<uint64_t>(cell_class(boxes, K, bg, v[0], v[1], v[2]));
+    fc |= cls << (8 * d);
+  }
+  return fc;
+}
+
+__device__ uint64_t cell_room(const uint64_t* boxes, int K, int n, uint32_t node) {
+  uint64_t room = 0x0101ull << 48;  // two unused bytes kept non-zero
+#pragma unroll 1
+  for (int a = 0; a < 3; ++a) {
+    int lo, hi;
+    const int v = coord(node, a);
+    cell_extent(boxes, K, n, a, v, &lo, &hi);
+    room |= static_cast<uint64_t>(v - lo) << (16 * a);
+    room |= static_cast<uint64_t>(hi - v) << (16 * a + 8);
+  }
+  return room;
+}
+
+// compile the MicroWalk job of a general cube into the slot
+__device__ bool compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
+                               double h, int n, DCounters* C) {
+  uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
+  int K = 0;
+  for (int d = 0; d < s.nd; ++d) {
+    const double* b = s.dbox + 6 * d;
+    int lo[3], hi[3];
+    bool empty = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      clip_axis(c[a], h, n, __ldg(b + a), __ldg(b + 3 + a), &lo[a], &hi[a]);
+      empty |= lo[a] > hi[a];
+    }
+    if (empty) continue;
+    if (K == KMAX) {
+      set_err(C, FRW_EINVAL);  // more than KMAX boxes reach into one cube
+      return false;
+    }
+    boxes[K++] = static_cast<uint64_t>(lo[0]) | static_cast<uint64_t>(lo[1]) << 8 |
+                 static_cast<uint64_t>(lo[2]) << 16 | static_cast<uint64_t>(hi[0]) << 24 |
+                 static_cast<uint64_t>(hi[1]) << 32 | static_cast<uint64_t>(hi[2]) << 40 |
+                 static_cast<uint64_t>(__ldg(s.dcls + d)) << 48;
+  }
+  const int m = (n - 1) / 2;  // start_node (sgf.hpp:58-61)
+  const uint32_t node = m | (m << 8) | (m << 16);
+  const uint64_t room = cell_room(boxes, K, n, node);
+  const int c0 = cell_class(boxes, K, s.bg, m, m, m);
+  W.nbox[slot] = static_cast<uint8_t>(K);
+  W.room[slot] = room;
+  W.fc[slot] = face_classes(boxes, K, s.bg, n, node, room, c0);
+  W.cube[4 * slot + 0] = c[0];
+  W.cube[4 * slot + 1] = c[1];
+  W.cube[4 * slot + 2] = c[2];
+  W.cube[4 * slot + 3] = h;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// first transition (engine.cpp:201-288); returns 1 ok, 0 degenerate point,
+// 2 table miss (key recorded), <0 error
+
+struct FirstOut {
+  double p[3];
+  double weight;
+  int branch;
+};
+
+__device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& P, long long wid,
+                                Rng& rng, const double g[3], int gaxis, int gsign,
+                                uint64_t* boxes, DCounters* C, const DMiss& M, FirstOut* out) {
+  if (conductor_at(s, g, P.snap) >= 0) return 0;
+  double fh;
+  if (!max_free_cube(s, g, &fh)) return -1;
+  if (!(fh > P.snap)) return 0;
+  const int n = P.n;
+  double c[3], h;
+  transit_cube(g, fh, n, c, &h);
+  double layers[NMAX];
+  int branch = 0;
+  int axis = stratified_key(s, c, h, n, layers);
+  if (axis == -2) return -1;
+  if (axis < 0) {
+    for (int i = 19; i >= 6; --i) {  // concentric shrink, engine.cpp:218-226
+      double c2[3], h2;
+      transit_cube(g, 0.05 * i * fh, n, c2, &h2);
+      axis = stratified_key(s, c2, h2, n, layers);
+      if (axis == -2) return -1;
+      if (axis >= 0) {
+        c[0] = c2[0];
+        c[1] = c2[1];
+        c[2] = c2[2];
+        h = h2;
+        branch = 1;
+        break;
+      }
+    }
+  }
+  if (axis < 0) {
+    // build_grid + slice means (engine.cpp:228-265), summed in the
+    // reference's loop order so the means are bit-identical
+    int K = 0;
+    for (int d = 0; d < s.nd; ++d) {
+      const double* b = s.dbox + 6 * d;
+      int lo[3], hi[3];
+      bool empty = false;
+      for (int a = 0; a < 3; ++a) {
+        clip_axis(c[a], h, n, __ldg(b + a), __ldg(b + 3 + a), &lo[a], &hi[a]);
+        empty |= lo[a] > hi[a];
+      }
+      if (empty) continue;
+      if (K == KMAX) return -1;
+      boxes[K++] = static_cast<uint64_t>(lo[0]) | static_cast<uint64_t>(lo[1]) << 8 |
+                   static_cast<uint64_t>(lo[2]) << 16 | static_cast<uint64_t>(hi[0]) << 24 |
+                   static_cast<uint64_t>(hi[1]) << 32 | static_cast<uint64_t>(hi[2]) << 40 |
+                   static_cast<uint64_t>(__ldg(s.dcls + d)) << 48;
+    }
+    double sl[3][NMAX];
+    for (int a = 0; a < 3; ++a)
+      for (int t = 0; t < n; ++t) sl[a][t] = 0.0;
+    for (int k = 0; k < n; ++k)
+      for (int j = 0; j < n; ++j) {
+        // the class is constant between x-breakpoints: walk the row by cells
+        int i = 0;
+        while (i < n) {
+          int lo, hi;
+          cell_extent(boxes, K, n, 0, i, &lo, &hi);
+          const double e = __ldg(s.pal + cell_class(boxes, K, s.bg, i, j, k));
+          for (; i <= hi; ++i) {
+            sl[0][i] += e;
+            sl[1][j] += e;
+            sl[2][k] += e;
+          }
+        }
+      }
+    int best = 0;
+    double bvar = -1.0;
+    for (int a = 0; a < 3; ++a) {
+      double mean = 0;
+      for (int t = 0; t < n; ++t) {
+        sl[a][t] /= static_cast<double>(n) * n;
+        mean += sl[a][t];
+      }
+      mean /= n;
+      double var = 0;
+      for (int t = 0; t < n; ++t) var += (sl[a][t] - mean) * (sl[a][t] - mean);
+      if (var > bvar) {
+        bvar = var;
+        best = a;
+      }
+    }
+    axis = best;
+    bool same = true;
+    for (int t = 0; t < n; ++t) {
+      layers[t] = round_sig6(sl[best][t]);
+      same &= layers[t] == layers[0];
+    }
+    branch = 2;
+    if (same) {
+      branch = 3;
+      axis = 0;
+    }
+  }
+  const int e = sgf_find(T, n, axis, layers);
+  if (e < 0) {
+    record_miss(C, M, n, axis, layers, wid);
+    return 2;
+  }
+  const double* data = T.data[e];
+  const int panels = P.panels;
+  const int panel = sample_panel(data, panels, uniform(P, wid, rng));
+  const double pitch_nm = 2.0 * h / n;
+  const double kern_per_m =
+      __ldg(data + 2 * panels + gaxis * panels + panel) * (__ldg(T.pitch + e) / pitch_nm) /
+      kMPerNm;
+  const int ecls = eps_class_at(s, g);
+  if (ecls < 0) return -1;
+  const double eps_r = __ldg(s.pal + ecls);
+  panel_center(c, h, n, panel, out->p);
+  out->weight = -P.area * kEps0 * eps_r * gsign * kern_per_m / __ldg(data + panels + panel);
+  out->branch = branch;
+  return 1;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+
+__device__ void finish_walk(const DSlots& W, WalkRec* recs, DCounters* C, int slot, int term,
+                            bool aborted) {
+  const long long wid = W.wid[slot];
+  WalkRec r;
+  r.weight = W.weight[slot];
+  r.mw_steps = W.mwsteps[slot];
+  r.slot = term;
+  r.cached = W.cached[slot];
+  r.mw = W.mw[slot];
+  r.aborted = aborted;
+  r.branch = W.branch[slot];
+  r.resampled = W.resampled[slot];
+  r.done = 1;
+  recs[wid] = r;
+  W.state[slot] = S_FREE;
+  atomicAdd(&C->done, 1ull);
+}
+
+// Gaussian sample + first transition for every free slot
+__global__ void k_spawn(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C,
+                        DMiss M) {
+  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
+       slot += gridDim.x * blockDim.x) {
+    if (W.state[slot] != S_FREE) continue;
+    long long wid = -1;
+    if (C->pend_head < C->npend) {
+      const unsigned long long q = atomicAdd(&C->pend_head, 1ull);
+      if (q < C->npend) wid = M.pend[q];
+    }
+    if (wid < 0) {
+      if (C->next >= static_cast<unsigned long long>(P.count)) continue;
+      const unsigned long long q = atomicAdd(&C->next, 1ull);
+      if (q >= static_cast<unsigned long long>(P.count)) continue;
+      wid = static_cast<long long>(q);
+    }
+    Rng rng;
+    rng.s = P.rng == FRW_RNG_SPLITMIX_PARITY
+                ? sm64_stream_from_mixed(P.mixed_seed, P.walk_begin + wid)
+                : 0;
+    W.wid[slot] = wid;
+    W.cached[slot] = 0;
+    W.mw[slot] = 0;
+    W.mwsteps[slot] = 0;
+    W.hops[slot] = 0;
+    FirstOut fo;
+    int rc = 0, resampled = 0;
+    for (int attempt = 0; attempt < 100 && rc == 0; ++attempt) {  // engine.cpp:359-363
+      // sample_gaussian (engine.cpp:126-148)
+      const double u = uniform(P, wid, rng);
+      int face = 5;
+      for (int f = 0; f < 5; ++f)
+        if (u < P.fcdf[f]) {
+          face = f;
+          break;
+        }
+      const int a = face >> 1;
+      const int b1 = a == 0 ? 1 : 0;
+      const int b2 = a == 2 ? 1 : 2;
+      const int sign = ((face & 1) ? 1 : -1);
+      double g[3];
+      g[a] = sign < 0 ? P.gbox[a] : P.gbox[3 + a];
+      g[b1] = P.gbox[b1] + uniform(P, wid, rng) * (P.gbox[3 + b1] - P.gbox[b1]);
+      g[b2] = P.gbox[b2] + uniform(P, wid, rng) * (P.gbox[3 + b2] - P.gbox[b2]);
+      rc = first_transition(s, T, P, wid, rng, g, a, sign,
+                            W.boxes + static_cast<size_t>(slot) * KMAX, C, M, &fo);
+      if (rc == 0) ++resampled;
+    }
+    W.resampled[slot] = static_cast<uint8_t>(resampled);
+    if (rc < 0) {
+      set_err(C, FRW_EINVAL);
+      continue;
+    }
+    if (rc == 2) continue;  // miss: parked for a restart, slot stays free
+    if (rc == 0) {          // resample cap: folded into ground as aborted
+      W.weight[slot] = 0.0;
+      W.branch[slot] = 0xFF;
+      finish_walk(W, recs, C, slot, s.nc, true);
+      continue;
+    }
+    W.p[3 * slot + 0] = fo.p[0];
+    W.p[3 * slot + 1] = fo.p[1];
+    W.p[3 * slot + 2] = fo.p[2];
+    W.weight[slot] = fo.weight;
+    W.branch[slot] = static_cast<uint8_t>(fo.branch);
+    W.rng[slot] = rng.s;
+    W.state[slot] = S_ACTIVE;
+  }
+}
+
+// One transition (engine.cpp:290-350) for an ACTIVE slot; cached hops loop
+// inline.  Returns true when the slot still needs work (NEED_MW).
+__device__ bool advance_slot(const DStruct& s, const DSgf& T, const DParams& P, const DSlots& W,
+                             WalkRec* recs, DCounters* C, const DMiss& M, int slot) {
+  const long long wid = W.wid[slot];
+  double p[3] = {W.p[3 * slot], W.p[3 * slot + 1], W.p[3 * slot + 2]};
+  Rng rng;
+  rng.s = W.rng[slot];
+  int hops = W.hops[slot];
+  uint32_t cached = W.cached[slot];
+  const int n = P.n;
+  for (;;) {
+    if (hops >= P.hop_cap) {  // engine.cpp:367-375
+      W.cached[slot] = cached;
+      finish_walk(W, recs, C, slot, s.nc, true);
+      return false;
+    }
+    const int ci = conductor_at(s, p, P.snap);
+    if (ci >= 0) {
+      W.cached[slot] = cached;
+      finish_walk(W, recs, C, slot, ci, false);
+      return false;
+    }
+    if (cheb_wall(s.world, p) <= P.snap) {
+      W.cached[slot] = cached;
+      finish_walk(W, recs, C, slot, s.nc, false);
+      return false;
+    }
+    double fh;
+    if (!max_free_cube(s, p, &fh)) {
+      set_err(C, FRW_EINVAL);
+      W.state[slot] = S_FREE;
+      return false;
+    }
+    double c[3], h;
+    transit_cube(p, fh, n, c, &h);
+    double layers[NMAX];
+    const int axis = stratified_key(s, c, h, n, layers);
+    if (axis == -2) {
+      set_err(C, FRW_EINVAL);
+      W.state[slot] = S_FREE;
+      return false;
+    }
+    if (axis >= 0) {
+      const int e = sgf_find(T, n, axis, layers);
+      if (e < 0) {
+        record_miss(C, M, n, axis, layers, wid);
+        W.state[slot] = S_FREE;
+        return false;
+      }
+      const int panel = sample_panel(T.data[e], P.panels, uniform(P, wid, rng));
+      panel_center(c, h, n, panel, p);
+      ++cached;
+      ++hops;
+      continue;
+    }
+    // general cube: MicroWalk (HYBRID-MW, engine.cpp:319-326)
+    if (!compile_mw_job(s, W, slot, c, h, n, C)) {
+      W.state[slot] = S_FREE;
+      return false;
+    }
+    W.p[3 * slot + 0] = p[0];
+    W.p[3 * slot + 1] = p[1];
+    W.p[3 * slot + 2] = p[2];
+    W.rng[slot] = rng.s;
+    W.hops[slot] = hops + 1;
+    W.cached[slot] = cached;
+    W.state[slot] = S_NEED_MW;
+    return true;
+  }
+}
+
+__global__ void k_advance(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C,
+                          DMiss M, int* queue) {
+  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
+       slot += gridDim.x * blockDim.x) {
+    if (W.state[slot] != S_ACTIVE) continue;
+    if (advance_slot(s, T, P, W, recs, C, M, slot)) {
+      const unsigned long long q = atomicAdd(&C->qlen, 1ull);
+      queue[q] = slot;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the lazy MicroWalk hop (microwalk.cpp:77-156 with LazyField)
+
+struct MwLane {
+  int slot;
+  long long wid;
+  uint32_t node;
+  uint64_t room;  // distance to the cell faces, one byte per direction
+  uint64_t fc;    // face-neighbour classes (byte per dir), current class in byte 6
+  uint64_t rng;   // SplitMix64 state or Philox block counter
+  int steps;
+  int K;
+};
+
+__device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int n, MwLane& L) {
+  const int m = (n - 1) / 2;
+  L.slot = slot;
+  L.wid = W.wid[slot];
+  L.node = m | (m << 8) | (m << 16);
+  L.room = W.room[slot];
+  L.fc = W.fc[slot];
+  L.rng = W.rng[slot];
+  L.K = W.nbox[slot];
+  L.steps = 0;
+}
+
+// handles a move that left the current cell along dir d into the adjacent
+// cell (same segments on the other two axes)
+__device__ void mw_cell_change(const DSlots& W, const DStruct& s, int n, MwLane& L, int d) {
+  const uint64_t* boxes = W.boxes + static_cast<size_t>(L.slot) * KMAX;
+  const int a = d >> 1;
+  int lo, hi;
+  const int v = coord(L.node, a);
+  cell_extent(boxes, L.K, n, a, v, &lo, &hi);
+  const int c0 = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
+  uint64_t room = L.room & ~(0xFFFFull << (16 * a));
+  room |= static_cast<uint64_t>(v - lo) << (16 * a);
+  room |= static_cast<uint64_t>(hi - v) << (16 * a + 8);
+  L.room = room;
+  L.fc = face_classes(boxes, L.K, s.bg, n, L.node, room, c0);
+}
+
+// surface exit: continuation point, counters, slot back to ACTIVE
+__device__ void mw_exit(const DSlots& W, int n, MwLane& L, int dir) {
+  const int a = dir >> 1;
+  const int i = coord(L.node, 0), j = coord(L.node, 1), k = coord(L.node, 2);
+  const int u = a == 0 ? j : i;
+  const int v = a == 2 ? j : k;
+  const int panel = (dir * n + v) * n + u;  // surface_panel_of (sgf.cpp:13-30)
+  const double c[3] = {W.cube[4 * L.slot], W.cube[4 * L.slot + 1], W.cube[4 * L.slot + 2]};
+  const double h = W.cube[4 * L.slot + 3];
+  double p[3];
+  panel_center(c, h, n, panel, p);
+  W.p[3 * L.slot + 0] = p[0];
+  W.p[3 * L.slot + 1] = p[1];
+  W.p[3 * L.slot + 2] = p[2];
+  W.rng[L.slot] = L.rng;
+  W.mw[L.slot] += 1;
+  W.mwsteps[L.slot] += L.steps;
+  W.state[L.slot] = S_ACTIVE;
+}
+
+// f64 direction scan (microwalk.cpp:91-121) for a node next to a cell face
+__device__ __forceinline__ int general_dir(const double* alpha_sm, int P, const MwLane& L,
+                                           double u, bool* exit_surface, bool* leaves) {
+  const int c0 = static_cast<int>((L.fc >> 48) & 0xFF);
+  double al[6], sum = 0;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const bool inside = ((L.room >> (8 * d)) & 0xFF) != 0;
+    const int cn = inside ? c0 : static_cast<int>((L.fc >> (8 * d)) & 0xFF);
+    const double a = (cn == 0xFF) ? 1.0 : alpha_sm[cn * P + c0];
+    al[d] = a;
+    sum += a;
+  }
+  const double target = u * sum;
+  double acc = 0;
+  int dir = 5;
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    acc += al[d];
+    if (dir == 5 && target < acc) dir = d;
+  }
+  const bool inside = ((L.room >> (8 * dir)) & 0xFF) != 0;
+  *leaves = !inside;
+  *exit_surface = !inside && ((L.fc >> (8 * dir)) & 0xFF) == 0xFF;
+  return dir;
+}
+
+struct DirDelta {
+  uint64_t room;
+  uint32_t node;
+  uint32_t pad;
+};
+
+// One lattice step for lane L; returns 0 continue, 1 surface exit (xdir set)
+template <int RNG>
+__device__ __forceinline__ int mw_step(const DStruct& s, const DSlots& W, const DParams& P,
+                                       const double* alpha_sm, const DirDelta* dd, int n,
+                                       MwLane& L, uint32_t w, uint64_t z, uint32_t tie_ctr,
+                                       int* xdir) {
+  ++L.steps;
+  const uint64_t r = L.room & 0x0000FFFFFFFFFFFFull;
+  const bool interior = ((r - 0x010101010101ull) & ~r & 0x808080808080ull) == 0;
+  int dir;
+  if (interior) {
+    // all seven voxels share one class: alpha = 1/2 everywhere
+    const uint32_t x10 = RNG == FRW_RNG_SPLITMIX_PARITY ? static_cast<uint32_t>(z >> 54) : (w >> 22);
+    const uint64_t d1 = static_cast<uint64_t>(x10) * kOnes + P.urec;
+    const uint32_t lo = static_cast<uint32_t>(d1), hi = static_cast<uint32_t>(d1 >> 32);
+    dir = __popc((lo & static_cast<uint32_t>(kGuard)) | (hi & static_cast<uint32_t>(kGuard >> 32)));
+    if ((((d1 + kOnes) ^ d1) & kGuard) != 0) {
+      uint64_t x53;
+      if (RNG == FRW_RNG_SPLITMIX_PARITY)
+        x53 = z >> 11;
+      else
+        x53 = (static_cast<uint64_t>(w) << 21) |
+              (philox53(P, L.wid, tie_ctr, 1u) & 0x1FFFFF);
+      dir = 0;
+#pragma unroll
+      for (int d = 0; d < 5; ++d) dir += x53 >= P.ufull[d];
+    }
+    const DirDelta del = dd[dir];
+    L.node += del.node;
+    L.room += del.room;
+    return 0;
+  }
+  bool ex, leaves;
+  if (RNG == FRW_RNG_SPLITMIX_PARITY) {
+    dir = general_dir(alpha_sm, s.P, L, static_cast<double>(z >> 11) * 0x1.0p-53, &ex, &leaves);
+  } else {
+    // the 32-bit word fixes x to [w*2^21, w*2^21 + 2^21): scan both ends;
+    // only when they disagree are the low 21 bits drawn
+    const uint64_t xl = static_cast<uint64_t>(w) << 21;
+    bool ex2, lv2;
+    dir = general_dir(alpha_sm, s.P, L, static_cast<double>(xl) * 0x1.0p-53, &ex, &leaves);
+    const int d2 = general_dir(alpha_sm, s.P, L, static_cast<double>(xl | 0x1FFFFF) * 0x1.0p-53,
+                               &ex2, &lv2);
+    if (d2 != dir) {
+      const uint64_t x53 =
+          xl | (philox53(P, L.wid, tie_ctr, 1u) & 0x1FFFFF);
+      dir = general_dir(alpha_sm, s.P, L, static_cast<double>(x53) * 0x1.0p-53, &ex, &leaves);
+    }
+  }
+  if (ex) {
+    *xdir = dir;
+    return 1;
+  }
+  const DirDelta del = dd[dir];
+  L.node += del.node;
+  if (leaves)
+    mw_cell_change(W, s, n, L, dir);
+  else
+    L.room += del.room;
+  return 0;
+}
+
+__device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* dd) {
+  for (int i = threadIdx.x; i < s.P * s.P; i += blockDim.x) alpha_sm[i] = __ldg(s.alpha + i);
+  if (threadIdx.x < 6) {
+    const int d = threadIdx.x, a = d >> 1;
+    DirDelta x;
+    // moving -a: distance to the low face -1, to the high face +1
+    const uint64_t lo_b = 1ull << (16 * a), hi_b = 1ull << (16 * a + 8);
+    x.room = (d & 1) ? (lo_b - hi_b) : (hi_b - lo_b);
+    x.node = (d & 1) ? (1u << (8 * a)) : static_cast<uint32_t>(-(1 << (8 * a)));
+    x.pad = 0;
+    dd[d] = x;
+  }
+  __syncthreads();
+}
+
+// persistent MicroWalk kernel: each thread runs queued hops back to back
+template <int RNG>
+__global__ void __launch_bounds__(512)
+    k_mw(DStruct s, DParams P, DSlots W, DCounters* C, const int* queue) {
+  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ DirDelta dd[6];
+  setup_smem_tables(s, alpha_sm, dd);
+  const int n = P.n;
+  const int cap = 1000 * n * n;  // microwalk.cpp:81
+  const unsigned long long qlen = C->qlen;
+  MwLane L;
+  unsigned long long item = atomicAdd(&C->qhead, 1ull);
+  bool live = item < qlen;
+  if (live) mw_arm(W, queue[item], n, L);
+  while (__any_sync(0xFFFFFFFFu, live)) {
+    uint32_t w4[4] = {0, 0, 0, 0};
+    if (RNG == FRW_RNG_PHILOX && live) {
+      const uint64_t id = P.walk_begin + L.wid;
+      const U32x4 o = philox4x32_10(
+          {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
+           static_cast<uint32_t>(L.rng), 2u},
+          static_cast<uint32_t>(P.seed), static_cast<uint32_t>(P.seed >> 32));
+      w4[0] = o.x;
+      w4[1] = o.y;
+      w4[2] = o.z;
+      w4[3] = o.w;
+    }
+    bool exited = false;
+    int xdir = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (live && !exited) {
+        uint64_t z = 0;
+        if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
+        if (mw_step<RNG>(s, W, P, alpha_sm, dd, n, L, w4[u], z,
+                         static_cast<uint32_t>(L.rng * 4 + u), &xdir))
+          exited = true;
+      }
+    }
+    if (RNG == FRW_RNG_PHILOX && live) ++L.rng;  // next 4-word block
+    if (live && (exited || L.steps >= cap)) {
+      if (exited)
+        mw_exit(W, n, L, xdir);
+      else
+        set_err(C, FRW_ESTEPCAP);
+      item = atomicAdd(&C->qhead, 1ull);
+      live = item < qlen;
+      if (live) mw_arm(W, queue[item], n, L);
+    }
+  }
+}
+
+// tail: every remaining walk runs to completion in its own thread
+template <int RNG>
+__global__ void __launch_bounds__(256)
+    k_finish(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M) {
+  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ DirDelta dd[6];
+  setup_smem_tables(s, alpha_sm, dd);
+  const int n = P.n;
+  const int cap = 1000 * n * n;
+  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
+       slot += gridDim.x * blockDim.x) {
+    for (;;) {
+      const uint8_t st = W.state[slot];
+      if (st == S_ACTIVE) {
+        if (!advance_slot(s, T, P, W, recs, C, M, slot)) break;
+      } else if (st == S_NEED_MW) {
+        MwLane L;
+        mw_arm(W, slot, n, L);
+        int xdir = -1;
+        bool done = false;
+        while (!done) {
+          uint32_t w4[4] = {0, 0, 0, 0};
+          if (RNG == FRW_RNG_PHILOX) {
+            const uint64_t id = P.walk_begin + L.wid;
+            const U32x4 o = philox4x32_10(
+                {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
+                 static_cast<uint32_t>(L.rng), 2u},
+                static_cast<uint32_t>(P.seed), static_cast<uint32_t>(P.seed >> 32));
+            w4[0] = o.x;
+            w4[1] = o.y;
+            w4[2] = o.z;
+            w4[3] = o.w;
+          }
+          for (int u = 0; u < 4 && !done; ++u) {
+            uint64_t z = 0;
+            if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
+            if (mw_step<RNG>(s, W, P, alpha_sm, dd, n, L, w4[u], z,
+                             static_cast<uint32_t>(L.rng * 4 + u), &xdir))
+              done = true;
+            if (!done && L.steps >= cap) {
+              set_err(C, FRW_ESTEPCAP);
+              done = true;
+              xdir = -1;
+            }
+          }
+          if (RNG == FRW_RNG_PHILOX) ++L.rng;
+        }
+        if (xdir < 0) {
+          W.state[slot] = S_FREE;
+          break;
+        }
+        mw_exit(W, n, L, xdir);
+      } else {
+        break;
+      }
+    }
+  }
+}
+
+// count slots still holding a walk
+__global__ void k_count_active(DSlots W, DCounters* C) {
+  unsigned long long c = 0;
+  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
+       slot += gridDim.x * blockDim.x)
+    c += W.state[slot] != S_FREE;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&C->active, c);
+}
+
+// ---- deterministic tallies -------------------------------------------------
+constexpr int kChunk = 1024;
+
+// per block of kChunk walk records: per-slot sums in walk order
+__global__ void __launch_bounds__(256)
+    k_reduce_chunks(const WalkRec* recs, long long count, int nslots, double* psum,
+                    double* psq, unsigned long long* pland, unsigned long long* pstat) {
+  __shared__ int sl[kChunk];
+  __shared__ double wt[kChunk];
+  const long long base = static_cast<long long>(blockIdx.x) * kChunk;
+  const int m = static_cast<int>(min(static_cast<long long>(kChunk), count - base));
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    sl[i] = recs[base + i].slot;
+    wt[i] = recs[base + i].weight;
+  }
+  __syncthreads();
+  for (int slot = threadIdx.x; slot < nslots; slot += blockDim.x) {
+    double s1 = 0, s2 = 0;
+    unsigned long long c = 0;
+    for (int i = 0; i < m; ++i)
+      if (sl[i] == slot) {
+        const double w = wt[i];
+        s1 += w;
+        s2 += w * w;
+        ++c;
+      }
+    psum[static_cast<size_t>(blockIdx.x) * nslots + slot] = s1;
+    psq[static_cast<size_t>(blockIdx.x) * nslots + slot] = s2;
+    pland[static_cast<size_t>(blockIdx.x) * nslots + slot] = c;
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long st[12] = {0};
+    for (int i = 0; i < m; ++i) {
+      const WalkRec& r = recs[base + i];
+      st[0] += r.aborted;
+      st[1] += r.resampled;
+      if (r.branch < 4) st[2 + r.branch] += 1;
+      st[6] += r.cached;
+      st[7] += r.mw;
+      st[8] += r.mw_steps;
+    }
+    for (int q = 0; q < 12; ++q) pstat[static_cast<size_t>(blockIdx.x) * 12 + q] = st[q];
+  }
+}
+
+__global__ void k_reduce_final(int nblocks, int nslots, const double* psum, const double* psq,
+                               const unsigned long long* pland,
+                               const unsigned long long* pstat, double* osum, double* osq,
+                               unsigned long long* oland, unsigned long long* ostat) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nslots) {
+    double s1 = 0, s2 = 0;
+    unsigned long long c = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      s1 += psum[static_cast<size_t>(b) * nslots + t];
+      s2 += psq[static_cast<size_t>(b) * nslots + t];
+      c += pland[static_cast<size_t>(b) * nslots + t];
+    }
+    osum[t] = s1;
+    osq[t] = s2;
+    oland[t] = c;
+  } else if (t < nslots + 12) {
+    const int q = t - nslots;
+    unsigned long long c = 0;
+    for (int b = 0; b < nblocks; ++b) c += pstat[static_cast<size_t>(b) * 12 + q];
+    ostat[q] = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+// smallest x in [0, 2^53] with fl(x * sum) >= acc * 2^53 (see mw_grid.cu)
+uint64_t threshold_of(double acc, double sum) {
+  const double target = std::ldexp(acc, 53);
+  uint64_t lo = 0, hi = 1ull << 53;
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (static_cast<double>(mid) * sum >= target)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+double host_round_sig(double x, int digits) {  // sgf_cache.cpp:13-18
+  if (x == 0 || !std::isfinite(x)) return x;
+  const double e10 = std::floor(std::log10(std::fabs(x)));
+  const double mag = std::pow(10.0, digits - 1 - e10);
+  return std::round(x * mag) / mag;
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (cudaMalloc(&p, sizeof(T) * (n ? n : 1)) != cudaSuccess) return nullptr;
+  return p;
+}
+
+struct SgfHost {
+  int n = 0;
+  int cap = 0;
+  std::vector<uint64_t> hash;
+  std::vector<int> entry;
+  std::vector<int> axis;
+  std::vector<double> keys;
+  std::vector<double> pitch;
+  std::vector<double*> data;  // device blocks
+  // device mirrors
+  uint64_t* d_hash = nullptr;
+  int* d_entry = nullptr;
+  int* d_axis = nullptr;
+  double* d_keys = nullptr;
+  double* d_pitch = nullptr;
+  double** d_data = nullptr;
+  size_t dev_entries_cap = 0;
+  bool dirty = false;
+};
+
+struct Engine {
+  // structure
+  int nc = 0, nd = 0, P = 0, bg = 0;
+  double world[6];
+  double *d_cbox = nullptr, *d_dbox = nullptr, *d_pal = nullptr, *d_alpha = nullptr,
+         *d_rpal = nullptr;
+  uint8_t* d_dcls = nullptr;
+  bool have_structure = false;
+  SgfHost sgf;
+  // slots
+  int S = 0;
+  DSlots W{};
+  WalkRec* recs = nullptr;
+  long long recs_cap = 0;
+  DCounters* d_cnt = nullptr;
+  DMiss M{};
+  int* queue = nullptr;
+  // reduction scratch
+  double *psum = nullptr, *psq = nullptr, *osum = nullptr, *osq = nullptr;
+  unsigned long long *pland = nullptr, *pstat = nullptr, *oland = nullptr, *ostat = nullptr;
+  size_t red_cap = 0;
+  int red_slots = 0;
+};
+
+void free_slots(Engine& E) {
+  cudaFree(E.W.state);
+  cudaFree(E.W.wid);
+  cudaFree(E.W.p);
+  cudaFree(E.W.weight);
+  cudaFree(E.W.rng);
+  cudaFree(E.W.hops);
+  cudaFree(E.W.cached);
+  cudaFree(E.W.mw);
+  cudaFree(E.W.mwsteps);
+  cudaFree(E.W.branch);
+  cudaFree(E.W.resampled);
+  cudaFree(E.W.cube);
+  cudaFree(E.W.nbox);
+  cudaFree(E.W.boxes);
+  cudaFree(E.W.room);
+  cudaFree(E.W.fc);
+  cudaFree(E.queue);
+  cudaFree(E.M.retry);
+  cudaFree(E.M.pend);
+  E.W = DSlots{};
+  E.S = 0;
+}
+
+void engine_free(frw_ctx* ctx) {
+  Engine* E = static_cast<Engine*>(ctx->walk);
+  if (!E) return;
+  cudaFree(E->d_cbox);
+  cudaFree(E->d_dbox);
+  cudaFree(E->d_pal);
+  cudaFree(E->d_alpha);
+  cudaFree(E->d_rpal);
+  cudaFree(E->d_dcls);
+  for (double* p : E->sgf.data) cudaFree(p);
+  cudaFree(E->sgf.d_hash);
+  cudaFree(E->sgf.d_entry);
+  cudaFree(E->sgf.d_axis);
+  cudaFree(E->sgf.d_keys);
+  cudaFree(E->sgf.d_pitch);
+  cudaFree(E->sgf.d_data);
+  free_slots(*E);
+  cudaFree(E->recs);
+  cudaFree(E->d_cnt);
+  cudaFree(E->M.axis);
+  cudaFree(E->M.layers);
+  cudaFree(E->psum);
+  cudaFree(E->psq);
+  cudaFree(E->pland);
+  cudaFree(E->pstat);
+  cudaFree(E->osum);
+  cudaFree(E->osq);
+  cudaFree(E->oland);
+  cudaFree(E->ostat);
+  delete E;
+  ctx->walk = nullptr;
+}
+
+Engine* engine_of(frw_ctx* ctx) {
+  if (!ctx->walk) {
+    ctx->walk = new Engine;
+    ctx->walk_free = engine_free;
+  }
+  return static_cast<Engine*>(ctx->walk);
+}
+
+uint64_t host_key_hash(int n, int axis, const double* layers) {
+  uint64_t h = sm64_mix((static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis));
+  for (int t = 0; t < n; ++t) {
+    uint64_t b;
+    std::memcpy(&b, &layers[t], 8);
+    h = sm64_mix(h ^ b);
+  }
+  return h;
+}
+
+int sgf_sync(frw_ctx* ctx, SgfHost& T) {
+  if (!T.dirty) return FRW_OK;
+  const size_t ne = T.axis.size();
+  if (ne > T.dev_entries_cap || !T.d_axis) {
+    const size_t cap = std::max<size_t>(64, ne * 2);
+    cudaFree(T.d_axis);
+    cudaFree(T.d_keys);
+    cudaFree(T.d_pitch);
+    cudaFree(T.d_data);
+    T.d_axis = dalloc<int>(cap);
+    T.d_keys = dalloc<double>(cap * NMAX);
+    T.d_pitch = dalloc<double>(cap);
+    T.d_data = dalloc<double*>(cap);
+    if (!T.d_axis || !T.d_keys || !T.d_pitch || !T.d_data)
+      return frw_fail(ctx, FRW_ENOMEM, "sgf table: device allocation failed");
+    T.dev_entries_cap = cap;
+  }
+  cudaFree(T.d_hash);
+  cudaFree(T.d_entry);
+  T.d_hash = dalloc<uint64_t>(T.cap);
+  T.d_entry = dalloc<int>(T.cap);
+  FRW_CUDA(ctx, cudaMemcpy(T.d_hash, T.hash.data(), 8 * T.cap, cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpy(T.d_entry, T.entry.data(), 4 * T.cap, cudaMemcpyHostToDevice));
+  if (ne) {
+    FRW_CUDA(ctx, cudaMemcpy(T.d_axis, T.axis.data(), 4 * ne, cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(T.d_keys, T.keys.data(), 8 * ne * NMAX, cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(T.d_pitch, T.pitch.data(), 8 * ne, cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(T.d_data, T.data.data(), sizeof(double*) * ne,
+                             cudaMemcpyHostToDevice));
+  }
+  T.dirty = false;
+  return FRW_OK;
+}
+
+void sgf_insert_index(SgfHost& T, uint64_t h, int e) {
+  if ((T.axis.size() + 1) * 2 > static_cast<size_t>(T.cap)) {
+    const int ncap = std::max(256, T.cap * 2);
+    std::vector<uint64_t> nh(ncap, 0);
+    std::vector<int> ne(ncap, -1);
+    for (int i = 0; i < T.cap; ++i)
+      if (T.entry[i] >= 0) {
+        int j = static_cast<int>(T.hash[i] & (ncap - 1));
+        while (ne[j] >= 0) j = (j + 1) & (ncap - 1);
+        nh[j] = T.hash[i];
+        ne[j] = T.entry[i];
+      }
+    T.hash.swap(nh);
+    T.entry.swap(ne);
+    T.cap = ncap;
+  }
+  int j = static_cast<int>(h & (T.cap - 1));
+  while (T.entry[j] >= 0) j = (j + 1) & (T.cap - 1);
+  T.hash[j] = h;
+  T.entry[j] = e;
+}
+
+int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
+  if (E.S == S) return FRW_OK;
+  free_slots(E);
+  DSlots& W = E.W;
+  W.S = S;
+  W.state = dalloc<uint8_t>(S);
+  W.wid = dalloc<long long>(S);
+  W.p = dalloc<double>(3 * size_t(S));
+  W.weight = dalloc<double>(S);
+  W.rng = dalloc<uint64_t>(S);
+  W.hops = dalloc<int>(S);
+  W.cached = dalloc<uint32_t>(S);
+  W.mw = dalloc<uint32_t>(S);
+  W.mwsteps = dalloc<uint64_t>(S);
+  W.branch = dalloc<uint8_t>(S);
+  W.resampled = dalloc<uint8_t>(S);
+  W.cube = dalloc<double>(4 * size_t(S));
+  W.nbox = dalloc<uint8_t>(S);
+  W.boxes = dalloc<uint64_t>(size_t(S) * KMAX);
+  W.room = dalloc<uint64_t>(S);
+  W.fc = dalloc<uint64_t>(S);
+  E.queue = dalloc<int>(S);
+  E.M.retry = dalloc<long long>(S);
+  E.M.pend = dalloc<long long>(S);
+  if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
+      !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes || !W.room ||
+      !W.fc || !E.queue || !E.M.retry || !E.M.pend) {
+    free_slots(E);
+    return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
+  }
+  E.S = S;
+  return FRW_OK;
+}
+
+}  // namespace
+}  // namespace frw
+
+using namespace frw;
+
+extern "C" {
+
+int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
+  if (!ctx || !s) return FRW_EINVAL;
+  if (s->n_cond < 1 || s->n_diel < 0 || !s->cond_box || (s->n_diel > 0 && (!s->diel_box || !s->diel_eps)))
+    return frw_fail(ctx, FRW_EINVAL, "upload_structure: malformed structure");
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  Engine& E = *engine_of(ctx);
+  // palette of distinct permittivities (background first)
+  std::vector<double> pal{s->background_eps};
+  std::vector<uint8_t> dcls(s->n_diel);
+  for (int d = 0; d < s->n_diel; ++d) {
+    const double e = s->diel_eps[d];
+    int k = -1;
+    for (size_t q = 0; q < pal.size(); ++q)
+      if (std::memcmp(&pal[q], &e, 8) == 0) k = static_cast<int>(q);
+    if (k < 0) {
+      if (pal.size() >= static_cast<size_t>(PMAX) - 1)
+        return frw_fail(ctx, FRW_EINVAL, "upload_structure: more than 63 distinct permittivities");
+      k = static_cast<int>(pal.size());
+      pal.push_back(e);
+    }
+    dcls[d] = static_cast<uint8_t>(k);
+  }
+  const int P = static_cast<int>(pal.size());
+  std::vector<double> alpha(static_cast<size_t>(P) * P), rpal(P);
+  for (int a = 0; a < P; ++a) {
+    rpal[a] = host_round_sig(pal[a], 6);
+    for (int b = 0; b < P; ++b) alpha[a * P + b] = pal[a] / (pal[a] + pal[b]);
+  }
+  cudaFree(E.d_cbox);
+  cudaFree(E.d_dbox);
+  cudaFree(E.d_pal);
+  cudaFree(E.d_alpha);
+  cudaFree(E.d_rpal);
+  cudaFree(E.d_dcls);
+  E.d_cbox = dalloc<double>(6 * size_t(s->n_cond));
+  E.d_dbox = dalloc<double>(6 * size_t(s->n_diel));
+  E.d_dcls = dalloc<uint8_t>(s->n_diel);
+  E.d_pal = dalloc<double>(P);
+  E.d_alpha = dalloc<double>(size_t(P) * P);
+  E.d_rpal = dalloc<double>(P);
+  if (!E.d_cbox || !E.d_dbox || !E.d_dcls || !E.d_pal || !E.d_alpha || !E.d_rpal)
+    return frw_fail(ctx, FRW_ENOMEM, "upload_structure: device allocation failed");
+  FRW_CUDA(ctx, cudaMemcpy(E.d_cbox, s->cond_box, 48 * size_t(s->n_cond), cudaMemcpyHostToDevice));
+  if (s->n_diel) {
+    FRW_CUDA(ctx, cudaMemcpy(E.d_dbox, s->diel_box, 48 * size_t(s->n_diel), cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(E.d_dcls, dcls.data(), s->n_diel, cudaMemcpyHostToDevice));
+  }
+  FRW_CUDA(ctx, cudaMemcpy(E.d_pal, pal.data(), 8 * P, cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpy(E.d_alpha, alpha.data(), 8 * size_t(P) * P, cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpy(E.d_rpal, rpal.data(), 8 * P, cudaMemcpyHostToDevice));
+  E.nc = s->n_cond;
+  E.nd = s->n_diel;
+  E.P = P;
+  E.bg = 0;
+  std::memcpy(E.world, s->world, sizeof E.world);
+  E.have_structure = true;
+  return FRW_OK;
+}
+
+int frw_sgf_put(frw_ctx* ctx, int n, int axis, const double* layers, double pitch,
+                const double* probs, const double* cdf, const double* kernels) {
+  if (!ctx || !layers || !probs || !cdf) return FRW_EINVAL;
+  if (n < 1 || n > NMAX || axis < 0 || axis > 2)
+    return frw_fail(ctx, FRW_EINVAL, "sgf_put: need 1 <= n <= 64 and 0 <= axis <= 2");
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  Engine& E = *engine_of(ctx);
+  SgfHost& T = E.sgf;
+  if (T.n && T.n != n) return frw_fail(ctx, FRW_EINVAL, "sgf_put: one lattice size per table");
+  T.n = n;
+  const uint64_t h = host_key_hash(n, axis, layers);
+  for (int i = static_cast<int>(h & (T.cap ? T.cap - 1 : 0)); T.cap; i = (i + 1) & (T.cap - 1)) {
+    const int e = T.entry[i];
+    if (e < 0) break;
+    if (T.hash[i] == h && T.axis[e] == axis &&
+        std::memcmp(&T.keys[static_cast<size_t>(e) * NMAX], layers, 8 * n) == 0)
+      return FRW_OK;  // first stored result wins (sgf_cache.cpp:133-153)
+  }
+  const size_t panels = 6ull * n * n;
+  double* blk = dalloc<double>(5 * panels);
+  if (!blk) return frw_fail(ctx, FRW_ENOMEM, "sgf_put: device allocation failed");
+  FRW_CUDA(ctx, cudaMemcpy(blk, cdf, 8 * panels, cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpy(blk + panels, probs, 8 * panels, cudaMemcpyHostToDevice));
+  if (kernels)
+    FRW_CUDA(ctx, cudaMemcpy(blk + 2 * panels, kernels, 24 * panels, cudaMemcpyHostToDevice));
+  else
+    FRW_CUDA(ctx, cudaMemset(blk + 2 * panels, 0, 24 * panels));
+  const int e = static_cast<int>(T.axis.size());
+  T.axis.push_back(axis);
+  T.keys.resize(static_cast<size_t>(e + 1) * NMAX, 0.0);
+  std::memcpy(&T.keys[static_cast<size_t>(e) * NMAX], layers, 8 * n);
+  T.pitch.push_back(pitch);
+  T.data.push_back(blk);
+  sgf_insert_index(T, h, e);
+  T.dirty = true;
+  return FRW_OK;
+}
+
+int frw_sgf_count(const frw_ctx* ctx, int* entries) {
+  if (!ctx || !entries) return FRW_EINVAL;
+  const Engine* E = static_cast<const Engine*>(ctx->walk);
+  *entries = E ? static_cast<int>(E->sgf.axis.size()) : 0;
+  return FRW_OK;
+}
+
+int frw_sgf_clear(frw_ctx* ctx) {
+  if (!ctx) return FRW_EINVAL;
+  Engine& E = *engine_of(ctx);
+  for (double* p : E.sgf.data) cudaFree(p);
+  SgfHost fresh;
+  fresh.d_hash = E.sgf.d_hash;
+  fresh.d_entry = E.sgf.d_entry;
+  fresh.d_axis = E.sgf.d_axis;
+  fresh.d_keys = E.sgf.d_keys;
+  fresh.d_pitch = E.sgf.d_pitch;
+  fresh.d_data = E.sgf.d_data;
+  fresh.dev_entries_cap = E.sgf.dev_entries_cap;
+  fresh.dirty = true;
+  E.sgf = fresh;
+  return FRW_OK;
+}
+
+static_assert(sizeof(WalkRec) == sizeof(frw_walk_record), "record layout");
+
+int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint64_t walk_begin,
+                  int64_t count, frw_miss_fn miss, void* user, frw_tally* out,
+                  frw_walk_record* records) {
+  if (!ctx || !prm || !out) return FRW_EINVAL;
+  Engine& E = *engine_of(ctx);
+  if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "run_walks: no structure uploaded");
+  if (prm->grid_n < 2 || prm->grid_n > NMAX)
+    return frw_fail(ctx, FRW_EINVAL, "run_walks: grid_n must lie in [2, 64]");
+  if (prm->mode != FRW_MODE_MW && prm->mode != FRW_MODE_HYBRID_MW)
+    return frw_fail(ctx, FRW_EINVAL,
+                    "run_walks: only MW / HYBRID-MW transitions run on the device in this build");
+  if (master < 0 || master >= E.nc) return frw_fail(ctx, FRW_EINVAL, "run_walks: bad master");
+  if (count < 0) return frw_fail(ctx, FRW_EINVAL, "run_walks: count < 0");
+  if (E.sgf.n && E.sgf.n != prm->grid_n)
+    return frw_fail(ctx, FRW_EINVAL, "run_walks: SGF table holds another lattice size");
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int nslots = E.nc + 1;
+  cudaEvent_t t0, t1, m0, m1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  cudaEventCreate(&m0);
+  cudaEventCreate(&m1);
+  cudaEventRecord(t0, ctx->stream);
+
+  const int S = prm->n_slots > 0 ? prm->n_slots : kSlotsDefault;
+  if (int rc = ensure_slots(ctx, E, S)) return rc;
+  if (E.recs_cap < count) {
+    cudaFree(E.recs);
+    E.recs = dalloc<WalkRec>(count);
+    if (!E.recs) return frw_fail(ctx, FRW_ENOMEM, "run_walks: record allocation failed");
+    E.recs_cap = count;
+  }
+  if (!E.d_cnt) {
+    E.d_cnt = dalloc<DCounters>(1);
+    E.M.axis = dalloc<int>(kMissMax);
+    E.M.layers = dalloc<double>(size_t(kMissMax) * NMAX);
+  }
+  if (int rc = sgf_sync(ctx, E.sgf)) return rc;
+
+  DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal, {}};
+  std::memcpy(s.world, E.world, sizeof s.world);
+  DParams P{};
+  P.n = prm->grid_n;
+  P.panels = 6 * P.n * P.n;
+  P.mode = prm->mode;
+  P.rng = prm->rng_mode;
+  P.snap = prm->snap;
+  P.hop_cap = prm->hop_cap;
+  P.seed = prm->seed;
+  P.mixed_seed = sm64_mix(prm->seed);
+  std::memcpy(P.gbox, prm->gauss_box, sizeof P.gbox);
+  std::memcpy(P.fcdf, prm->face_cdf, sizeof P.fcdf);
+  P.area = prm->area_m2;
+  {
+    // uniform interior record: alpha = 1/2 in all six directions
+    double acc = 0;
+    uint64_t rec = 0;
+    for (int d = 0; d < 5; ++d) {
+      acc += 0.5;
+      const uint64_t X = threshold_of(acc, 3.0);
+      P.ufull[d] = X;
+      rec |= (1023 - std::min<uint64_t>(X >> 43, 1023)) << (11 * d);
+    }
+    P.urec = rec;
+  }
+  P.walk_begin = walk_begin;
+  P.count = count;
+  P.master = master;
+  DMiss M = E.M;
+
+  FRW_CUDA(ctx, cudaMemsetAsync(E.W.state, 0, S, ctx->stream));
+  FRW_CUDA(ctx, cudaMemsetAsync(E.recs, 0, sizeof(WalkRec) * count, ctx->stream));
+  FRW_CUDA(ctx, cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), ctx->stream));
+  const int grid = ctx->sm_count * 8;
+  const int mw_grid = ctx->sm_count * 2;  // 2 x 512 threads per SM
+  float mw_ms = 0;
+  uint64_t misses_total = 0, restarts = 0;
+  std::vector<int> maxis;
+  std::vector<double> mlayers;
+  int status = FRW_OK;
+  bool tail = false;
+  for (int round = 0;; ++round) {
+    DSgf T{E.sgf.cap, E.sgf.d_hash, E.sgf.d_entry, E.sgf.d_axis, E.sgf.d_keys, E.sgf.d_pitch,
+           E.sgf.d_data};
+    if (!tail) {
+      k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M);
+      k_advance<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, E.queue);
+      cudaEventRecord(m0, ctx->stream);
+      if (P.rng == FRW_RNG_PHILOX)
+        k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt, E.queue);
+      else
+        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt,
+                                                                        E.queue);
+      cudaEventRecord(m1, ctx->stream);
+    } else {
+      if (P.rng == FRW_RNG_PHILOX)
+        k_finish<FRW_RNG_PHILOX><<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M);
+      else
+        k_finish<FRW_RNG_SPLITMIX_PARITY><<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs,
+                                                                         E.d_cnt, M);
+    }
+    FRW_CUDA(ctx, cudaGetLastError());
+    FRW_CUDA(ctx, cudaMemsetAsync(&E.d_cnt->active, 0, 8, ctx->stream));
+    k_count_active<<<grid, 256, 0, ctx->stream>>>(E.W, E.d_cnt);
+    DCounters c;
+    FRW_CUDA(ctx, cudaMemcpyAsync(&c, E.d_cnt, sizeof c, cudaMemcpyDeviceToHost, ctx->stream));
+    FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (!tail) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, m0, m1);
+      mw_ms += ms;
+    }
+    if (c.err) {
+      status = -static_cast<int>(c.err);
+      frw_fail(ctx, status,
+               status == FRW_ESTEPCAP
+                   ? "microwalk transit exceeded the step cap; the lattice is malformed"
+                   : "walk engine: geometry error (point outside the world or inside a "
+                     "conductor, or more than 32 dielectric boxes in one cube)");
+      break;
+    }
+    // reset the MicroWalk queue for the next round
+    FRW_CUDA(ctx, cudaMemsetAsync(&E.d_cnt->qlen, 0, 16, ctx->stream));
+    if (c.nmiss) {
+      if (!miss) {
+        status = frw_fail(ctx, FRW_EMISS, "run_walks: SGF table miss and no miss callback");
+        break;
+      }
+      const int nm = static_cast<int>(std::min<unsigned long long>(c.nmiss, kMissMax));
+      maxis.resize(nm);
+      mlayers.resize(static_cast<size_t>(nm) * NMAX);
+      FRW_CUDA(ctx, cudaMemcpy(maxis.data(), M.axis, 4 * nm, cudaMemcpyDeviceToHost));
+      FRW_CUDA(ctx, cudaMemcpy(mlayers.data(), M.layers, 8 * size_t(nm) * NMAX,
+                               cudaMemcpyDeviceToHost));
+      std::unordered_map<uint64_t, int> seen;
+      std::vector<int> uaxis;
+      std::vector<double> ulayers;
+      for (int q = 0; q < nm; ++q) {
+        const double* L = &mlayers[static_cast<size_t>(q) * NMAX];
+        const uint64_t h = host_key_hash(P.n, maxis[q], L);
+        auto it = seen.find(h);
+        if (it != seen.end() && maxis[it->second] == maxis[q] &&
+            std::memcmp(&mlayers[static_cast<size_t>(it->second) * NMAX], L, 8 * P.n) == 0)
+          continue;
+        seen[h] = q;
+        uaxis.push_back(maxis[q]);
+        ulayers.insert(ulayers.end(), L, L + P.n);
+      }
+      const int before = static_cast<int>(E.sgf.axis.size());
+      if (miss(user, P.n, static_cast<int>(uaxis.size()), uaxis.data(), ulayers.data()) != 0) {
+        status = frw_fail(ctx, FRW_ESOLVE, "run_walks: miss callback failed");
+        break;
+      }
+      if (static_cast<int>(E.sgf.axis.size()) == before) {
+        status = frw_fail(ctx, FRW_EMISS, "run_walks: miss callback added no table entry");
+        break;
+      }
+      misses_total += E.sgf.axis.size() - before;
+      if (status) break;
+      if (int rc = sgf_sync(ctx, E.sgf)) {
+        status = rc;
+        break;
+      }
+      // parked walks restart from scratch; nothing of their partial run was
+      // committed.  pend <- retry
+      FRW_CUDA(ctx, cudaMemcpyAsync(M.pend, M.retry, 8 * c.nretry, cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+      DCounters upd = c;
+      upd.npend = c.nretry;
+      upd.pend_head = 0;
+      upd.nretry = 0;
+      upd.nmiss = 0;
+      upd.qlen = 0;
+      upd.qhead = 0;
+      upd.active = 0;
+      FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cnt, &upd, sizeof upd, cudaMemcpyHostToDevice,
+                                    ctx->stream));
+      restarts += c.nretry;
+      tail = false;
+      continue;
+    }
+    const bool all_spawned = c.next >= static_cast<unsigned long long>(count) &&
+                             c.pend_head >= c.npend;
+    if (all_spawned && c.active == 0 && c.done >= static_cast<unsigned long long>(count)) break;
+    if (all_spawned && c.active == 0 && c.done < static_cast<unsigned long long>(count)) {
+      status = frw_fail(ctx, FRW_ECUDA, "run_walks: lost walks (internal error)");
+      break;
+    }
+    // few walks left: finish them in-thread instead of paying a round each
+    tail = all_spawned && c.active < static_cast<unsigned long long>(S) / 16;
+  }
+  if (status == FRW_OK) {
+    // deterministic tallies
+    const int nblocks = static_cast<int>((count + kChunk - 1) / kChunk);
+    if (E.red_cap < static_cast<size_t>(std::max(nblocks, 1)) * nslots || E.red_slots != nslots) {
+      cudaFree(E.psum);
+      cudaFree(E.psq);
+      cudaFree(E.pland);
+      cudaFree(E.pstat);
+      cudaFree(E.osum);
+      cudaFree(E.osq);
+      cudaFree(E.oland);
+      cudaFree(E.ostat);
+      const size_t cap = static_cast<size_t>(std::max(nblocks, 1)) * nslots;
+      E.psum = dalloc<double>(cap);
+      E.psq = dalloc<double>(cap);
+      E.pland = dalloc<unsigned long long>(cap);
+      E.pstat = dalloc<unsigned long long>(static_cast<size_t>(std::max(nblocks, 1)) * 12);
+      E.osum = dalloc<double>(nslots);
+      E.osq = dalloc<double>(nslots);
+      E.oland = dalloc<unsigned long long>(nslots);
+      E.ostat = dalloc<unsigned long long>(12);
+      E.red_cap = cap;
+      E.red_slots = nslots;
+    }
+    std::vector<unsigned long long> st(12, 0);
+    if (count > 0) {
+      k_reduce_chunks<<<nblocks, 256, 0, ctx->stream>>>(E.recs, count, nslots, E.psum, E.psq,
+                                                         E.pland, E.pstat);
+      k_reduce_final<<<(nslots + 12 + 127) / 128, 128, 0, ctx->stream>>>(
+          nblocks, nslots, E.psum, E.psq, E.pland, E.pstat, E.osum, E.osq, E.oland, E.ostat);
+      FRW_CUDA(ctx, cudaGetLastError());
+      if (out->sum)
+        FRW_CUDA(ctx, cudaMemcpyAsync(out->sum, E.osum, 8 * nslots, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+      if (out->sumsq)
+        FRW_CUDA(ctx, cudaMemcpyAsync(out->sumsq, E.osq, 8 * nslots, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+      if (out->landed)
+        FRW_CUDA(ctx, cudaMemcpyAsync(out->landed, E.oland, 8 * nslots, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+      FRW_CUDA(ctx, cudaMemcpyAsync(st.data(), E.ostat, 8 * 12, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    } else {
+      for (int k = 0; k < nslots; ++k) {
+        if (out->sum) out->sum[k] = 0;
+        if (out->sumsq) out->sumsq[k] = 0;
+        if (out->landed) out->landed[k] = 0;
+      }
+    }
+    if (records && count > 0)
+      FRW_CUDA(ctx, cudaMemcpyAsync(records, E.recs, sizeof(WalkRec) * count,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    cudaEventRecord(t1, ctx->stream);
+    FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    out->aborted = st[0];
+    out->resampled = st[1];
+    for (int b = 0; b < 4; ++b) out->first[b] = st[2 + b];
+    out->sub[0] = st[6];
+    out->sub[1] = st[7];
+    out->sub[2] = 0;
+    out->sub[3] = 0;
+    out->mw_steps = st[8];
+    out->cache_misses = misses_total;
+    out->cache_hits = 0;
+    out->restarts = restarts;
+    out->mw_ms = mw_ms;
+    float tot = 0;
+    cudaEventElapsedTime(&tot, t0, t1);
+    out->total_ms = tot;
+  }
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaEventDestroy(m0);
+  cudaEventDestroy(m1);
+  return status;
+}
+
+}  // extern "C"

@@ -1,0 +1,29 @@
+"""Floating random walk capacitance extraction -- B200 device build.
+
+Drop-in for the reference package `frwcap` (proj/python/frwcap/__init__.py):
+the same eight names, backed by the pybind11 module `_core` built from
+paper_2507_09730_b200/csrc/host over the CUDA library lib/libfrwgpu.so.
+"""
+from .._core import (  # noqa: F401
+    __version__,
+    analytic_plate_capacitance,
+    expected_steps_uniform,
+    extract_file,
+    extract_json,
+    reference_capacitance_file,
+    run_cli,
+    transit_tv,
+)
+from .._core import run_walks_json, sgf_cache_clear, sgf_cache_load, sgf_cache_save  # noqa: F401
+from .._core import sgf_cache_stats  # noqa: F401
+
+__all__ = [
+    "analytic_plate_capacitance",
+    "expected_steps_uniform",
+    "extract_file",
+    "extract_json",
+    "reference_capacitance_file",
+    "run_cli",
+    "transit_tv",
+    "__version__",
+]
