@@ -196,6 +196,8 @@ typedef struct {
   uint64_t cache_misses;  /* distinct keys handed to the miss callback    */
   uint64_t mw_steps;      /* total MicroWalk lattice steps                */
   uint64_t restarts;      /* walks re-run after a table miss              */
+  uint64_t mw_general_steps; /* MicroWalk steps next to a cell face        */
+  uint64_t mw_cell_changes;  /* MicroWalk moves across a cell face         */
   double mw_ms;           /* device time of the MicroWalk kernel          */
   double total_ms;        /* device time of the whole call                */
 } frw_tally;

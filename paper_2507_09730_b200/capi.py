@@ -69,7 +69,9 @@ class Tally(C.Structure):
                 ("landed", C.POINTER(C.c_uint64)), ("aborted", C.c_uint64),
                 ("resampled", C.c_uint64), ("first", C.c_uint64 * 4), ("sub", C.c_uint64 * 4),
                 ("cache_hits", C.c_uint64), ("cache_misses", C.c_uint64),
-                ("mw_steps", C.c_uint64), ("restarts", C.c_uint64), ("mw_ms", C.c_double),
+                ("mw_steps", C.c_uint64), ("restarts", C.c_uint64),
+                ("mw_general_steps", C.c_uint64), ("mw_cell_changes", C.c_uint64),
+                ("mw_ms", C.c_double),
                 ("total_ms", C.c_double)]
 
 
@@ -325,6 +327,7 @@ class Context:
         tally = dict(sum=s1, sumsq=s2, landed=land, aborted=t.aborted, resampled=t.resampled,
                      first=list(t.first), sub=list(t.sub), misses=t.cache_misses,
                      mw_steps=t.mw_steps, restarts=t.restarts, mw_ms=t.mw_ms,
+                     mw_general_steps=t.mw_general_steps, mw_cell_changes=t.mw_cell_changes,
                      total_ms=t.total_ms)
         return tally, rec
 

@@ -23,7 +23,6 @@
 //              integer threshold compare of mw_grid.cu, steps next to an
 //              interface use the reference's f64 scan with alphas read from
 //              a palette-pair table (no division)
-//   k_finish   the tail: each remaining walk runs to completion in-thread
 //   k_reduce*  per-walk records -> per-terminal tallies in a fixed order
 // All geometry and voxel-centre arithmetic is compiled with -fmad=false so
 // it rounds exactly like the reference (x86-64 baseline, no contraction).
@@ -44,7 +43,7 @@ namespace {
 constexpr int KMAX = 32;    // clipped dielectric boxes per MicroWalk cube
 constexpr int NMAX = 64;    // lattice size cap (layers per key)
 constexpr int PMAX = 64;    // permittivity palette cap
-constexpr int kSlotsDefault = 1 << 19;
+constexpr int kSlotsDefault = 1 << 20;
 constexpr double kEps0 = 8.8541878128e-12;  // constants.hpp:5
 constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
@@ -123,17 +122,25 @@ struct DSlots {
   uint64_t* fc;          // [S] start cell + face-neighbour classes
 };
 
+// Work queues of one round: k_spawn and the previous round's k_mw fill the
+// ACTIVE queue; k_advance drains it (one transition per pop, lanes re-armed
+// as their walk leaves the stage) and fills the MicroWalk queue; k_mw drains
+// that and fills the next round's ACTIVE queue.
 struct DCounters {
   unsigned long long next;       // next new walk id
   unsigned long long done;       // walks finished
   unsigned long long qlen;       // MicroWalk queue length
   unsigned long long qhead;      // MicroWalk queue head
+  unsigned long long alen;       // ACTIVE queue length (this round)
+  unsigned long long ahead;      // ACTIVE queue head
+  unsigned long long a2len;      // ACTIVE queue of the next round
   unsigned long long nmiss;      // miss records written
   unsigned long long npend;      // pending restarts available
   unsigned long long pend_head;  // pending restarts consumed
   unsigned long long nretry;     // walks parked by a miss this round
-  unsigned long long active;     // slots ACTIVE/NEED_MW after k_advance
   unsigned long long err;        // error code (first)
+  unsigned long long gen_steps;  // MicroWalk steps next to a cell face
+  unsigned long long cell_chg;   // MicroWalk moves into another cell
 };
 
 constexpr int kMissMax = 4096;
@@ -189,6 +196,25 @@ __device__ bool max_free_cube(const DStruct& s, const double p[3], double* h) {
   }
   *h = r;
   return true;
+}
+
+// The geometry prologue of Engine::transition (engine.cpp:293-298) in one
+// pass over the conductors: conductor_at(p, snap) -> its declaration index;
+// the world wall within snap -> -1 (ground); else the max free cube half
+// width in *h and -3.  (A conductor at d <= 0 would have been caught by the
+// snap test first, so max_free_cube's inside-conductor throw cannot fire.)
+__device__ int hop_scan(const DStruct& s, const double p[3], double snap, double* h) {
+  const double wall = cheb_wall(s.world, p);
+  double r = wall;
+  for (int c = 0; c < s.nc; ++c) {
+    const double d = cheb_to(s.cbox + 6 * c, p);
+    if (d <= snap) return c;
+    if (d <= r) r = d;
+  }
+  if (wall <= snap) return -1;
+  if (r <= 0) return -2;
+  *h = r;
+  return -3;
 }
 
 // Structure::permittivity_at (geometry.cpp:47-55) as a palette class;
@@ -329,15 +355,23 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
   const double pitch = 2.0 * h / n;
   int cls0 = -1;
   bool uniform = true;
+  // Every hit box covers the cube's cross-section, so it contains the slice
+  // centre's other two coordinates (the cube centre) and, the cube lying in
+  // the world, so does the world box: only the axis coordinate decides.
+  double hl[KMAX], hh[KMAX];
+  if (!overflow)
+    for (int q = 0; q < nh; ++q) {
+      hl[q] = __ldg(s.dbox + 6 * hits[q] + axis);
+      hh[q] = __ldg(s.dbox + 6 * hits[q] + 3 + axis);
+    }
   for (int t = 0; t < n; ++t) {
     double p[3] = {c[0], c[1], c[2]};
     p[axis] = c[axis] - h + (t + 0.5) * pitch;
     int cls;
     if (!overflow) {
-      if (!box_contains(s.world, p)) return -2;
       cls = s.bg;
       for (int q = 0; q < nh; ++q)
-        if (box_contains(s.dbox + 6 * hits[q], p)) cls = __ldg(s.dcls + hits[q]);
+        if (p[axis] >= hl[q] && p[axis] <= hh[q]) cls = __ldg(s.dcls + hits[q]);
     } else {
       cls = eps_class_at(s, p);
       if (cls < 0) return -2;
@@ -355,10 +389,16 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
   return axis;
 }
 
+// multiply-xorshift over the layer bit patterns, one full mix at the end
+__host__ __device__ __forceinline__ uint64_t key_step(uint64_t h, uint64_t w) {
+  h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+  return h ^ (h >> 29);
+}
 __device__ __forceinline__ uint64_t key_hash(int n, int axis, const double* layers) {
-  uint64_t h = sm64_mix((static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis));
-  for (int t = 0; t < n; ++t) h = sm64_mix(h ^ static_cast<uint64_t>(__double_as_longlong(layers[t])));
-  return h;
+  uint64_t h = (static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis);
+  for (int t = 0; t < n; ++t)
+    h = key_step(h, static_cast<uint64_t>(__double_as_longlong(layers[t])));
+  return sm64_mix(h);
 }
 
 // table lookup; entry index or -1
@@ -376,18 +416,17 @@ __device__ int sgf_find(const DSgf& T, int n, int axis, const double* layers) {
   }
 }
 
-// sample_panel (sgf.cpp:301-308): upper_bound on the inclusive cdf
-__device__ int sample_panel(const double* cdf, int count, double u) {
+// sample_panel (sgf.cpp:301-308): upper_bound on the inclusive cdf, entered
+// through a guide table (Chen & Asau).  guide[b] is the first index whose
+// cdf exceeds fl((b/G)*total); since b = floor(u*G) gives b/G <= u exactly
+// and rounding is monotone, every earlier index has cdf <= target, so the
+// forward scan returns exactly the upper_bound answer.
+constexpr int kGuide = 2048;
+__device__ int sample_panel(const double* cdf, const int* guide, int count, double u) {
   const double target = u * __ldg(cdf + count - 1);
-  int lo = 0, hi = count;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (target < __ldg(cdf + mid))
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  return lo == count ? count - 1 : lo;
+  int i = __ldg(guide + static_cast<int>(u * kGuide));
+  while (i < count && __ldg(cdf + i) <= target) ++i;
+  return i == count ? count - 1 : i;
 }
 
 __device__ void record_miss(DCounters* C, const DMiss& M, int n, int axis, const double* layers,
@@ -642,7 +681,8 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
   }
   const double* data = T.data[e];
   const int panels = P.panels;
-  const int panel = sample_panel(data, panels, uniform(P, wid, rng));
+  const int panel = sample_panel(data, reinterpret_cast<const int*>(data + 5 * panels), panels,
+                                 uniform(P, wid, rng));
   const double pitch_nm = 2.0 * h / n;
   const double kern_per_m =
       __ldg(data + 2 * panels + gaxis * panels + panel) * (__ldg(T.pitch + e) / pitch_nm) /
@@ -679,7 +719,7 @@ __device__ void finish_walk(const DSlots& W, WalkRec* recs, DCounters* C, int sl
 
 // Gaussian sample + first transition for every free slot
 __global__ void k_spawn(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C,
-                        DMiss M) {
+                        DMiss M, int* aq) {
   for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
        slot += gridDim.x * blockDim.x) {
     if (W.state[slot] != S_FREE) continue;
@@ -745,91 +785,122 @@ __global__ void k_spawn(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, D
     W.branch[slot] = static_cast<uint8_t>(fo.branch);
     W.rng[slot] = rng.s;
     W.state[slot] = S_ACTIVE;
+    aq[atomicAdd(&C->alen, 1ull)] = slot;
   }
 }
 
-// One transition (engine.cpp:290-350) for an ACTIVE slot; cached hops loop
-// inline.  Returns true when the slot still needs work (NEED_MW).
-__device__ bool advance_slot(const DStruct& s, const DSgf& T, const DParams& P, const DSlots& W,
-                             WalkRec* recs, DCounters* C, const DMiss& M, int slot) {
-  const long long wid = W.wid[slot];
-  double p[3] = {W.p[3 * slot], W.p[3 * slot + 1], W.p[3 * slot + 2]};
+// Lane-held state of a walk in the advance stage.
+struct AdvLane {
+  int slot;
+  long long wid;
+  double p[3];
   Rng rng;
-  rng.s = W.rng[slot];
-  int hops = W.hops[slot];
-  uint32_t cached = W.cached[slot];
+  int hops;
+  uint32_t cached;
+};
+
+__device__ __forceinline__ void adv_load(const DSlots& W, int slot, AdvLane& L) {
+  L.slot = slot;
+  L.wid = W.wid[slot];
+  L.p[0] = W.p[3 * slot];
+  L.p[1] = W.p[3 * slot + 1];
+  L.p[2] = W.p[3 * slot + 2];
+  L.rng.s = W.rng[slot];
+  L.hops = W.hops[slot];
+  L.cached = W.cached[slot];
+}
+
+// One transition (engine.cpp:290-350; hop cap engine.cpp:367-375) of the
+// lane's walk.  Returns 0 when a cached hop was taken (the walk stays with
+// the lane), 1 when the walk left the stage: terminated, parked by a table
+// miss, or queued for a MicroWalk hop.
+__device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, const DSlots& W,
+                            WalkRec* recs, DCounters* C, const DMiss& M, int* mq, AdvLane& L) {
+  const int slot = L.slot;
   const int n = P.n;
-  for (;;) {
-    if (hops >= P.hop_cap) {  // engine.cpp:367-375
-      W.cached[slot] = cached;
-      finish_walk(W, recs, C, slot, s.nc, true);
-      return false;
-    }
-    const int ci = conductor_at(s, p, P.snap);
-    if (ci >= 0) {
-      W.cached[slot] = cached;
-      finish_walk(W, recs, C, slot, ci, false);
-      return false;
-    }
-    if (cheb_wall(s.world, p) <= P.snap) {
-      W.cached[slot] = cached;
-      finish_walk(W, recs, C, slot, s.nc, false);
-      return false;
-    }
-    double fh;
-    if (!max_free_cube(s, p, &fh)) {
-      set_err(C, FRW_EINVAL);
+  if (L.hops >= P.hop_cap) {
+    W.cached[slot] = L.cached;
+    finish_walk(W, recs, C, slot, s.nc, true);
+    return 1;
+  }
+  double fh;
+  const int g = hop_scan(s, L.p, P.snap, &fh);
+  if (g >= 0 || g == -1) {  // snapped to a conductor / to the grounded wall
+    W.cached[slot] = L.cached;
+    finish_walk(W, recs, C, slot, g >= 0 ? g : s.nc, false);
+    return 1;
+  }
+  if (g == -2) {
+    set_err(C, FRW_EINVAL);
+    W.state[slot] = S_FREE;
+    return 1;
+  }
+  double c[3], h;
+  transit_cube(L.p, fh, n, c, &h);
+  double layers[NMAX];
+  const int axis = stratified_key(s, c, h, n, layers);
+  if (axis == -2) {
+    set_err(C, FRW_EINVAL);
+    W.state[slot] = S_FREE;
+    return 1;
+  }
+  if (axis >= 0) {
+    const int e = sgf_find(T, n, axis, layers);
+    if (e < 0) {
+      record_miss(C, M, n, axis, layers, L.wid);
       W.state[slot] = S_FREE;
-      return false;
+      return 1;
     }
-    double c[3], h;
-    transit_cube(p, fh, n, c, &h);
-    double layers[NMAX];
-    const int axis = stratified_key(s, c, h, n, layers);
-    if (axis == -2) {
-      set_err(C, FRW_EINVAL);
-      W.state[slot] = S_FREE;
-      return false;
+    const double* data = T.data[e];
+    const int panel = sample_panel(data, reinterpret_cast<const int*>(data + 5 * P.panels),
+                                   P.panels, uniform(P, L.wid, L.rng));
+    panel_center(c, h, n, panel, L.p);
+    ++L.cached;
+    ++L.hops;
+    return 0;
+  }
+  // general cube: MicroWalk (HYBRID-MW, engine.cpp:319-326)
+  if (!compile_mw_job(s, W, slot, c, h, n, C)) {
+    W.state[slot] = S_FREE;
+    return 1;
+  }
+  W.p[3 * slot + 0] = L.p[0];
+  W.p[3 * slot + 1] = L.p[1];
+  W.p[3 * slot + 2] = L.p[2];
+  W.rng[slot] = L.rng.s;
+  W.hops[slot] = L.hops + 1;
+  W.cached[slot] = L.cached;
+  W.state[slot] = S_NEED_MW;
+  mq[atomicAdd(&C->qlen, 1ull)] = slot;
+  return 1;
+}
+
+// persistent: each thread takes ACTIVE walks from the queue and advances
+// them one transition per iteration, re-armed as soon as its walk leaves
+__global__ void __launch_bounds__(256)
+    k_advance(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
+              const int* aq, int* mq) {
+  const unsigned long long alen = C->alen;
+  unsigned long long item = atomicAdd(&C->ahead, 1ull);
+  bool live = item < alen;
+  AdvLane L;
+  if (live) adv_load(W, aq[item], L);
+  while (__any_sync(0xFFFFFFFFu, live)) {
+    if (live && advance_once(s, T, P, W, recs, C, M, mq, L) != 0) {
+      item = atomicAdd(&C->ahead, 1ull);
+      live = item < alen;
+      if (live) adv_load(W, aq[item], L);
     }
-    if (axis >= 0) {
-      const int e = sgf_find(T, n, axis, layers);
-      if (e < 0) {
-        record_miss(C, M, n, axis, layers, wid);
-        W.state[slot] = S_FREE;
-        return false;
-      }
-      const int panel = sample_panel(T.data[e], P.panels, uniform(P, wid, rng));
-      panel_center(c, h, n, panel, p);
-      ++cached;
-      ++hops;
-      continue;
-    }
-    // general cube: MicroWalk (HYBRID-MW, engine.cpp:319-326)
-    if (!compile_mw_job(s, W, slot, c, h, n, C)) {
-      W.state[slot] = S_FREE;
-      return false;
-    }
-    W.p[3 * slot + 0] = p[0];
-    W.p[3 * slot + 1] = p[1];
-    W.p[3 * slot + 2] = p[2];
-    W.rng[slot] = rng.s;
-    W.hops[slot] = hops + 1;
-    W.cached[slot] = cached;
-    W.state[slot] = S_NEED_MW;
-    return true;
   }
 }
 
-__global__ void k_advance(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C,
-                          DMiss M, int* queue) {
-  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
-       slot += gridDim.x * blockDim.x) {
-    if (W.state[slot] != S_ACTIVE) continue;
-    if (advance_slot(s, T, P, W, recs, C, M, slot)) {
-      const unsigned long long q = atomicAdd(&C->qlen, 1ull);
-      queue[q] = slot;
-    }
-  }
+// between rounds: the next round's ACTIVE queue becomes current
+__global__ void k_round(DCounters* C) {
+  C->alen = C->a2len;
+  C->ahead = 0;
+  C->a2len = 0;
+  C->qlen = 0;
+  C->qhead = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -844,6 +915,8 @@ struct MwLane {
   uint64_t rng;   // SplitMix64 state or Philox block counter
   int steps;
   int K;
+  uint32_t gsteps;  // diagnostics, accumulated across the lane's hops
+  uint32_t cchg;
 };
 
 __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int n, MwLane& L) {
@@ -894,31 +967,9 @@ __device__ void mw_exit(const DSlots& W, int n, MwLane& L, int dir) {
   W.state[L.slot] = S_ACTIVE;
 }
 
-// f64 direction scan (microwalk.cpp:91-121) for a node next to a cell face
-__device__ __forceinline__ int general_dir(const double* alpha_sm, int P, const MwLane& L,
-                                           double u, bool* exit_surface, bool* leaves) {
-  const int c0 = static_cast<int>((L.fc >> 48) & 0xFF);
-  double al[6], sum = 0;
-#pragma unroll
-  for (int d = 0; d < 6; ++d) {
-    const bool inside = ((L.room >> (8 * d)) & 0xFF) != 0;
-    const int cn = inside ? c0 : static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-    const double a = (cn == 0xFF) ? 1.0 : alpha_sm[cn * P + c0];
-    al[d] = a;
-    sum += a;
-  }
-  const double target = u * sum;
-  double acc = 0;
-  int dir = 5;
-#pragma unroll
-  for (int d = 0; d < 5; ++d) {
-    acc += al[d];
-    if (dir == 5 && target < acc) dir = d;
-  }
-  const bool inside = ((L.room >> (8 * dir)) & 0xFF) != 0;
-  *leaves = !inside;
-  *exit_surface = !inside && ((L.fc >> (8 * dir)) & 0xFF) == 0xFF;
-  return dir;
+// the walk goes back to the next round's ACTIVE queue
+__device__ __forceinline__ void mw_requeue(DCounters* C, int* aq_out, int slot) {
+  aq_out[atomicAdd(&C->a2len, 1ull)] = slot;
 }
 
 struct DirDelta {
@@ -927,65 +978,71 @@ struct DirDelta {
   uint32_t pad;
 };
 
-// One lattice step for lane L; returns 0 continue, 1 surface exit (xdir set)
+// One lattice step (microwalk.cpp:88-152) for lane L.  Every node takes the
+// same code path: a neighbour inside the current cell has the node's own
+// permittivity, so its alpha is e/(e+e) = 1/2 exactly; a neighbour across a
+// cell face takes the face-neighbour class's alpha from the palette-pair
+// table (1 on a lattice face).  The six alphas, their in-order partial sums
+// and the scan are the reference's f64 arithmetic.  Returns 0 (moved inside
+// the cell), 1 (surface exit through *xdir) or 2 (moved into the adjacent
+// cell along *xdir; the caller refreshes the cell data).
 template <int RNG>
-__device__ __forceinline__ int mw_step(const DStruct& s, const DSlots& W, const DParams& P,
-                                       const double* alpha_sm, const DirDelta* dd, int n,
-                                       MwLane& L, uint32_t w, uint64_t z, uint32_t tie_ctr,
-                                       int* xdir) {
+__device__ __forceinline__ int mw_step(const DParams& P, const double* alpha_sm, int Pn,
+                                       const DirDelta* dd, MwLane& L, uint32_t w, uint64_t z,
+                                       uint32_t tie_ctr, int* xdir) {
   ++L.steps;
+  const int c0 = static_cast<int>((L.fc >> 48) & 0xFF);
+  // exact zero-byte mask of the six room bytes: bit 8d+7 set <=> on face d
   const uint64_t r = L.room & 0x0000FFFFFFFFFFFFull;
-  const bool interior = ((r - 0x010101010101ull) & ~r & 0x808080808080ull) == 0;
-  int dir;
-  if (interior) {
-    // all seven voxels share one class: alpha = 1/2 everywhere
-    const uint32_t x10 = RNG == FRW_RNG_SPLITMIX_PARITY ? static_cast<uint32_t>(z >> 54) : (w >> 22);
-    const uint64_t d1 = static_cast<uint64_t>(x10) * kOnes + P.urec;
-    const uint32_t lo = static_cast<uint32_t>(d1), hi = static_cast<uint32_t>(d1 >> 32);
-    dir = __popc((lo & static_cast<uint32_t>(kGuard)) | (hi & static_cast<uint32_t>(kGuard >> 32)));
-    if ((((d1 + kOnes) ^ d1) & kGuard) != 0) {
-      uint64_t x53;
-      if (RNG == FRW_RNG_SPLITMIX_PARITY)
-        x53 = z >> 11;
-      else
-        x53 = (static_cast<uint64_t>(w) << 21) |
-              (philox53(P, L.wid, tie_ctr, 1u) & 0x1FFFFF);
+  const uint64_t t = (r & 0x00007F7F7F7F7F7Full) + 0x00007F7F7F7F7F7Full;
+  const uint64_t onface = ~(t | r | 0x00007F7F7F7F7F7Full) & 0x0000808080808080ull;
+  double acc[6];
+  double sum = 0;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    double a = 0.5;
+    if ((onface >> (8 * d + 7)) & 1) {
+      const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
+      a = cn == 0xFF ? 1.0 : alpha_sm[cn * Pn + c0];
+    }
+    sum += a;
+    acc[d] = sum;
+  }
+  if (onface) ++L.gsteps;
+  int dir = 0;
+  if (RNG == FRW_RNG_SPLITMIX_PARITY) {
+    const double target = static_cast<double>(z >> 11) * 0x1.0p-53 * sum;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) dir += acc[d] <= target;  // first d with target < acc_d
+  } else {
+    // the 32-bit word fixes x to [w*2^21, w*2^21 + 2^21): decide at both
+    // ends; only when they disagree are the low 21 bits drawn
+    const uint64_t xl = static_cast<uint64_t>(w) << 21;
+    const double tl = static_cast<double>(xl) * 0x1.0p-53 * sum;
+    const double th = static_cast<double>(xl | 0x1FFFFF) * 0x1.0p-53 * sum;
+    int dh = 0;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+      dir += acc[d] <= tl;
+      dh += acc[d] <= th;
+    }
+    if (dh != dir) {
+      const uint64_t x53 = xl | (philox53(P, L.wid, tie_ctr, 1u) & 0x1FFFFF);
+      const double target = static_cast<double>(x53) * 0x1.0p-53 * sum;
       dir = 0;
 #pragma unroll
-      for (int d = 0; d < 5; ++d) dir += x53 >= P.ufull[d];
+      for (int d = 0; d < 5; ++d) dir += acc[d] <= target;
     }
-    const DirDelta del = dd[dir];
-    L.node += del.node;
-    L.room += del.room;
-    return 0;
-  }
-  bool ex, leaves;
-  if (RNG == FRW_RNG_SPLITMIX_PARITY) {
-    dir = general_dir(alpha_sm, s.P, L, static_cast<double>(z >> 11) * 0x1.0p-53, &ex, &leaves);
-  } else {
-    // the 32-bit word fixes x to [w*2^21, w*2^21 + 2^21): scan both ends;
-    // only when they disagree are the low 21 bits drawn
-    const uint64_t xl = static_cast<uint64_t>(w) << 21;
-    bool ex2, lv2;
-    dir = general_dir(alpha_sm, s.P, L, static_cast<double>(xl) * 0x1.0p-53, &ex, &leaves);
-    const int d2 = general_dir(alpha_sm, s.P, L, static_cast<double>(xl | 0x1FFFFF) * 0x1.0p-53,
-                               &ex2, &lv2);
-    if (d2 != dir) {
-      const uint64_t x53 =
-          xl | (philox53(P, L.wid, tie_ctr, 1u) & 0x1FFFFF);
-      dir = general_dir(alpha_sm, s.P, L, static_cast<double>(x53) * 0x1.0p-53, &ex, &leaves);
-    }
-  }
-  if (ex) {
-    *xdir = dir;
-    return 1;
   }
   const DirDelta del = dd[dir];
+  *xdir = dir;
+  if ((onface >> (8 * dir + 7)) & 1) {
+    if (((L.fc >> (8 * dir)) & 0xFF) == 0xFF) return 1;  // left the lattice
+    L.node += del.node;
+    return 2;
+  }
   L.node += del.node;
-  if (leaves)
-    mw_cell_change(W, s, n, L, dir);
-  else
-    L.room += del.room;
+  L.room += del.room;
   return 0;
 }
 
@@ -1007,7 +1064,7 @@ __device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* 
 // persistent MicroWalk kernel: each thread runs queued hops back to back
 template <int RNG>
 __global__ void __launch_bounds__(512)
-    k_mw(DStruct s, DParams P, DSlots W, DCounters* C, const int* queue) {
+    k_mw(DStruct s, DParams P, DSlots W, DCounters* C, const int* queue, int* aq_out) {
   __shared__ double alpha_sm[PMAX * PMAX];
   __shared__ DirDelta dd[6];
   setup_smem_tables(s, alpha_sm, dd);
@@ -1015,6 +1072,8 @@ __global__ void __launch_bounds__(512)
   const int cap = 1000 * n * n;  // microwalk.cpp:81
   const unsigned long long qlen = C->qlen;
   MwLane L;
+  L.gsteps = 0;
+  L.cchg = 0;
   unsigned long long item = atomicAdd(&C->qhead, 1ull);
   bool live = item < qlen;
   if (live) mw_arm(W, queue[item], n, L);
@@ -1031,98 +1090,45 @@ __global__ void __launch_bounds__(512)
       w4[2] = o.z;
       w4[3] = o.w;
     }
-    bool exited = false;
-    int xdir = 0;
+    int code = 0, xdir = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (live && !exited) {
+      if (live && code == 0 && L.steps < cap) {
         uint64_t z = 0;
         if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
-        if (mw_step<RNG>(s, W, P, alpha_sm, dd, n, L, w4[u], z,
-                         static_cast<uint32_t>(L.rng * 4 + u), &xdir))
-          exited = true;
+        code = mw_step<RNG>(P, alpha_sm, s.P, dd, L, w4[u], z,
+                            static_cast<uint32_t>(L.rng * 4 + u), &xdir);
       }
     }
     if (RNG == FRW_RNG_PHILOX && live) ++L.rng;  // next 4-word block
-    if (live && (exited || L.steps >= cap)) {
-      if (exited)
+    // cell changes of the super-step, processed together by the lanes that
+    // crossed a face (they skipped the rest of the super-step)
+    if (live && code == 2) {
+      ++L.cchg;
+      mw_cell_change(W, s, n, L, xdir);
+      code = 0;
+    }
+    if (live && (code == 1 || L.steps >= cap)) {
+      if (code == 1) {
         mw_exit(W, n, L, xdir);
-      else
+        mw_requeue(C, aq_out, L.slot);
+      } else {
         set_err(C, FRW_ESTEPCAP);
+      }
       item = atomicAdd(&C->qhead, 1ull);
       live = item < qlen;
       if (live) mw_arm(W, queue[item], n, L);
     }
   }
-}
-
-// tail: every remaining walk runs to completion in its own thread
-template <int RNG>
-__global__ void __launch_bounds__(256)
-    k_finish(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M) {
-  __shared__ double alpha_sm[PMAX * PMAX];
-  __shared__ DirDelta dd[6];
-  setup_smem_tables(s, alpha_sm, dd);
-  const int n = P.n;
-  const int cap = 1000 * n * n;
-  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
-       slot += gridDim.x * blockDim.x) {
-    for (;;) {
-      const uint8_t st = W.state[slot];
-      if (st == S_ACTIVE) {
-        if (!advance_slot(s, T, P, W, recs, C, M, slot)) break;
-      } else if (st == S_NEED_MW) {
-        MwLane L;
-        mw_arm(W, slot, n, L);
-        int xdir = -1;
-        bool done = false;
-        while (!done) {
-          uint32_t w4[4] = {0, 0, 0, 0};
-          if (RNG == FRW_RNG_PHILOX) {
-            const uint64_t id = P.walk_begin + L.wid;
-            const U32x4 o = philox4x32_10(
-                {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
-                 static_cast<uint32_t>(L.rng), 2u},
-                static_cast<uint32_t>(P.seed), static_cast<uint32_t>(P.seed >> 32));
-            w4[0] = o.x;
-            w4[1] = o.y;
-            w4[2] = o.z;
-            w4[3] = o.w;
-          }
-          for (int u = 0; u < 4 && !done; ++u) {
-            uint64_t z = 0;
-            if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
-            if (mw_step<RNG>(s, W, P, alpha_sm, dd, n, L, w4[u], z,
-                             static_cast<uint32_t>(L.rng * 4 + u), &xdir))
-              done = true;
-            if (!done && L.steps >= cap) {
-              set_err(C, FRW_ESTEPCAP);
-              done = true;
-              xdir = -1;
-            }
-          }
-          if (RNG == FRW_RNG_PHILOX) ++L.rng;
-        }
-        if (xdir < 0) {
-          W.state[slot] = S_FREE;
-          break;
-        }
-        mw_exit(W, n, L, xdir);
-      } else {
-        break;
-      }
-    }
+  unsigned long long g = L.gsteps, cc = L.cchg;
+  for (int o = 16; o > 0; o >>= 1) {
+    g += __shfl_xor_sync(0xFFFFFFFFu, g, o);
+    cc += __shfl_xor_sync(0xFFFFFFFFu, cc, o);
   }
-}
-
-// count slots still holding a walk
-__global__ void k_count_active(DSlots W, DCounters* C) {
-  unsigned long long c = 0;
-  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < W.S;
-       slot += gridDim.x * blockDim.x)
-    c += W.state[slot] != S_FREE;
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&C->active, c);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&C->gen_steps, g);
+    atomicAdd(&C->cell_chg, cc);
+  }
 }
 
 // ---- deterministic tallies -------------------------------------------------
@@ -1261,7 +1267,8 @@ struct Engine {
   long long recs_cap = 0;
   DCounters* d_cnt = nullptr;
   DMiss M{};
-  int* queue = nullptr;
+  int* queue = nullptr;   // MicroWalk queue
+  int* aq[2] = {nullptr, nullptr};  // ACTIVE queues (current / next round)
   // reduction scratch
   double *psum = nullptr, *psq = nullptr, *osum = nullptr, *osq = nullptr;
   unsigned long long *pland = nullptr, *pstat = nullptr, *oland = nullptr, *ostat = nullptr;
@@ -1287,6 +1294,9 @@ void free_slots(Engine& E) {
   cudaFree(E.W.room);
   cudaFree(E.W.fc);
   cudaFree(E.queue);
+  cudaFree(E.aq[0]);
+  cudaFree(E.aq[1]);
+  E.aq[0] = E.aq[1] = nullptr;
   cudaFree(E.M.retry);
   cudaFree(E.M.pend);
   E.W = DSlots{};
@@ -1334,14 +1344,14 @@ Engine* engine_of(frw_ctx* ctx) {
   return static_cast<Engine*>(ctx->walk);
 }
 
-uint64_t host_key_hash(int n, int axis, const double* layers) {
-  uint64_t h = sm64_mix((static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis));
+uint64_t host_key_hash(int n, int axis, const double* layers) {  // == key_hash
+  uint64_t h = (static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis);
   for (int t = 0; t < n; ++t) {
     uint64_t b;
     std::memcpy(&b, &layers[t], 8);
-    h = sm64_mix(h ^ b);
+    h = key_step(h, b);
   }
-  return h;
+  return sm64_mix(h);
 }
 
 int sgf_sync(frw_ctx* ctx, SgfHost& T) {
@@ -1422,11 +1432,13 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   W.room = dalloc<uint64_t>(S);
   W.fc = dalloc<uint64_t>(S);
   E.queue = dalloc<int>(S);
+  E.aq[0] = dalloc<int>(S);
+  E.aq[1] = dalloc<int>(S);
   E.M.retry = dalloc<long long>(S);
   E.M.pend = dalloc<long long>(S);
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
       !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes || !W.room ||
-      !W.fc || !E.queue || !E.M.retry || !E.M.pend) {
+      !W.fc || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
   }
@@ -1519,8 +1531,20 @@ int frw_sgf_put(frw_ctx* ctx, int n, int axis, const double* layers, double pitc
       return FRW_OK;  // first stored result wins (sgf_cache.cpp:133-153)
   }
   const size_t panels = 6ull * n * n;
-  double* blk = dalloc<double>(5 * panels);
+  // data block: cdf, probs, kernels[3], guide table (kGuide int32)
+  double* blk = dalloc<double>(5 * panels + kGuide / 2);
   if (!blk) return frw_fail(ctx, FRW_ENOMEM, "sgf_put: device allocation failed");
+  {
+    std::vector<int> guide(kGuide);
+    const double total = cdf[panels - 1];
+    size_t i = 0;
+    for (int b = 0; b < kGuide; ++b) {
+      const double gb = (static_cast<double>(b) / kGuide) * total;
+      while (i < panels && cdf[i] <= gb) ++i;  // first cdf > fl((b/G)*total)
+      guide[b] = static_cast<int>(i);
+    }
+    FRW_CUDA(ctx, cudaMemcpy(blk + 5 * panels, guide.data(), 4 * kGuide, cudaMemcpyHostToDevice));
+  }
   FRW_CUDA(ctx, cudaMemcpy(blk, cdf, 8 * panels, cudaMemcpyHostToDevice));
   FRW_CUDA(ctx, cudaMemcpy(blk + panels, probs, 8 * panels, cudaMemcpyHostToDevice));
   if (kernels)
@@ -1638,40 +1662,33 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   FRW_CUDA(ctx, cudaMemsetAsync(E.recs, 0, sizeof(WalkRec) * count, ctx->stream));
   FRW_CUDA(ctx, cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), ctx->stream));
   const int grid = ctx->sm_count * 8;
-  const int mw_grid = ctx->sm_count * 2;  // 2 x 512 threads per SM
+  const int adv_grid = ctx->sm_count * 4;  // persistent: 4 x 256 threads per SM
+  const int mw_grid = ctx->sm_count * 2;   // persistent: 2 x 512 threads per SM
   float mw_ms = 0;
   uint64_t misses_total = 0, restarts = 0;
   std::vector<int> maxis;
   std::vector<double> mlayers;
   int status = FRW_OK;
-  bool tail = false;
   for (int round = 0;; ++round) {
     DSgf T{E.sgf.cap, E.sgf.d_hash, E.sgf.d_entry, E.sgf.d_axis, E.sgf.d_keys, E.sgf.d_pitch,
            E.sgf.d_data};
-    if (!tail) {
-      k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M);
-      k_advance<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, E.queue);
-      cudaEventRecord(m0, ctx->stream);
-      if (P.rng == FRW_RNG_PHILOX)
-        k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt, E.queue);
-      else
-        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt,
-                                                                        E.queue);
-      cudaEventRecord(m1, ctx->stream);
-    } else {
-      if (P.rng == FRW_RNG_PHILOX)
-        k_finish<FRW_RNG_PHILOX><<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M);
-      else
-        k_finish<FRW_RNG_SPLITMIX_PARITY><<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs,
-                                                                         E.d_cnt, M);
-    }
+    int* aq_in = E.aq[round & 1];
+    int* aq_out = E.aq[(round + 1) & 1];
+    k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in);
+    k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in,
+                                                 E.queue);
+    cudaEventRecord(m0, ctx->stream);
+    if (P.rng == FRW_RNG_PHILOX)
+      k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt, E.queue, aq_out);
+    else
+      k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt,
+                                                                      E.queue, aq_out);
+    cudaEventRecord(m1, ctx->stream);
     FRW_CUDA(ctx, cudaGetLastError());
-    FRW_CUDA(ctx, cudaMemsetAsync(&E.d_cnt->active, 0, 8, ctx->stream));
-    k_count_active<<<grid, 256, 0, ctx->stream>>>(E.W, E.d_cnt);
     DCounters c;
     FRW_CUDA(ctx, cudaMemcpyAsync(&c, E.d_cnt, sizeof c, cudaMemcpyDeviceToHost, ctx->stream));
     FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    if (!tail) {
+    {
       float ms = 0;
       cudaEventElapsedTime(&ms, m0, m1);
       mw_ms += ms;
@@ -1685,8 +1702,6 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                      "conductor, or more than 32 dielectric boxes in one cube)");
       break;
     }
-    // reset the MicroWalk queue for the next round
-    FRW_CUDA(ctx, cudaMemsetAsync(&E.d_cnt->qlen, 0, 16, ctx->stream));
     if (c.nmiss) {
       if (!miss) {
         status = frw_fail(ctx, FRW_EMISS, "run_walks: SGF table miss and no miss callback");
@@ -1722,13 +1737,12 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         break;
       }
       misses_total += E.sgf.axis.size() - before;
-      if (status) break;
       if (int rc = sgf_sync(ctx, E.sgf)) {
         status = rc;
         break;
       }
-      // parked walks restart from scratch; nothing of their partial run was
-      // committed.  pend <- retry
+      // parked walks restart from scratch (nothing of their partial run was
+      // committed): pend <- retry; the round transition happens here too
       FRW_CUDA(ctx, cudaMemcpyAsync(M.pend, M.retry, 8 * c.nretry, cudaMemcpyDeviceToDevice,
                                     ctx->stream));
       DCounters upd = c;
@@ -1736,24 +1750,24 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       upd.pend_head = 0;
       upd.nretry = 0;
       upd.nmiss = 0;
+      upd.alen = c.a2len;
+      upd.ahead = 0;
+      upd.a2len = 0;
       upd.qlen = 0;
       upd.qhead = 0;
-      upd.active = 0;
       FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cnt, &upd, sizeof upd, cudaMemcpyHostToDevice,
                                     ctx->stream));
       restarts += c.nretry;
-      tail = false;
       continue;
     }
     const bool all_spawned = c.next >= static_cast<unsigned long long>(count) &&
                              c.pend_head >= c.npend;
-    if (all_spawned && c.active == 0 && c.done >= static_cast<unsigned long long>(count)) break;
-    if (all_spawned && c.active == 0 && c.done < static_cast<unsigned long long>(count)) {
-      status = frw_fail(ctx, FRW_ECUDA, "run_walks: lost walks (internal error)");
+    if (all_spawned && c.a2len == 0) {
+      if (c.done < static_cast<unsigned long long>(count))
+        status = frw_fail(ctx, FRW_ECUDA, "run_walks: lost walks (internal error)");
       break;
     }
-    // few walks left: finish them in-thread instead of paying a round each
-    tail = all_spawned && c.active < static_cast<unsigned long long>(S) / 16;
+    k_round<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
   }
   if (status == FRW_OK) {
     // deterministic tallies
@@ -1821,6 +1835,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     out->cache_hits = 0;
     out->restarts = restarts;
     out->mw_ms = mw_ms;
+    DCounters cfin;
+    FRW_CUDA(ctx, cudaMemcpy(&cfin, E.d_cnt, sizeof cfin, cudaMemcpyDeviceToHost));
+    out->mw_general_steps = cfin.gen_steps;
+    out->mw_cell_changes = cfin.cell_chg;
     float tot = 0;
     cudaEventElapsedTime(&tot, t0, t1);
     out->total_ms = tot;
