@@ -162,6 +162,82 @@ def run_reference(args):
     return 0
 
 
+def walk_cpu_baseline(doc, seconds=12.0):
+    """The reference's own Engine::extract (oracle/_ref: engine.cpp,
+    microwalk.cpp, geometry.cpp, sgf_cache.cpp built from the reference
+    sources) on all host threads, C3, HYBRID-MW, warm SGF cache."""
+    from oracle.oracle import LIB_REF, Oracle, Ref
+    from tests.scenes import scene_from_doc
+    threads = os.cpu_count() or 1
+    sc = scene_from_doc(json.loads(doc))
+    kw = dict(mode="HYBRID-MW", grid_n=24)
+    if os.path.exists(LIB_REF):
+        h, kind = Ref().structure(sc), "reference"
+        run = lambda n, seed: h.extract(threads=threads, warm_cache=True, min_walks=n,  # noqa
+                                        max_walks=n, seed=seed, **kw)
+    else:
+        O, kind = Oracle(), "port"
+        run = lambda n, seed: O.extract(sc, threads=threads, min_walks=n, max_walks=n,  # noqa
+                                        seed=seed, **kw)
+    run(2048, 99)  # warm the SGF cache
+    t0 = time.perf_counter()
+    run(1024, 98)
+    dt = time.perf_counter() - t0
+    n = max(1024, int(1024 * seconds / max(dt, 1e-3)) // 1024 * 1024)
+    t0 = time.perf_counter()
+    run(n, 1)
+    dt = time.perf_counter() - t0
+    return dict(value=n / dt, unit="walks/s", cores=threads, kind=kind,
+                sample=f"{n} C3 walks (HYBRID-MW, N=24, warm SGF cache) on {threads} threads "
+                       f"in {dt:.1f} s")
+
+
+def walk_engine_bench(args, rank, world, dist, torch):
+    """FRW walks/s (the metric's first half) on C3 through the drop-in API
+    extract_json: a warm-up call fills the stratified-SGF table, then each
+    timed call runs `walks` fresh walks (seed = step + rank: independent
+    streams per rank); per-rank tallies are combined with one NCCL
+    all-reduce.  `value` is device time of the walk launches (CUDA events
+    inside frw_run_walks), `e2e` the wall time of the public call."""
+    import paper_2507_09730_b200.frwcap as frwcap
+    from paper_2507_09730_b200.workloads import c3_structure
+    doc = json.dumps(c3_structure())
+    W = args.walks
+    kw = dict(mode="HYBRID-MW", min_walks=W, max_walks=W, device=int(os.environ.get("LOCAL_RANK", 0)))
+    frwcap.extract_json(doc, seed=10_000 + rank, **kw)  # warm the SGF table
+    dev_s, wall_s, res = 0.0, 0.0, None
+    for i in range(args.walk_steps):
+        t0 = time.perf_counter()
+        res = frwcap.extract_json(doc, seed=1 + i * 1000 + rank, **kw)
+        wall_s += time.perf_counter() - t0
+        dev_s += res["t_device_seconds"]
+    sums = torch.tensor([t["capacitance_farads"] * res["walks"] for t in res["terminals"]] +
+                        [dev_s, wall_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        mx = sums[-2:].clone()
+        dist.all_reduce(sums)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sums[-2:] = mx
+    dev_s, wall_s = float(sums[-2]), float(sums[-1])
+    total = world * W * args.walk_steps
+    ids = [t["conductor_id"] for t in res["terminals"]]
+    return {"metric": "frw_walks_per_s", "unit": "walks/s",
+            "value": total / dev_s, "e2e": {"value": total / wall_s, "unit": "walks/s",
+                                            "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
+            "config": {"workload": "C3 (BASELINE configs[2]): two 100x100x5000 nm wires, 100 nm "
+                                   "apart, 200 nm over a 2x2 um plane, 3 z layers, 20 nm coatings; "
+                                   "HYBRID-MW, N=24, Gaussian gap 0.5", "walks_per_rank_per_step": W,
+                       "steps": args.walk_steps, "sgf_table": "warm (filled by a warm-up call)"},
+            "capacitance_aF_rank0_last": dict(zip(map(str, ids),
+                                                  [round(t["capacitance_farads"] * 1e18, 3)
+                                                   for t in res["terminals"]])),
+            "cpu_baseline": walk_cpu_baseline(doc) if (world == 1 and not args.no_cpu_baseline)
+            else None,
+            "dispatch_rank0_last": res["dispatch_stats"], "mw_steps_per_walk":
+                res["mw_steps"] / res["walks"], "t_mw_fraction": res["t_mw_seconds"] /
+                max(res["t_device_seconds"], 1e-12)}
+
+
 def run_gpu(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -285,6 +361,8 @@ def run_gpu(args):
         e2e_v = world * per * args.steps / e_s
         ctx2.close()
 
+    walks = None if args.no_walks else walk_engine_bench(args, rank, world, dist, torch)
+
     if rank != 0:
         if dist is not None:
             dist.barrier()
@@ -326,6 +404,8 @@ def run_gpu(args):
         "clocks": clocks,
         "device": ctx.name,
     }
+    if walks is not None:
+        out["walk_engine"] = walks
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(seconds=args.ref_seconds)
     print(json.dumps(out))
@@ -344,6 +424,9 @@ def main():
     ap.add_argument("--count", type=int, default=COUNT)
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-walks", action="store_true")
+    ap.add_argument("--walks", type=int, default=1_000_000)
+    ap.add_argument("--walk-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3

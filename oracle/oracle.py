@@ -384,6 +384,7 @@ class Ref:
         L.ref_round_sig.argtypes = [C.c_double, C.c_int]
         L.ref_extract.argtypes = [C.c_void_p, _dp, _lp, C.c_int, _dp, _dp, _up, _up, _dp]
         L.ref_run_walks.argtypes = [C.c_void_p, _dp, _lp, C.c_uint64, C.c_int64, _ip, _dp, _bp]
+        L.ref_extract_warm.argtypes = [C.c_void_p, _dp, _lp, C.c_int, _dp, _dp, _up, _up, _dp]
 
     def err(self):
         return self.lib.ref_last_error().decode()
@@ -549,7 +550,7 @@ class _RefHandle:
             raise RuntimeError(self.ref.err())
         return out
 
-    def extract(self, threads=1, **kw):
+    def extract(self, threads=1, warm_cache=False, **kw):
         d, i = Ref.cfg_arrays(**kw)
         nc, nd = C.c_int(), C.c_int()
         self.lib.ref_structure_counts(self.h, C.byref(nc), C.byref(nd))
@@ -558,8 +559,9 @@ class _RefHandle:
         landed = np.zeros(k, np.uint64)
         st = np.zeros(14, np.uint64)
         tm = np.zeros(2)
-        if self.lib.ref_extract(self.h, _ptr(d, _dp), _ptr(i, _lp), threads, _ptr(val, _dp),
-                                _ptr(se, _dp), _ptr(landed, _up), _ptr(st, _up), _ptr(tm, _dp)):
+        fn = self.lib.ref_extract_warm if warm_cache else self.lib.ref_extract
+        if fn(self.h, _ptr(d, _dp), _ptr(i, _lp), threads, _ptr(val, _dp),
+              _ptr(se, _dp), _ptr(landed, _up), _ptr(st, _up), _ptr(tm, _dp)):
             raise RuntimeError(self.ref.err())
         return dict(value=val, std_err=se, landed=landed, walks=int(st[0]),
                     converged=bool(st[1]), aborted=int(st[2]), resampled=int(st[3]),

@@ -352,6 +352,35 @@ int ref_extract(const void* h, const double* cfg_d, const int64_t* cfg_i,
   }
 }
 
+// extract() with a process-wide StratifiedSgfCache, so a second call runs
+// against a warm table (the CLI's --cache behaviour, cli.cpp:186-193)
+int ref_extract_warm(const void* h, const double* cfg_d, const int64_t* cfg_i, int threads,
+                     double* value, double* std_err, uint64_t* landed, uint64_t* stats,
+                     double* times) {
+  static StratifiedSgfCache cache;
+  try {
+    const auto& s = *static_cast<const Structure*>(h);
+    const CapacitanceResult r = extract(s, make_config(cfg_d, cfg_i), threads, &cache);
+    for (size_t k = 0; k < r.terminals.size(); ++k) {
+      value[k] = r.terminals[k].value;
+      std_err[k] = r.terminals[k].std_err;
+      landed[k] = r.terminals[k].walks_landed;
+    }
+    const uint64_t st[14] = {r.walks, r.converged, r.aborted, r.resampled,
+                             r.dispatch.first_stratified, r.dispatch.first_shrunk,
+                             r.dispatch.first_layered, r.dispatch.first_homogenized,
+                             r.dispatch.cached, r.dispatch.microwalk,
+                             r.dispatch.microwalk_e, r.dispatch.fdm,
+                             r.cache_hits, r.cache_misses};
+    std::memcpy(stats, st, sizeof st);
+    times[0] = r.t_mw_seconds;
+    times[1] = r.t_total_seconds;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // per-walk records, restating the 20-line Engine::run_walk
 // (engine.cpp:352-376, private) over the public first_transition/transition
 int ref_run_walks(const void* h, const double* cfg_d, const int64_t* cfg_i,

@@ -536,13 +536,22 @@ __device__ bool compile_mw_job(const DStruct& s, const DSlots& W, int slot, cons
                                double h, int n, DCounters* C) {
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
   int K = 0;
+  const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
   for (int d = 0; d < s.nd; ++d) {
     const double* b = s.dbox + 6 * d;
+    double bb[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) bb[q] = __ldg(b + q);
+    // voxel centres lie inside the closed cube: a box that misses the cube
+    // cannot contain one (cheap reject before the exact clip)
+    if (bb[0] > cb[3] || bb[3] < cb[0] || bb[1] > cb[4] || bb[4] < cb[1] || bb[2] > cb[5] ||
+        bb[5] < cb[2])
+      continue;
     int lo[3], hi[3];
     bool empty = false;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      clip_axis(c[a], h, n, __ldg(b + a), __ldg(b + 3 + a), &lo[a], &hi[a]);
+      clip_axis(c[a], h, n, bb[a], bb[3 + a], &lo[a], &hi[a]);
       empty |= lo[a] > hi[a];
     }
     if (empty) continue;
@@ -615,6 +624,9 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
     int K = 0;
     for (int d = 0; d < s.nd; ++d) {
       const double* b = s.dbox + 6 * d;
+      if (__ldg(b) > c[0] + h || __ldg(b + 3) < c[0] - h || __ldg(b + 1) > c[1] + h ||
+          __ldg(b + 4) < c[1] - h || __ldg(b + 2) > c[2] + h || __ldg(b + 5) < c[2] - h)
+        continue;
       int lo[3], hi[3];
       bool empty = false;
       for (int a = 0; a < 3; ++a) {
