@@ -80,7 +80,7 @@ WALK_RECORD = np.dtype([("weight", "<f8"), ("mw_steps", "<u8"), ("slot", "<i4"),
                         ("branch", "u1"), ("resampled", "u1"), ("done", "u1")])
 MISS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int),
                       C.POINTER(C.c_double))
-MODE_MW, MODE_HYBRID_MW = 1, 3
+MODE_MW, MODE_MWE, MODE_HYBRID_MW, MODE_HYBRID_MWE = 1, 2, 3, 4
 
 _lib = None
 

@@ -176,10 +176,9 @@ Engine::Engine(const Structure& s, const Config& cfg, StratifiedSgfCache* cache)
     : s_(s), cfg_(cfg) {
   cfg_.validate();
   s_.validate();
-  if (cfg_.mode != Mode::MW && cfg_.mode != Mode::HybridMW)
-    throw std::invalid_argument("mode " + mode_name(cfg_.mode) +
-                                " is not available on the B200 device build yet; use "
-                                "HYBRID-MW or MW");
+  if (cfg_.mode == Mode::FDM)
+    throw std::invalid_argument("mode FDM (a direct solve per hop) is not available on the B200 "
+                                "device build yet; use HYBRID-MW or HYBRID-MWE");
   if (cache) {
     cache_ = cache;
   } else {
@@ -233,7 +232,12 @@ void Engine::upload() {
 frw_walk_params Engine::params() const {
   frw_walk_params p{};
   p.grid_n = cfg_.grid_n;
-  p.mode = cfg_.mode == Mode::MW ? FRW_MODE_MW : FRW_MODE_HYBRID_MW;
+  switch (cfg_.mode) {
+    case Mode::MW: p.mode = FRW_MODE_MW; break;
+    case Mode::MWE: p.mode = FRW_MODE_MWE; break;
+    case Mode::HybridMWE: p.mode = FRW_MODE_HYBRID_MWE; break;
+    default: p.mode = FRW_MODE_HYBRID_MW; break;
+  }
   p.expansion = cfg_.expansion;
   p.snap = snap_;
   p.hop_cap = cfg_.hop_cap;
@@ -378,7 +382,10 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
           default: break;
         }
         res.dispatch.cached += r.cached;
-        res.dispatch.microwalk += r.microwalk;
+        if (cfg_.mode == Mode::MWE || cfg_.mode == Mode::HybridMWE)
+          res.dispatch.microwalk_e += r.microwalk;  // engine.cpp:328 counts every MWE hop
+        else
+          res.dispatch.microwalk += r.microwalk;
         res.mw_steps += r.mw_steps;
       }
       walks += end - off;

@@ -40,7 +40,7 @@
 namespace frw {
 namespace {
 
-constexpr int KMAX = 32;    // clipped dielectric boxes per MicroWalk cube
+constexpr int KMAX = 64;    // clipped boxes (conductors + dielectrics) per MicroWalk cube
 constexpr int NMAX = 64;    // lattice size cap (layers per key)
 constexpr int PMAX = 64;    // permittivity palette cap
 constexpr int kSlotsDefault = 1 << 20;
@@ -82,6 +82,7 @@ struct DSgf {
 struct DParams {
   int n, panels, mode, rng;
   double snap;
+  double expansion;
   long long hop_cap;
   uint64_t seed, mixed_seed;
   double gbox[6], fcdf[6], area;
@@ -117,7 +118,8 @@ struct DSlots {
   // MicroWalk job compiled by k_advance
   double* cube;          // [S][4] center, half width
   uint8_t* nbox;         // [S]
-  uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class
+  uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class / conductor index
+  uint8_t* mwkind;       // [S] 0 plain MicroWalk job, 1 expanded (MicroWalk-E)
   uint64_t* room;        // [S] start cell distances (6 bytes, dir order)
   uint64_t* fc;          // [S] start cell + face-neighbour classes
 };
@@ -472,17 +474,45 @@ __device__ void clip_axis(double c, double h, int n, double lo, double hi, int* 
 __device__ __forceinline__ int box_lo(uint64_t b, int a) { return static_cast<int>((b >> (8 * a)) & 0xFF); }
 __device__ __forceinline__ int box_hi(uint64_t b, int a) { return static_cast<int>((b >> (24 + 8 * a)) & 0xFF); }
 __device__ __forceinline__ int box_cls(uint64_t b) { return static_cast<int>((b >> 48) & 0xFF); }
+// conductor boxes (MicroWalk-E cubes) carry bit 63 and their declaration
+// index in bits 48..62; a voxel inside any conductor box is conductor
+// (first declared wins, geometry.cpp:57-62 with tol 0), class code kCond
+constexpr int kCond = 0xFE;
+constexpr int kFace = 0xFF;
+__device__ __forceinline__ bool box_is_cond(uint64_t b) { return (b >> 63) != 0; }
+__device__ __forceinline__ int box_cond(uint64_t b) { return static_cast<int>((b >> 48) & 0x7FFF); }
+__device__ __forceinline__ uint64_t pack_box(const int lo[3], const int hi[3], uint64_t tag) {
+  return static_cast<uint64_t>(lo[0]) | static_cast<uint64_t>(lo[1]) << 8 |
+         static_cast<uint64_t>(lo[2]) << 16 | static_cast<uint64_t>(hi[0]) << 24 |
+         static_cast<uint64_t>(hi[1]) << 32 | static_cast<uint64_t>(hi[2]) << 40 | tag << 48;
+}
+__device__ __forceinline__ bool box_has(uint64_t b, int i, int j, int k) {
+  return i >= box_lo(b, 0) && i <= box_hi(b, 0) && j >= box_lo(b, 1) && j <= box_hi(b, 1) &&
+         k >= box_lo(b, 2) && k <= box_hi(b, 2);
+}
+// declaration index of the first conductor box containing voxel (i,j,k), -1
+__device__ int cell_conductor(const uint64_t* boxes, int K, int i, int j, int k) {
+  for (int q = 0; q < K; ++q) {
+    const uint64_t b = boxes[q];
+    if (box_is_cond(b) && box_has(b, i, j, k)) return box_cond(b);
+  }
+  return -1;
+}
 
 // class of voxel (i,j,k): the last clipped box containing it, else background
 __device__ int cell_class(const uint64_t* boxes, int K, int bg, int i, int j, int k) {
   int cls = bg;
+  bool cond = false;
   for (int q = 0; q < K; ++q) {
     const uint64_t b = boxes[q];
-    if (i >= box_lo(b, 0) && i <= box_hi(b, 0) && j >= box_lo(b, 1) && j <= box_hi(b, 1) &&
-        k >= box_lo(b, 2) && k <= box_hi(b, 2))
-      cls = box_cls(b);
+    if (box_has(b, i, j, k)) {
+      if (box_is_cond(b))
+        cond = true;
+      else
+        cls = box_cls(b);
+    }
   }
-  return cls;
+  return cond ? kCond : cls;
 }
 
 // extent [lo, hi] of the cell segment containing v along axis a
@@ -532,11 +562,39 @@ __device__ uint64_t cell_room(const uint64_t* boxes, int K, int n, uint32_t node
 }
 
 // compile the MicroWalk job of a general cube into the slot
-__device__ bool compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
-                               double h, int n, DCounters* C) {
+// Compiles the MicroWalk job of a cube into the slot: the boxes that reach
+// into the cube clipped to voxel-index ranges (with the reference's
+// voxel-centre arithmetic, microwalk.cpp:25-30), the start node's cell
+// extents and face-neighbour classes.  With `conductors` (MicroWalk-E,
+// microwalk.cpp:206-228) conductor boxes are clipped too.  Returns 1 ok,
+// 0 when the start voxel is conductor (EngulfedStart), -1 on overflow.
+__device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
+                              double h, int n, bool conductors, DCounters* C) {
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
   int K = 0;
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
+  for (int q = 0; conductors && q < s.nc; ++q) {
+    const double* b = s.cbox + 6 * q;
+    double bb[6];
+#pragma unroll
+    for (int t = 0; t < 6; ++t) bb[t] = __ldg(b + t);
+    if (bb[0] > cb[3] || bb[3] < cb[0] || bb[1] > cb[4] || bb[4] < cb[1] || bb[2] > cb[5] ||
+        bb[5] < cb[2])
+      continue;
+    int lo[3], hi[3];
+    bool empty = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      clip_axis(c[a], h, n, bb[a], bb[3 + a], &lo[a], &hi[a]);
+      empty |= lo[a] > hi[a];
+    }
+    if (empty) continue;
+    if (K == KMAX) {
+      set_err(C, FRW_EINVAL);
+      return -1;
+    }
+    boxes[K++] = pack_box(lo, hi, 0x8000ull | static_cast<uint64_t>(q));
+  }
   for (int d = 0; d < s.nd; ++d) {
     const double* b = s.dbox + 6 * d;
     double bb[6];
@@ -557,17 +615,15 @@ __device__ bool compile_mw_job(const DStruct& s, const DSlots& W, int slot, cons
     if (empty) continue;
     if (K == KMAX) {
       set_err(C, FRW_EINVAL);  // more than KMAX boxes reach into one cube
-      return false;
+      return -1;
     }
-    boxes[K++] = static_cast<uint64_t>(lo[0]) | static_cast<uint64_t>(lo[1]) << 8 |
-                 static_cast<uint64_t>(lo[2]) << 16 | static_cast<uint64_t>(hi[0]) << 24 |
-                 static_cast<uint64_t>(hi[1]) << 32 | static_cast<uint64_t>(hi[2]) << 40 |
-                 static_cast<uint64_t>(__ldg(s.dcls + d)) << 48;
+    boxes[K++] = pack_box(lo, hi, static_cast<uint64_t>(__ldg(s.dcls + d)));
   }
   const int m = (n - 1) / 2;  // start_node (sgf.hpp:58-61)
   const uint32_t node = m | (m << 8) | (m << 16);
-  const uint64_t room = cell_room(boxes, K, n, node);
   const int c0 = cell_class(boxes, K, s.bg, m, m, m);
+  if (c0 == kCond) return 0;  // EngulfedStart (microwalk.cpp:83-86)
+  const uint64_t room = cell_room(boxes, K, n, node);
   W.nbox[slot] = static_cast<uint8_t>(K);
   W.room[slot] = room;
   W.fc[slot] = face_classes(boxes, K, s.bg, n, node, room, c0);
@@ -575,7 +631,7 @@ __device__ bool compile_mw_job(const DStruct& s, const DSlots& W, int slot, cons
   W.cube[4 * slot + 1] = c[1];
   W.cube[4 * slot + 2] = c[2];
   W.cube[4 * slot + 3] = h;
-  return true;
+  return 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -635,10 +691,7 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
       }
       if (empty) continue;
       if (K == KMAX) return -1;
-      boxes[K++] = static_cast<uint64_t>(lo[0]) | static_cast<uint64_t>(lo[1]) << 8 |
-                   static_cast<uint64_t>(lo[2]) << 16 | static_cast<uint64_t>(hi[0]) << 24 |
-                   static_cast<uint64_t>(hi[1]) << 32 | static_cast<uint64_t>(hi[2]) << 40 |
-                   static_cast<uint64_t>(__ldg(s.dcls + d)) << 48;
+      boxes[K++] = pack_box(lo, hi, static_cast<uint64_t>(__ldg(s.dcls + d)));
     }
     double sl[3][NMAX];
     for (int a = 0; a < 3; ++a)
@@ -871,11 +924,30 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     ++L.hops;
     return 0;
   }
-  // general cube: MicroWalk (HYBRID-MW, engine.cpp:319-326)
-  if (!compile_mw_job(s, W, slot, c, h, n, C)) {
+  // general cube (engine.cpp:311-347): MicroWalk on the transit cube, or
+  // MicroWalk-E on the expanded cube, falling back to the transit cube when
+  // the expanded lattice swallows the start voxel (EngulfedStart)
+  int rc = -1;
+  uint8_t kind = 0;
+  if (P.mode == FRW_MODE_MWE || P.mode == FRW_MODE_HYBRID_MWE) {
+    kind = 1;
+    const double wall = cheb_wall(s.world, L.p);
+    const double half = mn(P.expansion * fh, wall);  // microwalk.cpp:213-214
+    if (!(half > 0)) {
+      set_err(C, FRW_EINVAL);
+      W.state[slot] = S_FREE;
+      return 1;
+    }
+    double ec[3], eh;
+    transit_cube(L.p, half, n, ec, &eh);
+    rc = compile_mw_job(s, W, slot, ec, eh, n, true, C);
+  }
+  if (rc == 0 || kind == 0) rc = compile_mw_job(s, W, slot, c, h, n, false, C);
+  if (rc < 0) {
     W.state[slot] = S_FREE;
     return 1;
   }
+  W.mwkind[slot] = kind;
   W.p[3 * slot + 0] = L.p[0];
   W.p[3 * slot + 1] = L.p[1];
   W.p[3 * slot + 2] = L.p[2];
@@ -1015,7 +1087,7 @@ __device__ __forceinline__ int mw_step(const DParams& P, const double* alpha_sm,
     double a = 0.5;
     if ((onface >> (8 * d + 7)) & 1) {
       const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-      a = cn == 0xFF ? 1.0 : alpha_sm[cn * Pn + c0];
+      a = cn >= kCond ? 1.0 : alpha_sm[cn * Pn + c0];  // lattice / conductor faces absorb
     }
     sum += a;
     acc[d] = sum;
@@ -1049,7 +1121,9 @@ __device__ __forceinline__ int mw_step(const DParams& P, const double* alpha_sm,
   const DirDelta del = dd[dir];
   *xdir = dir;
   if ((onface >> (8 * dir + 7)) & 1) {
-    if (((L.fc >> (8 * dir)) & 0xFF) == 0xFF) return 1;  // left the lattice
+    const int cn = static_cast<int>((L.fc >> (8 * dir)) & 0xFF);
+    if (cn == kFace) return 1;  // left the lattice (microwalk.cpp:126-135)
+    if (cn == kCond) return 3;  // absorbed by a conductor (microwalk.cpp:136-149)
     L.node += del.node;
     return 2;
   }
@@ -1076,7 +1150,8 @@ __device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* 
 // persistent MicroWalk kernel: each thread runs queued hops back to back
 template <int RNG>
 __global__ void __launch_bounds__(512)
-    k_mw(DStruct s, DParams P, DSlots W, DCounters* C, const int* queue, int* aq_out) {
+    k_mw(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* queue,
+         int* aq_out) {
   __shared__ double alpha_sm[PMAX * PMAX];
   __shared__ DirDelta dd[6];
   setup_smem_tables(s, alpha_sm, dd);
@@ -1120,10 +1195,20 @@ __global__ void __launch_bounds__(512)
       mw_cell_change(W, s, n, L, xdir);
       code = 0;
     }
-    if (live && (code == 1 || L.steps >= cap)) {
+    if (live && (code == 1 || code == 3 || L.steps >= cap)) {
       if (code == 1) {
         mw_exit(W, n, L, xdir);
         mw_requeue(C, aq_out, L.slot);
+      } else if (code == 3) {
+        // conductor exit: the walk terminates on that conductor
+        // (engine.cpp:333-336 -> run_walk's Terminate branch)
+        int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+        v[xdir >> 1] += (xdir & 1) ? 1 : -1;
+        const int ci = cell_conductor(W.boxes + static_cast<size_t>(L.slot) * KMAX, L.K, v[0],
+                                      v[1], v[2]);
+        W.mw[L.slot] += 1;
+        W.mwsteps[L.slot] += L.steps;
+        finish_walk(W, recs, C, L.slot, ci, false);
       } else {
         set_err(C, FRW_ESTEPCAP);
       }
@@ -1303,6 +1388,7 @@ void free_slots(Engine& E) {
   cudaFree(E.W.cube);
   cudaFree(E.W.nbox);
   cudaFree(E.W.boxes);
+  cudaFree(E.W.mwkind);
   cudaFree(E.W.room);
   cudaFree(E.W.fc);
   cudaFree(E.queue);
@@ -1441,6 +1527,7 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   W.cube = dalloc<double>(4 * size_t(S));
   W.nbox = dalloc<uint8_t>(S);
   W.boxes = dalloc<uint64_t>(size_t(S) * KMAX);
+  W.mwkind = dalloc<uint8_t>(S);
   W.room = dalloc<uint64_t>(S);
   W.fc = dalloc<uint64_t>(S);
   E.queue = dalloc<int>(S);
@@ -1450,7 +1537,7 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   E.M.pend = dalloc<long long>(S);
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
       !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes || !W.room ||
-      !W.fc || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend) {
+      !W.fc || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
   }
@@ -1608,9 +1695,12 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "run_walks: no structure uploaded");
   if (prm->grid_n < 2 || prm->grid_n > NMAX)
     return frw_fail(ctx, FRW_EINVAL, "run_walks: grid_n must lie in [2, 64]");
-  if (prm->mode != FRW_MODE_MW && prm->mode != FRW_MODE_HYBRID_MW)
+  if (prm->mode == FRW_MODE_FDM)
     return frw_fail(ctx, FRW_EINVAL,
-                    "run_walks: only MW / HYBRID-MW transitions run on the device in this build");
+                    "run_walks: FDM transitions (a PCG solve per hop) are not on the device yet");
+  if (prm->mode < FRW_MODE_FDM || prm->mode > FRW_MODE_HYBRID_MWE)
+    return frw_fail(ctx, FRW_EINVAL, "run_walks: unknown mode");
+  if (!(prm->expansion >= 1.0)) return frw_fail(ctx, FRW_EINVAL, "run_walks: expansion < 1");
   if (master < 0 || master >= E.nc) return frw_fail(ctx, FRW_EINVAL, "run_walks: bad master");
   if (count < 0) return frw_fail(ctx, FRW_EINVAL, "run_walks: count < 0");
   if (E.sgf.n && E.sgf.n != prm->grid_n)
@@ -1647,6 +1737,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   P.mode = prm->mode;
   P.rng = prm->rng_mode;
   P.snap = prm->snap;
+  P.expansion = prm->expansion;
   P.hop_cap = prm->hop_cap;
   P.seed = prm->seed;
   P.mixed_seed = sm64_mix(prm->seed);
@@ -1691,9 +1782,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                                                  E.queue);
     cudaEventRecord(m0, ctx->stream);
     if (P.rng == FRW_RNG_PHILOX)
-      k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt, E.queue, aq_out);
+      k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs, E.d_cnt, E.queue,
+                                                             aq_out);
     else
-      k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.d_cnt,
+      k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs, E.d_cnt,
                                                                       E.queue, aq_out);
     cudaEventRecord(m1, ctx->stream);
     FRW_CUDA(ctx, cudaGetLastError());
@@ -1838,9 +1930,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     out->aborted = st[0];
     out->resampled = st[1];
     for (int b = 0; b < 4; ++b) out->first[b] = st[2 + b];
+    const bool mwe = P.mode == FRW_MODE_MWE || P.mode == FRW_MODE_HYBRID_MWE;
     out->sub[0] = st[6];
-    out->sub[1] = st[7];
-    out->sub[2] = 0;
+    out->sub[1] = mwe ? 0 : st[7];
+    out->sub[2] = mwe ? st[7] : 0;  // lattice hops count as microwalk_e in MWE mode
     out->sub[3] = 0;
     out->mw_steps = st[8];
     out->cache_misses = misses_total;

@@ -42,16 +42,22 @@ CASES = {
 }
 
 
+MODES = {"HYBRID-MW": capi.MODE_HYBRID_MW, "HYBRID-MWE": capi.MODE_HYBRID_MWE}
+
+
+@pytest.mark.parametrize("mode", sorted(MODES))
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_walks_bit_exact_vs_oracle(gpu_ctx, oracle, case):
+def test_walks_bit_exact_vs_oracle(gpu_ctx, oracle, case, mode):
     make, n = CASES[case]
     sc = make()
     count = 600 if n == 24 else 2000
+    if mode == "HYBRID-MWE" and case in ("c3", "c4"):
+        count = 300  # expanded cubes: the oracle classifies far more voxels
     upload_scene(gpu_ctx, sc)
     gpu_ctx.sgf_clear()
-    p = walk_params(sc, grid_n=n, seed=77, rng=PARITY, n_slots=4096)
+    p = walk_params(sc, grid_n=n, seed=77, rng=PARITY, n_slots=4096, mode=MODES[mode])
     tally, rec = gpu_ctx.run_walks(p, sc.master_slot(), 0, count, oracle_solver(oracle))
-    slot, w, ab = oracle.run_walks(sc, 0, count, threads=8, grid_n=n, mode="HYBRID-MW", seed=77)
+    slot, w, ab = oracle.run_walks(sc, 0, count, threads=8, grid_n=n, mode=mode, seed=77)
     assert np.array_equal(rec["slot"], slot), np.nonzero(rec["slot"] != slot)[0][:10]
     assert np.array_equal(rec["aborted"], ab)
     assert np.array_equal(rec["weight"], w)  # bitwise: same arithmetic, no FMA
@@ -95,15 +101,16 @@ def _combined_z(a, sa, b, sb):
     return abs(a - b) / np.sqrt(sa ** 2 + sb ** 2)
 
 
-@pytest.mark.parametrize("case,walks_gpu,walks_cpu", [("c3", 200_000, 20_000),
-                                                      ("highk_cross", 200_000, 20_000)])
-def test_capacitance_within_3_se_of_oracle(oracle, case, walks_gpu, walks_cpu):
+@pytest.mark.parametrize("case,walks_gpu,walks_cpu,mode", [
+    ("c3", 200_000, 20_000, "HYBRID-MW"), ("highk_cross", 200_000, 20_000, "HYBRID-MW"),
+    ("c3", 200_000, 10_000, "HYBRID-MWE"), ("conformal_staircase", 200_000, 20_000, "HYBRID-MWE")])
+def test_capacitance_within_3_se_of_oracle(oracle, case, walks_gpu, walks_cpu, mode):
     import paper_2507_09730_b200.frwcap as frwcap
     make, n = CASES[case]
     sc = make()
-    g = frwcap.extract_json(sc.to_json(), mode="HYBRID-MW", grid_n=n, min_walks=walks_gpu,
+    g = frwcap.extract_json(sc.to_json(), mode=mode, grid_n=n, min_walks=walks_gpu,
                             max_walks=walks_gpu, seed=11)
-    o = oracle.extract(sc, threads=os.cpu_count() or 8, grid_n=n, mode="HYBRID-MW",
+    o = oracle.extract(sc, threads=os.cpu_count() or 8, grid_n=n, mode=mode,
                        min_walks=walks_cpu, max_walks=walks_cpu, seed=12)
     assert g["walks"] == walks_gpu
     for tg, to in zip(g["terminals"], o["terminals"]):
@@ -181,3 +188,13 @@ def test_c5_runs_and_lands_everywhere():
     assert res["walks"] == 50000 and res["aborted"] == 0
     assert res["terminals"][0]["capacitance_farads"] > 0
     assert sum(t["walks_landed"] > 0 for t in res["terminals"]) > 5
+
+
+def test_default_mode_is_hybrid_mwe_and_dispatch_counts():
+    """Reference default mode HYBRID-MWE (engine.hpp:31): every lattice hop
+    counts as microwalk_e (engine.cpp:328), none as microwalk."""
+    import paper_2507_09730_b200.frwcap as frwcap
+    res = frwcap.extract_json(json.dumps(c3_structure()), min_walks=20000, max_walks=20000, seed=2)
+    sub = res["dispatch_stats"]["subsequent"]
+    assert sub["microwalk"] == 0 and sub["microwalk_e"] > 0 and sub["fdm"] == 0
+    assert sum(res["dispatch_stats"]["first"].values()) == res["walks"]
