@@ -150,11 +150,20 @@ int frw_sgf_put(frw_ctx *ctx, int n, int axis, const double *layers,
                 double pitch, const double *probs, const double *cdf,
                 const double *kernels);
 int frw_sgf_count(const frw_ctx *ctx, int *entries);
+/* Device miss solver (sgf.cpp:57-290 on the canonical grid of each key,
+ * sgf_cache.cpp:78-96): `count` keys of lattice size n, axes[count],
+ * layers count x n (rounded).  Writes probs (count x 6n^2, clamped at 0 as
+ * in sgf.cpp:255-262) and, if non-NULL, kernels (count x 3 x 6n^2) to host
+ * memory; does not insert into the table.  FRW_ESOLVE when a PCG fails to
+ * converge or the normalization check fails. */
+int frw_sgf_solve(frw_ctx *ctx, int n, int count, const int *axes,
+                  const double *layers, double *probs, double *kernels);
 int frw_sgf_clear(frw_ctx *ctx);
 
 /* Called by frw_run_walks with the keys the table lacks (deduplicated;
- * layers is count x n, row-major); the host solves the canonical grids and
- * calls frw_sgf_put for each before returning 0.  The walks that missed
+ * layers is count x n, row-major); the host solves the canonical grids (or
+ * calls frw_sgf_solve) and frw_sgf_put's each before returning 0.  With a
+ * NULL callback frw_run_walks solves the misses on the device itself.  The walks that missed
  * are re-run from their start (their random streams are a pure function of
  * the walk id), so results do not depend on when an entry arrived. */
 typedef int (*frw_miss_fn)(void *user, int n, int count, const int *axes,

@@ -123,6 +123,8 @@ def lib():
         L.frw_sgf_put.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_double, _dp, _dp, _dp]
         L.frw_sgf_count.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
         L.frw_sgf_clear.argtypes = [C.c_void_p]
+        L.frw_sgf_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int), _dp, _dp,
+                                    _dp]
         L.frw_run_walks.argtypes = [C.c_void_p, C.POINTER(WalkParams), C.c_int32, C.c_uint64,
                                     C.c_int64, MISS_FN, C.c_void_p, C.POINTER(Tally),
                                     C.c_void_p]
@@ -289,6 +291,18 @@ class Context:
                                        probs.ctypes.data_as(_dp), cdf.ctypes.data_as(_dp),
                                        None if k is None else k.ctypes.data_as(_dp)))
 
+    def sgf_solve(self, n, axes, layers, kernels=True):
+        """Device miss solver: canonical SGFs of `len(axes)` keys."""
+        axes = np.ascontiguousarray(axes, np.int32)
+        layers = np.ascontiguousarray(layers, np.float64).reshape(len(axes), n)
+        P = 6 * n * n
+        probs = np.empty((len(axes), P))
+        ker = np.empty((len(axes), 3, P)) if kernels else None
+        self._check(self.L.frw_sgf_solve(self.h, n, len(axes), axes.ctypes.data_as(C.POINTER(C.c_int)),
+                                         layers.ctypes.data_as(_dp), probs.ctypes.data_as(_dp),
+                                         None if ker is None else ker.ctypes.data_as(_dp)))
+        return probs, ker
+
     def sgf_count(self):
         c = C.c_int()
         self._check(self.L.frw_sgf_count(self.h, C.byref(c)))
@@ -318,7 +332,7 @@ class Context:
                 errors.append(e)
                 return 1
 
-        fn = MISS_FN(cb)
+        fn = MISS_FN(cb) if solver is not None else MISS_FN()  # NULL: device solves
         rc = self.L.frw_run_walks(self.h, C.byref(params), master, walk_begin, count, fn, None,
                                   C.byref(t), None if rec is None else rec.ctypes.data_as(C.c_void_p))
         if errors:

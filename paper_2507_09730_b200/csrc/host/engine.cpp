@@ -257,20 +257,52 @@ namespace {
 struct MissCtx {
   frw_ctx* ctx;
   StratifiedSgfCache* cache;
+  bool host_solver;
   std::string err;
 };
 
+// Table misses: keys already in the host cache (e.g. loaded from an SGF1
+// file) are uploaded; the rest are solved -- on the device by default
+// (frw_sgf_solve), on host threads with host_sgf_solver -- stored in the
+// host cache (persistable) and uploaded.
 int miss_cb(void* user, int n, int count, const int* axes, const double* layers) {
   auto* m = static_cast<MissCtx*>(user);
   try {
-    std::vector<ProfileKey> keys(count);
+    std::vector<ProfileKey> keys(count), todo;
     for (int q = 0; q < count; ++q) {
       keys[q].n = n;
       keys[q].axis = axes[q];
       keys[q].layers.assign(layers + static_cast<size_t>(q) * n,
                             layers + static_cast<size_t>(q + 1) * n);
+      if (!m->cache->find(keys[q])) todo.push_back(keys[q]);
     }
-    m->cache->solve_many(keys);
+    if (m->host_solver) {
+      m->cache->solve_many(todo);
+    } else if (!todo.empty()) {
+      const size_t P = 6ull * n * n;
+      std::vector<int> ax;
+      std::vector<double> lay;
+      for (const auto& k : todo) {
+        ax.push_back(k.axis);
+        lay.insert(lay.end(), k.layers.begin(), k.layers.end());
+      }
+      std::vector<double> pr(P * todo.size()), ke(3 * P * todo.size());
+      throw_status(m->ctx, frw_sgf_solve(m->ctx, n, static_cast<int>(todo.size()), ax.data(),
+                                         lay.data(), pr.data(), ke.data()));
+      m->cache->count_misses(todo.size());
+      for (size_t q = 0; q < todo.size(); ++q) {
+        auto g = std::make_shared<DiscreteSGF>();
+        g->n = n;
+        g->pitch = 1.0;  // canonical unit pitch
+        g->probs.assign(pr.begin() + q * P, pr.begin() + (q + 1) * P);
+        g->cdf.resize(P);
+        double run = 0;
+        for (size_t b = 0; b < P; ++b) g->cdf[b] = run += g->probs[b];
+        for (int a = 0; a < 3; ++a)
+          g->grad_kernels[a].assign(ke.begin() + (3 * q + a) * P, ke.begin() + (3 * q + a + 1) * P);
+        m->cache->insert(todo[q], std::move(g));
+      }
+    }
     for (const auto& k : keys) put_entry(m->ctx, k, *m->cache->find(k));
     return 0;
   } catch (const std::exception& e) {
@@ -289,7 +321,7 @@ std::vector<frw_walk_record> Engine::run_walks(uint64_t begin, int64_t count) {
   t.sum = sum.data();
   t.sumsq = sq.data();
   t.landed = landed.data();
-  MissCtx mc{ctx_, cache_, {}};
+  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
   const frw_walk_params p = params();
   const int rc = frw_run_walks(ctx_, &p, master_slot_, begin, count, miss_cb, &mc, &t, rec.data());
   if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
@@ -346,7 +378,7 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   };
 
   const frw_walk_params p = params();
-  MissCtx mc{ctx_, cache_, {}};
+  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
   std::vector<frw_walk_record> rec;
   std::vector<double> ts(nslots), tq(nslots);
   std::vector<uint64_t> tl(nslots);

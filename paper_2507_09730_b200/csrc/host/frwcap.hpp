@@ -123,6 +123,10 @@ class StratifiedSgfCache {
   std::shared_ptr<const DiscreteSGF> find(const ProfileKey& key) const;
   // solves the missing keys in parallel (host threads)
   void solve_many(const std::vector<ProfileKey>& keys, int threads = 0);
+  // first stored result wins (sgf_cache.cpp:133-153)
+  std::shared_ptr<const DiscreteSGF> insert(const ProfileKey& key,
+                                            std::shared_ptr<const DiscreteSGF> sgf);
+  void count_misses(uint64_t k);
   struct Stats {
     uint64_t hits = 0, misses = 0;
     size_t size = 0;
@@ -166,6 +170,7 @@ struct Config {
   bool all_couplings_rule = false;  // stop when every coupling meets tol (C4)
   long device_batch = 1 << 20;      // walks per device launch sequence
   int device = 0;
+  bool host_sgf_solver = false;     // solve table misses on the host instead
 
   void validate() const;
 };

@@ -307,6 +307,17 @@ void StratifiedSgfCache::solve_many(const std::vector<ProfileKey>& keys, int thr
     if (e) std::rethrow_exception(e);
 }
 
+std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::insert(
+    const ProfileKey& key, std::shared_ptr<const DiscreteSGF> sgf) {
+  std::lock_guard<std::mutex> lk(mu_);
+  return map_.emplace(key, std::move(sgf)).first->second;
+}
+
+void StratifiedSgfCache::count_misses(uint64_t k) {
+  std::lock_guard<std::mutex> lk(mu_);
+  misses_ += k;
+}
+
 StratifiedSgfCache::Stats StratifiedSgfCache::stats() const {
   std::lock_guard<std::mutex> lk(mu_);
   return {hits_, misses_, map_.size()};

@@ -1807,10 +1807,6 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       break;
     }
     if (c.nmiss) {
-      if (!miss) {
-        status = frw_fail(ctx, FRW_EMISS, "run_walks: SGF table miss and no miss callback");
-        break;
-      }
       const int nm = static_cast<int>(std::min<unsigned long long>(c.nmiss, kMissMax));
       maxis.resize(nm);
       mlayers.resize(static_cast<size_t>(nm) * NMAX);
@@ -1832,9 +1828,27 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         ulayers.insert(ulayers.end(), L, L + P.n);
       }
       const int before = static_cast<int>(E.sgf.axis.size());
-      if (miss(user, P.n, static_cast<int>(uaxis.size()), uaxis.data(), ulayers.data()) != 0) {
-        status = frw_fail(ctx, FRW_ESOLVE, "run_walks: miss callback failed");
-        break;
+      if (miss) {
+        if (miss(user, P.n, static_cast<int>(uaxis.size()), uaxis.data(), ulayers.data()) != 0) {
+          status = frw_fail(ctx, FRW_ESOLVE, "run_walks: miss callback failed");
+          break;
+        }
+      } else {  // solve on the device and insert
+        const int cnt = static_cast<int>(uaxis.size());
+        const size_t pan = 6ull * P.n * P.n;
+        std::vector<double> pr(pan * cnt), ke(3 * pan * cnt), cdf(pan);
+        if (int rc = frw_sgf_solve(ctx, P.n, cnt, uaxis.data(), ulayers.data(), pr.data(),
+                                   ke.data())) {
+          status = rc;
+          break;
+        }
+        for (int q = 0; q < cnt && status == FRW_OK; ++q) {
+          double run = 0;
+          for (size_t b = 0; b < pan; ++b) cdf[b] = run += pr[q * pan + b];
+          status = frw_sgf_put(ctx, P.n, uaxis[q], &ulayers[static_cast<size_t>(q) * P.n], 1.0,
+                               &pr[q * pan], cdf.data(), &ke[3 * q * pan]);
+        }
+        if (status) break;
       }
       if (static_cast<int>(E.sgf.axis.size()) == before) {
         status = frw_fail(ctx, FRW_EMISS, "run_walks: miss callback added no table entry");

@@ -9,7 +9,7 @@ for name in which:
     doc = json.dumps({"c3": c3_structure, "c4": c4_structure, "c5": c5_structure}[name]())
     for walks in (100_000, 1_000_000, 1_000_000):
         t = time.time()
-        r = frwcap.extract_json(doc, mode="HYBRID-MW", min_walks=walks, max_walks=walks, seed=7)
+        r = frwcap.extract_json(doc, mode=os.environ.get("FRW_MODE", "HYBRID-MW"), min_walks=walks, max_walks=walks, seed=7)
         dt = time.time() - t
         print(f"{name} walks={walks} wall={dt:.2f}s dev={r['t_device_seconds']:.3f}s mw={r['t_mw_seconds']:.3f}s "
               f"walks/s(dev)={walks / r['t_device_seconds']:.3e} misses={r['cache']['misses']} "
