@@ -24,8 +24,9 @@
 //    162 KB for C2, so every step costs one LDS.U16 + one LDS.64 + one LDS.32
 //    (stride table, broadcast) instead of 7 conflicted loads.
 //  * Persistent CTAs, one walker per thread, refilled from a global transit
-//    counter; lanes step in phase-aligned super-steps of 4 so Philox blocks
-//    and exit bookkeeping are warp-uniform (the re-binning of live walkers: a
+//    counter; lanes step in phase-aligned super-steps (8 steps per Philox
+//    call, 16 bits of each word per step) so Philox blocks and exit
+//    bookkeeping are warp-uniform (the re-binning of live walkers: a
 //    lane whose transit ends is re-armed with the next transit at the next
 //    super-step boundary instead of idling).
 //  * Histogram (RED.64 to global), exact u64 step moments and optional
@@ -301,8 +302,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t k0 = static_cast<uint32_t>(p.seed);
   const uint32_t k1 = static_cast<uint32_t>(p.seed >> 32);
 
+  // Philox: one 4x32-10 call per super-step of 8 steps -- each 32-bit word
+  // gives two steps their top 16 bits of x; the low 37 bits are drawn from
+  // the (id, step slot, 1) counter only when the 16-bit prefix ties a
+  // threshold, so x is still an exact 53-bit uniform.  Parity: 4 steps.
+  constexpr int SS = RNG == FRW_RNG_PHILOX ? 8 : 4;
   while (__any_sync(0xFFFFFFFFu, live)) {
-    // ---- one phase-aligned super-step of 4 lattice steps ----------------
+    // ---- one phase-aligned super-step of SS lattice steps ----------------
     uint32_t w[4];
     if (RNG == FRW_RNG_PHILOX) {
       const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
@@ -315,21 +321,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     bool exited = false;
     int xdir = 0;
-    // The four steps run unconditionally (predicated state updates, no
-    // per-step branch); a lane that has exited, or reached the cap, keeps
-    // re-reading its last node without consuming randomness.
+    // The steps run unconditionally (predicated state updates, no per-step
+    // branch); a lane that has exited keeps re-reading its last node without
+    // consuming randomness.  The step cap is checked per super-step: a
+    // transit is an error iff it needs more than `cap` steps
+    // (microwalk.cpp:81, :153-155), whichever step inside the super-step
+    // crossed it.
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool act = live && !exited && steps < cap;
+    for (int u = 0; u < SS; ++u) {
+      const bool act = live && !exited;
       uint64_t z = 0;
-      uint32_t x10;
+      uint32_t x10, h16 = 0;
       if (RNG == FRW_RNG_SPLITMIX_PARITY) {
         const uint64_t s1 = sm + kGamma;  // SplitMix64::next (rng.hpp:19-22)
         z = sm64_mix(s1);
         sm = act ? s1 : sm;
         x10 = static_cast<uint32_t>(z >> 54);  // top 10 bits of x = z >> 11
       } else {
-        x10 = w[u] >> 22;
+        h16 = (u & 1) ? (w[u >> 1] & 0xFFFFu) : (w[u >> 1] >> 16);
+        x10 = h16 >> 6;
       }
       steps += act;
       const uint32_t r = SMEM ? lds_u16(s_map + 2u * idx) : __ldg(g.map + idx);
@@ -353,24 +363,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int d = 0; d < 5; ++d) dir += x53 >= __ldg(f + d);
         } else {
-          // the 32-bit word is the top of x; its low 21 bits are drawn
-          // from the (id, step, 1) counter only on a further tie
-          const uint32_t xh = w[u];
           dir = 0;
-          bool tie32 = false;
+          bool tie16 = false;
 #pragma unroll
           for (int d = 0; d < 5; ++d) {
-            const uint32_t th = static_cast<uint32_t>(__ldg(f + d) >> 21);
-            dir += xh > th;
-            tie32 |= xh == th;
+            const uint64_t th = __ldg(f + d) >> 37;
+            dir += h16 > th;
+            tie16 |= h16 == th;
           }
-          if (tie32) {
+          if (tie16) {
             const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
-            const uint32_t lo = philox4x32_10({static_cast<uint32_t>(id),
-                                               static_cast<uint32_t>(id >> 32),
-                                               static_cast<uint32_t>(steps), 1u},
-                                              k0, k1).x >> 11;
-            const uint64_t x53 = (static_cast<uint64_t>(xh) << 21) | lo;
+            const U32x4 o = philox4x32_10({static_cast<uint32_t>(id),
+                                           static_cast<uint32_t>(id >> 32), blk * SS + u, 1u},
+                                          k0, k1);
+            const uint64_t low37 = ((static_cast<uint64_t>(o.x) << 32) | o.y) >> 27;
+            const uint64_t x53 = (static_cast<uint64_t>(h16) << 37) | low37;
             dir = 0;
 #pragma unroll
             for (int d = 0; d < 5; ++d) dir += x53 >= __ldg(f + d);
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- exit bookkeeping, batched once per super-step -------------------
     if (live && (exited || steps >= cap)) {
       int32_t panel = -1, cid = -1;
-      if (exited) {
+      if (exited && steps <= cap) {
         const int k = fdiv(idx, g.nn, g.inv_nn);
         const int rem = idx - k * g.nn;
         const int j = fdiv(rem, n, g.inv_n);
