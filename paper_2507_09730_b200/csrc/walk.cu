@@ -44,6 +44,16 @@ constexpr int KMAX = 64;    // clipped boxes (conductors + dielectrics) per Micr
 constexpr int NMAX = 64;    // lattice size cap (layers per key)
 constexpr int PMAX = 64;    // permittivity palette cap
 constexpr int kSlotsDefault = 1 << 20;
+// Cell atlas of a MicroWalk job (u64 words per slot).  Along each axis the
+// clipped boxes' faces cut [0, n) into segments; bm[a] holds one bit per
+// segment start.  mask[a][s] is the set of clipped boxes (bit q = box q)
+// spanning segment s, so the boxes containing a cell are the AND of its
+// three segment masks and its class is a bit scan.  n <= NMAX = 64 keeps
+// every bitmap in one word.
+constexpr int kAtMask = 0;    // [3][64] segment masks
+constexpr int kAtBm = 192;    // [3] segment-start bitmaps
+constexpr int kAtCls = 195;   // [KMAX] class byte of each clipped box
+constexpr int kAtlasWords = 208;
 constexpr double kEps0 = 8.8541878128e-12;  // constants.hpp:5
 constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
@@ -117,8 +127,9 @@ struct DSlots {
   uint8_t* resampled;
   // MicroWalk job compiled by k_advance
   double* cube;          // [S][4] center, half width
-  uint8_t* nbox;         // [S]
+  uint8_t* nbox;         // [S] conductor boxes among the clipped boxes
   uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class / conductor index
+  uint64_t* atlas;       // [S][kAtlasWords] cell atlas of the job (see cell_info)
   uint8_t* mwkind;       // [S] 0 plain MicroWalk job, 1 expanded (MicroWalk-E)
   uint64_t* room;        // [S] start cell distances (6 bytes, dir order)
   uint64_t* fc;          // [S] start cell + face-neighbour classes
@@ -490,15 +501,6 @@ __device__ __forceinline__ bool box_has(uint64_t b, int i, int j, int k) {
   return i >= box_lo(b, 0) && i <= box_hi(b, 0) && j >= box_lo(b, 1) && j <= box_hi(b, 1) &&
          k >= box_lo(b, 2) && k <= box_hi(b, 2);
 }
-// declaration index of the first conductor box containing voxel (i,j,k), -1
-__device__ int cell_conductor(const uint64_t* boxes, int K, int i, int j, int k) {
-  for (int q = 0; q < K; ++q) {
-    const uint64_t b = boxes[q];
-    if (box_is_cond(b) && box_has(b, i, j, k)) return box_cond(b);
-  }
-  return -1;
-}
-
 // class of voxel (i,j,k): the last clipped box containing it, else background
 __device__ int cell_class(const uint64_t* boxes, int K, int bg, int i, int j, int k) {
   int cls = bg;
@@ -531,34 +533,94 @@ __device__ void cell_extent(const uint64_t* boxes, int K, int n, int a, int v, i
 // node packing: i | j<<8 | k<<16
 __device__ __forceinline__ int coord(uint32_t node, int a) { return (node >> (8 * a)) & 0xFF; }
 
-// face-neighbour classes of the cell containing `node` (0xFF: lattice face)
-__device__ uint64_t face_classes(const uint64_t* boxes, int K, int bg, int n, uint32_t node,
-                                 uint64_t room, int c0) {
-  uint64_t fc = static_cast<uint64_t>(c0) << 48;
-#pragma unroll 1
-  for (int d = 0; d < 6; ++d) {
-    const int a = d >> 1;
-    const int dist = static_cast<int>((room >> (8 * d)) & 0xFF);
-    int v[3] = {coord(node, 0), coord(node, 1), coord(node, 2)};
-    v[a] += (d & 1) ? dist + 1 : -(dist + 1);
-    uint64_t cls = 0xFF;
-    if (v[a] >= 0 && v[a] < n) cls = static_cast<uint64_t>(cell_class(boxes, K, bg, v[0], v[1], v[2]));
-    fc |= cls << (8 * d);
+// ---- cell atlas lookups ---------------------------------------------------
+__device__ __forceinline__ uint64_t upto(int v) { return (2ull << v) - 1; }  // bits 0..v
+
+// class of the voxels contained in exactly the clipped boxes of M: any
+// conductor box (bits [0, ncond)) makes it conductor, else the last
+// declared dielectric box wins (geometry.cpp:42-55), else background
+__device__ __forceinline__ int class_of(const uint8_t* cls, uint64_t M, uint64_t cmask, int bg) {
+  if (M & cmask) return kCond;
+  const uint64_t d = M & ~cmask;
+  return d ? cls[63 - __clzll(d)] : bg;
+}
+
+__device__ __forceinline__ uint64_t cond_mask(int ncond) {
+  return ncond >= 64 ? ~0ull : (1ull << ncond) - 1;
+}
+
+// box set of the voxel at integer coordinates v
+__device__ __forceinline__ uint64_t voxel_mask(const uint64_t* A, const uint64_t bm[3],
+                                               const int v[3]) {
+  uint64_t M = ~0ull;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) M &= A[kAtMask + 64 * a + __popcll(bm[a] & upto(v[a])) - 1];
+  return M;
+}
+
+// The cell (maximal box of voxels with one box set) containing `node`: its
+// face distances (room, one byte per direction 2a+side) and the classes of
+// the six face-neighbour cells (kFace on a lattice face) with its own class
+// in byte 6.  O(1): three bit scans per axis and nine mask loads.
+__device__ uint64_t cell_info(const uint64_t* A, const uint64_t bm[3], int ncond, int bg, int n,
+                              uint32_t node, uint64_t* room_out) {
+  const uint8_t* cls = reinterpret_cast<const uint8_t*>(A + kAtCls);
+  const uint64_t cmask = cond_mask(ncond);
+  uint64_t M[3], Ml[3], Mh[3];
+  bool hl[3], hh[3];
+  uint64_t room = 0x0101ull << 48;  // two unused bytes kept non-zero
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int v = coord(node, a);
+    const uint64_t below = bm[a] & upto(v), above = bm[a] & ~upto(v);
+    const int sg = __popcll(below) - 1;
+    const int lo = 63 - __clzll(below);
+    const int hi = above ? __ffsll(above) - 2 : n - 1;
+    room |= static_cast<uint64_t>(v - lo) << (16 * a);
+    room |= static_cast<uint64_t>(hi - v) << (16 * a + 8);
+    const uint64_t* mk = A + kAtMask + 64 * a;
+    hl[a] = lo > 0;
+    hh[a] = hi < n - 1;
+    M[a] = mk[sg];
+    Ml[a] = hl[a] ? mk[sg - 1] : 0;
+    Mh[a] = hh[a] ? mk[sg + 1] : 0;
   }
+  uint64_t fc = static_cast<uint64_t>(class_of(cls, M[0] & M[1] & M[2], cmask, bg)) << 48;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const uint64_t rest = M[(a + 1) % 3] & M[(a + 2) % 3];
+    const uint64_t cl = hl[a] ? class_of(cls, Ml[a] & rest, cmask, bg) : kFace;
+    const uint64_t ch = hh[a] ? class_of(cls, Mh[a] & rest, cmask, bg) : kFace;
+    fc |= cl << (16 * a) | ch << (16 * a + 8);
+  }
+  *room_out = room;
   return fc;
 }
 
-__device__ uint64_t cell_room(const uint64_t* boxes, int K, int n, uint32_t node) {
-  uint64_t room = 0x0101ull << 48;  // two unused bytes kept non-zero
+// builds the atlas of the K clipped boxes of a job (compile_mw_job)
+__device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, uint64_t bm[3]) {
 #pragma unroll 1
   for (int a = 0; a < 3; ++a) {
-    int lo, hi;
-    const int v = coord(node, a);
-    cell_extent(boxes, K, n, a, v, &lo, &hi);
-    room |= static_cast<uint64_t>(v - lo) << (16 * a);
-    room |= static_cast<uint64_t>(hi - v) << (16 * a + 8);
+    uint64_t b = 1;  // segment starting at 0
+    for (int q = 0; q < K; ++q) {
+      const uint64_t x = boxes[q];
+      const int h = box_hi(x, a) + 1;
+      b |= 1ull << box_lo(x, a);
+      if (h < n) b |= 1ull << h;
+    }
+    bm[a] = b;
+    A[kAtBm + a] = b;
+    int sg = 0;
+    for (uint64_t y = b; y; y &= y - 1, ++sg) {
+      const int st = __ffsll(y) - 1;
+      uint64_t m = 0;
+      for (int q = 0; q < K; ++q) {
+        const uint64_t x = boxes[q];
+        if (box_lo(x, a) <= st && st <= box_hi(x, a)) m |= 1ull << q;
+      }
+      A[kAtMask + 64 * a + sg] = m;
+    }
   }
-  return room;
 }
 
 // compile the MicroWalk job of a general cube into the slot
@@ -571,6 +633,7 @@ __device__ uint64_t cell_room(const uint64_t* boxes, int K, int n, uint32_t node
 __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
                               double h, int n, bool conductors, DCounters* C) {
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
+  uint64_t* A = W.atlas + static_cast<size_t>(slot) * kAtlasWords;
   int K = 0;
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
   for (int q = 0; conductors && q < s.nc; ++q) {
@@ -595,6 +658,8 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
     }
     boxes[K++] = pack_box(lo, hi, 0x8000ull | static_cast<uint64_t>(q));
   }
+  const int ncond = K;
+  uint8_t* cls = reinterpret_cast<uint8_t*>(A + kAtCls);
   for (int d = 0; d < s.nd; ++d) {
     const double* b = s.dbox + 6 * d;
     double bb[6];
@@ -617,16 +682,20 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
       set_err(C, FRW_EINVAL);  // more than KMAX boxes reach into one cube
       return -1;
     }
-    boxes[K++] = pack_box(lo, hi, static_cast<uint64_t>(__ldg(s.dcls + d)));
+    const int dc = __ldg(s.dcls + d);
+    cls[K] = static_cast<uint8_t>(dc);
+    boxes[K++] = pack_box(lo, hi, static_cast<uint64_t>(dc));
   }
+  uint64_t bm[3];
+  build_atlas(boxes, K, n, A, bm);
   const int m = (n - 1) / 2;  // start_node (sgf.hpp:58-61)
   const uint32_t node = m | (m << 8) | (m << 16);
-  const int c0 = cell_class(boxes, K, s.bg, m, m, m);
-  if (c0 == kCond) return 0;  // EngulfedStart (microwalk.cpp:83-86)
-  const uint64_t room = cell_room(boxes, K, n, node);
-  W.nbox[slot] = static_cast<uint8_t>(K);
+  uint64_t room;
+  const uint64_t fc = cell_info(A, bm, ncond, s.bg, n, node, &room);
+  if (((fc >> 48) & 0xFF) == kCond) return 0;  // EngulfedStart (microwalk.cpp:83-86)
+  W.nbox[slot] = static_cast<uint8_t>(ncond);
   W.room[slot] = room;
-  W.fc[slot] = face_classes(boxes, K, s.bg, n, node, room, c0);
+  W.fc[slot] = fc;
   W.cube[4 * slot + 0] = c[0];
   W.cube[4 * slot + 1] = c[1];
   W.cube[4 * slot + 2] = c[2];
@@ -998,37 +1067,51 @@ struct MwLane {
   uint64_t fc;    // face-neighbour classes (byte per dir), current class in byte 6
   uint64_t rng;   // SplitMix64 state or Philox block counter
   int steps;
-  int K;
+  int ncond;      // conductor boxes of the job (atlas bits [0, ncond))
+  uint64_t bm[3]; // segment-start bitmaps of the job's atlas
+  double al[6];   // alpha of the neighbour across each face of the cell
   uint32_t gsteps;  // diagnostics, accumulated across the lane's hops
   uint32_t cchg;
 };
 
-__device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int n, MwLane& L) {
+// the per-face alphas of the lane's cell: palette pair (face class, own
+// class), 1 for lattice and conductor faces (both absorb the step)
+__device__ __forceinline__ void lane_alphas(const double* alpha_sm, int Pn, MwLane& L) {
+  const int c0 = static_cast<int>((L.fc >> 48) & 0xFF);
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
+    L.al[d] = cn >= kCond ? 1.0 : alpha_sm[cn * Pn + c0];
+  }
+}
+
+__device__ __forceinline__ const uint64_t* lane_atlas(const DSlots& W, int slot) {
+  return W.atlas + static_cast<size_t>(slot) * kAtlasWords;
+}
+
+__device__ __forceinline__ void mw_arm(const DSlots& W, const double* alpha_sm, int Pn, int slot,
+                                       int n, MwLane& L) {
   const int m = (n - 1) / 2;
+  const uint64_t* A = lane_atlas(W, slot);
   L.slot = slot;
   L.wid = W.wid[slot];
   L.node = m | (m << 8) | (m << 16);
   L.room = W.room[slot];
   L.fc = W.fc[slot];
   L.rng = W.rng[slot];
-  L.K = W.nbox[slot];
+  L.ncond = W.nbox[slot];
+  L.bm[0] = A[kAtBm];
+  L.bm[1] = A[kAtBm + 1];
+  L.bm[2] = A[kAtBm + 2];
   L.steps = 0;
+  lane_alphas(alpha_sm, Pn, L);
 }
 
-// handles a move that left the current cell along dir d into the adjacent
-// cell (same segments on the other two axes)
-__device__ void mw_cell_change(const DSlots& W, const DStruct& s, int n, MwLane& L, int d) {
-  const uint64_t* boxes = W.boxes + static_cast<size_t>(L.slot) * KMAX;
-  const int a = d >> 1;
-  int lo, hi;
-  const int v = coord(L.node, a);
-  cell_extent(boxes, L.K, n, a, v, &lo, &hi);
-  const int c0 = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-  uint64_t room = L.room & ~(0xFFFFull << (16 * a));
-  room |= static_cast<uint64_t>(v - lo) << (16 * a);
-  room |= static_cast<uint64_t>(hi - v) << (16 * a + 8);
-  L.room = room;
-  L.fc = face_classes(boxes, L.K, s.bg, n, L.node, room, c0);
+// a move left the current cell: look the new cell up in the atlas
+__device__ __forceinline__ void mw_cell_change(const DSlots& W, const double* alpha_sm, int Pn,
+                                               int bg, int n, MwLane& L) {
+  L.fc = cell_info(lane_atlas(W, L.slot), L.bm, L.ncond, bg, n, L.node, &L.room);
+  lane_alphas(alpha_sm, Pn, L);
 }
 
 // surface exit: continuation point, counters, slot back to ACTIVE
@@ -1071,11 +1154,9 @@ struct DirDelta {
 // the cell), 1 (surface exit through *xdir) or 2 (moved into the adjacent
 // cell along *xdir; the caller refreshes the cell data).
 template <int RNG>
-__device__ __forceinline__ int mw_step(const DParams& P, const double* alpha_sm, int Pn,
-                                       const DirDelta* dd, MwLane& L, uint32_t w, uint64_t z,
-                                       uint32_t tie_ctr, int* xdir) {
+__device__ __forceinline__ int mw_step(const DParams& P, const DirDelta* dd, MwLane& L, uint32_t w,
+                                       uint64_t z, uint32_t tie_ctr, int* xdir) {
   ++L.steps;
-  const int c0 = static_cast<int>((L.fc >> 48) & 0xFF);
   // exact zero-byte mask of the six room bytes: bit 8d+7 set <=> on face d
   const uint64_t r = L.room & 0x0000FFFFFFFFFFFFull;
   const uint64_t t = (r & 0x00007F7F7F7F7F7Full) + 0x00007F7F7F7F7F7Full;
@@ -1084,12 +1165,7 @@ __device__ __forceinline__ int mw_step(const DParams& P, const double* alpha_sm,
   double sum = 0;
 #pragma unroll
   for (int d = 0; d < 6; ++d) {
-    double a = 0.5;
-    if ((onface >> (8 * d + 7)) & 1) {
-      const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-      a = cn >= kCond ? 1.0 : alpha_sm[cn * Pn + c0];  // lattice / conductor faces absorb
-    }
-    sum += a;
+    sum += ((onface >> (8 * d + 7)) & 1) ? L.al[d] : 0.5;
     acc[d] = sum;
   }
   if (onface) ++L.gsteps;
@@ -1163,7 +1239,7 @@ __global__ void __launch_bounds__(512)
   L.cchg = 0;
   unsigned long long item = atomicAdd(&C->qhead, 1ull);
   bool live = item < qlen;
-  if (live) mw_arm(W, queue[item], n, L);
+  if (live) mw_arm(W, alpha_sm, s.P, queue[item], n, L);
   while (__any_sync(0xFFFFFFFFu, live)) {
     uint32_t w4[4] = {0, 0, 0, 0};
     if (RNG == FRW_RNG_PHILOX && live) {
@@ -1183,8 +1259,7 @@ __global__ void __launch_bounds__(512)
       if (live && code == 0 && L.steps < cap) {
         uint64_t z = 0;
         if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
-        code = mw_step<RNG>(P, alpha_sm, s.P, dd, L, w4[u], z,
-                            static_cast<uint32_t>(L.rng * 4 + u), &xdir);
+        code = mw_step<RNG>(P, dd, L, w4[u], z, static_cast<uint32_t>(L.rng * 4 + u), &xdir);
       }
     }
     if (RNG == FRW_RNG_PHILOX && live) ++L.rng;  // next 4-word block
@@ -1192,7 +1267,7 @@ __global__ void __launch_bounds__(512)
     // crossed a face (they skipped the rest of the super-step)
     if (live && code == 2) {
       ++L.cchg;
-      mw_cell_change(W, s, n, L, xdir);
+      mw_cell_change(W, alpha_sm, s.P, s.bg, n, L);
       code = 0;
     }
     if (live && (code == 1 || code == 3 || L.steps >= cap)) {
@@ -1202,10 +1277,11 @@ __global__ void __launch_bounds__(512)
       } else if (code == 3) {
         // conductor exit: the walk terminates on that conductor
         // (engine.cpp:333-336 -> run_walk's Terminate branch)
+        // the first declared conductor box holding the voxel across the face
         int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
         v[xdir >> 1] += (xdir & 1) ? 1 : -1;
-        const int ci = cell_conductor(W.boxes + static_cast<size_t>(L.slot) * KMAX, L.K, v[0],
-                                      v[1], v[2]);
+        const uint64_t cm = voxel_mask(lane_atlas(W, L.slot), L.bm, v) & cond_mask(L.ncond);
+        const int ci = box_cond(W.boxes[static_cast<size_t>(L.slot) * KMAX + __ffsll(cm) - 1]);
         W.mw[L.slot] += 1;
         W.mwsteps[L.slot] += L.steps;
         finish_walk(W, recs, C, L.slot, ci, false);
@@ -1214,7 +1290,7 @@ __global__ void __launch_bounds__(512)
       }
       item = atomicAdd(&C->qhead, 1ull);
       live = item < qlen;
-      if (live) mw_arm(W, queue[item], n, L);
+      if (live) mw_arm(W, alpha_sm, s.P, queue[item], n, L);
     }
   }
   unsigned long long g = L.gsteps, cc = L.cchg;
@@ -1391,6 +1467,7 @@ void free_slots(Engine& E) {
   cudaFree(E.W.mwkind);
   cudaFree(E.W.room);
   cudaFree(E.W.fc);
+  cudaFree(E.W.atlas);
   cudaFree(E.queue);
   cudaFree(E.aq[0]);
   cudaFree(E.aq[1]);
@@ -1530,6 +1607,7 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   W.mwkind = dalloc<uint8_t>(S);
   W.room = dalloc<uint64_t>(S);
   W.fc = dalloc<uint64_t>(S);
+  W.atlas = dalloc<uint64_t>(size_t(S) * kAtlasWords);
   E.queue = dalloc<int>(S);
   E.aq[0] = dalloc<int>(S);
   E.aq[1] = dalloc<int>(S);
@@ -1537,7 +1615,7 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   E.M.pend = dalloc<long long>(S);
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
       !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes || !W.room ||
-      !W.fc || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend) {
+      !W.fc || !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
   }
