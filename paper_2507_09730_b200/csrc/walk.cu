@@ -30,6 +30,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -946,8 +948,9 @@ __device__ __forceinline__ void adv_load(const DSlots& W, int slot, AdvLane& L) 
 
 // One transition (engine.cpp:290-350; hop cap engine.cpp:367-375) of the
 // lane's walk.  Returns 0 when a cached hop was taken (the walk stays with
-// the lane), 1 when the walk left the stage: terminated, parked by a table
-// miss, or queued for a MicroWalk hop.
+// the lane), 1 when the walk left the stage (terminated or parked by a
+// table miss), 2 when its MicroWalk job is compiled (pushed to `mq` unless
+// null).
 __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, const DSlots& W,
                             WalkRec* recs, DCounters* C, const DMiss& M, int* mq, AdvLane& L) {
   const int slot = L.slot;
@@ -1024,8 +1027,8 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   W.hops[slot] = L.hops + 1;
   W.cached[slot] = L.cached;
   W.state[slot] = S_NEED_MW;
-  mq[atomicAdd(&C->qlen, 1ull)] = slot;
-  return 1;
+  if (mq) mq[atomicAdd(&C->qlen, 1ull)] = slot;
+  return 2;
 }
 
 // persistent: each thread takes ACTIVE walks from the queue and advances
@@ -1223,6 +1226,74 @@ __device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* 
   __syncthreads();
 }
 
+// Events of a MicroWalk super-step
+enum : int { MW_GO = 0, MW_SURFACE = 1, MW_COND = 3, MW_CAP = 4 };
+
+// Up to four lattice steps of the lane's hop from one Philox block (four
+// SplitMix64 draws in parity mode); a move into another cell ends the
+// super-step and refreshes the cell from the atlas.  Returns an MW_* event.
+template <int RNG>
+__device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
+                                            const double* alpha_sm, int Pn, int bg,
+                                            const DirDelta* dd, int n, int cap, MwLane& L,
+                                            int* xdir) {
+  uint32_t w4[4] = {0, 0, 0, 0};
+  if (RNG == FRW_RNG_PHILOX) {
+    const uint64_t id = P.walk_begin + L.wid;
+    const U32x4 o = philox4x32_10(
+        {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
+         static_cast<uint32_t>(L.rng), 2u},
+        static_cast<uint32_t>(P.seed), static_cast<uint32_t>(P.seed >> 32));
+    w4[0] = o.x;
+    w4[1] = o.y;
+    w4[2] = o.z;
+    w4[3] = o.w;
+  }
+  int code = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (code == 0 && L.steps < cap) {
+      uint64_t z = 0;
+      if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
+      code = mw_step<RNG>(P, dd, L, w4[u], z, static_cast<uint32_t>(L.rng * 4 + u), xdir);
+    }
+  }
+  if (RNG == FRW_RNG_PHILOX) ++L.rng;  // next 4-word block
+  if (code == 2) {
+    ++L.cchg;
+    mw_cell_change(W, alpha_sm, Pn, bg, n, L);
+    code = 0;
+  }
+  if (code == 0 && L.steps >= cap) return MW_CAP;
+  return code;
+}
+
+// conductor exit: the walk terminates on the first declared conductor box
+// holding the voxel across the face (engine.cpp:333-336 -> run_walk's
+// Terminate branch)
+__device__ void mw_conductor_exit(const DSlots& W, WalkRec* recs, DCounters* C, MwLane& L,
+                                  int xdir) {
+  int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+  v[xdir >> 1] += (xdir & 1) ? 1 : -1;
+  const uint64_t cm = voxel_mask(lane_atlas(W, L.slot), L.bm, v) & cond_mask(L.ncond);
+  const int ci = box_cond(W.boxes[static_cast<size_t>(L.slot) * KMAX + __ffsll(cm) - 1]);
+  W.mw[L.slot] += 1;
+  W.mwsteps[L.slot] += L.steps;
+  finish_walk(W, recs, C, L.slot, ci, false);
+}
+
+__device__ __forceinline__ void flush_mw_stats(DCounters* C, const MwLane& L) {
+  unsigned long long g = L.gsteps, cc = L.cchg;
+  for (int o = 16; o > 0; o >>= 1) {
+    g += __shfl_xor_sync(0xFFFFFFFFu, g, o);
+    cc += __shfl_xor_sync(0xFFFFFFFFu, cc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&C->gen_steps, g);
+    atomicAdd(&C->cell_chg, cc);
+  }
+}
+
 // persistent MicroWalk kernel: each thread runs queued hops back to back
 template <int RNG>
 __global__ void __launch_bounds__(512)
@@ -1241,50 +1312,14 @@ __global__ void __launch_bounds__(512)
   bool live = item < qlen;
   if (live) mw_arm(W, alpha_sm, s.P, queue[item], n, L);
   while (__any_sync(0xFFFFFFFFu, live)) {
-    uint32_t w4[4] = {0, 0, 0, 0};
-    if (RNG == FRW_RNG_PHILOX && live) {
-      const uint64_t id = P.walk_begin + L.wid;
-      const U32x4 o = philox4x32_10(
-          {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
-           static_cast<uint32_t>(L.rng), 2u},
-          static_cast<uint32_t>(P.seed), static_cast<uint32_t>(P.seed >> 32));
-      w4[0] = o.x;
-      w4[1] = o.y;
-      w4[2] = o.z;
-      w4[3] = o.w;
-    }
-    int code = 0, xdir = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (live && code == 0 && L.steps < cap) {
-        uint64_t z = 0;
-        if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
-        code = mw_step<RNG>(P, dd, L, w4[u], z, static_cast<uint32_t>(L.rng * 4 + u), &xdir);
-      }
-    }
-    if (RNG == FRW_RNG_PHILOX && live) ++L.rng;  // next 4-word block
-    // cell changes of the super-step, processed together by the lanes that
-    // crossed a face (they skipped the rest of the super-step)
-    if (live && code == 2) {
-      ++L.cchg;
-      mw_cell_change(W, alpha_sm, s.P, s.bg, n, L);
-      code = 0;
-    }
-    if (live && (code == 1 || code == 3 || L.steps >= cap)) {
-      if (code == 1) {
+    int code = MW_GO, xdir = 0;
+    if (live) code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
+    if (live && code != MW_GO) {
+      if (code == MW_SURFACE) {
         mw_exit(W, n, L, xdir);
         mw_requeue(C, aq_out, L.slot);
-      } else if (code == 3) {
-        // conductor exit: the walk terminates on that conductor
-        // (engine.cpp:333-336 -> run_walk's Terminate branch)
-        // the first declared conductor box holding the voxel across the face
-        int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
-        v[xdir >> 1] += (xdir & 1) ? 1 : -1;
-        const uint64_t cm = voxel_mask(lane_atlas(W, L.slot), L.bm, v) & cond_mask(L.ncond);
-        const int ci = box_cond(W.boxes[static_cast<size_t>(L.slot) * KMAX + __ffsll(cm) - 1]);
-        W.mw[L.slot] += 1;
-        W.mwsteps[L.slot] += L.steps;
-        finish_walk(W, recs, C, L.slot, ci, false);
+      } else if (code == MW_COND) {
+        mw_conductor_exit(W, recs, C, L, xdir);
       } else {
         set_err(C, FRW_ESTEPCAP);
       }
@@ -1293,15 +1328,93 @@ __global__ void __launch_bounds__(512)
       if (live) mw_arm(W, alpha_sm, s.P, queue[item], n, L);
     }
   }
-  unsigned long long g = L.gsteps, cc = L.cchg;
-  for (int o = 16; o > 0; o >>= 1) {
-    g += __shfl_xor_sync(0xFFFFFFFFu, g, o);
-    cc += __shfl_xor_sync(0xFFFFFFFFu, cc, o);
+  flush_mw_stats(C, L);
+}
+
+__device__ __forceinline__ void adv_store(const DSlots& W, const AdvLane& L) {
+  W.p[3 * L.slot] = L.p[0];
+  W.p[3 * L.slot + 1] = L.p[1];
+  W.p[3 * L.slot + 2] = L.p[2];
+  W.rng[L.slot] = L.rng.s;
+  W.hops[L.slot] = L.hops;
+  W.cached[L.slot] = L.cached;
+}
+
+// Run-to-completion kernel for the tail of a run: once few walks remain,
+// rounds would each cost the longest hop chain of the round, so every lane
+// takes an ACTIVE walk and runs it to its end, alternating transitions and
+// MicroWalk super-steps in-thread.  A table miss parks its walk as in
+// k_advance; once any miss is recorded the kernel yields: a walk that has
+// completed a MicroWalk hop in this launch stops at its next transition
+// boundary and goes to the next round's ACTIVE queue, so the host can insert
+// the missing tables without waiting for the longest walk (the host then
+// returns to rounds until a round is miss-free).
+template <int RNG>
+__global__ void __launch_bounds__(256)
+    k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
+           const int* aq, int* aq_out) {
+  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ DirDelta dd[6];
+  setup_smem_tables(s, alpha_sm, dd);
+  const int n = P.n;
+  const int cap = 1000 * n * n;
+  const unsigned long long alen = C->alen;
+  const volatile unsigned long long* nmiss = &C->nmiss;
+  AdvLane A;
+  MwLane L;
+  L.gsteps = 0;
+  L.cchg = 0;
+  bool in_mw = false, hopped = false;
+  unsigned long long item = atomicAdd(&C->ahead, 1ull);
+  bool live = item < alen;
+  if (live) adv_load(W, aq[item], A);
+  while (__any_sync(0xFFFFFFFFu, live)) {
+    if (live && !in_mw) {
+      int r;
+      if (hopped && *nmiss != 0) {  // yield
+        adv_store(W, A);
+        mw_requeue(C, aq_out, A.slot);
+        r = 1;
+      } else {
+        r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
+      }
+      if (r == 2) {
+        in_mw = true;
+        mw_arm(W, alpha_sm, s.P, A.slot, n, L);
+      } else if (r == 1) {
+        item = atomicAdd(&C->ahead, 1ull);
+        live = item < alen;
+        hopped = false;
+        if (live) adv_load(W, aq[item], A);
+      }
+    }
+    // several super-steps per transition: a hop is ~50 super-steps
+#pragma unroll 1
+    for (int rep = 0; rep < 8 && __any_sync(0xFFFFFFFFu, live && in_mw); ++rep) {
+      if (!(live && in_mw)) continue;
+      int xdir = 0;
+      const int code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
+      if (code == MW_GO) continue;
+      in_mw = false;
+      if (code == MW_SURFACE) {
+        mw_exit(W, n, L, xdir);
+        adv_load(W, L.slot, A);
+        hopped = true;
+        continue;
+      }
+      if (code == MW_COND)
+        mw_conductor_exit(W, recs, C, L, xdir);
+      else {
+        set_err(C, FRW_ESTEPCAP);
+        W.state[L.slot] = S_FREE;
+      }
+      item = atomicAdd(&C->ahead, 1ull);
+      live = item < alen;
+      hopped = false;
+      if (live) adv_load(W, aq[item], A);
+    }
   }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&C->gen_steps, g);
-    atomicAdd(&C->cell_chg, cc);
-  }
+  flush_mw_stats(C, L);
 }
 
 // ---- deterministic tallies -------------------------------------------------
@@ -1790,6 +1903,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   cudaEventCreate(&t1);
   cudaEventCreate(&m0);
   cudaEventCreate(&m1);
+  // FRW_TRACE_ROUNDS=1: per-round queue lengths and stage times on stderr
+  const bool trace = std::getenv("FRW_TRACE_ROUNDS") != nullptr;
+  cudaEvent_t a0 = nullptr;
+  if (trace) cudaEventCreate(&a0);
   cudaEventRecord(t0, ctx->stream);
 
   const int S = prm->n_slots > 0 ? prm->n_slots : kSlotsDefault;
@@ -1845,6 +1962,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   const int grid = ctx->sm_count * 8;
   const int adv_grid = ctx->sm_count * 4;  // persistent: 4 x 256 threads per SM
   const int mw_grid = ctx->sm_count * 2;   // persistent: 2 x 512 threads per SM
+  // run-to-completion threshold (active walks); FRW_TAIL_WALKS overrides
+  unsigned long long tail_threshold = static_cast<unsigned long long>(ctx->sm_count) * 512;
+  if (const char* e = std::getenv("FRW_TAIL_WALKS")) tail_threshold = std::strtoull(e, nullptr, 10);
+  bool tail = false;
   float mw_ms = 0;
   uint64_t misses_total = 0, restarts = 0;
   std::vector<int> maxis;
@@ -1855,16 +1976,28 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
            E.sgf.d_data};
     int* aq_in = E.aq[round & 1];
     int* aq_out = E.aq[(round + 1) & 1];
+    if (trace) cudaEventRecord(a0, ctx->stream);
     k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in);
-    k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in,
-                                                 E.queue);
-    cudaEventRecord(m0, ctx->stream);
-    if (P.rng == FRW_RNG_PHILOX)
-      k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs, E.d_cnt, E.queue,
-                                                             aq_out);
-    else
-      k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs, E.d_cnt,
-                                                                      E.queue, aq_out);
+    if (tail) {
+      cudaEventRecord(m0, ctx->stream);
+      const int tb = ctx->sm_count * 2;  // persistent, >= threshold lanes
+      if (P.rng == FRW_RNG_PHILOX)
+        k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M,
+                                                           aq_in, aq_out);
+      else
+        k_tail<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs,
+                                                                    E.d_cnt, M, aq_in, aq_out);
+    } else {
+      k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in,
+                                                   E.queue);
+      cudaEventRecord(m0, ctx->stream);
+      if (P.rng == FRW_RNG_PHILOX)
+        k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs, E.d_cnt,
+                                                               E.queue, aq_out);
+      else
+        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs,
+                                                                        E.d_cnt, E.queue, aq_out);
+    }
     cudaEventRecord(m1, ctx->stream);
     FRW_CUDA(ctx, cudaGetLastError());
     DCounters c;
@@ -1874,6 +2007,14 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       float ms = 0;
       cudaEventElapsedTime(&ms, m0, m1);
       mw_ms += ms;
+      if (trace) {
+        float ams = 0;
+        cudaEventElapsedTime(&ams, a0, m0);
+        std::fprintf(stderr,
+                     "round %d: active %llu mw %llu next-active %llu done %llu misses %llu "
+                     "spawn+advance %.3f ms mw %.3f ms\n",
+                     round, c.alen, c.qlen, c.a2len, c.done, c.nmiss, ams, ms);
+      }
     }
     if (c.err) {
       status = -static_cast<int>(c.err);
@@ -1954,6 +2095,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cnt, &upd, sizeof upd, cudaMemcpyHostToDevice,
                                     ctx->stream));
       restarts += c.nretry;
+      tail = false;  // back to rounds until a round is miss-free
       continue;
     }
     const bool all_spawned = c.next >= static_cast<unsigned long long>(count) &&
@@ -1963,6 +2105,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         status = frw_fail(ctx, FRW_ECUDA, "run_walks: lost walks (internal error)");
       break;
     }
+    // few walks left: run them to completion in one launch
+    if (all_spawned && c.a2len <= tail_threshold) tail = true;
     k_round<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
   }
   if (status == FRW_OK) {
@@ -2044,6 +2188,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   cudaEventDestroy(t1);
   cudaEventDestroy(m0);
   cudaEventDestroy(m1);
+  if (a0) cudaEventDestroy(a0);
   return status;
 }
 
