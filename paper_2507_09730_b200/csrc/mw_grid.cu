@@ -62,26 +62,48 @@ struct Key {
   uint64_t a, b;
   bool operator==(const Key& o) const { return a == o.a && b == o.b; }
 };
-struct KeyHash {
-  size_t operator()(const Key& k) const {
-    return static_cast<size_t>(sm64_mix(k.a ^ sm64_mix(k.b)));
-  }
-};
 
 // smallest x in [0, 2^53] with fl(x * sum) >= acc * 2^53 (2^53 if none);
-// fl(x*sum) is monotone in x, so "x >= X" <=> "not (target < acc)"
+// fl(x*sum) is monotone in x, so "x >= X" <=> "not (target < acc)".  The
+// quotient lands within a few units of X; the two walks settle it exactly.
 uint64_t threshold_of(double acc, double sum) {
   const double target = std::ldexp(acc, 53);
-  uint64_t lo = 0, hi = 1ull << 53;
-  while (lo < hi) {
-    const uint64_t mid = lo + (hi - lo) / 2;
-    if (static_cast<double>(mid) * sum >= target)
-      hi = mid;
-    else
-      lo = mid + 1;
+  constexpr uint64_t kTop = 1ull << 53;
+  const auto ok = [&](uint64_t x) { return static_cast<double>(x) * sum >= target; };
+  const double g = target / sum;
+  uint64_t x = !(g > 0) ? 0 : (g >= static_cast<double>(kTop) ? kTop : static_cast<uint64_t>(g));
+  if (ok(x)) {
+    while (x > 0 && ok(x - 1)) --x;
+  } else {
+    while (x < kTop && !ok(x)) ++x;
   }
-  return lo;
+  return x;
 }
+
+// open-addressing map from a 112-bit stencil key to its record index
+struct KeyTable {
+  std::vector<Key> key;
+  std::vector<uint32_t> val;
+  uint64_t mask;
+  explicit KeyTable(size_t expect) {
+    size_t cap = 1024;
+    while (cap < 2 * expect) cap <<= 1;
+    key.resize(cap);
+    val.assign(cap, 0xFFFFFFFFu);
+    mask = cap - 1;
+  }
+  // index of the key, inserting `next` when absent (returns {index, fresh})
+  std::pair<uint32_t, bool> find_or_insert(const Key& k, uint32_t next) {
+    uint64_t h = sm64_mix(k.a ^ sm64_mix(k.b)) & mask;
+    while (val[h] != 0xFFFFFFFFu) {
+      if (key[h] == k) return {val[h], false};
+      h = (h + 1) & mask;
+    }
+    key[h] = k;
+    val[h] = next;
+    return {next, true};
+  }
+};
 
 struct Compiled {
   std::vector<uint16_t> map;
@@ -95,12 +117,18 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   std::unordered_map<uint64_t, uint32_t> pal_of;
   std::vector<double> pal;
   std::vector<uint32_t> node_pal(nodes);
+  uint64_t last_bits = 0;
+  uint32_t last_idx = 0xFFFFFFFFu;
   for (int v = 0; v < nodes; ++v) {
     const double e = eps[v];
     if (!(e > 0) || !std::isfinite(e))
       return frw_fail(ctx, FRW_EINVAL, "grid permittivities must be finite and > 0");
     uint64_t bits;
     std::memcpy(&bits, &e, 8);
+    if (bits == last_bits && last_idx != 0xFFFFFFFFu) {  // runs of equal permittivity
+      node_pal[v] = last_idx;
+      continue;
+    }
     auto it = pal_of.find(bits);
     if (it == pal_of.end()) {
       if (pal.size() >= 0xFFF0)
@@ -109,9 +137,12 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
       pal.push_back(e);
     }
     node_pal[v] = it->second;
+    last_bits = bits;
+    last_idx = it->second;
   }
   constexpr uint32_t kSurface = 0xFFFF, kCond = 0xFFFE;
-  std::unordered_map<Key, uint32_t, KeyHash> rec_of;
+  KeyTable rec_of(std::min<size_t>(nodes, 1u << 16));
+  uint32_t nrec = 0;
   out.map.resize(nodes);
   for (int k = 0; k < n; ++k)
     for (int j = 0; j < n; ++j)
@@ -134,12 +165,11 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
         Key key{(uint64_t(self) << 48) | (uint64_t(code[0]) << 32) |
                     (uint64_t(code[1]) << 16) | code[2],
                 (uint64_t(code[3]) << 32) | (uint64_t(code[4]) << 16) | code[5]};
-        auto it = rec_of.find(key);
-        if (it == rec_of.end()) {
-          const uint32_t r = static_cast<uint32_t>(rec_of.size());
+        const auto [r, fresh] = rec_of.find_or_insert(key, nrec);
+        if (fresh) {
           if (r > 0xFFFF)
             return frw_fail(ctx, FRW_EINVAL, "more than 65536 distinct stencil records");
-          it = rec_of.emplace(key, r).first;
+          ++nrec;
           // microwalk.cpp:91-109: alphas (1 on absorbing faces) and their
           // in-order partial sums
           double acc[6], sum = 0;
@@ -168,7 +198,7 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
           }
           out.rec.push_back(packed);
         }
-        out.map[v] = static_cast<uint16_t>(it->second);
+        out.map[v] = static_cast<uint16_t>(r);
       }
   return FRW_OK;
 }
@@ -448,7 +478,7 @@ template <int RNG, bool SMEM>
 int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned long long* ms,
            unsigned long long* mq, unsigned long long* mc) {
   const GridTable& G = ctx->grid;
-  DevGrid g{G.d_map, G.d_rec, G.d_full, G.d_mask, G.n, G.n * G.n, G.start_idx,
+  DevGrid g{G.d_map, G.d_rec, G.d_full, G.has_mask ? G.d_mask : nullptr, G.n, G.n * G.n, G.start_idx,
             static_cast<uint32_t>(G.map_bytes), static_cast<uint32_t>(G.rec_bytes),
             1.0f / G.n, 1.0f / (G.n * G.n)};
   DevParams dp{p->seed, sm64_mix(p->seed), p->stream_begin, p->count,
@@ -484,10 +514,6 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   if (int rc = compile_grid(ctx, n, eps, mask, cg)) return rc;
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   GridTable& G = ctx->grid;
-  cudaFree(G.d_map);  // also releases d_rec (same allocation)
-  cudaFree(G.d_full);
-  cudaFree(G.d_mask);
-  G = GridTable{};
   G.n = n;
   G.records = static_cast<int>(cg.rec.size());
   const int c = (n - 1) / 2;  // start_node, sgf.hpp:58-61
@@ -499,25 +525,45 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   G.half_width = half_width;
   G.map_bytes = (cg.map.size() * 2 + 15) / 16 * 16;
   G.rec_bytes = (cg.rec.size() * 8 + 15) / 16 * 16;
-  // one allocation: map then packed records, so one bulk stage covers both
-  char* blob = nullptr;
-  FRW_CUDA(ctx, cudaMalloc(&blob, G.map_bytes + G.rec_bytes));
-  G.d_map = reinterpret_cast<uint16_t*>(blob);
-  G.d_rec = reinterpret_cast<uint64_t*>(blob + G.map_bytes);
+  // one allocation: map then packed records, so one bulk stage covers both;
+  // buffers are kept across uploads and grown only when too small
+  const size_t blob = G.map_bytes + G.rec_bytes, full = cg.full.size() * 8;
+  if (G.blob_cap < blob) {
+    cudaFree(G.d_map);  // also releases d_rec (same allocation)
+    G.d_map = nullptr;
+    G.blob_cap = 0;
+    char* p = nullptr;
+    FRW_CUDA(ctx, cudaMalloc(&p, blob));
+    G.d_map = reinterpret_cast<uint16_t*>(p);
+    G.blob_cap = blob;
+  }
+  G.d_rec = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(G.d_map) + G.map_bytes);
+  if (G.full_cap < full) {
+    cudaFree(G.d_full);
+    G.d_full = nullptr;
+    G.full_cap = 0;
+    FRW_CUDA(ctx, cudaMalloc(&G.d_full, full));
+    G.full_cap = full;
+  }
   FRW_CUDA(ctx, cudaMemcpyAsync(G.d_map, cg.map.data(), cg.map.size() * 2,
                                 cudaMemcpyHostToDevice, ctx->stream));
   FRW_CUDA(ctx, cudaMemcpyAsync(G.d_rec, cg.rec.data(), cg.rec.size() * 8,
                                 cudaMemcpyHostToDevice, ctx->stream));
-  FRW_CUDA(ctx, cudaMalloc(&G.d_full, cg.full.size() * 8));
-  FRW_CUDA(ctx, cudaMemcpyAsync(G.d_full, cg.full.data(), cg.full.size() * 8,
-                                cudaMemcpyHostToDevice, ctx->stream));
-  G.h2d_bytes = cg.map.size() * 2 + cg.rec.size() * 8 + cg.full.size() * 8;
+  FRW_CUDA(ctx, cudaMemcpyAsync(G.d_full, cg.full.data(), full, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  G.h2d_bytes = cg.map.size() * 2 + cg.rec.size() * 8 + full;
+  G.has_mask = mask != nullptr;
   if (mask) {
-    const size_t nodes = static_cast<size_t>(n) * n * n;
-    FRW_CUDA(ctx, cudaMalloc(&G.d_mask, nodes * 4));
-    FRW_CUDA(ctx, cudaMemcpyAsync(G.d_mask, mask, nodes * 4, cudaMemcpyHostToDevice,
-                                  ctx->stream));
-    G.h2d_bytes += nodes * 4;
+    const size_t bytes = static_cast<size_t>(n) * n * n * 4;
+    if (G.mask_cap < bytes) {
+      cudaFree(G.d_mask);
+      G.d_mask = nullptr;
+      G.mask_cap = 0;
+      FRW_CUDA(ctx, cudaMalloc(&G.d_mask, bytes));
+      G.mask_cap = bytes;
+    }
+    FRW_CUDA(ctx, cudaMemcpyAsync(G.d_mask, mask, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    G.h2d_bytes += bytes;
   }
   FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FRW_OK;

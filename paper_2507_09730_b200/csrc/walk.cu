@@ -2012,8 +2012,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         cudaEventElapsedTime(&ams, a0, m0);
         std::fprintf(stderr,
                      "round %d: active %llu mw %llu next-active %llu done %llu misses %llu "
-                     "spawn+advance %.3f ms mw %.3f ms\n",
-                     round, c.alen, c.qlen, c.a2len, c.done, c.nmiss, ams, ms);
+                     "spawn+advance %.3f ms %s %.3f ms\n",
+                     round, c.alen, c.qlen, c.a2len, c.done, c.nmiss, ams, tail ? "tail" : "mw", ms);
       }
     }
     if (c.err) {

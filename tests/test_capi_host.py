@@ -119,3 +119,49 @@ def test_packed_thresholds_are_monotone_prefixes():
 def test_invalid_grid_rejected():
     with pytest.raises(capi.FrwError):
         capi.grid_compile(np.array([1.0, -2.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0]))
+
+
+def _bisect_threshold(acc, s):
+    """the definition: smallest x in [0, 2^53] with fl(x*s) >= acc*2^53"""
+    import math
+    target = math.ldexp(acc, 53)
+    lo, hi = 0, 1 << 53
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if float(mid) * s >= target:
+            hi = mid
+        else:
+            lo = mid + 1
+    return lo
+
+
+@pytest.mark.parametrize("which", ["c2", "rv6"])
+def test_exact_thresholds_match_bisection(which):
+    """frw_grid_compile's X_d (quotient estimate + exact walk) equal the
+    bisection definition for every record, recomputing the alphas from the
+    grid as microwalk.cpp:91-109 does"""
+    eps = c2_grid(1)[0] if which == "c2" else random_voxel_grid(6, 12)
+    n = round(len(eps) ** (1 / 3))
+    mp, rec, full = capi.grid_compile(eps)
+    e3 = eps.reshape(n, n, n)  # [k][j][i]
+    seen = set()
+    for v in range(n ** 3):
+        r = int(mp[v])
+        if r in seen:
+            continue
+        seen.add(r)
+        k, j, i = v // (n * n), (v // n) % n, v % n
+        ev = float(e3[k, j, i])
+        acc, s = [], 0.0
+        for d in range(6):
+            nb = [i, j, k]
+            nb[d >> 1] += 1 if d & 1 else -1
+            if not 0 <= nb[d >> 1] < n:
+                a = 1.0
+            else:
+                en = float(e3[nb[2], nb[1], nb[0]])
+                a = en / (en + ev)
+            s += a
+            acc.append(s)
+        for d in range(5):
+            assert int(full[r, d]) == _bisect_threshold(acc[d], s), (r, d)
