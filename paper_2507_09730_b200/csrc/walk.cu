@@ -1349,8 +1349,12 @@ __device__ __forceinline__ void adv_store(const DSlots& W, const AdvLane& L) {
 // boundary and goes to the next round's ACTIVE queue, so the host can insert
 // the missing tables without waiting for the longest walk (the host then
 // returns to rounds until a round is miss-free).
+#ifndef FRW_TAIL_BLOCKS
+#define FRW_TAIL_BLOCKS 2
+#endif
+constexpr int kTailBlocks = FRW_TAIL_BLOCKS;  // resident 256-thread CTAs per SM
 template <int RNG>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, kTailBlocks)
     k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
            const int* aq, int* aq_out) {
   __shared__ double alpha_sm[PMAX * PMAX];
@@ -1963,7 +1967,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   const int adv_grid = ctx->sm_count * 4;  // persistent: 4 x 256 threads per SM
   const int mw_grid = ctx->sm_count * 2;   // persistent: 2 x 512 threads per SM
   // run-to-completion threshold (active walks); FRW_TAIL_WALKS overrides
-  unsigned long long tail_threshold = static_cast<unsigned long long>(ctx->sm_count) * 512;
+  unsigned long long tail_threshold = static_cast<unsigned long long>(ctx->sm_count) * 2048;
   if (const char* e = std::getenv("FRW_TAIL_WALKS")) tail_threshold = std::strtoull(e, nullptr, 10);
   bool tail = false;
   float mw_ms = 0;
@@ -1980,7 +1984,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in);
     if (tail) {
       cudaEventRecord(m0, ctx->stream);
-      const int tb = ctx->sm_count * 2;  // persistent, >= threshold lanes
+      const int tb = ctx->sm_count * kTailBlocks;  // persistent, one wave
       if (P.rng == FRW_RNG_PHILOX)
         k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M,
                                                            aq_in, aq_out);
