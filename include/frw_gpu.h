@@ -47,7 +47,13 @@ enum {
  * transit/walk bit for bit (rng.hpp:12-40, SplitMix64(seed, stream));
  * PHILOX is the production generator, Philox4x32-10 keyed by seed with
  * counter (transit or walk id, step). */
-enum { FRW_RNG_SPLITMIX_PARITY = 0, FRW_RNG_PHILOX = 1 };
+/* FRW_RNG_SPLITMIX_PARITY: transit/walk t draws from SplitMix64(seed, t)
+ * (rng.hpp:16-17), bit-exact with the reference.  FRW_RNG_PHILOX: Philox4x32-10
+ * keyed by seed, counter (t, step block).  FRW_RNG_SPLITMIX_STATES: transit t
+ * continues a caller-owned SplitMix64 whose raw state is states[t] (the
+ * single-transit API, microwalk.hpp:77-100); the state after the transit is
+ * states[t] + steps * 0x9E3779B97F4A7C15. */
+enum { FRW_RNG_SPLITMIX_PARITY = 0, FRW_RNG_PHILOX = 1, FRW_RNG_SPLITMIX_STATES = 2 };
 
 /* ---- context ------------------------------------------------------------ */
 int frw_ctx_create(int device, frw_ctx **out);
@@ -95,6 +101,7 @@ typedef struct {
   int64_t count;         /* number of transits                             */
   int32_t step_cap;      /* 0: 1000*n^2, like microwalk.cpp:81             */
   int32_t blocks;        /* 0: one persistent CTA per SM                   */
+  const uint64_t *states; /* FRW_RNG_SPLITMIX_STATES: [count] raw states    */
 } frw_mw_params;
 
 /* Outputs.  panels/steps/cond are per transit (may be NULL): panel is the
@@ -110,6 +117,8 @@ typedef struct {
   uint64_t *step_sum;   /* [1] */
   uint64_t *step_sumsq; /* [1] */
   uint64_t *cond_exits; /* [1] */
+  int64_t *exit_nd;     /* per transit: node index * 8 + exit direction
+                           (Exit::voxel / Exit::dir, microwalk.hpp:18-27) */
 } frw_mw_out;
 
 /* Host-pointer batch: runs `count` transits of the uploaded cube
@@ -231,6 +240,28 @@ typedef struct {
 int frw_run_walks(frw_ctx *ctx, const frw_walk_params *p, int32_t master,
                   uint64_t walk_begin, int64_t count, frw_miss_fn miss,
                   void *user, frw_tally *out, frw_walk_record *records);
+
+/* One lattice transit per entry over a cube of the uploaded structure:
+ * microwalk_transit_lazy (microwalk.cpp:199-204; with_conductors = 0) or the
+ * expanded-cube transit of microwalk_e_transit (microwalk.cpp:206-228;
+ * with_conductors = 1, the caller has already applied min(expansion*h, wall)
+ * and transit_cube).  cubes: [count][4] centre xyz, half width (nm); states:
+ * [count] raw SplitMix64 states (advanced by steps * gamma).  kind: 0
+ * surface exit, 1 conductor exit (conductor = declaration index), -1
+ * EngulfedStart (start voxel inside a conductor).  Step-cap overruns fail the
+ * call with FRW_ESTEPCAP.  Host buffers; synchronous. */
+typedef struct {
+  int32_t kind;
+  int32_t panel;
+  int32_t conductor;
+  int32_t dir;
+  int32_t voxel[3];
+  int32_t steps;
+  double point[3];
+} frw_exit;
+int frw_structure_transits(frw_ctx *ctx, int n, int count, const double *cubes,
+                           int with_conductors, const uint64_t *states, int32_t step_cap,
+                           frw_exit *out);
 
 /* Events on the context stream for device timing of _dev launches:
  * elapsed ms between frw_event_record(ctx, 0) and frw_event_record(ctx, 1). */

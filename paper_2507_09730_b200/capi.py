@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libfrwgpu.so")
 
 FRW_OK, FRW_EINVAL, FRW_ECUDA, FRW_ESTEPCAP, FRW_EENGULFED, FRW_ESOLVE = 0, -1, -2, -3, -4, -5
 FRW_ENOMEM, FRW_EMISS = -6, -7
-RNG_SPLITMIX_PARITY, RNG_PHILOX = 0, 1
+RNG_SPLITMIX_PARITY, RNG_PHILOX, RNG_SPLITMIX_STATES = 0, 1, 2
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -41,13 +41,20 @@ class EngulfedStart(FrwError):
 
 class MwParams(C.Structure):
     _fields_ = [("rng_mode", C.c_int), ("seed", C.c_uint64), ("stream_begin", C.c_uint64),
-                ("count", C.c_int64), ("step_cap", C.c_int32), ("blocks", C.c_int32)]
+                ("count", C.c_int64), ("step_cap", C.c_int32), ("blocks", C.c_int32),
+                ("states", C.c_void_p)]
 
 
 class MwOut(C.Structure):
     _fields_ = [("panels", C.c_void_p), ("steps", C.c_void_p), ("cond", C.c_void_p),
                 ("hist", C.c_void_p), ("step_sum", C.c_void_p), ("step_sumsq", C.c_void_p),
-                ("cond_exits", C.c_void_p)]
+                ("cond_exits", C.c_void_p), ("exit_nd", C.c_void_p)]
+
+
+class Exit(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("panel", C.c_int32), ("conductor", C.c_int32),
+                ("dir", C.c_int32), ("voxel", C.c_int32 * 3), ("steps", C.c_int32),
+                ("point", C.c_double * 3)]
 
 
 class StructureDesc(C.Structure):
@@ -125,6 +132,8 @@ def lib():
         L.frw_sgf_clear.argtypes = [C.c_void_p]
         L.frw_sgf_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int), _dp, _dp,
                                     _dp]
+        L.frw_structure_transits.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _up,
+                                             C.c_int32, C.POINTER(Exit)]
         L.frw_run_walks.argtypes = [C.c_void_p, C.POINTER(WalkParams), C.c_int32, C.c_uint64,
                                     C.c_int64, MISS_FN, C.c_void_p, C.POINTER(Tally),
                                     C.c_void_p]
@@ -217,22 +226,28 @@ class Context:
                     h2d_bytes=h2d.value)
 
     def microwalk_batch(self, count, seed=1, stream_begin=0, rng=RNG_PHILOX, step_cap=0,
-                        per_transit=False, blocks=0):
-        """Host-buffer batch (frw_microwalk_batch)."""
+                        per_transit=False, blocks=0, states=None):
+        """Host-buffer batch (frw_microwalk_batch).  `states` (raw SplitMix64
+        states, one per transit) selects RNG_SPLITMIX_STATES."""
         n = self.n
         hist = np.zeros(6 * n * n, np.uint64)
         s1, s2, cx = C.c_uint64(), C.c_uint64(), C.c_uint64()
-        panel = steps = cond = None
+        panel = steps = cond = nd = None
+        if states is not None:
+            states = np.ascontiguousarray(states, np.uint64)
+            count, rng = len(states), RNG_SPLITMIX_STATES
         if per_transit:
             panel = np.empty(count, np.int32)
             steps = np.empty(count, np.int32)
             cond = np.empty(count, np.int32)
-        p = MwParams(rng, seed, stream_begin, count, step_cap, blocks)
+            nd = np.empty(count, np.int64)
+        p = MwParams(rng, seed, stream_begin, count, step_cap, blocks, _p(states))
         o = MwOut(_p(panel), _p(steps), _p(cond), _p(hist), C.cast(C.byref(s1), C.c_void_p),
-                  C.cast(C.byref(s2), C.c_void_p), C.cast(C.byref(cx), C.c_void_p))
+                  C.cast(C.byref(s2), C.c_void_p), C.cast(C.byref(cx), C.c_void_p), _p(nd))
         self._check(self.L.frw_microwalk_batch(self.h, C.byref(p), C.byref(o)))
         return dict(hist=hist, step_sum=s1.value, step_sumsq=s2.value, cond_exits=cx.value,
-                    panel=panel, steps=steps, cond=cond)
+                    panel=panel, steps=steps, cond=cond,
+                    voxel=None if nd is None else nd >> 3, dir=None if nd is None else nd & 7)
 
     # device-resident interface (bench value path) -------------------------
     def alloc(self, nbytes):
@@ -251,8 +266,8 @@ class Context:
 
     def microwalk_batch_dev(self, count, hist_ptr, mom_ptr, seed=1, stream_begin=0,
                             rng=RNG_PHILOX, step_cap=0, blocks=0):
-        p = MwParams(rng, seed, stream_begin, count, step_cap, blocks)
-        o = MwOut(None, None, None, hist_ptr, mom_ptr, mom_ptr + 8, mom_ptr + 16)
+        p = MwParams(rng, seed, stream_begin, count, step_cap, blocks, None)
+        o = MwOut(None, None, None, hist_ptr, mom_ptr, mom_ptr + 8, mom_ptr + 16, None)
         self._check(self.L.frw_microwalk_batch_dev(self.h, C.byref(p), C.byref(o)))
 
     def check(self):
@@ -281,6 +296,21 @@ class Context:
                           float(background_eps), (C.c_double * 6)(*[float(x) for x in world]))
         self._check(self.L.frw_upload_structure(self.h, C.byref(d)))
         self.n_slots_out = len(keep[0]) + 1
+
+    def structure_transits(self, n, cubes, states, with_conductors=False, step_cap=0):
+        """frw_structure_transits: one lazy (or expanded) transit per cube
+        ([count][4] centre, half width) continuing raw SplitMix64 states."""
+        cubes = np.ascontiguousarray(cubes, np.float64).reshape(-1, 4)
+        states = np.ascontiguousarray(states, np.uint64)
+        out = (Exit * len(states))()
+        self._check(self.L.frw_structure_transits(self.h, n, len(states), cubes.ctypes.data_as(_dp),
+                                                  int(with_conductors),
+                                                  states.ctypes.data_as(_up), step_cap, out))
+        a = np.frombuffer(out, dtype=np.dtype([("kind", "<i4"), ("panel", "<i4"),
+                                               ("conductor", "<i4"), ("dir", "<i4"),
+                                               ("voxel", "<i4", 3), ("steps", "<i4"),
+                                               ("point", "<f8", 3)]), count=len(states))
+        return {k: a[k].copy() for k in a.dtype.names}
 
     def sgf_put(self, n, axis, layers, pitch, probs, cdf, kernels=None):
         layers = np.ascontiguousarray(layers, np.float64)

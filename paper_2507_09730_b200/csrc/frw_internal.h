@@ -56,8 +56,8 @@ struct frw_ctx {
   uint64_t* d_hist = nullptr;
   size_t hist_cap = 0;
   uint64_t* d_mom = nullptr;            // [3]
-  int32_t* d_tr = nullptr;              // per-transit outputs (3 arrays)
-  size_t tr_cap = 0;
+  int32_t* d_tr = nullptr;              // per-transit outputs and states
+  size_t tr_cap = 0;                    // bytes
 };
 
 #define FRW_CUDA(ctx, call)                                         \

@@ -123,6 +123,7 @@ void throw_status(frw_ctx* ctx, int rc) {
   switch (rc) {
     case FRW_EINVAL: throw std::invalid_argument(msg);
     case FRW_ESOLVE: throw SolveError(msg, 0.0);
+    case FRW_EENGULFED: throw EngulfedStart(msg);
     default: throw std::runtime_error(msg);
   }
 }
@@ -194,31 +195,7 @@ Engine::Engine(const Structure& s, const Config& cfg, StratifiedSgfCache* cache)
 }
 
 void Engine::upload() {
-  std::vector<int32_t> ids;
-  std::vector<double> cb, db, de;
-  for (const auto& c : s_.conductors) {
-    ids.push_back(c.id);
-    for (int a = 0; a < 3; ++a) cb.push_back(c.box.lo[a]);
-    for (int a = 0; a < 3; ++a) cb.push_back(c.box.hi[a]);
-  }
-  for (const auto& d : s_.dielectrics) {
-    for (int a = 0; a < 3; ++a) db.push_back(d.box.lo[a]);
-    for (int a = 0; a < 3; ++a) db.push_back(d.box.hi[a]);
-    de.push_back(d.eps_r);
-  }
-  frw_structure fs{};
-  fs.n_cond = static_cast<int32_t>(ids.size());
-  fs.cond_id = ids.data();
-  fs.cond_box = cb.data();
-  fs.n_diel = static_cast<int32_t>(de.size());
-  fs.diel_box = db.data();
-  fs.diel_eps = de.data();
-  fs.background_eps = s_.background_eps;
-  for (int a = 0; a < 3; ++a) {
-    fs.world[a] = s_.world.lo[a];
-    fs.world[3 + a] = s_.world.hi[a];
-  }
-  throw_status(ctx_, frw_upload_structure(ctx_, &fs));
+  upload_structure(ctx_, s_);
   // device table: one lattice size; carry over every cached key of this size
   DeviceTable& T = tables()[ctx_];
   if (T.n != cfg_.grid_n) {
@@ -453,33 +430,6 @@ CapacitanceResult extract(const Structure& s, const Config& cfg, int threads,
                           StratifiedSgfCache* cache) {
   Engine e(s, cfg, cache);
   return e.extract(threads);
-}
-
-// ---- single-cube transits ------------------------------------------------------
-
-TransitBatch microwalk_transit_batch(int n, const std::vector<double>& eps, const Vec3& c,
-                                     double half_width, uint64_t seed, uint64_t stream_begin,
-                                     int64_t count, RngMode rng, bool per_transit, int device) {
-  frw_ctx* ctx = Device::get(device).ctx();
-  throw_status(ctx, frw_upload_grid(ctx, n, eps.data(), nullptr, c.x, c.y, c.z, half_width));
-  TransitBatch out;
-  out.hist.assign(6ull * n * n, 0);
-  if (per_transit) {
-    out.panels.resize(count);
-    out.steps.resize(count);
-  }
-  frw_mw_params p{rng == RngMode::Philox ? FRW_RNG_PHILOX : FRW_RNG_SPLITMIX_PARITY, seed,
-                  stream_begin, count, 0, 0};
-  frw_mw_out o{};
-  o.hist = out.hist.data();
-  o.step_sum = &out.step_sum;
-  o.step_sumsq = &out.step_sumsq;
-  if (per_transit) {
-    o.panels = out.panels.data();
-    o.steps = out.steps.data();
-  }
-  throw_status(ctx, frw_microwalk_batch(ctx, &p, &o));
-  return out;
 }
 
 }  // namespace frwcap

@@ -30,6 +30,16 @@ struct Vec3 {
   double x = 0, y = 0, z = 0;
   double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
   double& operator[](int a) { return a == 0 ? x : (a == 1 ? y : z); }
+  Vec3 operator+(const Vec3& o) const { return {x + o.x, y + o.y, z + o.z}; }
+  Vec3 operator-(const Vec3& o) const { return {x - o.x, y - o.y, z - o.z}; }
+  bool operator==(const Vec3& o) const = default;
+};
+
+struct Vec3i {
+  int x = 0, y = 0, z = 0;
+  int operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
+  int& operator[](int a) { return a == 0 ? x : (a == 1 ? y : z); }
+  bool operator==(const Vec3i& o) const = default;
 };
 
 struct Box {
@@ -39,6 +49,12 @@ struct Box {
   double chebyshev_to_wall(const Vec3& p) const;
   bool contains_box(const Box& o) const;
   bool valid() const;
+  // open-interval overlap: touching faces do not count (geometry.hpp:49-52)
+  bool intersects_open(const Box& o) const {
+    return lo.x < o.hi.x && o.lo.x < hi.x && lo.y < o.hi.y && o.lo.y < hi.y && lo.z < o.hi.z &&
+           o.lo.z < hi.z;
+  }
+  Vec3 center() const { return {(lo.x + hi.x) / 2, (lo.y + hi.y) / 2, (lo.z + hi.z) / 2}; }
   Vec3 half_extent() const { return {(hi.x - lo.x) / 2, (hi.y - lo.y) / 2, (hi.z - lo.z) / 2}; }
 };
 
@@ -64,6 +80,12 @@ class ValidationError : public std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// result of the conductor-free cube query (geometry.hpp:93-97)
+struct FreeCube {
+  double half_width = 0;
+  std::optional<int> nearest_id;  // empty when the world wall is nearest
+};
+
 struct Structure {
   std::vector<Conductor> conductors;
   std::vector<Dielectric> dielectrics;
@@ -73,12 +95,103 @@ struct Structure {
 
   double permittivity_at(const Vec3& p) const;
   std::optional<int> conductor_at(const Vec3& p, double tol) const;
+  FreeCube max_free_cube(const Vec3& p) const;
   const Conductor* find_conductor(int id) const;
   void validate() const;
 };
 
 Structure parse_structure(std::string_view text, double world_margin = 5.0);
 Structure parse_structure_file(const std::string& path, double world_margin = 5.0);
+
+// permittivity comparison at relative tolerance 1e-9 (geometry.cpp:17-19)
+bool eps_equal(double a, double b);
+
+// ---- transition-cube voxelisation (geometry.hpp:124-182) --------------------
+enum class GridTag : uint8_t { Uniform, Stratified, General };
+
+struct Cube {
+  Vec3 center;
+  double half_width = 0;
+  Box box() const {
+    return {{center.x - half_width, center.y - half_width, center.z - half_width},
+            {center.x + half_width, center.y + half_width, center.z + half_width}};
+  }
+};
+
+// N^3 permittivity lattice of one cube, x-fastest; conductor_mask (-1 free,
+// else the conductor id) only when built with allow_conductors
+struct DielectricGrid {
+  int n = 0;
+  Cube cube;
+  std::vector<double> eps;
+  std::vector<int32_t> conductor_mask;
+  GridTag tag = GridTag::Uniform;
+  int strat_axis = -1;
+  int index(int i, int j, int k) const { return (k * n + j) * n + i; }
+  double eps_at(int i, int j, int k) const { return eps[index(i, j, k)]; }
+  bool has_mask() const { return !conductor_mask.empty(); }
+  int conductor(int i, int j, int k) const {
+    return has_mask() ? conductor_mask[index(i, j, k)] : -1;
+  }
+  double pitch() const { return 2.0 * cube.half_width / n; }
+  Vec3 voxel_center(int i, int j, int k) const {
+    const double h = cube.half_width, p = pitch();
+    return {cube.center.x - h + (i + 0.5) * p, cube.center.y - h + (j + 0.5) * p,
+            cube.center.z - h + (k + 0.5) * p};
+  }
+};
+void classify_grid(DielectricGrid& g);
+DielectricGrid build_grid(const Structure& s, const Cube& cube, int n,
+                          bool allow_conductors = false);
+
+// ---- lattice and panel algebra (sgf.hpp:24-61, sgf.cpp:13-55) ---------------
+inline constexpr int kDirAxis[6] = {0, 0, 1, 1, 2, 2};
+inline constexpr int kDirSign[6] = {-1, +1, -1, +1, -1, +1};
+inline int surface_panel_index(int n, int face, int u, int v) { return (face * n + v) * n + u; }
+int surface_panel_of(int n, const Vec3i& voxel, int dir);
+std::array<int, 3> decode_surface_panel(int n, int panel);
+Vec3 surface_panel_center(const Cube& cube, int n, int panel);
+std::array<double, 2> surface_panel_offsets(int n, int panel);
+inline Vec3i start_node(int n) {
+  const int c = (n - 1) / 2;
+  return {c, c, c};
+}
+// the walk lattice placed so the point sits on start_node(n)
+// (microwalk.hpp:39-44)
+inline Cube transit_cube(const Vec3& p, double half_width, int n) {
+  if (n % 2 == 1) return {p, half_width};
+  const double delta = half_width / (n + 1);
+  const double h = (half_width - delta) * (1.0 - 1e-12);
+  return {{p.x + delta, p.y + delta, p.z + delta}, h};
+}
+
+// ---- SplitMix64 streams (rng.hpp:12-40) ---------------------------------------
+class SplitMix64 {
+ public:
+  SplitMix64() = default;
+  explicit SplitMix64(uint64_t seed) : state_(mix(seed)) {}
+  SplitMix64(uint64_t seed, uint64_t stream) : state_(mix(mix(seed) + (stream + 1) * kGamma)) {}
+  uint64_t next() {
+    state_ += kGamma;
+    return mix(state_);
+  }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  uint64_t below(uint64_t n) { return next() % n; }
+  static uint64_t mix(uint64_t z) {
+    z += kGamma;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  // B200: the raw state crosses to the device (FRW_RNG_SPLITMIX_STATES)
+  uint64_t state() const { return state_; }
+  void set_state(uint64_t s) { state_ = s; }
+  void skip(uint64_t draws) { state_ += draws * kGamma; }
+  static constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+
+ private:
+  uint64_t state_ = 0;
+};
 
 // ---- SGF (sgf.hpp:116-147) and its cache (sgf_cache.hpp) -------------------
 struct DiscreteSGF {
@@ -256,7 +369,68 @@ class Engine {
 CapacitanceResult extract(const Structure& s, const Config& cfg, int threads = 0,
                           StratifiedSgfCache* cache = nullptr);
 
-// ---- MicroWalk over a materialised cube (microwalk.hpp:77-79, batched) ------
+// ---- MicroWalk transits (microwalk.hpp:18-100) -------------------------------
+struct Exit {
+  enum class Kind : uint8_t { Surface, Conductor };
+  Kind kind = Kind::Surface;
+  int panel = -1;
+  int conductor_id = -1;
+  Vec3 point;
+  Vec3i voxel;
+  int dir = -1;
+  int steps = 0;
+};
+
+class EngulfedStart : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Per-caller state of the reference (memo arrays); here it only selects the
+// device, the transits themselves keep no host-side memo.
+class MicroWalkScratch {
+ public:
+  void prepare(int n_) {
+    n = n_;
+    ++epoch;
+  }
+  int n = 0;
+  bool memoize = true;
+  uint64_t epoch = 0;
+  int device = 0;
+};
+
+// beta_i = alpha_i / sum(alpha) at an interior node (microwalk.cpp:160-186)
+std::array<double, 6> neighbor_weights(const DielectricGrid& grid, const Vec3i& node);
+
+// One transit per call, on the device, continuing the caller's SplitMix64
+// (bit-identical to the reference for the same stream).  Batched forms
+// below run many transits per launch.
+Exit microwalk_transit(const DielectricGrid& grid, SplitMix64& rng, MicroWalkScratch& scratch,
+                       int step_cap = 0);
+Exit microwalk_transit(const DielectricGrid& grid, SplitMix64& rng);
+Exit microwalk_e_transit(const Structure& s, const Vec3& center, double base_half_width,
+                         double expansion, int n, SplitMix64& rng, MicroWalkScratch& scratch,
+                         int step_cap = 0);
+Exit microwalk_e_transit(const Structure& s, const Vec3& center, double base_half_width,
+                         double expansion, int n, SplitMix64& rng);
+Exit microwalk_transit_lazy(const Structure& s, const Cube& cube, int n, SplitMix64& rng,
+                            MicroWalkScratch& scratch, int step_cap = 0);
+
+// B200 batched forms: transit t continues rngs[t] (advanced in place).
+std::vector<Exit> microwalk_transits(const DielectricGrid& grid, std::vector<SplitMix64>& rngs,
+                                     int step_cap = 0, int device = 0);
+// lazy (with_conductors = false, cubes as given) or expanded (true; cubes
+// already min(expansion*h, wall)-sized and transit_cube-placed); a start
+// voxel inside a conductor yields kind Conductor with conductor_id -1 and
+// steps 0 (EngulfedStart in the single-transit form)
+std::vector<Exit> microwalk_structure_transits(const Structure& s, const std::vector<Cube>& cubes,
+                                               int n, bool with_conductors,
+                                               std::vector<SplitMix64>& rngs, int step_cap = 0,
+                                               int device = 0);
+
+// uploads `s` to the context unless it is the structure uploaded last
+void upload_structure(frw_ctx* ctx, const Structure& s);
+
 struct TransitBatch {
   std::vector<uint64_t> hist;
   std::vector<int32_t> panels, steps;

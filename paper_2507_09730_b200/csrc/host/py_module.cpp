@@ -57,6 +57,40 @@ Config config_from_kwargs(const py::kwargs& kw, int& threads) {
   return cfg;
 }
 
+
+// per-transit Exit fields as numpy arrays; kind -1 marks EngulfedStart
+py::dict exits_dict(const std::vector<Exit>& ex, const std::vector<SplitMix64>& rngs) {
+  const size_t cnt = ex.size();
+  py::array_t<int32_t> kind(cnt), panel(cnt), cond(cnt), dir(cnt), steps(cnt);
+  py::array_t<int32_t> voxel({cnt, static_cast<size_t>(3)});
+  py::array_t<double> point({cnt, static_cast<size_t>(3)});
+  py::array_t<uint64_t> state(cnt);
+  for (size_t t = 0; t < cnt; ++t) {
+    const Exit& e = ex[t];
+    const bool engulfed = e.kind == Exit::Kind::Conductor && e.conductor_id < 0;
+    kind.mutable_at(t) = engulfed ? -1 : (e.kind == Exit::Kind::Surface ? 0 : 1);
+    panel.mutable_at(t) = e.panel;
+    cond.mutable_at(t) = e.conductor_id;
+    dir.mutable_at(t) = e.dir;
+    steps.mutable_at(t) = e.steps;
+    for (int a = 0; a < 3; ++a) {
+      voxel.mutable_at(t, a) = e.voxel[a];
+      point.mutable_at(t, a) = e.point[a];
+    }
+    state.mutable_at(t) = rngs[t].state();
+  }
+  py::dict d;
+  d["kind"] = kind;
+  d["panel"] = panel;
+  d["cond"] = cond;
+  d["dir"] = dir;
+  d["steps"] = steps;
+  d["voxel"] = voxel;
+  d["point"] = point;
+  d["state"] = state;
+  return d;
+}
+
 // py_module.cpp:59-98
 py::dict result_to_dict(const CapacitanceResult& r) {
   py::list terms;
@@ -293,6 +327,115 @@ PYBIND11_MODULE(_core, m) {
       },
       py::arg("structure_json"), py::arg("begin"), py::arg("count"),
       "Per-walk outcomes of walks [begin, begin+count) (parity tests).");
+
+
+  // single-transit API (microwalk.hpp:70-100) -- test and integration hooks
+  m.def(
+      "transits_grid",
+      [](py::array_t<double, py::array::c_style | py::array::forcecast> eps,
+         std::vector<double> center, double half_width,
+         py::array_t<uint64_t, py::array::c_style | py::array::forcecast> states, py::object mask,
+         bool single, int step_cap) {
+        DielectricGrid g;
+        g.n = static_cast<int>(std::lround(std::cbrt(static_cast<double>(eps.size()))));
+        g.cube = {{center.at(0), center.at(1), center.at(2)}, half_width};
+        g.eps.assign(eps.data(), eps.data() + eps.size());
+        if (!mask.is_none()) {
+          auto mk = py::cast<py::array_t<int32_t, py::array::c_style | py::array::forcecast>>(mask);
+          g.conductor_mask.assign(mk.data(), mk.data() + mk.size());
+        }
+        std::vector<SplitMix64> rngs(states.size());
+        for (size_t t = 0; t < rngs.size(); ++t) rngs[t].set_state(states.data()[t]);
+        std::vector<Exit> ex;
+        {
+          py::gil_scoped_release release;
+          if (single) {
+            MicroWalkScratch scr;
+            for (auto& r : rngs) ex.push_back(microwalk_transit(g, r, scr, step_cap));
+          } else {
+            ex = microwalk_transits(g, rngs, step_cap);
+          }
+        }
+        return exits_dict(ex, rngs);
+      },
+      py::arg("eps"), py::arg("center"), py::arg("half_width"), py::arg("states"),
+      py::arg("mask") = py::none(), py::arg("single") = false, py::arg("step_cap") = 0);
+
+  m.def(
+      "transits_structure",
+      [](const std::string& text, py::array_t<double, py::array::c_style | py::array::forcecast> cubes,
+         int n, bool expanded, double expansion,
+         py::array_t<uint64_t, py::array::c_style | py::array::forcecast> states, bool single,
+         int step_cap) {
+        const Structure s = parse_structure(text);
+        const size_t cnt = states.size();
+        if (cubes.size() != 4 * cnt) throw py::value_error("cubes must be [count][4]");
+        std::vector<SplitMix64> rngs(cnt);
+        for (size_t t = 0; t < cnt; ++t) rngs[t].set_state(states.data()[t]);
+        std::vector<Exit> ex(cnt);
+        const double* c = cubes.data();
+        {
+          py::gil_scoped_release release;
+          if (single) {
+            // expanded: cubes hold (point, base half width) as for microwalk_e_transit
+            MicroWalkScratch scr;
+            for (size_t t = 0; t < cnt; ++t) {
+              const Vec3 p{c[4 * t], c[4 * t + 1], c[4 * t + 2]};
+              try {
+                ex[t] = expanded ? microwalk_e_transit(s, p, c[4 * t + 3], expansion, n, rngs[t],
+                                                       scr, step_cap)
+                                 : microwalk_transit_lazy(s, {p, c[4 * t + 3]}, n, rngs[t], scr,
+                                                          step_cap);
+              } catch (const EngulfedStart&) {
+                ex[t].kind = Exit::Kind::Conductor;
+                ex[t].conductor_id = -1;
+                ex[t].steps = 0;
+              }
+            }
+          } else {
+            std::vector<Cube> cb(cnt);
+            for (size_t t = 0; t < cnt; ++t)
+              cb[t] = {{c[4 * t], c[4 * t + 1], c[4 * t + 2]}, c[4 * t + 3]};
+            ex = microwalk_structure_transits(s, cb, n, expanded, rngs, step_cap);
+          }
+        }
+        return exits_dict(ex, rngs);
+      },
+      py::arg("structure_json"), py::arg("cubes"), py::arg("n"), py::arg("expanded"),
+      py::arg("expansion") = 5.0, py::arg("states"), py::arg("single") = false,
+      py::arg("step_cap") = 0);
+
+  m.def(
+      "neighbor_weights",
+      [](py::array_t<double, py::array::c_style | py::array::forcecast> eps,
+         std::vector<int> node) {
+        DielectricGrid g;
+        g.n = static_cast<int>(std::lround(std::cbrt(static_cast<double>(eps.size()))));
+        g.cube = {{0, 0, 0}, g.n / 2.0};
+        g.eps.assign(eps.data(), eps.data() + eps.size());
+        return neighbor_weights(g, {node.at(0), node.at(1), node.at(2)});
+      },
+      py::arg("eps"), py::arg("node"));
+
+  m.def(
+      "build_grid",
+      [](const std::string& text, std::vector<double> center, double hw, int n,
+         bool allow_conductors) {
+        const Structure s = parse_structure(text);
+        const DielectricGrid g = build_grid(s, {{center.at(0), center.at(1), center.at(2)}, hw},
+                                            n, allow_conductors);
+        py::array_t<double> eps(g.eps.size());
+        std::copy(g.eps.begin(), g.eps.end(), eps.mutable_data());
+        py::object mask = py::none();
+        if (g.has_mask()) {
+          py::array_t<int32_t> mk(g.conductor_mask.size());
+          std::copy(g.conductor_mask.begin(), g.conductor_mask.end(), mk.mutable_data());
+          mask = mk;
+        }
+        return py::make_tuple(eps, mask, static_cast<int>(g.tag), g.strat_axis);
+      },
+      py::arg("structure_json"), py::arg("center"), py::arg("half_width"), py::arg("n"),
+      py::arg("allow_conductors") = false);
 
   m.def("sgf_cache_save", [](const std::string& path) { shared_cache().save(path); });
   m.def("sgf_cache_load", [](const std::string& path) { return shared_cache().load(path); });

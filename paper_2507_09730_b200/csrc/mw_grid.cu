@@ -225,6 +225,7 @@ struct DevParams {
   uint64_t stream_begin;
   long long count;
   int step_cap;
+  const uint64_t* states;  // FRW_RNG_SPLITMIX_STATES
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -300,8 +301,10 @@ template <int RNG, bool SMEM>
 __global__ void __launch_bounds__(kThreads, 1)
     mw_grid_kernel(DevGrid g, DevParams p, unsigned long long* ctr, int* err,
                    int32_t* out_panel, int32_t* out_steps, int32_t* out_cond,
-                   unsigned long long* hist, unsigned long long* m_sum,
+                   long long* out_nd, unsigned long long* hist, unsigned long long* m_sum,
                    unsigned long long* m_sq, unsigned long long* m_cx) {
+  // SplitMix64 draws (parity streams or caller states) vs Philox words
+  constexpr bool SM = RNG != FRW_RNG_PHILOX;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ int stride[6];
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t blk = 0;  // philox: 4-step block index within the transit
   if (RNG == FRW_RNG_SPLITMIX_PARITY && live)
     sm = sm64_stream_from_mixed(p.mixed_seed, p.stream_begin + t);
+  if (RNG == FRW_RNG_SPLITMIX_STATES && live) sm = p.states[t];
   const uint32_t k0 = static_cast<uint32_t>(p.seed);
   const uint32_t k1 = static_cast<uint32_t>(p.seed >> 32);
 
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // gives two steps their top 16 bits of x; the low 37 bits are drawn from
   // the (id, step slot, 1) counter only when the 16-bit prefix ties a
   // threshold, so x is still an exact 53-bit uniform.  Parity: 4 steps.
-  constexpr int SS = RNG == FRW_RNG_PHILOX ? 8 : 4;
+  constexpr int SS = SM ? 4 : 8;
   while (__any_sync(0xFFFFFFFFu, live)) {
     // ---- one phase-aligned super-step of SS lattice steps ----------------
     uint32_t w[4];
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool act = live && !exited;
       uint64_t z = 0;
       uint32_t x10, h16 = 0;
-      if (RNG == FRW_RNG_SPLITMIX_PARITY) {
+      if (SM) {
         const uint64_t s1 = sm + kGamma;  // SplitMix64::next (rng.hpp:19-22)
         z = sm64_mix(s1);
         sm = act ? s1 : sm;
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (__builtin_expect(__any_sync(0xFFFFFFFFu, act && tie), 0) && act && tie) {
         // 10-bit tie: exact comparison against the 53-bit thresholds
         const uint64_t* f = g.full + 5 * r;
-        if (RNG == FRW_RNG_SPLITMIX_PARITY) {
+        if (SM) {
           const uint64_t x53 = z >> 11;
           dir = 0;
 #pragma unroll
@@ -446,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (out_panel) out_panel[t] = panel;
       if (out_steps) out_steps[t] = steps;
       if (out_cond) out_cond[t] = cid;
+      if (out_nd) out_nd[t] = (exited && steps <= cap) ? 8ll * idx + xdir : -1ll;
       ssum += steps;
       ssq += static_cast<unsigned long long>(steps) * steps;
       // re-arm with the prefetched transit, prefetch the following one
@@ -458,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         blk = 0;
         if (RNG == FRW_RNG_SPLITMIX_PARITY)
           sm = sm64_stream_from_mixed(p.mixed_seed, p.stream_begin + t);
+        if (RNG == FRW_RNG_SPLITMIX_STATES) sm = p.states[t];
       }
     }
   }
@@ -482,7 +488,7 @@ int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned l
             static_cast<uint32_t>(G.map_bytes), static_cast<uint32_t>(G.rec_bytes),
             1.0f / G.n, 1.0f / (G.n * G.n)};
   DevParams dp{p->seed, sm64_mix(p->seed), p->stream_begin, p->count,
-               p->step_cap > 0 ? p->step_cap : 1000 * G.n * G.n};
+               p->step_cap > 0 ? p->step_cap : 1000 * G.n * G.n, p->states};
   const size_t smem = SMEM ? G.map_bytes + G.rec_bytes : 0;
   auto kern = mw_grid_kernel<RNG, SMEM>;
   if (SMEM)
@@ -492,7 +498,8 @@ int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned l
   const int blocks = p->blocks > 0 ? p->blocks : ctx->sm_count;
   kern<<<blocks, kThreads, smem, ctx->stream>>>(
       g, dp, ctx->d_ctr, ctx->d_err, o->panels, o->steps, o->cond,
-      reinterpret_cast<unsigned long long*>(o->hist), ms, mq, mc);
+      reinterpret_cast<long long*>(o->exit_nd), reinterpret_cast<unsigned long long*>(o->hist),
+      ms, mq, mc);
   FRW_CUDA(ctx, cudaGetLastError());
   return FRW_OK;
 }
@@ -606,8 +613,11 @@ int frw_microwalk_batch_dev(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_o
   if (p->count < 0) return frw_fail(ctx, FRW_EINVAL, "microwalk_batch: count < 0");
   if (G.start_is_conductor)
     return frw_fail(ctx, FRW_EENGULFED, "transit start voxel lies inside a conductor");
-  if (p->rng_mode != FRW_RNG_SPLITMIX_PARITY && p->rng_mode != FRW_RNG_PHILOX)
+  if (p->rng_mode != FRW_RNG_SPLITMIX_PARITY && p->rng_mode != FRW_RNG_PHILOX &&
+      p->rng_mode != FRW_RNG_SPLITMIX_STATES)
     return frw_fail(ctx, FRW_EINVAL, "microwalk_batch: unknown rng mode");
+  if (p->rng_mode == FRW_RNG_SPLITMIX_STATES && !p->states)
+    return frw_fail(ctx, FRW_EINVAL, "microwalk_batch: states required");
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   if (p->count == 0) return FRW_OK;
   auto* ms = reinterpret_cast<unsigned long long*>(o->step_sum ? o->step_sum : ctx->d_mom);
@@ -617,6 +627,9 @@ int frw_microwalk_batch_dev(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_o
   if (p->rng_mode == FRW_RNG_SPLITMIX_PARITY)
     return smem ? launch<FRW_RNG_SPLITMIX_PARITY, true>(ctx, p, o, ms, mq, mc)
                 : launch<FRW_RNG_SPLITMIX_PARITY, false>(ctx, p, o, ms, mq, mc);
+  if (p->rng_mode == FRW_RNG_SPLITMIX_STATES)
+    return smem ? launch<FRW_RNG_SPLITMIX_STATES, true>(ctx, p, o, ms, mq, mc)
+                : launch<FRW_RNG_SPLITMIX_STATES, false>(ctx, p, o, ms, mq, mc);
   return smem ? launch<FRW_RNG_PHILOX, true>(ctx, p, o, ms, mq, mc)
               : launch<FRW_RNG_PHILOX, false>(ctx, p, o, ms, mq, mc);
 }
@@ -644,12 +657,20 @@ int frw_microwalk_batch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* 
     FRW_CUDA(ctx, cudaMalloc(&ctx->d_hist, bins * 8));
     ctx->hist_cap = bins;
   }
-  const bool per = host->panels || host->steps || host->cond;
-  if (per && ctx->tr_cap < static_cast<size_t>(p->count)) {
+  // per-transit scratch: panels | steps | cond (int32) | exit_nd (int64) |
+  // states (u64)
+  const size_t cnt = static_cast<size_t>(std::max<int64_t>(p->count, 0));
+  const bool states = p->rng_mode == FRW_RNG_SPLITMIX_STATES;
+  const bool per = host->panels || host->steps || host->cond || host->exit_nd || states;
+  const size_t off_nd = (12 * cnt + 7) / 8 * 8, off_st = off_nd + 8 * cnt, need = off_st + 8 * cnt;
+  if (per && ctx->tr_cap < need) {
     cudaFree(ctx->d_tr);
-    FRW_CUDA(ctx, cudaMalloc(&ctx->d_tr, static_cast<size_t>(p->count) * 12));
-    ctx->tr_cap = p->count;
+    ctx->d_tr = nullptr;
+    ctx->tr_cap = 0;
+    FRW_CUDA(ctx, cudaMalloc(&ctx->d_tr, need));
+    ctx->tr_cap = need;
   }
+  char* tr = reinterpret_cast<char*>(ctx->d_tr);
   FRW_CUDA(ctx, cudaMemsetAsync(ctx->d_hist, 0, bins * 8, ctx->stream));
   FRW_CUDA(ctx, cudaMemsetAsync(ctx->d_mom, 0, 32, ctx->stream));
   FRW_CUDA(ctx, cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
@@ -658,16 +679,23 @@ int frw_microwalk_batch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* 
   d.step_sum = ctx->d_mom;
   d.step_sumsq = ctx->d_mom + 1;
   d.cond_exits = ctx->d_mom + 2;
-  if (host->panels) d.panels = ctx->d_tr;
-  if (host->steps) d.steps = ctx->d_tr + p->count;
-  if (host->cond) d.cond = ctx->d_tr + 2 * p->count;
-  if (int rc = frw_microwalk_batch_dev(ctx, p, &d)) return rc;
+  if (host->panels) d.panels = reinterpret_cast<int32_t*>(tr);
+  if (host->steps) d.steps = reinterpret_cast<int32_t*>(tr) + cnt;
+  if (host->cond) d.cond = reinterpret_cast<int32_t*>(tr) + 2 * cnt;
+  if (host->exit_nd) d.exit_nd = reinterpret_cast<int64_t*>(tr + off_nd);
+  frw_mw_params pd = *p;
+  if (states) {
+    if (!p->states) return frw_fail(ctx, FRW_EINVAL, "microwalk_batch: states required");
+    FRW_CUDA(ctx, cudaMemcpyAsync(tr + off_st, p->states, 8 * cnt, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+    pd.states = reinterpret_cast<const uint64_t*>(tr + off_st);
+  }
+  if (int rc = frw_microwalk_batch_dev(ctx, &pd, &d)) return rc;
   if (host->hist)
     FRW_CUDA(ctx, cudaMemcpyAsync(host->hist, ctx->d_hist, bins * 8, cudaMemcpyDeviceToHost,
                                   ctx->stream));
   uint64_t mom[4];
   FRW_CUDA(ctx, cudaMemcpyAsync(mom, ctx->d_mom, 32, cudaMemcpyDeviceToHost, ctx->stream));
-  const size_t cnt = static_cast<size_t>(p->count);
   if (host->panels)
     FRW_CUDA(ctx, cudaMemcpyAsync(host->panels, d.panels, cnt * 4, cudaMemcpyDeviceToHost,
                                   ctx->stream));
@@ -676,6 +704,9 @@ int frw_microwalk_batch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* 
                                   ctx->stream));
   if (host->cond)
     FRW_CUDA(ctx, cudaMemcpyAsync(host->cond, d.cond, cnt * 4, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+  if (host->exit_nd)
+    FRW_CUDA(ctx, cudaMemcpyAsync(host->exit_nd, d.exit_nd, cnt * 8, cudaMemcpyDeviceToHost,
                                   ctx->stream));
   FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   if (host->step_sum) *host->step_sum = mom[0];

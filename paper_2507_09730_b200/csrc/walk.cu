@@ -61,10 +61,6 @@ constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
 
 
-// SWAR step record layout shared with mw_grid.cu
-constexpr uint64_t kOnes = 0x0000100200400801ull;
-constexpr uint64_t kGuard = kOnes << 10;
-
 enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2 };
 
 // ---------------------------------------------------------------------------
@@ -98,8 +94,6 @@ struct DParams {
   long long hop_cap;
   uint64_t seed, mixed_seed;
   double gbox[6], fcdf[6], area;
-  uint64_t urec;      // packed SWAR record of the uniform (alpha=1/2) cell
-  uint64_t ufull[5];  // its exact 53-bit thresholds
   uint64_t walk_begin;
   long long count;
   int master;
@@ -1421,6 +1415,79 @@ __global__ void __launch_bounds__(256, kTailBlocks)
   flush_mw_stats(C, L);
 }
 
+// ---- single transits over structure cubes (the single-transit API) --------
+// microwalk_transit_lazy / microwalk_e_transit (microwalk.cpp:199-228): one
+// thread per transit compiles the cube into slot t and walks it with the
+// caller's SplitMix64 state (the lane machinery of k_mw in parity mode).
+struct DevExit {
+  int32_t kind, panel, conductor, dir;
+  int32_t voxel[3];
+  int32_t steps;
+  double point[3];
+};
+static_assert(sizeof(DevExit) == sizeof(frw_exit), "exit layout");
+
+__global__ void __launch_bounds__(128)
+    k_transits(DStruct s, DParams P, DSlots W, DCounters* C, const double* cubes,
+               const uint64_t* states, int count, int with_cond, int cap, DevExit* out) {
+  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ DirDelta dd[6];
+  setup_smem_tables(s, alpha_sm, dd);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int n = P.n;
+  const double c[3] = {cubes[4 * t], cubes[4 * t + 1], cubes[4 * t + 2]};
+  const double h = cubes[4 * t + 3];
+  DevExit e{};
+  e.conductor = -1;
+  e.panel = -1;
+  const int rc = compile_mw_job(s, W, t, c, h, n, with_cond != 0, C);
+  if (rc <= 0) {
+    e.kind = rc == 0 ? -1 : -2;  // EngulfedStart / too many boxes (error set)
+    out[t] = e;
+    return;
+  }
+  W.wid[t] = t;
+  W.rng[t] = states[t];
+  W.mw[t] = 0;
+  W.mwsteps[t] = 0;
+  MwLane L;
+  L.gsteps = 0;
+  L.cchg = 0;
+  mw_arm(W, alpha_sm, s.P, t, n, L);
+  int code = MW_GO, xdir = 0;
+  while (code == MW_GO) code = mw_superstep<FRW_RNG_SPLITMIX_PARITY>(P, W, alpha_sm, s.P, s.bg,
+                                                                     dd, n, cap, L, &xdir);
+  const int a = xdir >> 1;
+  e.kind = code == MW_SURFACE ? 0 : 1;
+  e.dir = xdir;
+  e.steps = L.steps;
+  e.voxel[0] = coord(L.node, 0);
+  e.voxel[1] = coord(L.node, 1);
+  e.voxel[2] = coord(L.node, 2);
+  if (code == MW_SURFACE) {
+    const int u = a == 0 ? e.voxel[1] : e.voxel[0];
+    const int v = a == 2 ? e.voxel[1] : e.voxel[2];
+    e.panel = (xdir * n + v) * n + u;  // surface_panel_of (sgf.cpp:13-30)
+    panel_center(c, h, n, e.panel, e.point);
+  } else if (code == MW_COND) {
+    int v[3] = {e.voxel[0], e.voxel[1], e.voxel[2]};
+    v[a] += (xdir & 1) ? 1 : -1;
+    const uint64_t cm = voxel_mask(lane_atlas(W, t), L.bm, v) & cond_mask(L.ncond);
+    e.conductor = box_cond(W.boxes[static_cast<size_t>(t) * KMAX + __ffsll(cm) - 1]);
+    // lattice_voxel_center + half a pitch towards the conductor
+    // (microwalk.cpp:24-30, :141-143)
+    const double pitch = 2.0 * h / n;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) e.point[q] = vcenter(c[q], h, pitch, e.voxel[q]);
+    e.point[a] += ((xdir & 1) ? 1 : -1) * h / n;
+  } else {
+    e.kind = -3;
+    set_err(C, FRW_ESTEPCAP);
+  }
+  out[t] = e;
+}
+
 // ---- deterministic tallies -------------------------------------------------
 constexpr int kChunk = 1024;
 
@@ -1492,20 +1559,6 @@ __global__ void k_reduce_final(int nblocks, int nslots, const double* psum, cons
 
 // ---------------------------------------------------------------------------
 // host side
-
-// smallest x in [0, 2^53] with fl(x * sum) >= acc * 2^53 (see mw_grid.cu)
-uint64_t threshold_of(double acc, double sum) {
-  const double target = std::ldexp(acc, 53);
-  uint64_t lo = 0, hi = 1ull << 53;
-  while (lo < hi) {
-    const uint64_t mid = lo + (hi - lo) / 2;
-    if (static_cast<double>(mid) * sum >= target)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  return lo;
-}
 
 double host_round_sig(double x, int digits) {  // sgf_cache.cpp:13-18
   if (x == 0 || !std::isfinite(x)) return x;
@@ -1882,6 +1935,78 @@ int frw_sgf_clear(frw_ctx* ctx) {
 
 static_assert(sizeof(WalkRec) == sizeof(frw_walk_record), "record layout");
 
+int frw_structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
+                           int with_conductors, const uint64_t* states, int32_t step_cap,
+                           frw_exit* out) {
+  if (!ctx) return FRW_EINVAL;
+  Engine& E = *engine_of(ctx);
+  if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "transits: no structure uploaded");
+  if (n < 1 || n > NMAX) return frw_fail(ctx, FRW_EINVAL, "transits: n must lie in [1, 64]");
+  if (count < 0 || (count > 0 && (!cubes || !states || !out)))
+    return frw_fail(ctx, FRW_EINVAL, "transits: bad arguments");
+  if (count == 0) return FRW_OK;
+  for (int t = 0; t < count; ++t)
+    if (!(cubes[4 * t + 3] > 0))
+      return frw_fail(ctx, FRW_EINVAL, "transits: cube half width must be > 0");
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  if (E.S < count)
+    if (int rc = ensure_slots(ctx, E, count)) return rc;
+  if (!E.d_cnt) {
+    E.d_cnt = dalloc<DCounters>(1);
+    E.M.axis = dalloc<int>(kMissMax);
+    E.M.layers = dalloc<double>(size_t(kMissMax) * NMAX);
+  }
+  double* d_cubes = dalloc<double>(4 * size_t(count));
+  uint64_t* d_states = dalloc<uint64_t>(count);
+  DevExit* d_out = dalloc<DevExit>(count);
+  auto release = [&] {
+    cudaFree(d_cubes);
+    cudaFree(d_states);
+    cudaFree(d_out);
+  };
+  if (!d_cubes || !d_states || !d_out) {
+    release();
+    return frw_fail(ctx, FRW_ENOMEM, "transits: device allocation failed");
+  }
+  DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal, {}};
+  std::memcpy(s.world, E.world, sizeof s.world);
+  DParams P{};
+  P.n = n;
+  P.panels = 6 * n * n;
+  P.rng = FRW_RNG_SPLITMIX_PARITY;
+  const int cap = step_cap > 0 ? step_cap : 1000 * n * n;  // microwalk.cpp:81
+  int status = FRW_OK;
+  do {
+    if (cudaMemcpyAsync(d_cubes, cubes, 32 * size_t(count), cudaMemcpyHostToDevice,
+                        ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(d_states, states, 8 * size_t(count), cudaMemcpyHostToDevice,
+                        ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), ctx->stream) != cudaSuccess) {
+      status = frw_fail(ctx, FRW_ECUDA, "transits: copy failed");
+      break;
+    }
+    k_transits<<<(count + 127) / 128, 128, 0, ctx->stream>>>(
+        s, P, E.W, E.d_cnt, d_cubes, d_states, count, with_conductors, cap, d_out);
+    DCounters c;
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(out, d_out, sizeof(DevExit) * count, cudaMemcpyDeviceToHost,
+                        ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(&c, E.d_cnt, sizeof c, cudaMemcpyDeviceToHost, ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+      status = frw_fail(ctx, FRW_ECUDA, "transits: kernel failed");
+      break;
+    }
+    if (c.err == static_cast<unsigned long long>(-FRW_ESTEPCAP))
+      status = frw_fail(ctx, FRW_ESTEPCAP,
+                        "microwalk transit exceeded the step cap; the lattice is malformed");
+    else if (c.err)
+      status = frw_fail(ctx, FRW_EINVAL, "transits: more than 64 boxes reach into one cube");
+  } while (false);
+  release();
+  return status;
+}
+
 int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint64_t walk_begin,
                   int64_t count, frw_miss_fn miss, void* user, frw_tally* out,
                   frw_walk_record* records) {
@@ -1943,18 +2068,6 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   std::memcpy(P.gbox, prm->gauss_box, sizeof P.gbox);
   std::memcpy(P.fcdf, prm->face_cdf, sizeof P.fcdf);
   P.area = prm->area_m2;
-  {
-    // uniform interior record: alpha = 1/2 in all six directions
-    double acc = 0;
-    uint64_t rec = 0;
-    for (int d = 0; d < 5; ++d) {
-      acc += 0.5;
-      const uint64_t X = threshold_of(acc, 3.0);
-      P.ufull[d] = X;
-      rec |= (1023 - std::min<uint64_t>(X >> 43, 1023)) << (11 * d);
-    }
-    P.urec = rec;
-  }
   P.walk_begin = walk_begin;
   P.count = count;
   P.master = master;
