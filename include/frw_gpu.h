@@ -263,6 +263,35 @@ int frw_structure_transits(frw_ctx *ctx, int n, int count, const double *cubes,
                            int with_conductors, const uint64_t *states, int32_t step_cap,
                            frw_exit *out);
 
+/* Engine::first_transition / Engine::transition (engine.hpp:146-159;
+ * engine.cpp:201-350), one per entry, continuing caller-owned SplitMix64
+ * states (states[] in/out).  prm selects grid_n, mode, expansion, snap and
+ * the Gaussian area/surface as for frw_run_walks (rng_mode and n_slots are
+ * ignored).  Table misses are solved on the device (or through `miss`) and
+ * the entry re-run, so no entry reports a miss.  Host buffers. */
+typedef struct {
+  int32_t ok;      /* 1 transition, 0 degenerate free cube (redraw)          */
+  int32_t branch;  /* ladder branch 0..3 (DispatchStats order)               */
+  double weight;   /* farads                                                 */
+  double point[3];
+} frw_first;
+int frw_first_transitions(frw_ctx *ctx, const frw_walk_params *prm, int count,
+                          const double *gpoints, const int32_t *axis_sign,
+                          uint64_t *states, frw_miss_fn miss, void *user,
+                          frw_first *out);
+
+typedef struct {
+  int32_t kind;      /* 0 continue, 1 terminate on a conductor, 2 ground    */
+  int32_t conductor; /* declaration index (kind 1)                          */
+  int32_t dispatch;  /* -1 snapped, 0 cached, 1 microwalk, 2 microwalk_e    */
+  int32_t pad;
+  double point[3];   /* continue: next point                                */
+  uint64_t mw_steps; /* lattice steps of a MicroWalk transition             */
+} frw_event;
+int frw_transitions(frw_ctx *ctx, const frw_walk_params *prm, int count,
+                    const double *points, uint64_t *states, frw_miss_fn miss,
+                    void *user, frw_event *out);
+
 /* Events on the context stream for device timing of _dev launches:
  * elapsed ms between frw_event_record(ctx, 0) and frw_event_record(ctx, 1). */
 int frw_event_record(frw_ctx *ctx, int which);

@@ -194,7 +194,7 @@ Engine::Engine(const Structure& s, const Config& cfg, StratifiedSgfCache* cache)
   ctx_ = Device::get(cfg_.device).ctx();
 }
 
-void Engine::upload() {
+void Engine::upload() const {
   upload_structure(ctx_, s_);
   // device table: one lattice size; carry over every cached key of this size
   DeviceTable& T = tables()[ctx_];
@@ -430,6 +430,145 @@ CapacitanceResult extract(const Structure& s, const Config& cfg, int threads,
                           StratifiedSgfCache* cache) {
   Engine e(s, cfg, cache);
   return e.extract(threads);
+}
+
+
+// ---- single transitions (engine.cpp:126-148, :201-350) -------------------------
+GaussianSample sample_gaussian(const GaussianSurface& g, SplitMix64& rng) {
+  const double u = rng.uniform();
+  int face = 5;
+  for (int f = 0; f < 5; ++f)
+    if (u < g.face_cdf[f]) {
+      face = f;
+      break;
+    }
+  const int axis = kDirAxis[face];
+  const int b1 = axis == 0 ? 1 : 0;
+  const int b2 = axis == 2 ? 1 : 2;
+  GaussianSample out;
+  out.axis = axis;
+  out.sign = kDirSign[face];
+  out.point[axis] = out.sign < 0 ? g.box.lo[axis] : g.box.hi[axis];
+  out.point[b1] = g.box.lo[b1] + rng.uniform() * (g.box.hi[b1] - g.box.lo[b1]);
+  out.point[b2] = g.box.lo[b2] + rng.uniform() * (g.box.hi[b2] - g.box.lo[b2]);
+  return out;
+}
+
+DispatchStats& DispatchStats::operator+=(const DispatchStats& o) {
+  first_stratified += o.first_stratified;
+  first_shrunk += o.first_shrunk;
+  first_layered += o.first_layered;
+  first_homogenized += o.first_homogenized;
+  cached += o.cached;
+  microwalk += o.microwalk;
+  microwalk_e += o.microwalk_e;
+  fdm += o.fdm;
+  return *this;
+}
+
+std::vector<std::optional<FirstTransition>> Engine::first_transitions(
+    const std::vector<GaussianSample>& g, std::vector<SplitMix64>& rngs,
+    DispatchStats& stats) const {
+  if (g.size() != rngs.size()) throw std::invalid_argument("first_transitions: one rng per sample");
+  upload();
+  const int count = static_cast<int>(g.size());
+  std::vector<double> pts(3 * g.size());
+  std::vector<int32_t> ax(2 * g.size());
+  std::vector<uint64_t> st(g.size());
+  for (int t = 0; t < count; ++t) {
+    for (int a = 0; a < 3; ++a) pts[3 * t + a] = g[t].point[a];
+    ax[2 * t] = g[t].axis;
+    ax[2 * t + 1] = g[t].sign;
+    st[t] = rngs[t].state();
+  }
+  std::vector<frw_first> out(count);
+  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
+  const frw_walk_params p = params();
+  const int rc = frw_first_transitions(ctx_, &p, count, pts.data(), ax.data(), st.data(), miss_cb,
+                                       &mc, out.data());
+  if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
+  throw_status(ctx_, rc);
+  std::vector<std::optional<FirstTransition>> res(count);
+  for (int t = 0; t < count; ++t) {
+    rngs[t].set_state(st[t]);
+    if (!out[t].ok) continue;
+    FirstTransition f;
+    f.point = {out[t].point[0], out[t].point[1], out[t].point[2]};
+    f.weight = out[t].weight;
+    f.branch = out[t].branch;
+    switch (f.branch) {
+      case 0: ++stats.first_stratified; break;
+      case 1: ++stats.first_shrunk; break;
+      case 2: ++stats.first_layered; break;
+      default: ++stats.first_homogenized; break;
+    }
+    res[t] = f;
+  }
+  return res;
+}
+
+std::optional<FirstTransition> Engine::first_transition(const GaussianSample& g, SplitMix64& rng,
+                                                        DispatchStats& stats) const {
+  std::vector<SplitMix64> r{rng};
+  auto res = first_transitions({g}, r, stats);
+  rng = r[0];
+  return res[0];
+}
+
+std::vector<WalkEvent> Engine::transitions(const std::vector<Vec3>& points,
+                                           std::vector<SplitMix64>& rngs,
+                                           DispatchStats& stats) const {
+  if (points.size() != rngs.size()) throw std::invalid_argument("transitions: one rng per point");
+  upload();
+  const int count = static_cast<int>(points.size());
+  std::vector<double> pts(3 * points.size());
+  std::vector<uint64_t> st(points.size());
+  for (int t = 0; t < count; ++t) {
+    for (int a = 0; a < 3; ++a) pts[3 * t + a] = points[t][a];
+    st[t] = rngs[t].state();
+  }
+  std::vector<frw_event> out(count);
+  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
+  const frw_walk_params p = params();
+  const int rc = frw_transitions(ctx_, &p, count, pts.data(), st.data(), miss_cb, &mc, out.data());
+  if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
+  throw_status(ctx_, rc);
+  std::vector<WalkEvent> res(count);
+  for (int t = 0; t < count; ++t) {
+    rngs[t].set_state(st[t]);
+    const frw_event& e = out[t];
+    WalkEvent& w = res[t];
+    if (e.kind == 0) {
+      w.kind = WalkEvent::Kind::Continue;
+      w.point = {e.point[0], e.point[1], e.point[2]};
+    } else if (e.kind == 1) {
+      w.kind = WalkEvent::Kind::Terminate;
+      w.conductor_id = s_.conductors.at(e.conductor).id;
+    } else {
+      w.kind = WalkEvent::Kind::TerminateGround;
+    }
+    switch (e.dispatch) {
+      case 0: ++stats.cached; break;
+      case 1: ++stats.microwalk; break;
+      case 2: ++stats.microwalk_e; break;
+      default: break;
+    }
+  }
+  return res;
+}
+
+WalkEvent Engine::transition(const Vec3& point, SplitMix64& rng, MicroWalkScratch& scratch,
+                             DispatchStats& stats, double* t_mw) const {
+  (void)scratch;
+  const auto t0 = Clock::now();
+  std::vector<SplitMix64> r{rng};
+  DispatchStats local;
+  const WalkEvent e = transitions({point}, r, local)[0];
+  if (t_mw && (local.microwalk || local.microwalk_e))
+    *t_mw += std::chrono::duration<double>(Clock::now() - t0).count();
+  stats += local;
+  rng = r[0];
+  return e;
 }
 
 }  // namespace frwcap

@@ -193,6 +193,20 @@ class SplitMix64 {
   uint64_t state_ = 0;
 };
 
+// Per-caller state of the reference (memo arrays); here it only selects the
+// device, the transits themselves keep no host-side memo.
+class MicroWalkScratch {
+ public:
+  void prepare(int n_) {
+    n = n_;
+    ++epoch;
+  }
+  int n = 0;
+  bool memoize = true;
+  uint64_t epoch = 0;
+  int device = 0;
+};
+
 // ---- SGF (sgf.hpp:116-147) and its cache (sgf_cache.hpp) -------------------
 struct DiscreteSGF {
   int n = 0;
@@ -295,6 +309,26 @@ struct GaussianSurface {
 };
 GaussianSurface gaussian_surface(const Structure& s, double gap_fraction);
 
+struct GaussianSample {
+  Vec3 point;
+  int axis = 0;  // outward normal axis of the sampled face
+  int sign = 1;  // outward normal sign
+};
+GaussianSample sample_gaussian(const GaussianSurface& g, SplitMix64& rng);
+
+struct WalkEvent {
+  enum class Kind { Continue, Terminate, TerminateGround };
+  Kind kind = Kind::TerminateGround;
+  Vec3 point;             // Continue: next point on the transition cube surface
+  int conductor_id = -1;  // Terminate
+};
+
+struct FirstTransition {
+  Vec3 point;
+  double weight = 0;  // farads
+  int branch = 0;     // ladder branch taken, DispatchStats order
+};
+
 struct DispatchStats {
   uint64_t first_stratified = 0, first_shrunk = 0, first_layered = 0, first_homogenized = 0;
   uint64_t cached = 0, microwalk = 0, microwalk_e = 0, fdm = 0;
@@ -302,6 +336,7 @@ struct DispatchStats {
     return first_stratified + first_shrunk + first_layered + first_homogenized;
   }
   uint64_t subsequent_total() const { return cached + microwalk + microwalk_e + fdm; }
+  DispatchStats& operator+=(const DispatchStats& o);
 };
 
 struct TerminalEstimate {
@@ -353,8 +388,22 @@ class Engine {
   // per-walk outcomes of walks [begin, begin+count) (parity tests)
   std::vector<frw_walk_record> run_walks(uint64_t begin, int64_t count);
 
+  // One weighted first transition / one subsequent transition on the device,
+  // continuing the caller's SplitMix64 (engine.hpp:146-159).  Table misses
+  // are solved and inserted before the draw, like extract does.
+  std::optional<FirstTransition> first_transition(const GaussianSample& g, SplitMix64& rng,
+                                                  DispatchStats& stats) const;
+  WalkEvent transition(const Vec3& point, SplitMix64& rng, MicroWalkScratch& scratch,
+                       DispatchStats& stats, double* t_mw = nullptr) const;
+  // batched forms (B200): entry t continues rngs[t]
+  std::vector<std::optional<FirstTransition>> first_transitions(
+      const std::vector<GaussianSample>& g, std::vector<SplitMix64>& rngs,
+      DispatchStats& stats) const;
+  std::vector<WalkEvent> transitions(const std::vector<Vec3>& points,
+                                     std::vector<SplitMix64>& rngs, DispatchStats& stats) const;
+
  private:
-  void upload();
+  void upload() const;
   frw_walk_params params() const;
   const Structure& s_;
   Config cfg_;
@@ -383,20 +432,6 @@ struct Exit {
 
 class EngulfedStart : public std::runtime_error {
   using std::runtime_error::runtime_error;
-};
-
-// Per-caller state of the reference (memo arrays); here it only selects the
-// device, the transits themselves keep no host-side memo.
-class MicroWalkScratch {
- public:
-  void prepare(int n_) {
-    n = n_;
-    ++epoch;
-  }
-  int n = 0;
-  bool memoize = true;
-  uint64_t epoch = 0;
-  int device = 0;
 };
 
 // beta_i = alpha_i / sum(alpha) at an interior node (microwalk.cpp:160-186)

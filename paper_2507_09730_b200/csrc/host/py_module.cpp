@@ -329,6 +329,111 @@ PYBIND11_MODULE(_core, m) {
       "Per-walk outcomes of walks [begin, begin+count) (parity tests).");
 
 
+  m.def(
+      "walks_by_transitions",
+      [](const std::string& text, uint64_t begin, int64_t count, bool single,
+         const py::kwargs& kw) {
+        // run_walk (engine.cpp:352-376) composed from Engine::first_transition
+        // and Engine::transition, all walks in lockstep (or one call each)
+        int threads = 0;
+        const Config cfg = config_from_kwargs(kw, threads);
+        const Structure s = parse_structure(text, cfg.world_margin);
+        const int ground = static_cast<int>(s.conductors.size());
+        auto slot_of = [&](int id) {
+          for (size_t i = 0; i < s.conductors.size(); ++i)
+            if (s.conductors[i].id == id) return static_cast<int>(i);
+          return ground;
+        };
+        std::vector<int32_t> slot(count, ground);
+        std::vector<double> weight(count, 0.0);
+        std::vector<uint8_t> aborted(count, 0);
+        DispatchStats stats;
+        {
+          py::gil_scoped_release release;
+          Engine e(s, cfg, &shared_cache());
+          std::vector<SplitMix64> rng(count);
+          for (int64_t w = 0; w < count; ++w) rng[w] = SplitMix64(cfg.seed, begin + w);
+          std::vector<int64_t> live(count);
+          for (int64_t w = 0; w < count; ++w) live[w] = w;
+          std::vector<Vec3> pos(count);
+          for (int attempt = 0; attempt < 100 && !live.empty(); ++attempt) {
+            std::vector<GaussianSample> g;
+            std::vector<SplitMix64> r;
+            for (int64_t w : live) {
+              g.push_back(sample_gaussian(e.surface(), rng[w]));
+              r.push_back(rng[w]);
+            }
+            std::vector<std::optional<FirstTransition>> f;
+            if (single) {
+              for (size_t q = 0; q < g.size(); ++q) f.push_back(e.first_transition(g[q], r[q], stats));
+            } else {
+              f = e.first_transitions(g, r, stats);
+            }
+            std::vector<int64_t> next;
+            for (size_t q = 0; q < live.size(); ++q) {
+              const int64_t w = live[q];
+              rng[w] = r[q];
+              if (f[q]) {
+                weight[w] = f[q]->weight;
+                pos[w] = f[q]->point;
+              } else {
+                next.push_back(w);
+              }
+            }
+            live.swap(next);
+          }
+          for (int64_t w : live) aborted[w] = 1;  // resample cap: ground, weight 0
+          std::vector<int64_t> act;
+          for (int64_t w = 0; w < count; ++w)
+            if (!aborted[w]) act.push_back(w);
+          MicroWalkScratch scr;
+          for (long hop = 0; hop < cfg.hop_cap && !act.empty(); ++hop) {
+            std::vector<Vec3> p;
+            std::vector<SplitMix64> r;
+            for (int64_t w : act) {
+              p.push_back(pos[w]);
+              r.push_back(rng[w]);
+            }
+            std::vector<WalkEvent> ev;
+            if (single) {
+              for (size_t q = 0; q < p.size(); ++q) ev.push_back(e.transition(p[q], r[q], scr, stats));
+            } else {
+              ev = e.transitions(p, r, stats);
+            }
+            std::vector<int64_t> next;
+            for (size_t q = 0; q < act.size(); ++q) {
+              const int64_t w = act[q];
+              rng[w] = r[q];
+              if (ev[q].kind == WalkEvent::Kind::Terminate) {
+                slot[w] = slot_of(ev[q].conductor_id);
+              } else if (ev[q].kind == WalkEvent::Kind::TerminateGround) {
+                slot[w] = ground;
+              } else {
+                pos[w] = ev[q].point;
+                next.push_back(w);
+              }
+            }
+            act.swap(next);
+          }
+          for (int64_t w : act) aborted[w] = 1;  // hop cap
+        }
+        py::dict d;
+        d["slot"] = py::array_t<int32_t>(count, slot.data());
+        d["weight"] = py::array_t<double>(count, weight.data());
+        d["aborted"] = py::array_t<uint8_t>(count, aborted.data());
+        py::dict st;
+        st["first_stratified"] = stats.first_stratified;
+        st["first_shrunk"] = stats.first_shrunk;
+        st["first_layered"] = stats.first_layered;
+        st["first_homogenized"] = stats.first_homogenized;
+        st["cached"] = stats.cached;
+        st["microwalk"] = stats.microwalk;
+        st["microwalk_e"] = stats.microwalk_e;
+        d["stats"] = st;
+        return d;
+      },
+      py::arg("structure_json"), py::arg("begin"), py::arg("count"), py::arg("single") = false);
+
   // single-transit API (microwalk.hpp:70-100) -- test and integration hooks
   m.def(
       "transits_grid",

@@ -1488,6 +1488,130 @@ __global__ void __launch_bounds__(128)
   out[t] = e;
 }
 
+// ---- single engine transitions (Engine::first_transition / transition) -----
+struct DevFirst {
+  int32_t ok, branch;
+  double weight;
+  double point[3];
+};
+static_assert(sizeof(DevFirst) == sizeof(frw_first), "first layout");
+struct DevEvent {
+  int32_t kind, conductor, dispatch, pad;
+  double point[3];
+  uint64_t mw_steps;
+};
+static_assert(sizeof(DevEvent) == sizeof(frw_event), "event layout");
+
+// rc per entry: 1 done, 2 table miss (re-run after the key is inserted), <0 error
+__global__ void __launch_bounds__(128)
+    k_first_single(DStruct s, DSgf T, DParams P, DSlots W, DCounters* C, DMiss M,
+                   const double* gpts, const int32_t* axsign, uint64_t* states, const int* idx,
+                   int count, int* rc_out, DevFirst* out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const int t = idx[q];
+  Rng rng;
+  rng.s = states[t];
+  const double g[3] = {gpts[3 * t], gpts[3 * t + 1], gpts[3 * t + 2]};
+  FirstOut fo;
+  const int rc = first_transition(s, T, P, t, rng, g, axsign[2 * t], axsign[2 * t + 1],
+                                  W.boxes + static_cast<size_t>(q) * KMAX, C, M, &fo);
+  rc_out[q] = rc;
+  if (rc == 2) return;  // miss: nothing drawn, the state stays
+  DevFirst f{};
+  f.ok = rc == 1;
+  if (rc == 1) {
+    f.branch = fo.branch;
+    f.weight = fo.weight;
+    f.point[0] = fo.p[0];
+    f.point[1] = fo.p[1];
+    f.point[2] = fo.p[2];
+  }
+  out[t] = f;
+  states[t] = rng.s;
+  if (rc < 0) set_err(C, FRW_EINVAL);
+}
+
+__global__ void __launch_bounds__(128)
+    k_transition_single(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C,
+                        DMiss M, const double* pts, uint64_t* states, const int* idx, int count,
+                        int* rc_out, DevEvent* out) {
+  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ DirDelta dd[6];
+  setup_smem_tables(s, alpha_sm, dd);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const int t = idx[q];
+  const int slot = q;
+  W.wid[slot] = t;
+  W.p[3 * slot] = pts[3 * t];
+  W.p[3 * slot + 1] = pts[3 * t + 1];
+  W.p[3 * slot + 2] = pts[3 * t + 2];
+  W.rng[slot] = states[t];
+  W.hops[slot] = 0;
+  W.cached[slot] = 0;
+  W.mw[slot] = 0;
+  W.mwsteps[slot] = 0;
+  W.weight[slot] = 0;
+  W.state[slot] = S_ACTIVE;
+  recs[t].done = 0;
+  AdvLane L;
+  adv_load(W, slot, L);
+  const int r = advance_once(s, T, P, W, recs, C, M, nullptr, L);
+  DevEvent e{};
+  e.conductor = -1;
+  e.dispatch = -1;
+  if (r == 0) {  // cached hop
+    e.kind = 0;
+    e.dispatch = 0;
+    e.point[0] = L.p[0];
+    e.point[1] = L.p[1];
+    e.point[2] = L.p[2];
+    states[t] = L.rng.s;
+  } else if (r == 1) {
+    if (!recs[t].done) {  // table miss (or geometry error, flagged in C->err)
+      rc_out[q] = 2;
+      return;
+    }
+    const int sl = recs[t].slot;
+    e.kind = sl == s.nc ? 2 : 1;
+    e.conductor = sl == s.nc ? -1 : sl;
+    states[t] = L.rng.s;
+  } else {  // MicroWalk / MicroWalk-E hop on the compiled job
+    const int n = P.n;
+    const int cap = 1000 * n * n;
+    MwLane ml;
+    ml.gsteps = 0;
+    ml.cchg = 0;
+    mw_arm(W, alpha_sm, s.P, slot, n, ml);
+    ml.wid = t;
+    int code = MW_GO, xdir = 0;
+    while (code == MW_GO)
+      code = mw_superstep<FRW_RNG_SPLITMIX_PARITY>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, ml,
+                                                   &xdir);
+    e.dispatch = W.mwkind[slot] ? 2 : 1;
+    e.mw_steps = ml.steps;
+    if (code == MW_SURFACE) {
+      mw_exit(W, n, ml, xdir);
+      e.kind = 0;
+      e.point[0] = W.p[3 * slot];
+      e.point[1] = W.p[3 * slot + 1];
+      e.point[2] = W.p[3 * slot + 2];
+    } else if (code == MW_COND) {
+      int v[3] = {coord(ml.node, 0), coord(ml.node, 1), coord(ml.node, 2)};
+      v[xdir >> 1] += (xdir & 1) ? 1 : -1;
+      const uint64_t cm = voxel_mask(lane_atlas(W, slot), ml.bm, v) & cond_mask(ml.ncond);
+      e.kind = 1;
+      e.conductor = box_cond(W.boxes[static_cast<size_t>(slot) * KMAX + __ffsll(cm) - 1]);
+    } else {
+      set_err(C, FRW_ESTEPCAP);
+    }
+    states[t] = ml.rng;
+  }
+  rc_out[q] = 1;
+  out[t] = e;
+}
+
 // ---- deterministic tallies -------------------------------------------------
 constexpr int kChunk = 1024;
 
@@ -1720,14 +1844,19 @@ int sgf_sync(frw_ctx* ctx, SgfHost& T) {
   cudaFree(T.d_entry);
   T.d_hash = dalloc<uint64_t>(T.cap);
   T.d_entry = dalloc<int>(T.cap);
-  FRW_CUDA(ctx, cudaMemcpy(T.d_hash, T.hash.data(), 8 * T.cap, cudaMemcpyHostToDevice));
-  FRW_CUDA(ctx, cudaMemcpy(T.d_entry, T.entry.data(), 4 * T.cap, cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpyAsync(T.d_hash, T.hash.data(), 8 * T.cap, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  FRW_CUDA(ctx, cudaMemcpyAsync(T.d_entry, T.entry.data(), 4 * T.cap, cudaMemcpyHostToDevice,
+                                ctx->stream));
   if (ne) {
-    FRW_CUDA(ctx, cudaMemcpy(T.d_axis, T.axis.data(), 4 * ne, cudaMemcpyHostToDevice));
-    FRW_CUDA(ctx, cudaMemcpy(T.d_keys, T.keys.data(), 8 * ne * NMAX, cudaMemcpyHostToDevice));
-    FRW_CUDA(ctx, cudaMemcpy(T.d_pitch, T.pitch.data(), 8 * ne, cudaMemcpyHostToDevice));
-    FRW_CUDA(ctx, cudaMemcpy(T.d_data, T.data.data(), sizeof(double*) * ne,
-                             cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpyAsync(T.d_axis, T.axis.data(), 4 * ne, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    FRW_CUDA(ctx, cudaMemcpyAsync(T.d_keys, T.keys.data(), 8 * ne * NMAX, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    FRW_CUDA(ctx, cudaMemcpyAsync(T.d_pitch, T.pitch.data(), 8 * ne, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    FRW_CUDA(ctx, cudaMemcpyAsync(T.d_data, T.data.data(), sizeof(double*) * ne,
+                                  cudaMemcpyHostToDevice, ctx->stream));
   }
   T.dirty = false;
   return FRW_OK;
@@ -1753,6 +1882,72 @@ void sgf_insert_index(SgfHost& T, uint64_t h, int e) {
   while (T.entry[j] >= 0) j = (j + 1) & (T.cap - 1);
   T.hash[j] = h;
   T.entry[j] = e;
+}
+
+DParams params_of(const frw_walk_params* prm) {
+  DParams P{};
+  P.n = prm->grid_n;
+  P.panels = 6 * P.n * P.n;
+  P.mode = prm->mode;
+  P.rng = prm->rng_mode;
+  P.snap = prm->snap;
+  P.expansion = prm->expansion;
+  P.hop_cap = prm->hop_cap;
+  P.seed = prm->seed;
+  P.mixed_seed = sm64_mix(prm->seed);
+  std::memcpy(P.gbox, prm->gauss_box, sizeof P.gbox);
+  std::memcpy(P.fcdf, prm->face_cdf, sizeof P.fcdf);
+  P.area = prm->area_m2;
+  return P;
+}
+
+// Solves the distinct keys of `nmiss` recorded table misses (device solver,
+// or the caller's callback) and inserts them; *added = new entries.
+int resolve_misses(frw_ctx* ctx, Engine& E, int n, unsigned long long nmiss, frw_miss_fn miss,
+                   void* user, int* added) {
+  const DMiss& M = E.M;
+  const int nm = static_cast<int>(std::min<unsigned long long>(nmiss, kMissMax));
+  std::vector<int> maxis(nm);
+  std::vector<double> mlayers(static_cast<size_t>(nm) * NMAX);
+  FRW_CUDA(ctx, cudaMemcpy(maxis.data(), M.axis, 4 * nm, cudaMemcpyDeviceToHost));
+  FRW_CUDA(ctx, cudaMemcpy(mlayers.data(), M.layers, 8 * size_t(nm) * NMAX,
+                           cudaMemcpyDeviceToHost));
+  std::unordered_map<uint64_t, int> seen;
+  std::vector<int> uaxis;
+  std::vector<double> ulayers;
+  for (int q = 0; q < nm; ++q) {
+    const double* L = &mlayers[static_cast<size_t>(q) * NMAX];
+    const uint64_t h = host_key_hash(n, maxis[q], L);
+    auto it = seen.find(h);
+    if (it != seen.end() && maxis[it->second] == maxis[q] &&
+        std::memcmp(&mlayers[static_cast<size_t>(it->second) * NMAX], L, 8 * n) == 0)
+      continue;
+    seen[h] = q;
+    uaxis.push_back(maxis[q]);
+    ulayers.insert(ulayers.end(), L, L + n);
+  }
+  const int before = static_cast<int>(E.sgf.axis.size());
+  if (miss) {
+    if (miss(user, n, static_cast<int>(uaxis.size()), uaxis.data(), ulayers.data()) != 0)
+      return frw_fail(ctx, FRW_ESOLVE, "run_walks: miss callback failed");
+  } else {  // solve on the device and insert
+    const int cnt = static_cast<int>(uaxis.size());
+    const size_t pan = 6ull * n * n;
+    std::vector<double> pr(pan * cnt), ke(3 * pan * cnt), cdf(pan);
+    if (int rc = frw_sgf_solve(ctx, n, cnt, uaxis.data(), ulayers.data(), pr.data(), ke.data()))
+      return rc;
+    for (int q = 0; q < cnt; ++q) {
+      double run = 0;
+      for (size_t b = 0; b < pan; ++b) cdf[b] = run += pr[q * pan + b];
+      if (int rc = frw_sgf_put(ctx, n, uaxis[q], &ulayers[static_cast<size_t>(q) * n], 1.0,
+                               &pr[q * pan], cdf.data(), &ke[3 * q * pan]))
+        return rc;
+    }
+  }
+  if (static_cast<int>(E.sgf.axis.size()) == before)
+    return frw_fail(ctx, FRW_EMISS, "run_walks: miss callback added no table entry");
+  *added = static_cast<int>(E.sgf.axis.size()) - before;
+  return sgf_sync(ctx, E.sgf);
 }
 
 int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
@@ -1798,6 +1993,120 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
 
 using namespace frw;
 
+namespace frw {
+namespace {
+// Shared driver of frw_first_transitions / frw_transitions: uploads the
+// inputs, runs `launch` over the pending entries, resolves table misses and
+// re-runs the entries that missed (they drew nothing), then copies back.
+template <class Out, class Launch>
+int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double* pts,
+               const int32_t* axsign, uint64_t* states, frw_miss_fn miss, void* user, Out* out,
+               Launch launch) {
+  Engine& E = *engine_of(ctx);
+  if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "transitions: no structure uploaded");
+  if (!prm || prm->grid_n < 2 || prm->grid_n > NMAX)
+    return frw_fail(ctx, FRW_EINVAL, "transitions: grid_n must lie in [2, 64]");
+  if (prm->mode == FRW_MODE_FDM)
+    return frw_fail(ctx, FRW_EINVAL, "transitions: FDM transitions are not on the device yet");
+  if (count < 0 || (count > 0 && (!pts || !states || !out)))
+    return frw_fail(ctx, FRW_EINVAL, "transitions: bad arguments");
+  if (E.sgf.n && E.sgf.n != prm->grid_n)
+    return frw_fail(ctx, FRW_EINVAL, "transitions: SGF table holds another lattice size");
+  if (count == 0) return FRW_OK;
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  if (E.S < count)
+    if (int rc = ensure_slots(ctx, E, count)) return rc;
+  if (E.recs_cap < count) {
+    cudaFree(E.recs);
+    E.recs = dalloc<WalkRec>(count);
+    if (!E.recs) return frw_fail(ctx, FRW_ENOMEM, "transitions: record allocation failed");
+    E.recs_cap = count;
+  }
+  if (!E.d_cnt) {
+    E.d_cnt = dalloc<DCounters>(1);
+    E.M.axis = dalloc<int>(kMissMax);
+    E.M.layers = dalloc<double>(size_t(kMissMax) * NMAX);
+  }
+  if (int rc = sgf_sync(ctx, E.sgf)) return rc;
+  DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal, {}};
+  std::memcpy(s.world, E.world, sizeof s.world);
+  DParams P = params_of(prm);
+  P.rng = FRW_RNG_SPLITMIX_PARITY;  // the caller's SplitMix64 streams
+  P.count = count;
+  double* d_pts = dalloc<double>(3 * size_t(count));
+  int32_t* d_ax = axsign ? dalloc<int32_t>(2 * size_t(count)) : nullptr;
+  uint64_t* d_st = dalloc<uint64_t>(count);
+  int* d_idx = dalloc<int>(count);
+  int* d_rc = dalloc<int>(count);
+  Out* d_out = dalloc<Out>(count);
+  auto release = [&] {
+    cudaFree(d_pts);
+    cudaFree(d_ax);
+    cudaFree(d_st);
+    cudaFree(d_idx);
+    cudaFree(d_rc);
+    cudaFree(d_out);
+  };
+  if (!d_pts || (axsign && !d_ax) || !d_st || !d_idx || !d_rc || !d_out) {
+    release();
+    return frw_fail(ctx, FRW_ENOMEM, "transitions: device allocation failed");
+  }
+  std::vector<int> pend(count), rc(count);
+  for (int t = 0; t < count; ++t) pend[t] = t;
+  int status = FRW_OK;
+  cudaStream_t st = ctx->stream;
+  cudaMemcpyAsync(d_pts, pts, 24 * size_t(count), cudaMemcpyHostToDevice, st);
+  if (axsign) cudaMemcpyAsync(d_ax, axsign, 8 * size_t(count), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_st, states, 8 * size_t(count), cudaMemcpyHostToDevice, st);
+  for (int pass = 0; !pend.empty() && status == FRW_OK; ++pass) {
+    if (pass > 64) {
+      status = frw_fail(ctx, FRW_EMISS, "transitions: table misses keep recurring");
+      break;
+    }
+    const int np = static_cast<int>(pend.size());
+    DSgf T{E.sgf.cap, E.sgf.d_hash, E.sgf.d_entry, E.sgf.d_axis, E.sgf.d_keys, E.sgf.d_pitch,
+           E.sgf.d_data};
+    cudaMemcpyAsync(d_idx, pend.data(), 4 * size_t(np), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), st);
+    launch(s, T, P, E, d_pts, d_ax, d_st, d_idx, np, d_rc, d_out);
+    DCounters c;
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(rc.data(), d_rc, 4 * size_t(np), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(&c, E.d_cnt, sizeof c, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      status = frw_fail(ctx, FRW_ECUDA, "transitions: kernel failed");
+      break;
+    }
+    if (c.err) {
+      status = c.err == static_cast<unsigned long long>(-FRW_ESTEPCAP)
+                   ? frw_fail(ctx, FRW_ESTEPCAP, "microwalk transit exceeded the step cap")
+                   : frw_fail(ctx, FRW_EINVAL,
+                              "transitions: point outside the world or inside a conductor");
+      break;
+    }
+    std::vector<int> next;
+    for (int q = 0; q < np; ++q)
+      if (rc[q] == 2) next.push_back(pend[q]);
+    if (!next.empty()) {
+      int added = 0;
+      status = resolve_misses(ctx, E, P.n, c.nmiss, miss, user, &added);
+    }
+    pend.swap(next);
+  }
+  if (status == FRW_OK &&
+      (cudaMemcpyAsync(out, d_out, sizeof(Out) * count, cudaMemcpyDeviceToHost, st) !=
+           cudaSuccess ||
+       cudaMemcpyAsync(states, d_st, 8 * size_t(count), cudaMemcpyDeviceToHost, st) !=
+           cudaSuccess ||
+       cudaStreamSynchronize(st) != cudaSuccess))
+    status = frw_fail(ctx, FRW_ECUDA, "transitions: copy-back failed");
+  release();
+  return status;
+}
+}  // namespace
+}  // namespace frw
+
 extern "C" {
 
 int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
@@ -1842,14 +2151,20 @@ int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
   E.d_rpal = dalloc<double>(P);
   if (!E.d_cbox || !E.d_dbox || !E.d_dcls || !E.d_pal || !E.d_alpha || !E.d_rpal)
     return frw_fail(ctx, FRW_ENOMEM, "upload_structure: device allocation failed");
-  FRW_CUDA(ctx, cudaMemcpy(E.d_cbox, s->cond_box, 48 * size_t(s->n_cond), cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cbox, s->cond_box, 48 * size_t(s->n_cond), cudaMemcpyHostToDevice,
+                                ctx->stream));
   if (s->n_diel) {
-    FRW_CUDA(ctx, cudaMemcpy(E.d_dbox, s->diel_box, 48 * size_t(s->n_diel), cudaMemcpyHostToDevice));
-    FRW_CUDA(ctx, cudaMemcpy(E.d_dcls, dcls.data(), s->n_diel, cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpyAsync(E.d_dbox, s->diel_box, 48 * size_t(s->n_diel), cudaMemcpyHostToDevice,
+                                ctx->stream));
+    FRW_CUDA(ctx, cudaMemcpyAsync(E.d_dcls, dcls.data(), s->n_diel, cudaMemcpyHostToDevice,
+                                ctx->stream));
   }
-  FRW_CUDA(ctx, cudaMemcpy(E.d_pal, pal.data(), 8 * P, cudaMemcpyHostToDevice));
-  FRW_CUDA(ctx, cudaMemcpy(E.d_alpha, alpha.data(), 8 * size_t(P) * P, cudaMemcpyHostToDevice));
-  FRW_CUDA(ctx, cudaMemcpy(E.d_rpal, rpal.data(), 8 * P, cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpyAsync(E.d_pal, pal.data(), 8 * P, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  FRW_CUDA(ctx, cudaMemcpyAsync(E.d_alpha, alpha.data(), 8 * size_t(P) * P, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  FRW_CUDA(ctx, cudaMemcpyAsync(E.d_rpal, rpal.data(), 8 * P, cudaMemcpyHostToDevice,
+                                ctx->stream));
   E.nc = s->n_cond;
   E.nd = s->n_diel;
   E.P = P;
@@ -1890,14 +2205,18 @@ int frw_sgf_put(frw_ctx* ctx, int n, int axis, const double* layers, double pitc
       while (i < panels && cdf[i] <= gb) ++i;  // first cdf > fl((b/G)*total)
       guide[b] = static_cast<int>(i);
     }
-    FRW_CUDA(ctx, cudaMemcpy(blk + 5 * panels, guide.data(), 4 * kGuide, cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpyAsync(blk + 5 * panels, guide.data(), 4 * kGuide, cudaMemcpyHostToDevice,
+                                ctx->stream));
   }
-  FRW_CUDA(ctx, cudaMemcpy(blk, cdf, 8 * panels, cudaMemcpyHostToDevice));
-  FRW_CUDA(ctx, cudaMemcpy(blk + panels, probs, 8 * panels, cudaMemcpyHostToDevice));
+  FRW_CUDA(ctx, cudaMemcpyAsync(blk, cdf, 8 * panels, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  FRW_CUDA(ctx, cudaMemcpyAsync(blk + panels, probs, 8 * panels, cudaMemcpyHostToDevice,
+                                ctx->stream));
   if (kernels)
-    FRW_CUDA(ctx, cudaMemcpy(blk + 2 * panels, kernels, 24 * panels, cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpyAsync(blk + 2 * panels, kernels, 24 * panels, cudaMemcpyHostToDevice,
+                                ctx->stream));
   else
-    FRW_CUDA(ctx, cudaMemset(blk + 2 * panels, 0, 24 * panels));
+    FRW_CUDA(ctx, cudaMemsetAsync(blk + 2 * panels, 0, 24 * panels, ctx->stream));
   const int e = static_cast<int>(T.axis.size());
   T.axis.push_back(axis);
   T.keys.resize(static_cast<size_t>(e + 1) * NMAX, 0.0);
@@ -2007,6 +2326,32 @@ int frw_structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
   return status;
 }
 
+int frw_first_transitions(frw_ctx* ctx, const frw_walk_params* prm, int count,
+                          const double* gpoints, const int32_t* axis_sign, uint64_t* states,
+                          frw_miss_fn miss, void* user, frw_first* out) {
+  if (!ctx) return FRW_EINVAL;
+  if (count > 0 && !axis_sign) return frw_fail(ctx, FRW_EINVAL, "first_transitions: axis_sign");
+  return run_single(
+      ctx, prm, count, gpoints, axis_sign, states, miss, user, reinterpret_cast<DevFirst*>(out),
+      [&](const DStruct& s, const DSgf& T, const DParams& P, Engine& E, const double* pts,
+          const int32_t* ax, uint64_t* st, const int* idx, int np, int* rc, DevFirst* o) {
+        k_first_single<<<(np + 127) / 128, 128, 0, ctx->stream>>>(s, T, P, E.W, E.d_cnt, E.M, pts,
+                                                                  ax, st, idx, np, rc, o);
+      });
+}
+
+int frw_transitions(frw_ctx* ctx, const frw_walk_params* prm, int count, const double* points,
+                    uint64_t* states, frw_miss_fn miss, void* user, frw_event* out) {
+  if (!ctx) return FRW_EINVAL;
+  return run_single(
+      ctx, prm, count, points, nullptr, states, miss, user, reinterpret_cast<DevEvent*>(out),
+      [&](const DStruct& s, const DSgf& T, const DParams& P, Engine& E, const double* pts,
+          const int32_t*, uint64_t* st, const int* idx, int np, int* rc, DevEvent* o) {
+        k_transition_single<<<(np + 127) / 128, 128, 0, ctx->stream>>>(
+            s, T, P, E.W, E.recs, E.d_cnt, E.M, pts, st, idx, np, rc, o);
+      });
+}
+
 int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint64_t walk_begin,
                   int64_t count, frw_miss_fn miss, void* user, frw_tally* out,
                   frw_walk_record* records) {
@@ -2055,19 +2400,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
 
   DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal, {}};
   std::memcpy(s.world, E.world, sizeof s.world);
-  DParams P{};
-  P.n = prm->grid_n;
-  P.panels = 6 * P.n * P.n;
-  P.mode = prm->mode;
-  P.rng = prm->rng_mode;
-  P.snap = prm->snap;
-  P.expansion = prm->expansion;
-  P.hop_cap = prm->hop_cap;
-  P.seed = prm->seed;
-  P.mixed_seed = sm64_mix(prm->seed);
-  std::memcpy(P.gbox, prm->gauss_box, sizeof P.gbox);
-  std::memcpy(P.fcdf, prm->face_cdf, sizeof P.fcdf);
-  P.area = prm->area_m2;
+  DParams P = params_of(prm);
   P.walk_begin = walk_begin;
   P.count = count;
   P.master = master;
@@ -2085,8 +2418,6 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   bool tail = false;
   float mw_ms = 0;
   uint64_t misses_total = 0, restarts = 0;
-  std::vector<int> maxis;
-  std::vector<double> mlayers;
   int status = FRW_OK;
   for (int round = 0;; ++round) {
     DSgf T{E.sgf.cap, E.sgf.d_hash, E.sgf.d_entry, E.sgf.d_axis, E.sgf.d_keys, E.sgf.d_pitch,
@@ -2143,58 +2474,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       break;
     }
     if (c.nmiss) {
-      const int nm = static_cast<int>(std::min<unsigned long long>(c.nmiss, kMissMax));
-      maxis.resize(nm);
-      mlayers.resize(static_cast<size_t>(nm) * NMAX);
-      FRW_CUDA(ctx, cudaMemcpy(maxis.data(), M.axis, 4 * nm, cudaMemcpyDeviceToHost));
-      FRW_CUDA(ctx, cudaMemcpy(mlayers.data(), M.layers, 8 * size_t(nm) * NMAX,
-                               cudaMemcpyDeviceToHost));
-      std::unordered_map<uint64_t, int> seen;
-      std::vector<int> uaxis;
-      std::vector<double> ulayers;
-      for (int q = 0; q < nm; ++q) {
-        const double* L = &mlayers[static_cast<size_t>(q) * NMAX];
-        const uint64_t h = host_key_hash(P.n, maxis[q], L);
-        auto it = seen.find(h);
-        if (it != seen.end() && maxis[it->second] == maxis[q] &&
-            std::memcmp(&mlayers[static_cast<size_t>(it->second) * NMAX], L, 8 * P.n) == 0)
-          continue;
-        seen[h] = q;
-        uaxis.push_back(maxis[q]);
-        ulayers.insert(ulayers.end(), L, L + P.n);
-      }
-      const int before = static_cast<int>(E.sgf.axis.size());
-      if (miss) {
-        if (miss(user, P.n, static_cast<int>(uaxis.size()), uaxis.data(), ulayers.data()) != 0) {
-          status = frw_fail(ctx, FRW_ESOLVE, "run_walks: miss callback failed");
-          break;
-        }
-      } else {  // solve on the device and insert
-        const int cnt = static_cast<int>(uaxis.size());
-        const size_t pan = 6ull * P.n * P.n;
-        std::vector<double> pr(pan * cnt), ke(3 * pan * cnt), cdf(pan);
-        if (int rc = frw_sgf_solve(ctx, P.n, cnt, uaxis.data(), ulayers.data(), pr.data(),
-                                   ke.data())) {
-          status = rc;
-          break;
-        }
-        for (int q = 0; q < cnt && status == FRW_OK; ++q) {
-          double run = 0;
-          for (size_t b = 0; b < pan; ++b) cdf[b] = run += pr[q * pan + b];
-          status = frw_sgf_put(ctx, P.n, uaxis[q], &ulayers[static_cast<size_t>(q) * P.n], 1.0,
-                               &pr[q * pan], cdf.data(), &ke[3 * q * pan]);
-        }
-        if (status) break;
-      }
-      if (static_cast<int>(E.sgf.axis.size()) == before) {
-        status = frw_fail(ctx, FRW_EMISS, "run_walks: miss callback added no table entry");
-        break;
-      }
-      misses_total += E.sgf.axis.size() - before;
-      if (int rc = sgf_sync(ctx, E.sgf)) {
-        status = rc;
-        break;
-      }
+      int added = 0;
+      status = resolve_misses(ctx, E, P.n, c.nmiss, miss, user, &added);
+      if (status) break;
+      misses_total += added;
       // parked walks restart from scratch (nothing of their partial run was
       // committed): pend <- retry; the round transition happens here too
       FRW_CUDA(ctx, cudaMemcpyAsync(M.pend, M.retry, 8 * c.nretry, cudaMemcpyDeviceToDevice,

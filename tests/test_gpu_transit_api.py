@@ -221,3 +221,26 @@ def test_c_abi_states_and_structure_transits(gpu_ctx, oracle, ref):
         r = rs.microwalk_lazy(cubes[t, :3], cubes[t, 3], 24, 12, t, 1)
         assert d["panel"][t] == r["panel"][0] and d["steps"][t] == r["steps"][0]
         assert list(d["point"][t]) == list(r["point"][0])
+
+
+@pytest.mark.parametrize("mode", ["HYBRID-MW", "HYBRID-MWE"])
+@pytest.mark.parametrize("name", ["c3", "highk_cross"])
+def test_engine_transitions_compose_the_walk_engine(name, mode):
+    """Engine::first_transition / Engine::transition (engine.hpp:146-159) on
+    the device, composed into run_walk (engine.cpp:352-376) on the host,
+    reproduce the device walk engine's per-walk outcome bit for bit (same
+    SplitMix64 streams, same SGF tables)"""
+    text = json.dumps(c3_structure()) if name == "c3" else SCENES[name]().to_json()
+    kw = dict(mode=mode, rng="splitmix", seed=31, grid_n=24)
+    dev = frwcap.run_walks_json(text, 0, 300, **kw)
+    comp = frwcap.walks_by_transitions(text, 0, 300, False, **kw)
+    assert np.array_equal(comp["slot"], dev["slot"])
+    assert np.array_equal(comp["weight"], dev["weight"])
+    assert np.array_equal(comp["aborted"], dev["aborted"])
+    st = comp["stats"]
+    assert st["first_stratified"] + st["first_shrunk"] + st["first_layered"] + \
+        st["first_homogenized"] >= 300
+    assert (st["microwalk"] if mode == "HYBRID-MW" else st["microwalk_e"]) > 0
+    one = frwcap.walks_by_transitions(text, 0, 12, True, **kw)
+    for k in ("slot", "weight", "aborted"):
+        assert np.array_equal(one[k], comp[k][:12])
