@@ -283,7 +283,7 @@ int frw_first_transitions(frw_ctx *ctx, const frw_walk_params *prm, int count,
 typedef struct {
   int32_t kind;      /* 0 continue, 1 terminate on a conductor, 2 ground    */
   int32_t conductor; /* declaration index (kind 1)                          */
-  int32_t dispatch;  /* -1 snapped, 0 cached, 1 microwalk, 2 microwalk_e    */
+  int32_t dispatch;  /* -1 snapped, 0 cached, 1 microwalk, 2 microwalk_e, 3 fdm */
   int32_t pad;
   double point[3];   /* continue: next point                                */
   uint64_t mw_steps; /* lattice steps of a MicroWalk transition             */

@@ -177,9 +177,6 @@ Engine::Engine(const Structure& s, const Config& cfg, StratifiedSgfCache* cache)
     : s_(s), cfg_(cfg) {
   cfg_.validate();
   s_.validate();
-  if (cfg_.mode == Mode::FDM)
-    throw std::invalid_argument("mode FDM (a direct solve per hop) is not available on the B200 "
-                                "device build yet; use HYBRID-MW or HYBRID-MWE");
   if (cache) {
     cache_ = cache;
   } else {
@@ -210,6 +207,7 @@ frw_walk_params Engine::params() const {
   frw_walk_params p{};
   p.grid_n = cfg_.grid_n;
   switch (cfg_.mode) {
+    case Mode::FDM: p.mode = FRW_MODE_FDM; break;
     case Mode::MW: p.mode = FRW_MODE_MW; break;
     case Mode::MWE: p.mode = FRW_MODE_MWE; break;
     case Mode::HybridMWE: p.mode = FRW_MODE_HYBRID_MWE; break;
@@ -393,6 +391,8 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
         res.dispatch.cached += r.cached;
         if (cfg_.mode == Mode::MWE || cfg_.mode == Mode::HybridMWE)
           res.dispatch.microwalk_e += r.microwalk;  // engine.cpp:328 counts every MWE hop
+        else if (cfg_.mode == Mode::FDM)
+          res.dispatch.fdm += r.microwalk;  // general cubes solved per hop (engine.cpp:312)
         else
           res.dispatch.microwalk += r.microwalk;
         res.mw_steps += r.mw_steps;
@@ -551,6 +551,7 @@ std::vector<WalkEvent> Engine::transitions(const std::vector<Vec3>& points,
       case 0: ++stats.cached; break;
       case 1: ++stats.microwalk; break;
       case 2: ++stats.microwalk_e; break;
+      case 3: ++stats.fdm; break;
       default: break;
     }
   }

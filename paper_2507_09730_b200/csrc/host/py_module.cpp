@@ -434,6 +434,54 @@ PYBIND11_MODULE(_core, m) {
       },
       py::arg("structure_json"), py::arg("begin"), py::arg("count"), py::arg("single") = false);
 
+  m.def(
+      "transitions_json",
+      [](const std::string& text, py::array_t<double, py::array::c_style | py::array::forcecast> pts,
+         py::array_t<uint64_t, py::array::c_style | py::array::forcecast> states,
+         const py::kwargs& kw) {
+        // Engine::transitions (batched Engine::transition, engine.hpp:156-159)
+        int threads = 0;
+        const Config cfg = config_from_kwargs(kw, threads);
+        const Structure s = parse_structure(text, cfg.world_margin);
+        const size_t cnt = states.size();
+        if (pts.size() != 3 * cnt) throw py::value_error("points must be [count][3]");
+        std::vector<Vec3> p(cnt);
+        std::vector<SplitMix64> r(cnt);
+        for (size_t t = 0; t < cnt; ++t) {
+          p[t] = {pts.data()[3 * t], pts.data()[3 * t + 1], pts.data()[3 * t + 2]};
+          r[t].set_state(states.data()[t]);
+        }
+        std::vector<WalkEvent> ev;
+        DispatchStats st;
+        {
+          py::gil_scoped_release release;
+          Engine e(s, cfg, &shared_cache());
+          ev = e.transitions(p, r, st);
+        }
+        py::array_t<int32_t> kind(cnt), cond(cnt);
+        py::array_t<double> point({cnt, static_cast<size_t>(3)});
+        py::array_t<uint64_t> state(cnt);
+        for (size_t t = 0; t < cnt; ++t) {
+          kind.mutable_at(t) = static_cast<int>(ev[t].kind);
+          cond.mutable_at(t) = ev[t].conductor_id;
+          for (int a = 0; a < 3; ++a) point.mutable_at(t, a) = ev[t].point[a];
+          state.mutable_at(t) = r[t].state();
+        }
+        py::dict d;
+        d["kind"] = kind;
+        d["conductor_id"] = cond;
+        d["point"] = point;
+        d["state"] = state;
+        py::dict sd;
+        sd["cached"] = st.cached;
+        sd["microwalk"] = st.microwalk;
+        sd["microwalk_e"] = st.microwalk_e;
+        sd["fdm"] = st.fdm;
+        d["stats"] = sd;
+        return d;
+      },
+      py::arg("structure_json"), py::arg("points"), py::arg("states"));
+
   // single-transit API (microwalk.hpp:70-100) -- test and integration hooks
   m.def(
       "transits_grid",

@@ -126,7 +126,7 @@ struct DSlots {
   uint8_t* nbox;         // [S] conductor boxes among the clipped boxes
   uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class / conductor index
   uint64_t* atlas;       // [S][kAtlasWords] cell atlas of the job (see cell_info)
-  uint8_t* mwkind;       // [S] 0 plain MicroWalk job, 1 expanded (MicroWalk-E)
+  uint8_t* mwkind;       // [S] 0 plain MicroWalk job, 1 expanded (MicroWalk-E), 2 FDM
   uint64_t* room;        // [S] start cell distances (6 bytes, dir order)
   uint64_t* fc;          // [S] start cell + face-neighbour classes
 };
@@ -994,7 +994,7 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   // MicroWalk-E on the expanded cube, falling back to the transit cube when
   // the expanded lattice swallows the start voxel (EngulfedStart)
   int rc = -1;
-  uint8_t kind = 0;
+  uint8_t kind = P.mode == FRW_MODE_FDM ? 2 : 0;  // 2: FDM solve (engine.cpp:311-318)
   if (P.mode == FRW_MODE_MWE || P.mode == FRW_MODE_HYBRID_MWE) {
     kind = 1;
     const double wall = cheb_wall(s.world, L.p);
@@ -1008,7 +1008,7 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     transit_cube(L.p, half, n, ec, &eh);
     rc = compile_mw_job(s, W, slot, ec, eh, n, true, C);
   }
-  if (rc == 0 || kind == 0) rc = compile_mw_job(s, W, slot, c, h, n, false, C);
+  if (rc == 0 || kind != 1) rc = compile_mw_job(s, W, slot, c, h, n, false, C);
   if (rc < 0) {
     W.state[slot] = S_FREE;
     return 1;
@@ -1577,6 +1577,9 @@ __global__ void __launch_bounds__(128)
     e.kind = sl == s.nc ? 2 : 1;
     e.conductor = sl == s.nc ? -1 : sl;
     states[t] = L.rng.s;
+  } else if (W.mwkind[slot] == 2) {  // FDM: solved by k_fdm, events gathered after
+    rc_out[q] = 3;
+    return;
   } else {  // MicroWalk / MicroWalk-E hop on the compiled job
     const int n = P.n;
     const int cap = 1000 * n * n;
@@ -1610,6 +1613,275 @@ __global__ void __launch_bounds__(128)
   }
   rc_out[q] = 1;
   out[t] = e;
+}
+
+// ---- FDM transitions (engine.cpp:311-318) ------------------------------------
+// One CTA per general cube: the voxel classes come from the job's cell atlas
+// (the same voxelisation as build_grid, geometry.cpp:320-349); s_ii of the FD
+// system (sgf.cpp:57-155) is applied matrix-free from palette-pair tables;
+// Jacobi-PCG from zero to |r| < 1e-10 |b| (cap 20 rows) gives the adjoint row
+// of the start node, probs = A_IB^T (eps .* z) with the normalisation check of
+// sgf.cpp:249-253; the CDF is summed in panel order and sampled with one
+// uniform (upper_bound, sgf.cpp:301-308).
+constexpr int kFdmThreads = 1024;
+
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < static_cast<int>(blockDim.x >> 5) ? red[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (l == 0) red[32] = v;
+  }
+  __syncthreads();
+  return red[32];
+}
+constexpr int kFdmMaxN = 32;  // voxel classes held in shared memory
+struct FdmQueue {
+  const int* queue;
+  const unsigned long long* qlen;
+  unsigned long long* qhead;
+  int* out;                     // next-round ACTIVE queue (null: none)
+  unsigned long long* outlen;
+};
+
+__device__ __forceinline__ void fdm_row(const uint8_t* cls, const double* pal, const double* apair,
+                                        const double* spair, int Pn, int n, int v, double* diag,
+                                        double off[6], int nbr[6]) {
+  const int nn = n * n;
+  const int c[3] = {v % n, (v / n) % n, v / nn};
+  const int cv = cls[v];
+  double rs = 0;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const int a = d >> 1;
+    const int st = a == 0 ? 1 : (a == 1 ? n : nn);
+    const bool face = (d & 1) ? c[a] == n - 1 : c[a] == 0;
+    if (face) {  // cube-surface panel: alpha 1, no interior coupling
+      rs += 1.0;
+      off[d] = 0.0;
+      nbr[d] = v;
+      continue;
+    }
+    const int u = (d & 1) ? v + st : v - st;
+    const int q = cls[u] * Pn + cv;
+    rs += apair[q];
+    off[d] = spair[q];
+    nbr[d] = u;
+  }
+  *diag = pal[cv] * rs;
+}
+
+__device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+    b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    red[w] = a;
+    red[32 + w] = b;
+  }
+  __syncthreads();
+  if (w == 0) {
+    a = l < static_cast<int>(blockDim.x >> 5) ? red[l] : 0.0;
+    b = l < static_cast<int>(blockDim.x >> 5) ? red[32 + l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+      b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+    }
+    if (l == 0) {
+      red[64] = a;
+      red[65] = b;
+    }
+  }
+  __syncthreads();
+  return make_double2(red[64], red[65]);
+}
+
+// PSM: the search direction p lives in shared memory (the SpMV reads six
+// neighbours of every node from it); the other Krylov vectors stay in the
+// CTA's L2-resident scratch slab.
+template <bool PSM>
+__global__ void __launch_bounds__(kFdmThreads)
+    k_fdm(DStruct s, DParams P, DSlots W, DCounters* C, FdmQueue Q, double* slab) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  __shared__ double red[66];
+  __shared__ int job_sh;
+  const int n = P.n, m = n * n * n, nn = n * n, Pn = s.P;
+  const int panels = 6 * nn;
+  double* pal = reinterpret_cast<double*>(fsm);
+  double* apair = pal + Pn;
+  double* spair = apair + Pn * Pn;
+  double* psm = spair + Pn * Pn;  // [m] when PSM
+  uint8_t* cls = reinterpret_cast<uint8_t*>(PSM ? psm + m : psm);
+  for (int i = threadIdx.x; i < Pn; i += blockDim.x) pal[i] = __ldg(s.pal + i);
+  __syncthreads();
+  for (int q = threadIdx.x; q < Pn * Pn; q += blockDim.x) {
+    const double ei = pal[q / Pn], ev = pal[q % Pn];
+    apair[q] = ei / (ei + ev);          // sgf.cpp:129
+    spair[q] = -(ev * ei) / (ev + ei);  // sgf.cpp:135-137, bit-symmetric
+  }
+  double* x = slab + static_cast<size_t>(blockIdx.x) * 5 * m;
+  double* r = x + m;
+  double* p = PSM ? psm : r + m;
+  double* t = r + 2 * m;
+  double* dinv = t + m;
+  const int cc = (n - 1) / 2;
+  const int crow = (cc * n + cc) * n + cc;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long j = atomicAdd(Q.qhead, 1ull);
+      job_sh = j < *Q.qlen ? static_cast<int>(j) : -1;
+    }
+    __syncthreads();
+    const int job = job_sh;
+    if (job < 0) break;
+    const int slot = Q.queue[job];
+    // voxel classes of the cube from the job's atlas
+    const uint64_t* A = lane_atlas(W, slot);
+    const uint64_t bm[3] = {A[kAtBm], A[kAtBm + 1], A[kAtBm + 2]};
+    const uint8_t* cb = reinterpret_cast<const uint8_t*>(A + kAtCls);
+    const uint64_t cm = cond_mask(W.nbox[slot]);
+    for (int v = threadIdx.x; v < m; v += blockDim.x) {
+      const int vv[3] = {v % n, (v / n) % n, v / nn};
+      cls[v] = static_cast<uint8_t>(class_of(cb, voxel_mask(A, bm, vv), cm, s.bg));
+    }
+    __syncthreads();
+    // PCG on s_ii z = e_c (Jacobi preconditioner, x0 = 0)
+    double rz_loc = 0;
+    for (int v = threadIdx.x; v < m; v += blockDim.x) {
+      double dg, off[6];
+      int nb[6];
+      fdm_row(cls, pal, apair, spair, Pn, n, v, &dg, off, nb);
+      const double b = v == crow ? 1.0 : 0.0;
+      const double di = 1.0 / dg;
+      dinv[v] = di;
+      x[v] = 0.0;
+      r[v] = b;
+      p[v] = b * di;
+      rz_loc += b * (b * di);
+    }
+    const double thresh = 1e-20;  // (rel_tol 1e-10)^2 |e_c|^2
+    double rz = block_sum(rz_loc, red);
+    double res2 = 1.0;
+    const long cap = 20L * m;
+    long it = 0;
+    while (res2 >= thresh && it < cap) {
+      double pt = 0;
+      for (int v = threadIdx.x; v < m; v += blockDim.x) {
+        double dg, off[6];
+        int nb[6];
+        fdm_row(cls, pal, apair, spair, Pn, n, v, &dg, off, nb);
+        double acc = dg * p[v];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) acc += off[d] * p[nb[d]];
+        t[v] = acc;
+        pt += p[v] * acc;
+      }
+      const double alpha = rz / block_sum(pt, red);
+      double rr = 0, rzn = 0;
+      for (int v = threadIdx.x; v < m; v += blockDim.x) {
+        x[v] += alpha * p[v];
+        const double rv = r[v] - alpha * t[v];
+        r[v] = rv;
+        rr += rv * rv;
+        rzn += rv * (rv * dinv[v]);
+      }
+      const double2 sums = block_sum2(rr, rzn, red);
+      res2 = sums.x;
+      const double rz_new = sums.y;
+      ++it;
+      if (res2 < thresh) break;
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int v = threadIdx.x; v < m; v += blockDim.x) p[v] = r[v] * dinv[v] + beta * p[v];
+      __syncthreads();
+    }
+    // probs = A_IB^T (eps .* z), panel = (face*n + w)*n + u (sgf.hpp:34-36)
+    double sum_loc = 0;
+    for (int q = threadIdx.x; q < panels; q += blockDim.x) {
+      const int face = q / nn, rem = q - face * nn;
+      const int u = rem % n, w = rem / n;
+      const int a = face >> 1;
+      int ci[3];
+      ci[a] = (face & 1) ? n - 1 : 0;
+      ci[a == 0 ? 1 : 0] = u;
+      ci[a == 2 ? 1 : 2] = w;
+      const int v = (ci[2] * n + ci[1]) * n + ci[0];
+      const double pr = pal[cls[v]] * x[v];
+      t[q] = pr;
+      sum_loc += pr;
+    }
+    const double psum = block_sum(sum_loc, red);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bool bad = res2 >= thresh || fabs(psum - 1.0) > 1e-9;
+      // sequential CDF in panel order (sgf.cpp:255-262), min check
+      double run = 0;
+      for (int q = 0; q < panels; ++q) {
+        const double pr = t[q];
+        bad |= pr < -1e-9;
+        run += pr > 0.0 ? pr : 0.0;
+        t[q] = run;
+      }
+      if (bad) {
+        set_err(C, FRW_ESOLVE);
+        W.state[slot] = S_FREE;
+      } else {
+        Rng rng;
+        rng.s = W.rng[slot];
+        const long long wid = W.wid[slot];
+        const double target = uniform(P, wid, rng) * run;
+        int lo = 0, hi = panels;  // upper_bound
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (t[mid] <= target)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        const int panel = lo == panels ? panels - 1 : lo;
+        const double c[3] = {W.cube[4 * slot], W.cube[4 * slot + 1], W.cube[4 * slot + 2]};
+        double pt3[3];
+        panel_center(c, W.cube[4 * slot + 3], n, panel, pt3);
+        W.p[3 * slot] = pt3[0];
+        W.p[3 * slot + 1] = pt3[1];
+        W.p[3 * slot + 2] = pt3[2];
+        W.rng[slot] = rng.s;
+        W.mw[slot] += 1;
+        W.state[slot] = S_ACTIVE;
+        if (Q.out) Q.out[atomicAdd(Q.outlen, 1ull)] = slot;
+      }
+    }
+  }
+}
+
+// events of single FDM transitions solved by k_fdm (slot q holds entry idx[q])
+__global__ void k_fdm_events(DSlots W, const int* slots, const int* idx, int count,
+                             uint64_t* states, DevEvent* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const int slot = slots[k], t = idx[slot];
+  DevEvent e{};
+  e.kind = 0;
+  e.conductor = -1;
+  e.dispatch = 3;
+  e.point[0] = W.p[3 * slot];
+  e.point[1] = W.p[3 * slot + 1];
+  e.point[2] = W.p[3 * slot + 2];
+  out[t] = e;
+  states[t] = W.rng[slot];
+}
+
+size_t fdm_smem_bytes(int n, int Pn, bool psm) {
+  const size_t m = static_cast<size_t>(n) * n * n;
+  return 8 * static_cast<size_t>(Pn) * (1 + 2 * Pn) + (psm ? 8 * m : 0) + m;
 }
 
 // ---- deterministic tallies -------------------------------------------------
@@ -1741,6 +2013,9 @@ struct Engine {
   unsigned long long *pland = nullptr, *pstat = nullptr, *oland = nullptr, *ostat = nullptr;
   size_t red_cap = 0;
   int red_slots = 0;
+  // FDM solve scratch (5 Krylov vectors per persistent CTA)
+  double* fdm_slab = nullptr;
+  size_t fdm_cap = 0;
 };
 
 void free_slots(Engine& E) {
@@ -1801,6 +2076,7 @@ void engine_free(frw_ctx* ctx) {
   cudaFree(E->osq);
   cudaFree(E->oland);
   cudaFree(E->ostat);
+  cudaFree(E->fdm_slab);
   delete E;
   ctx->walk = nullptr;
 }
@@ -1901,6 +2177,32 @@ DParams params_of(const frw_walk_params* prm) {
   return P;
 }
 
+// launches k_fdm over `Q` with enough persistent CTAs; scratch grows on demand
+int launch_fdm(frw_ctx* ctx, Engine& E, const DStruct& s, const DParams& P, DCounters* C,
+               const FdmQueue& Q) {
+  const size_t cap = static_cast<size_t>(ctx->max_smem_optin);
+  const bool psm = fdm_smem_bytes(P.n, s.P, true) <= cap;
+  const size_t smem = fdm_smem_bytes(P.n, s.P, psm);
+  if (smem > cap)
+    return frw_fail(ctx, FRW_EINVAL, "FDM: lattice too large for the shared-memory class field");
+  // one CTA per SM keeps every CTA's five Krylov vectors (5 x 8 n^3 bytes)
+  // L2-resident: 148 x 553 KB at n = 24 against 126 MB of L2
+  const int grid = ctx->sm_count;
+  const size_t need = static_cast<size_t>(grid) * 5 * P.n * P.n * P.n;
+  if (E.fdm_cap < need) {
+    cudaFree(E.fdm_slab);
+    E.fdm_slab = dalloc<double>(need);
+    E.fdm_cap = E.fdm_slab ? need : 0;
+    if (!E.fdm_slab) return frw_fail(ctx, FRW_ENOMEM, "FDM: scratch allocation failed");
+  }
+  auto kern = psm ? k_fdm<true> : k_fdm<false>;
+  FRW_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+  kern<<<grid, kFdmThreads, smem, ctx->stream>>>(s, P, E.W, C, Q, E.fdm_slab);
+  FRW_CUDA(ctx, cudaGetLastError());
+  return FRW_OK;
+}
+
 // Solves the distinct keys of `nmiss` recorded table misses (device solver,
 // or the caller's callback) and inserts them; *added = new entries.
 int resolve_misses(frw_ctx* ctx, Engine& E, int n, unsigned long long nmiss, frw_miss_fn miss,
@@ -1998,16 +2300,16 @@ namespace {
 // Shared driver of frw_first_transitions / frw_transitions: uploads the
 // inputs, runs `launch` over the pending entries, resolves table misses and
 // re-runs the entries that missed (they drew nothing), then copies back.
-template <class Out, class Launch>
+template <class Out, class Launch, class Post>
 int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double* pts,
                const int32_t* axsign, uint64_t* states, frw_miss_fn miss, void* user, Out* out,
-               Launch launch) {
+               Launch launch, Post post) {
   Engine& E = *engine_of(ctx);
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "transitions: no structure uploaded");
   if (!prm || prm->grid_n < 2 || prm->grid_n > NMAX)
     return frw_fail(ctx, FRW_EINVAL, "transitions: grid_n must lie in [2, 64]");
-  if (prm->mode == FRW_MODE_FDM)
-    return frw_fail(ctx, FRW_EINVAL, "transitions: FDM transitions are not on the device yet");
+  if (prm->mode == FRW_MODE_FDM && prm->grid_n > kFdmMaxN)
+    return frw_fail(ctx, FRW_EINVAL, "transitions: FDM mode supports grid_n <= 32");
   if (count < 0 || (count > 0 && (!pts || !states || !out)))
     return frw_fail(ctx, FRW_EINVAL, "transitions: bad arguments");
   if (E.sgf.n && E.sgf.n != prm->grid_n)
@@ -2085,6 +2387,8 @@ int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double
                               "transitions: point outside the world or inside a conductor");
       break;
     }
+    status = post(s, P, E, d_idx, np, rc, d_st, d_out);
+    if (status) break;
     std::vector<int> next;
     for (int q = 0; q < np; ++q)
       if (rc[q] == 2) next.push_back(pend[q]);
@@ -2337,7 +2641,9 @@ int frw_first_transitions(frw_ctx* ctx, const frw_walk_params* prm, int count,
           const int32_t* ax, uint64_t* st, const int* idx, int np, int* rc, DevFirst* o) {
         k_first_single<<<(np + 127) / 128, 128, 0, ctx->stream>>>(s, T, P, E.W, E.d_cnt, E.M, pts,
                                                                   ax, st, idx, np, rc, o);
-      });
+      },
+      [](const DStruct&, const DParams&, Engine&, const int*, int, const std::vector<int>&,
+         uint64_t*, DevFirst*) { return FRW_OK; });
 }
 
 int frw_transitions(frw_ctx* ctx, const frw_walk_params* prm, int count, const double* points,
@@ -2349,6 +2655,41 @@ int frw_transitions(frw_ctx* ctx, const frw_walk_params* prm, int count, const d
           const int32_t*, uint64_t* st, const int* idx, int np, int* rc, DevEvent* o) {
         k_transition_single<<<(np + 127) / 128, 128, 0, ctx->stream>>>(
             s, T, P, E.W, E.recs, E.d_cnt, E.M, pts, st, idx, np, rc, o);
+      },
+      [&](const DStruct& s, const DParams& P, Engine& E, const int* d_idx, int np,
+          const std::vector<int>& rc, uint64_t* d_st, DevEvent* d_out) -> int {
+        // FDM jobs (rc 3): slot q holds the compiled cube of entry idx[q]
+        std::vector<int> slots;
+        for (int q = 0; q < np; ++q)
+          if (rc[q] == 3) slots.push_back(q);
+        if (slots.empty()) return FRW_OK;
+        const int nf = static_cast<int>(slots.size());
+        int* d_slots = dalloc<int>(nf);
+        unsigned long long* d_q = dalloc<unsigned long long>(2);
+        if (!d_slots || !d_q) {
+          cudaFree(d_slots);
+          cudaFree(d_q);
+          return frw_fail(ctx, FRW_ENOMEM, "transitions: FDM queue allocation failed");
+        }
+        const unsigned long long qh[2] = {static_cast<unsigned long long>(nf), 0ull};
+        cudaMemcpyAsync(d_slots, slots.data(), 4 * size_t(nf), cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(d_q, qh, sizeof qh, cudaMemcpyHostToDevice, ctx->stream);
+        const FdmQueue Q{d_slots, d_q, d_q + 1, nullptr, nullptr};
+        int st = launch_fdm(ctx, E, s, P, E.d_cnt, Q);
+        if (st == FRW_OK) {
+          k_fdm_events<<<(nf + 127) / 128, 128, 0, ctx->stream>>>(E.W, d_slots, d_idx, nf, d_st,
+                                                                  d_out);
+          DCounters c;
+          if (cudaMemcpyAsync(&c, E.d_cnt, sizeof c, cudaMemcpyDeviceToHost, ctx->stream) !=
+                  cudaSuccess ||
+              cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            st = frw_fail(ctx, FRW_ECUDA, "transitions: FDM solve failed");
+          else if (c.err)
+            st = frw_fail(ctx, FRW_ESOLVE, "transition cube solve failed normalization check");
+        }
+        cudaFree(d_slots);
+        cudaFree(d_q);
+        return st;
       });
 }
 
@@ -2360,9 +2701,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "run_walks: no structure uploaded");
   if (prm->grid_n < 2 || prm->grid_n > NMAX)
     return frw_fail(ctx, FRW_EINVAL, "run_walks: grid_n must lie in [2, 64]");
-  if (prm->mode == FRW_MODE_FDM)
-    return frw_fail(ctx, FRW_EINVAL,
-                    "run_walks: FDM transitions (a PCG solve per hop) are not on the device yet");
+  if (prm->mode == FRW_MODE_FDM && prm->grid_n > kFdmMaxN)
+    return frw_fail(ctx, FRW_EINVAL, "run_walks: FDM mode supports grid_n <= 32");
   if (prm->mode < FRW_MODE_FDM || prm->mode > FRW_MODE_HYBRID_MWE)
     return frw_fail(ctx, FRW_EINVAL, "run_walks: unknown mode");
   if (!(prm->expansion >= 1.0)) return frw_fail(ctx, FRW_EINVAL, "run_walks: expansion < 1");
@@ -2439,7 +2779,13 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in,
                                                    E.queue);
       cudaEventRecord(m0, ctx->stream);
-      if (P.rng == FRW_RNG_PHILOX)
+      if (P.mode == FRW_MODE_FDM) {
+        const FdmQueue Q{E.queue, &E.d_cnt->qlen, &E.d_cnt->qhead, aq_out, &E.d_cnt->a2len};
+        if (int rc = launch_fdm(ctx, E, s, P, E.d_cnt, Q)) {
+          status = rc;
+          break;
+        }
+      } else if (P.rng == FRW_RNG_PHILOX)
         k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs, E.d_cnt,
                                                                E.queue, aq_out);
       else
@@ -2506,7 +2852,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       break;
     }
     // few walks left: run them to completion in one launch
-    if (all_spawned && c.a2len <= tail_threshold) tail = true;
+    if (all_spawned && c.a2len <= tail_threshold && P.mode != FRW_MODE_FDM) tail = true;
     k_round<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
   }
   if (status == FRW_OK) {
@@ -2567,10 +2913,11 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     out->resampled = st[1];
     for (int b = 0; b < 4; ++b) out->first[b] = st[2 + b];
     const bool mwe = P.mode == FRW_MODE_MWE || P.mode == FRW_MODE_HYBRID_MWE;
+    const bool fdm = P.mode == FRW_MODE_FDM;
     out->sub[0] = st[6];
-    out->sub[1] = mwe ? 0 : st[7];
+    out->sub[1] = mwe || fdm ? 0 : st[7];
     out->sub[2] = mwe ? st[7] : 0;  // lattice hops count as microwalk_e in MWE mode
-    out->sub[3] = 0;
+    out->sub[3] = fdm ? st[7] : 0;  // general cubes solved by FDM
     out->mw_steps = st[8];
     out->cache_misses = misses_total;
     out->cache_hits = 0;

@@ -65,13 +65,6 @@ def test_parse_and_validation_errors():
         frwcap.extract_json(json.dumps(bad), mode="HYBRID-MW")
 
 
-def test_fdm_mode_not_silently_substituted():
-    # FDM transitions are not on the device yet: a clear error, never a
-    # quiet switch to another mode
-    with pytest.raises(ValueError, match="FDM"):
-        frwcap.extract_json(json.dumps(c3_structure()), mode="FDM")
-
-
 def test_no_cpu_fallback():
     import torch
     if torch.cuda.is_available():
