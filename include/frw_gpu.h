@@ -275,6 +275,14 @@ typedef struct {
   double weight;   /* farads                                                 */
   double point[3];
 } frw_first;
+/* The reference's full-domain finite-volume capacitance solver
+ * (reference_capacitance, oracle.cpp:92-213; validation machinery): R^3
+ * voxels over the world box, one CG per terminal.  cap: [n_cond][n_cond]
+ * row-major farads, cap[i*n + t] = charge on conductor i when t is at 1 V;
+ * residual: worst relative CG residual.  16 <= R, R^3 <= 3.5e6. */
+int frw_reference_capacitance(frw_ctx *ctx, const frw_structure *s, int resolution,
+                              double *cap, double *residual);
+
 int frw_first_transitions(frw_ctx *ctx, const frw_walk_params *prm, int count,
                           const double *gpoints, const int32_t *axis_sign,
                           uint64_t *states, frw_miss_fn miss, void *user,

@@ -418,6 +418,16 @@ class Engine {
 CapacitanceResult extract(const Structure& s, const Config& cfg, int threads = 0,
                           StratifiedSgfCache* cache = nullptr);
 
+// ---- full-domain FV reference (oracle.hpp:25-31), on the device ----------------
+struct ReferenceSolution {
+  int resolution = 0;
+  std::vector<int> terminal_ids;    // structure declaration order
+  std::vector<double> capacitance;  // [n][n] row-major, farads; column t = excitation of t
+  double residual = 0;              // worst relative CG residual
+  double at(int i, int t) const { return capacitance[i * terminal_ids.size() + t]; }
+};
+ReferenceSolution reference_capacitance(const Structure& s, int resolution, int device = 0);
+
 // ---- MicroWalk transits (microwalk.hpp:18-100) -------------------------------
 struct Exit {
   enum class Kind : uint8_t { Surface, Conductor };

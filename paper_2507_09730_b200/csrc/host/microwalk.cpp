@@ -437,4 +437,39 @@ TransitBatch microwalk_transit_batch(int n, const std::vector<double>& eps, cons
   return out;
 }
 
+ReferenceSolution reference_capacitance(const Structure& s, int resolution, int device) {
+  frw_ctx* ctx = Device::get(device).ctx();
+  std::vector<int32_t> ids;
+  std::vector<double> cb, db, de;
+  for (const auto& c : s.conductors) {
+    ids.push_back(c.id);
+    for (int a = 0; a < 3; ++a) cb.push_back(c.box.lo[a]);
+    for (int a = 0; a < 3; ++a) cb.push_back(c.box.hi[a]);
+  }
+  for (const auto& d : s.dielectrics) {
+    for (int a = 0; a < 3; ++a) db.push_back(d.box.lo[a]);
+    for (int a = 0; a < 3; ++a) db.push_back(d.box.hi[a]);
+    de.push_back(d.eps_r);
+  }
+  frw_structure fs{};
+  fs.n_cond = static_cast<int32_t>(ids.size());
+  fs.cond_id = ids.data();
+  fs.cond_box = cb.data();
+  fs.n_diel = static_cast<int32_t>(de.size());
+  fs.diel_box = db.data();
+  fs.diel_eps = de.data();
+  fs.background_eps = s.background_eps;
+  for (int a = 0; a < 3; ++a) {
+    fs.world[a] = s.world.lo[a];
+    fs.world[3 + a] = s.world.hi[a];
+  }
+  ReferenceSolution r;
+  r.resolution = resolution;
+  r.terminal_ids.assign(ids.begin(), ids.end());
+  r.capacitance.assign(ids.size() * ids.size(), 0.0);
+  throw_status(ctx, frw_reference_capacitance(ctx, &fs, resolution, r.capacitance.data(),
+                                              &r.residual));
+  return r;
+}
+
 }  // namespace frwcap

@@ -192,10 +192,28 @@ PYBIND11_MODULE(_core, m) {
 
   m.def(
       "reference_capacitance_file",
-      [](const std::string&, int, double) -> py::dict {
-        throw std::runtime_error(
-            "reference_capacitance_file (full-domain FV oracle, oracle.cpp:92-213) is validation "
-            "machinery outside the B200 hot path; it is not part of this build");
+      [](const std::string& path, int resolution, double world_margin) {
+        const Structure s = parse_structure_file(path, world_margin);
+        ReferenceSolution ref;
+        {
+          py::gil_scoped_release release;
+          ref = reference_capacitance(s, resolution);
+        }
+        // py_module.cpp:110-125
+        py::list ids;
+        for (int id : ref.terminal_ids) ids.append(id);
+        py::list rows;
+        const int T = static_cast<int>(ref.terminal_ids.size());
+        for (int i = 0; i < T; ++i) {
+          py::list row;
+          for (int j = 0; j < T; ++j) row.append(ref.at(i, j));
+          rows.append(row);
+        }
+        py::dict d;
+        d["terminal_ids"] = ids;
+        d["capacitance_farads"] = rows;
+        d["residual"] = ref.residual;
+        return d;
       },
       py::arg("path"), py::arg("resolution") = 48, py::arg("world_margin") = 5.0);
 
