@@ -275,6 +275,14 @@ typedef struct {
   double weight;   /* farads                                                 */
   double point[3];
 } frw_first;
+/* solve_sgf + expected_steps of `count` unmasked materialised grids
+ * (assemble_system / solve_sgf / expected_steps, sgf.cpp:57-299): eps
+ * [count][n^3] x-fastest, cube half width (sets the kernels' pitch).
+ * probs [count][6n^2], kernels [count][3][6n^2], steps [count] (E[tau] at
+ * start_node); any output may be NULL.  Jacobi-PCG, tol 1e-10, cap 20 rows. */
+int frw_grid_sgf_solve(frw_ctx *ctx, int n, int count, const double *eps,
+                       double half_width, double *probs, double *kernels, double *steps);
+
 /* The reference's full-domain finite-volume capacitance solver
  * (reference_capacitance, oracle.cpp:92-213; validation machinery): R^3
  * voxels over the world box, one CG per terminal.  cap: [n_cond][n_cond]

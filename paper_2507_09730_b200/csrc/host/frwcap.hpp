@@ -9,6 +9,7 @@
 #include <array>
 #include <cstdint>
 #include <functional>
+#include <iosfwd>
 #include <memory>
 #include <mutex>
 #include <optional>
@@ -237,11 +238,6 @@ ProfileKey profile_key(int n, int axis, const std::vector<double>& layers);
 
 // canonical unit-pitch solve of a key (sgf_cache.cpp:78-131 + sgf.cpp:231-290)
 DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels = true);
-// surface law of an arbitrary unmasked n^3 grid (probs only)
-DiscreteSGF solve_grid(int n, const std::vector<double>& eps, double half_width,
-                       bool with_kernels = false);
-// e_c^T A_II^{-1} d (sgf.cpp:292-299)
-double expected_steps(int n, const std::vector<double>& eps);
 
 class StratifiedSgfCache {
  public:
@@ -417,6 +413,18 @@ class Engine {
 
 CapacitanceResult extract(const Structure& s, const Config& cfg, int threads = 0,
                           StratifiedSgfCache* cache = nullptr);
+
+// ---- surface Green's function of a materialised (unmasked) grid, on the device
+// (assemble_system + solve_sgf + expected_steps, sgf.cpp:57-299)
+DiscreteSGF solve_sgf(const DielectricGrid& g, bool with_kernels = true, int device = 0);
+double expected_steps(const DielectricGrid& g, int device = 0);
+// oracle.cpp:300-339 test lattices: exponential(mean 10) permittivities
+DielectricGrid random_voxel_grid(int n, SplitMix64& rng);
+DielectricGrid random_block_grid(int n, int blocks, SplitMix64& rng);
+
+// the reference CLI (cli.cpp:545-620): extract, validate-sgf, bench-scaling,
+// oracle-compare; JSON report on `out`, summary on `err`; exit codes 0/1/2
+int run_cli(const std::vector<std::string>& args, std::ostream& out, std::ostream& err);
 
 // ---- full-domain FV reference (oracle.hpp:25-31), on the device ----------------
 struct ReferenceSolution {

@@ -472,4 +472,74 @@ ReferenceSolution reference_capacitance(const Structure& s, int resolution, int 
   return r;
 }
 
+DiscreteSGF solve_sgf(const DielectricGrid& g, bool with_kernels, int device) {
+  if (g.has_mask())
+    throw std::invalid_argument("solve_sgf: masked grids are not supported on the device");
+  frw_ctx* ctx = Device::get(device).ctx();
+  const size_t P = 6ull * g.n * g.n;
+  DiscreteSGF out;
+  out.n = g.n;
+  out.pitch = g.pitch();
+  out.probs.resize(P);
+  std::vector<double> ker(with_kernels ? 3 * P : 0);
+  throw_status(ctx, frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width,
+                                       out.probs.data(), with_kernels ? ker.data() : nullptr,
+                                       nullptr));
+  out.cdf.resize(P);
+  double run = 0;
+  for (size_t b = 0; b < P; ++b) out.cdf[b] = run += out.probs[b];
+  if (with_kernels)
+    for (int a = 0; a < 3; ++a) out.grad_kernels[a].assign(ker.begin() + a * P, ker.begin() + (a + 1) * P);
+  return out;
+}
+
+double expected_steps(const DielectricGrid& g, int device) {
+  if (g.has_mask())
+    throw std::invalid_argument("expected_steps: masked grids are not supported on the device");
+  frw_ctx* ctx = Device::get(device).ctx();
+  double st = 0;
+  throw_status(ctx, frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width, nullptr,
+                                       nullptr, &st));
+  return st;
+}
+
+namespace {
+double exp_eps(SplitMix64& rng) {  // oracle.cpp:300-303
+  return std::max(-10.0 * std::log1p(-rng.uniform()), 1e-9);
+}
+DielectricGrid blank_grid(int n) {  // oracle.cpp:305-311
+  DielectricGrid g;
+  g.n = n;
+  g.cube = {{0, 0, 0}, n / 2.0};
+  g.eps.assign(static_cast<size_t>(n) * n * n, 1.0);
+  return g;
+}
+}  // namespace
+
+DielectricGrid random_voxel_grid(int n, SplitMix64& rng) {
+  DielectricGrid g = blank_grid(n);
+  for (auto& e : g.eps) e = exp_eps(rng);
+  classify_grid(g);
+  return g;
+}
+
+DielectricGrid random_block_grid(int n, int blocks, SplitMix64& rng) {
+  DielectricGrid g = blank_grid(n);
+  for (int b = 0; b < blocks; ++b) {
+    int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      const int x = static_cast<int>(rng.uniform() * n);
+      const int y = static_cast<int>(rng.uniform() * n);
+      lo[a] = std::min(std::min(x, y), n - 1);
+      hi[a] = std::min(std::max(x, y), n - 1);
+    }
+    const double e = exp_eps(rng);
+    for (int k = lo[2]; k <= hi[2]; ++k)
+      for (int j = lo[1]; j <= hi[1]; ++j)
+        for (int i = lo[0]; i <= hi[0]; ++i) g.eps[g.index(i, j, k)] = e;
+  }
+  classify_grid(g);
+  return g;
+}
+
 }  // namespace frwcap

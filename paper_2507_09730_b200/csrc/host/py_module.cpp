@@ -144,28 +144,6 @@ py::dict extract_structure(const Structure& s, const Config& cfg, int threads) {
   return result_to_dict(res);
 }
 
-// random_voxel_grid (oracle.cpp:315-320) on SplitMix64 (rng.hpp:12-40)
-struct Sm64 {
-  uint64_t s;
-  static uint64_t mix(uint64_t z) {
-    z += 0x9E3779B97F4A7C15ULL;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
-  }
-  Sm64(uint64_t seed, uint64_t stream) : s(mix(mix(seed) + (stream + 1) * 0x9E3779B97F4A7C15ULL)) {}
-  double uniform() {
-    s += 0x9E3779B97F4A7C15ULL;
-    return static_cast<double>(mix(s) >> 11) * 0x1.0p-53;
-  }
-};
-
-std::vector<double> random_voxel_grid(int n, Sm64& r) {
-  std::vector<double> e(static_cast<size_t>(n) * n * n);
-  for (double& v : e) v = std::max(-10.0 * std::log1p(-r.uniform()), 1e-9);
-  return e;
-}
-
 }  // namespace
 
 PYBIND11_MODULE(_core, m) {
@@ -237,11 +215,12 @@ PYBIND11_MODULE(_core, m) {
       "transit_tv",
       [](int n, uint64_t grid_seed, long samples, uint64_t sample_seed) {
         py::gil_scoped_release release;
-        Sm64 g(grid_seed, 0);
-        const auto eps = random_voxel_grid(n, g);
-        const DiscreteSGF sgf = solve_grid(n, eps, n / 2.0, false);
-        const TransitBatch b = microwalk_transit_batch(n, eps, {0, 0, 0}, n / 2.0, sample_seed, 0,
-                                                       samples, RngMode::Philox, false);
+        // py_module.cpp:176-193: random voxel grid, exact solve, transits
+        SplitMix64 g(grid_seed, 0);
+        const DielectricGrid grid = random_voxel_grid(n, g);
+        const DiscreteSGF sgf = solve_sgf(grid, false);
+        const TransitBatch b = microwalk_transit_batch(n, grid.eps, {0, 0, 0}, n / 2.0, sample_seed,
+                                                       0, samples, RngMode::Philox, false);
         double tv = 0;
         for (size_t q = 0; q < sgf.probs.size(); ++q)
           tv += std::fabs(static_cast<double>(b.hist[q]) / samples - sgf.probs[q]);
@@ -253,58 +232,23 @@ PYBIND11_MODULE(_core, m) {
       "expected_steps_uniform",
       [](int n) {
         py::gil_scoped_release release;
-        return expected_steps(n, std::vector<double>(static_cast<size_t>(n) * n * n, 1.0));
+        DielectricGrid g;
+        g.n = n;
+        g.cube = {{0, 0, 0}, n / 2.0};
+        g.eps.assign(static_cast<size_t>(n) * n * n, 1.0);
+        return expected_steps(g);
       },
       py::arg("n"));
 
-  // minimal in-process CLI: the `extract` subcommand of cli.cpp:165-213
+  // the reference CLI in-process (cli.hpp run_cli): (rc, stdout, stderr)
   m.def(
       "run_cli",
       [](const std::vector<std::string>& args) -> py::tuple {
         std::ostringstream out, err;
-        int rc = 0;
-        try {
-          if (args.empty() || args[0] != "extract") {
-            err << "error: only the 'extract' subcommand is available in the B200 build\n";
-            return py::make_tuple(2, out.str(), err.str());
-          }
-          std::string path;
-          Config cfg;
-          int threads = 0;
-          for (size_t i = 1; i < args.size(); ++i) {
-            const std::string& a = args[i];
-            auto val = [&]() -> std::string {
-              if (i + 1 >= args.size()) throw std::invalid_argument(a + " needs a value");
-              return args[++i];
-            };
-            if (a == "--structure") path = val();
-            else if (a == "--grid-n") cfg.grid_n = std::stoi(val());
-            else if (a == "--mode") cfg.mode = parse_mode(val());
-            else if (a == "--tol") cfg.rel_std_tol = std::stod(val());
-            else if (a == "--min-walks") cfg.min_walks = std::stol(val());
-            else if (a == "--max-walks") cfg.max_walks = std::stol(val());
-            else if (a == "--batch") cfg.batch = std::stoi(val());
-            else if (a == "--seed") cfg.seed = std::stoull(val());
-            else if (a == "--threads") threads = std::stoi(val());
-            else throw std::invalid_argument("unknown option " + a);
-          }
-          if (path.empty()) throw std::invalid_argument("--structure is required");
-          cfg.validate();
-          CapacitanceResult r;
-          {
-            py::gil_scoped_release release;
-            r = extract(parse_structure_file(path, cfg.world_margin), cfg, threads, &shared_cache());
-          }
-          py::dict rep;
-          rep["schema_version"] = 1;
-          rep["command"] = "extract";
-          rep["argv"] = args;
-          rep["results"] = result_to_dict(r);
-          out << py::module_::import("json").attr("dumps")(rep, py::arg("indent") = 2).cast<std::string>()
-              << "\n";
-        } catch (const std::exception& e) {
-          err << "error: " << e.what() << "\n";
-          rc = 2;
+        int rc;
+        {
+          py::gil_scoped_release release;
+          rc = run_cli(args, out, err);
         }
         return py::make_tuple(rc, out.str(), err.str());
       },

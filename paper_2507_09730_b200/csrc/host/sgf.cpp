@@ -221,13 +221,6 @@ DiscreteSGF solve_stencil(const Stencil& S, double half_width, bool with_kernels
 
 }  // namespace
 
-DiscreteSGF solve_grid(int n, const std::vector<double>& eps, double half_width,
-                       bool with_kernels) {
-  if (n < 1 || eps.size() != size_t(n) * n * n)
-    throw std::invalid_argument("solve_grid: need n^3 permittivities");
-  return solve_stencil(Stencil(n, eps), half_width, with_kernels);
-}
-
 DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels) {
   const int n = key.n;
   if (static_cast<int>(key.layers.size()) != n)
@@ -243,13 +236,6 @@ DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels) {
   return solve_stencil(Stencil(n, eps), n / 2.0, with_kernels);
 }
 
-double expected_steps(int n, const std::vector<double>& eps) {
-  Stencil S(n, eps);
-  std::vector<double> rhs(S.m);
-  for (size_t v = 0; v < S.m; ++v) rhs[v] = S.eps[v] * S.rowsum[v];
-  const int c = (n - 1) / 2;
-  return S.solve(rhs)[(size_t(c) * n + c) * n + c];
-}
 
 // ---- cache -------------------------------------------------------------------
 

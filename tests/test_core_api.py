@@ -33,7 +33,10 @@ def test_analytic_plate_capacitance():
     assert math.isclose(c2, 8.8541878128e-12 * 1e-12 / (25e-9 + 6.25e-9), rel_tol=1e-12)
 
 
-def test_expected_steps_uniform_host_solver():
+@pytest.mark.gpu
+def test_expected_steps_uniform_device_solver():
+    """E[tau]/N^2 = 0.3373 +- 5% at n = 24 (test_sgf.cpp:300-304), solved on
+    the device (frw_grid_sgf_solve)"""
     s4, s8 = frwcap.expected_steps_uniform(4), frwcap.expected_steps_uniform(8)
     assert 2.5 < s8 / s4 < 6.0
     assert abs(frwcap.expected_steps_uniform(24) / 576 - 0.3373) <= 0.05 * 0.3373
