@@ -232,14 +232,12 @@ namespace {
 struct MissCtx {
   frw_ctx* ctx;
   StratifiedSgfCache* cache;
-  bool host_solver;
   std::string err;
 };
 
 // Table misses: keys already in the host cache (e.g. loaded from an SGF1
-// file) are uploaded; the rest are solved -- on the device by default
-// (frw_sgf_solve), on host threads with host_sgf_solver -- stored in the
-// host cache (persistable) and uploaded.
+// file) are uploaded; the rest are solved on the device (frw_sgf_solve),
+// stored in the host cache (persistable) and uploaded.
 int miss_cb(void* user, int n, int count, const int* axes, const double* layers) {
   auto* m = static_cast<MissCtx*>(user);
   try {
@@ -251,9 +249,7 @@ int miss_cb(void* user, int n, int count, const int* axes, const double* layers)
                             layers + static_cast<size_t>(q + 1) * n);
       if (!m->cache->find(keys[q])) todo.push_back(keys[q]);
     }
-    if (m->host_solver) {
-      m->cache->solve_many(todo);
-    } else if (!todo.empty()) {
+    if (!todo.empty()) {
       const size_t P = 6ull * n * n;
       std::vector<int> ax;
       std::vector<double> lay;
@@ -296,7 +292,7 @@ std::vector<frw_walk_record> Engine::run_walks(uint64_t begin, int64_t count) {
   t.sum = sum.data();
   t.sumsq = sq.data();
   t.landed = landed.data();
-  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
+  MissCtx mc{ctx_, cache_, {}};
   const frw_walk_params p = params();
   const int rc = frw_run_walks(ctx_, &p, master_slot_, begin, count, miss_cb, &mc, &t, rec.data());
   if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
@@ -353,7 +349,7 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   };
 
   const frw_walk_params p = params();
-  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
+  MissCtx mc{ctx_, cache_, {}};
   std::vector<frw_walk_record> rec;
   std::vector<double> ts(nslots), tq(nslots);
   std::vector<uint64_t> tl(nslots);
@@ -482,7 +478,7 @@ std::vector<std::optional<FirstTransition>> Engine::first_transitions(
     st[t] = rngs[t].state();
   }
   std::vector<frw_first> out(count);
-  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
+  MissCtx mc{ctx_, cache_, {}};
   const frw_walk_params p = params();
   const int rc = frw_first_transitions(ctx_, &p, count, pts.data(), ax.data(), st.data(), miss_cb,
                                        &mc, out.data());
@@ -528,7 +524,7 @@ std::vector<WalkEvent> Engine::transitions(const std::vector<Vec3>& points,
     st[t] = rngs[t].state();
   }
   std::vector<frw_event> out(count);
-  MissCtx mc{ctx_, cache_, cfg_.host_sgf_solver, {}};
+  MissCtx mc{ctx_, cache_, {}};
   const frw_walk_params p = params();
   const int rc = frw_transitions(ctx_, &p, count, pts.data(), st.data(), miss_cb, &mc, out.data());
   if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);

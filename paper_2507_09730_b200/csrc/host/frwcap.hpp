@@ -237,11 +237,12 @@ struct ProfileKeyHash {
 ProfileKey profile_key(int n, int axis, const std::vector<double>& layers);
 
 // canonical unit-pitch solve of a key (sgf_cache.cpp:78-131 + sgf.cpp:231-290)
-DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels = true);
+DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels = true, int device = 0);
 
 class StratifiedSgfCache {
  public:
   explicit StratifiedSgfCache(size_t capacity = 0) : capacity_(capacity) {}
+  void set_device(int device) { device_ = device; }
   std::shared_ptr<const DiscreteSGF> get(const ProfileKey& key);
   std::shared_ptr<const DiscreteSGF> find(const ProfileKey& key) const;
   // solves the missing keys in parallel (host threads)
@@ -263,6 +264,7 @@ class StratifiedSgfCache {
 
  private:
   size_t capacity_;
+  int device_ = 0;
   mutable std::mutex mu_;
   std::unordered_map<ProfileKey, std::shared_ptr<const DiscreteSGF>, ProfileKeyHash> map_;
   uint64_t hits_ = 0, misses_ = 0;
@@ -293,7 +295,6 @@ struct Config {
   bool all_couplings_rule = false;  // stop when every coupling meets tol (C4)
   long device_batch = 1 << 20;      // walks per device launch sequence
   int device = 0;
-  bool host_sgf_solver = false;     // solve table misses on the host instead
 
   void validate() const;
 };

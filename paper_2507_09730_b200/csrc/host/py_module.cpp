@@ -45,12 +45,6 @@ Config config_from_kwargs(const py::kwargs& kw, int& threads) {
     } else if (key == "all_couplings") cfg.all_couplings_rule = py::cast<bool>(v);
     else if (key == "device_batch") cfg.device_batch = py::cast<long>(v);
     else if (key == "device") cfg.device = py::cast<int>(v);
-    else if (key == "sgf_solver") {
-      const std::string r = py::cast<std::string>(v);
-      if (r == "device") cfg.host_sgf_solver = false;
-      else if (r == "host") cfg.host_sgf_solver = true;
-      else throw py::value_error("sgf_solver must be 'device' or 'host'");
-    }
     else throw py::value_error("unknown option: " + key);
   }
   cfg.validate();

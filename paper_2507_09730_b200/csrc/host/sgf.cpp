@@ -1,8 +1,9 @@
-// sgf.cpp -- stratified-SGF miss solver and cache of the B200 build.
+// sgf.cpp -- stratified-SGF cache of the B200 build.
 //
-// The walk-time lookup and CDF sampling run on the device (walk.cu); this
-// file solves the canonical grid of a missing key on the host and keeps
-// the host copy of the table.  Algorithm restated from the reference:
+// The walk-time lookup and CDF sampling run on the device (walk.cu); so do
+// the canonical solves of missing keys (frw_sgf_solve, sgf_solve.cu).  This
+// file keeps the host copy of the table (keys, SGF1 files).  The solver
+// restates the reference:
 //   FD system       proj/src/sgf.cpp:57-155 (alpha = e_i/(e_i+e_v), absorbing
 //                   faces alpha = 1, bit-symmetric s_ii = diag(eps) A_II)
 //   adjoint solve   sgf.cpp:162-290 (s_ii z = b, y = eps .* z, probs = A_IB^T y;
@@ -60,182 +61,50 @@ ProfileKey profile_key(int n, int axis, const std::vector<double>& layers) {
   return k;
 }
 
+
+// canonical unit-pitch solves of stratified keys (sgf_cache.cpp:78-131) on the
+// device solver (frw_sgf_solve, sgf_solve.cu)
 namespace {
-
-// matrix-free s_ii of an unmasked n^3 lattice
-struct Stencil {
-  int n = 0;
-  size_t m = 0;
-  std::vector<double> eps, diag, rowsum;
-  std::vector<std::array<double, 6>> off;  // 0 where the face absorbs
-
-  Stencil(int n_, const std::vector<double>& e) : n(n_), m(size_t(n_) * n_ * n_), eps(e) {
-    diag.resize(m);
-    rowsum.resize(m);
-    off.resize(m);
-    for (int k = 0; k < n; ++k)
-      for (int j = 0; j < n; ++j)
-        for (int i = 0; i < n; ++i) {
-          const size_t v = (size_t(k) * n + j) * n + i;
-          const double ev = eps[v];
-          double rs = 0;
-          const int c[3] = {i, j, k};
-          for (int d = 0; d < 6; ++d) {
-            const int a = d >> 1, s = (d & 1) ? 1 : -1;
-            int nb[3] = {c[0], c[1], c[2]};
-            nb[a] += s;
-            off[v][d] = 0;
-            if (nb[a] < 0 || nb[a] >= n) {
-              rs += 1.0;
-              continue;
-            }
-            const double ei = eps[(size_t(nb[2]) * n + nb[1]) * n + nb[0]];
-            off[v][d] = -(ev * ei) / (ev + ei);
-            rs += ei / (ei + ev);
-          }
-          rowsum[v] = rs;
-          diag[v] = ev * rs;
-        }
+std::vector<std::shared_ptr<DiscreteSGF>> solve_keys(const std::vector<ProfileKey>& keys,
+                                                     bool with_kernels, int device) {
+  std::vector<std::shared_ptr<DiscreteSGF>> out;
+  if (keys.empty()) return out;
+  const int n = keys[0].n;
+  std::vector<int> axes;
+  std::vector<double> layers;
+  for (const auto& k : keys) {
+    if (k.n != n || static_cast<int>(k.layers.size()) != n)
+      throw std::invalid_argument("canonical_grid: malformed key");
+    axes.push_back(k.axis);
+    layers.insert(layers.end(), k.layers.begin(), k.layers.end());
   }
-
-  void apply(const std::vector<double>& x, std::vector<double>& y) const {
-    const long st[6] = {-1, 1, -long(n), long(n), -long(n) * n, long(n) * n};
-    for (size_t v = 0; v < m; ++v) {
-      double acc = diag[v] * x[v];
-      for (int d = 0; d < 6; ++d)
-        if (off[v][d] != 0.0) acc += off[v][d] * x[v + st[d]];
-      y[v] = acc;
-    }
-  }
-
-  // Jacobi-PCG from zero; converged when |r|^2 < tol^2 |b|^2
-  std::vector<double> solve(const std::vector<double>& b, double tol = 1e-10) const {
-    std::vector<double> x(m, 0.0), r = b, z(m), p(m), t(m);
-    auto dot = [&](const std::vector<double>& a, const std::vector<double>& c) {
-      double s = 0;
-      for (size_t i = 0; i < m; ++i) s += a[i] * c[i];
-      return s;
-    };
-    const double b2 = dot(b, b);
-    if (b2 == 0) return x;
-    const double thr = tol * tol * b2;
-    if (dot(r, r) < thr) return x;
-    for (size_t i = 0; i < m; ++i) p[i] = r[i] / diag[i];
-    double rz = dot(r, p);
-    const size_t cap = 20 * m;
-    for (size_t it = 0; it < cap; ++it) {
-      apply(p, t);
-      const double a = rz / dot(p, t);
-      for (size_t i = 0; i < m; ++i) {
-        x[i] += a * p[i];
-        r[i] -= a * t[i];
-      }
-      const double rr = dot(r, r);
-      if (rr < thr) return x;
-      for (size_t i = 0; i < m; ++i) z[i] = r[i] / diag[i];
-      const double old = rz;
-      rz = dot(r, z);
-      const double beta = rz / old;
-      for (size_t i = 0; i < m; ++i) p[i] = z[i] + beta * p[i];
-    }
-    throw SolveError("transition cube solve failed: PCG did not converge",
-                     std::sqrt(dot(r, r) / b2));
-  }
-
-  // A_IB^T (eps .* z): the boundary row of the adjoint solution
-  std::vector<double> boundary(const std::vector<double>& z) const {
-    std::vector<double> out(6 * size_t(n) * n, 0.0);
-    for (int k = 0; k < n; ++k)
-      for (int j = 0; j < n; ++j)
-        for (int i = 0; i < n; ++i) {
-          const size_t v = (size_t(k) * n + j) * n + i;
-          const int c[3] = {i, j, k};
-          for (int d = 0; d < 6; ++d) {
-            const int a = d >> 1;
-            const int nb = c[a] + ((d & 1) ? 1 : -1);
-            if (nb >= 0 && nb < n) continue;
-            const int u = a == 0 ? j : i;
-            const int w = a == 2 ? j : k;
-            out[(size_t(d) * n + w) * n + u] = eps[v] * z[v];
-          }
-        }
-    return out;
-  }
-};
-
-DiscreteSGF solve_stencil(const Stencil& S, double half_width, bool with_kernels) {
-  const int n = S.n;
-  DiscreteSGF out;
-  out.n = n;
-  out.pitch = 2.0 * half_width / n;
-  const int c = (n - 1) / 2;
-  const size_t crow = (size_t(c) * n + c) * n + c;
-  std::vector<double> e(S.m, 0.0);
-  e[crow] = 1.0;
-  const std::vector<double> p = S.boundary(S.solve(e));
-  double total = 0, lowest = 0;
-  for (double v : p) {
-    total += v;
-    lowest = std::min(lowest, v);
-  }
-  if (std::fabs(total - 1.0) > 1e-9 || lowest < -1e-9)
-    throw SolveError("transition cube solve failed normalization check", std::fabs(total - 1));
-  out.probs.resize(p.size());
-  out.cdf.resize(p.size());
-  double run = 0;
-  for (size_t b = 0; b < p.size(); ++b) {
-    out.probs[b] = std::max(p[b], 0.0);
-    run += out.probs[b];
-    out.cdf[b] = run;
-  }
-  if (!with_kernels) return out;
-  for (int a = 0; a < 3; ++a) {
-    out.grad_kernels[a].assign(p.size(), 0.0);
-    int up[3] = {c, c, c}, dn[3] = {c, c, c};
-    up[a] += 1;
-    dn[a] -= 1;
-    const bool hu = up[a] < n, hd = dn[a] >= 0;
-    std::vector<double> rhs(S.m, 0.0);
-    double denom;
-    auto idx = [&](const int* q) { return (size_t(q[2]) * n + q[1]) * n + q[0]; };
-    if (hu && hd) {
-      rhs[idx(up)] += 1.0;
-      rhs[idx(dn)] -= 1.0;
-      denom = 2.0 * out.pitch;
-    } else if (hu) {
-      rhs[idx(up)] += 1.0;
-      rhs[crow] -= 1.0;
-      denom = out.pitch;
-    } else if (hd) {
-      rhs[crow] += 1.0;
-      rhs[idx(dn)] -= 1.0;
-      denom = out.pitch;
-    } else {
-      continue;  // n = 1: zero kernel
-    }
-    const std::vector<double> k = S.boundary(S.solve(rhs));
-    for (size_t b = 0; b < k.size(); ++b) out.grad_kernels[a][b] = k[b] / denom;
+  const size_t P = 6ull * n * n;
+  std::vector<double> pr(P * keys.size()), ke(with_kernels ? 3 * P * keys.size() : 0);
+  frw_ctx* ctx = Device::get(device).ctx();
+  const int rc = frw_sgf_solve(ctx, n, static_cast<int>(keys.size()), axes.data(), layers.data(),
+                               pr.data(), with_kernels ? ke.data() : nullptr);
+  if (rc == FRW_ESOLVE) throw SolveError(frw_last_error(ctx), 0.0);
+  throw_status(ctx, rc);
+  for (size_t q = 0; q < keys.size(); ++q) {
+    auto g = std::make_shared<DiscreteSGF>();
+    g->n = n;
+    g->pitch = 1.0;  // canonical unit pitch
+    g->probs.assign(pr.begin() + q * P, pr.begin() + (q + 1) * P);
+    g->cdf.resize(P);
+    double run = 0;
+    for (size_t b = 0; b < P; ++b) g->cdf[b] = run += g->probs[b];
+    if (with_kernels)
+      for (int a = 0; a < 3; ++a)
+        g->grad_kernels[a].assign(ke.begin() + (3 * q + a) * P, ke.begin() + (3 * q + a + 1) * P);
+    out.push_back(std::move(g));
   }
   return out;
 }
-
 }  // namespace
 
-DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels) {
-  const int n = key.n;
-  if (static_cast<int>(key.layers.size()) != n)
-    throw std::invalid_argument("canonical_grid: malformed key");
-  std::vector<double> eps(size_t(n) * n * n);
-  for (int k = 0; k < n; ++k)
-    for (int j = 0; j < n; ++j)
-      for (int i = 0; i < n; ++i) {
-        const int v[3] = {i, j, k};
-        eps[(size_t(k) * n + j) * n + i] = key.layers[v[key.axis]];
-      }
-  // canonical unit-pitch cube: half width n/2 (sgf_cache.cpp:78-96)
-  return solve_stencil(Stencil(n, eps), n / 2.0, with_kernels);
+DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels, int device) {
+  return *solve_keys({key}, with_kernels, device)[0];
 }
-
 
 // ---- cache -------------------------------------------------------------------
 
@@ -255,42 +124,32 @@ std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::get(const ProfileKey& key
     }
     ++misses_;
   }
-  auto sgf = std::make_shared<DiscreteSGF>(solve_canonical(key, true));
+  auto sgf = solve_keys({key}, true, device_)[0];
   std::lock_guard<std::mutex> lk(mu_);
   auto [it, inserted] = map_.emplace(key, sgf);  // first stored result wins
   if (inserted && capacity_ > 0 && map_.size() > capacity_) map_.erase(map_.begin());
   return it->second;
 }
 
-void StratifiedSgfCache::solve_many(const std::vector<ProfileKey>& keys, int threads) {
+void StratifiedSgfCache::solve_many(const std::vector<ProfileKey>& keys, int /*threads*/) {
+  // one device batch per lattice size (the reference fans keys out to host threads)
   std::vector<ProfileKey> todo;
   {
     std::lock_guard<std::mutex> lk(mu_);
     for (const auto& k : keys)
-      if (!map_.count(k)) todo.push_back(k);
+      if (!map_.count(k) && std::find(todo.begin(), todo.end(), k) == todo.end()) todo.push_back(k);
     misses_ += todo.size();
   }
-  if (todo.empty()) return;
-  if (threads <= 0) threads = std::max(1u, std::thread::hardware_concurrency());
-  threads = std::min<int>(threads, static_cast<int>(todo.size()));
-  std::atomic<size_t> next{0};
-  std::vector<std::exception_ptr> errs(threads);
-  std::vector<std::thread> pool;
-  for (int t = 0; t < threads; ++t)
-    pool.emplace_back([&, t] {
-      try {
-        for (size_t i = next++; i < todo.size(); i = next++) {
-          auto sgf = std::make_shared<DiscreteSGF>(solve_canonical(todo[i], true));
-          std::lock_guard<std::mutex> lk(mu_);
-          map_.emplace(todo[i], sgf);
-        }
-      } catch (...) {
-        errs[t] = std::current_exception();
-      }
-    });
-  for (auto& th : pool) th.join();
-  for (auto& e : errs)
-    if (e) std::rethrow_exception(e);
+  std::sort(todo.begin(), todo.end(), [](const ProfileKey& a, const ProfileKey& b) { return a.n < b.n; });
+  for (size_t i = 0; i < todo.size();) {
+    size_t j = i;
+    while (j < todo.size() && todo[j].n == todo[i].n) ++j;
+    const std::vector<ProfileKey> part(todo.begin() + i, todo.begin() + j);
+    const auto sol = solve_keys(part, true, device_);
+    std::lock_guard<std::mutex> lk(mu_);
+    for (size_t q = 0; q < part.size(); ++q) map_.emplace(part[q], sol[q]);
+    i = j;
+  }
 }
 
 std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::insert(
