@@ -80,9 +80,11 @@ int frw_upload_grid(frw_ctx *ctx, int n, const double *eps,
 
 /* Host-only compilation of a cube into the stencil table (no device calls;
  * used by the CPU tests to check the threshold construction).  Pass NULL
- * buffers to query *records first; map has n^3 entries, rec `records`
- * packed words (five 10-bit threshold lanes at bits 11d, exit bits 55..60),
- * full 5*records exact 53-bit thresholds. */
+ * buffers to query *records first; map has (n+2)^3 entries (the lattice
+ * with a one-node halo, x-fastest; halo nodes and conductor voxels hold the
+ * exit record records-1), rec `records` packed words (five 11-bit threshold
+ * lanes 2047 - T_d at bits 12d, guard bits 12d+11), full 5*records exact
+ * 53-bit thresholds. */
 int frw_grid_compile(int n, const double *eps, const int32_t *mask,
                      uint16_t *map, uint64_t *rec, uint64_t *full,
                      int *records);

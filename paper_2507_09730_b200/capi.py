@@ -156,7 +156,7 @@ def grid_compile(eps, mask=None):
                             None, None, None, C.byref(R))
     if rc:
         raise FrwError(rc, "grid_compile failed")
-    mp = np.empty(n ** 3, np.uint16)
+    mp = np.empty((n + 2) ** 3, np.uint16)  # lattice with a one-node halo
     rec = np.empty(R.value, np.uint64)
     full = np.empty((R.value, 5), np.uint64)
     L.frw_grid_compile(n, eps.ctypes.data_as(_dp), None if m is None else m.ctypes.data_as(_ip),

@@ -50,10 +50,10 @@ constexpr int kDirAxis[6] = {0, 0, 1, 1, 2, 2};
 constexpr int kDirSign[6] = {-1, +1, -1, +1, -1, +1};
 
 // SWAR layout of a packed record
-constexpr int kLane = 11;                          // 10-bit threshold + guard
-constexpr uint64_t kOnes = 0x0000100200400801ull;  // 1 in each of the 5 lanes
-constexpr uint64_t kGuard = kOnes << 10;           // guard bit of each lane
-constexpr int kExitShift = 55;                     // six exit bits 55..60
+constexpr int kLane = 12;                          // 11-bit threshold + guard
+constexpr uint64_t kOnes = 0x0000001001001001ull | (1ull << 48);  // 1 in each of 5 lanes
+constexpr uint64_t kGuard = kOnes << 11;           // guard bit of each lane (11,23,35,47,59)
+constexpr int kTop = 2047;                         // 11-bit lane maximum
 
 // ---------------------------------------------------------------------------
 // host: compile the grid into node map + step records
@@ -143,12 +143,18 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   constexpr uint32_t kSurface = 0xFFFF, kCond = 0xFFFE;
   KeyTable rec_of(std::min<size_t>(nodes, 1u << 16));
   uint32_t nrec = 0;
-  out.map.resize(nodes);
+  // Padded map: a one-node halo around the lattice.  Halo nodes and conductor
+  // voxels are absorbing: they map to the exit record, appended after the
+  // step records once their count is known.
+  const int np = n + 2;
+  std::vector<uint32_t> pmap(static_cast<size_t>(np) * np * np, 0xFFFFFFFFu);
   for (int k = 0; k < n; ++k)
     for (int j = 0; j < n; ++j)
       for (int i = 0; i < n; ++i) {
         const int v = (k * n + j) * n + i;
+        const size_t pv = (static_cast<size_t>(k + 1) * np + (j + 1)) * np + (i + 1);
         const bool self_cond = mask && mask[v] >= 0;
+        if (self_cond) continue;  // conductor voxel: exit record
         uint32_t code[6];
         for (int d = 0; d < 6; ++d) {
           int nb[3] = {i, j, k};
@@ -160,26 +166,23 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
           const int nv = (nb[2] * n + nb[1]) * n + nb[0];
           code[d] = (mask && mask[nv] >= 0) ? kCond : node_pal[nv];
         }
-        // conductor voxels are never stepped on; give them a benign key
-        const uint32_t self = self_cond ? kCond : node_pal[v];
+        const uint32_t self = node_pal[v];
         Key key{(uint64_t(self) << 48) | (uint64_t(code[0]) << 32) |
                     (uint64_t(code[1]) << 16) | code[2],
                 (uint64_t(code[3]) << 32) | (uint64_t(code[4]) << 16) | code[5]};
         const auto [r, fresh] = rec_of.find_or_insert(key, nrec);
         if (fresh) {
-          if (r > 0xFFFF)
-            return frw_fail(ctx, FRW_EINVAL, "more than 65536 distinct stencil records");
+          if (r >= 0xFFFF)
+            return frw_fail(ctx, FRW_EINVAL, "more than 65535 distinct stencil records");
           ++nrec;
           // microwalk.cpp:91-109: alphas (1 on absorbing faces) and their
           // in-order partial sums
           double acc[6], sum = 0;
           uint64_t packed = 0;
-          const double ev = self_cond ? 1.0 : pal[node_pal[v]];
+          const double ev = pal[node_pal[v]];
           for (int d = 0; d < 6; ++d) {
             double a = 1.0;
-            if (code[d] == kSurface || code[d] == kCond)
-              packed |= 1ull << (kExitShift + d);
-            else {
+            if (code[d] != kSurface && code[d] != kCond) {
               const double en = pal[code[d]];
               a = en / (en + ev);
             }
@@ -189,17 +192,23 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
           for (int d = 0; d < 5; ++d) {
             const uint64_t X = threshold_of(acc[d], sum);
             out.full.push_back(X);
-            // X = 2^53 (never reached) clamps to 1023: every x with top bits
-            // 1023 then ties and the exact fallback decides
-            const uint64_t t10 = std::min<uint64_t>(X >> 43, 1023);
-            // stored pre-negated: lane = 1023 - T_d, so x10*ones + record
-            // carries into the lane's guard bit exactly when x10 > T_d
-            packed |= (1023 - t10) << (kLane * d);
+            // X = 2^53 (never reached) clamps to 2047: every x with top bits
+            // 2047 then ties and the exact fallback decides
+            const uint64_t t11 = std::min<uint64_t>(X >> 42, kTop);
+            // stored pre-negated: lane = 2047 - T_d, so x11*ones + record
+            // carries into the lane's guard bit exactly when x11 > T_d
+            packed |= (kTop - t11) << (kLane * d);
           }
           out.rec.push_back(packed);
         }
-        out.map[v] = static_cast<uint16_t>(r);
+        pmap[pv] = r;
       }
+  // the exit record: never stepped from (an absorbed walker stops)
+  out.rec.push_back(0);
+  for (int d = 0; d < 5; ++d) out.full.push_back(1ull << 53);
+  out.map.resize(pmap.size());
+  for (size_t q = 0; q < pmap.size(); ++q)
+    out.map[q] = static_cast<uint16_t>(pmap[q] == 0xFFFFFFFFu ? nrec : pmap[q]);
   return FRW_OK;
 }
 
@@ -207,16 +216,17 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
 // device
 
 struct DevGrid {
-  const uint16_t* map;
-  const uint64_t* rec;
+  const uint16_t* map;  // [(n+2)^3] padded lattice: halo and conductor voxels -> exit
+  const uint64_t* rec;  // [R+1] packed SWAR records, R = the exit record
   const uint64_t* full;
   const int32_t* mask;
   int n;
-  int nn;
-  int start_idx;
+  int np, npp;          // padded extents n+2, (n+2)^2
+  int start_idx;        // padded index of start_node
+  uint32_t exit_rec;    // R
   uint32_t map_bytes;  // padded to 16
   uint32_t rec_bytes;  // padded to 16
-  float inv_n, inv_nn;
+  float inv_np, inv_npp;
 };
 
 struct DevParams {
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (SMEM) bulk_stage(smem, g.map, g.map_bytes + g.rec_bytes, &bar);
   if (threadIdx.x < 6) {
     const int d = threadIdx.x, ax = d >> 1;
-    stride[d] = ((d & 1) ? 1 : -1) * (ax == 0 ? 1 : ax == 1 ? g.n : g.nn);
+    stride[d] = ((d & 1) ? 1 : -1) * (ax == 0 ? 1 : ax == 1 ? g.np : g.npp);
   }
   __syncthreads();
   const uint32_t s_map = smem_base(smem);
@@ -321,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int n = g.n;
   const int cap = p.step_cap;
+  const uint32_t kExit = g.exit_rec;
   unsigned long long ssum = 0, ssq = 0, cexit = 0;
 
   long long t = static_cast<long long>(atomicAdd(ctr, 1ull));
@@ -329,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int idx = g.start_idx;
   int steps = 0;
   uint64_t sm = 0;   // parity: SplitMix64 state
-  uint32_t blk = 0;  // philox: 4-step block index within the transit
+  uint32_t blk = 0;  // philox: 8-step block index within the transit
   if (RNG == FRW_RNG_SPLITMIX_PARITY && live)
     sm = sm64_stream_from_mixed(p.mixed_seed, p.stream_begin + t);
   if (RNG == FRW_RNG_SPLITMIX_STATES && live) sm = p.states[t];
@@ -341,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the (id, step slot, 1) counter only when the 16-bit prefix ties a
   // threshold, so x is still an exact 53-bit uniform.  Parity: 4 steps.
   constexpr int SS = SM ? 4 : 8;
+  int xdir = 0;  // direction of the last move
   while (__any_sync(0xFFFFFFFFu, live)) {
     // ---- one phase-aligned super-step of SS lattice steps ----------------
     uint32_t w[4];
@@ -354,42 +366,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       w[3] = o.w;
     }
     bool exited = false;
-    int xdir = 0;
     // The steps run unconditionally (predicated state updates, no per-step
-    // branch); a lane that has exited keeps re-reading its last node without
-    // consuming randomness.  The step cap is checked per super-step: a
-    // transit is an error iff it needs more than `cap` steps
-    // (microwalk.cpp:81, :153-155), whichever step inside the super-step
-    // crossed it.
+    // branch).  A move onto an absorbing node (the halo around the lattice,
+    // or a conductor voxel) is seen when that node's record id is loaded for
+    // the next step; the walker then stops without consuming randomness.
+    // The step cap is checked per super-step: a transit is an error iff it
+    // needs more than `cap` steps (microwalk.cpp:81, :153-155), whichever
+    // step inside the super-step crossed it.
 #pragma unroll
     for (int u = 0; u < SS; ++u) {
-      const bool act = live && !exited;
+      const uint32_t r = SMEM ? lds_u16(s_map + 2u * idx) : __ldg(g.map + idx);
+      const bool act = live && !exited && r != kExit;
+      exited |= live && r == kExit;
       uint64_t z = 0;
-      uint32_t x10, h16 = 0;
+      uint32_t x11, h16 = 0;
       if (SM) {
         const uint64_t s1 = sm + kGamma;  // SplitMix64::next (rng.hpp:19-22)
         z = sm64_mix(s1);
         sm = act ? s1 : sm;
-        x10 = static_cast<uint32_t>(z >> 54);  // top 10 bits of x = z >> 11
+        x11 = static_cast<uint32_t>(z >> 53);  // top 11 bits of x = z >> 11
       } else {
         h16 = (u & 1) ? (w[u >> 1] & 0xFFFFu) : (w[u >> 1] >> 16);
-        x10 = h16 >> 6;
+        x11 = h16 >> 5;
       }
       steps += act;
-      const uint32_t r = SMEM ? lds_u16(s_map + 2u * idx) : __ldg(g.map + idx);
       const uint64_t rc = SMEM ? lds_u64(s_rec + 8u * r) : __ldg(g.rec + r);
-      // SWAR: lane d of x10*ones + rec = x10 + 1023 - T_d reaches its guard
-      // bit iff x10 > T_d; the guard bits (10,21 | 32,43,54) of the low and
+      // SWAR: lane d of x11*ones + rec = x11 + 2047 - T_d reaches its guard
+      // bit iff x11 > T_d; the guard bits (11,23 | 35,47,59) of the low and
       // high words are disjoint, so one POPC of their OR counts them.  A lane
-      // whose low 10 bits are all ones has x10 == T_d: a tie.
-      const uint64_t d1 = static_cast<uint64_t>(x10) * kOnes + rc;
+      // whose low 11 bits are all ones has x11 == T_d: a tie.
+      const uint64_t d1 = static_cast<uint64_t>(x11) * kOnes + rc;
       const uint32_t lo = static_cast<uint32_t>(d1), hi = static_cast<uint32_t>(d1 >> 32);
       int dir = __popc((lo & static_cast<uint32_t>(kGuard)) |
                        (hi & static_cast<uint32_t>(kGuard >> 32)));
       const uint64_t d2 = d1 + kOnes;
       const bool tie = ((d2 ^ d1) & kGuard) != 0;
       if (__builtin_expect(__any_sync(0xFFFFFFFFu, act && tie), 0) && act && tie) {
-        // 10-bit tie: exact comparison against the 53-bit thresholds
+        // 11-bit tie: exact comparison against the 53-bit thresholds
         const uint64_t* f = g.full + 5 * r;
         if (SM) {
           const uint64_t x53 = z >> 11;
@@ -418,30 +431,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      const bool ex = ((static_cast<uint32_t>(rc >> 32) >> dir) & (1u << (kExitShift - 32))) != 0;
       const int s = SMEM ? lds_s32(s_str + 4u * dir) : stride[dir];
-      xdir = (act && ex) ? dir : xdir;
-      idx += (act && !ex) ? s : 0;
-      exited |= act && ex;
+      xdir = act ? dir : xdir;
+      idx += act ? s : 0;
+    }
+    // the last step of the super-step may have moved onto an absorbing node
+    {
+      const uint32_t r = SMEM ? lds_u16(s_map + 2u * idx) : __ldg(g.map + idx);
+      exited |= live && r == kExit;
     }
     ++blk;
     // ---- exit bookkeeping, batched once per super-step -------------------
     if (live && (exited || steps >= cap)) {
       int32_t panel = -1, cid = -1;
+      long long nd = -1;
       if (exited && steps <= cap) {
-        const int k = fdiv(idx, g.nn, g.inv_nn);
-        const int rem = idx - k * g.nn;
-        const int j = fdiv(rem, n, g.inv_n);
-        const int i = rem - j * n;
+        // absorbing node (padded coordinates) and the interior node before it
+        const int hk = fdiv(idx, g.npp, g.inv_npp);
+        const int hrem = idx - hk * g.npp;
+        const int hj = fdiv(hrem, g.np, g.inv_np);
+        const int hc[3] = {hrem - hj * g.np, hj, hk};
         const int ax = xdir >> 1;
-        const int c = ax == 0 ? i : ax == 1 ? j : k;
-        if ((xdir & 1) ? c == n - 1 : c == 0) {  // left the lattice: surface
-          const int uu = ax == 0 ? j : i;
-          const int vv = ax == 2 ? j : k;
+        int c[3] = {hc[0] - 1, hc[1] - 1, hc[2] - 1};  // unpadded
+        c[ax] -= (xdir & 1) ? 1 : -1;                  // step back inside
+        nd = 8ll * ((c[2] * n + c[1]) * n + c[0]) + xdir;
+        if (hc[ax] == 0 || hc[ax] == n + 1) {  // left the lattice: surface
+          const int uu = ax == 0 ? c[1] : c[0];
+          const int vv = ax == 2 ? c[1] : c[2];
           panel = (xdir * n + vv) * n + uu;  // sgf.hpp:34-36, sgf.cpp:13-30
           atomicAdd(hist + panel, 1ull);
         } else {  // absorbed by a conductor voxel (masked lattices)
-          cid = g.mask[idx + stride[xdir]];
+          cid = g.mask[((hc[2] - 1) * n + (hc[1] - 1)) * n + (hc[0] - 1)];
           ++cexit;
         }
       } else {
@@ -450,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (out_panel) out_panel[t] = panel;
       if (out_steps) out_steps[t] = steps;
       if (out_cond) out_cond[t] = cid;
-      if (out_nd) out_nd[t] = (exited && steps <= cap) ? 8ll * idx + xdir : -1ll;
+      if (out_nd) out_nd[t] = nd;
       ssum += steps;
       ssq += static_cast<unsigned long long>(steps) * steps;
       // re-arm with the prefetched transit, prefetch the following one
@@ -484,9 +504,11 @@ template <int RNG, bool SMEM>
 int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned long long* ms,
            unsigned long long* mq, unsigned long long* mc) {
   const GridTable& G = ctx->grid;
-  DevGrid g{G.d_map, G.d_rec, G.d_full, G.has_mask ? G.d_mask : nullptr, G.n, G.n * G.n, G.start_idx,
+  const int np = G.n + 2;
+  DevGrid g{G.d_map, G.d_rec, G.d_full, G.has_mask ? G.d_mask : nullptr, G.n, np, np * np,
+            G.start_idx, static_cast<uint32_t>(G.records),
             static_cast<uint32_t>(G.map_bytes), static_cast<uint32_t>(G.rec_bytes),
-            1.0f / G.n, 1.0f / (G.n * G.n)};
+            1.0f / np, 1.0f / (np * np)};
   DevParams dp{p->seed, sm64_mix(p->seed), p->stream_begin, p->count,
                p->step_cap > 0 ? p->step_cap : 1000 * G.n * G.n, p->states};
   const size_t smem = SMEM ? G.map_bytes + G.rec_bytes : 0;
@@ -514,18 +536,19 @@ extern "C" {
 int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask, double cx,
                     double cy, double cz, double half_width) {
   if (!ctx) return FRW_EINVAL;
-  if (n < 1 || n > 1000 || !eps)
-    return frw_fail(ctx, FRW_EINVAL, "upload_grid: need 1 <= n <= 1000 and eps");
+  if (n < 1 || n > 253 || !eps)
+    return frw_fail(ctx, FRW_EINVAL, "upload_grid: need 1 <= n <= 253 and eps");
   if (!(half_width > 0)) return frw_fail(ctx, FRW_EINVAL, "upload_grid: half_width <= 0");
   Compiled cg;
   if (int rc = compile_grid(ctx, n, eps, mask, cg)) return rc;
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   GridTable& G = ctx->grid;
   G.n = n;
-  G.records = static_cast<int>(cg.rec.size());
+  G.records = static_cast<int>(cg.rec.size()) - 1;  // step records; [R] is the exit record
   const int c = (n - 1) / 2;  // start_node, sgf.hpp:58-61
-  G.start_idx = (c * n + c) * n + c;
-  G.start_is_conductor = mask && mask[G.start_idx] >= 0;
+  const int np = n + 2;
+  G.start_idx = ((c + 1) * np + (c + 1)) * np + (c + 1);  // padded
+  G.start_is_conductor = mask && mask[(c * n + c) * n + c] >= 0;
   G.center[0] = cx;
   G.center[1] = cy;
   G.center[2] = cz;
@@ -578,7 +601,7 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
 
 int frw_grid_compile(int n, const double* eps, const int32_t* mask, uint16_t* map,
                      uint64_t* rec, uint64_t* full, int* records) {
-  if (n < 1 || n > 1000 || !eps || !records) return FRW_EINVAL;
+  if (n < 1 || n > 253 || !eps || !records) return FRW_EINVAL;
   frw_ctx tmp;
   Compiled cg;
   if (int rc = compile_grid(&tmp, n, eps, mask, cg)) return rc;

@@ -40,16 +40,20 @@ M64 = (1 << 64) - 1
 
 
 def _emulate(oracle, eps, seed, count, mask=None):
-    """Host replay of the kernel's table-driven step (mw_grid.cu)."""
+    """Host replay of the kernel's table-driven step (mw_grid.cu): padded
+    map with an absorbing halo, five 11-bit SWAR lanes, exact fallback."""
     n = round(len(eps) ** (1 / 3))
     mp, rec, full = capi.grid_compile(eps, mask)
-    strides = [-1, 1, -n, n, -n * n, n * n]
-    ones, guard = 0x0000100200400801, 0x0000100200400801 << 10
+    npad = n + 2
+    exit_rec = len(rec) - 1
+    strides = [-1, 1, -npad, npad, -npad * npad, npad * npad]
+    ones = sum(1 << (12 * d) for d in range(5))
+    guard = ones << 11
     c = (n - 1) // 2
-    out, ties = [], 0
+    out = []
     for t in range(count):
         st = oracle.stream_state(seed, t)
-        idx = (c * n + c) * n + c
+        idx = ((c + 1) * npad + (c + 1)) * npad + (c + 1)
         node = [c, c, c]
         steps = 0
         while True:
@@ -58,25 +62,23 @@ def _emulate(oracle, eps, seed, count, mask=None):
             z = int(oracle.lib.frwo_mix(st))
             r = int(mp[idx])
             rc = int(rec[r])
-            d1 = ((z >> 54) * ones + rc) & M64               # SWAR lanes
-            gt = d1 & guard                                   # x10 > T_d
-            d = bin(gt).count("1")
-            if (((d1 + ones) ^ d1) & guard) != 0:             # 10-bit tie
-                ties += 1
+            d1 = ((z >> 53) * ones + rc) & M64               # SWAR lanes
+            d = bin(d1 & guard).count("1")                    # x11 > T_d
+            if (((d1 + ones) ^ d1) & guard) != 0:             # 11-bit tie
                 d = sum((z >> 11) >= int(full[r, q]) for q in range(5))
-            if (rc >> (55 + d)) & 1:
+            prev = list(node)
+            node[d >> 1] += 1 if d & 1 else -1
+            idx += strides[d]
+            if int(mp[idx]) == exit_rec:                      # absorbing node
                 ax = d >> 1
-                i, j, k = node
-                cc = node[ax]
-                if (cc == n - 1) if d & 1 else (cc == 0):
+                if not 0 <= node[ax] < n:
+                    i, j, k = prev
                     u = j if ax == 0 else i
                     v = j if ax == 2 else k
                     out.append(((d * n + v) * n + u, steps))
                 else:
                     out.append((-1, steps))
                 break
-            idx += strides[d]
-            node[d >> 1] += 1 if d & 1 else -1
     return np.array(out)
 
 
@@ -104,16 +106,24 @@ def test_record_counts_fit_shared_memory():
     for eps in (c1_grid(1)[0], c2_grid(1)[0]):
         n = round(len(eps) ** (1 / 3))
         _, rec, _ = capi.grid_compile(eps)
-        smem = (2 * n ** 3 + 15) // 16 * 16 + (8 * rec.shape[0] + 15) // 16 * 16
+        smem = (2 * (n + 2) ** 3 + 15) // 16 * 16 + (8 * rec.shape[0] + 15) // 16 * 16
         assert smem <= 227 * 1024
 
 
 def test_packed_thresholds_are_monotone_prefixes():
-    """lane d holds 1023 minus the top 10 bits of X_d; X_d is non-decreasing"""
-    _, rec, full = capi.grid_compile(c2_grid(1)[0])
+    """lane d holds 2047 minus the top 11 bits of X_d; X_d is non-decreasing;
+    the halo and only the halo maps to the exit record"""
+    eps = c2_grid(1)[0]
+    mp, rec, full = capi.grid_compile(eps)
+    rec, full = rec[:-1], full[:-1]  # the last record is the exit record
     assert (np.diff(full.astype(np.float64), axis=1) >= 0).all()
-    lanes = np.stack([(rec >> np.uint64(11 * d)) & np.uint64(2047) for d in range(5)], axis=1)
-    assert np.array_equal(lanes, 1023 - np.minimum(full >> np.uint64(43), np.uint64(1023)))
+    lanes = np.stack([(rec >> np.uint64(12 * d)) & np.uint64(4095) for d in range(5)], axis=1)
+    assert np.array_equal(lanes, 2047 - np.minimum(full >> np.uint64(42), np.uint64(2047)))
+    n = 41
+    m3 = mp.reshape(n + 2, n + 2, n + 2)
+    ex = len(rec)
+    assert (m3[0] == ex).all() and (m3[-1] == ex).all() and (m3[:, 0] == ex).all()
+    assert (m3[:, :, -1] == ex).all() and (m3[1:-1, 1:-1, 1:-1] < ex).all()
 
 
 def test_invalid_grid_rejected():
@@ -145,12 +155,13 @@ def test_exact_thresholds_match_bisection(which):
     mp, rec, full = capi.grid_compile(eps)
     e3 = eps.reshape(n, n, n)  # [k][j][i]
     seen = set()
+    npad = n + 2
     for v in range(n ** 3):
-        r = int(mp[v])
+        k, j, i = v // (n * n), (v // n) % n, v % n
+        r = int(mp[((k + 1) * npad + (j + 1)) * npad + (i + 1)])
         if r in seen:
             continue
         seen.add(r)
-        k, j, i = v // (n * n), (v // n) % n, v % n
         ev = float(e3[k, j, i])
         acc, s = [], 0.0
         for d in range(6):
