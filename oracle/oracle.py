@@ -385,9 +385,31 @@ class Ref:
         L.ref_extract.argtypes = [C.c_void_p, _dp, _lp, C.c_int, _dp, _dp, _up, _up, _dp]
         L.ref_run_walks.argtypes = [C.c_void_p, _dp, _lp, C.c_uint64, C.c_int64, _ip, _dp, _bp]
         L.ref_extract_warm.argtypes = [C.c_void_p, _dp, _lp, C.c_int, _dp, _dp, _up, _up, _dp]
+        L.ref_cache_save.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_char_p]
+        L.ref_cache_load_probs.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, _dp, _lp]
 
     def err(self):
         return self.lib.ref_last_error().decode()
+
+    def cache_save(self, n, axes, layers, path):
+        """SGF1 file written by the reference's StratifiedSgfCache"""
+        ax = np.ascontiguousarray(axes, np.int32)
+        lay = np.ascontiguousarray(layers, np.float64).reshape(len(ax), n)
+        if self.lib.ref_cache_save(n, len(ax), _ptr(ax, _ip), _ptr(lay, _dp), path.encode()):
+            raise RuntimeError(self.err())
+
+    def cache_load_probs(self, path, n, axis, layers):
+        """the reference's StratifiedSgfCache::load of `path`, then find(key)"""
+        lay = np.ascontiguousarray(layers, np.float64)
+        probs = np.empty(6 * n * n)
+        loaded = C.c_int64()
+        rc = self.lib.ref_cache_load_probs(path.encode(), n, axis, _ptr(lay, _dp),
+                                           _ptr(probs, _dp), C.byref(loaded))
+        if rc == -2:
+            return None, loaded.value
+        if rc:
+            raise RuntimeError(self.err())
+        return probs, loaded.value
 
     def microwalk_grid(self, eps, center, half_width, seed, stream0, count, mask=None,
                        step_cap=0, threads=1, per_transit=True, hist=True):

@@ -429,4 +429,38 @@ int ref_run_walks(const void* h, const double* cfg_d, const int64_t* cfg_i,
   }
 }
 
+// StratifiedSgfCache::get for each key, then save (sgf_cache.cpp:98-131,
+// :210-250): an SGF1 file written by the reference's own cache code
+int ref_cache_save(int n, int count, const int32_t* axes, const double* layers,
+                   const char* path) {
+  try {
+    StratifiedSgfCache cache;
+    for (int q = 0; q < count; ++q) {
+      const std::vector<double> lay(layers + static_cast<size_t>(q) * n,
+                                    layers + static_cast<size_t>(q + 1) * n);
+      cache.get(profile_key(n, axes[q], lay));
+    }
+    cache.save(path, n);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// loads an SGF1 file with the reference's cache and returns the probs of
+// one key (n*n*6 doubles) -- reads files written by the B200 build
+int ref_cache_load_probs(const char* path, int n, int axis, const double* layers,
+                         double* probs, int64_t* loaded) {
+  try {
+    StratifiedSgfCache cache;
+    *loaded = static_cast<int64_t>(cache.load(path));
+    const auto g = cache.find(profile_key(n, axis, std::vector<double>(layers, layers + n)));
+    if (!g) return -2;
+    std::copy(g->probs.begin(), g->probs.end(), probs);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 }  // extern "C"

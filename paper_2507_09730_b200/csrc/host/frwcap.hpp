@@ -245,7 +245,7 @@ class StratifiedSgfCache {
   void set_device(int device) { device_ = device; }
   std::shared_ptr<const DiscreteSGF> get(const ProfileKey& key);
   std::shared_ptr<const DiscreteSGF> find(const ProfileKey& key) const;
-  // solves the missing keys in parallel (host threads)
+  // solves the missing keys (one device batch per lattice size)
   void solve_many(const std::vector<ProfileKey>& keys, int threads = 0);
   // first stored result wins (sgf_cache.cpp:133-153)
   std::shared_ptr<const DiscreteSGF> insert(const ProfileKey& key,
@@ -263,10 +263,20 @@ class StratifiedSgfCache {
   size_t load(const std::string& path);
 
  private:
+  // capacity > 0: least-recently-used entries (last get/find/store) are
+  // evicted on insert (sgf_cache.hpp:51-55, sgf_cache.cpp:133-153)
+  struct Entry {
+    std::shared_ptr<const DiscreteSGF> sgf;
+    mutable uint64_t used = 0;
+  };
+  std::shared_ptr<const DiscreteSGF> store_locked(const ProfileKey& key,
+                                                  std::shared_ptr<const DiscreteSGF> sgf);
+  void touch(const Entry& e) const { e.used = ++clock_; }
   size_t capacity_;
   int device_ = 0;
   mutable std::mutex mu_;
-  std::unordered_map<ProfileKey, std::shared_ptr<const DiscreteSGF>, ProfileKeyHash> map_;
+  std::unordered_map<ProfileKey, Entry, ProfileKeyHash> map_;
+  mutable uint64_t clock_ = 0;
   uint64_t hits_ = 0, misses_ = 0;
 };
 

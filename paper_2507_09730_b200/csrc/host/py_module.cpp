@@ -546,6 +546,51 @@ PYBIND11_MODULE(_core, m) {
       py::arg("structure_json"), py::arg("center"), py::arg("half_width"), py::arg("n"),
       py::arg("allow_conductors") = false);
 
+  // StratifiedSgfCache (sgf_cache.hpp:47-101) -- B200 extra for tests and tools
+  py::class_<StratifiedSgfCache>(m, "SgfCache")
+      .def(py::init<size_t>(), py::arg("capacity") = 0)
+      .def("get",
+           [](StratifiedSgfCache& c, int n, int axis, const std::vector<double>& layers) {
+             std::shared_ptr<const DiscreteSGF> g;
+             {
+               py::gil_scoped_release release;
+               g = c.get(profile_key(n, axis, layers));
+             }
+             return py::array_t<double>(g->probs.size(), g->probs.data());
+           },
+           py::arg("n"), py::arg("axis"), py::arg("layers"))
+      .def("find",
+           [](const StratifiedSgfCache& c, int n, int axis,
+              const std::vector<double>& layers) -> py::object {
+             const auto g = c.find(profile_key(n, axis, layers));
+             if (!g) return py::none();
+             return py::array_t<double>(g->probs.size(), g->probs.data());
+           },
+           py::arg("n"), py::arg("axis"), py::arg("layers"))
+      .def("kernels",
+           [](const StratifiedSgfCache& c, int n, int axis, const std::vector<double>& layers) {
+             const auto g = c.find(profile_key(n, axis, layers));
+             if (!g || g->grad_kernels[0].empty()) throw py::key_error("no kernels for key");
+             const size_t P = g->probs.size();
+             py::array_t<double> k({static_cast<size_t>(3), P});
+             for (int a = 0; a < 3; ++a)
+               std::copy(g->grad_kernels[a].begin(), g->grad_kernels[a].end(),
+                         k.mutable_data() + a * P);
+             return k;
+           })
+      .def("stats",
+           [](const StratifiedSgfCache& c) {
+             const auto st = c.stats();
+             py::dict d;
+             d["hits"] = st.hits;
+             d["misses"] = st.misses;
+             d["size"] = st.size;
+             return d;
+           })
+      .def("save", &StratifiedSgfCache::save, py::arg("path"), py::arg("only_n") = 0)
+      .def("load", &StratifiedSgfCache::load, py::arg("path"))
+      .def("clear", &StratifiedSgfCache::clear);
+
   m.def("sgf_cache_save", [](const std::string& path) { shared_cache().save(path); });
   m.def("sgf_cache_load", [](const std::string& path) { return shared_cache().load(path); });
   m.def("sgf_cache_clear", []() { shared_cache().clear(); });

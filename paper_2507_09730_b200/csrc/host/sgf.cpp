@@ -108,10 +108,32 @@ DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels, int device
 
 // ---- cache -------------------------------------------------------------------
 
+std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::store_locked(
+    const ProfileKey& key, std::shared_ptr<const DiscreteSGF> sgf) {
+  auto it = map_.find(key);
+  if (it != map_.end()) {  // first stored result wins
+    touch(it->second);
+    return it->second.sgf;
+  }
+  Entry e;
+  e.sgf = std::move(sgf);
+  touch(e);
+  auto out = map_.emplace(key, e).first->second.sgf;
+  while (capacity_ > 0 && map_.size() > capacity_) {
+    auto victim = map_.begin();
+    for (auto jt = map_.begin(); jt != map_.end(); ++jt)
+      if (jt->second.used < victim->second.used) victim = jt;
+    map_.erase(victim);
+  }
+  return out;
+}
+
 std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::find(const ProfileKey& key) const {
   std::lock_guard<std::mutex> lk(mu_);
   auto it = map_.find(key);
-  return it == map_.end() ? nullptr : it->second;
+  if (it == map_.end()) return nullptr;
+  touch(it->second);
+  return it->second.sgf;
 }
 
 std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::get(const ProfileKey& key) {
@@ -120,15 +142,14 @@ std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::get(const ProfileKey& key
     auto it = map_.find(key);
     if (it != map_.end()) {
       ++hits_;
-      return it->second;
+      touch(it->second);
+      return it->second.sgf;
     }
     ++misses_;
   }
   auto sgf = solve_keys({key}, true, device_)[0];
   std::lock_guard<std::mutex> lk(mu_);
-  auto [it, inserted] = map_.emplace(key, sgf);  // first stored result wins
-  if (inserted && capacity_ > 0 && map_.size() > capacity_) map_.erase(map_.begin());
-  return it->second;
+  return store_locked(key, std::move(sgf));
 }
 
 void StratifiedSgfCache::solve_many(const std::vector<ProfileKey>& keys, int /*threads*/) {
@@ -140,14 +161,15 @@ void StratifiedSgfCache::solve_many(const std::vector<ProfileKey>& keys, int /*t
       if (!map_.count(k) && std::find(todo.begin(), todo.end(), k) == todo.end()) todo.push_back(k);
     misses_ += todo.size();
   }
-  std::sort(todo.begin(), todo.end(), [](const ProfileKey& a, const ProfileKey& b) { return a.n < b.n; });
+  std::stable_sort(todo.begin(), todo.end(),
+                   [](const ProfileKey& a, const ProfileKey& b) { return a.n < b.n; });
   for (size_t i = 0; i < todo.size();) {
     size_t j = i;
     while (j < todo.size() && todo[j].n == todo[i].n) ++j;
     const std::vector<ProfileKey> part(todo.begin() + i, todo.begin() + j);
     const auto sol = solve_keys(part, true, device_);
     std::lock_guard<std::mutex> lk(mu_);
-    for (size_t q = 0; q < part.size(); ++q) map_.emplace(part[q], sol[q]);
+    for (size_t q = 0; q < part.size(); ++q) store_locked(part[q], sol[q]);
     i = j;
   }
 }
@@ -155,7 +177,7 @@ void StratifiedSgfCache::solve_many(const std::vector<ProfileKey>& keys, int /*t
 std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::insert(
     const ProfileKey& key, std::shared_ptr<const DiscreteSGF> sgf) {
   std::lock_guard<std::mutex> lk(mu_);
-  return map_.emplace(key, std::move(sgf)).first->second;
+  return store_locked(key, std::move(sgf));
 }
 
 void StratifiedSgfCache::count_misses(uint64_t k) {
@@ -176,7 +198,9 @@ void StratifiedSgfCache::clear() {
 std::vector<std::pair<ProfileKey, std::shared_ptr<const DiscreteSGF>>>
 StratifiedSgfCache::entries() const {
   std::lock_guard<std::mutex> lk(mu_);
-  return {map_.begin(), map_.end()};
+  std::vector<std::pair<ProfileKey, std::shared_ptr<const DiscreteSGF>>> out;
+  for (const auto& [k, e] : map_) out.emplace_back(k, e.sgf);
+  return out;
 }
 
 namespace {
@@ -297,7 +321,7 @@ size_t StratifiedSgfCache::load(const std::string& path) {
     // which this build does not serve from the table; keep them out
     if (!expanded && !has_sig) {
       std::lock_guard<std::mutex> lk(mu_);
-      map_.emplace(std::move(key), std::move(sgf));
+      store_locked(key, std::move(sgf));
       ++loaded;
     }
   }

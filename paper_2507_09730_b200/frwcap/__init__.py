@@ -19,6 +19,7 @@ from .._core import sgf_cache_stats  # noqa: F401
 # single-transit API (microwalk.hpp:70-100, geometry.hpp:151-182) -- B200 extras
 from .._core import build_grid, neighbor_weights, transits_grid, transits_structure  # noqa: F401
 from .._core import transitions_json, walks_by_transitions  # noqa: F401
+from .._core import SgfCache  # noqa: F401
 
 __all__ = [
     "analytic_plate_capacitance",
