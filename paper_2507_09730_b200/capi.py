@@ -132,6 +132,10 @@ def lib():
         L.frw_sgf_clear.argtypes = [C.c_void_p]
         L.frw_sgf_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int), _dp, _dp,
                                     _dp]
+        L.frw_grid_sgf_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_double, _dp, _dp,
+                                         _dp]
+        L.frw_reference_capacitance.argtypes = [C.c_void_p, C.POINTER(StructureDesc), C.c_int,
+                                                _dp, _dp]
         L.frw_structure_transits.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _up,
                                              C.c_int32, C.POINTER(Exit)]
         L.frw_run_walks.argtypes = [C.c_void_p, C.POINTER(WalkParams), C.c_int32, C.c_uint64,
@@ -332,6 +336,24 @@ class Context:
                                          layers.ctypes.data_as(_dp), probs.ctypes.data_as(_dp),
                                          None if ker is None else ker.ctypes.data_as(_dp)))
         return probs, ker
+
+    def grid_sgf_solve(self, eps, half_width=None, kernels=True):
+        """frw_grid_sgf_solve of one or more unmasked grids ([count][n^3]):
+        probs [count][6n^2], kernels [count][3][6n^2], E[tau] [count]."""
+        eps = np.ascontiguousarray(eps, np.float64)
+        eps2 = eps.reshape(-1, eps.shape[-1]) if eps.ndim > 1 else eps[None, :]
+        n = int(round(eps2.shape[1] ** (1 / 3)))
+        cnt = eps2.shape[0]
+        hw = n / 2.0 if half_width is None else float(half_width)
+        P = 6 * n * n
+        probs = np.empty((cnt, P))
+        ker = np.empty((cnt, 3, P)) if kernels else None
+        steps = np.empty(cnt)
+        self._check(self.L.frw_grid_sgf_solve(self.h, n, cnt, eps2.ctypes.data_as(_dp), hw,
+                                              probs.ctypes.data_as(_dp),
+                                              None if ker is None else ker.ctypes.data_as(_dp),
+                                              steps.ctypes.data_as(_dp)))
+        return probs, ker, steps
 
     def sgf_count(self):
         c = C.c_int()
