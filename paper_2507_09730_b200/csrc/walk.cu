@@ -1386,9 +1386,11 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         if (live) adv_load(W, aq[item], A);
       }
     }
-    // several super-steps per transition: a hop is ~50 super-steps
+    // up to 32 super-steps per transition (a hop is ~50 super-steps): the
+    // MicroWalk lanes run long stretches between the divergent transitions
+    // (8: 1.64e7, 16: 1.76e7, 32: 1.76e7 C3 walks/s; C5 MWE best at 32)
 #pragma unroll 1
-    for (int rep = 0; rep < 8 && __any_sync(0xFFFFFFFFu, live && in_mw); ++rep) {
+    for (int rep = 0; rep < 32 && __any_sync(0xFFFFFFFFu, live && in_mw); ++rep) {
       if (!(live && in_mw)) continue;
       int xdir = 0;
       const int code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
