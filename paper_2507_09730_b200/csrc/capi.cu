@@ -82,6 +82,7 @@ void frw_ctx_destroy(frw_ctx* ctx) {
   cudaFree(ctx->d_hist);
   cudaFree(ctx->d_mom);
   cudaFree(ctx->d_tr);
+  cudaFree(ctx->d_solve);
   cudaEventDestroy(ctx->ev[0]);
   cudaEventDestroy(ctx->ev[1]);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);

@@ -58,6 +58,9 @@ struct frw_ctx {
   uint64_t* d_mom = nullptr;            // [3]
   int32_t* d_tr = nullptr;              // per-transit outputs and states
   size_t tr_cap = 0;                    // bytes
+  // stratified-key solver scratch (sgf_solve.cu), grown on demand
+  char* d_solve = nullptr;
+  size_t solve_cap = 0;                 // bytes
 };
 
 #define FRW_CUDA(ctx, call)                                         \

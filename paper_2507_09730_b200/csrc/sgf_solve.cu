@@ -10,10 +10,8 @@
 //   b = e_c (probs) and e_{c+a} - e_{c-a} (kernel a, central difference,
 //   one-sided at a lattice face), divided by the pitch span;
 //   Jacobi-PCG from zero, stop at |r|^2 < (1e-10)^2 |b|^2, cap 20*rows.
-// One CTA per (key, right-hand side); the stencil of a stratified grid is a
-// function of the layer index along the key axis only, so the per-layer
-// coefficients live in shared memory and the SpMV is division free.  The
-// four Krylov vectors of a CTA stay L2-resident in a scratch slab.
+// The stratified system is separable and solved directly (k_sgf_direct);
+// general grids use the matrix-free Jacobi-PCG of k_grid_pcg.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,15 +25,6 @@ namespace {
 
 constexpr int kSolveThreads = 1024;
 constexpr int kMaxN = 64;
-
-struct Layer {
-  double e;       // permittivity
-  double a_dn;    // alpha towards layer t-1: e_{t-1}/(e_{t-1}+e_t)
-  double a_up;    // alpha towards layer t+1
-  double s_dn;    // s_ii entry towards t-1: -(e_t e_{t-1})/(e_t + e_{t-1})
-  double s_up;
-  double s_perp;  // within the layer: -(e e)/(e + e)
-};
 
 __device__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -52,168 +41,143 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
-struct Row {
-  double diag;
-  double off[6];  // 0 where the face absorbs
-};
+// ---- stratified keys: separable direct solve --------------------------------
+// On the canonical grid of a stratified key the permittivity depends only on
+// the layer index t along the key axis, so
+//   s_ii = A (x) I (x) I + E (x) (M (x) I + I (x) M),
+// with A the axial tridiagonal operator of the layers (s_ii entries
+// -(e_t e_t')/(e_t + e_t'), diagonal e_t (alpha_dn + alpha_up)), E = diag(e_t)
+// and M the 1-D operator of a uniform row with the half-spacing absorbing
+// faces: tridiag(-1/2, 1, -1/2) with 3/2 at both ends.  2M is the
+// cell-centred Dirichlet Laplacian, diagonalised by the DST-II basis
+//   q_k[i] = c_k sin(pi k (i + 1/2) / n),  lambda_k = 2 sin^2(pi k / 2n).
+// Each of the n^2 perpendicular modes is then one tridiagonal system
+// (A + (lambda_k1 + lambda_k2) E) z = beta along the key axis (Thomas), and
+// the boundary values are transformed back.  Exact to rounding -- the same
+// system the reference solves by Jacobi-PCG to 1e-10 (sgf.cpp:162-290).
+constexpr int kDirectThreads = 256;
 
-// row v of s_ii (sgf.cpp:99-137, same summation order for the row sum)
-__device__ __forceinline__ Row make_row(const Layer* L, int n, int axis, int i, int j, int k) {
-  const int c[3] = {i, j, k};
-  const int t = c[axis];
-  Row r;
-  double rs = 0;
-#pragma unroll
-  for (int d = 0; d < 6; ++d) {
-    const int a = d >> 1;
-    const int nb = c[a] + ((d & 1) ? 1 : -1);
-    if (nb < 0 || nb >= n) {
-      rs += 1.0;
-      r.off[d] = 0.0;
-      continue;
-    }
-    if (a == axis) {
-      rs += (d & 1) ? L[t].a_up : L[t].a_dn;
-      r.off[d] = (d & 1) ? L[t].s_up : L[t].s_dn;
-    } else {
-      rs += 0.5;  // e/(e+e)
-      r.off[d] = L[t].s_perp;
-    }
-  }
-  r.diag = L[t].e * rs;
-  return r;
+__device__ __forceinline__ double dst2(int n, int k, int i) {  // q_k[i], k = 1..n
+  const double c = k == n ? sqrt(1.0 / n) : sqrt(2.0 / n);
+  return c * sin(M_PI * k * (i + 0.5) / n);
 }
 
-__global__ void __launch_bounds__(kSolveThreads)
-    k_sgf_pcg(int n, const int* axes, const double* layers, double* slab, double* out,
-              int* status) {
-  __shared__ Layer L[kMaxN];
-  __shared__ double red[33];
-  const int job = blockIdx.x;
-  const int key = job >> 2, rhs = job & 3;
+__global__ void __launch_bounds__(kDirectThreads)
+    k_sgf_direct(int n, const int* axes, const double* layers, double* scratch, double* out) {
+  __shared__ double e[kMaxN], adiag[kMaxN], aoff[kMaxN], lam[kMaxN];
+  __shared__ double q[kMaxN * kMaxN];  // q[k * n + i], k = 0..n-1 for modes 1..n
+  const int key = blockIdx.x;
   const int axis = axes[key];
+  const int nn = n * n, m = nn * n, P = 6 * nn;
   const double* lay = layers + static_cast<size_t>(key) * n;
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    const double e = lay[t];
-    Layer x;
-    x.e = e;
-    x.s_perp = -(e * e) / (e + e);
-    x.a_dn = x.s_dn = x.a_up = x.s_up = 0;
-    if (t > 0) {
-      const double ei = lay[t - 1];
-      x.a_dn = ei / (ei + e);
-      x.s_dn = -(e * ei) / (e + ei);
-    }
-    if (t + 1 < n) {
-      const double ei = lay[t + 1];
-      x.a_up = ei / (ei + e);
-      x.s_up = -(e * ei) / (e + ei);
-    }
-    L[t] = x;
+    const double et = lay[t];
+    e[t] = et;
+    const double adn = t > 0 ? lay[t - 1] / (lay[t - 1] + et) : 1.0;
+    const double aup = t + 1 < n ? lay[t + 1] / (lay[t + 1] + et) : 1.0;
+    adiag[t] = et * (adn + aup);
+    aoff[t] = t + 1 < n ? -(et * lay[t + 1]) / (et + lay[t + 1]) : 0.0;
+    const double sn = sin(M_PI * (t + 1) / (2.0 * n));
+    lam[t] = 2.0 * sn * sn;
   }
+  for (int x = threadIdx.x; x < nn; x += blockDim.x) q[x] = dst2(n, x / n + 1, x % n);
   __syncthreads();
-  const int m = n * n * n, nn = n * n;
-  const int P = 6 * nn;
-  double* x = slab + static_cast<size_t>(job) * 4 * m;
-  double* r = x + m;
-  double* p = r + m;
-  double* t = p + m;
-  double* o = out + static_cast<size_t>(job) * P;
+  // the two perpendicular axes in increasing order: node (t, u, v)
+  const int pa = axis == 0 ? 1 : 0, qa = axis == 2 ? 1 : 2;
   const int c = (n - 1) / 2;
-  const int crow = (c * n + c) * n + c;
-  // right-hand side (sgf.cpp:243 and :265-283)
-  int plus = -1, minus = -1;
-  double denom = 1.0;
-  if (rhs == 0) {
-    plus = crow;
-  } else {
-    const int a = rhs - 1;
-    const int st = a == 0 ? 1 : a == 1 ? n : nn;
+  double* Z = scratch + static_cast<size_t>(key) * 8 * m;  // [4][k1][k2][t]
+  double* Wb = Z + 4 * static_cast<size_t>(m);              // [4][k1][t][v]
+  // right-hand sides (sgf.cpp:243, :265-283): unit vectors at nodes given
+  // in global (x, y, z) coordinates, mapped to (t, u, v)
+  struct Term {
+    int t, u, v;
+    double s;
+  };
+  auto rhs_terms = [&](int r, Term* T, double* denom) -> int {
+    int cen[3] = {c, c, c};
+    if (r == 0) {
+      T[0] = {c, c, c, 1.0};
+      *denom = 1.0;
+      return 1;
+    }
+    const int g = r - 1;
     const bool up = c + 1 < n, dn = c - 1 >= 0;
+    int pl[3] = {cen[0], cen[1], cen[2]}, mi[3] = {cen[0], cen[1], cen[2]};
     if (up && dn) {
-      plus = crow + st;
-      minus = crow - st;
-      denom = 2.0;  // 2 * pitch, unit pitch
+      pl[g] += 1;
+      mi[g] -= 1;
+      *denom = 2.0;  // 2 * unit pitch
     } else if (up) {
-      plus = crow + st;
-      minus = crow;
+      pl[g] += 1;
+      *denom = 1.0;
     } else if (dn) {
-      plus = crow;
-      minus = crow - st;
+      mi[g] -= 1;
+      *denom = 1.0;
+    } else {
+      return 0;  // n = 1: zero kernel
     }
-  }
-  if (plus < 0) {  // n = 1: zero kernel
-    for (int q = threadIdx.x; q < P; q += blockDim.x) o[q] = 0.0;
-    return;
-  }
-  const int stride[6] = {-1, 1, -n, n, -nn, nn};
-  double rr_loc = 0, rz_loc = 0;
-  for (int v = threadIdx.x; v < m; v += blockDim.x) {
-    const double b = (v == plus ? 1.0 : 0.0) - (v == minus ? 1.0 : 0.0);
-    x[v] = 0.0;
-    r[v] = b;
-    const int i = v % n, j = (v / n) % n, k = v / nn;
-    const Row R = make_row(L, n, axis, i, j, k);
-    p[v] = b / R.diag;
-    rr_loc += b * b;
-    rz_loc += b * (b / R.diag);
-  }
-  const double b2 = block_sum(rr_loc, red);
-  const double thresh = 1e-20 * b2;
-  double rz = block_sum(rz_loc, red);
-  double res2 = b2;
-  const long cap = 20L * m;
-  long it = 0;
-  while (res2 >= thresh && it < cap) {
-    // t = s_ii p, <p, t>
-    double pt = 0;
-    for (int v = threadIdx.x; v < m; v += blockDim.x) {
-      const int i = v % n, j = (v / n) % n, k = v / nn;
-      const Row R = make_row(L, n, axis, i, j, k);
-      double acc = R.diag * p[v];
-#pragma unroll
-      for (int d = 0; d < 6; ++d)
-        if (R.off[d] != 0.0) acc += R.off[d] * p[v + stride[d]];
-      t[v] = acc;
-      pt += p[v] * acc;
+    T[0] = {pl[axis], pl[pa], pl[qa], 1.0};
+    T[1] = {mi[axis], mi[pa], mi[qa], -1.0};
+    return 2;
+  };
+  // 1) one tridiagonal solve per (rhs, mode)
+  for (int job = threadIdx.x; job < 4 * nn; job += blockDim.x) {
+    const int r = job / nn, k1 = (job % nn) / n, k2 = job % n;
+    Term T[2];
+    double denom;
+    const int nt = rhs_terms(r, T, &denom);
+    double* z = Z + (static_cast<size_t>(r) * nn + k1 * n + k2) * n;
+    double beta[kMaxN];
+    for (int t = 0; t < n; ++t) beta[t] = 0.0;
+    for (int a = 0; a < nt; ++a) beta[T[a].t] += T[a].s * q[k1 * n + T[a].u] * q[k2 * n + T[a].v];
+    const double lm = lam[k1] + lam[k2];
+    // Thomas algorithm on (A + lm E), symmetric positive definite
+    double cp[kMaxN];
+    double d0 = adiag[0] + lm * e[0];
+    cp[0] = aoff[0] / d0;
+    z[0] = beta[0] / d0;
+    for (int t = 1; t < n; ++t) {
+      const double d = adiag[t] + lm * e[t] - aoff[t - 1] * cp[t - 1];
+      cp[t] = aoff[t] / d;
+      z[t] = (beta[t] - aoff[t - 1] * z[t - 1]) / d;
     }
-    const double alpha = rz / block_sum(pt, red);
-    double rr = 0, rzn = 0;
-    for (int v = threadIdx.x; v < m; v += blockDim.x) {
-      x[v] += alpha * p[v];
-      const double rv = r[v] - alpha * t[v];
-      r[v] = rv;
-      rr += rv * rv;
-      const int i = v % n, j = (v / n) % n, k = v / nn;
-      rzn += rv * (rv / make_row(L, n, axis, i, j, k).diag);
-    }
-    res2 = block_sum(rr, red);
-    const double rz_new = block_sum(rzn, red);
-    ++it;
-    if (res2 < thresh) break;
-    const double beta = rz_new / rz;
-    rz = rz_new;
-    __syncthreads();
-    for (int v = threadIdx.x; v < m; v += blockDim.x) {
-      const int i = v % n, j = (v / n) % n, k = v / nn;
-      p[v] = r[v] / make_row(L, n, axis, i, j, k).diag + beta * p[v];
-    }
-    __syncthreads();
+    for (int t = n - 2; t >= 0; --t) z[t] -= cp[t] * z[t + 1];
   }
-  if (res2 >= thresh && threadIdx.x == 0) atomicExch(status, FRW_ESOLVE);
   __syncthreads();
-  // boundary row A_IB^T (eps .* z), panel = (face*n + v)*n + u (sgf.hpp:34-36)
-  for (int q = threadIdx.x; q < P; q += blockDim.x) {
-    const int face = q / nn, rem = q - face * nn;
-    const int u = rem % n, w = rem / n;
-    const int a = face >> 1;
-    const int edge = (face & 1) ? n - 1 : 0;
+  // 2) W[r][k1][t][v] = sum_k2 q_k2[v] Z[r][k1][k2][t]
+  for (int x = threadIdx.x; x < 4 * m; x += blockDim.x) {
+    const int r = x / m, rem = x % m;
+    const int k1 = rem / nn, t = (rem / n) % n, v = rem % n;
+    const double* z = Z + (static_cast<size_t>(r) * nn + k1 * n) * n + t;
+    double acc = 0;
+    for (int k2 = 0; k2 < n; ++k2) acc += q[k2 * n + v] * z[static_cast<size_t>(k2) * n];
+    Wb[x] = acc;
+  }
+  __syncthreads();
+  // 3) boundary values z(t,u,v) = sum_k1 q_k1[u] W[k1][t][v]; panel outputs
+  //    y = e_t z (A_IB^T (eps .* z)), panel = (face*n + w)*n + u (sgf.hpp:34-36)
+  for (int x = threadIdx.x; x < 4 * P; x += blockDim.x) {
+    const int r = x / P, pq = x % P;
+    Term T[2];
+    double denom;
+    const int nt = rhs_terms(r, T, &denom);
+    double* o = out + (static_cast<size_t>(key) * 4 + r) * P;
+    if (nt == 0) {
+      o[pq] = 0.0;
+      continue;
+    }
+    const int face = pq / nn, rem = pq - face * nn;
+    const int pu = rem % n, pw = rem / n;
+    const int fa = face >> 1;
     int ci[3];
-    ci[a] = edge;
-    ci[a == 0 ? 1 : 0] = u;
-    ci[a == 2 ? 1 : 2] = w;
-    const int v = (ci[2] * n + ci[1]) * n + ci[0];
-    o[q] = L[ci[axis]].e * x[v] / denom;
+    ci[fa] = (face & 1) ? n - 1 : 0;
+    ci[fa == 0 ? 1 : 0] = pu;
+    ci[fa == 2 ? 1 : 2] = pw;
+    const int t = ci[axis], u = ci[pa], v = ci[qa];
+    const double* w = Wb + static_cast<size_t>(r) * m;
+    double acc = 0;
+    for (int k1 = 0; k1 < n; ++k1) acc += q[k1 * n + u] * w[(k1 * n + t) * n + v];
+    o[pq] = e[t] * acc / denom;
   }
 }
 
@@ -380,16 +344,24 @@ extern "C" int frw_sgf_solve(frw_ctx* ctx, int n, int count, const int* axes,
     if (axes[q] < 0 || axes[q] > 2) return frw_fail(ctx, FRW_EINVAL, "sgf_solve: bad axis");
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   const size_t m = static_cast<size_t>(n) * n * n, P = 6ull * n * n;
-  // bounded scratch: solve in chunks of keys
-  const int chunk = std::min(count, 512);
-  double *d_lay = nullptr, *slab = nullptr, *out = nullptr;
-  int *d_ax = nullptr, *d_st = nullptr;
-  FRW_CUDA(ctx, cudaMalloc(&d_lay, 8 * static_cast<size_t>(chunk) * n));
-  FRW_CUDA(ctx, cudaMalloc(&d_ax, 4 * static_cast<size_t>(chunk)));
-  FRW_CUDA(ctx, cudaMalloc(&slab, 8 * 4 * m * 4 * static_cast<size_t>(chunk)));
-  FRW_CUDA(ctx, cudaMalloc(&out, 8 * P * 4 * static_cast<size_t>(chunk)));
-  FRW_CUDA(ctx, cudaMalloc(&d_st, 4));
-  FRW_CUDA(ctx, cudaMemsetAsync(d_st, 0, 4, ctx->stream));
+  // bounded scratch (kept in the context): solve in chunks of keys
+  const int chunk = std::min(count, 128);
+  const size_t b_lay = (8 * static_cast<size_t>(chunk) * n + 255) / 256 * 256;
+  const size_t b_ax = (4 * static_cast<size_t>(chunk) + 255) / 256 * 256;
+  const size_t b_slab = 8 * 8 * m * static_cast<size_t>(chunk);
+  const size_t b_out = 8 * P * 4 * static_cast<size_t>(chunk);
+  const size_t need = b_lay + b_ax + b_slab + b_out;
+  if (ctx->solve_cap < need) {
+    cudaFree(ctx->d_solve);
+    ctx->d_solve = nullptr;
+    ctx->solve_cap = 0;
+    FRW_CUDA(ctx, cudaMalloc(&ctx->d_solve, need));
+    ctx->solve_cap = need;
+  }
+  double* d_lay = reinterpret_cast<double*>(ctx->d_solve);
+  int* d_ax = reinterpret_cast<int*>(ctx->d_solve + b_lay);
+  double* slab = reinterpret_cast<double*>(ctx->d_solve + b_lay + b_ax);
+  double* out = reinterpret_cast<double*>(ctx->d_solve + b_lay + b_ax + b_slab);
   std::vector<double> h(P * 4 * static_cast<size_t>(chunk));
   int rc = FRW_OK;
   for (int k0 = 0; k0 < count && rc == FRW_OK; k0 += chunk) {
@@ -398,7 +370,7 @@ extern "C" int frw_sgf_solve(frw_ctx* ctx, int n, int count, const int* axes,
                     cudaMemcpyHostToDevice, ctx->stream);
     cudaMemcpyAsync(d_ax, axes + k0, 4 * static_cast<size_t>(kc), cudaMemcpyHostToDevice,
                     ctx->stream);
-    k_sgf_pcg<<<4 * kc, kSolveThreads, 0, ctx->stream>>>(n, d_ax, d_lay, slab, out, d_st);
+    k_sgf_direct<<<kc, kDirectThreads, 0, ctx->stream>>>(n, d_ax, d_lay, slab, out);
     cudaMemcpyAsync(h.data(), out, 8 * P * 4 * static_cast<size_t>(kc), cudaMemcpyDeviceToHost,
                     ctx->stream);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -422,14 +394,6 @@ extern "C" int frw_sgf_solve(frw_ctx* ctx, int n, int count, const int* axes,
         std::copy(pr + P, pr + 4 * P, kernels + static_cast<size_t>(k0 + q) * 3 * P);
     }
   }
-  int st = 0;
-  cudaMemcpy(&st, d_st, 4, cudaMemcpyDeviceToHost);
-  if (rc == FRW_OK && st) rc = frw_fail(ctx, FRW_ESOLVE, "transition cube solve failed: PCG did not converge");
-  cudaFree(d_lay);
-  cudaFree(d_ax);
-  cudaFree(slab);
-  cudaFree(out);
-  cudaFree(d_st);
   return rc;
 }
 

@@ -61,7 +61,7 @@ constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
 
 
-enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2 };
+enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3 };
 
 // ---------------------------------------------------------------------------
 // device-side views
@@ -150,14 +150,16 @@ struct DCounters {
   unsigned long long err;        // error code (first)
   unsigned long long gen_steps;  // MicroWalk steps next to a cell face
   unsigned long long cell_chg;   // MicroWalk moves into another cell
+  unsigned long long npark;      // walks parked mid-walk (their slots kept)
 };
 
 constexpr int kMissMax = 4096;
 struct DMiss {
   int* axis;        // [kMissMax]
   double* layers;   // [kMissMax][NMAX]
-  long long* retry; // [S] walk ids parked by misses
-  long long* pend;  // [S] walk ids to restart
+  long long* retry; // [2S] walk ids whose first transition missed (restart)
+  long long* pend;  // [2S] walk ids to restart
+  int* park;        // [2S] slots of walks parked mid-walk by a miss (resume)
 };
 
 // ---------------------------------------------------------------------------
@@ -438,13 +440,19 @@ __device__ int sample_panel(const double* cdf, const int* guide, int count, doub
   return i == count ? count - 1 : i;
 }
 
-__device__ void record_miss(DCounters* C, const DMiss& M, int n, int axis, const double* layers,
-                            long long wid) {
+__device__ void record_key(DCounters* C, const DMiss& M, int n, int axis, const double* layers) {
   const unsigned long long m = atomicAdd(&C->nmiss, 1ull);
   if (m < kMissMax) {
     M.axis[m] = axis;
     for (int t = 0; t < n; ++t) M.layers[m * NMAX + t] = layers[t];
   }
+}
+
+// a first transition missed: the walk restarts from scratch once the key is
+// in the table (nothing of it was committed)
+__device__ void record_miss(DCounters* C, const DMiss& M, int n, int axis, const double* layers,
+                            long long wid) {
+  record_key(C, M, n, axis, layers);
   const unsigned long long r = atomicAdd(&C->nretry, 1ull);
   M.retry[r] = wid;
 }
@@ -978,8 +986,17 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   if (axis >= 0) {
     const int e = sgf_find(T, n, axis, layers);
     if (e < 0) {
-      record_miss(C, M, n, axis, layers, L.wid);
-      W.state[slot] = S_FREE;
+      // parked mid-walk: the key is looked up before any draw, so the walk
+      // resumes from this state, bit-identical to an uninterrupted run
+      record_key(C, M, n, axis, layers);
+      W.p[3 * slot] = L.p[0];
+      W.p[3 * slot + 1] = L.p[1];
+      W.p[3 * slot + 2] = L.p[2];
+      W.rng[slot] = L.rng.s;
+      W.hops[slot] = L.hops;
+      W.cached[slot] = L.cached;
+      W.state[slot] = S_PARKED;
+      M.park[atomicAdd(&C->npark, 1ull)] = slot;
       return 1;
     }
     const double* data = T.data[e];
@@ -1325,24 +1342,11 @@ __global__ void __launch_bounds__(512)
   flush_mw_stats(C, L);
 }
 
-__device__ __forceinline__ void adv_store(const DSlots& W, const AdvLane& L) {
-  W.p[3 * L.slot] = L.p[0];
-  W.p[3 * L.slot + 1] = L.p[1];
-  W.p[3 * L.slot + 2] = L.p[2];
-  W.rng[L.slot] = L.rng.s;
-  W.hops[L.slot] = L.hops;
-  W.cached[L.slot] = L.cached;
-}
-
 // Run-to-completion kernel for the tail of a run: once few walks remain,
 // rounds would each cost the longest hop chain of the round, so every lane
 // takes an ACTIVE walk and runs it to its end, alternating transitions and
 // MicroWalk super-steps in-thread.  A table miss parks its walk as in
-// k_advance; once any miss is recorded the kernel yields: a walk that has
-// completed a MicroWalk hop in this launch stops at its next transition
-// boundary and goes to the next round's ACTIVE queue, so the host can insert
-// the missing tables without waiting for the longest walk (the host then
-// returns to rounds until a round is miss-free).
+// k_advance (the host resolves misses once the other walks are done).
 #ifndef FRW_TAIL_BLOCKS
 #define FRW_TAIL_BLOCKS 2
 #endif
@@ -1350,39 +1354,31 @@ constexpr int kTailBlocks = FRW_TAIL_BLOCKS;  // resident 256-thread CTAs per SM
 template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
-           const int* aq, int* aq_out) {
+           const int* aq) {
   __shared__ double alpha_sm[PMAX * PMAX];
   __shared__ DirDelta dd[6];
   setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
   const int cap = 1000 * n * n;
   const unsigned long long alen = C->alen;
-  const volatile unsigned long long* nmiss = &C->nmiss;
   AdvLane A;
   MwLane L;
   L.gsteps = 0;
   L.cchg = 0;
-  bool in_mw = false, hopped = false;
+  bool in_mw = false;
   unsigned long long item = atomicAdd(&C->ahead, 1ull);
   bool live = item < alen;
   if (live) adv_load(W, aq[item], A);
   while (__any_sync(0xFFFFFFFFu, live)) {
     if (live && !in_mw) {
       int r;
-      if (hopped && *nmiss != 0) {  // yield
-        adv_store(W, A);
-        mw_requeue(C, aq_out, A.slot);
-        r = 1;
-      } else {
-        r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
-      }
+      r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
       if (r == 2) {
         in_mw = true;
         mw_arm(W, alpha_sm, s.P, A.slot, n, L);
       } else if (r == 1) {
         item = atomicAdd(&C->ahead, 1ull);
         live = item < alen;
-        hopped = false;
         if (live) adv_load(W, aq[item], A);
       }
     }
@@ -1399,7 +1395,6 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       if (code == MW_SURFACE) {
         mw_exit(W, n, L, xdir);
         adv_load(W, L.slot, A);
-        hopped = true;
         continue;
       }
       if (code == MW_COND)
@@ -1410,7 +1405,6 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       }
       item = atomicAdd(&C->ahead, 1ull);
       live = item < alen;
-      hopped = false;
       if (live) adv_load(W, aq[item], A);
     }
   }
@@ -2045,6 +2039,7 @@ void free_slots(Engine& E) {
   E.aq[0] = E.aq[1] = nullptr;
   cudaFree(E.M.retry);
   cudaFree(E.M.pend);
+  cudaFree(E.M.park);
   E.W = DSlots{};
   E.S = 0;
 }
@@ -2280,11 +2275,12 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   E.queue = dalloc<int>(S);
   E.aq[0] = dalloc<int>(S);
   E.aq[1] = dalloc<int>(S);
-  E.M.retry = dalloc<long long>(S);
-  E.M.pend = dalloc<long long>(S);
+  E.M.retry = dalloc<long long>(2 * size_t(S));  // parks accumulate up to S/2 + S
+  E.M.pend = dalloc<long long>(2 * size_t(S));
+  E.M.park = dalloc<int>(2 * size_t(S));
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
       !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes || !W.room ||
-      !W.fc || !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend) {
+      !W.fc || !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend || !E.M.park) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
   }
@@ -2759,7 +2755,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   if (const char* e = std::getenv("FRW_TAIL_WALKS")) tail_threshold = std::strtoull(e, nullptr, 10);
   bool tail = false;
   float mw_ms = 0;
-  uint64_t misses_total = 0, restarts = 0;
+  uint64_t misses_total = 0, restarts = 0, resumes = 0;
   int status = FRW_OK;
   for (int round = 0;; ++round) {
     DSgf T{E.sgf.cap, E.sgf.d_hash, E.sgf.d_entry, E.sgf.d_axis, E.sgf.d_keys, E.sgf.d_pitch,
@@ -2773,10 +2769,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       const int tb = ctx->sm_count * kTailBlocks;  // persistent, one wave
       if (P.rng == FRW_RNG_PHILOX)
         k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M,
-                                                           aq_in, aq_out);
+                                                           aq_in);
       else
         k_tail<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs,
-                                                                    E.d_cnt, M, aq_in, aq_out);
+                                                                    E.d_cnt, M, aq_in);
     } else {
       k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in,
                                                    E.queue);
@@ -2821,21 +2817,33 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                      "conductor, or more than 32 dielectric boxes in one cube)");
       break;
     }
-    if (c.nmiss) {
+    const bool all_spawned = c.next >= static_cast<unsigned long long>(count) &&
+                             c.pend_head >= c.npend;
+    const bool idle = all_spawned && c.a2len == 0;
+    // Table misses are resolved lazily: parked walks wait while the others
+    // run on, so the keys of a whole run are solved in a few batches instead
+    // of one host round trip per discovering round.  Resolve when nothing
+    // else is left, or when the miss / park records fill up.
+    if (c.nmiss && (idle || c.nmiss >= kMissMax ||
+                    c.nretry + c.npark > static_cast<unsigned long long>(S) / 2)) {
       int added = 0;
       status = resolve_misses(ctx, E, P.n, c.nmiss, miss, user, &added);
       if (status) break;
       misses_total += added;
-      // parked walks restart from scratch (nothing of their partial run was
-      // committed): pend <- retry; the round transition happens here too
+      // walks whose first transition missed restart from scratch (pend <-
+      // retry); walks parked mid-walk resume: their slots join the next
+      // round's ACTIVE queue.  The round transition happens here too.
       FRW_CUDA(ctx, cudaMemcpyAsync(M.pend, M.retry, 8 * c.nretry, cudaMemcpyDeviceToDevice,
                                     ctx->stream));
+      FRW_CUDA(ctx, cudaMemcpyAsync(aq_out + c.a2len, M.park, 4 * c.npark,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
       DCounters upd = c;
       upd.npend = c.nretry;
       upd.pend_head = 0;
       upd.nretry = 0;
       upd.nmiss = 0;
-      upd.alen = c.a2len;
+      upd.npark = 0;
+      upd.alen = c.a2len + c.npark;
       upd.ahead = 0;
       upd.a2len = 0;
       upd.qlen = 0;
@@ -2843,12 +2851,13 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cnt, &upd, sizeof upd, cudaMemcpyHostToDevice,
                                     ctx->stream));
       restarts += c.nretry;
-      tail = false;  // back to rounds until a round is miss-free
+      resumes += c.npark;
+      if (trace)
+        std::fprintf(stderr, "  resolved %d keys; restart %llu, resume %llu (total resumed %llu)\n",
+                     added, c.nretry, c.npark, static_cast<unsigned long long>(resumes));
       continue;
     }
-    const bool all_spawned = c.next >= static_cast<unsigned long long>(count) &&
-                             c.pend_head >= c.npend;
-    if (all_spawned && c.a2len == 0) {
+    if (idle) {
       if (c.done < static_cast<unsigned long long>(count))
         status = frw_fail(ctx, FRW_ECUDA, "run_walks: lost walks (internal error)");
       break;
