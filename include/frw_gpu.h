@@ -319,6 +319,9 @@ int frw_event_elapsed_ms(frw_ctx *ctx, float *ms);
 int frw_dev_alloc(frw_ctx *ctx, size_t bytes, void **ptr);
 int frw_dev_free(frw_ctx *ctx, void *ptr);
 int frw_dev_memset(frw_ctx *ctx, void *ptr, int value, size_t bytes);
+/* Page-locked host memory (fast copies of per-walk records / outputs). */
+int frw_host_alloc(frw_ctx *ctx, size_t bytes, void **ptr);
+int frw_host_free(frw_ctx *ctx, void *ptr);
 int frw_memcpy_h2d(frw_ctx *ctx, void *dst, const void *src, size_t bytes);
 int frw_memcpy_d2h(frw_ctx *ctx, void *dst, const void *src, size_t bytes);
 

@@ -145,6 +145,19 @@ int frw_dev_free(frw_ctx* ctx, void* ptr) {
   return FRW_OK;
 }
 
+int frw_host_alloc(frw_ctx* ctx, size_t bytes, void** ptr) {
+  if (!ctx || !ptr) return FRW_EINVAL;
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  FRW_CUDA(ctx, cudaMallocHost(ptr, bytes));
+  return FRW_OK;
+}
+
+int frw_host_free(frw_ctx* ctx, void* ptr) {
+  if (!ctx) return FRW_EINVAL;
+  FRW_CUDA(ctx, cudaFreeHost(ptr));
+  return FRW_OK;
+}
+
 int frw_dev_memset(frw_ctx* ctx, void* ptr, int value, size_t bytes) {
   if (!ctx) return FRW_EINVAL;
   FRW_CUDA(ctx, cudaMemsetAsync(ptr, value, bytes, ctx->stream));

@@ -14,6 +14,7 @@
 #include <limits>
 #include <map>
 #include <mutex>
+#include <unordered_set>
 
 #include "frwcap.hpp"
 
@@ -136,6 +137,10 @@ std::map<int, Device*>& devices() {
 }
 struct DeviceTable {
   int n = 0;  // lattice size of the keys currently on the device
+  std::unordered_set<ProfileKey, ProfileKeyHash> keys;  // keys already put
+  // page-locked staging for per-walk records, kept across extract calls
+  frw_walk_record* rec = nullptr;
+  size_t rec_cap = 0;
 };
 std::map<frw_ctx*, DeviceTable>& tables() {
   static auto* m = new std::map<frw_ctx*, DeviceTable>;
@@ -143,6 +148,8 @@ std::map<frw_ctx*, DeviceTable>& tables() {
 }
 
 void put_entry(frw_ctx* ctx, const ProfileKey& k, const DiscreteSGF& g) {
+  auto& keys = tables()[ctx].keys;
+  if (keys.count(k)) return;  // on the device already (frw_sgf_put would skip it too)
   std::vector<double> kern;
   const bool has = !g.grad_kernels[0].empty();
   if (has) {
@@ -151,6 +158,7 @@ void put_entry(frw_ctx* ctx, const ProfileKey& k, const DiscreteSGF& g) {
   }
   throw_status(ctx, frw_sgf_put(ctx, k.n, k.axis, k.layers.data(), g.pitch, g.probs.data(),
                                 g.cdf.data(), has ? kern.data() : nullptr));
+  keys.insert(k);
 }
 }  // namespace
 
@@ -197,6 +205,7 @@ void Engine::upload() const {
   DeviceTable& T = tables()[ctx_];
   if (T.n != cfg_.grid_n) {
     throw_status(ctx_, frw_sgf_clear(ctx_));
+    T.keys.clear();
     T.n = cfg_.grid_n;
   }
   for (const auto& [k, g] : cache_->entries())
@@ -350,19 +359,29 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
 
   const frw_walk_params p = params();
   MissCtx mc{ctx_, cache_, {}};
-  std::vector<frw_walk_record> rec;
+  // per-walk records land in page-locked memory kept with the context
+  DeviceTable& DT = tables()[ctx_];
   std::vector<double> ts(nslots), tq(nslots);
   std::vector<uint64_t> tl(nslots);
   const long batch = cfg_.batch;
   const long dev_batch = std::max<long>(batch, cfg_.device_batch / batch * batch);
   while (walks < static_cast<uint64_t>(cfg_.max_walks) && !converged) {
     const int64_t chunk = std::min<int64_t>(dev_batch, cfg_.max_walks - static_cast<int64_t>(walks));
-    rec.resize(chunk);
+    if (DT.rec_cap < static_cast<size_t>(chunk)) {
+      if (DT.rec) frw_host_free(ctx_, DT.rec);
+      DT.rec = nullptr;
+      DT.rec_cap = 0;
+      void* mem = nullptr;
+      throw_status(ctx_, frw_host_alloc(ctx_, sizeof(frw_walk_record) * chunk, &mem));
+      DT.rec = static_cast<frw_walk_record*>(mem);
+      DT.rec_cap = chunk;
+    }
+    frw_walk_record* const rec = DT.rec;
     frw_tally t{};
     t.sum = ts.data();
     t.sumsq = tq.data();
     t.landed = tl.data();
-    const int rc = frw_run_walks(ctx_, &p, master, walks, chunk, miss_cb, &mc, &t, rec.data());
+    const int rc = frw_run_walks(ctx_, &p, master, walks, chunk, miss_cb, &mc, &t, rec);
     if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
     throw_status(ctx_, rc);
     mw_ms += t.mw_ms;
