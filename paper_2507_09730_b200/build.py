@@ -72,6 +72,29 @@ def build_core(force=False):
     return out
 
 
+def build_cpp_lib(force=False):
+    """libfrwcap.so: the C++ API mirror (csrc/host, without the Python
+    bindings) for C++ callers of the reference's frwcap API, plus the example
+    caller examples/frwcap_main."""
+    host = sorted(p for p in glob.glob(os.path.join(CSRC, "host", "*.cpp"))
+                  if not p.endswith("py_module.cpp"))
+    out = os.path.join(LIB, "libfrwcap.so")
+    exe = os.path.join(LIB, "frwcap_main")
+    deps = host + glob.glob(os.path.join(CSRC, "host", "*.hpp")) + \
+        [os.path.join(ROOT, "include", "frw_gpu.h"), os.path.join(LIB, "libfrwgpu.so")]
+    json_inc = os.path.join(sysconfig.get_paths()["purelib"],
+                            "include/cudnn_frontend/thirdparty/nlohmann")
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(CSRC, "host"), "-I", json_inc]
+    if force or _stale(out, deps):
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-ffp-contract=off", *inc,
+              "-o", out, *host, "-L", LIB, "-lfrwgpu", "-Wl,-rpath,$ORIGIN", "-lpthread"])
+    src = os.path.join(ROOT, "examples", "frwcap_main.cpp")
+    if os.path.exists(src) and (force or _stale(exe, [src, out])):
+        _run(["g++", "-O2", "-std=c++20", *inc, "-o", exe, src, "-L", LIB, "-lfrwcap",
+              "-lfrwgpu", "-Wl,-rpath,$ORIGIN", "-lpthread"])
+    return out
+
+
 def build_oracle(with_ref=None):
     tgts = ["all"]
     if with_ref is None:
@@ -84,6 +107,7 @@ def build_oracle(with_ref=None):
 def build_all(force=False):
     build_gpu_lib(force)
     build_core(force)
+    build_cpp_lib(force)
     build_oracle()
 
 
