@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -46,6 +47,7 @@ constexpr int KMAX = 64;    // clipped boxes (conductors + dielectrics) per Micr
 constexpr int NMAX = 64;    // lattice size cap (layers per key)
 constexpr int PMAX = 64;    // permittivity palette cap
 constexpr int kSlotsDefault = 1 << 20;
+constexpr int kGridMinConductors = 24;  // conductor bins above this count
 // Cell atlas of a MicroWalk job (u64 words per slot).  Along each axis the
 // clipped boxes' faces cut [0, n) into segments; bm[a] holds one bit per
 // segment start.  mask[a][s] is the set of clipped boxes (bit q = box q)
@@ -66,6 +68,25 @@ enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3 };
 // ---------------------------------------------------------------------------
 // device-side views
 
+// Uniform bin grid over the world box with per-bin conductor lists (CSR),
+// used by the conductor queries once a structure has many conductors.  A
+// box is listed in every bin its closed extent overlaps, with bins taken by
+// floor((x - lo) / bs) on host and device alike (monotone, identical
+// rounding), so every query below returns exactly the linear scan's result.
+struct DGrid {
+  int dims[3];          // 0: no grid, linear scans
+  double lo[3], bs[3];  // origin, bin size per axis
+  double bsmin;
+  const int* cstart;    // [bins + 1] conductors overlapping the bin (CSR)
+  const int* citem;
+  const int* nstart;    // [bins + 1] conductors that can be nearest to a
+  const int* nitem;     //   point of the bin (see frw_upload_structure)
+  const int* dstart;    // [bins + 1] small dielectrics overlapping the bin
+  const int* ditem;
+  const int* dlarge;    // dielectrics spanning many bins: always candidates
+  int ndlarge;
+};
+
 struct DStruct {
   int nc, nd, P, bg;
   const double* cbox;   // [nc][6]
@@ -75,6 +96,7 @@ struct DStruct {
   const double* alpha;  // [P][P]: alpha[nb*P + self] = e_nb/(e_nb+e_self)
   const double* rpal;   // [P] value rounded to 6 significant digits
   double world[6];
+  DGrid g;
 };
 
 struct DSgf {
@@ -189,7 +211,97 @@ __device__ __forceinline__ bool box_contains(const double* b, const double p[3])
 }
 
 // Structure::conductor_at (geometry.cpp:57-62): declaration index or -1
+__device__ __forceinline__ int bin_of(const DGrid& g, int a, double x) {
+  const int i = static_cast<int>(floor((x - g.lo[a]) / g.bs[a]));
+  return min(max(i, 0), g.dims[a] - 1);
+}
+
+// first declared conductor within Chebyshev distance tol of p, -1 if none:
+// its box overlaps the bins of [p - tol, p + tol]
+__device__ int grid_conductor_within(const DStruct& s, const double p[3], double tol) {
+  const DGrid& g = s.g;
+  int b0[3], b1[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b0[a] = bin_of(g, a, p[a] - tol);
+    b1[a] = bin_of(g, a, p[a] + tol);
+  }
+  int best = 0x7FFFFFFF;
+  for (int z = b0[2]; z <= b1[2]; ++z)
+    for (int y = b0[1]; y <= b1[1]; ++y)
+      for (int x = b0[0]; x <= b1[0]; ++x) {
+        const int bin = (z * g.dims[1] + y) * g.dims[0] + x;
+        for (int q = __ldg(g.cstart + bin), e = __ldg(g.cstart + bin + 1); q < e; ++q) {
+          const int c = __ldg(g.citem + q);
+          if (c < best && cheb_to(s.cbox + 6 * c, p) <= tol) best = c;
+        }
+      }
+  return best == 0x7FFFFFFF ? -1 : best;
+}
+
+// min(r, Chebyshev distance from p to every conductor) over the bin's
+// nearest-candidate list, which holds every conductor that can be closest to
+// some point of the bin (or closer than the world wall there), so the
+// minimum equals the linear scan's.  *inside: some conductor contains p
+// (such a conductor is a candidate of p's bin: its distance there is 0).
+__device__ double grid_min_cheb(const DStruct& s, const double p[3], double r, bool* inside) {
+  const DGrid& g = s.g;
+  const int bin = (bin_of(g, 2, p[2]) * g.dims[1] + bin_of(g, 1, p[1])) * g.dims[0] +
+                  bin_of(g, 0, p[0]);
+  for (int q = __ldg(g.nstart + bin), e = __ldg(g.nstart + bin + 1); q < e; ++q) {
+    const double d = cheb_to(s.cbox + 6 * __ldg(g.nitem + q), p);
+    if (d <= 0) *inside = true;
+    if (d <= r) r = d;
+  }
+  return r;
+}
+
+// Candidates for "every box of a kind meeting the closed region [lo, hi]",
+// ascending declaration order, deduplicated: the boxes listed in the bins the
+// region overlaps (plus, for dielectrics, the large ones).  Returns -1 when
+// there is no grid, the region spans too many bins or the list overflows:
+// the caller then scans every box, so results never depend on the bins.
+constexpr int kCandMax = 96;
+constexpr int kCandBins = 64;
+__device__ __forceinline__ bool cand_insert(int* a, int& n, int v) {
+  int i = n;
+  while (i > 0 && a[i - 1] > v) --i;
+  if (i > 0 && a[i - 1] == v) return true;
+  if (n == kCandMax) return false;
+  for (int j = n; j > i; --j) a[j] = a[j - 1];
+  a[i] = v;
+  ++n;
+  return true;
+}
+__device__ int grid_candidates(const DStruct& s, bool diel, const double* cb, int* out) {
+  const DGrid& g = s.g;
+  if (!g.dims[0]) return -1;
+  int b0[3], b1[3], nb = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b0[a] = bin_of(g, a, cb[a]);
+    b1[a] = bin_of(g, a, cb[3 + a]);
+    nb *= b1[a] - b0[a] + 1;
+  }
+  if (nb > kCandBins) return -1;
+  const int* st = diel ? g.dstart : g.cstart;
+  const int* it = diel ? g.ditem : g.citem;
+  int n = 0;
+  if (diel)
+    for (int q = 0; q < g.ndlarge; ++q)
+      if (!cand_insert(out, n, __ldg(g.dlarge + q))) return -1;
+  for (int z = b0[2]; z <= b1[2]; ++z)
+    for (int y = b0[1]; y <= b1[1]; ++y)
+      for (int x = b0[0]; x <= b1[0]; ++x) {
+        const int bin = (z * g.dims[1] + y) * g.dims[0] + x;
+        for (int q = __ldg(st + bin), e = __ldg(st + bin + 1); q < e; ++q)
+          if (!cand_insert(out, n, __ldg(it + q))) return -1;
+      }
+  return n;
+}
+
 __device__ int conductor_at(const DStruct& s, const double p[3], double tol) {
+  if (s.g.dims[0]) return grid_conductor_within(s, p, tol);
   for (int c = 0; c < s.nc; ++c)
     if (cheb_to(s.cbox + 6 * c, p) <= tol) return c;
   return -1;
@@ -200,6 +312,13 @@ __device__ int conductor_at(const DStruct& s, const double p[3], double tol) {
 __device__ bool max_free_cube(const DStruct& s, const double p[3], double* h) {
   double r = cheb_wall(s.world, p);
   if (r <= 0) return false;
+  if (s.g.dims[0]) {
+    bool inside = false;
+    r = grid_min_cheb(s, p, r, &inside);
+    if (inside) return false;
+    *h = r;
+    return true;
+  }
   for (int c = 0; c < s.nc; ++c) {
     const double d = cheb_to(s.cbox + 6 * c, p);
     if (d <= 0) return false;
@@ -216,6 +335,16 @@ __device__ bool max_free_cube(const DStruct& s, const double p[3], double* h) {
 // snap test first, so max_free_cube's inside-conductor throw cannot fire.)
 __device__ int hop_scan(const DStruct& s, const double p[3], double snap, double* h) {
   const double wall = cheb_wall(s.world, p);
+  if (s.g.dims[0]) {
+    const int c = grid_conductor_within(s, p, snap);
+    if (c >= 0) return c;
+    if (wall <= snap) return -1;
+    bool inside = false;
+    const double r = grid_min_cheb(s, p, wall, &inside);
+    if (r <= 0) return -2;
+    *h = r;
+    return -3;
+  }
   double r = wall;
   for (int c = 0; c < s.nc; ++c) {
     const double d = cheb_to(s.cbox + 6 * c, p);
@@ -232,6 +361,21 @@ __device__ int hop_scan(const DStruct& s, const double p[3], double snap, double
 // -1 outside the world
 __device__ int eps_class_at(const DStruct& s, const double p[3]) {
   if (!box_contains(s.world, p)) return -1;
+  if (s.g.dims[0]) {  // the last declared box containing p: max index among candidates
+    const DGrid& g = s.g;
+    int best = -1;
+    for (int q = 0; q < g.ndlarge; ++q) {
+      const int d = __ldg(g.dlarge + q);
+      if (d > best && box_contains(s.dbox + 6 * d, p)) best = d;
+    }
+    const int bin = (bin_of(g, 2, p[2]) * g.dims[1] + bin_of(g, 1, p[1])) * g.dims[0] +
+                    bin_of(g, 0, p[0]);
+    for (int q = __ldg(g.dstart + bin), e = __ldg(g.dstart + bin + 1); q < e; ++q) {
+      const int d = __ldg(g.ditem + q);
+      if (d > best && box_contains(s.dbox + 6 * d, p)) best = d;
+    }
+    return best < 0 ? s.bg : __ldg(s.dcls + best);
+  }
   int cls = s.bg;
   for (int d = 0; d < s.nd; ++d)
     if (box_contains(s.dbox + 6 * d, p)) cls = __ldg(s.dcls + d);
@@ -334,7 +478,10 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
   int nh = 0;
   bool overflow = false;
   bool cov[3] = {true, true, true};
-  for (int d = 0; d < s.nd; ++d) {
+  int cand[kCandMax];
+  const int ncand = grid_candidates(s, true, cb, cand);
+  for (int i = 0, ni = ncand < 0 ? s.nd : ncand; i < ni; ++i) {
+    const int d = ncand < 0 ? i : cand[i];
     const double* b = s.dbox + 6 * d;
     double bb[6];
 #pragma unroll
@@ -640,7 +787,10 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
   uint64_t* A = W.atlas + static_cast<size_t>(slot) * kAtlasWords;
   int K = 0;
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
-  for (int q = 0; conductors && q < s.nc; ++q) {
+  int cand[kCandMax];
+  const int ccand = conductors ? grid_candidates(s, false, cb, cand) : 0;
+  for (int i = 0, ni = !conductors ? 0 : (ccand < 0 ? s.nc : ccand); i < ni; ++i) {
+    const int q = ccand < 0 ? i : cand[i];
     const double* b = s.cbox + 6 * q;
     double bb[6];
 #pragma unroll
@@ -664,7 +814,9 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
   }
   const int ncond = K;
   uint8_t* cls = reinterpret_cast<uint8_t*>(A + kAtCls);
-  for (int d = 0; d < s.nd; ++d) {
+  const int dcand = grid_candidates(s, true, cb, cand);
+  for (int i = 0, ni = dcand < 0 ? s.nd : dcand; i < ni; ++i) {
+    const int d = dcand < 0 ? i : cand[i];
     const double* b = s.dbox + 6 * d;
     double bb[6];
 #pragma unroll
@@ -751,7 +903,11 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
     // build_grid + slice means (engine.cpp:228-265), summed in the
     // reference's loop order so the means are bit-identical
     int K = 0;
-    for (int d = 0; d < s.nd; ++d) {
+    int cand[kCandMax];
+    const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
+    const int dcand = grid_candidates(s, true, cb, cand);
+    for (int i = 0, ni = dcand < 0 ? s.nd : dcand; i < ni; ++i) {
+      const int d = dcand < 0 ? i : cand[i];
       const double* b = s.dbox + 6 * d;
       if (__ldg(b) > c[0] + h || __ldg(b + 3) < c[0] - h || __ldg(b + 1) > c[1] + h ||
           __ldg(b + 4) < c[1] - h || __ldg(b + 2) > c[2] + h || __ldg(b + 5) < c[2] - h)
@@ -1994,6 +2150,14 @@ struct Engine {
          *d_rpal = nullptr;
   uint8_t* d_dcls = nullptr;
   bool have_structure = false;
+  DGrid grid{};             // conductor bins (dims 0: none)
+  int* d_cstart = nullptr;
+  int* d_citem = nullptr;
+  int* d_nstart = nullptr;
+  int* d_nitem = nullptr;
+  int* d_dstart = nullptr;
+  int* d_ditem = nullptr;
+  int* d_dlarge = nullptr;
   SgfHost sgf;
   // slots
   int S = 0;
@@ -2048,6 +2212,13 @@ void engine_free(frw_ctx* ctx) {
   Engine* E = static_cast<Engine*>(ctx->walk);
   if (!E) return;
   cudaFree(E->d_cbox);
+  cudaFree(E->d_cstart);
+  cudaFree(E->d_citem);
+  cudaFree(E->d_nstart);
+  cudaFree(E->d_nitem);
+  cudaFree(E->d_dstart);
+  cudaFree(E->d_ditem);
+  cudaFree(E->d_dlarge);
   cudaFree(E->d_dbox);
   cudaFree(E->d_pal);
   cudaFree(E->d_alpha);
@@ -2155,6 +2326,13 @@ void sgf_insert_index(SgfHost& T, uint64_t h, int e) {
   while (T.entry[j] >= 0) j = (j + 1) & (T.cap - 1);
   T.hash[j] = h;
   T.entry[j] = e;
+}
+
+DStruct make_dstruct(const Engine& E) {
+  DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal,
+            {}, E.grid};
+  std::memcpy(s.world, E.world, sizeof s.world);
+  return s;
 }
 
 DParams params_of(const frw_walk_params* prm) {
@@ -2328,8 +2506,7 @@ int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double
     E.M.layers = dalloc<double>(size_t(kMissMax) * NMAX);
   }
   if (int rc = sgf_sync(ctx, E.sgf)) return rc;
-  DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal, {}};
-  std::memcpy(s.world, E.world, sizeof s.world);
+  const DStruct s = make_dstruct(E);
   DParams P = params_of(prm);
   P.rng = FRW_RNG_SPLITMIX_PARITY;  // the caller's SplitMix64 streams
   P.count = count;
@@ -2467,6 +2644,180 @@ int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
                                 ctx->stream));
   FRW_CUDA(ctx, cudaMemcpyAsync(E.d_rpal, rpal.data(), 8 * P, cudaMemcpyHostToDevice,
                                 ctx->stream));
+  // conductor bins for many-conductor structures (C5: 200 conductors)
+  cudaFree(E.d_cstart);
+  cudaFree(E.d_citem);
+  cudaFree(E.d_nstart);
+  cudaFree(E.d_nitem);
+  cudaFree(E.d_dstart);
+  cudaFree(E.d_ditem);
+  cudaFree(E.d_dlarge);
+  E.d_cstart = E.d_citem = E.d_nstart = E.d_nitem = nullptr;
+  E.d_dstart = E.d_ditem = E.d_dlarge = nullptr;
+  E.grid = DGrid{};
+  int grid_min = kGridMinConductors;  // FRW_GRID_MIN overrides (tests force the bins)
+  if (const char* e = std::getenv("FRW_GRID_MIN")) grid_min = std::atoi(e);
+  if (s->n_cond > grid_min) {
+    DGrid g{};
+    double ext[3], vol = 1;
+    for (int a = 0; a < 3; ++a) {
+      g.lo[a] = s->world[a];
+      ext[a] = s->world[3 + a] - s->world[a];
+      vol *= ext[a];
+    }
+    const double target = std::min(std::max(32.0 * s->n_cond, 512.0), 262144.0);
+    const double b = std::cbrt(vol / target);
+    g.bsmin = 1e300;
+    for (int a = 0; a < 3; ++a) {
+      g.dims[a] = static_cast<int>(std::min(256.0, std::max(1.0, std::round(ext[a] / b))));
+      g.bs[a] = ext[a] / g.dims[a];
+      g.bsmin = std::min(g.bsmin, g.bs[a]);
+    }
+    const size_t bins = static_cast<size_t>(g.dims[0]) * g.dims[1] * g.dims[2];
+    auto bin1 = [&](int a, double x) {  // bin_of, host copy of the same arithmetic
+      const int i = static_cast<int>(std::floor((x - g.lo[a]) / g.bs[a]));
+      return std::min(std::max(i, 0), g.dims[a] - 1);
+    };
+    std::vector<int> count(bins + 1, 0), start(bins + 1, 0), item;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) {
+        for (size_t q = 0; q < bins; ++q) start[q + 1] = start[q] + count[q];
+        item.assign(start[bins], 0);
+        std::fill(count.begin(), count.end(), 0);
+      }
+      for (int c = 0; c < s->n_cond; ++c) {
+        const double* bx = s->cond_box + 6 * c;
+        const int x0 = bin1(0, bx[0]), x1 = bin1(0, bx[3]), y0 = bin1(1, bx[1]),
+                  y1 = bin1(1, bx[4]), z0 = bin1(2, bx[2]), z1 = bin1(2, bx[5]);
+        for (int z = z0; z <= z1; ++z)
+          for (int y = y0; y <= y1; ++y)
+            for (int x = x0; x <= x1; ++x) {
+              const size_t bin = (static_cast<size_t>(z) * g.dims[1] + y) * g.dims[0] + x;
+              if (pass == 1) item[start[bin] + count[bin]] = c;
+              ++count[bin];
+            }
+      }
+    }
+    // Nearest candidates of a bin B (slightly inflated against rounding in
+    // the point-to-bin map): with bound = min(min_c maxdist(B, c), an upper
+    // bound of the wall distance over B), every conductor with
+    // mindist(B, c) <= bound.  For p in B the nearest conductor c* has
+    // mindist(B, c*) <= d(p, c*) <= d(p, c') <= maxdist(B, c') for all c',
+    // and conductors beyond the wall distance cannot lower min(wall, d).
+    std::vector<int> nstart(bins + 1, 0), nitem;
+    {
+      double wext = 0;
+      for (int a = 0; a < 3; ++a) wext = std::max(wext, s->world[3 + a] - s->world[a]);
+      const double slack = 1e-9 * wext;
+      std::vector<double> mind(s->n_cond);
+      for (int z = 0; z < g.dims[2]; ++z)
+        for (int y = 0; y < g.dims[1]; ++y)
+          for (int x = 0; x < g.dims[0]; ++x) {
+            const int bi[3] = {x, y, z};
+            double blo[3], bhi[3];
+            for (int a = 0; a < 3; ++a) {
+              blo[a] = g.lo[a] + bi[a] * g.bs[a] - slack;
+              bhi[a] = g.lo[a] + (bi[a] + 1) * g.bs[a] + slack;
+            }
+            double wall = 1e300;  // upper bound of the wall distance over B
+            for (int a = 0; a < 3; ++a) {
+              const double wl = s->world[a], wh = s->world[3 + a], mid = 0.5 * (wl + wh);
+              const double t = (blo[a] <= mid && mid <= bhi[a])
+                                   ? 0.5 * (wh - wl)
+                                   : std::max(std::min(blo[a] - wl, wh - blo[a]),
+                                              std::min(bhi[a] - wl, wh - bhi[a]));
+              wall = std::min(wall, t);
+            }
+            double bound = wall;
+            for (int c = 0; c < s->n_cond; ++c) {
+              const double* bx = s->cond_box + 6 * c;
+              double mn = 0, mx = 0;
+              for (int a = 0; a < 3; ++a) {
+                mn = std::max(mn, std::max(bx[a] - bhi[a], blo[a] - bx[3 + a]));
+                mx = std::max(mx, std::max(bx[a] - blo[a], bhi[a] - bx[3 + a]));
+              }
+              mind[c] = mn;
+              bound = std::min(bound, mx);
+            }
+            const size_t bin = (static_cast<size_t>(z) * g.dims[1] + y) * g.dims[0] + x;
+            for (int c = 0; c < s->n_cond; ++c)
+              if (mind[c] <= bound + slack) nitem.push_back(c);
+            nstart[bin + 1] = static_cast<int>(nitem.size());
+          }
+    }
+    // dielectrics: those spanning more than a quarter of the bins (layers)
+    // are always candidates; the others are listed in the bins they overlap
+    std::vector<int> dlarge, dcount(bins, 0), dstart(bins + 1, 0), ditem;
+    {
+      std::vector<std::array<int, 6>> rng(s->n_diel);
+      for (int d = 0; d < s->n_diel; ++d) {
+        const double* bx = s->diel_box + 6 * d;
+        rng[d] = {bin1(0, bx[0]), bin1(1, bx[1]), bin1(2, bx[2]),
+                  bin1(0, bx[3]), bin1(1, bx[4]), bin1(2, bx[5])};
+        const size_t cnt = static_cast<size_t>(rng[d][3] - rng[d][0] + 1) *
+                           (rng[d][4] - rng[d][1] + 1) * (rng[d][5] - rng[d][2] + 1);
+        if (cnt * 4 > bins) {
+          dlarge.push_back(d);
+          rng[d][0] = -1;  // not binned
+        }
+      }
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+          for (size_t q = 0; q < bins; ++q) dstart[q + 1] = dstart[q] + dcount[q];
+          ditem.assign(dstart[bins], 0);
+          std::fill(dcount.begin(), dcount.end(), 0);
+        }
+        for (int d = 0; d < s->n_diel; ++d) {
+          if (rng[d][0] < 0) continue;
+          for (int z = rng[d][2]; z <= rng[d][5]; ++z)
+            for (int y = rng[d][1]; y <= rng[d][4]; ++y)
+              for (int x = rng[d][0]; x <= rng[d][3]; ++x) {
+                const size_t bin = (static_cast<size_t>(z) * g.dims[1] + y) * g.dims[0] + x;
+                if (pass == 1) ditem[dstart[bin] + dcount[bin]] = d;
+                ++dcount[bin];
+              }
+        }
+      }
+    }
+    E.d_cstart = dalloc<int>(bins + 1);
+    E.d_citem = dalloc<int>(std::max<size_t>(item.size(), 1));
+    E.d_nstart = dalloc<int>(bins + 1);
+    E.d_nitem = dalloc<int>(std::max<size_t>(nitem.size(), 1));
+    E.d_dstart = dalloc<int>(bins + 1);
+    E.d_ditem = dalloc<int>(std::max<size_t>(ditem.size(), 1));
+    E.d_dlarge = dalloc<int>(std::max<size_t>(dlarge.size(), 1));
+    if (!E.d_cstart || !E.d_citem || !E.d_nstart || !E.d_nitem || !E.d_dstart || !E.d_ditem ||
+        !E.d_dlarge)
+      return frw_fail(ctx, FRW_ENOMEM, "upload_structure: bin allocation failed");
+    FRW_CUDA(ctx, cudaMemcpyAsync(E.d_dstart, dstart.data(), 4 * (bins + 1),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    if (!ditem.empty())
+      FRW_CUDA(ctx, cudaMemcpyAsync(E.d_ditem, ditem.data(), 4 * ditem.size(),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+    if (!dlarge.empty())
+      FRW_CUDA(ctx, cudaMemcpyAsync(E.d_dlarge, dlarge.data(), 4 * dlarge.size(),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+    g.dstart = E.d_dstart;
+    g.ditem = E.d_ditem;
+    g.dlarge = E.d_dlarge;
+    g.ndlarge = static_cast<int>(dlarge.size());
+    FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cstart, start.data(), 4 * (bins + 1), cudaMemcpyHostToDevice,
+                                  ctx->stream));
+    if (!item.empty())
+      FRW_CUDA(ctx, cudaMemcpyAsync(E.d_citem, item.data(), 4 * item.size(),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+    FRW_CUDA(ctx, cudaMemcpyAsync(E.d_nstart, nstart.data(), 4 * (bins + 1),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    if (!nitem.empty())
+      FRW_CUDA(ctx, cudaMemcpyAsync(E.d_nitem, nitem.data(), 4 * nitem.size(),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+    FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+    g.cstart = E.d_cstart;
+    g.citem = E.d_citem;
+    g.nstart = E.d_nstart;
+    g.nitem = E.d_nitem;
+    E.grid = g;
+  }
   E.nc = s->n_cond;
   E.nd = s->n_diel;
   E.P = P;
@@ -2589,8 +2940,7 @@ int frw_structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
     release();
     return frw_fail(ctx, FRW_ENOMEM, "transits: device allocation failed");
   }
-  DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal, {}};
-  std::memcpy(s.world, E.world, sizeof s.world);
+  const DStruct s = make_dstruct(E);
   DParams P{};
   P.n = n;
   P.panels = 6 * n * n;
@@ -2736,8 +3086,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   }
   if (int rc = sgf_sync(ctx, E.sgf)) return rc;
 
-  DStruct s{E.nc, E.nd, E.P, E.bg, E.d_cbox, E.d_dbox, E.d_dcls, E.d_pal, E.d_alpha, E.d_rpal, {}};
-  std::memcpy(s.world, E.world, sizeof s.world);
+  const DStruct s = make_dstruct(E);
   DParams P = params_of(prm);
   P.walk_begin = walk_begin;
   P.count = count;

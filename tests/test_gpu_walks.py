@@ -39,6 +39,7 @@ CASES = {
     "stratified_stack": (lambda: scenes.load_fixture("stratified_stack"), 24),
     "c3": (lambda: _scene(c3_structure()), 24),
     "c4": (lambda: _scene(c4_structure()), 24),
+    "c5": (lambda: _scene(c5_structure()), 24),
 }
 
 
@@ -51,8 +52,10 @@ def test_walks_bit_exact_vs_oracle(gpu_ctx, oracle, case, mode):
     make, n = CASES[case]
     sc = make()
     count = 600 if n == 24 else 2000
-    if mode == "HYBRID-MWE" and case in ("c3", "c4"):
+    if mode == "HYBRID-MWE" and case in ("c3", "c4", "c5"):
         count = 300  # expanded cubes: the oracle classifies far more voxels
+    if case == "c5":
+        count = 200  # 200 conductors / 254 dielectrics: the oracle scans them all
     upload_scene(gpu_ctx, sc)
     gpu_ctx.sgf_clear()
     p = walk_params(sc, grid_n=n, seed=77, rng=PARITY, n_slots=4096, mode=MODES[mode])

@@ -7,7 +7,7 @@ from paper_2507_09730_b200.workloads import c3_structure, c4_structure, c5_struc
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 walks = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
 doc = json.dumps({"c3": c3_structure, "c4": c4_structure, "c5": c5_structure}[name]())
-kw = dict(mode="HYBRID-MW", seed=7)
+kw = dict(mode=os.environ.get("FRW_MODE", "HYBRID-MW"), seed=7)
 frwcap.extract_json(doc, min_walks=walks, max_walks=walks, **kw)   # warm table
 r = frwcap.extract_json(doc, min_walks=walks, max_walks=walks, **kw)
 print(name, "device s", r["t_device_seconds"], "mw s", r["t_mw_seconds"], "misses", r["cache"]["misses"])
