@@ -471,6 +471,8 @@ __device__ __forceinline__ double uniform(const DParams& P, long long wid, Rng& 
 
 // returns the key axis (0..2) and rounded layers, or -1 (general cube),
 // -2 (error: slice centre outside the world)
+__device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih);
+
 __device__ int stratified_key(const DStruct& s, const double c[3], double h, int n,
                               double* layers) {
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
@@ -516,27 +518,33 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
   // Every hit box covers the cube's cross-section, so it contains the slice
   // centre's other two coordinates (the cube centre) and, the cube lying in
   // the world, so does the world box: only the axis coordinate decides.
-  double hl[KMAX], hh[KMAX];
-  if (!overflow)
+  // slice classes: paint each hit's slice range in declaration order (later
+  // boxes win); clip_axis finds exactly the slices whose centre
+  // c - h + (t + 0.5) pitch lies in [lo, hi], the reference's inclusion test
+  int scls[NMAX];
+  if (!overflow) {
+    for (int t = 0; t < n; ++t) scls[t] = s.bg;
     for (int q = 0; q < nh; ++q) {
-      hl[q] = __ldg(s.dbox + 6 * hits[q] + axis);
-      hh[q] = __ldg(s.dbox + 6 * hits[q] + 3 + axis);
+      int lo, hi;
+      clip_axis(c[axis], h, n, __ldg(s.dbox + 6 * hits[q] + axis),
+                __ldg(s.dbox + 6 * hits[q] + 3 + axis), &lo, &hi);
+      const int cq = __ldg(s.dcls + hits[q]);
+      for (int t = lo; t <= hi; ++t) scls[t] = cq;
     }
+  }
   for (int t = 0; t < n; ++t) {
-    double p[3] = {c[0], c[1], c[2]};
-    p[axis] = c[axis] - h + (t + 0.5) * pitch;
     int cls;
     if (!overflow) {
-      cls = s.bg;
-      for (int q = 0; q < nh; ++q)
-        if (p[axis] >= hl[q] && p[axis] <= hh[q]) cls = __ldg(s.dcls + hits[q]);
+      cls = scls[t];
     } else {
+      double p[3] = {c[0], c[1], c[2]};
+      p[axis] = c[axis] - h + (t + 0.5) * pitch;
       cls = eps_class_at(s, p);
       if (cls < 0) return -2;
     }
     if (t == 0) cls0 = cls;
     // StratifiedProfile::uniform() compares raw permittivities
-    if (!eps_equal(__ldg(s.pal + cls), __ldg(s.pal + cls0))) uniform = false;
+    if (cls != cls0 && !eps_equal(__ldg(s.pal + cls), __ldg(s.pal + cls0))) uniform = false;
     layers[t] = __ldg(s.rpal + cls);  // round_sig(layer, 6), host-exact
   }
   if (uniform) axis = 0;
