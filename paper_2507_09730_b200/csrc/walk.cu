@@ -1259,7 +1259,7 @@ __device__ __forceinline__ void lane_alphas(const double* alpha_sm, int Pn, MwLa
 #pragma unroll
   for (int d = 0; d < 6; ++d) {
     const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-    L.al[d] = cn >= kCond ? 1.0 : alpha_sm[cn * Pn + c0];
+    L.al[d] = alpha_sm[cn >= kCond ? PMAX * PMAX : cn * Pn + c0];
   }
 }
 
@@ -1386,8 +1386,11 @@ __device__ __forceinline__ int mw_step(const DParams& P, const DirDelta* dd, MwL
   return 0;
 }
 
+// alpha_sm: the palette-pair alphas, then alpha 1 (absorbing faces) at
+// index PMAX*PMAX so a face alpha is one unconditional shared load
 __device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* dd) {
   for (int i = threadIdx.x; i < s.P * s.P; i += blockDim.x) alpha_sm[i] = __ldg(s.alpha + i);
+  if (threadIdx.x == 0) alpha_sm[PMAX * PMAX] = 1.0;
   if (threadIdx.x < 6) {
     const int d = threadIdx.x, a = d >> 1;
     DirDelta x;
@@ -1474,7 +1477,7 @@ template <int RNG>
 __global__ void __launch_bounds__(512)
     k_mw(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* queue,
          int* aq_out) {
-  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];
   __shared__ DirDelta dd[6];
   setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
@@ -1519,7 +1522,7 @@ template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
            const int* aq) {
-  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];
   __shared__ DirDelta dd[6];
   setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
@@ -1590,7 +1593,7 @@ static_assert(sizeof(DevExit) == sizeof(frw_exit), "exit layout");
 __global__ void __launch_bounds__(128)
     k_transits(DStruct s, DParams P, DSlots W, DCounters* C, const double* cubes,
                const uint64_t* states, int count, int with_cond, int cap, DevExit* out) {
-  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];
   __shared__ DirDelta dd[6];
   setup_smem_tables(s, alpha_sm, dd);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1696,7 +1699,7 @@ __global__ void __launch_bounds__(128)
     k_transition_single(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C,
                         DMiss M, const double* pts, uint64_t* states, const int* idx, int count,
                         int* rc_out, DevEvent* out) {
-  __shared__ double alpha_sm[PMAX * PMAX];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];
   __shared__ DirDelta dd[6];
   setup_smem_tables(s, alpha_sm, dd);
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
