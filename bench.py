@@ -405,6 +405,19 @@ def run_gpu(args):
         "device": ctx.name,
     }
     if walks is not None:
+        # SURVEY.md §8(d) algorithmic bytes per walk: 56 B per MicroWalk step,
+        # 8 B x 12 per CDF inversion (cached hops and the first transition),
+        # 4 x 8 B for the first-transition kernel/prob/eps reads
+        d = walks["dispatch_rank0_last"]
+        inversions = (d["subsequent"]["cached"] + sum(d["first"].values())) / args.walks
+        bpw = 56.0 * walks["mw_steps_per_walk"] + 96.0 * inversions + 32.0
+        ach = bpw * walks["value"] / 1e9
+        walks["roofline"] = {"bound": "smem", "achieved": ach, "peak": smem_peak / 1e9,
+                             "unit": "GB/s", "frac": ach * 1e9 / smem_peak,
+                             "algorithmic_bytes_per_walk": bpw,
+                             "note": "whole engine (all walk kernels) over device time; the "
+                                     "geometry queries, table lookups and divergence are the "
+                                     "gap to the on-chip roofline"}
         out["walk_engine"] = walks
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(seconds=args.ref_seconds)

@@ -1,0 +1,73 @@
+"""Run every BASELINE.json config at its stated size on one device and write
+a JSON summary (profiles/r01_configs.json): C1/C2 transits/s, C3 walks/s and
+capacitances, C4 under the all-couplings stopping rule, C5 as 10 masters x
+1e7 walks (1e8 walks, HYBRID-MW, N=24)."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2507_09730_b200.frwcap as frwcap
+from paper_2507_09730_b200 import capi
+from paper_2507_09730_b200.workloads import c1_grid, c2_grid, c3_structure, c4_structure, c5_structure
+
+out = {}
+ctx = capi.Context(0)
+for name, (eps, c, h, _), count in (("C1", c1_grid(1), 1_000_000), ("C2", c2_grid(1), 10_000_000)):
+    ctx.upload_grid(eps, c, h)
+    n = ctx.n
+    hist = ctx.alloc(6 * n * n * 8); mom = ctx.alloc(32)
+    for it in range(3):
+        ctx.memset(hist, 6 * n * n * 8); ctx.memset(mom, 32)
+        ctx.event_record(0)
+        ctx.microwalk_batch_dev(count, hist, mom, seed=it + 1, rng=capi.RNG_PHILOX)
+        ctx.event_record(1)
+        ms = ctx.elapsed_ms()
+    m = np.zeros(4, np.uint64); ctx.d2h(m, mom)
+    out[name] = {"transits": count, "ms": ms, "transits_per_s": count / ms * 1e3,
+                 "mean_steps": int(m[0]) / count}
+    print(name, out[name], flush=True)
+
+def row(res):
+    return {str(t["conductor_id"]): [t["capacitance_farads"], t["std_err_farads"]]
+            for t in res["terminals"]}
+
+doc3 = json.dumps(c3_structure())
+frwcap.extract_json(doc3, mode="HYBRID-MW", min_walks=100000, max_walks=100000, seed=99)
+t = time.time()
+r = frwcap.extract_json(doc3, mode="HYBRID-MW", min_walks=1_000_000, max_walks=1_000_000, seed=1)
+out["C3"] = {"walks": r["walks"], "wall_s": time.time() - t, "device_s": r["t_device_seconds"],
+             "walks_per_s_device": r["walks"] / r["t_device_seconds"], "row_farads": row(r)}
+print("C3", out["C3"]["walks_per_s_device"], flush=True)
+
+doc4 = json.dumps(c4_structure())
+t = time.time()
+r = frwcap.extract_json(doc4, mode="HYBRID-MW", all_couplings=True, tol=0.01,
+                        min_walks=100000, max_walks=50_000_000, seed=2)
+out["C4"] = {"walks": r["walks"], "converged": r["converged"], "wall_s": time.time() - t,
+             "device_s": r["t_device_seconds"], "walks_per_s_device": r["walks"] / r["t_device_seconds"],
+             "rule": "every coupling rel. SE <= 1% (all_couplings)", "row_farads": row(r)}
+print("C4", out["C4"]["walks"], out["C4"]["converged"], out["C4"]["walks_per_s_device"], flush=True)
+
+c5 = c5_structure()
+ids = [c["id"] for c in c5["conductors"]][:10]
+rows, dev, wall, walks = {}, 0.0, 0.0, 0
+for mid in ids:
+    c5["master"] = mid
+    t = time.time()
+    r = frwcap.extract_json(json.dumps(c5), mode="HYBRID-MW", min_walks=10_000_000,
+                            max_walks=10_000_000, seed=3 + mid)
+    wall += time.time() - t
+    dev += r["t_device_seconds"]
+    walks += r["walks"]
+    self_c = next(x for x in r["terminals"] if x["conductor_id"] == mid)
+    coup = sum(abs(x["capacitance_farads"]) for x in r["terminals"]
+               if x["conductor_id"] not in (mid, -1))
+    rows[str(mid)] = {"self_farads": self_c["capacitance_farads"],
+                      "self_rel_se": self_c["std_err_farads"] / self_c["capacitance_farads"],
+                      "sum_abs_couplings_farads": coup,
+                      "ground_farads": next(x for x in r["terminals"] if x["conductor_id"] == -1)["capacitance_farads"]}
+    print("C5 master", mid, rows[str(mid)], flush=True)
+out["C5"] = {"masters": ids, "walks": walks, "wall_s": wall, "device_s": dev,
+             "walks_per_s_device": walks / dev, "walks_per_s_wall": walks / wall, "rows": rows}
+print("C5", out["C5"]["walks_per_s_device"], out["C5"]["walks_per_s_wall"], flush=True)
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump(out, open("gpurun_out/configs.json", "w"), indent=1)
