@@ -32,6 +32,8 @@ def _scene(doc):
 
 CASES = {
     "plate_pocket": (scenes.plate_pocket_scene, 8),
+    "plate_pocket_odd_n": (scenes.plate_pocket_scene, 9),  # odd lattice: cube centred on p
+    "highk_cross_n5": (lambda: scenes.load_fixture("highk_cross"), 5),
     "layered_plates": (scenes.layered_plate_scene, 8),
     "two_plates_small": (scenes.two_plates_small, 12),
     "conformal_staircase": (lambda: scenes.load_fixture("conformal_staircase"), 24),
