@@ -75,7 +75,7 @@ enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3 };
 // rounding), so every query below returns exactly the linear scan's result.
 struct DGrid {
   int dims[3];          // 0: no grid, linear scans
-  double lo[3], bs[3];  // origin, bin size per axis
+  double lo[3], bs[3], ibs[3];  // origin, bin size per axis, its inverse
   double bsmin;
   const int* cstart;    // [bins + 1] conductors overlapping the bin (CSR)
   const int* citem;
@@ -212,7 +212,7 @@ __device__ __forceinline__ bool box_contains(const double* b, const double p[3])
 
 // Structure::conductor_at (geometry.cpp:57-62): declaration index or -1
 __device__ __forceinline__ int bin_of(const DGrid& g, int a, double x) {
-  const int i = static_cast<int>(floor((x - g.lo[a]) / g.bs[a]));
+  const int i = static_cast<int>(floor((x - g.lo[a]) * g.ibs[a]));
   return min(max(i, 0), g.dims[a] - 1);
 }
 
@@ -263,6 +263,7 @@ __device__ double grid_min_cheb(const DStruct& s, const double p[3], double r, b
 // the caller then scans every box, so results never depend on the bins.
 constexpr int kCandMax = 96;
 constexpr int kCandBins = 64;
+constexpr int kCandWords = 16;  // bitmap dedup for up to 1024 boxes
 __device__ __forceinline__ bool cand_insert(int* a, int& n, int v) {
   int i = n;
   while (i > 0 && a[i - 1] > v) --i;
@@ -286,7 +287,34 @@ __device__ int grid_candidates(const DStruct& s, bool diel, const double* cb, in
   if (nb > kCandBins) return -1;
   const int* st = diel ? g.dstart : g.cstart;
   const int* it = diel ? g.ditem : g.citem;
+  const int count = diel ? s.nd : s.nc;
   int n = 0;
+  if (count <= 64 * kCandWords) {
+    // dedup + ordering through a bitmap of box ids, then extract ascending
+    const int W = (count + 63) >> 6;
+    uint64_t bits[kCandWords];
+    for (int w = 0; w < W; ++w) bits[w] = 0;
+    if (diel)
+      for (int q = 0; q < g.ndlarge; ++q) {
+        const int v = __ldg(g.dlarge + q);
+        bits[v >> 6] |= 1ull << (v & 63);
+      }
+    for (int z = b0[2]; z <= b1[2]; ++z)
+      for (int y = b0[1]; y <= b1[1]; ++y)
+        for (int x = b0[0]; x <= b1[0]; ++x) {
+          const int bin = (z * g.dims[1] + y) * g.dims[0] + x;
+          for (int q = __ldg(st + bin), e = __ldg(st + bin + 1); q < e; ++q) {
+            const int v = __ldg(it + q);
+            bits[v >> 6] |= 1ull << (v & 63);
+          }
+        }
+    for (int w = 0; w < W; ++w)
+      for (uint64_t y = bits[w]; y; y &= y - 1) {
+        if (n == kCandMax) return -1;
+        out[n++] = 64 * w + __ffsll(y) - 1;
+      }
+    return n;
+  }
   if (diel)
     for (int q = 0; q < g.ndlarge; ++q)
       if (!cand_insert(out, n, __ldg(g.dlarge + q))) return -1;
@@ -758,6 +786,7 @@ __device__ uint64_t cell_info(const uint64_t* A, const uint64_t bm[3], int ncond
 
 // builds the atlas of the K clipped boxes of a job (compile_mw_job)
 __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, uint64_t bm[3]) {
+  uint64_t on[64], off[64];  // per segment: boxes starting / ending there
 #pragma unroll 1
   for (int a = 0; a < 3; ++a) {
     uint64_t b = 1;  // segment starting at 0
@@ -769,15 +798,19 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
     }
     bm[a] = b;
     A[kAtBm + a] = b;
-    int sg = 0;
-    for (uint64_t y = b; y; y &= y - 1, ++sg) {
-      const int st = __ffsll(y) - 1;
-      uint64_t m = 0;
-      for (int q = 0; q < K; ++q) {
-        const uint64_t x = boxes[q];
-        if (box_lo(x, a) <= st && st <= box_hi(x, a)) m |= 1ull << q;
-      }
+    // sweep: box q spans segments seg(lo_q) .. seg(hi_q), O(K + segments)
+    const int S = __popcll(b);
+    for (int sg = 0; sg < S; ++sg) on[sg] = off[sg] = 0;
+    for (int q = 0; q < K; ++q) {
+      const uint64_t x = boxes[q];
+      on[__popcll(b & upto(box_lo(x, a))) - 1] |= 1ull << q;
+      off[__popcll(b & upto(box_hi(x, a))) - 1] |= 1ull << q;
+    }
+    uint64_t m = 0;
+    for (int sg = 0; sg < S; ++sg) {
+      m |= on[sg];
       A[kAtMask + 64 * a + sg] = m;
+      m &= ~off[sg];
     }
   }
 }
@@ -2682,11 +2715,12 @@ int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
     for (int a = 0; a < 3; ++a) {
       g.dims[a] = static_cast<int>(std::min(256.0, std::max(1.0, std::round(ext[a] / b))));
       g.bs[a] = ext[a] / g.dims[a];
+      g.ibs[a] = 1.0 / g.bs[a];
       g.bsmin = std::min(g.bsmin, g.bs[a]);
     }
     const size_t bins = static_cast<size_t>(g.dims[0]) * g.dims[1] * g.dims[2];
     auto bin1 = [&](int a, double x) {  // bin_of, host copy of the same arithmetic
-      const int i = static_cast<int>(std::floor((x - g.lo[a]) / g.bs[a]));
+      const int i = static_cast<int>(std::floor((x - g.lo[a]) * g.ibs[a]));
       return std::min(std::max(i, 0), g.dims[a] - 1);
     };
     std::vector<int> count(bins + 1, 0), start(bins + 1, 0), item;
