@@ -24,10 +24,11 @@ struct GridTable {
   uint64_t* d_full = nullptr;     // [R][5] exact 53-bit thresholds
   uint64_t h2d_bytes = 0;         // bytes copied by the last upload
   int32_t* d_mask = nullptr;      // [n^3] conductor ids (valid when has_mask)
+  int32_t* d_exit = nullptr;      // [(n+2)^3] absorbing node -> panel, or -2 - conductor id
   bool has_mask = false;
   size_t map_bytes = 0, rec_bytes = 0;  // padded to 16 B
   // allocation capacities (re-uploads of a same-sized grid reuse them)
-  size_t blob_cap = 0, full_cap = 0, mask_cap = 0;
+  size_t blob_cap = 0, full_cap = 0, mask_cap = 0, exit_cap = 0;
 };
 
 }  // namespace frw

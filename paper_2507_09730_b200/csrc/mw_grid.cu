@@ -14,23 +14,26 @@
 //    in-order partial sums (microwalk.cpp:105-121).  Integer comparisons
 //    against X_d reproduce the reference's f64 scan bit for bit, with no
 //    division and no FP64 on the step path.
-//  * On chip a record is ONE 64-bit word: the top 10 bits of the five
-//    thresholds in 11-bit SWAR lanes (guard bit per lane) plus six exit bits.
-//    The step compares the top 10 bits of x against all five lanes with two
-//    64-bit subtractions; only on a 10-bit tie (~0.5% of steps) does a lane
-//    fetch the exact 53-bit thresholds from global memory (L1/L2 resident).
+//  * On chip a record is ONE 64-bit word: the top 11 bits of the five
+//    thresholds in 12-bit SWAR lanes (guard bit per lane).  One 64-bit
+//    multiply-add of x11 against all five lanes and a popcount of the guard
+//    bits give the direction; only on an 11-bit tie (~0.25% of steps per
+//    lane) are the exact 53-bit thresholds read from global memory (L1/L2).
 //  * Node map (2 B/node) + packed records (8 B/record) are staged into shared
 //    memory with cp.async.bulk (TMA bulk-copy engine, mbarrier completion):
-//    162 KB for C2, so every step costs one LDS.U16 + one LDS.64 + one LDS.32
-//    (stride table, broadcast) instead of 7 conflicted loads.
+//    183 KB for C2.  In the fast path (mw_grid_fast) the map holds each
+//    node's record as its shared byte address and the walker's position is
+//    the address of its map entry, so a step is LDS.U16 -> LDS.64 -> SHFL
+//    (stride) with no address arithmetic: ~19 instructions per step, bound
+//    by the shared-memory wavefronts of the two random gathers.
 //  * Persistent CTAs, one walker per thread, refilled from a global transit
 //    counter; lanes step in phase-aligned super-steps (8 steps per Philox
-//    call, 16 bits of each word per step) so Philox blocks and exit
-//    bookkeeping are warp-uniform (the re-binning of live walkers: a
-//    lane whose transit ends is re-armed with the next transit at the next
-//    super-step boundary instead of idling).
+//    call) so Philox blocks and exit bookkeeping are warp-uniform: a lane
+//    whose transit ends is re-armed with the next transit at the next
+//    super-step boundary instead of idling.
 //  * Histogram (RED.64 to global), exact u64 step moments and optional
-//    per-transit records are fused into the exit path.
+//    per-transit records are fused into the exit path; the exit panel is one
+//    lookup in a per-absorbing-node table.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,6 +48,11 @@
 namespace frw {
 namespace {
 
+// stride lookup by warp shuffle (lane d holds stride d) instead of a shared
+// load: it keeps the step's shared-memory wavefronts to the two gathers
+#ifndef FRW_STRIDE_SHFL
+#define FRW_STRIDE_SHFL 1
+#endif
 constexpr int kThreads = 1024;
 constexpr int kDirAxis[6] = {0, 0, 1, 1, 2, 2};
 constexpr int kDirSign[6] = {-1, +1, -1, +1, -1, +1};
@@ -54,6 +62,11 @@ constexpr int kLane = 12;                          // 11-bit threshold + guard
 constexpr uint64_t kOnes = 0x0000001001001001ull | (1ull << 48);  // 1 in each of 5 lanes
 constexpr uint64_t kGuard = kOnes << 11;           // guard bit of each lane (11,23,35,47,59)
 constexpr int kTop = 2047;                         // 11-bit lane maximum
+// the exit record: every guard bit plus bit 63, counted by the fast path's
+// popcount as direction 6 (stride 0); the other paths test the id first
+constexpr uint32_t kGuardLo = static_cast<uint32_t>(kGuard);
+constexpr uint32_t kGuardHi = static_cast<uint32_t>(kGuard >> 32) | 0x80000000u;
+constexpr uint64_t kExitRec = kGuard | (1ull << 63);
 
 // ---------------------------------------------------------------------------
 // host: compile the grid into node map + step records
@@ -109,7 +122,41 @@ struct Compiled {
   std::vector<uint16_t> map;
   std::vector<uint64_t> rec;   // [R] packed
   std::vector<uint64_t> full;  // [R][5] exact thresholds X_d
+  std::vector<int32_t> exit_info;  // [(n+2)^3] see exit_info_of
 };
+
+// What absorbing padded node p means to a walker that lands on it: a halo
+// face node has exactly one lattice neighbour, so it names one surface panel
+// (sgf.hpp:34-36, sgf.cpp:13-30); a conductor voxel names its conductor
+// (-2 - id).  Edge/corner halo nodes and lattice nodes are never landed on
+// from outside (-1).
+void exit_info_of(int n, const int32_t* mask, std::vector<int32_t>& info) {
+  const int np = n + 2;
+  info.assign(static_cast<size_t>(np) * np * np, -1);
+  for (int k = 0; k < np; ++k)
+    for (int j = 0; j < np; ++j)
+      for (int i = 0; i < np; ++i) {
+        const int h[3] = {i, j, k};
+        int out = 0, ax = -1;
+        for (int a = 0; a < 3; ++a)
+          if (h[a] == 0 || h[a] == n + 1) ++out, ax = a;
+        const size_t pv = (static_cast<size_t>(k) * np + j) * np + i;
+        if (out == 0) {
+          if (mask) {
+            const int m = mask[((k - 1) * n + (j - 1)) * n + (i - 1)];
+            if (m >= 0) info[pv] = -2 - m;
+          }
+          continue;
+        }
+        if (out != 1) continue;
+        const int dir = 2 * ax + (h[ax] == n + 1 ? 1 : 0);
+        int c[3] = {i - 1, j - 1, k - 1};
+        c[ax] = h[ax] == 0 ? 0 : n - 1;  // the interior node stepped from
+        const int uu = ax == 0 ? c[1] : c[0];
+        const int vv = ax == 2 ? c[1] : c[2];
+        info[pv] = (dir * n + vv) * n + uu;
+      }
+}
 
 int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
                  Compiled& out) {
@@ -204,8 +251,9 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
         pmap[pv] = r;
       }
   // the exit record: never stepped from (an absorbed walker stops)
-  out.rec.push_back(0);
+  out.rec.push_back(kExitRec);
   for (int d = 0; d < 5; ++d) out.full.push_back(1ull << 53);
+  exit_info_of(n, mask, out.exit_info);
   out.map.resize(pmap.size());
   for (size_t q = 0; q < pmap.size(); ++q)
     out.map[q] = static_cast<uint16_t>(pmap[q] == 0xFFFFFFFFu ? nrec : pmap[q]);
@@ -220,6 +268,7 @@ struct DevGrid {
   const uint64_t* rec;  // [R+1] packed SWAR records, R = the exit record
   const uint64_t* full;
   const int32_t* mask;
+  const int32_t* exit_info;  // [(n+2)^3] absorbing node -> panel / -2 - conductor
   int n;
   int np, npp;          // padded extents n+2, (n+2)^2
   int start_idx;        // padded index of start_node
@@ -500,19 +549,300 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path (table resident in shared memory, every record address < 64 KB):
+//  * the staged node map holds each node's record as its shared-window byte
+//    address, so a step is LDS.U16 -> LDS.64 with no address arithmetic, and
+//    the walker's position is kept as the byte address of its map entry;
+//  * the exit record is kGuard | 1<<63: every guard bit plus a sixth
+//    counted bit, so an absorbed walker (and a retired lane parked on a halo
+//    node) draws direction 6, whose stride is 0 -- no per-step predicates
+//    on the move;
+//  * tie test on one lane: with monotone thresholds the lanes whose guard
+//    fired are exactly 0..dir-1, so x11 ties a threshold iff lane `dir` of
+//    x11*ones + rec reads 2047 (its low 11 bits all ones);
+//  * the step count is rebuilt at the super-step boundary from the index of
+//    the last real step (steps = SS*blk + u_last + 1), so the loop carries
+//    one predicated write per step instead of counter/select updates.
+
+// low 32 bits of v >> s for 0 <= s <= 72 (PTX clamps shifts past 64 to 0)
+__device__ __forceinline__ uint32_t shr64_lo(uint64_t v, uint32_t s) {
+  uint32_t r;
+  asm("{ .reg .b64 t; shr.b64 t, %1, %2; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(v), "r"(s));
+  return r;
+}
+
+// Stage two segments into shared memory on one mbarrier.
+__device__ void bulk_stage2(void* d0, const void* s0, uint32_t b0, void* d1, const void* s1,
+                            uint32_t b1, uint64_t* bar) {
+  const uint32_t b = smem_u32(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(b0 + b1)
+                 : "memory");
+    constexpr uint32_t kChunk = 32768;
+    for (int seg = 0; seg < 2; ++seg) {
+      char* dst = static_cast<char*>(seg ? d1 : d0);
+      const char* src = static_cast<const char*>(seg ? s1 : s0);
+      const uint32_t bytes = seg ? b1 : b0;
+      for (uint32_t off = 0; off < bytes; off += kChunk) {
+        const uint32_t sz = min(kChunk, bytes - off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst + off)),
+            "l"(src + off), "r"(sz), "r"(b)
+            : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(b)
+        : "memory");
+  }
+}
+
+template <int RNG, bool TRACK>
+__global__ void __launch_bounds__(kThreads, 1)
+    mw_grid_fast(DevGrid g, DevParams p, unsigned long long* ctr, int* err,
+                 int32_t* out_panel, int32_t* out_steps, int32_t* out_cond,
+                 long long* out_nd, unsigned long long* hist, unsigned long long* m_sum,
+                 unsigned long long* m_sq, unsigned long long* m_cx) {
+  // TRACK: keep the direction of the last real step (for exit_nd); otherwise
+  // the step count comes from a dwell counter and the exit panel from the
+  // absorbing node alone (exit_info)
+  constexpr bool SM = RNG != FRW_RNG_PHILOX;
+  constexpr int SS = SM ? 4 : 8;
+  // shared: records | node map | stride table (8 x s32) | mbarrier
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* rec_p = smem;
+  uint8_t* map_p = smem + g.rec_bytes;
+  int* str_p = reinterpret_cast<int*>(map_p + g.map_bytes);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(str_p + 8);
+  bulk_stage2(rec_p, g.rec, g.rec_bytes, map_p, g.map, g.map_bytes, bar);
+  const uint32_t s_rec = smem_base(rec_p);
+  if (s_rec + g.rec_bytes > 65536u) {  // host guarantees this; never silently wrong
+    if (threadIdx.x == 0) atomicExch(err, FRW_EINVAL);
+    return;
+  }
+  // record ids -> record byte addresses, in place (two entries per word)
+  for (uint32_t i = threadIdx.x; i < g.map_bytes / 4; i += kThreads) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(map_p) + i;
+    const uint32_t v = *w;
+    *w = (s_rec + 8u * (v & 0xFFFFu)) | ((s_rec + 8u * (v >> 16)) << 16);
+  }
+  if (threadIdx.x < 8) {
+    const int d = threadIdx.x, ax = d >> 1;
+    str_p[d] = d >= 6 ? 0 : ((d & 1) ? 2 : -2) * (ax == 0 ? 1 : ax == 1 ? g.np : g.npp);
+  }
+  __syncthreads();
+  const uint32_t s_map = smem_base(map_p);
+#if FRW_STRIDE_SHFL
+  const int lane_stride = str_p[threadIdx.x & 7];
+#else
+  const uint32_t s_str = smem_base(str_p);
+#endif
+  const uint32_t s_exit = s_rec + 8u * g.exit_rec;
+  const uint32_t a_start = s_map + 2u * g.start_idx;
+  const uint32_t ra_start = lds_u16(a_start);
+  const uint32_t a_dead = s_map;  // padded node 0: a halo corner, absorbing
+
+  const int n = g.n;
+  const int cap = p.step_cap;
+  unsigned long long ssum = 0, ssq = 0, cexit = 0;
+
+  long long t = static_cast<long long>(atomicAdd(ctr, 1ull));
+  long long t_next = static_cast<long long>(atomicAdd(ctr, 1ull));
+  bool live = t < p.count;
+  uint32_t a = live ? a_start : a_dead;
+  uint32_t ra = live ? ra_start : s_exit;  // record address of the node at a
+  uint32_t xinfo = 0;  // TRACK: (u << 3) | dir of the last real step
+  int dwell = 0;       // !TRACK: steps drawn on an absorbing node this transit
+  int blk = 0;         // super-steps completed in the current transit
+  uint64_t sm = 0;
+  if (RNG == FRW_RNG_SPLITMIX_PARITY && live)
+    sm = sm64_stream_from_mixed(p.mixed_seed, p.stream_begin + t);
+  if (RNG == FRW_RNG_SPLITMIX_STATES && live) sm = p.states[t];
+  const uint32_t k0 = static_cast<uint32_t>(p.seed);
+  const uint32_t k1 = static_cast<uint32_t>(p.seed >> 32);
+
+  while (__any_sync(0xFFFFFFFFu, live)) {
+    uint32_t w[4];
+    if (RNG == FRW_RNG_PHILOX) {
+      // one 4x32-10 call per 8 steps: word k gives step 2k its x11 from bits
+      // 31..21 (16-bit prefix 31..16) and step 2k+1 from bits 10..0 (prefix
+      // continues with bits 15..11); the low 37 bits of x come from the
+      // (id, step slot, 1) counter only on a 16-bit tie
+      const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
+      const U32x4 o = philox4x32_10(
+          {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
+           static_cast<uint32_t>(blk), 0u},
+          k0, k1);
+      w[0] = o.x;
+      w[1] = o.y;
+      w[2] = o.z;
+      w[3] = o.w;
+    }
+#pragma unroll
+    for (int u = 0; u < SS; ++u) {
+      const bool act = ra != s_exit;
+      const uint64_t rc = lds_u64(ra);
+      uint64_t z = 0;
+      uint32_t x11;
+      if (SM) {
+        const uint64_t s1 = sm + kGamma;  // SplitMix64::next (rng.hpp:19-22)
+        z = sm64_mix(s1);
+        if (act) sm = s1;  // an absorbed walker consumes no randomness
+        x11 = static_cast<uint32_t>(z >> 53);
+      } else {
+        x11 = (u & 1) ? (w[u >> 1] & 0x7FFu) : (w[u >> 1] >> 21);
+      }
+      const uint64_t d1 = static_cast<uint64_t>(x11) * kOnes + rc;
+      const uint32_t d1h = static_cast<uint32_t>(d1 >> 32);
+      int dir = __popc((static_cast<uint32_t>(d1) & kGuardLo) | (d1h & kGuardHi));
+      // (absorbed lanes never tie: their shift is 72, which PTX clamps to 0)
+      const bool tie = (~shr64_lo(d1, 12u * dir) & 0x7FFu) == 0;
+      if (__builtin_expect(__any_sync(0xFFFFFFFFu, tie), 0)) {
+        // 11-bit tie: exact comparison against the 53-bit thresholds.  The
+        // block is warp-uniform (predicated per lane), so the common path
+        // carries no reconvergence barrier.
+        const uint64_t* f = g.full + 5 * ((ra - s_rec) >> 3);
+        uint64_t th[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) th[d] = tie ? __ldg(f + d) : 0;
+        int dx = 0;
+        if (SM) {
+          const uint64_t x53 = z >> 11;
+#pragma unroll
+          for (int d = 0; d < 5; ++d) dx += x53 >= th[d];
+        } else {
+          const uint32_t wu = w[u >> 1];
+          const uint32_t h16 =
+              (u & 1) ? (((wu & 0x7FFu) << 5) | ((wu >> 11) & 0x1Fu)) : (wu >> 16);
+          bool tie16 = false;
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            const uint32_t t16 = static_cast<uint32_t>(th[d] >> 37);
+            dx += h16 > t16;
+            tie16 |= h16 == t16;
+          }
+          tie16 = tie16 && tie;
+          if (__any_sync(0xFFFFFFFFu, tie16)) {
+            const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
+            const U32x4 o = philox4x32_10(
+                {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
+                 static_cast<uint32_t>(blk * SS + u), 1u},
+                k0, k1);
+            const uint64_t low37 = ((static_cast<uint64_t>(o.x) << 32) | o.y) >> 27;
+            const uint64_t x53 = (static_cast<uint64_t>(h16) << 37) | low37;
+            int de = 0;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) de += x53 >= th[d];
+            dx = tie16 ? de : dx;
+          }
+        }
+        dir = tie ? dx : dir;
+      }
+#if FRW_STRIDE_SHFL
+      a += static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, lane_stride, dir));
+#else
+      a += static_cast<uint32_t>(lds_s32(s_str + 4u * dir));
+#endif
+      ra = lds_u16(a);
+      if (TRACK) {
+        if (act) xinfo = (u << 3) | dir;
+      } else {
+        dwell += d1h >> 31;  // the exit record's bit 63 survives the add
+      }
+    }
+    // ---- exit bookkeeping, once per super-step ---------------------------
+    const bool exited = ra == s_exit;
+    const int steps = TRACK ? (exited ? SS * blk + static_cast<int>(xinfo >> 3) + 1 : SS * (blk + 1))
+                            : SS * (blk + 1) - dwell;
+    ++blk;
+    if (live && (exited || steps >= cap)) {
+      int32_t panel = -1, cid = -1;
+      long long nd = -1;
+      if (exited && steps <= cap) {
+        const int idx = static_cast<int>((a - s_map) >> 1);
+        const int info = __ldg(g.exit_info + idx);
+        if (info >= 0) {  // left the lattice: surface panel
+          panel = info;
+          atomicAdd(hist + panel, 1ull);
+        } else {  // absorbed by a conductor voxel (masked lattices)
+          cid = -2 - info;
+          ++cexit;
+        }
+        if (TRACK) {  // the interior node before the exit and the direction
+          const int xdir = static_cast<int>(xinfo & 7u);
+          const int hk = fdiv(idx, g.npp, g.inv_npp);
+          const int hrem = idx - hk * g.npp;
+          const int hj = fdiv(hrem, g.np, g.inv_np);
+          int c[3] = {hrem - hj * g.np - 1, hj - 1, hk - 1};  // unpadded
+          const int ax = xdir >> 1;
+          c[ax] -= (xdir & 1) ? 1 : -1;  // step back inside
+          nd = 8ll * ((c[2] * n + c[1]) * n + c[0]) + xdir;
+        }
+      } else {
+        atomicExch(err, FRW_ESTEPCAP);  // microwalk.cpp:153-155
+      }
+      if (out_panel) out_panel[t] = panel;
+      if (out_steps) out_steps[t] = steps;
+      if (out_cond) out_cond[t] = cid;
+      if (out_nd) out_nd[t] = nd;
+      ssum += steps;
+      ssq += static_cast<unsigned long long>(steps) * steps;
+      // re-arm with the prefetched transit, prefetch the following one
+      t = t_next;
+      live = t < p.count;
+      blk = 0;
+      dwell = 0;
+      a = live ? a_start : a_dead;
+      ra = live ? ra_start : s_exit;
+      if (live) {
+        t_next = static_cast<long long>(atomicAdd(ctr, 1ull));
+        if (RNG == FRW_RNG_SPLITMIX_PARITY)
+          sm = sm64_stream_from_mixed(p.mixed_seed, p.stream_begin + t);
+        if (RNG == FRW_RNG_SPLITMIX_STATES) sm = p.states[t];
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ssum += __shfl_xor_sync(0xFFFFFFFFu, ssum, o);
+    ssq += __shfl_xor_sync(0xFFFFFFFFu, ssq, o);
+    cexit += __shfl_xor_sync(0xFFFFFFFFu, cexit, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(m_sum, ssum);
+    atomicAdd(m_sq, ssq);
+    atomicAdd(m_cx, cexit);
+  }
+}
+
 template <int RNG, bool SMEM>
 int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned long long* ms,
            unsigned long long* mq, unsigned long long* mc) {
   const GridTable& G = ctx->grid;
   const int np = G.n + 2;
-  DevGrid g{G.d_map, G.d_rec, G.d_full, G.has_mask ? G.d_mask : nullptr, G.n, np, np * np,
+  DevGrid g{G.d_map, G.d_rec, G.d_full, G.has_mask ? G.d_mask : nullptr, G.d_exit, G.n, np, np * np,
             G.start_idx, static_cast<uint32_t>(G.records),
             static_cast<uint32_t>(G.map_bytes), static_cast<uint32_t>(G.rec_bytes),
             1.0f / np, 1.0f / (np * np)};
   DevParams dp{p->seed, sm64_mix(p->seed), p->stream_begin, p->count,
                p->step_cap > 0 ? p->step_cap : 1000 * G.n * G.n, p->states};
-  const size_t smem = SMEM ? G.map_bytes + G.rec_bytes : 0;
-  auto kern = mw_grid_kernel<RNG, SMEM>;
+  // fast path: records addressable by 16-bit shared addresses (the window
+  // base is at most a few KB; the kernel checks the exact bound)
+  const bool fast = SMEM && G.rec_bytes + 4096 <= 65536;
+  const size_t smem = !SMEM ? 0 : fast ? G.map_bytes + G.rec_bytes + 48 : G.map_bytes + G.rec_bytes;
+  auto kern = !fast ? mw_grid_kernel<RNG, SMEM>
+              : o->exit_nd ? mw_grid_fast<RNG, true> : mw_grid_fast<RNG, false>;
   if (SMEM)
     FRW_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
@@ -581,7 +911,17 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
                                 cudaMemcpyHostToDevice, ctx->stream));
   FRW_CUDA(ctx, cudaMemcpyAsync(G.d_full, cg.full.data(), full, cudaMemcpyHostToDevice,
                                 ctx->stream));
-  G.h2d_bytes = cg.map.size() * 2 + cg.rec.size() * 8 + full;
+  const size_t ebytes = cg.exit_info.size() * 4;
+  if (G.exit_cap < ebytes) {
+    cudaFree(G.d_exit);
+    G.d_exit = nullptr;
+    G.exit_cap = 0;
+    FRW_CUDA(ctx, cudaMalloc(&G.d_exit, ebytes));
+    G.exit_cap = ebytes;
+  }
+  FRW_CUDA(ctx, cudaMemcpyAsync(G.d_exit, cg.exit_info.data(), ebytes, cudaMemcpyHostToDevice,
+                                ctx->stream));
+  G.h2d_bytes = cg.map.size() * 2 + cg.rec.size() * 8 + full + ebytes;
   G.has_mask = mask != nullptr;
   if (mask) {
     const size_t bytes = static_cast<size_t>(n) * n * n * 4;

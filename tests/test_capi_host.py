@@ -63,8 +63,12 @@ def _emulate(oracle, eps, seed, count, mask=None):
             r = int(mp[idx])
             rc = int(rec[r])
             d1 = ((z >> 53) * ones + rc) & M64               # SWAR lanes
-            d = bin(d1 & guard).count("1")                    # x11 > T_d
-            if (((d1 + ones) ^ d1) & guard) != 0:             # 11-bit tie
+            d = bin(d1 & (guard | 1 << 63)).count("1")        # x11 > T_d
+            # 11-bit tie: lane d reads 2047 (mw_grid_fast); the same test as
+            # "some lane's low 11 bits are all ones" (mw_grid_kernel)
+            tie = ((d1 >> (12 * d)) & 0x7FF) == 0x7FF
+            assert tie == ((((d1 + ones) ^ d1) & guard) != 0)
+            if tie:
                 d = sum((z >> 11) >= int(full[r, q]) for q in range(5))
             prev = list(node)
             node[d >> 1] += 1 if d & 1 else -1
@@ -114,9 +118,10 @@ def test_packed_thresholds_are_monotone_prefixes():
     """lane d holds 2047 minus the top 11 bits of X_d; X_d is non-decreasing;
     the halo and only the halo maps to the exit record"""
     eps = c2_grid(1)[0]
-    mp, rec, full = capi.grid_compile(eps)
-    rec, full = rec[:-1], full[:-1]  # the last record is the exit record
+    mp, rec_all, full = capi.grid_compile(eps)
+    rec, full = rec_all[:-1], full[:-1]  # the last record is the exit record
     assert (np.diff(full.astype(np.float64), axis=1) >= 0).all()
+    assert int(rec_all[-1]) == sum(1 << (12 * d + 11) for d in range(5)) | 1 << 63  # exit: dir 6
     lanes = np.stack([(rec >> np.uint64(12 * d)) & np.uint64(4095) for d in range(5)], axis=1)
     assert np.array_equal(lanes, 2047 - np.minimum(full >> np.uint64(42), np.uint64(2047)))
     n = 41

@@ -41,8 +41,17 @@ def to_bytes(k):
 stalls = {k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]: num(k)
           for k in h if k.startswith("smsp__average_warps_issue_stalled_")
           and k.endswith("_per_issue_active.ratio")}
+# shared-memory data pipe: one wavefront per clock per SM
+pipe = None
+if "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum" in d and "gpu__time_duration.sum" in d:
+    t_ms = num("gpu__time_duration.sum") * {"ms": 1, "us": 1e-3, "usecond": 1e-3,
+                                             "msecond": 1}.get(d["gpu__time_duration.sum"][1], 1)
+    cyc = t_ms * 1e-3 * num("sm__cycles_elapsed.avg.per_second") * 1e9
+    sms = num("launch__grid_size") if num("launch__grid_size") <= 148 else 148
+    pipe = num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") / (cyc * sms)
 out = {"kernel": label, "workload": workload, "launch": launch, "source": source,
        "dram_bytes_per_launch": to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum"),
+       "smem_wavefront_pipe_frac": pipe,
        "metrics": {k: f"{d[k][0]} {d[k][1]}".strip() for k in keep if k in d},
        "top_stalls_per_issue": dict(sorted(stalls.items(), key=lambda t: -t[1])[:8])}
 json.dump(out, sys.stdout, indent=1)
