@@ -204,7 +204,7 @@ def walk_engine_bench(args, rank, world, dist, torch):
     from paper_2507_09730_b200.workloads import c3_structure
     doc = json.dumps(c3_structure())
     W = args.walks
-    kw = dict(mode="HYBRID-MW", min_walks=W, max_walks=W, device=int(os.environ.get("LOCAL_RANK", 0)))
+    kw = dict(mode="HYBRID-MW", min_walks=W, max_walks=W, device=torch.cuda.current_device())
     frwcap.extract_json(doc, seed=10_000 + rank, **kw)  # warm the SGF table
     dev_s, wall_s, res = 0.0, 0.0, None
     for i in range(args.walk_steps):
@@ -245,10 +245,19 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # FRW_DIST_BACKEND=gloo (with ranks folded onto the visible devices) is a
+    # smoke test of the launch/reduction path on a one-GPU box; the bench
+    # itself is one rank per GPU over NCCL
+    backend = os.environ.get("FRW_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(local)
 

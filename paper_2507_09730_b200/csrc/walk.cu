@@ -173,6 +173,8 @@ struct DCounters {
   unsigned long long gen_steps;  // MicroWalk steps next to a cell face
   unsigned long long cell_chg;   // MicroWalk moves into another cell
   unsigned long long npark;      // walks parked mid-walk (their slots kept)
+  // k_flow: ring heads/tails (ACTIVE, MicroWalk) and walks still in the flow
+  unsigned long long fah, fat, fmh, fmt, flive;
 };
 
 constexpr int kMissMax = 4096;
@@ -1547,6 +1549,9 @@ __global__ void __launch_bounds__(512)
 // takes an ACTIVE walk and runs it to its end, alternating transitions and
 // MicroWalk super-steps in-thread.  A table miss parks its walk as in
 // k_advance (the host resolves misses once the other walks are done).
+#ifndef FRW_TAIL_POLICY
+#define FRW_TAIL_POLICY 0
+#endif
 #ifndef FRW_TAIL_BLOCKS
 #define FRW_TAIL_BLOCKS 2
 #endif
@@ -1586,7 +1591,16 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     // MicroWalk lanes run long stretches between the divergent transitions
     // (8: 1.64e7, 16: 1.76e7, 32: 1.76e7 C3 walks/s; C5 MWE best at 32)
 #pragma unroll 1
-    for (int rep = 0; rep < 32 && __any_sync(0xFFFFFFFFu, live && in_mw); ++rep) {
+    for (int rep = 0; rep < 32; ++rep) {
+      const unsigned mwm = __ballot_sync(0xFFFFFFFFu, live && in_mw);
+      if (!mwm) break;
+#if FRW_TAIL_POLICY
+      // leave early once the lanes waiting for a transition outnumber the
+      // walking ones by FRW_TAIL_POLICY (they would idle a whole stretch)
+      if (rep >= 2 && __popc(__ballot_sync(0xFFFFFFFFu, live && !in_mw)) >
+                          FRW_TAIL_POLICY * __popc(mwm))
+        break;
+#endif
       if (!(live && in_mw)) continue;
       int xdir = 0;
       const int code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
@@ -1609,6 +1623,147 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     }
   }
   flush_mw_stats(C, L);
+}
+
+
+// ---- warp-specialised run-to-completion kernel ----------------------------
+// In k_tail one lane alternates transitions and MicroWalk stretches, so a
+// cached hop (microseconds) waits out the warp's whole MicroWalk stretch and
+// only ~7 of 32 lanes do useful work.  k_flow splits the roles by warp:
+// advance warps take walks from the ACTIVE ring (first the round's ACTIVE
+// list), run transitions until the walk needs a MicroWalk hop or ends, and
+// push compiled jobs to the MicroWalk ring; MicroWalk warps run jobs back to
+// back (lanes refilled independently, as in k_mw) and push surface exits to
+// the ACTIVE ring.  Handoffs go through the slot arrays: the producer's
+// writes are published by a gpu-scope fence before the ring entry, and the
+// consumer fences after seeing the entry.  Every lane holds at most one ring
+// reservation; the kernel ends when no walk is left in the flow (finished,
+// parked by a table miss, or dropped by an error).
+#ifndef FRW_FLOW_ADV_WARPS
+#define FRW_FLOW_ADV_WARPS 3
+#endif
+constexpr int kFlowAdvWarps = FRW_FLOW_ADV_WARPS;  // of the 8 warps of a CTA
+
+__device__ __forceinline__ int ring_poll(const int* ring, unsigned long long h, unsigned mask) {
+  return *reinterpret_cast<const volatile int*>(ring + (h & mask));
+}
+__device__ __forceinline__ void ring_push(int* ring, unsigned long long* tail, unsigned mask,
+                                          int slot) {
+  __threadfence();  // the walk's slot data before its ring entry
+  const unsigned long long t = atomicAdd(tail, 1ull);
+  volatile int* e = ring + (t & mask);
+  while (*e >= 0) __nanosleep(64);  // (a wrapped entry not yet consumed)
+  *e = slot;
+}
+__device__ __forceinline__ unsigned long long flow_live(const DCounters* C) {
+  return *reinterpret_cast<const volatile unsigned long long*>(&C->flive);
+}
+
+__global__ void k_flow_init(DCounters* C) {
+  C->fah = C->fat = C->fmh = C->fmt = 0;
+  C->flive = C->alen;
+}
+
+template <int RNG>
+__global__ void __launch_bounds__(256, kTailBlocks)
+    k_flow(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
+           const int* aq, int* ring_a, int* ring_m, unsigned mask) {
+  __shared__ double alpha_sm[PMAX * PMAX + 1];
+  __shared__ DirDelta dd[6];
+  setup_smem_tables(s, alpha_sm, dd);
+  const int n = P.n;
+  const unsigned long long alen = C->alen;
+  if ((threadIdx.x >> 5) < kFlowAdvWarps) {
+    // ---- advance warp ----
+    AdvLane A;
+    bool have = false, first = true;
+    long long res = -1;  // reserved ACTIVE-ring index
+    for (;;) {
+      if (!have) {
+        if (first) {
+          const unsigned long long item = atomicAdd(&C->ahead, 1ull);
+          if (item < alen) {
+            adv_load(W, aq[item], A);
+            have = true;
+          } else {
+            first = false;
+          }
+        }
+        if (!have && !first) {
+          if (res < 0) res = static_cast<long long>(atomicAdd(&C->fah, 1ull));
+          const int v = ring_poll(ring_a, res, mask);
+          if (v >= 0) {
+            ring_a[res & mask] = -1;
+            __threadfence();
+            adv_load(W, v, A);
+            have = true;
+            res = -1;
+          }
+        }
+      }
+      if (!__any_sync(0xFFFFFFFFu, have)) {
+        if (flow_live(C) == 0) break;
+        __nanosleep(256);
+        continue;
+      }
+      if (have) {
+        const int r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
+        if (r == 2) {
+          ring_push(ring_m, &C->fmt, mask, A.slot);
+          have = false;
+        } else if (r == 1) {
+          atomicAdd(&C->flive, ~0ull);  // -1
+          have = false;
+        }
+      }
+    }
+  } else {
+    // ---- MicroWalk warp ----
+    const int cap = 1000 * n * n;  // microwalk.cpp:81
+    MwLane L;
+    L.gsteps = 0;
+    L.cchg = 0;
+    bool have = false;
+    long long res = -1;
+    for (;;) {
+      if (!have) {
+        if (res < 0) res = static_cast<long long>(atomicAdd(&C->fmh, 1ull));
+        const int v = ring_poll(ring_m, res, mask);
+        if (v >= 0) {
+          ring_m[res & mask] = -1;
+          __threadfence();
+          mw_arm(W, alpha_sm, s.P, v, n, L);
+          have = true;
+          res = -1;
+        }
+      }
+      if (!__any_sync(0xFFFFFFFFu, have)) {
+        if (flow_live(C) == 0) break;
+        __nanosleep(256);
+        continue;
+      }
+      if (have) {
+        int xdir = 0;
+        const int code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
+        if (code != MW_GO) {
+          have = false;
+          if (code == MW_SURFACE) {
+            mw_exit(W, n, L, xdir);
+            ring_push(ring_a, &C->fat, mask, L.slot);
+          } else {
+            if (code == MW_COND)
+              mw_conductor_exit(W, recs, C, L, xdir);
+            else {
+              set_err(C, FRW_ESTEPCAP);
+              W.state[L.slot] = S_FREE;
+            }
+            atomicAdd(&C->flive, ~0ull);  // -1
+          }
+        }
+      }
+    }
+    flush_mw_stats(C, L);
+  }
 }
 
 // ---- single transits over structure cubes (the single-transit API) --------
@@ -2212,6 +2367,9 @@ struct Engine {
   DMiss M{};
   int* queue = nullptr;   // MicroWalk queue
   int* aq[2] = {nullptr, nullptr};  // ACTIVE queues (current / next round)
+  int* ring_a = nullptr;  // k_flow rings of walk slots (-1 = empty entry)
+  int* ring_m = nullptr;
+  unsigned ring_mask = 0;
   // reduction scratch
   double *psum = nullptr, *psq = nullptr, *osum = nullptr, *osq = nullptr;
   unsigned long long *pland = nullptr, *pstat = nullptr, *oland = nullptr, *ostat = nullptr;
@@ -2245,6 +2403,10 @@ void free_slots(Engine& E) {
   cudaFree(E.aq[0]);
   cudaFree(E.aq[1]);
   E.aq[0] = E.aq[1] = nullptr;
+  cudaFree(E.ring_a);
+  cudaFree(E.ring_m);
+  E.ring_a = E.ring_m = nullptr;
+  E.ring_mask = 0;
   cudaFree(E.M.retry);
   cudaFree(E.M.pend);
   cudaFree(E.M.park);
@@ -2497,12 +2659,22 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   E.queue = dalloc<int>(S);
   E.aq[0] = dalloc<int>(S);
   E.aq[1] = dalloc<int>(S);
+  {
+    // k_flow rings: every walk sits in at most one ring, and every waiting
+    // lane holds at most one reservation, so 2S + resident lanes suffices
+    unsigned cap = 1;
+    while (cap < 2u * static_cast<unsigned>(S) + (1u << 20)) cap <<= 1;
+    E.ring_a = dalloc<int>(cap);
+    E.ring_m = dalloc<int>(cap);
+    E.ring_mask = cap - 1;
+  }
   E.M.retry = dalloc<long long>(2 * size_t(S));  // parks accumulate up to S/2 + S
   E.M.pend = dalloc<long long>(2 * size_t(S));
   E.M.park = dalloc<int>(2 * size_t(S));
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
       !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes || !W.room ||
-      !W.fc || !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.M.retry || !E.M.pend || !E.M.park) {
+      !W.fc || !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.ring_a ||
+      !E.ring_m || !E.M.retry || !E.M.pend || !E.M.park) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
   }
@@ -3147,6 +3319,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   // run-to-completion threshold (active walks); FRW_TAIL_WALKS overrides
   unsigned long long tail_threshold = static_cast<unsigned long long>(ctx->sm_count) * 2048;
   if (const char* e = std::getenv("FRW_TAIL_WALKS")) tail_threshold = std::strtoull(e, nullptr, 10);
+  // tail kernel: k_tail by default; FRW_TAIL_KERNEL=flow selects the
+  // warp-specialised k_flow (C3/C5 within a few % either way)
+  const char* tk = std::getenv("FRW_TAIL_KERNEL");
+  const bool use_flow = tk && std::strcmp(tk, "flow") == 0;
   bool tail = false;
   float mw_ms = 0;
   uint64_t misses_total = 0, restarts = 0, resumes = 0;
@@ -3161,7 +3337,18 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     if (tail) {
       cudaEventRecord(m0, ctx->stream);
       const int tb = ctx->sm_count * kTailBlocks;  // persistent, one wave
-      if (P.rng == FRW_RNG_PHILOX)
+      if (use_flow) {
+        // rings start empty (a run that stopped on an error may leave entries)
+        FRW_CUDA(ctx, cudaMemsetAsync(E.ring_a, 0xFF, 4ull * (E.ring_mask + 1), ctx->stream));
+        FRW_CUDA(ctx, cudaMemsetAsync(E.ring_m, 0xFF, 4ull * (E.ring_mask + 1), ctx->stream));
+        k_flow_init<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
+        if (P.rng == FRW_RNG_PHILOX)
+          k_flow<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(
+              s, T, P, E.W, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
+        else
+          k_flow<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(
+              s, T, P, E.W, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
+      } else if (P.rng == FRW_RNG_PHILOX)
         k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M,
                                                            aq_in);
       else

@@ -89,6 +89,26 @@ def test_walk_offsets_and_slots_are_irrelevant(gpu_ctx, oracle):
         assert np.array_equal(a[f][1000:2000], c[f])
 
 
+@pytest.mark.parametrize("mode", sorted(MODES))
+def test_tail_kernels_agree_bitwise(gpu_ctx, oracle, monkeypatch, mode):
+    """k_tail (one lane per walk) and k_flow (warp-specialised, ring
+    handoffs) run the same walks to the same records, whatever the order"""
+    sc = _scene(c3_structure())
+    upload_scene(gpu_ctx, sc)
+    gpu_ctx.sgf_clear()
+    solve = oracle_solver(oracle)
+    p = walk_params(sc, grid_n=24, seed=9, rng=PHILOX, mode=MODES[mode])
+    monkeypatch.setenv("FRW_TAIL_WALKS", str(1 << 30))  # everything after round 0
+    out = {}
+    for k in ("tail", "flow"):
+        monkeypatch.setenv("FRW_TAIL_KERNEL", k)
+        out[k] = gpu_ctx.run_walks(p, sc.master_slot(), 0, 50_000, solve)
+    (ta, a), (tb, b) = out["tail"], out["flow"]
+    for f in ("slot", "weight", "aborted", "mw_steps", "cached", "microwalk"):
+        assert np.array_equal(a[f], b[f]), f
+    assert np.array_equal(ta["sum"], tb["sum"]) and np.array_equal(ta["landed"], tb["landed"])
+
+
 def test_hop_cap_aborts_into_ground(gpu_ctx, oracle):
     """test_engine.cpp:598-612"""
     sc = scenes.plate_scene()

@@ -9,5 +9,11 @@ walks = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
 doc = json.dumps({"c3": c3_structure, "c4": c4_structure, "c5": c5_structure}[name]())
 kw = dict(mode=os.environ.get("FRW_MODE", "HYBRID-MW"), seed=7)
 frwcap.extract_json(doc, min_walks=walks, max_walks=walks, **kw)   # warm table
+# the warm run is bracketed by cuProfilerStart/Stop: `ncu --profile-from-start off`
+# captures only its launches
+import ctypes
+cu = ctypes.CDLL("libcuda.so.1")
+cu.cuProfilerStart()
 r = frwcap.extract_json(doc, min_walks=walks, max_walks=walks, **kw)
+cu.cuProfilerStop()
 print(name, "device s", r["t_device_seconds"], "mw s", r["t_mw_seconds"], "misses", r["cache"]["misses"])
