@@ -50,6 +50,20 @@ def test_c2_parity_bit_exact(gpu_ctx, oracle):
     _bitexact(gpu_ctx, oracle, eps, c, h, 40_000, seed=5)
 
 
+def test_kernel_variants_bit_exact(gpu_ctx, oracle):
+    """every table placement runs the same walk: mw_grid_fast (records
+    addressable by 16-bit shared addresses: C2), the shared-memory kernel
+    with record ids (n=24 random grid: 13.8k records, 110 KB), and the
+    global-memory kernel (n=61 block cube: 0.5 MB map, beyond shared memory)"""
+    for eps, resident in ((c2_grid(1)[0], True), (random_voxel_grid(24, 64), True),
+                          (c2_grid(3, n=61)[0], False)):
+        n = round(len(eps) ** (1 / 3))
+        gpu_ctx.upload_grid(eps, np.zeros(3), n / 2.0)
+        assert gpu_ctx.grid_info()["smem_resident"] == resident
+        _bitexact(gpu_ctx, oracle, eps, np.zeros(3), n / 2.0, 3000 if n > 41 else 20_000,
+                  seed=n, stream0=7)
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 8, 12, 24])
 def test_random_voxel_grids_bit_exact(gpu_ctx, oracle, n):
     eps = random_voxel_grid(n, 40 + n)
