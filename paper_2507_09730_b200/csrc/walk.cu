@@ -265,7 +265,6 @@ __device__ double grid_min_cheb(const DStruct& s, const double p[3], double r, b
 // the caller then scans every box, so results never depend on the bins.
 constexpr int kCandMax = 96;
 constexpr int kCandBins = 64;
-constexpr int kCandWords = 16;  // bitmap dedup for up to 1024 boxes
 __device__ __forceinline__ bool cand_insert(int* a, int& n, int v) {
   int i = n;
   while (i > 0 && a[i - 1] > v) --i;
@@ -289,34 +288,7 @@ __device__ int grid_candidates(const DStruct& s, bool diel, const double* cb, in
   if (nb > kCandBins) return -1;
   const int* st = diel ? g.dstart : g.cstart;
   const int* it = diel ? g.ditem : g.citem;
-  const int count = diel ? s.nd : s.nc;
   int n = 0;
-  if (count <= 64 * kCandWords) {
-    // dedup + ordering through a bitmap of box ids, then extract ascending
-    const int W = (count + 63) >> 6;
-    uint64_t bits[kCandWords];
-    for (int w = 0; w < W; ++w) bits[w] = 0;
-    if (diel)
-      for (int q = 0; q < g.ndlarge; ++q) {
-        const int v = __ldg(g.dlarge + q);
-        bits[v >> 6] |= 1ull << (v & 63);
-      }
-    for (int z = b0[2]; z <= b1[2]; ++z)
-      for (int y = b0[1]; y <= b1[1]; ++y)
-        for (int x = b0[0]; x <= b1[0]; ++x) {
-          const int bin = (z * g.dims[1] + y) * g.dims[0] + x;
-          for (int q = __ldg(st + bin), e = __ldg(st + bin + 1); q < e; ++q) {
-            const int v = __ldg(it + q);
-            bits[v >> 6] |= 1ull << (v & 63);
-          }
-        }
-    for (int w = 0; w < W; ++w)
-      for (uint64_t y = bits[w]; y; y &= y - 1) {
-        if (n == kCandMax) return -1;
-        out[n++] = 64 * w + __ffsll(y) - 1;
-      }
-    return n;
-  }
   if (diel)
     for (int q = 0; q < g.ndlarge; ++q)
       if (!cand_insert(out, n, __ldg(g.dlarge + q))) return -1;
@@ -788,7 +760,8 @@ __device__ uint64_t cell_info(const uint64_t* A, const uint64_t bm[3], int ncond
 
 // builds the atlas of the K clipped boxes of a job (compile_mw_job)
 __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, uint64_t bm[3]) {
-  uint64_t on[64], off[64];  // per segment: boxes starting / ending there
+  // register-only scan (an O(K + segments) sweep needs per-segment event
+  // arrays in local memory, which cost the walk kernels more than it saved)
 #pragma unroll 1
   for (int a = 0; a < 3; ++a) {
     uint64_t b = 1;  // segment starting at 0
@@ -800,19 +773,15 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
     }
     bm[a] = b;
     A[kAtBm + a] = b;
-    // sweep: box q spans segments seg(lo_q) .. seg(hi_q), O(K + segments)
-    const int S = __popcll(b);
-    for (int sg = 0; sg < S; ++sg) on[sg] = off[sg] = 0;
-    for (int q = 0; q < K; ++q) {
-      const uint64_t x = boxes[q];
-      on[__popcll(b & upto(box_lo(x, a))) - 1] |= 1ull << q;
-      off[__popcll(b & upto(box_hi(x, a))) - 1] |= 1ull << q;
-    }
-    uint64_t m = 0;
-    for (int sg = 0; sg < S; ++sg) {
-      m |= on[sg];
+    int sg = 0;
+    for (uint64_t y = b; y; y &= y - 1, ++sg) {
+      const int st = __ffsll(y) - 1;
+      uint64_t m = 0;
+      for (int q = 0; q < K; ++q) {
+        const uint64_t x = boxes[q];
+        if (box_lo(x, a) <= st && st <= box_hi(x, a)) m |= 1ull << q;
+      }
       A[kAtMask + 64 * a + sg] = m;
-      m &= ~off[sg];
     }
   }
 }
@@ -1508,11 +1477,8 @@ __device__ __forceinline__ void flush_mw_stats(DCounters* C, const MwLane& L) {
 }
 
 // persistent MicroWalk kernel: each thread runs queued hops back to back
-#ifndef FRW_MW_BLOCKS
-#define FRW_MW_BLOCKS 1
-#endif
 template <int RNG>
-__global__ void __launch_bounds__(512, FRW_MW_BLOCKS)
+__global__ void __launch_bounds__(512)
     k_mw(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* queue,
          int* aq_out) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];
