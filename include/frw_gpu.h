@@ -220,6 +220,7 @@ typedef struct {
   uint64_t mw_cell_changes;  /* MicroWalk moves across a cell face         */
   double mw_ms;           /* device time of the MicroWalk kernel          */
   double total_ms;        /* device time of the whole call                */
+  uint64_t mw_jumps;      /* MicroWalk lattice jumps (Philox mode)        */
 } frw_tally;
 
 /* Per-walk outcome (Engine::WalkOut, engine.hpp:157-161, plus the walk's
@@ -264,6 +265,19 @@ typedef struct {
 int frw_structure_transits(frw_ctx *ctx, int n, int count, const double *cubes,
                            int with_conductors, const uint64_t *states, int32_t step_cap,
                            frw_exit *out);
+/* Production-mode transits of the same cubes: transit t draws from
+ * Philox4x32-10 (seed, t); with jumps != 0 uniform-cell stretches are taken
+ * as lattice jumps (the law the walk engine uses in FRW_RNG_PHILOX mode;
+ * DESIGN.md §4).  Same outputs as frw_structure_transits; `steps` counts a
+ * jump as E[tau] of its radius, stochastically rounded. */
+/* The lattice-jump law of radius m (2 <= m <= 31; host-only, no context):
+ * the simple symmetric walk's first-hit probabilities of one face of the
+ * L-inf sphere of radius m from its centre, face[(2m-1)^2] indexed v*(2m-1)+u
+ * (each of the six faces carries 1/6), and E[tau] (steps to the hit). */
+int frw_lattice_jump_law(int m, double *face, double *esteps);
+int frw_structure_transits_philox(frw_ctx *ctx, int n, int count, const double *cubes,
+                                  int with_conductors, uint64_t seed, int jumps,
+                                  int32_t step_cap, frw_exit *out);
 
 /* Engine::first_transition / Engine::transition (engine.hpp:146-159;
  * engine.cpp:201-350), one per entry, continuing caller-owned SplitMix64

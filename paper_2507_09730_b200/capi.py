@@ -79,7 +79,7 @@ class Tally(C.Structure):
                 ("mw_steps", C.c_uint64), ("restarts", C.c_uint64),
                 ("mw_general_steps", C.c_uint64), ("mw_cell_changes", C.c_uint64),
                 ("mw_ms", C.c_double),
-                ("total_ms", C.c_double)]
+                ("total_ms", C.c_double), ("mw_jumps", C.c_uint64)]
 
 
 WALK_RECORD = np.dtype([("weight", "<f8"), ("mw_steps", "<u8"), ("slot", "<i4"),
@@ -138,6 +138,10 @@ def lib():
                                                 _dp, _dp]
         L.frw_structure_transits.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _up,
                                              C.c_int32, C.POINTER(Exit)]
+        L.frw_lattice_jump_law.argtypes = [C.c_int, _dp, _dp]
+        L.frw_structure_transits_philox.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int,
+                                                    C.c_uint64, C.c_int, C.c_int32,
+                                                    C.POINTER(Exit)]
         L.frw_run_walks.argtypes = [C.c_void_p, C.POINTER(WalkParams), C.c_int32, C.c_uint64,
                                     C.c_int64, MISS_FN, C.c_void_p, C.POINTER(Tally),
                                     C.c_void_p]
@@ -166,6 +170,18 @@ def grid_compile(eps, mask=None):
     L.frw_grid_compile(n, eps.ctypes.data_as(_dp), None if m is None else m.ctypes.data_as(_ip),
                        _p(mp), _p(rec), _p(full), C.byref(R))
     return mp, rec, full
+
+
+def lattice_jump_law(m):
+    """Host-only: the face law ((2m-1)^2, v-major) and E[tau] of a radius-m
+    lattice jump (frw_lattice_jump_law)."""
+    side = 2 * m - 1
+    face = np.empty(side * side, np.float64)
+    et = C.c_double()
+    rc = lib().frw_lattice_jump_law(int(m), face.ctypes.data_as(_dp), C.byref(et))
+    if rc:
+        raise FrwError(rc, "lattice_jump_law failed")
+    return face.reshape(side, side), et.value
 
 
 class Context:
@@ -316,6 +332,22 @@ class Context:
                                                ("point", "<f8", 3)]), count=len(states))
         return {k: a[k].copy() for k in a.dtype.names}
 
+    def structure_transits_philox(self, n, cubes, seed, jumps=True, with_conductors=False,
+                                  step_cap=0):
+        """frw_structure_transits_philox: production-mode transits of the
+        cubes (transit t keyed by Philox (seed, t)), lattice jumps on/off."""
+        cubes = np.ascontiguousarray(cubes, np.float64).reshape(-1, 4)
+        count = len(cubes)
+        out = (Exit * count)()
+        self._check(self.L.frw_structure_transits_philox(
+            self.h, n, count, cubes.ctypes.data_as(_dp), int(with_conductors), int(seed),
+            int(bool(jumps)), step_cap, out))
+        a = np.frombuffer(out, dtype=np.dtype([("kind", "<i4"), ("panel", "<i4"),
+                                               ("conductor", "<i4"), ("dir", "<i4"),
+                                               ("voxel", "<i4", 3), ("steps", "<i4"),
+                                               ("point", "<f8", 3)]), count=count)
+        return {k: a[k].copy() for k in a.dtype.names}
+
     def sgf_put(self, n, axis, layers, pitch, probs, cdf, kernels=None):
         layers = np.ascontiguousarray(layers, np.float64)
         probs = np.ascontiguousarray(probs, np.float64)
@@ -394,7 +426,7 @@ class Context:
                      first=list(t.first), sub=list(t.sub), misses=t.cache_misses,
                      mw_steps=t.mw_steps, restarts=t.restarts, mw_ms=t.mw_ms,
                      mw_general_steps=t.mw_general_steps, mw_cell_changes=t.mw_cell_changes,
-                     total_ms=t.total_ms)
+                     total_ms=t.total_ms, mw_jumps=t.mw_jumps)
         return tally, rec
 
     def smem_bandwidth(self, iters=4096):

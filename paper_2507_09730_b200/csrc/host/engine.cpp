@@ -386,6 +386,7 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
     throw_status(ctx_, rc);
     mw_ms += t.mw_ms;
     dev_ms += t.total_ms;
+    res.mw_jumps += t.mw_jumps;
     // fold per-walk results in walk order, one reference batch at a time
     for (int64_t off = 0; off < chunk; off += batch) {
       const int64_t end = std::min<int64_t>(chunk, off + batch);

@@ -366,6 +366,7 @@ struct CapacitanceResult {
   double t_mw_seconds = 0;
   double t_total_seconds = 0;
   uint64_t mw_steps = 0;       // B200 extra: total lattice steps
+  uint64_t mw_jumps = 0;       // B200 extra: lattice jumps (Philox mode)
   double t_device_seconds = 0; // B200 extra: device time of the walk launches
   const TerminalEstimate* find_terminal(int conductor_id) const;
   const TerminalEstimate& self() const;

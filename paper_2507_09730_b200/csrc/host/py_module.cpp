@@ -120,6 +120,7 @@ py::dict result_to_dict(const CapacitanceResult& r) {
   d["t_mw_seconds"] = r.t_mw_seconds;
   d["t_total_seconds"] = r.t_total_seconds;
   d["mw_steps"] = r.mw_steps;                   // B200 extra
+  d["mw_jumps"] = r.mw_jumps;                   // B200 extra
   d["t_device_seconds"] = r.t_device_seconds;   // B200 extra
   return d;
 }

@@ -109,7 +109,33 @@ struct DSgf {
   const double* const* data; // [entries] -> cdf[P], probs[P], kern[3][P]
 };
 
+// Lattice jumps (Philox mode only).  Inside one cell every alpha is 1/2, so
+// the MicroWalk is the simple symmetric walk there.  From a node whose six
+// face distances are all >= m the walk's first hit of the L-inf sphere of
+// radius m is the discrete harmonic measure of the (2m-1)^3 interior: the
+// surface Green's function of the uniform cube with n' = 2m-1 nodes (the
+// device solve of sgf_solve.cu).  By the strong Markov property replacing
+// those steps by one draw from it leaves the law of the hop's exit (and the
+// expected step count) unchanged.  Per radius m: the face law as u64
+// thresholds over (2m-1)^2 positions (face chosen uniformly: the cube is
+// octahedrally symmetric), a guide table, and E[tau] in 32.32 fixed point.
+struct JumpMeta {
+  uint32_t thr_off;    // into DJump::thr
+  uint32_t guide_off;  // into DJump::guide
+  uint32_t gbits;      // log2 of the guide-table size
+  uint32_t side;       // 2m - 1
+  uint64_t esteps;     // E[tau] * 2^32
+};
+struct DJump {
+  int mmax;  // largest radius tabulated; < 2: jumps off
+  int twice; // a second jump from words 2-3 of the block when it fits
+  const JumpMeta* meta;   // [mmax + 1]
+  const uint64_t* thr;    // per radius: side^2 thresholds, last = UINT64_MAX
+  const uint16_t* guide;  // per radius: 2^gbits first candidates
+};
+
 struct DParams {
+  DJump jump;
   int n, panels, mode, rng;
   double snap;
   double expansion;
@@ -175,6 +201,7 @@ struct DCounters {
   unsigned long long npark;      // walks parked mid-walk (their slots kept)
   // k_flow: ring heads/tails (ACTIVE, MicroWalk) and walks still in the flow
   unsigned long long fah, fat, fmh, fmt, flive;
+  unsigned long long jumps;      // MicroWalk lattice jumps (Philox mode)
 };
 
 constexpr int kMissMax = 4096;
@@ -1254,6 +1281,7 @@ struct MwLane {
   double al[6];   // alpha of the neighbour across each face of the cell
   uint32_t gsteps;  // diagnostics, accumulated across the lane's hops
   uint32_t cchg;
+  uint32_t jumps;
 };
 
 // the per-face alphas of the lane's cell: palette pair (face class, own
@@ -1411,6 +1439,56 @@ __device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* 
 // Events of a MicroWalk super-step
 enum : int { MW_GO = 0, MW_SURFACE = 1, MW_COND = 3, MW_CAP = 4 };
 
+// One lattice jump (see DJump) from 64 random bits when all six face
+// distances are >= 2: radius m = min(face distances, mmax); the face is
+// floor(6x), the position on it the CDF inversion of the fractional part;
+// the walker moves to that node of the radius-m sphere (still in its cell),
+// the face distances follow, and the hop's step count takes E[tau_m]
+// (stochastically rounded).  Returns false (nothing consumed) otherwise.
+// the jump of radius m (2 <= m <= mmax) from 64 random bits
+__device__ __forceinline__ void mw_jump_r(const DJump& J, MwLane& L, int m, uint32_t w0,
+                                          uint32_t w1) {
+  const JumpMeta jm = J.meta[m];
+  const uint64_t x = (static_cast<uint64_t>(w0) << 32) | w1;
+  const int face = static_cast<int>(__umul64hi(x, 6ull));
+  const uint64_t y = x * 6ull;  // uniform given the face
+  const uint64_t* T = J.thr + jm.thr_off;
+  uint32_t idx = __ldg(J.guide + jm.guide_off + (y >> (64 - jm.gbits)));
+  while (y >= __ldg(T + idx)) ++idx;  // T[last] = UINT64_MAX ends the scan
+  const int side = static_cast<int>(jm.side);
+  const int v = static_cast<int>(idx) / side;
+  const int u = static_cast<int>(idx) - v * side;
+  const int a = face >> 1;
+  int dl[3];
+  dl[a] = (face & 1) ? m : -m;
+  // panel (face, v, u) conventions of surface_panel_of (sgf.cpp:13-30)
+  dl[a == 0 ? 1 : 0] = u - (m - 1);
+  dl[a == 2 ? 1 : 2] = v - (m - 1);
+  L.node += static_cast<uint32_t>(dl[0] + dl[1] * 256 + dl[2] * 65536);
+  // byte 2a: distance to the low face (+delta), byte 2a+1: to the high face
+  long long dr = 0;
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    dr += static_cast<long long>(dl[q]) * ((1ll << (16 * q)) - (1ll << (16 * q + 8)));
+  L.room += static_cast<uint64_t>(dr);
+  ++L.jumps;
+  L.steps += static_cast<int>(jm.esteps >> 32) +
+             (static_cast<uint32_t>(jm.esteps) > static_cast<uint32_t>(y >> 8) ? 1 : 0);
+}
+
+__device__ __forceinline__ bool mw_jump(const DJump& J, MwLane& L, uint32_t w0, uint32_t w1) {
+  const uint64_t r = L.room & 0x0000FFFFFFFFFFFFull;
+  // bytes are < 128: byte | 0x80 minus 2 keeps its top bit iff byte >= 2
+  if ((((r | 0x0000808080808080ull) - 0x0000020202020202ull) & 0x0000808080808080ull) !=
+      0x0000808080808080ull)
+    return false;
+  int m = J.mmax;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) m = min(m, static_cast<int>((r >> (8 * d)) & 0xFF));
+  mw_jump_r(J, L, m, w0, w1);
+  return true;
+}
+
 // Up to four lattice steps of the lane's hop from one Philox block (four
 // SplitMix64 draws in parity mode); a move into another cell ends the
 // super-step and refreshes the cell from the atlas.  Returns an MW_* event.
@@ -1432,9 +1510,15 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
     w4[3] = o.w;
   }
   int code = 0;
+  int u0 = 0;  // words taken by jumps (two per jump)
+  if (RNG == FRW_RNG_PHILOX && P.jump.mmax >= 2 && L.steps < cap &&
+      mw_jump(P.jump, L, w4[0], w4[1])) {
+    u0 = 2;
+    if (P.jump.twice && L.steps < cap && mw_jump(P.jump, L, w4[2], w4[3])) u0 = 4;
+  }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    if (code == 0 && L.steps < cap) {
+    if (u >= u0 && code == 0 && L.steps < cap) {
       uint64_t z = 0;
       if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
       code = mw_step<RNG>(P, dd, L, w4[u], z, static_cast<uint32_t>(L.rng * 4 + u), xdir);
@@ -1465,14 +1549,16 @@ __device__ void mw_conductor_exit(const DSlots& W, WalkRec* recs, DCounters* C, 
 }
 
 __device__ __forceinline__ void flush_mw_stats(DCounters* C, const MwLane& L) {
-  unsigned long long g = L.gsteps, cc = L.cchg;
+  unsigned long long g = L.gsteps, cc = L.cchg, jp = L.jumps;
   for (int o = 16; o > 0; o >>= 1) {
     g += __shfl_xor_sync(0xFFFFFFFFu, g, o);
     cc += __shfl_xor_sync(0xFFFFFFFFu, cc, o);
+    jp += __shfl_xor_sync(0xFFFFFFFFu, jp, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&C->gen_steps, g);
     atomicAdd(&C->cell_chg, cc);
+    atomicAdd(&C->jumps, jp);
   }
 }
 
@@ -1489,6 +1575,7 @@ __global__ void __launch_bounds__(512)
   const unsigned long long qlen = C->qlen;
   MwLane L;
   L.gsteps = 0;
+  L.jumps = 0;
   L.cchg = 0;
   unsigned long long item = atomicAdd(&C->qhead, 1ull);
   bool live = item < qlen;
@@ -1538,6 +1625,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
   AdvLane A;
   MwLane L;
   L.gsteps = 0;
+  L.jumps = 0;
   L.cchg = 0;
   bool in_mw = false;
   unsigned long long item = atomicAdd(&C->ahead, 1ull);
@@ -1691,6 +1779,8 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     const int cap = 1000 * n * n;  // microwalk.cpp:81
     MwLane L;
     L.gsteps = 0;
+    L.jumps = 0;
+  L.jumps = 0;
     L.cchg = 0;
     bool have = false;
     long long res = -1;
@@ -1747,6 +1837,9 @@ struct DevExit {
 };
 static_assert(sizeof(DevExit) == sizeof(frw_exit), "exit layout");
 
+// RNG = PHILOX: transit t draws from Philox (seed, t) (states unused) and
+// takes lattice jumps when P.jump is set -- the production-mode transit law
+template <int RNG>
 __global__ void __launch_bounds__(128)
     k_transits(DStruct s, DParams P, DSlots W, DCounters* C, const double* cubes,
                const uint64_t* states, int count, int with_cond, int cap, DevExit* out) {
@@ -1768,16 +1861,17 @@ __global__ void __launch_bounds__(128)
     return;
   }
   W.wid[t] = t;
-  W.rng[t] = states[t];
+  W.rng[t] = RNG == FRW_RNG_PHILOX ? 0 : states[t];
   W.mw[t] = 0;
   W.mwsteps[t] = 0;
   MwLane L;
   L.gsteps = 0;
+  L.jumps = 0;
   L.cchg = 0;
   mw_arm(W, alpha_sm, s.P, t, n, L);
   int code = MW_GO, xdir = 0;
-  while (code == MW_GO) code = mw_superstep<FRW_RNG_SPLITMIX_PARITY>(P, W, alpha_sm, s.P, s.bg,
-                                                                     dd, n, cap, L, &xdir);
+  while (code == MW_GO)
+    code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
   const int a = xdir >> 1;
   e.kind = code == MW_SURFACE ? 0 : 1;
   e.dir = xdir;
@@ -1905,6 +1999,7 @@ __global__ void __launch_bounds__(128)
     const int cap = 1000 * n * n;
     MwLane ml;
     ml.gsteps = 0;
+    ml.jumps = 0;
     ml.cchg = 0;
     mw_arm(W, alpha_sm, s.P, slot, n, ml);
     ml.wid = t;
@@ -2347,6 +2442,11 @@ struct Engine {
   // FDM solve scratch (5 Krylov vectors per persistent CTA)
   double* fdm_slab = nullptr;
   size_t fdm_cap = 0;
+  // lattice-jump tables (DJump) for lattice size jump_n, radii 2..jump_mmax
+  int jump_n = 0, jump_mmax = 0;
+  JumpMeta* d_jmeta = nullptr;
+  uint64_t* d_jthr = nullptr;
+  uint16_t* d_jguide = nullptr;
 };
 
 void free_slots(Engine& E) {
@@ -2420,6 +2520,9 @@ void engine_free(frw_ctx* ctx) {
   cudaFree(E->oland);
   cudaFree(E->ostat);
   cudaFree(E->fdm_slab);
+  cudaFree(E->d_jmeta);
+  cudaFree(E->d_jthr);
+  cudaFree(E->d_jguide);
   delete E;
   ctx->walk = nullptr;
 }
@@ -2525,6 +2628,132 @@ DParams params_of(const frw_walk_params* prm) {
   std::memcpy(P.fcdf, prm->face_cdf, sizeof P.fcdf);
   P.area = prm->area_m2;
   return P;
+}
+
+// The face law f[v * s + u] (u, v = 0..s-1, s = 2m - 1; the six faces are
+// equal) and E[tau] of the radius-m jump (see ensure_jumps).
+void jump_law(int m, std::vector<long double>& f, long double& tot, long double& et) {
+  const int side = 2 * m - 1, L = side + 1;
+  const size_t K = static_cast<size_t>(side) * side;
+  const long double pi = 3.141592653589793238462643383279502884L;
+  std::vector<long double> phi(K), cs(side), pc(side), ps(side);
+  for (int k = 1; k <= side; ++k) {
+    cs[k - 1] = std::cos(pi * k / L);
+    long double sum = 0;
+    for (int i = 1; i <= side; ++i) {
+      phi[(k - 1) * side + (i - 1)] = std::sqrt(2.0L / L) * std::sin(pi * k * i / L);
+      sum += phi[(k - 1) * side + (i - 1)];
+    }
+    pc[k - 1] = phi[(k - 1) * side + (m - 1)];  // centre index m
+    ps[k - 1] = sum;
+  }
+  // Bs[k2][k3] = sum_k1 phi_k1(1) phi_k1(c) phi_k2(c) phi_k3(c) / (6 (1 - lambda))
+  std::vector<long double> Bs(K, 0.0L);
+  et = 0;
+  for (int k1 = 0; k1 < side; ++k1)
+    for (int k2 = 0; k2 < side; ++k2)
+      for (int k3 = 0; k3 < side; ++k3) {
+        const long double inv = 1.0L / (1.0L - (cs[k1] + cs[k2] + cs[k3]) / 3.0L);
+        Bs[k2 * side + k3] += phi[k1 * side] * pc[k1] * pc[k2] * pc[k3] * inv / 6.0L;
+        et += pc[k1] * ps[k1] * pc[k2] * ps[k2] * pc[k3] * ps[k3] * inv;
+      }
+  // f[v][u] = sum_{k2,k3} phi_k2(u) Bs[k2][k3] phi_k3(v): the face law
+  std::vector<long double> tmp(K, 0.0L);
+  f.assign(K, 0.0L);
+  for (int k2 = 0; k2 < side; ++k2)
+    for (int v = 0; v < side; ++v) {
+      long double acc = 0;
+      for (int k3 = 0; k3 < side; ++k3) acc += Bs[k2 * side + k3] * phi[k3 * side + v];
+      tmp[k2 * side + v] = acc;
+    }
+  tot = 0;
+  for (int v = 0; v < side; ++v)
+    for (int u = 0; u < side; ++u) {
+      long double acc = 0;
+      for (int k2 = 0; k2 < side; ++k2) acc += phi[k2 * side + u] * tmp[k2 * side + v];
+      f[v * side + u] = std::max(acc, 0.0L);
+      tot += f[v * side + u];
+    }
+}
+
+// Lattice-jump tables (DJump) for lattice size n: radii m = 2..mmax with
+// mmax = min((n - 1) / 2, 31, FRW_MW_JUMP); FRW_MW_JUMP=0 turns jumps off.
+// The law of radius m is the simple symmetric walk's first hit of the
+// sphere, i.e. its Green's function on the s^3 interior (s = 2m - 1, the
+// sphere at indices 0 and s + 1 absorbing) next to a face.  That Green's
+// function is diagonal in the DST-I basis phi_k(i) = sqrt(2/L) sin(pi k i/L),
+// L = s + 1, with eigenvalue 1 - (cos(pi k1/L) + cos(pi k2/L) + cos(pi k3/L))/3,
+// so P(hit (0, j, k)) = G((1, j, k), c) / 6 and E[tau] = sum_x G(x, c) are
+// exact finite sums (O(s^3) per radius after factoring the k1 sum).
+// (Not the reference SGF of a 2m-1 cube: its lattice faces step out with
+// alpha 1, microwalk.cpp:97-104, while the sphere here sits inside a cell.)
+int ensure_jumps(frw_ctx* ctx, Engine& E, int n, DJump* out) {
+  int cap = 31;
+  if (const char* e = std::getenv("FRW_MW_JUMP")) cap = std::atoi(e);
+  const int mmax = std::min((n - 1) / 2, std::min(cap, 31));
+  *out = DJump{};
+  if (mmax < 2) return FRW_OK;
+  if (E.jump_n != n || E.jump_mmax != mmax) {
+    std::vector<JumpMeta> meta(mmax + 1, JumpMeta{});
+    std::vector<uint64_t> thr;
+    std::vector<uint16_t> guide;
+    for (int m = 2; m <= mmax; ++m) {
+      const int side = 2 * m - 1;
+      const size_t K = static_cast<size_t>(side) * side;
+      std::vector<long double> f;
+      long double tot = 0, et = 0;
+      jump_law(m, f, tot, et);
+      if (std::fabs(static_cast<double>(6.0L * tot) - 1.0) > 1e-9)
+        return frw_fail(ctx, FRW_ESOLVE, "run_walks: lattice-jump law failed its normalisation");
+      const double st = static_cast<double>(et);
+      JumpMeta& jm = meta[m];
+      jm.thr_off = static_cast<uint32_t>(thr.size());
+      jm.side = static_cast<uint32_t>(side);
+      const long double two64 = 18446744073709551616.0L;
+      long double cum = 0;
+      for (size_t k = 0; k < K; ++k) {
+        cum += f[k];
+        const long double q = cum / tot * two64;
+        thr.push_back(q >= two64 ? UINT64_MAX : static_cast<uint64_t>(q));
+      }
+      thr.back() = UINT64_MAX;
+      uint32_t gb = 0;
+      while ((size_t{1} << gb) < K) ++gb;
+      jm.gbits = gb;
+      jm.guide_off = static_cast<uint32_t>(guide.size());
+      size_t i = 0;
+      for (size_t g = 0; g < (size_t{1} << gb); ++g) {
+        const uint64_t lo = static_cast<uint64_t>(g) << (64 - gb);
+        while (thr[jm.thr_off + i] <= lo) ++i;  // first i with T[i] > lo
+        guide.push_back(static_cast<uint16_t>(i));
+      }
+      jm.esteps = static_cast<uint64_t>(st * 4294967296.0 + 0.5);
+    }
+    cudaFree(E.d_jmeta);
+    cudaFree(E.d_jthr);
+    cudaFree(E.d_jguide);
+    E.jump_n = 0;
+    E.d_jmeta = dalloc<JumpMeta>(meta.size());
+    E.d_jthr = dalloc<uint64_t>(thr.size());
+    E.d_jguide = dalloc<uint16_t>(guide.size());
+    if (!E.d_jmeta || !E.d_jthr || !E.d_jguide)
+      return frw_fail(ctx, FRW_ENOMEM, "run_walks: jump table allocation failed");
+    FRW_CUDA(ctx, cudaMemcpy(E.d_jmeta, meta.data(), sizeof(JumpMeta) * meta.size(),
+                             cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(E.d_jthr, thr.data(), 8 * thr.size(), cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(E.d_jguide, guide.data(), 2 * guide.size(), cudaMemcpyHostToDevice));
+    E.jump_n = n;
+    E.jump_mmax = mmax;
+  }
+  out->mmax = mmax;
+  // a second jump per Philox block measured 3-4% slower (C3/C5 HYBRID-MW):
+  // more divergence between jumping and stepping lanes
+  out->twice = 0;
+  if (const char* e = std::getenv("FRW_MW_JUMP_TWICE")) out->twice = std::atoi(e);
+  out->meta = E.d_jmeta;
+  out->thr = E.d_jthr;
+  out->guide = E.d_jguide;
+  return FRW_OK;
 }
 
 // launches k_fdm over `Q` with enough persistent CTAs; scratch grows on demand
@@ -3093,14 +3322,14 @@ int frw_sgf_clear(frw_ctx* ctx) {
 
 static_assert(sizeof(WalkRec) == sizeof(frw_walk_record), "record layout");
 
-int frw_structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
-                           int with_conductors, const uint64_t* states, int32_t step_cap,
-                           frw_exit* out) {
+static int structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
+                              int with_conductors, const uint64_t* states, int rng, uint64_t seed,
+                        int jumps, int32_t step_cap, frw_exit* out) {
   if (!ctx) return FRW_EINVAL;
   Engine& E = *engine_of(ctx);
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "transits: no structure uploaded");
   if (n < 1 || n > NMAX) return frw_fail(ctx, FRW_EINVAL, "transits: n must lie in [1, 64]");
-  if (count < 0 || (count > 0 && (!cubes || !states || !out)))
+  if (count < 0 || (count > 0 && (!cubes || (!states && rng != FRW_RNG_PHILOX) || !out)))
     return frw_fail(ctx, FRW_EINVAL, "transits: bad arguments");
   if (count == 0) return FRW_OK;
   for (int t = 0; t < count; ++t)
@@ -3130,20 +3359,31 @@ int frw_structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
   DParams P{};
   P.n = n;
   P.panels = 6 * n * n;
-  P.rng = FRW_RNG_SPLITMIX_PARITY;
+  P.rng = rng;
+  P.seed = seed;
+  if (rng == FRW_RNG_PHILOX && jumps) {
+    if (int rc = ensure_jumps(ctx, E, n, &P.jump)) {
+      release();
+      return rc;
+    }
+  }
   const int cap = step_cap > 0 ? step_cap : 1000 * n * n;  // microwalk.cpp:81
   int status = FRW_OK;
   do {
     if (cudaMemcpyAsync(d_cubes, cubes, 32 * size_t(count), cudaMemcpyHostToDevice,
                         ctx->stream) != cudaSuccess ||
-        cudaMemcpyAsync(d_states, states, 8 * size_t(count), cudaMemcpyHostToDevice,
-                        ctx->stream) != cudaSuccess ||
+        (states && cudaMemcpyAsync(d_states, states, 8 * size_t(count), cudaMemcpyHostToDevice,
+                                   ctx->stream) != cudaSuccess) ||
         cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), ctx->stream) != cudaSuccess) {
       status = frw_fail(ctx, FRW_ECUDA, "transits: copy failed");
       break;
     }
-    k_transits<<<(count + 127) / 128, 128, 0, ctx->stream>>>(
-        s, P, E.W, E.d_cnt, d_cubes, d_states, count, with_conductors, cap, d_out);
+    if (rng == FRW_RNG_PHILOX)
+      k_transits<FRW_RNG_PHILOX><<<(count + 127) / 128, 128, 0, ctx->stream>>>(
+          s, P, E.W, E.d_cnt, d_cubes, d_states, count, with_conductors, cap, d_out);
+    else
+      k_transits<FRW_RNG_SPLITMIX_PARITY><<<(count + 127) / 128, 128, 0, ctx->stream>>>(
+          s, P, E.W, E.d_cnt, d_cubes, d_states, count, with_conductors, cap, d_out);
     DCounters c;
     if (cudaGetLastError() != cudaSuccess ||
         cudaMemcpyAsync(out, d_out, sizeof(DevExit) * count, cudaMemcpyDeviceToHost,
@@ -3162,6 +3402,30 @@ int frw_structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
   } while (false);
   release();
   return status;
+}
+
+int frw_structure_transits(frw_ctx* ctx, int n, int count, const double* cubes,
+                           int with_conductors, const uint64_t* states, int32_t step_cap,
+                           frw_exit* out) {
+  return structure_transits(ctx, n, count, cubes, with_conductors, states,
+                            FRW_RNG_SPLITMIX_PARITY, 0, 0, step_cap, out);
+}
+
+int frw_structure_transits_philox(frw_ctx* ctx, int n, int count, const double* cubes,
+                                  int with_conductors, uint64_t seed, int jumps,
+                                  int32_t step_cap, frw_exit* out) {
+  return structure_transits(ctx, n, count, cubes, with_conductors, nullptr, FRW_RNG_PHILOX,
+                            seed, jumps, step_cap, out);
+}
+
+int frw_lattice_jump_law(int m, double* face, double* esteps) {
+  if (m < 2 || m > 31 || !face) return FRW_EINVAL;
+  std::vector<long double> f;
+  long double tot = 0, et = 0;
+  jump_law(m, f, tot, et);
+  for (size_t k = 0; k < f.size(); ++k) face[k] = static_cast<double>(f[k]);
+  if (esteps) *esteps = static_cast<double>(et);
+  return FRW_OK;
 }
 
 int frw_first_transitions(frw_ctx* ctx, const frw_walk_params* prm, int count,
@@ -3278,6 +3542,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   P.count = count;
   P.master = master;
   DMiss M = E.M;
+  // lattice jumps in plain MicroWalk hops only: MicroWalk-E cubes (with
+  // their conductor faces) leave few jumps and lose 1-4% to the test
+  if (P.rng == FRW_RNG_PHILOX && P.mode != FRW_MODE_MWE && P.mode != FRW_MODE_HYBRID_MWE)
+    if (int rc = ensure_jumps(ctx, E, P.n, &P.jump)) return rc;
 
   FRW_CUDA(ctx, cudaMemsetAsync(E.W.state, 0, S, ctx->stream));
   FRW_CUDA(ctx, cudaMemsetAsync(E.recs, 0, sizeof(WalkRec) * count, ctx->stream));
@@ -3488,6 +3756,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     FRW_CUDA(ctx, cudaMemcpy(&cfin, E.d_cnt, sizeof cfin, cudaMemcpyDeviceToHost));
     out->mw_general_steps = cfin.gen_steps;
     out->mw_cell_changes = cfin.cell_chg;
+    out->mw_jumps = cfin.jumps;
     float tot = 0;
     cudaEventElapsedTime(&tot, t0, t1);
     out->total_ms = tot;
