@@ -44,8 +44,10 @@ def build_gpu_lib(force=False):
     if force or _stale(out, deps):
         # -fmad=false: geometry/voxel-centre arithmetic must round like the
         # reference (x86-64 baseline, no FMA contraction)
+        # FRW_NVCC_EXTRA: extra flags for A/B builds of kernel knobs (-D...)
+        extra = os.environ.get("FRW_NVCC_EXTRA", "").split()
         _run([NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "-Xptxas", "-v",
-              "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
+              "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), *extra,
               "-o", out, *cu])
     return out
 

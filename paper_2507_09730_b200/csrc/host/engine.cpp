@@ -14,6 +14,7 @@
 #include <limits>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <unordered_set>
 
 #include "frwcap.hpp"
@@ -138,9 +139,10 @@ std::map<int, Device*>& devices() {
 struct DeviceTable {
   int n = 0;  // lattice size of the keys currently on the device
   std::unordered_set<ProfileKey, ProfileKeyHash> keys;  // keys already put
-  // page-locked staging for per-walk records, kept across extract calls
-  frw_walk_record* rec = nullptr;
-  size_t rec_cap = 0;
+  // page-locked staging for per-walk records (two buffers: the host folds
+  // one chunk while the device fills the other), kept across extract calls
+  frw_walk_record* rec[2] = {nullptr, nullptr};
+  size_t rec_cap[2] = {0, 0};
 };
 std::map<frw_ctx*, DeviceTable>& tables() {
   static auto* m = new std::map<frw_ctx*, DeviceTable>;
@@ -365,29 +367,9 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   std::vector<uint64_t> tl(nslots);
   const long batch = cfg_.batch;
   const long dev_batch = std::max<long>(batch, cfg_.device_batch / batch * batch);
-  while (walks < static_cast<uint64_t>(cfg_.max_walks) && !converged) {
-    const int64_t chunk = std::min<int64_t>(dev_batch, cfg_.max_walks - static_cast<int64_t>(walks));
-    if (DT.rec_cap < static_cast<size_t>(chunk)) {
-      if (DT.rec) frw_host_free(ctx_, DT.rec);
-      DT.rec = nullptr;
-      DT.rec_cap = 0;
-      void* mem = nullptr;
-      throw_status(ctx_, frw_host_alloc(ctx_, sizeof(frw_walk_record) * chunk, &mem));
-      DT.rec = static_cast<frw_walk_record*>(mem);
-      DT.rec_cap = chunk;
-    }
-    frw_walk_record* const rec = DT.rec;
-    frw_tally t{};
-    t.sum = ts.data();
-    t.sumsq = tq.data();
-    t.landed = tl.data();
-    const int rc = frw_run_walks(ctx_, &p, master, walks, chunk, miss_cb, &mc, &t, rec);
-    if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
-    throw_status(ctx_, rc);
-    mw_ms += t.mw_ms;
-    dev_ms += t.total_ms;
-    res.mw_jumps += t.mw_jumps;
-    // fold per-walk results in walk order, one reference batch at a time
+  // fold one chunk's per-walk results in walk order, one reference batch at
+  // a time, with the stopping rule after each batch (engine.cpp:378-420)
+  auto fold = [&](const frw_walk_record* rec, int64_t chunk) {
     for (int64_t off = 0; off < chunk; off += batch) {
       const int64_t end = std::min<int64_t>(chunk, off + batch);
       for (int64_t i = off; i < end; ++i) {
@@ -419,6 +401,50 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
         break;
       }
     }
+  };
+  // Device chunks of dev_batch walks (each drains its slot pool through the
+  // run-to-completion tail once, so large chunks amortise it).  While the
+  // device runs chunk k+1 a host thread folds chunk k; a chunk launched
+  // after the stopping rule fired inside an earlier one is discarded, so the
+  // result equals the sequential fold.
+  const int64_t max_walks = cfg_.max_walks;
+  int64_t launched = 0;
+  int cur = 0;
+  std::thread worker;
+  for (;;) {
+    const int64_t chunk = launched < max_walks ? std::min<int64_t>(dev_batch, max_walks - launched)
+                                               : 0;
+    int rc = FRW_OK;
+    frw_tally t{};
+    if (chunk > 0) {
+      if (DT.rec_cap[cur] < static_cast<size_t>(chunk)) {
+        if (DT.rec[cur]) frw_host_free(ctx_, DT.rec[cur]);
+        DT.rec[cur] = nullptr;
+        DT.rec_cap[cur] = 0;
+        void* mem = nullptr;
+        rc = frw_host_alloc(ctx_, sizeof(frw_walk_record) * chunk, &mem);
+        if (rc == FRW_OK) {
+          DT.rec[cur] = static_cast<frw_walk_record*>(mem);
+          DT.rec_cap[cur] = chunk;
+        }
+      }
+      if (rc == FRW_OK) {
+        t.sum = ts.data();
+        t.sumsq = tq.data();
+        t.landed = tl.data();
+        rc = frw_run_walks(ctx_, &p, master, launched, chunk, miss_cb, &mc, &t, DT.rec[cur]);
+      }
+    }
+    if (worker.joinable()) worker.join();
+    if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
+    throw_status(ctx_, rc);
+    mw_ms += t.mw_ms;
+    dev_ms += t.total_ms;
+    res.mw_jumps += t.mw_jumps;
+    if (converged || chunk == 0) break;
+    launched += chunk;
+    worker = std::thread(fold, DT.rec[cur], chunk);
+    cur ^= 1;
   }
   res.master_id = s_.master_id;
   res.walks = walks;

@@ -303,7 +303,7 @@ struct Config {
   // B200 knobs (defaults keep the reference behaviour)
   RngMode rng = RngMode::Philox;
   bool all_couplings_rule = false;  // stop when every coupling meets tol (C4)
-  long device_batch = 1 << 20;      // walks per device launch sequence
+  long device_batch = 1 << 22;      // walks per frw_run_walks call (one tail each)
   int device = 0;
 
   void validate() const;

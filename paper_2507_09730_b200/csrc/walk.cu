@@ -1563,8 +1563,11 @@ __device__ __forceinline__ void flush_mw_stats(DCounters* C, const MwLane& L) {
 }
 
 // persistent MicroWalk kernel: each thread runs queued hops back to back
+#ifndef FRW_KMW_MINB
+#define FRW_KMW_MINB 1
+#endif
 template <int RNG>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, FRW_KMW_MINB)
     k_mw(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* queue,
          int* aq_out) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];

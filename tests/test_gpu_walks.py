@@ -192,6 +192,23 @@ def test_convergence_rule_stops_on_a_batch_boundary():
     assert res["walks"] % 1024 == 0
 
 
+def test_convergence_independent_of_device_chunks():
+    """the stopping rule fires on the same reference batch whether the walks
+    come in one device call or in many (folded on a host thread while the
+    device runs the next chunk, a speculative chunk discarded)"""
+    import paper_2507_09730_b200.frwcap as frwcap
+    doc = scenes.plate_scene().to_json()
+    kw = dict(mode="HYBRID-MW", grid_n=8, seed=21, min_walks=1024, max_walks=1 << 20, tol=0.05)
+    one = frwcap.extract_json(doc, device_batch=1 << 20, **kw)
+    many = frwcap.extract_json(doc, device_batch=3072, **kw)
+    assert one["converged"] and many["converged"]
+    assert one["walks"] == many["walks"] and one["walks"] > 3 * 3072
+    for ta, tb in zip(one["terminals"], many["terminals"]):
+        assert ta["capacitance_farads"] == tb["capacitance_farads"]
+        assert ta["std_err_farads"] == tb["std_err_farads"]
+        assert ta["walks_landed"] == tb["walks_landed"]
+
+
 def test_all_couplings_rule_c4():
     """configs[3]: walk until every coupling has rel. SE < tol (here 5% to
     keep the test short; the bench uses 1%)."""
