@@ -199,7 +199,9 @@ def walk_engine_bench(args, rank, world, dist, torch):
     timed call runs `walks` fresh walks (seed = step + rank: independent
     streams per rank); per-rank tallies are combined with one NCCL
     all-reduce.  `value` is device time of the walk launches (CUDA events
-    inside frw_run_walks), `e2e` the wall time of the public call."""
+    inside frw_run_walks), `e2e` the wall time of the public call (its
+    inputs: the structure JSON; its outputs: 32-B per-walk records, folded
+    on the host)."""
     import paper_2507_09730_b200.frwcap as frwcap
     from paper_2507_09730_b200.workloads import c3_structure
     doc = json.dumps(c3_structure())
@@ -224,7 +226,8 @@ def walk_engine_bench(args, rank, world, dist, torch):
     ids = [t["conductor_id"] for t in res["terminals"]]
     return {"metric": "frw_walks_per_s", "unit": "walks/s",
             "value": total / dev_s, "e2e": {"value": total / wall_s, "unit": "walks/s",
-                                            "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
+                                            "h2d_bytes_per_step": len(doc),
+                                            "d2h_bytes_per_step": 32 * W},
             "config": {"workload": "C3 (BASELINE configs[2]): two 100x100x5000 nm wires, 100 nm "
                                    "apart, 200 nm over a 2x2 um plane, 3 z layers, 20 nm coatings; "
                                    "HYBRID-MW, N=24, Gaussian gap 0.5", "walks_per_rank_per_step": W,
@@ -237,6 +240,85 @@ def walk_engine_bench(args, rank, world, dist, torch):
             "dispatch_rank0_last": res["dispatch_stats"], "mw_steps_per_walk":
                 res["mw_steps"] / res["walks"], "t_mw_fraction": res["t_mw_seconds"] /
                 max(res["t_device_seconds"], 1e-12)}
+
+
+def walk_engine_c5(args, rank, world, dist, torch):
+    """FRW walks/s on C5 (BASELINE configs[4], the 1/2/4/8-GPU scaling
+    workload): 10 masters x 1e7 walks = 1e8 walks in total, split evenly over
+    the ranks (strong scaling); each rank runs its share of every master with
+    its own seed through extract_json, and the per-master rows are combined
+    with one all-reduce of (sum, sum of squares, walks).  Timed: the wall
+    time of the public calls (and the device time inside them), max over
+    ranks.  A warm-up pass of 2^18 walks per master fills the SGF table."""
+    import paper_2507_09730_b200.frwcap as frwcap
+    from paper_2507_09730_b200.workloads import c5_structure
+    c5 = c5_structure()
+    masters = [c["id"] for c in c5["conductors"]][:10]
+    per = args.c5_walks // len(masters) // world
+    kw = dict(mode="HYBRID-MW", device=torch.cuda.current_device())
+    docs = {}
+    for mid in masters:
+        c5["master"] = mid
+        docs[mid] = json.dumps(c5)
+        frwcap.extract_json(docs[mid], min_walks=1 << 18, max_walks=1 << 18,
+                            seed=50_000 + 100 * rank + mid, **kw)
+    if dist is not None:
+        dist.barrier()
+    dev_s = wall_s = 0.0
+    rows = {}
+    for mid in masters:
+        t0 = time.perf_counter()
+        r = frwcap.extract_json(docs[mid], min_walks=per, max_walks=per,
+                                seed=1 + 1000 * rank + mid, **kw)
+        wall_s += time.perf_counter() - t0
+        dev_s += r["t_device_seconds"]
+        rows[mid] = r
+    nt = len(rows[masters[0]]["terminals"])
+    # per master: sum (= mean * walks) and sum of squares rebuilt from the SE
+    acc = []
+    for mid in masters:
+        w = rows[mid]["walks"]
+        for t in rows[mid]["terminals"]:
+            m, se = t["capacitance_farads"], t["std_err_farads"]
+            acc += [m * w, (se * se * w * (w - 1)) + m * m * w]
+        acc.append(w)
+    red = torch.tensor(acc, dtype=torch.float64, device="cuda")
+    tm = torch.tensor([dev_s, wall_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(red)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    red = red.cpu().numpy()
+    dev_s, wall_s = float(tm[0]), float(tm[1])
+    out_rows = {}
+    k = 0
+    for mid in masters:
+        sums = red[k:k + 2 * nt].reshape(nt, 2)
+        w = red[k + 2 * nt]
+        k += 2 * nt + 1
+        ids = [t["conductor_id"] for t in rows[mid]["terminals"]]
+        mean = sums[:, 0] / w
+        se = np.sqrt(np.maximum(0.0, (sums[:, 1] - sums[:, 0] ** 2 / w) / (w - 1)) / w)
+        i_self = ids.index(mid)
+        out_rows[str(mid)] = {"self_aF": round(mean[i_self] * 1e18, 4),
+                              "self_rel_se": float(se[i_self] / mean[i_self]),
+                              "ground_aF": round(mean[ids.index(-1)] * 1e18, 4),
+                              "sum_abs_couplings_aF": round(float(np.sum(np.abs(
+                                  [mean[j] for j, c in enumerate(ids) if c not in (mid, -1)])))
+                                  * 1e18, 4)}
+    total = per * world * len(masters)
+    return {"metric": "frw_walks_per_s", "unit": "walks/s", "value": total / dev_s,
+            "e2e": {"value": total / wall_s, "unit": "walks/s",
+                    "h2d_bytes_per_step": sum(len(d) for d in docs.values()),
+                    "d2h_bytes_per_step": 32 * per * len(masters)},
+            "scaling": "strong",
+            "config": {"workload": "C5 (BASELINE configs[4]): 200 box conductors in a 10x10x2 um "
+                                   "world, 4 z layers, 20 nm coatings, 50 high-k blocks; "
+                                   "HYBRID-MW, N=24; 10 masters x 1e7 walks = 1e8 walks in total",
+                       "walks_total": total, "walks_per_rank_per_master": per,
+                       "parallelism": f"dp{world} (walk ranges per rank, one all-reduce of the "
+                                      "per-master tallies)",
+                       "sgf_table": "warm (2^18 walks per master first)"},
+            "rows": out_rows}
 
 
 def run_gpu(args):
@@ -372,6 +454,8 @@ def run_gpu(args):
         ctx2.close()
 
     walks = None if args.no_walks else walk_engine_bench(args, rank, world, dist, torch)
+    walks_c5 = None if (args.no_walks or args.c5_walks <= 0) else \
+        walk_engine_c5(args, rank, world, dist, torch)
 
     if rank != 0:
         if dist is not None:
@@ -438,6 +522,8 @@ def run_gpu(args):
                                      "geometry queries, table lookups and divergence are the "
                                      "gap to the on-chip roofline"}
         out["walk_engine"] = walks
+    if walks_c5 is not None:
+        out["walk_engine_c5"] = walks_c5
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(seconds=args.ref_seconds)
     print(json.dumps(out))
@@ -459,6 +545,7 @@ def main():
     ap.add_argument("--no-walks", action="store_true")
     ap.add_argument("--walks", type=int, default=1_000_000)
     ap.add_argument("--walk-steps", type=int, default=3)
+    ap.add_argument("--c5-walks", type=int, default=100_000_000)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
