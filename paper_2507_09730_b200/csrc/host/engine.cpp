@@ -61,7 +61,7 @@ void Config::validate() const {
   if (!(gaussian_gap_fraction > 0.0 && gaussian_gap_fraction < 1.0))
     throw std::invalid_argument("gaussian_gap_fraction must lie in (0,1)");
   if (grid_n > 64) throw std::invalid_argument("grid_n must be <= 64 on the device");
-  if (device_batch < 1) throw std::invalid_argument("device_batch must be >= 1");
+  if (device_batch < 0) throw std::invalid_argument("device_batch must be >= 0 (0 = auto)");
 }
 
 // engine.cpp:84-124
@@ -366,7 +366,9 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   std::vector<double> ts(nslots), tq(nslots);
   std::vector<uint64_t> tl(nslots);
   const long batch = cfg_.batch;
-  const long dev_batch = std::max<long>(batch, cfg_.device_batch / batch * batch);
+  const long db = cfg_.device_batch > 0 ? cfg_.device_batch
+                  : cfg_.min_walks >= cfg_.max_walks ? (1L << 24) : (1L << 22);
+  const long dev_batch = std::max<long>(batch, db / batch * batch);
   // fold one chunk's per-walk results in walk order, one reference batch at
   // a time, with the stopping rule after each batch (engine.cpp:378-420)
   auto fold = [&](const frw_walk_record* rec, int64_t chunk) {

@@ -303,7 +303,10 @@ struct Config {
   // B200 knobs (defaults keep the reference behaviour)
   RngMode rng = RngMode::Philox;
   bool all_couplings_rule = false;  // stop when every coupling meets tol (C4)
-  long device_batch = 1 << 22;      // walks per frw_run_walks call (one tail each)
+  // walks per frw_run_walks call (each drains its pool through one tail);
+  // 0 = auto: up to 2^24 when the walk count is fixed (min == max walks),
+  // 2^22 while a stopping rule is tested (a speculative chunk is discarded)
+  long device_batch = 0;
   int device = 0;
 
   void validate() const;

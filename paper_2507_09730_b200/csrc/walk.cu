@@ -65,6 +65,7 @@ constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
 enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3 };
 
+
 // ---------------------------------------------------------------------------
 // device-side views
 
@@ -1615,6 +1616,9 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
 #define FRW_TAIL_BLOCKS 2
 #endif
 constexpr int kTailBlocks = FRW_TAIL_BLOCKS;  // resident 256-thread CTAs per SM
+#ifndef FRW_TAIL_REPS
+#define FRW_TAIL_REPS 32  // MicroWalk super-steps per transition in k_tail
+#endif
 template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
@@ -1651,7 +1655,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     // MicroWalk lanes run long stretches between the divergent transitions
     // (8: 1.64e7, 16: 1.76e7, 32: 1.76e7 C3 walks/s; C5 MWE best at 32)
 #pragma unroll 1
-    for (int rep = 0; rep < 32; ++rep) {
+    for (int rep = 0; rep < FRW_TAIL_REPS; ++rep) {
       const unsigned mwm = __ballot_sync(0xFFFFFFFFu, live && in_mw);
       if (!mwm) break;
 #if FRW_TAIL_POLICY
