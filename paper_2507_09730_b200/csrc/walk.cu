@@ -1397,7 +1397,7 @@ __device__ __forceinline__ int mw_step(const DParams& P, const DirDelta* dd, MwL
       dir += acc[d] <= tl;
       dh += acc[d] <= th;
     }
-    if (dh != dir) {
+    if (__builtin_expect(dh != dir, 0)) {
       const uint64_t x53 = xl | (philox53(P, L.wid, tie_ctr, 1u) & 0x1FFFFF);
       const double target = static_cast<double>(x53) * 0x1.0p-53 * sum;
       dir = 0;
@@ -1437,6 +1437,10 @@ __device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* 
   __syncthreads();
 }
 
+#ifndef FRW_STEP_UNROLL
+#define FRW_STEP_UNROLL 0
+#endif
+
 // Events of a MicroWalk super-step
 enum : int { MW_GO = 0, MW_SURFACE = 1, MW_COND = 3, MW_CAP = 4 };
 
@@ -1460,11 +1464,11 @@ __device__ __forceinline__ void mw_jump_r(const DJump& J, MwLane& L, int m, uint
   const int v = static_cast<int>(idx) / side;
   const int u = static_cast<int>(idx) - v * side;
   const int a = face >> 1;
-  int dl[3];
-  dl[a] = (face & 1) ? m : -m;
-  // panel (face, v, u) conventions of surface_panel_of (sgf.cpp:13-30)
-  dl[a == 0 ? 1 : 0] = u - (m - 1);
-  dl[a == 2 ? 1 : 2] = v - (m - 1);
+  // displacement: +-m along the face axis a, the panel's (u, v) across it in
+  // the conventions of surface_panel_of (sgf.cpp:13-30: a=0 (y,z), a=1
+  // (x,z), a=2 (x,y)); selects, not an indexed array (no local memory)
+  const int sm = (face & 1) ? m : -m, du = u - (m - 1), dv = v - (m - 1);
+  const int dl[3] = {a == 0 ? sm : du, a == 0 ? du : (a == 1 ? sm : dv), a == 2 ? sm : dv};
   L.node += static_cast<uint32_t>(dl[0] + dl[1] * 256 + dl[2] * 65536);
   // byte 2a: distance to the low face (+delta), byte 2a+1: to the high face
   long long dr = 0;
@@ -1517,6 +1521,7 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
     u0 = 2;
     if (P.jump.twice && L.steps < cap && mw_jump(P.jump, L, w4[2], w4[3])) u0 = 4;
   }
+#if FRW_STEP_UNROLL
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     if (u >= u0 && code == 0 && L.steps < cap) {
@@ -1525,6 +1530,17 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
       code = mw_step<RNG>(P, dd, L, w4[u], z, static_cast<uint32_t>(L.rng * 4 + u), xdir);
     }
   }
+#else
+  // one copy of the step body (the unrolled four made the super-step ~24 KB
+  // of SASS: warps stalled on instruction fetch at its reconvergence points)
+#pragma unroll 1
+  for (int u = u0; u < 4 && code == 0 && L.steps < cap; ++u) {
+    const uint32_t w = u == 0 ? w4[0] : u == 1 ? w4[1] : u == 2 ? w4[2] : w4[3];
+    uint64_t z = 0;
+    if (RNG == FRW_RNG_SPLITMIX_PARITY) z = sm64_next(L.rng);
+    code = mw_step<RNG>(P, dd, L, w, z, static_cast<uint32_t>(L.rng * 4 + u), xdir);
+  }
+#endif
   if (RNG == FRW_RNG_PHILOX) ++L.rng;  // next 4-word block
   if (code == 2) {
     ++L.cchg;
