@@ -34,6 +34,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -108,6 +109,7 @@ struct DSgf {
   const double* keys;        // [entries][NMAX]
   const double* pitch;       // [entries]
   const double* const* data; // [entries] -> cdf[P], probs[P], kern[3][P]
+  const int* uentry;         // [PMAX] entry of the uniform key of each palette class, -1
 };
 
 // Lattice jumps (Philox mode only).  Inside one cell every alpha is 1/2, so
@@ -503,8 +505,12 @@ __device__ __forceinline__ double uniform(const DParams& P, long long wid, Rng& 
 // -2 (error: slice centre outside the world)
 __device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih);
 
+// ucls (optional): when every slice has one palette class the key is that
+// class's uniform key; *ucls gets the class and `layers` is left unwritten
+// (the caller looks the key up through DSgf::uentry), else *ucls = -1
 __device__ int stratified_key(const DStruct& s, const double c[3], double h, int n,
-                              double* layers) {
+                              double* layers, int* ucls = nullptr) {
+  if (ucls) *ucls = -1;
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
   int hits[KMAX];
   int nh = 0;
@@ -542,6 +548,10 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
     for (int a = 0; a < 3 && axis < 0; ++a)
       if (cov[a]) axis = a;
   if (axis < 0) return -1;
+  if (ucls && nh == 0) {  // background only: the uniform background key
+    *ucls = s.bg;
+    return 0;
+  }
   const double pitch = 2.0 * h / n;
   int cls0 = -1;
   bool uniform = true;
@@ -560,6 +570,14 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
                 __ldg(s.dbox + 6 * hits[q] + 3 + axis), &lo, &hi);
       const int cq = __ldg(s.dcls + hits[q]);
       for (int t = lo; t <= hi; ++t) scls[t] = cq;
+    }
+    if (ucls) {
+      bool one = true;
+      for (int t = 1; t < n && one; ++t) one = scls[t] == scls[0];
+      if (one) {
+        *ucls = scls[0];
+        return 0;
+      }
     }
   }
   for (int t = 0; t < n; ++t) {
@@ -1173,14 +1191,25 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   double c[3], h;
   transit_cube(L.p, fh, n, c, &h);
   double layers[NMAX];
-  const int axis = stratified_key(s, c, h, n, layers);
+  int ucls;
+  const int axis = stratified_key(s, c, h, n, layers, &ucls);
   if (axis == -2) {
     set_err(C, FRW_EINVAL);
     W.state[slot] = S_FREE;
     return 1;
   }
   if (axis >= 0) {
-    const int e = sgf_find(T, n, axis, layers);
+    // a single-class cube (2/3 of the cached hops on C3/C5) finds its entry
+    // through the per-class uniform index; otherwise (or when that key is
+    // not in the table yet) the full key is hashed and compared
+    int e = ucls >= 0 ? __ldg(T.uentry + ucls) : -1;
+    if (e < 0) {
+      if (ucls >= 0) {
+        const double v = __ldg(s.rpal + ucls);
+        for (int t = 0; t < n; ++t) layers[t] = v;
+      }
+      e = sgf_find(T, n, axis, layers);
+    }
     if (e < 0) {
       // parked mid-walk: the key is looked up before any draw, so the walk
       // resumes from this state, bit-identical to an uninterrupted run
@@ -1632,6 +1661,9 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
 #define FRW_TAIL_BLOCKS 2
 #endif
 constexpr int kTailBlocks = FRW_TAIL_BLOCKS;  // resident 256-thread CTAs per SM
+#ifndef FRW_TAIL_CHAIN
+#define FRW_TAIL_CHAIN 1  // transitions per k_tail iteration while cached
+#endif
 #ifndef FRW_TAIL_REPS
 #define FRW_TAIL_REPS 32  // MicroWalk super-steps per transition in k_tail
 #endif
@@ -1656,8 +1688,12 @@ __global__ void __launch_bounds__(256, kTailBlocks)
   if (live) adv_load(W, aq[item], A);
   while (__any_sync(0xFFFFFFFFu, live)) {
     if (live && !in_mw) {
-      int r;
-      r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
+      // up to FRW_TAIL_CHAIN transitions back to back while they are cached
+      // hops (each would otherwise wait out a whole MicroWalk stretch)
+      int r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
+#pragma unroll 1
+      for (int k = 1; k < FRW_TAIL_CHAIN && r == 0; ++k)
+        r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
       if (r == 2) {
         in_mw = true;
         mw_arm(W, alpha_sm, s.P, A.slot, n, L);
@@ -2426,6 +2462,10 @@ struct SgfHost {
   double** d_data = nullptr;
   size_t dev_entries_cap = 0;
   bool dirty = false;
+  // uniform keys (axis 0, all layers equal): layer value -> first entry,
+  // mirrored per palette class into d_uentry by uentry_sync
+  std::map<double, int> uniform;
+  int* d_uentry = nullptr;
 };
 
 struct Engine {
@@ -2465,6 +2505,7 @@ struct Engine {
   // FDM solve scratch (5 Krylov vectors per persistent CTA)
   double* fdm_slab = nullptr;
   size_t fdm_cap = 0;
+  std::vector<double> h_rpal;  // palette rounded to 6 significant digits (host copy)
   // lattice-jump tables (DJump) for lattice size jump_n, radii 2..jump_mmax
   int jump_n = 0, jump_mmax = 0;
   JumpMeta* d_jmeta = nullptr;
@@ -2529,6 +2570,7 @@ void engine_free(frw_ctx* ctx) {
   cudaFree(E->sgf.d_keys);
   cudaFree(E->sgf.d_pitch);
   cudaFree(E->sgf.d_data);
+  cudaFree(E->sgf.d_uentry);
   free_slots(*E);
   cudaFree(E->recs);
   cudaFree(E->d_cnt);
@@ -2604,6 +2646,23 @@ int sgf_sync(frw_ctx* ctx, SgfHost& T) {
                                   cudaMemcpyHostToDevice, ctx->stream));
   }
   T.dirty = false;
+  return FRW_OK;
+}
+
+// per palette class: the table entry of its uniform key, or -1
+int uentry_sync(frw_ctx* ctx, Engine& E) {
+  SgfHost& T = E.sgf;
+  if (!T.d_uentry) {
+    T.d_uentry = dalloc<int>(PMAX);
+    if (!T.d_uentry) return frw_fail(ctx, FRW_ENOMEM, "sgf table: device allocation failed");
+  }
+  std::vector<int> u(PMAX, -1);
+  for (size_t c = 0; c < E.h_rpal.size() && c < static_cast<size_t>(PMAX); ++c) {
+    const auto it = T.uniform.find(E.h_rpal[c]);
+    if (it != T.uniform.end()) u[c] = it->second;
+  }
+  FRW_CUDA(ctx, cudaMemcpyAsync(T.d_uentry, u.data(), 4 * PMAX, cudaMemcpyHostToDevice,
+                                ctx->stream));
   return FRW_OK;
 }
 
@@ -2851,7 +2910,8 @@ int resolve_misses(frw_ctx* ctx, Engine& E, int n, unsigned long long nmiss, frw
   if (static_cast<int>(E.sgf.axis.size()) == before)
     return frw_fail(ctx, FRW_EMISS, "run_walks: miss callback added no table entry");
   *added = static_cast<int>(E.sgf.axis.size()) - before;
-  return sgf_sync(ctx, E.sgf);
+  if (int rc = sgf_sync(ctx, E.sgf)) return rc;
+  return uentry_sync(ctx, E);
 }
 
 int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
@@ -2943,6 +3003,7 @@ int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double
     E.M.layers = dalloc<double>(size_t(kMissMax) * NMAX);
   }
   if (int rc = sgf_sync(ctx, E.sgf)) return rc;
+  if (int rc = uentry_sync(ctx, E)) return rc;
   const DStruct s = make_dstruct(E);
   DParams P = params_of(prm);
   P.rng = FRW_RNG_SPLITMIX_PARITY;  // the caller's SplitMix64 streams
@@ -2979,7 +3040,7 @@ int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double
     }
     const int np = static_cast<int>(pend.size());
     DSgf T{E.sgf.cap, E.sgf.d_hash, E.sgf.d_entry, E.sgf.d_axis, E.sgf.d_keys, E.sgf.d_pitch,
-           E.sgf.d_data};
+           E.sgf.d_data, E.sgf.d_uentry};
     cudaMemcpyAsync(d_idx, pend.data(), 4 * size_t(np), cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), st);
     launch(s, T, P, E, d_pts, d_ax, d_st, d_idx, np, d_rc, d_out);
@@ -3079,6 +3140,7 @@ int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
                                 ctx->stream));
   FRW_CUDA(ctx, cudaMemcpyAsync(E.d_alpha, alpha.data(), 8 * size_t(P) * P, cudaMemcpyHostToDevice,
                                 ctx->stream));
+  E.h_rpal = rpal;
   FRW_CUDA(ctx, cudaMemcpyAsync(E.d_rpal, rpal.data(), 8 * P, cudaMemcpyHostToDevice,
                                 ctx->stream));
   // conductor bins for many-conductor structures (C5: 200 conductors)
@@ -3315,6 +3377,11 @@ int frw_sgf_put(frw_ctx* ctx, int n, int axis, const double* layers, double pitc
   T.pitch.push_back(pitch);
   T.data.push_back(blk);
   sgf_insert_index(T, h, e);
+  if (axis == 0) {
+    bool same = true;
+    for (int t = 1; t < n && same; ++t) same = layers[t] == layers[0];
+    if (same) T.uniform.emplace(layers[0], e);  // the first stored entry wins
+  }
   T.dirty = true;
   return FRW_OK;
 }
@@ -3337,6 +3404,7 @@ int frw_sgf_clear(frw_ctx* ctx) {
   fresh.d_keys = E.sgf.d_keys;
   fresh.d_pitch = E.sgf.d_pitch;
   fresh.d_data = E.sgf.d_data;
+  fresh.d_uentry = E.sgf.d_uentry;
   fresh.dev_entries_cap = E.sgf.dev_entries_cap;
   fresh.dirty = true;
   E.sgf = fresh;
@@ -3558,6 +3626,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     E.M.layers = dalloc<double>(size_t(kMissMax) * NMAX);
   }
   if (int rc = sgf_sync(ctx, E.sgf)) return rc;
+  if (int rc = uentry_sync(ctx, E)) return rc;
 
   const DStruct s = make_dstruct(E);
   DParams P = params_of(prm);
@@ -3589,7 +3658,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   int status = FRW_OK;
   for (int round = 0;; ++round) {
     DSgf T{E.sgf.cap, E.sgf.d_hash, E.sgf.d_entry, E.sgf.d_axis, E.sgf.d_keys, E.sgf.d_pitch,
-           E.sgf.d_data};
+           E.sgf.d_data, E.sgf.d_uentry};
     int* aq_in = E.aq[round & 1];
     int* aq_out = E.aq[(round + 1) & 1];
     if (trace) cudaEventRecord(a0, ctx->stream);
