@@ -321,6 +321,15 @@ def walk_engine_c5(args, rank, world, dist, torch):
             "rows": out_rows}
 
 
+def _profile_walk():
+    """the committed ncu --set full summary of the walk engine's largest
+    kernel on C3 (profiles/r01_ncu_full_c3_ktail.json), else {}"""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full_c3_ktail.json")))
+    except Exception:
+        return {}
+
+
 def run_gpu(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -515,12 +524,31 @@ def run_gpu(args):
         inversions = (d["subsequent"]["cached"] + sum(d["first"].values())) / args.walks
         bpw = 56.0 * walks["mw_steps_per_walk"] + 96.0 * inversions + 32.0
         ach = bpw * walks["value"] / 1e9
+        pw = _profile_walk()
+        m = pw.get("metrics", {})
+
+        def _num(k):
+            try:
+                return float(str(m[k]).split()[0])
+            except Exception:
+                return None
+
         walks["roofline"] = {"bound": "smem", "achieved": ach, "peak": smem_peak / 1e9,
                              "unit": "GB/s", "frac": ach * 1e9 / smem_peak,
                              "algorithmic_bytes_per_walk": bpw,
                              "note": "whole engine (all walk kernels) over device time; the "
                                      "geometry queries, table lookups and divergence are the "
-                                     "gap to the on-chip roofline"}
+                                     "gap to the on-chip roofline.  The engine is bound by "
+                                     "instruction issue under SIMT divergence, not by bytes: "
+                                     "issue_* are the committed ncu capture of its largest "
+                                     "kernel (the run-to-completion tail)",
+                             "issue_kernel": pw.get("kernel"),
+                             "issue_active_frac": (_num("smsp__issue_active.avg."
+                                                        "pct_of_peak_sustained_active") or 0) / 100
+                             if m else None,
+                             "issue_active_lanes_per_inst": _num(
+                                 "smsp__thread_inst_executed_per_inst_executed.ratio"),
+                             "issue_top_stalls": pw.get("top_stalls_per_issue")}
         out["walk_engine"] = walks
     if walks_c5 is not None:
         out["walk_engine_c5"] = walks_c5

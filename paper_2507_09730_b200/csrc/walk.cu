@@ -505,6 +505,9 @@ __device__ __forceinline__ double uniform(const DParams& P, long long wid, Rng& 
 // -2 (error: slice centre outside the world)
 __device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih);
 
+#ifndef FRW_UKEY
+#define FRW_UKEY 1  // uniform-key index for single-class cubes (advance_once)
+#endif
 // ucls (optional): when every slice has one palette class the key is that
 // class's uniform key; *ucls gets the class and `layers` is left unwritten
 // (the caller looks the key up through DSgf::uentry), else *ucls = -1
@@ -1191,8 +1194,8 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   double c[3], h;
   transit_cube(L.p, fh, n, c, &h);
   double layers[NMAX];
-  int ucls;
-  const int axis = stratified_key(s, c, h, n, layers, &ucls);
+  int ucls = -1;
+  const int axis = stratified_key(s, c, h, n, layers, FRW_UKEY ? &ucls : nullptr);
   if (axis == -2) {
     set_err(C, FRW_EINVAL);
     W.state[slot] = S_FREE;
