@@ -846,62 +846,54 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
                               double h, int n, bool conductors, DCounters* C) {
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
   uint64_t* A = W.atlas + static_cast<size_t>(slot) * kAtlasWords;
-  int K = 0;
+  int K = 0, ncond = 0;
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
   int cand[kCandMax];
-  const int ccand = conductors ? grid_candidates(s, false, cb, cand) : 0;
-  for (int i = 0, ni = !conductors ? 0 : (ccand < 0 ? s.nc : ccand); i < ni; ++i) {
-    const int q = ccand < 0 ? i : cand[i];
-    const double* b = s.cbox + 6 * q;
-    double bb[6];
-#pragma unroll
-    for (int t = 0; t < 6; ++t) bb[t] = __ldg(b + t);
-    if (bb[0] > cb[3] || bb[3] < cb[0] || bb[1] > cb[4] || bb[4] < cb[1] || bb[2] > cb[5] ||
-        bb[5] < cb[2])
-      continue;
-    int lo[3], hi[3];
-    bool empty = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      clip_axis(c[a], h, n, bb[a], bb[3 + a], &lo[a], &hi[a]);
-      empty |= lo[a] > hi[a];
-    }
-    if (empty) continue;
-    if (K == KMAX) {
-      set_err(C, FRW_EINVAL);
-      return -1;
-    }
-    boxes[K++] = pack_box(lo, hi, 0x8000ull | static_cast<uint64_t>(q));
-  }
-  const int ncond = K;
   uint8_t* cls = reinterpret_cast<uint8_t*>(A + kAtCls);
-  const int dcand = grid_candidates(s, true, cb, cand);
-  for (int i = 0, ni = dcand < 0 ? s.nd : dcand; i < ni; ++i) {
-    const int d = dcand < 0 ? i : cand[i];
-    const double* b = s.dbox + 6 * d;
-    double bb[6];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) bb[q] = __ldg(b + q);
-    // voxel centres lie inside the closed cube: a box that misses the cube
-    // cannot contain one (cheap reject before the exact clip)
-    if (bb[0] > cb[3] || bb[3] < cb[0] || bb[1] > cb[4] || bb[4] < cb[1] || bb[2] > cb[5] ||
-        bb[5] < cb[2])
-      continue;
-    int lo[3], hi[3];
-    bool empty = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      clip_axis(c[a], h, n, bb[a], bb[3 + a], &lo[a], &hi[a]);
-      empty |= lo[a] > hi[a];
+  // phase 0: conductor boxes (MicroWalk-E only), phase 1: dielectric boxes,
+  // each in declaration order.  One rolled loop (one inlined copy of the
+  // candidate query and the clip): the walk kernels are instruction-fetch
+  // bound, and the box-axis work is not on a hot path
+#pragma unroll 1
+  for (int ph = conductors ? 0 : 1; ph < 2; ++ph) {
+    const bool cph = ph == 0;
+    if (!cph) ncond = K;
+    const int nca = grid_candidates(s, !cph, cb, cand);
+    const int ni = nca < 0 ? (cph ? s.nc : s.nd) : nca;
+    const double* base = cph ? s.cbox : s.dbox;
+#pragma unroll 1
+    for (int i = 0; i < ni; ++i) {
+      const int q = nca < 0 ? i : cand[i];
+      const double* bx = base + 6 * q;
+      // voxel centres lie inside the closed cube: a box that misses the
+      // cube cannot contain one (cheap reject before the exact clip)
+      if (__ldg(bx + 0) > cb[3] || __ldg(bx + 3) < cb[0] || __ldg(bx + 1) > cb[4] ||
+          __ldg(bx + 4) < cb[1] || __ldg(bx + 2) > cb[5] || __ldg(bx + 5) < cb[2])
+        continue;
+      uint64_t pk = 0;  // pack_box layout: lo bytes 0-2, hi bytes 3-5
+      bool empty = false;
+#pragma unroll 1
+      for (int ax = 0; ax < 3; ++ax) {
+        const double ca = ax == 0 ? c[0] : (ax == 1 ? c[1] : c[2]);
+        int l, hh;
+        clip_axis(ca, h, n, __ldg(bx + ax), __ldg(bx + 3 + ax), &l, &hh);
+        empty |= l > hh;
+        pk |= static_cast<uint64_t>(l & 0xFF) << (8 * ax) |
+              static_cast<uint64_t>(hh & 0xFF) << (24 + 8 * ax);
+      }
+      if (empty) continue;
+      if (K == KMAX) {
+        set_err(C, FRW_EINVAL);  // more than KMAX boxes reach into one cube
+        return -1;
+      }
+      if (cph) {
+        boxes[K++] = pk | (0x8000ull | static_cast<uint64_t>(q)) << 48;
+      } else {
+        const int dc = __ldg(s.dcls + q);
+        cls[K] = static_cast<uint8_t>(dc);
+        boxes[K++] = pk | static_cast<uint64_t>(dc) << 48;
+      }
     }
-    if (empty) continue;
-    if (K == KMAX) {
-      set_err(C, FRW_EINVAL);  // more than KMAX boxes reach into one cube
-      return -1;
-    }
-    const int dc = __ldg(s.dcls + d);
-    cls[K] = static_cast<uint8_t>(dc);
-    boxes[K++] = pack_box(lo, hi, static_cast<uint64_t>(dc));
   }
   uint64_t bm[3];
   build_atlas(boxes, K, n, A, bm);
@@ -1240,8 +1232,11 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   // the expanded lattice swallows the start voxel (EngulfedStart)
   int rc = -1;
   uint8_t kind = P.mode == FRW_MODE_FDM ? 2 : 0;  // 2: FDM solve (engine.cpp:311-318)
+  double jc[3] = {c[0], c[1], c[2]}, jh = h;
+  bool expanded = false;
   if (P.mode == FRW_MODE_MWE || P.mode == FRW_MODE_HYBRID_MWE) {
     kind = 1;
+    expanded = true;
     const double wall = cheb_wall(s.world, L.p);
     const double half = mn(P.expansion * fh, wall);  // microwalk.cpp:213-214
     if (!(half > 0)) {
@@ -1249,11 +1244,20 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
       W.state[slot] = S_FREE;
       return 1;
     }
-    double ec[3], eh;
-    transit_cube(L.p, half, n, ec, &eh);
-    rc = compile_mw_job(s, W, slot, ec, eh, n, true, C);
+    transit_cube(L.p, half, n, jc, &jh);
   }
-  if (rc == 0 || kind != 1) rc = compile_mw_job(s, W, slot, c, h, n, false, C);
+  // one inlined copy of the job compiler (the kernels are instruction-fetch
+  // bound): the expanded cube first, the transit cube on EngulfedStart
+#pragma unroll 1
+  for (;;) {
+    rc = compile_mw_job(s, W, slot, jc, jh, n, expanded, C);
+    if (rc != 0 || !expanded) break;
+    expanded = false;
+    jc[0] = c[0];
+    jc[1] = c[1];
+    jc[2] = c[2];
+    jh = h;
+  }
   if (rc < 0) {
     W.state[slot] = S_FREE;
     return 1;
@@ -1271,8 +1275,12 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
 }
 
 // persistent: each thread takes ACTIVE walks from the queue and advances
-// them one transition per iteration, re-armed as soon as its walk leaves
-__global__ void __launch_bounds__(256)
+// them one transition per iteration, re-armed as soon as its walk leaves.
+// The grid is 4 x 256 threads per SM, so registers must allow 4 CTAs
+#ifndef FRW_ADV_MINB
+#define FRW_ADV_MINB 4
+#endif
+__global__ void __launch_bounds__(256, FRW_ADV_MINB)
     k_advance(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
               const int* aq, int* mq) {
   const unsigned long long alen = C->alen;
