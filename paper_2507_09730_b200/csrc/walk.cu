@@ -585,7 +585,7 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
   }
   for (int t = 0; t < n; ++t) {
     int cls;
-    if (!overflow) {
+    if (__builtin_expect(!overflow, 1)) {
       cls = scls[t];
     } else {
       double p[3] = {c[0], c[1], c[2]};
@@ -613,6 +613,7 @@ __host__ __device__ __forceinline__ uint64_t key_step(uint64_t h, uint64_t w) {
 }
 __device__ __forceinline__ uint64_t key_hash(int n, int axis, const double* layers) {
   uint64_t h = (static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis);
+#pragma unroll 1
   for (int t = 0; t < n; ++t)
     h = key_step(h, static_cast<uint64_t>(__double_as_longlong(layers[t])));
   return sm64_mix(h);
@@ -628,6 +629,7 @@ __device__ int sgf_find(const DSgf& T, int n, int axis, const double* layers) {
     if (__ldg(T.hash + i) != h || __ldg(T.axis + e) != axis) continue;
     const double* k = T.keys + static_cast<size_t>(e) * NMAX;
     bool eq = true;
+#pragma unroll 1
     for (int t = 0; t < n && eq; ++t) eq = __ldg(k + t) == layers[t];
     if (eq) return e;
   }
@@ -814,6 +816,7 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
 #pragma unroll 1
   for (int a = 0; a < 3; ++a) {
     uint64_t b = 1;  // segment starting at 0
+#pragma unroll 1
     for (int q = 0; q < K; ++q) {
       const uint64_t x = boxes[q];
       const int h = box_hi(x, a) + 1;
@@ -826,6 +829,7 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
     for (uint64_t y = b; y; y &= y - 1, ++sg) {
       const int st = __ffsll(y) - 1;
       uint64_t m = 0;
+#pragma unroll 1
       for (int q = 0; q < K; ++q) {
         const uint64_t x = boxes[q];
         if (box_lo(x, a) <= st && st <= box_hi(x, a)) m |= 1ull << q;
