@@ -178,8 +178,6 @@ struct DSlots {
   uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class / conductor index
   uint64_t* atlas;       // [S][kAtlasWords] cell atlas of the job (see cell_info)
   uint8_t* mwkind;       // [S] 0 plain MicroWalk job, 1 expanded (MicroWalk-E), 2 FDM
-  uint64_t* room;        // [S] start cell distances (6 bytes, dir order)
-  uint64_t* fc;          // [S] start cell + face-neighbour classes
 };
 
 // Work queues of one round: k_spawn and the previous round's k_mw fill the
@@ -902,13 +900,11 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
   uint64_t bm[3];
   build_atlas(boxes, K, n, A, bm);
   const int m = (n - 1) / 2;  // start_node (sgf.hpp:58-61)
-  const uint32_t node = m | (m << 8) | (m << 16);
-  uint64_t room;
-  const uint64_t fc = cell_info(A, bm, ncond, s.bg, n, node, &room);
-  if (((fc >> 48) & 0xFF) == kCond) return 0;  // EngulfedStart (microwalk.cpp:83-86)
+  const int v0[3] = {m, m, m};
+  // EngulfedStart (microwalk.cpp:83-86): a conductor box holds the start
+  // voxel.  The start cell itself is looked up by the first super-step.
+  if (voxel_mask(A, bm, v0) & cond_mask(ncond)) return 0;
   W.nbox[slot] = static_cast<uint8_t>(ncond);
-  W.room[slot] = room;
-  W.fc[slot] = fc;
   W.cube[4 * slot + 0] = c[0];
   W.cube[4 * slot + 1] = c[1];
   W.cube[4 * slot + 2] = c[2];
@@ -1351,15 +1347,13 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, const double* alpha_sm, 
   L.slot = slot;
   L.wid = W.wid[slot];
   L.node = m | (m << 8) | (m << 16);
-  L.room = W.room[slot];
-  L.fc = W.fc[slot];
+  L.room = 0;  // cell pending: the first super-step looks it up
   L.rng = W.rng[slot];
   L.ncond = W.nbox[slot];
   L.bm[0] = A[kAtBm];
   L.bm[1] = A[kAtBm + 1];
   L.bm[2] = A[kAtBm + 2];
   L.steps = 0;
-  lane_alphas(alpha_sm, Pn, L);
 }
 
 // a move left the current cell: look the new cell up in the atlas
@@ -1558,6 +1552,9 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
     w4[2] = o.z;
     w4[3] = o.w;
   }
+  // a pending cell (new hop, or a move into another cell last super-step):
+  // one inlined copy of the atlas lookup serves both
+  if ((L.room >> 48) == 0) mw_cell_change(W, alpha_sm, Pn, bg, n, L);
   int code = 0;
   int u0 = 0;  // words taken by jumps (two per jump)
   if (RNG == FRW_RNG_PHILOX && P.jump.mmax >= 2 && L.steps < cap &&
@@ -1586,9 +1583,9 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
   }
 #endif
   if (RNG == FRW_RNG_PHILOX) ++L.rng;  // next 4-word block
-  if (code == 2) {
+  if (code == 2) {  // moved into another cell: looked up next super-step
     ++L.cchg;
-    mw_cell_change(W, alpha_sm, Pn, bg, n, L);
+    L.room = 0;
     code = 0;
   }
   if (code == 0 && L.steps >= cap) return MW_CAP;
@@ -2544,8 +2541,6 @@ void free_slots(Engine& E) {
   cudaFree(E.W.nbox);
   cudaFree(E.W.boxes);
   cudaFree(E.W.mwkind);
-  cudaFree(E.W.room);
-  cudaFree(E.W.fc);
   cudaFree(E.W.atlas);
   cudaFree(E.queue);
   cudaFree(E.aq[0]);
@@ -2949,8 +2944,6 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   W.nbox = dalloc<uint8_t>(S);
   W.boxes = dalloc<uint64_t>(size_t(S) * KMAX);
   W.mwkind = dalloc<uint8_t>(S);
-  W.room = dalloc<uint64_t>(S);
-  W.fc = dalloc<uint64_t>(S);
   W.atlas = dalloc<uint64_t>(size_t(S) * kAtlasWords);
   E.queue = dalloc<int>(S);
   E.aq[0] = dalloc<int>(S);
@@ -2968,8 +2961,8 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   E.M.pend = dalloc<long long>(2 * size_t(S));
   E.M.park = dalloc<int>(2 * size_t(S));
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
-      !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes || !W.room ||
-      !W.fc || !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.ring_a ||
+      !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes ||
+      !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.ring_a ||
       !E.ring_m || !E.M.retry || !E.M.pend || !E.M.park) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
