@@ -394,12 +394,14 @@ __device__ int eps_class_at(const DStruct& s, const double p[3]) {
   if (s.g.dims[0]) {  // the last declared box containing p: max index among candidates
     const DGrid& g = s.g;
     int best = -1;
+#pragma unroll 1
     for (int q = 0; q < g.ndlarge; ++q) {
       const int d = __ldg(g.dlarge + q);
       if (d > best && box_contains(s.dbox + 6 * d, p)) best = d;
     }
     const int bin = (bin_of(g, 2, p[2]) * g.dims[1] + bin_of(g, 1, p[1])) * g.dims[0] +
                     bin_of(g, 0, p[0]);
+#pragma unroll 1
     for (int q = __ldg(g.dstart + bin), e = __ldg(g.dstart + bin + 1); q < e; ++q) {
       const int d = __ldg(g.ditem + q);
       if (d > best && box_contains(s.dbox + 6 * d, p)) best = d;
@@ -407,6 +409,7 @@ __device__ int eps_class_at(const DStruct& s, const double p[3]) {
     return best < 0 ? s.bg : __ldg(s.dcls + best);
   }
   int cls = s.bg;
+#pragma unroll 1
   for (int d = 0; d < s.nd; ++d)
     if (box_contains(s.dbox + 6 * d, p)) cls = __ldg(s.dcls + d);
   return cls;
@@ -564,12 +567,14 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
   // c - h + (t + 0.5) pitch lies in [lo, hi], the reference's inclusion test
   int scls[NMAX];
   if (!overflow) {
+#pragma unroll 1
     for (int t = 0; t < n; ++t) scls[t] = s.bg;
     for (int q = 0; q < nh; ++q) {
       int lo, hi;
       clip_axis(c[axis], h, n, __ldg(s.dbox + 6 * hits[q] + axis),
                 __ldg(s.dbox + 6 * hits[q] + 3 + axis), &lo, &hi);
       const int cq = __ldg(s.dcls + hits[q]);
+#pragma unroll 1
       for (int t = lo; t <= hi; ++t) scls[t] = cq;
     }
     if (ucls) {
@@ -599,6 +604,7 @@ __device__ int stratified_key(const DStruct& s, const double c[3], double h, int
   if (uniform) axis = 0;
   // profile_key: uniform rounded layers normalise to axis 0
   bool same = true;
+#pragma unroll 1
   for (int t = 1; t < n; ++t) same &= layers[t] == layers[0];
   if (same) axis = 0;
   return axis;
@@ -650,6 +656,7 @@ __device__ void record_key(DCounters* C, const DMiss& M, int n, int axis, const 
   const unsigned long long m = atomicAdd(&C->nmiss, 1ull);
   if (m < kMissMax) {
     M.axis[m] = axis;
+#pragma unroll 1
     for (int t = 0; t < n; ++t) M.layers[m * NMAX + t] = layers[t];
   }
 }
@@ -1201,6 +1208,7 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     if (e < 0) {
       if (ucls >= 0) {
         const double v = __ldg(s.rpal + ucls);
+#pragma unroll 1
         for (int t = 0; t < n; ++t) layers[t] = v;
       }
       e = sgf_find(T, n, axis, layers);
