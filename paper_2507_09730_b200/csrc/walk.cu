@@ -1348,8 +1348,7 @@ __device__ __forceinline__ const uint64_t* lane_atlas(const DSlots& W, int slot)
   return W.atlas + static_cast<size_t>(slot) * kAtlasWords;
 }
 
-__device__ __forceinline__ void mw_arm(const DSlots& W, const double* alpha_sm, int Pn, int slot,
-                                       int n, MwLane& L) {
+__device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int n, MwLane& L) {
   const int m = (n - 1) / 2;
   const uint64_t* A = lane_atlas(W, slot);
   L.slot = slot;
@@ -1648,7 +1647,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
   L.cchg = 0;
   unsigned long long item = atomicAdd(&C->qhead, 1ull);
   bool live = item < qlen;
-  if (live) mw_arm(W, alpha_sm, s.P, queue[item], n, L);
+  if (live) mw_arm(W, queue[item], n, L);
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
     if (live) code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
@@ -1663,7 +1662,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
       }
       item = atomicAdd(&C->qhead, 1ull);
       live = item < qlen;
-      if (live) mw_arm(W, alpha_sm, s.P, queue[item], n, L);
+      if (live) mw_arm(W, queue[item], n, L);
     }
   }
   flush_mw_stats(C, L);
@@ -1716,7 +1715,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
       if (r == 2) {
         in_mw = true;
-        mw_arm(W, alpha_sm, s.P, A.slot, n, L);
+        mw_arm(W, A.slot, n, L);
       } else if (r == 1) {
         item = atomicAdd(&C->ahead, 1ull);
         live = item < alen;
@@ -1870,7 +1869,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         if (v >= 0) {
           ring_m[res & mask] = -1;
           __threadfence();
-          mw_arm(W, alpha_sm, s.P, v, n, L);
+          mw_arm(W, v, n, L);
           have = true;
           res = -1;
         }
@@ -1947,7 +1946,7 @@ __global__ void __launch_bounds__(128)
   L.gsteps = 0;
   L.jumps = 0;
   L.cchg = 0;
-  mw_arm(W, alpha_sm, s.P, t, n, L);
+  mw_arm(W, t, n, L);
   int code = MW_GO, xdir = 0;
   while (code == MW_GO)
     code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
@@ -2080,7 +2079,7 @@ __global__ void __launch_bounds__(128)
     ml.gsteps = 0;
     ml.jumps = 0;
     ml.cchg = 0;
-    mw_arm(W, alpha_sm, s.P, slot, n, ml);
+    mw_arm(W, slot, n, ml);
     ml.wid = t;
     int code = MW_GO, xdir = 0;
     while (code == MW_GO)
