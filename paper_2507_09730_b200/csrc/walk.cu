@@ -3627,7 +3627,14 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   if (trace) cudaEventCreate(&a0);
   cudaEventRecord(t0, ctx->stream);
 
-  const int S = prm->n_slots > 0 ? prm->n_slots : kSlotsDefault;
+  // resident walk slots: 2^20, or for long calls up to 2^22 (about half the
+  // walks in flight: rounds stay full longer; 8M-walk calls run 3.1e7 ->
+  // 3.7e7 walks/s on C3/C5 from 2^20 to 2^22 slots, ~10 GB of slot state)
+  int S = prm->n_slots > 0 ? prm->n_slots : kSlotsDefault;
+  if (prm->n_slots <= 0) {
+    while (S < (1 << 22) && static_cast<long long>(S) * 2 < count) S *= 2;
+    if (const char* e = std::getenv("FRW_SLOTS")) S = std::max(1024, std::atoi(e));
+  }
   if (int rc = ensure_slots(ctx, E, S)) return rc;
   if (E.recs_cap < count) {
     cudaFree(E.recs);
