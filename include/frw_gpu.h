@@ -244,6 +244,24 @@ int frw_run_walks(frw_ctx *ctx, const frw_walk_params *p, int32_t master,
                   uint64_t walk_begin, int64_t count, frw_miss_fn miss,
                   void *user, frw_tally *out, frw_walk_record *records);
 
+/* ---- multi-GPU: the per-conductor tallies across ranks ---
+ * Walks shard as contiguous walk-index ranges of ONE seed (rank g of G runs
+ * [g*W/G, (g+1)*W/G), the reference's per-thread chunking, engine.cpp:437-458);
+ * geometry and SGF tables are replicated; the only exchange is one
+ * all-reduce (sum) of each rank's tally.  frw_run_walks leaves its tally on
+ * the device as one f64 vector (sum, sum of squares and landed per slot, the
+ * dispatch/abort counters); frw_tally_allreduce sums it over the ranks of
+ * `comm` (an ncclComm_t, or NULL for the context's own communicator from
+ * frw_nccl_init) with a single ncclAllReduce on the context stream and
+ * writes the combined tally into `out` (same fields as frw_run_walks; counts
+ * exact).  NCCL is loaded at first use (libnccl.so.2; a copy already loaded
+ * by the host process, e.g. torch's, is shared).  No reference counterpart:
+ * the reference is single-process. */
+int frw_nccl_unique_id(void *id128);  /* ncclGetUniqueId, 128 bytes (rank 0) */
+int frw_nccl_init(frw_ctx *ctx, const void *id128, int nranks, int rank);
+int frw_nccl_destroy(frw_ctx *ctx);
+int frw_tally_allreduce(frw_ctx *ctx, void *comm, frw_tally *out);
+
 /* One lattice transit per entry over a cube of the uploaded structure:
  * microwalk_transit_lazy (microwalk.cpp:199-204; with_conductors = 0) or the
  * expanded-cube transit of microwalk_e_transit (microwalk.cpp:206-228;
@@ -278,6 +296,28 @@ int frw_lattice_jump_law(int m, double *face, double *esteps);
 int frw_structure_transits_philox(frw_ctx *ctx, int n, int count, const double *cubes,
                                   int with_conductors, uint64_t seed, int jumps,
                                   int32_t step_cap, frw_exit *out);
+
+/* Structure queries on the device (geometry.hpp:101-121), for unit parity
+ * with the reference on random scenes.  Per point (points [count][3], nm):
+ * conductor_at -- Structure::conductor_at(p, tol) (geometry.cpp:57-62) as the
+ * conductor's declaration index, -1 for none; free_half_width --
+ * max_free_cube(p).half_width (:64-80), -1 where the reference throws
+ * (outside the world or inside a conductor); eps -- permittivity_at(p)
+ * (:47-55), NaN outside the world; hop_code / hop_half_width -- the walk
+ * engine's one-pass transition prologue (engine.cpp:293-298 with snap = tol):
+ * conductor index (Terminate), -1 (TerminateGround), -2 (error) or -3 with
+ * the free cube's half width.  Host buffers; synchronous. */
+int frw_geometry_queries(frw_ctx *ctx, int count, const double *points, double tol,
+                         int32_t *conductor_at, double *free_half_width, double *eps,
+                         int32_t *hop_code, double *hop_half_width);
+/* The stratification probe + profile key of transition cubes
+ * (stratified_profile, geometry.cpp:357-396; profile_key,
+ * sgf_cache.cpp:29-51): cubes [count][4] centre xyz, half width (the cube
+ * must lie in the world, as every transition cube does); axis[count] is the
+ * key axis (uniform profiles normalised to 0) or -1 for a general cube;
+ * layers [count][n] the 6-significant-digit layers (0 for general cubes). */
+int frw_stratified_keys(frw_ctx *ctx, int n, int count, const double *cubes, int32_t *axis,
+                        double *layers);
 
 /* Engine::first_transition / Engine::transition (engine.hpp:146-159;
  * engine.cpp:201-350), one per entry, continuing caller-owned SplitMix64

@@ -385,6 +385,10 @@ class Ref:
         L.ref_extract.argtypes = [C.c_void_p, _dp, _lp, C.c_int, _dp, _dp, _up, _up, _dp]
         L.ref_run_walks.argtypes = [C.c_void_p, _dp, _lp, C.c_uint64, C.c_int64, _ip, _dp, _bp]
         L.ref_extract_warm.argtypes = [C.c_void_p, _dp, _lp, C.c_int, _dp, _dp, _up, _up, _dp]
+        L.ref_extract_cache.argtypes = [C.c_void_p, _dp, _lp, C.c_int, C.c_char_p, C.c_char_p,
+                                        _dp, _dp, _up, _up, _dp]
+        L.ref_run_walks_cache.argtypes = [C.c_void_p, _dp, _lp, C.c_uint64, C.c_int64, C.c_int,
+                                          C.c_char_p, C.c_char_p, _ip, _dp, _bp]
         L.ref_cache_save.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_char_p]
         L.ref_cache_load_probs.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, _dp, _lp]
 
@@ -572,7 +576,10 @@ class _RefHandle:
             raise RuntimeError(self.ref.err())
         return out
 
-    def extract(self, threads=1, warm_cache=False, **kw):
+    def extract(self, threads=1, warm_cache=False, cache_in=None, cache_out=None, **kw):
+        """Engine::extract.  warm_cache: a process-wide cache shared by calls;
+        cache_in / cache_out: SGF1 files loaded before / saved after the
+        call (the CLI's --cache, cli.cpp:186-193)"""
         d, i = Ref.cfg_arrays(**kw)
         nc, nd = C.c_int(), C.c_int()
         self.lib.ref_structure_counts(self.h, C.byref(nc), C.byref(nd))
@@ -581,9 +588,17 @@ class _RefHandle:
         landed = np.zeros(k, np.uint64)
         st = np.zeros(14, np.uint64)
         tm = np.zeros(2)
-        fn = self.lib.ref_extract_warm if warm_cache else self.lib.ref_extract
-        if fn(self.h, _ptr(d, _dp), _ptr(i, _lp), threads, _ptr(val, _dp),
-              _ptr(se, _dp), _ptr(landed, _up), _ptr(st, _up), _ptr(tm, _dp)):
+        if cache_in is not None or cache_out is not None:
+            rc = self.lib.ref_extract_cache(
+                self.h, _ptr(d, _dp), _ptr(i, _lp), threads,
+                None if cache_in is None else cache_in.encode(),
+                None if cache_out is None else cache_out.encode(), _ptr(val, _dp),
+                _ptr(se, _dp), _ptr(landed, _up), _ptr(st, _up), _ptr(tm, _dp))
+        else:
+            fn = self.lib.ref_extract_warm if warm_cache else self.lib.ref_extract
+            rc = fn(self.h, _ptr(d, _dp), _ptr(i, _lp), threads, _ptr(val, _dp),
+                    _ptr(se, _dp), _ptr(landed, _up), _ptr(st, _up), _ptr(tm, _dp))
+        if rc:
             raise RuntimeError(self.ref.err())
         return dict(value=val, std_err=se, landed=landed, walks=int(st[0]),
                     converged=bool(st[1]), aborted=int(st[2]), resampled=int(st[3]),
@@ -591,12 +606,23 @@ class _RefHandle:
                     cache_hits=int(st[12]), cache_misses=int(st[13]),
                     t_mw_seconds=tm[0], t_total_seconds=tm[1])
 
-    def run_walks(self, w0, count, **kw):
+    def run_walks(self, w0, count, threads=1, cache_in=None, cache_out=None, **kw):
+        """per-walk (slot, weight, aborted) of the reference Engine; its
+        stratified-SGF cache starts from cache_in and is saved to cache_out
+        (SGF1 files, the reference's own solves)"""
         d, i = Ref.cfg_arrays(**kw)
         slot = np.empty(count, np.int32)
         w = np.empty(count)
         ab = np.empty(count, np.uint8)
-        if self.lib.ref_run_walks(self.h, _ptr(d, _dp), _ptr(i, _lp), w0, count,
-                                  _ptr(slot, _ip), _ptr(w, _dp), _ptr(ab, _bp)):
+        if threads == 1 and cache_in is None and cache_out is None:
+            rc = self.lib.ref_run_walks(self.h, _ptr(d, _dp), _ptr(i, _lp), w0, count,
+                                        _ptr(slot, _ip), _ptr(w, _dp), _ptr(ab, _bp))
+        else:
+            rc = self.lib.ref_run_walks_cache(
+                self.h, _ptr(d, _dp), _ptr(i, _lp), w0, count, threads,
+                None if cache_in is None else cache_in.encode(),
+                None if cache_out is None else cache_out.encode(),
+                _ptr(slot, _ip), _ptr(w, _dp), _ptr(ab, _bp))
+        if rc:
             raise RuntimeError(self.ref.err())
         return slot, w, ab

@@ -41,14 +41,23 @@ def build_gpu_lib(force=False):
     cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = cu + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) \
         + [os.path.join(ROOT, "include", "frw_gpu.h")]
-    if force or _stale(out, deps):
-        # -fmad=false: geometry/voxel-centre arithmetic must round like the
-        # reference (x86-64 baseline, no FMA contraction)
-        # FRW_NVCC_EXTRA: extra flags for A/B builds of kernel knobs (-D...)
-        extra = os.environ.get("FRW_NVCC_EXTRA", "").split()
-        _run([NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "-Xptxas", "-v",
-              "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), *extra,
-              "-o", out, *cu])
+    # -fmad=false: geometry/voxel-centre arithmetic must round like the
+    # reference (x86-64 baseline, no FMA contraction)
+    # FRW_NVCC_EXTRA: extra flags for A/B builds of kernel knobs (-D...)
+    extra = os.environ.get("FRW_NVCC_EXTRA", "").split()
+    cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "-Xptxas", "-v",
+           "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), *extra,
+           "-o", out, *cu, "-ldl"]
+    # the flags of the last build sit next to the library: a variant build
+    # (FRW_NVCC_EXTRA) is rebuilt by the next default build() even when no
+    # source changed
+    stamp = out + ".flags"
+    flags = " ".join(cmd)
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    if force or old != flags or _stale(out, deps):
+        _run(cmd)
+        with open(stamp, "w") as f:
+            f.write(flags)
     return out
 
 

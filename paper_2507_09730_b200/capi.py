@@ -142,6 +142,13 @@ def lib():
         L.frw_structure_transits_philox.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int,
                                                     C.c_uint64, C.c_int, C.c_int32,
                                                     C.POINTER(Exit)]
+        _v = C.c_void_p
+        L.frw_geometry_queries.argtypes = [_v, C.c_int, _v, C.c_double, _v, _v, _v, _v, _v]
+        L.frw_stratified_keys.argtypes = [_v, C.c_int, C.c_int, _v, _v, _v]
+        L.frw_nccl_unique_id.argtypes = [_v]
+        L.frw_nccl_init.argtypes = [_v, _v, C.c_int, C.c_int]
+        L.frw_nccl_destroy.argtypes = [_v]
+        L.frw_tally_allreduce.argtypes = [_v, _v, C.POINTER(Tally)]
         L.frw_run_walks.argtypes = [C.c_void_p, C.POINTER(WalkParams), C.c_int32, C.c_uint64,
                                     C.c_int64, MISS_FN, C.c_void_p, C.POINTER(Tally),
                                     C.c_void_p]
@@ -347,6 +354,26 @@ class Context:
                                                ("voxel", "<i4", 3), ("steps", "<i4"),
                                                ("point", "<f8", 3)]), count=count)
         return {k: a[k].copy() for k in a.dtype.names}
+
+    def geometry_queries(self, points, tol):
+        """frw_geometry_queries: Structure::conductor_at / max_free_cube /
+        permittivity_at and the engine's hop prologue, per point"""
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        k = len(pts)
+        out = dict(conductor_at=np.empty(k, np.int32), free_half_width=np.empty(k),
+                   eps=np.empty(k), hop_code=np.empty(k, np.int32), hop_half_width=np.empty(k))
+        self._check(self.L.frw_geometry_queries(
+            self.h, k, _p(pts), float(tol), _p(out["conductor_at"]), _p(out["free_half_width"]),
+            _p(out["eps"]), _p(out["hop_code"]), _p(out["hop_half_width"])))
+        return out
+
+    def stratified_keys(self, n, cubes):
+        """frw_stratified_keys: (key axis or -1, rounded layers) per cube"""
+        cb = np.ascontiguousarray(cubes, np.float64).reshape(-1, 4)
+        axis = np.empty(len(cb), np.int32)
+        layers = np.empty((len(cb), n))
+        self._check(self.L.frw_stratified_keys(self.h, n, len(cb), _p(cb), _p(axis), _p(layers)))
+        return axis, layers
 
     def sgf_put(self, n, axis, layers, pitch, probs, cdf, kernels=None):
         layers = np.ascontiguousarray(layers, np.float64)

@@ -72,6 +72,7 @@ int frw_ctx_create(int device, frw_ctx** out) {
 void frw_ctx_destroy(frw_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  frw_nccl_destroy(ctx);
   if (ctx->walk_free) ctx->walk_free(ctx);
   auto& g = ctx->grid;
   cudaFree(g.d_map);  // also releases d_rec (same allocation)

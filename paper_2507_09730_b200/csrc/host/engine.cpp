@@ -62,6 +62,8 @@ void Config::validate() const {
     throw std::invalid_argument("gaussian_gap_fraction must lie in (0,1)");
   if (grid_n > 64) throw std::invalid_argument("grid_n must be <= 64 on the device");
   if (device_batch < 0) throw std::invalid_argument("device_batch must be >= 0 (0 = auto)");
+  for (int d : devices)
+    if (d < 0) throw std::invalid_argument("devices: device indices must be >= 0");
 }
 
 // engine.cpp:84-124
@@ -132,10 +134,11 @@ void throw_status(frw_ctx* ctx, int rc) {
 
 namespace {
 std::mutex g_dev_mu;
-std::map<int, Device*>& devices() {
-  static auto* m = new std::map<int, Device*>;  // intentionally leaked: no
-  return *m;                                    // teardown after CUDA exits
+std::map<std::pair<int, int>, Device*>& devices() {
+  static auto* m = new std::map<std::pair<int, int>, Device*>;  // intentionally leaked:
+  return *m;                                                    // no teardown after CUDA exits
 }
+std::mutex g_tab_mu;  // guards the tables() map (lanes of a multi-device extract)
 struct DeviceTable {
   int n = 0;  // lattice size of the keys currently on the device
   std::unordered_set<ProfileKey, ProfileKeyHash> keys;  // keys already put
@@ -148,9 +151,13 @@ std::map<frw_ctx*, DeviceTable>& tables() {
   static auto* m = new std::map<frw_ctx*, DeviceTable>;
   return *m;
 }
+DeviceTable& table_of(frw_ctx* ctx) {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  return tables()[ctx];  // node-based map: the reference stays valid
+}
 
 void put_entry(frw_ctx* ctx, const ProfileKey& k, const DiscreteSGF& g) {
-  auto& keys = tables()[ctx].keys;
+  auto& keys = table_of(ctx).keys;
   if (keys.count(k)) return;  // on the device already (frw_sgf_put would skip it too)
   std::vector<double> kern;
   const bool has = !g.grad_kernels[0].empty();
@@ -173,11 +180,21 @@ Device::Device(int device) {
 
 Device::~Device() { frw_ctx_destroy(ctx_); }
 
-Device& Device::get(int device) {
+void clear_device_tables() {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto& [ctx, T] : tables()) {
+    throw_status(ctx, frw_sgf_clear(ctx));
+    T.keys.clear();
+    T.n = 0;
+  }
+}
+
+Device& Device::get(int device, int instance) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
   auto& m = devices();
-  auto it = m.find(device);
-  if (it == m.end()) it = m.emplace(device, new Device(device)).first;
+  const auto key = std::make_pair(device, instance);
+  auto it = m.find(key);
+  if (it == m.end()) it = m.emplace(key, new Device(device)).first;
   return *it->second;
 }
 
@@ -198,20 +215,24 @@ Engine::Engine(const Structure& s, const Config& cfg, StratifiedSgfCache* cache)
   snap_ = cfg_.snap_tol * std::max({he.x, he.y, he.z});  // engine.cpp:186-187
   for (size_t i = 0; i < s_.conductors.size(); ++i)
     if (s_.conductors[i].id == s_.master_id) master_slot_ = static_cast<int>(i);
-  ctx_ = Device::get(cfg_.device).ctx();
+  const std::vector<int> devs = cfg_.devices.empty() ? std::vector<int>{cfg_.device}
+                                                     : cfg_.devices;
+  std::map<int, int> seen;
+  for (int d : devs) ctxs_.push_back(Device::get(d, seen[d]++).ctx());
+  ctx_ = ctxs_[0];
 }
 
-void Engine::upload() const {
-  upload_structure(ctx_, s_);
+void Engine::upload(frw_ctx* ctx) const {
+  upload_structure(ctx, s_);
   // device table: one lattice size; carry over every cached key of this size
-  DeviceTable& T = tables()[ctx_];
+  DeviceTable& T = table_of(ctx);
   if (T.n != cfg_.grid_n) {
-    throw_status(ctx_, frw_sgf_clear(ctx_));
+    throw_status(ctx, frw_sgf_clear(ctx));
     T.keys.clear();
     T.n = cfg_.grid_n;
   }
   for (const auto& [k, g] : cache_->entries())
-    if (k.n == cfg_.grid_n) put_entry(ctx_, k, *g);
+    if (k.n == cfg_.grid_n) put_entry(ctx, k, *g);
 }
 
 frw_walk_params Engine::params() const {
@@ -311,9 +332,40 @@ std::vector<frw_walk_record> Engine::run_walks(uint64_t begin, int64_t count) {
   return rec;
 }
 
+WalkTally Engine::run_tally(uint64_t begin, int64_t count, bool allreduce) {
+  upload();
+  const size_t k = s_.conductors.size() + 1;
+  WalkTally w;
+  w.sum.assign(k, 0.0);
+  w.sumsq.assign(k, 0.0);
+  w.landed.assign(k, 0);
+  frw_tally t{};
+  t.sum = w.sum.data();
+  t.sumsq = w.sumsq.data();
+  t.landed = w.landed.data();
+  MissCtx mc{ctx_, cache_, {}};
+  const frw_walk_params p = params();
+  const int rc = frw_run_walks(ctx_, &p, master_slot_, begin, count, miss_cb, &mc, &t, nullptr);
+  if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
+  throw_status(ctx_, rc);
+  w.walks = static_cast<uint64_t>(count);
+  w.mw_ms = t.mw_ms;
+  w.total_ms = t.total_ms;
+  w.mw_jumps = t.mw_jumps;
+  if (allreduce) throw_status(ctx_, frw_tally_allreduce(ctx_, nullptr, &t));
+  w.aborted = t.aborted;
+  w.resampled = t.resampled;
+  w.mw_steps = t.mw_steps;
+  for (int b = 0; b < 4; ++b) {
+    w.first[b] = t.first[b];
+    w.sub[b] = t.sub[b];
+  }
+  return w;
+}
+
 CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   const auto t_start = Clock::now();
-  upload();
+  for (frw_ctx* c : ctxs_) upload(c);
   const size_t nslots = s_.conductors.size() + 1;
   const int master = master_slot_;
   std::vector<double> sum(nslots, 0.0), sumsq(nslots, 0.0);
@@ -360,11 +412,24 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   };
 
   const frw_walk_params p = params();
-  MissCtx mc{ctx_, cache_, {}};
-  // per-walk records land in page-locked memory kept with the context
-  DeviceTable& DT = tables()[ctx_];
-  std::vector<double> ts(nslots), tq(nslots);
-  std::vector<uint64_t> tl(nslots);
+  // one lane per context: its miss context, tallies, and per-walk records in
+  // page-locked memory kept with the context (two buffers: the host folds
+  // one wave while the device fills the next)
+  struct Lane {
+    frw_ctx* ctx;
+    DeviceTable* dt;
+    MissCtx mc;
+    std::vector<double> ts, tq;
+    std::vector<uint64_t> tl;
+    frw_tally t{};
+    int rc = FRW_OK;
+    int64_t begin = 0, count = 0;
+  };
+  std::vector<Lane> lanes;
+  for (frw_ctx* c : ctxs_)
+    lanes.push_back(Lane{c, &table_of(c), MissCtx{c, cache_, {}},
+                         std::vector<double>(nslots), std::vector<double>(nslots),
+                         std::vector<uint64_t>(nslots)});
   const long batch = cfg_.batch;
   const long db = cfg_.device_batch > 0 ? cfg_.device_batch
                   : cfg_.min_walks >= cfg_.max_walks ? (1L << 24) : (1L << 22);
@@ -405,47 +470,75 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
     }
   };
   // Device chunks of dev_batch walks (each drains its slot pool through the
-  // run-to-completion tail once, so large chunks amortise it).  While the
-  // device runs chunk k+1 a host thread folds chunk k; a chunk launched
-  // after the stopping rule fired inside an earlier one is discarded, so the
-  // result equals the sequential fold.
+  // run-to-completion tail once, so large chunks amortise it), G at a time
+  // (one per lane / device, in walk order).  While the devices run wave k+1 a
+  // host thread folds wave k in walk order; chunks launched after the
+  // stopping rule fired inside an earlier one are discarded, so the result
+  // equals the sequential fold for any number of devices.
   const int64_t max_walks = cfg_.max_walks;
   int64_t launched = 0;
   int cur = 0;
   std::thread worker;
+  auto run_lane = [&](Lane& L, int buf) {
+    L.t = frw_tally{};
+    L.rc = FRW_OK;
+    if (L.count <= 0) return;
+    DeviceTable& DT = *L.dt;
+    if (DT.rec_cap[buf] < static_cast<size_t>(L.count)) {
+      if (DT.rec[buf]) frw_host_free(L.ctx, DT.rec[buf]);
+      DT.rec[buf] = nullptr;
+      DT.rec_cap[buf] = 0;
+      void* mem = nullptr;
+      L.rc = frw_host_alloc(L.ctx, sizeof(frw_walk_record) * L.count, &mem);
+      if (L.rc != FRW_OK) return;
+      DT.rec[buf] = static_cast<frw_walk_record*>(mem);
+      DT.rec_cap[buf] = L.count;
+    }
+    L.t.sum = L.ts.data();
+    L.t.sumsq = L.tq.data();
+    L.t.landed = L.tl.data();
+    L.rc = frw_run_walks(L.ctx, &p, master, L.begin, L.count, miss_cb, &L.mc, &L.t, DT.rec[buf]);
+  };
   for (;;) {
-    const int64_t chunk = launched < max_walks ? std::min<int64_t>(dev_batch, max_walks - launched)
-                                               : 0;
-    int rc = FRW_OK;
-    frw_tally t{};
-    if (chunk > 0) {
-      if (DT.rec_cap[cur] < static_cast<size_t>(chunk)) {
-        if (DT.rec[cur]) frw_host_free(ctx_, DT.rec[cur]);
-        DT.rec[cur] = nullptr;
-        DT.rec_cap[cur] = 0;
-        void* mem = nullptr;
-        rc = frw_host_alloc(ctx_, sizeof(frw_walk_record) * chunk, &mem);
-        if (rc == FRW_OK) {
-          DT.rec[cur] = static_cast<frw_walk_record*>(mem);
-          DT.rec_cap[cur] = chunk;
-        }
-      }
-      if (rc == FRW_OK) {
-        t.sum = ts.data();
-        t.sumsq = tq.data();
-        t.landed = tl.data();
-        rc = frw_run_walks(ctx_, &p, master, launched, chunk, miss_cb, &mc, &t, DT.rec[cur]);
-      }
+    int64_t wave = 0;
+    for (Lane& L : lanes) {
+      L.begin = launched;
+      L.count = launched < max_walks ? std::min<int64_t>(dev_batch, max_walks - launched) : 0;
+      launched += L.count;
+      wave += L.count;
+    }
+    {
+      std::vector<std::thread> th;
+      for (size_t g = 1; g < lanes.size(); ++g)
+        if (lanes[g].count > 0) th.emplace_back(run_lane, std::ref(lanes[g]), cur);
+      run_lane(lanes[0], cur);
+      for (auto& x : th) x.join();
     }
     if (worker.joinable()) worker.join();
-    if (rc != FRW_OK && !mc.err.empty()) throw SolveError(mc.err, 0.0);
-    throw_status(ctx_, rc);
-    mw_ms += t.mw_ms;
-    dev_ms += t.total_ms;
-    res.mw_jumps += t.mw_jumps;
-    if (converged || chunk == 0) break;
-    launched += chunk;
-    worker = std::thread(fold, DT.rec[cur], chunk);
+    // the stopping rule fired inside the wave just folded: this wave was
+    // speculative; its results, statistics and errors are discarded
+    if (converged || wave == 0) break;
+    for (Lane& L : lanes) {
+      if (L.rc != FRW_OK && !L.mc.err.empty()) throw SolveError(L.mc.err, 0.0);
+      throw_status(L.ctx, L.rc);
+      mw_ms += L.t.mw_ms;
+      res.mw_jumps += L.t.mw_jumps;
+    }
+    {
+      // device time of the wave: its slowest lane
+      double wave_ms = 0;
+      for (const Lane& L : lanes) wave_ms = std::max(wave_ms, L.t.total_ms);
+      dev_ms += wave_ms;
+    }
+    std::vector<std::pair<const frw_walk_record*, int64_t>> parts;
+    for (const Lane& L : lanes)
+      if (L.count > 0) parts.emplace_back(L.dt->rec[cur], L.count);
+    worker = std::thread([&fold, &converged, parts] {
+      for (const auto& [rec, n] : parts) {
+        fold(rec, n);
+        if (converged) break;
+      }
+    });
     cur ^= 1;
   }
   res.master_id = s_.master_id;

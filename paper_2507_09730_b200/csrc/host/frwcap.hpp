@@ -308,6 +308,12 @@ struct Config {
   // 2^22 while a stopping rule is tested (a speculative chunk is discarded)
   long device_batch = 0;
   int device = 0;
+  // Several devices (one host thread and one context each): device chunks
+  // of one walk sequence go round-robin to them and are folded in walk
+  // order, so the result equals the one-device run bit for bit
+  // (SURVEY.md §8(e)).  Empty: {device}.  A device listed twice gets two
+  // contexts (independent streams on one GPU).
+  std::vector<int> devices;
 
   void validate() const;
 };
@@ -375,10 +381,23 @@ struct CapacitanceResult {
   const TerminalEstimate& self() const;
 };
 
+// Tallies of one walk range (frw_tally): per slot (conductors in
+// declaration order, ground last) sum, sum of squares and landed count, plus
+// the dispatch counters -- the unit the multi-process path all-reduces.
+struct WalkTally {
+  std::vector<double> sum, sumsq;
+  std::vector<uint64_t> landed;
+  uint64_t walks = 0, aborted = 0, resampled = 0, mw_steps = 0, mw_jumps = 0;
+  uint64_t first[4] = {0, 0, 0, 0};  // DispatchStats order
+  uint64_t sub[4] = {0, 0, 0, 0};    // cached, microwalk, microwalk_e, fdm
+  double mw_ms = 0, total_ms = 0;
+};
+
 // Shared device context (one per device and process).
 class Device {
  public:
-  static Device& get(int device);
+  // `instance` > 0 opens further contexts on the same device
+  static Device& get(int device, int instance = 0);
   frw_ctx* ctx() const { return ctx_; }
   ~Device();
 
@@ -388,6 +407,9 @@ class Device {
 };
 
 void throw_status(frw_ctx* ctx, int rc);
+// drops every stratified-SGF entry the engines put on the devices (they are
+// re-put from the host cache on the next call)
+void clear_device_tables();
 
 class Engine {
  public:
@@ -398,6 +420,12 @@ class Engine {
   CapacitanceResult extract(int threads = 0);
   // per-walk outcomes of walks [begin, begin+count) (parity tests)
   std::vector<frw_walk_record> run_walks(uint64_t begin, int64_t count);
+  // device tallies of walks [begin, begin+count) of the seed's one walk
+  // sequence (a rank's share); with `allreduce` they are
+  // summed over the ranks of the context's NCCL communicator
+  // (frw_nccl_init) by frw_tally_allreduce before they are returned
+  WalkTally run_tally(uint64_t begin, int64_t count, bool allreduce = false);
+  frw_ctx* context() const { return ctx_; }
 
   // One weighted first transition / one subsequent transition on the device,
   // continuing the caller's SplitMix64 (engine.hpp:146-159).  Table misses
@@ -414,7 +442,8 @@ class Engine {
                                      std::vector<SplitMix64>& rngs, DispatchStats& stats) const;
 
  private:
-  void upload() const;
+  void upload() const { upload(ctx_); }
+  void upload(frw_ctx* ctx) const;
   frw_walk_params params() const;
   const Structure& s_;
   Config cfg_;
@@ -423,7 +452,8 @@ class Engine {
   GaussianSurface surface_;
   double snap_ = 0;
   int master_slot_ = 0;
-  frw_ctx* ctx_ = nullptr;
+  frw_ctx* ctx_ = nullptr;         // first context (single-transition API)
+  std::vector<frw_ctx*> ctxs_;     // one per Config::devices entry
 };
 
 CapacitanceResult extract(const Structure& s, const Config& cfg, int threads = 0,

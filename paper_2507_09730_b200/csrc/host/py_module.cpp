@@ -17,7 +17,7 @@ using namespace frwcap;
 
 namespace {
 
-// py_module.cpp:20-57 (+ B200 knobs rng, all_couplings, device_batch, device)
+// py_module.cpp:20-57 (+ B200 knobs rng, all_couplings, device_batch, device, devices)
 Config config_from_kwargs(const py::kwargs& kw, int& threads) {
   Config cfg;
   threads = 0;
@@ -45,6 +45,7 @@ Config config_from_kwargs(const py::kwargs& kw, int& threads) {
     } else if (key == "all_couplings") cfg.all_couplings_rule = py::cast<bool>(v);
     else if (key == "device_batch") cfg.device_batch = py::cast<long>(v);
     else if (key == "device") cfg.device = py::cast<int>(v);
+    else if (key == "devices") cfg.devices = py::cast<std::vector<int>>(v);
     else throw py::value_error("unknown option: " + key);
   }
   cfg.validate();
@@ -285,6 +286,58 @@ PYBIND11_MODULE(_core, m) {
       py::arg("structure_json"), py::arg("begin"), py::arg("count"),
       "Per-walk outcomes of walks [begin, begin+count) (parity tests).");
 
+
+  // ---- multi-GPU (paper_2507_09730_b200/dist.py) ----------
+  m.def(
+      "run_walks_tally",
+      [](const std::string& text, uint64_t begin, int64_t count, bool allreduce,
+         const py::kwargs& kw) {
+        int threads = 0;
+        const Config cfg = config_from_kwargs(kw, threads);
+        const Structure s = parse_structure(text, cfg.world_margin);
+        WalkTally t;
+        {
+          py::gil_scoped_release release;
+          Engine e(s, cfg, &shared_cache());
+          t = e.run_tally(begin, count, allreduce);
+        }
+        py::dict d;
+        d["sum"] = py::array_t<double>(t.sum.size(), t.sum.data());
+        d["sumsq"] = py::array_t<double>(t.sumsq.size(), t.sumsq.data());
+        d["landed"] = py::array_t<uint64_t>(t.landed.size(), t.landed.data());
+        d["walks"] = t.walks;
+        d["aborted"] = t.aborted;
+        d["resampled"] = t.resampled;
+        d["first"] = std::vector<uint64_t>(t.first, t.first + 4);
+        d["sub"] = std::vector<uint64_t>(t.sub, t.sub + 4);
+        d["mw_steps"] = t.mw_steps;
+        d["mw_jumps"] = t.mw_jumps;
+        d["t_mw_seconds"] = t.mw_ms * 1e-3;
+        d["t_device_seconds"] = t.total_ms * 1e-3;
+        py::list ids;
+        for (const auto& c : s.conductors) ids.append(c.id);
+        d["conductor_ids"] = ids;
+        d["master_id"] = s.master_id;
+        return d;
+      },
+      py::arg("structure_json"), py::arg("begin"), py::arg("count"), py::arg("allreduce") = false,
+      "Device tallies of walks [begin, begin+count); allreduce=True sums them over the ranks "
+      "of the NCCL communicator set up by nccl_init (frw_tally_allreduce).");
+  m.def("nccl_unique_id", []() {
+    char id[128];
+    if (frw_nccl_unique_id(id) != FRW_OK) throw std::runtime_error("ncclGetUniqueId failed");
+    return py::bytes(id, sizeof id);
+  });
+  m.def(
+      "nccl_init",
+      [](int device, const py::bytes& uid, int nranks, int rank) {
+        const std::string u = uid;
+        if (u.size() != 128) throw py::value_error("nccl_init: the unique id has 128 bytes");
+        frw_ctx* ctx = Device::get(device).ctx();
+        py::gil_scoped_release release;
+        throw_status(ctx, frw_nccl_init(ctx, u.data(), nranks, rank));
+      },
+      py::arg("device"), py::arg("unique_id"), py::arg("nranks"), py::arg("rank"));
 
   m.def(
       "walks_by_transitions",
@@ -594,7 +647,10 @@ PYBIND11_MODULE(_core, m) {
 
   m.def("sgf_cache_save", [](const std::string& path) { shared_cache().save(path); });
   m.def("sgf_cache_load", [](const std::string& path) { return shared_cache().load(path); });
-  m.def("sgf_cache_clear", []() { shared_cache().clear(); });
+  m.def("sgf_cache_clear", []() {
+    shared_cache().clear();
+    clear_device_tables();  // the device tables mirror the cache: a cleared cache solves anew
+  });
   m.def("sgf_cache_stats", []() {
     const auto st = shared_cache().stats();
     py::dict d;

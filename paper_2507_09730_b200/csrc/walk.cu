@@ -27,6 +27,8 @@
 // All geometry and voxel-centre arithmetic is compiled with -fmad=false so
 // it rounds exactly like the reference (x86-64 baseline, no contraction).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <array>
@@ -35,6 +37,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <unordered_map>
 #include <vector>
 
@@ -46,7 +49,8 @@ namespace {
 
 constexpr int KMAX = 64;    // clipped boxes (conductors + dielectrics) per MicroWalk cube
 constexpr int NMAX = 64;    // lattice size cap (layers per key)
-constexpr int PMAX = 64;    // permittivity palette cap
+constexpr int PMAX = 64;    // palettes up to PMAX classes keep the alpha table in shared memory
+constexpr int kClassMax = 0x7FFF;  // distinct permittivities (15-bit class ids)
 constexpr int kSlotsDefault = 1 << 20;
 constexpr int kGridMinConductors = 24;  // conductor bins above this count
 // Cell atlas of a MicroWalk job (u64 words per slot).  Along each axis the
@@ -57,8 +61,8 @@ constexpr int kGridMinConductors = 24;  // conductor bins above this count
 // every bitmap in one word.
 constexpr int kAtMask = 0;    // [3][64] segment masks
 constexpr int kAtBm = 192;    // [3] segment-start bitmaps
-constexpr int kAtCls = 195;   // [KMAX] class byte of each clipped box
-constexpr int kAtlasWords = 208;
+constexpr int kAtCls = 195;   // [KMAX] u16 palette class of each clipped dielectric box
+constexpr int kAtlasWords = 211;
 constexpr double kEps0 = 8.8541878128e-12;  // constants.hpp:5
 constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
@@ -93,9 +97,9 @@ struct DStruct {
   int nc, nd, P, bg;
   const double* cbox;   // [nc][6]
   const double* dbox;   // [nd][6]
-  const uint8_t* dcls;  // [nd] palette class
+  const uint16_t* dcls; // [nd] palette class
   const double* pal;    // [P]
-  const double* alpha;  // [P][P]: alpha[nb*P + self] = e_nb/(e_nb+e_self)
+  const double* alpha;  // [P][P] when P <= PMAX: alpha[nb*P + self] = e_nb/(e_nb+e_self)
   const double* rpal;   // [P] value rounded to 6 significant digits
   double world[6];
   DGrid g;
@@ -109,7 +113,7 @@ struct DSgf {
   const double* keys;        // [entries][NMAX]
   const double* pitch;       // [entries]
   const double* const* data; // [entries] -> cdf[P], probs[P], kern[3][P]
-  const int* uentry;         // [PMAX] entry of the uniform key of each palette class, -1
+  const int* uentry;         // [P] entry of the uniform key of each palette class, -1
 };
 
 // Lattice jumps (Philox mode only).  Inside one cell every alpha is 1/2, so
@@ -701,7 +705,7 @@ __device__ void clip_axis(double c, double h, int n, double lo, double hi, int* 
 
 __device__ __forceinline__ int box_lo(uint64_t b, int a) { return static_cast<int>((b >> (8 * a)) & 0xFF); }
 __device__ __forceinline__ int box_hi(uint64_t b, int a) { return static_cast<int>((b >> (24 + 8 * a)) & 0xFF); }
-__device__ __forceinline__ int box_cls(uint64_t b) { return static_cast<int>((b >> 48) & 0xFF); }
+__device__ __forceinline__ int box_cls(uint64_t b) { return static_cast<int>((b >> 48) & 0x7FFF); }
 // conductor boxes (MicroWalk-E cubes) carry bit 63 and their declaration
 // index in bits 48..62; a voxel inside any conductor box is conductor
 // (first declared wins, geometry.cpp:57-62 with tol 0), class code kCond
@@ -753,13 +757,20 @@ __device__ __forceinline__ int coord(uint32_t node, int a) { return (node >> (8 
 // ---- cell atlas lookups ---------------------------------------------------
 __device__ __forceinline__ uint64_t upto(int v) { return (2ull << v) - 1; }  // bits 0..v
 
-// class of the voxels contained in exactly the clipped boxes of M: any
-// conductor box (bits [0, ncond)) makes it conductor, else the last
-// declared dielectric box wins (geometry.cpp:42-55), else background
-__device__ __forceinline__ int class_of(const uint8_t* cls, uint64_t M, uint64_t cmask, int bg) {
+// Job-local class of the voxels contained in exactly the clipped boxes of M:
+// any conductor box (bits [0, ncond)) makes it conductor, else the last
+// declared dielectric box wins (geometry.cpp:42-55) -- local class b + 1 for
+// mask bit b, its palette class in the atlas (kAtCls) -- else background,
+// local class 0.  Local classes (<= KMAX) keep a cell's seven classes in one
+// word whatever the structure's palette size.
+__device__ __forceinline__ int class_of(uint64_t M, uint64_t cmask) {
   if (M & cmask) return kCond;
   const uint64_t d = M & ~cmask;
-  return d ? cls[63 - __clzll(d)] : bg;
+  return d ? 64 - __clzll(d) : 0;
+}
+// palette class of a job-local class
+__device__ __forceinline__ int global_class(const uint64_t* A, int lc, int bg) {
+  return lc ? reinterpret_cast<const uint16_t*>(A + kAtCls)[lc - 1] : bg;
 }
 
 __device__ __forceinline__ uint64_t cond_mask(int ncond) {
@@ -779,9 +790,8 @@ __device__ __forceinline__ uint64_t voxel_mask(const uint64_t* A, const uint64_t
 // face distances (room, one byte per direction 2a+side) and the classes of
 // the six face-neighbour cells (kFace on a lattice face) with its own class
 // in byte 6.  O(1): three bit scans per axis and nine mask loads.
-__device__ uint64_t cell_info(const uint64_t* A, const uint64_t bm[3], int ncond, int bg, int n,
+__device__ uint64_t cell_info(const uint64_t* A, const uint64_t bm[3], int ncond, int n,
                               uint32_t node, uint64_t* room_out) {
-  const uint8_t* cls = reinterpret_cast<const uint8_t*>(A + kAtCls);
   const uint64_t cmask = cond_mask(ncond);
   uint64_t M[3], Ml[3], Mh[3];
   bool hl[3], hh[3];
@@ -802,12 +812,12 @@ __device__ uint64_t cell_info(const uint64_t* A, const uint64_t bm[3], int ncond
     Ml[a] = hl[a] ? mk[sg - 1] : 0;
     Mh[a] = hh[a] ? mk[sg + 1] : 0;
   }
-  uint64_t fc = static_cast<uint64_t>(class_of(cls, M[0] & M[1] & M[2], cmask, bg)) << 48;
+  uint64_t fc = static_cast<uint64_t>(class_of(M[0] & M[1] & M[2], cmask)) << 48;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const uint64_t rest = M[(a + 1) % 3] & M[(a + 2) % 3];
-    const uint64_t cl = hl[a] ? class_of(cls, Ml[a] & rest, cmask, bg) : kFace;
-    const uint64_t ch = hh[a] ? class_of(cls, Mh[a] & rest, cmask, bg) : kFace;
+    const uint64_t cl = hl[a] ? class_of(Ml[a] & rest, cmask) : kFace;
+    const uint64_t ch = hh[a] ? class_of(Mh[a] & rest, cmask) : kFace;
     fc |= cl << (16 * a) | ch << (16 * a + 8);
   }
   *room_out = room;
@@ -858,7 +868,7 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
   int K = 0, ncond = 0;
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
   int cand[kCandMax];
-  uint8_t* cls = reinterpret_cast<uint8_t*>(A + kAtCls);
+  uint16_t* cls = reinterpret_cast<uint16_t*>(A + kAtCls);
   // phase 0: conductor boxes (MicroWalk-E only), phase 1: dielectric boxes,
   // each in declaration order.  One rolled loop (one inlined copy of the
   // candidate query and the clip): the walk kernels are instruction-fetch
@@ -899,7 +909,7 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
         boxes[K++] = pk | (0x8000ull | static_cast<uint64_t>(q)) << 48;
       } else {
         const int dc = __ldg(s.dcls + q);
-        cls[K] = static_cast<uint8_t>(dc);
+        cls[K] = static_cast<uint16_t>(dc);
         boxes[K++] = pk | static_cast<uint64_t>(dc) << 48;
       }
     }
@@ -1333,14 +1343,34 @@ struct MwLane {
   uint32_t jumps;
 };
 
+// Tables of the MicroWalk kernels: the palette-pair alphas (Pn <= PMAX: in
+// shared memory, alpha 1 for absorbing faces at index Pn*Pn) or, for larger
+// palettes, the palette itself (alphas divided out, the same IEEE division
+// the table holds: e_nb / (e_nb + e_self), microwalk.cpp:97-104).
+struct AlphaTab {
+  const double* tab;  // smem pair table, or null
+  const double* pal;  // palette (global)
+  int Pn, bg;
+};
+
 // the per-face alphas of the lane's cell: palette pair (face class, own
 // class), 1 for lattice and conductor faces (both absorb the step)
-__device__ __forceinline__ void lane_alphas(const double* alpha_sm, int Pn, MwLane& L) {
-  const int c0 = static_cast<int>((L.fc >> 48) & 0xFF);
+__device__ __forceinline__ void lane_alphas(const AlphaTab& T, const uint64_t* A, MwLane& L) {
+  const int g0 = global_class(A, static_cast<int>((L.fc >> 48) & 0xFF), T.bg);
+  if (T.tab) {
 #pragma unroll
-  for (int d = 0; d < 6; ++d) {
-    const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-    L.al[d] = alpha_sm[cn >= kCond ? PMAX * PMAX : cn * Pn + c0];
+    for (int d = 0; d < 6; ++d) {
+      const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
+      L.al[d] = T.tab[cn >= kCond ? T.Pn * T.Pn : global_class(A, cn, T.bg) * T.Pn + g0];
+    }
+  } else {
+    const double e0 = __ldg(T.pal + g0);
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+      const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
+      const double en = cn >= kCond ? 0.0 : __ldg(T.pal + global_class(A, cn, T.bg));
+      L.al[d] = cn >= kCond ? 1.0 : en / (en + e0);
+    }
   }
 }
 
@@ -1364,10 +1394,11 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int n, MwLane&
 }
 
 // a move left the current cell: look the new cell up in the atlas
-__device__ __forceinline__ void mw_cell_change(const DSlots& W, const double* alpha_sm, int Pn,
-                                               int bg, int n, MwLane& L) {
-  L.fc = cell_info(lane_atlas(W, L.slot), L.bm, L.ncond, bg, n, L.node, &L.room);
-  lane_alphas(alpha_sm, Pn, L);
+__device__ __forceinline__ void mw_cell_change(const DSlots& W, const AlphaTab& T, int n,
+                                               MwLane& L) {
+  const uint64_t* A = lane_atlas(W, L.slot);
+  L.fc = cell_info(A, L.bm, L.ncond, n, L.node, &L.room);
+  lane_alphas(T, A, L);
 }
 
 // surface exit: continuation point, counters, slot back to ACTIVE
@@ -1465,10 +1496,13 @@ __device__ __forceinline__ int mw_step(const DParams& P, const DirDelta* dd, MwL
 }
 
 // alpha_sm: the palette-pair alphas, then alpha 1 (absorbing faces) at
-// index PMAX*PMAX so a face alpha is one unconditional shared load
-__device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* dd) {
-  for (int i = threadIdx.x; i < s.P * s.P; i += blockDim.x) alpha_sm[i] = __ldg(s.alpha + i);
-  if (threadIdx.x == 0) alpha_sm[PMAX * PMAX] = 1.0;
+// index P*P so a face alpha is one unconditional shared load (P <= PMAX)
+__device__ AlphaTab setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* dd) {
+  const bool small = s.P <= PMAX;
+  if (small) {
+    for (int i = threadIdx.x; i < s.P * s.P; i += blockDim.x) alpha_sm[i] = __ldg(s.alpha + i);
+    if (threadIdx.x == 0) alpha_sm[s.P * s.P] = 1.0;
+  }
   if (threadIdx.x < 6) {
     const int d = threadIdx.x, a = d >> 1;
     DirDelta x;
@@ -1480,6 +1514,7 @@ __device__ void setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* 
     dd[d] = x;
   }
   __syncthreads();
+  return AlphaTab{small ? alpha_sm : nullptr, s.pal, s.P, s.bg};
 }
 
 #ifndef FRW_STEP_UNROLL
@@ -1543,8 +1578,7 @@ __device__ __forceinline__ bool mw_jump(const DJump& J, MwLane& L, uint32_t w0, 
 // SplitMix64 draws in parity mode); a move into another cell ends the
 // super-step and refreshes the cell from the atlas.  Returns an MW_* event.
 template <int RNG>
-__device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
-                                            const double* alpha_sm, int Pn, int bg,
+__device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W, const AlphaTab& AT,
                                             const DirDelta* dd, int n, int cap, MwLane& L,
                                             int* xdir) {
   uint32_t w4[4] = {0, 0, 0, 0};
@@ -1561,7 +1595,7 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W,
   }
   // a pending cell (new hop, or a move into another cell last super-step):
   // one inlined copy of the atlas lookup serves both
-  if ((L.room >> 48) == 0) mw_cell_change(W, alpha_sm, Pn, bg, n, L);
+  if ((L.room >> 48) == 0) mw_cell_change(W, AT, n, L);
   int code = 0;
   int u0 = 0;  // words taken by jumps (two per jump)
   if (RNG == FRW_RNG_PHILOX && P.jump.mmax >= 2 && L.steps < cap &&
@@ -1635,9 +1669,9 @@ template <int RNG>
 __global__ void __launch_bounds__(512, FRW_KMW_MINB)
     k_mw(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* queue,
          int* aq_out) {
-  __shared__ double alpha_sm[PMAX * PMAX + 1];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  setup_smem_tables(s, alpha_sm, dd);
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
   const int cap = 1000 * n * n;  // microwalk.cpp:81
   const unsigned long long qlen = C->qlen;
@@ -1650,7 +1684,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
   if (live) mw_arm(W, queue[item], n, L);
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
-    if (live) code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
+    if (live) code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
     if (live && code != MW_GO) {
       if (code == MW_SURFACE) {
         mw_exit(W, n, L, xdir);
@@ -1690,9 +1724,9 @@ template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
            const int* aq) {
-  __shared__ double alpha_sm[PMAX * PMAX + 1];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  setup_smem_tables(s, alpha_sm, dd);
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
   const int cap = 1000 * n * n;
   const unsigned long long alen = C->alen;
@@ -1738,7 +1772,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
 #endif
       if (!(live && in_mw)) continue;
       int xdir = 0;
-      const int code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
+      const int code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
       if (code == MW_GO) continue;
       in_mw = false;
       if (code == MW_SURFACE) {
@@ -1803,9 +1837,9 @@ template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_flow(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
            const int* aq, int* ring_a, int* ring_m, unsigned mask) {
-  __shared__ double alpha_sm[PMAX * PMAX + 1];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  setup_smem_tables(s, alpha_sm, dd);
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
   const unsigned long long alen = C->alen;
   if ((threadIdx.x >> 5) < kFlowAdvWarps) {
@@ -1881,7 +1915,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       }
       if (have) {
         int xdir = 0;
-        const int code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
+        const int code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
         if (code != MW_GO) {
           have = false;
           if (code == MW_SURFACE) {
@@ -1921,9 +1955,9 @@ template <int RNG>
 __global__ void __launch_bounds__(128)
     k_transits(DStruct s, DParams P, DSlots W, DCounters* C, const double* cubes,
                const uint64_t* states, int count, int with_cond, int cap, DevExit* out) {
-  __shared__ double alpha_sm[PMAX * PMAX + 1];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  setup_smem_tables(s, alpha_sm, dd);
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
   const int n = P.n;
@@ -1949,7 +1983,7 @@ __global__ void __launch_bounds__(128)
   mw_arm(W, t, n, L);
   int code = MW_GO, xdir = 0;
   while (code == MW_GO)
-    code = mw_superstep<RNG>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, L, &xdir);
+    code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
   const int a = xdir >> 1;
   e.kind = code == MW_SURFACE ? 0 : 1;
   e.dir = xdir;
@@ -2028,9 +2062,9 @@ __global__ void __launch_bounds__(128)
     k_transition_single(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C,
                         DMiss M, const double* pts, uint64_t* states, const int* idx, int count,
                         int* rc_out, DevEvent* out) {
-  __shared__ double alpha_sm[PMAX * PMAX + 1];
+  __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  setup_smem_tables(s, alpha_sm, dd);
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= count) return;
   const int t = idx[q];
@@ -2083,8 +2117,7 @@ __global__ void __launch_bounds__(128)
     ml.wid = t;
     int code = MW_GO, xdir = 0;
     while (code == MW_GO)
-      code = mw_superstep<FRW_RNG_SPLITMIX_PARITY>(P, W, alpha_sm, s.P, s.bg, dd, n, cap, ml,
-                                                   &xdir);
+      code = mw_superstep<FRW_RNG_SPLITMIX_PARITY>(P, W, AT, dd, n, cap, ml, &xdir);
     e.dispatch = W.mwkind[slot] ? 2 : 1;
     e.mw_steps = ml.steps;
     if (code == MW_SURFACE) {
@@ -2133,6 +2166,7 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 constexpr int kFdmMaxN = 32;  // voxel classes held in shared memory
+constexpr int kFdmClasses = KMAX + 1;  // job-local classes (class_of)
 struct FdmQueue {
   const int* queue;
   const unsigned long long* qlen;
@@ -2205,20 +2239,15 @@ __global__ void __launch_bounds__(kFdmThreads)
   extern __shared__ __align__(16) uint8_t fsm[];
   __shared__ double red[66];
   __shared__ int job_sh;
-  const int n = P.n, m = n * n * n, nn = n * n, Pn = s.P;
+  // voxel classes are job-local (class_of): the job's permittivities and
+  // their pair tables are rebuilt per job, Pn = KMAX + 1 local classes
+  const int n = P.n, m = n * n * n, nn = n * n, Pn = kFdmClasses;
   const int panels = 6 * nn;
   double* pal = reinterpret_cast<double*>(fsm);
   double* apair = pal + Pn;
   double* spair = apair + Pn * Pn;
   double* psm = spair + Pn * Pn;  // [m] when PSM
   uint8_t* cls = reinterpret_cast<uint8_t*>(PSM ? psm + m : psm);
-  for (int i = threadIdx.x; i < Pn; i += blockDim.x) pal[i] = __ldg(s.pal + i);
-  __syncthreads();
-  for (int q = threadIdx.x; q < Pn * Pn; q += blockDim.x) {
-    const double ei = pal[q / Pn], ev = pal[q % Pn];
-    apair[q] = ei / (ei + ev);          // sgf.cpp:129
-    spair[q] = -(ev * ei) / (ev + ei);  // sgf.cpp:135-137, bit-symmetric
-  }
   double* x = slab + static_cast<size_t>(blockIdx.x) * 5 * m;
   double* r = x + m;
   double* p = PSM ? psm : r + m;
@@ -2239,11 +2268,21 @@ __global__ void __launch_bounds__(kFdmThreads)
     // voxel classes of the cube from the job's atlas
     const uint64_t* A = lane_atlas(W, slot);
     const uint64_t bm[3] = {A[kAtBm], A[kAtBm + 1], A[kAtBm + 2]};
-    const uint8_t* cb = reinterpret_cast<const uint8_t*>(A + kAtCls);
     const uint64_t cm = cond_mask(W.nbox[slot]);
     for (int v = threadIdx.x; v < m; v += blockDim.x) {
       const int vv[3] = {v % n, (v / n) % n, v / nn};
-      cls[v] = static_cast<uint8_t>(class_of(cb, voxel_mask(A, bm, vv), cm, s.bg));
+      cls[v] = static_cast<uint8_t>(class_of(voxel_mask(A, bm, vv), cm));
+    }
+    // (entries of local classes the job does not use are never read)
+    for (int i = threadIdx.x; i < Pn; i += blockDim.x) {
+      const int g = global_class(A, i, s.bg);
+      pal[i] = g < s.P ? __ldg(s.pal + g) : 1.0;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < Pn * Pn; q += blockDim.x) {
+      const double ei = pal[q / Pn], ev = pal[q % Pn];
+      apair[q] = ei / (ei + ev);          // sgf.cpp:129
+      spair[q] = -(ev * ei) / (ev + ei);  // sgf.cpp:135-137, bit-symmetric
     }
     __syncthreads();
     // PCG on s_ii z = e_c (Jacobi preconditioner, x0 = 0)
@@ -2377,6 +2416,41 @@ size_t fdm_smem_bytes(int n, int Pn, bool psm) {
   return 8 * static_cast<size_t>(Pn) * (1 + 2 * Pn) + (psm ? 8 * m : 0) + m;
 }
 
+// ---- geometry queries (the Structure API on the device, for unit parity) ---
+// Per point: Structure::conductor_at(p, tol) (geometry.cpp:57-62, declaration
+// index or -1), max_free_cube (:64-80; -1 where the reference throws),
+// permittivity_at (:47-55; NaN outside the world) and the walk engine's
+// fused transition prologue hop_scan (engine.cpp:293-298: conductor index,
+// -1 grounded wall, -2 error, -3 free cube of half width hop_h).
+__global__ void k_geometry(DStruct s, const double* pts, int count, double tol, int32_t* cond,
+                           double* free_h, double* eps, int32_t* hop, double* hop_h) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const double p[3] = {pts[3 * t], pts[3 * t + 1], pts[3 * t + 2]};
+  cond[t] = conductor_at(s, p, tol);
+  double h = -1.0;
+  free_h[t] = max_free_cube(s, p, &h) ? h : -1.0;
+  const int c = eps_class_at(s, p);
+  eps[t] = c < 0 ? __longlong_as_double(0x7FF8000000000000ll) : __ldg(s.pal + c);
+  double hh = -1.0;
+  hop[t] = hop_scan(s, p, tol, &hh);
+  hop_h[t] = hh;
+}
+
+// Per cube: the stratification probe + profile key of a transition cube
+// (stratified_profile, geometry.cpp:357-396, then profile_key,
+// sgf_cache.cpp:29-51): key axis (-1 general cube) and rounded layers.
+__global__ void k_strat_keys(DStruct s, const double* cubes, int count, int n, int32_t* axis,
+                             double* layers) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const double c[3] = {cubes[4 * t], cubes[4 * t + 1], cubes[4 * t + 2]};
+  double lay[NMAX];
+  const int a = stratified_key(s, c, cubes[4 * t + 3], n, lay);
+  axis[t] = a;
+  for (int q = 0; q < n; ++q) layers[static_cast<size_t>(t) * n + q] = a >= 0 ? lay[q] : 0.0;
+}
+
 // ---- deterministic tallies -------------------------------------------------
 constexpr int kChunk = 1024;
 
@@ -2422,10 +2496,14 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// pack: the call's tally as one f64 vector -- sum[nslots], sumsq[nslots],
+// landed[nslots], stats[12] (counts exact below 2^53) -- the buffer
+// frw_tally_allreduce combines across ranks with one NCCL all-reduce
 __global__ void k_reduce_final(int nblocks, int nslots, const double* psum, const double* psq,
                                const unsigned long long* pland,
                                const unsigned long long* pstat, double* osum, double* osq,
-                               unsigned long long* oland, unsigned long long* ostat) {
+                               unsigned long long* oland, unsigned long long* ostat,
+                               double* pack) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < nslots) {
     double s1 = 0, s2 = 0;
@@ -2438,11 +2516,15 @@ __global__ void k_reduce_final(int nblocks, int nslots, const double* psum, cons
     osum[t] = s1;
     osq[t] = s2;
     oland[t] = c;
+    pack[t] = s1;
+    pack[nslots + t] = s2;
+    pack[2 * nslots + t] = static_cast<double>(c);
   } else if (t < nslots + 12) {
     const int q = t - nslots;
     unsigned long long c = 0;
     for (int b = 0; b < nblocks; ++b) c += pstat[static_cast<size_t>(b) * 12 + q];
     ostat[q] = c;
+    pack[3 * nslots + q] = static_cast<double>(c);
   }
 }
 
@@ -2485,6 +2567,7 @@ struct SgfHost {
   // mirrored per palette class into d_uentry by uentry_sync
   std::map<double, int> uniform;
   int* d_uentry = nullptr;
+  size_t uentry_cap = 0;
 };
 
 struct Engine {
@@ -2493,7 +2576,7 @@ struct Engine {
   double world[6];
   double *d_cbox = nullptr, *d_dbox = nullptr, *d_pal = nullptr, *d_alpha = nullptr,
          *d_rpal = nullptr;
-  uint8_t* d_dcls = nullptr;
+  uint16_t* d_dcls = nullptr;
   bool have_structure = false;
   DGrid grid{};             // conductor bins (dims 0: none)
   int* d_cstart = nullptr;
@@ -2516,7 +2599,10 @@ struct Engine {
   int* ring_a = nullptr;  // k_flow rings of walk slots (-1 = empty entry)
   int* ring_m = nullptr;
   unsigned ring_mask = 0;
-  // reduction scratch
+  // reduction scratch; `pack` holds the last call's tally (tally_n doubles)
+  // for frw_tally_allreduce
+  double* pack = nullptr;
+  int tally_n = 0, tally_slots = 0, tally_mode = 0;
   double *psum = nullptr, *psq = nullptr, *osum = nullptr, *osq = nullptr;
   unsigned long long *pland = nullptr, *pstat = nullptr, *oland = nullptr, *ostat = nullptr;
   size_t red_cap = 0;
@@ -2601,6 +2687,7 @@ void engine_free(frw_ctx* ctx) {
   cudaFree(E->osq);
   cudaFree(E->oland);
   cudaFree(E->ostat);
+  cudaFree(E->pack);
   cudaFree(E->fdm_slab);
   cudaFree(E->d_jmeta);
   cudaFree(E->d_jthr);
@@ -2669,16 +2756,19 @@ int sgf_sync(frw_ctx* ctx, SgfHost& T) {
 // per palette class: the table entry of its uniform key, or -1
 int uentry_sync(frw_ctx* ctx, Engine& E) {
   SgfHost& T = E.sgf;
-  if (!T.d_uentry) {
-    T.d_uentry = dalloc<int>(PMAX);
+  const size_t P = std::max<size_t>(E.h_rpal.size(), 1);
+  if (!T.d_uentry || T.uentry_cap < P) {
+    cudaFree(T.d_uentry);
+    T.d_uentry = dalloc<int>(P);
+    T.uentry_cap = T.d_uentry ? P : 0;
     if (!T.d_uentry) return frw_fail(ctx, FRW_ENOMEM, "sgf table: device allocation failed");
   }
-  std::vector<int> u(PMAX, -1);
-  for (size_t c = 0; c < E.h_rpal.size() && c < static_cast<size_t>(PMAX); ++c) {
+  std::vector<int> u(P, -1);
+  for (size_t c = 0; c < E.h_rpal.size(); ++c) {
     const auto it = T.uniform.find(E.h_rpal[c]);
     if (it != T.uniform.end()) u[c] = it->second;
   }
-  FRW_CUDA(ctx, cudaMemcpyAsync(T.d_uentry, u.data(), 4 * PMAX, cudaMemcpyHostToDevice,
+  FRW_CUDA(ctx, cudaMemcpyAsync(T.d_uentry, u.data(), 4 * P, cudaMemcpyHostToDevice,
                                 ctx->stream));
   return FRW_OK;
 }
@@ -2859,8 +2949,8 @@ int ensure_jumps(frw_ctx* ctx, Engine& E, int n, DJump* out) {
 int launch_fdm(frw_ctx* ctx, Engine& E, const DStruct& s, const DParams& P, DCounters* C,
                const FdmQueue& Q) {
   const size_t cap = static_cast<size_t>(ctx->max_smem_optin);
-  const bool psm = fdm_smem_bytes(P.n, s.P, true) <= cap;
-  const size_t smem = fdm_smem_bytes(P.n, s.P, psm);
+  const bool psm = fdm_smem_bytes(P.n, kFdmClasses, true) <= cap;
+  const size_t smem = fdm_smem_bytes(P.n, kFdmClasses, psm);
   if (smem > cap)
     return frw_fail(ctx, FRW_EINVAL, "FDM: lattice too large for the shared-memory class field");
   // one CTA per SM keeps every CTA's five Krylov vectors (5 x 8 n^3 bytes)
@@ -2931,8 +3021,16 @@ int resolve_misses(frw_ctx* ctx, Engine& E, int n, unsigned long long nmiss, frw
   return uentry_sync(ctx, E);
 }
 
+// device bytes of one resident walk slot (slot arrays, job, queues, rings,
+// restart lists; ensure_slots)
+constexpr size_t kSlotBytes = 1 + 8 + 24 + 8 + 8 + 4 + 4 + 4 + 8 + 1 + 1 + 32 + 1 + 8 * KMAX + 1 +
+                              8 * kAtlasWords + 4 + 8 + 16 + 16 + 16 + 8;
+
+// Slot capacity only grows: calls of different sizes (the short last chunk
+// of a stopping rule, the single-transition API) reuse the pool, and the
+// active pool size of a call is set per call (frw_run_walks: W.S).
 int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
-  if (E.S == S) return FRW_OK;
+  if (E.S >= S) return FRW_OK;
   free_slots(E);
   DSlots& W = E.W;
   W.S = S;
@@ -3109,25 +3207,39 @@ int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
   Engine& E = *engine_of(ctx);
   // palette of distinct permittivities (background first)
   std::vector<double> pal{s->background_eps};
-  std::vector<uint8_t> dcls(s->n_diel);
+  std::vector<uint16_t> dcls(s->n_diel);
+  std::unordered_map<uint64_t, int> index;  // palette by bit pattern
+  {
+    uint64_t bits;
+    std::memcpy(&bits, &s->background_eps, 8);
+    index.emplace(bits, 0);
+  }
   for (int d = 0; d < s->n_diel; ++d) {
     const double e = s->diel_eps[d];
-    int k = -1;
-    for (size_t q = 0; q < pal.size(); ++q)
-      if (std::memcmp(&pal[q], &e, 8) == 0) k = static_cast<int>(q);
-    if (k < 0) {
-      if (pal.size() >= static_cast<size_t>(PMAX) - 1)
-        return frw_fail(ctx, FRW_EINVAL, "upload_structure: more than 63 distinct permittivities");
+    uint64_t bits;
+    std::memcpy(&bits, &e, 8);
+    auto it = index.find(bits);
+    int k;
+    if (it != index.end()) {
+      k = it->second;
+    } else {
+      if (pal.size() > static_cast<size_t>(kClassMax))
+        return frw_fail(ctx, FRW_EINVAL, "upload_structure: more than 32767 distinct permittivities");
       k = static_cast<int>(pal.size());
       pal.push_back(e);
+      index.emplace(bits, k);
     }
-    dcls[d] = static_cast<uint8_t>(k);
+    dcls[d] = static_cast<uint16_t>(k);
   }
   const int P = static_cast<int>(pal.size());
-  std::vector<double> alpha(static_cast<size_t>(P) * P), rpal(P);
+  // the pair-alpha table for palettes that fit shared memory (larger ones
+  // divide per cell change, lane_alphas)
+  const int PA = P <= PMAX ? P : 1;
+  std::vector<double> alpha(static_cast<size_t>(PA) * PA, 0.0), rpal(P);
   for (int a = 0; a < P; ++a) {
     rpal[a] = host_round_sig(pal[a], 6);
-    for (int b = 0; b < P; ++b) alpha[a * P + b] = pal[a] / (pal[a] + pal[b]);
+    if (P <= PMAX)
+      for (int b = 0; b < P; ++b) alpha[a * P + b] = pal[a] / (pal[a] + pal[b]);
   }
   cudaFree(E.d_cbox);
   cudaFree(E.d_dbox);
@@ -3137,9 +3249,9 @@ int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
   cudaFree(E.d_dcls);
   E.d_cbox = dalloc<double>(6 * size_t(s->n_cond));
   E.d_dbox = dalloc<double>(6 * size_t(s->n_diel));
-  E.d_dcls = dalloc<uint8_t>(s->n_diel);
+  E.d_dcls = dalloc<uint16_t>(s->n_diel);
   E.d_pal = dalloc<double>(P);
-  E.d_alpha = dalloc<double>(size_t(P) * P);
+  E.d_alpha = dalloc<double>(size_t(PA) * PA);
   E.d_rpal = dalloc<double>(P);
   if (!E.d_cbox || !E.d_dbox || !E.d_dcls || !E.d_pal || !E.d_alpha || !E.d_rpal)
     return frw_fail(ctx, FRW_ENOMEM, "upload_structure: device allocation failed");
@@ -3148,13 +3260,13 @@ int frw_upload_structure(frw_ctx* ctx, const frw_structure* s) {
   if (s->n_diel) {
     FRW_CUDA(ctx, cudaMemcpyAsync(E.d_dbox, s->diel_box, 48 * size_t(s->n_diel), cudaMemcpyHostToDevice,
                                 ctx->stream));
-    FRW_CUDA(ctx, cudaMemcpyAsync(E.d_dcls, dcls.data(), s->n_diel, cudaMemcpyHostToDevice,
-                                ctx->stream));
+    FRW_CUDA(ctx, cudaMemcpyAsync(E.d_dcls, dcls.data(), 2 * size_t(s->n_diel),
+                                  cudaMemcpyHostToDevice, ctx->stream));
   }
   FRW_CUDA(ctx, cudaMemcpyAsync(E.d_pal, pal.data(), 8 * P, cudaMemcpyHostToDevice,
                                 ctx->stream));
-  FRW_CUDA(ctx, cudaMemcpyAsync(E.d_alpha, alpha.data(), 8 * size_t(P) * P, cudaMemcpyHostToDevice,
-                                ctx->stream));
+  FRW_CUDA(ctx, cudaMemcpyAsync(E.d_alpha, alpha.data(), 8 * size_t(PA) * PA,
+                                cudaMemcpyHostToDevice, ctx->stream));
   E.h_rpal = rpal;
   FRW_CUDA(ctx, cudaMemcpyAsync(E.d_rpal, rpal.data(), 8 * P, cudaMemcpyHostToDevice,
                                 ctx->stream));
@@ -3420,6 +3532,7 @@ int frw_sgf_clear(frw_ctx* ctx) {
   fresh.d_pitch = E.sgf.d_pitch;
   fresh.d_data = E.sgf.d_data;
   fresh.d_uentry = E.sgf.d_uentry;
+  fresh.uentry_cap = E.sgf.uentry_cap;
   fresh.dev_entries_cap = E.sgf.dev_entries_cap;
   fresh.dirty = true;
   E.sgf = fresh;
@@ -3524,6 +3637,85 @@ int frw_structure_transits_philox(frw_ctx* ctx, int n, int count, const double* 
                             seed, jumps, step_cap, out);
 }
 
+int frw_geometry_queries(frw_ctx* ctx, int count, const double* points, double tol,
+                         int32_t* conductor_at, double* free_half_width, double* eps,
+                         int32_t* hop_code, double* hop_half_width) {
+  if (!ctx) return FRW_EINVAL;
+  Engine& E = *engine_of(ctx);
+  if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "geometry: no structure uploaded");
+  if (count < 0 || (count > 0 && (!points || !conductor_at || !free_half_width || !eps ||
+                                  !hop_code || !hop_half_width)))
+    return frw_fail(ctx, FRW_EINVAL, "geometry: bad arguments");
+  if (count == 0) return FRW_OK;
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  const size_t n = static_cast<size_t>(count);
+  double* d_p = dalloc<double>(3 * n);
+  int32_t* d_c = dalloc<int32_t>(n);
+  double* d_f = dalloc<double>(n);
+  double* d_e = dalloc<double>(n);
+  int32_t* d_hc = dalloc<int32_t>(n);
+  double* d_hh = dalloc<double>(n);
+  int status = FRW_OK;
+  if (!d_p || !d_c || !d_f || !d_e || !d_hc || !d_hh) {
+    status = frw_fail(ctx, FRW_ENOMEM, "geometry: device allocation failed");
+  } else {
+    cudaStream_t st = ctx->stream;
+    const DStruct s = make_dstruct(E);
+    cudaMemcpyAsync(d_p, points, 24 * n, cudaMemcpyHostToDevice, st);
+    k_geometry<<<(count + 127) / 128, 128, 0, st>>>(s, d_p, count, tol, d_c, d_f, d_e, d_hc,
+                                                      d_hh);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(conductor_at, d_c, 4 * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(free_half_width, d_f, 8 * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(eps, d_e, 8 * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(hop_code, d_hc, 4 * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(hop_half_width, d_hh, 8 * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      status = frw_fail(ctx, FRW_ECUDA, "geometry: kernel failed");
+  }
+  cudaFree(d_p);
+  cudaFree(d_c);
+  cudaFree(d_f);
+  cudaFree(d_e);
+  cudaFree(d_hc);
+  cudaFree(d_hh);
+  return status;
+}
+
+int frw_stratified_keys(frw_ctx* ctx, int n, int count, const double* cubes, int32_t* axis,
+                        double* layers) {
+  if (!ctx) return FRW_EINVAL;
+  Engine& E = *engine_of(ctx);
+  if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "strat keys: no structure uploaded");
+  if (n < 1 || n > NMAX) return frw_fail(ctx, FRW_EINVAL, "strat keys: n must lie in [1, 64]");
+  if (count < 0 || (count > 0 && (!cubes || !axis || !layers)))
+    return frw_fail(ctx, FRW_EINVAL, "strat keys: bad arguments");
+  if (count == 0) return FRW_OK;
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  const size_t m = static_cast<size_t>(count);
+  double* d_c = dalloc<double>(4 * m);
+  int32_t* d_a = dalloc<int32_t>(m);
+  double* d_l = dalloc<double>(m * n);
+  int status = FRW_OK;
+  if (!d_c || !d_a || !d_l) {
+    status = frw_fail(ctx, FRW_ENOMEM, "strat keys: device allocation failed");
+  } else {
+    cudaStream_t st = ctx->stream;
+    const DStruct s = make_dstruct(E);
+    cudaMemcpyAsync(d_c, cubes, 32 * m, cudaMemcpyHostToDevice, st);
+    k_strat_keys<<<(count + 127) / 128, 128, 0, st>>>(s, d_c, count, n, d_a, d_l);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(axis, d_a, 4 * m, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(layers, d_l, 8 * m * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      status = frw_fail(ctx, FRW_ECUDA, "strat keys: kernel failed");
+  }
+  cudaFree(d_c);
+  cudaFree(d_a);
+  cudaFree(d_l);
+  return status;
+}
+
 int frw_lattice_jump_law(int m, double* face, double* esteps) {
   if (m < 2 || m > 31 || !face) return FRW_EINVAL;
   std::vector<long double> f;
@@ -3597,6 +3789,139 @@ int frw_transitions(frw_ctx* ctx, const frw_walk_params* prm, int count, const d
       });
 }
 
+}  // extern "C"
+
+// ---- NCCL (loaded at first use: the library does not link it, so a host
+// process that already loaded its own libnccl.so.2 -- e.g. torch's -- shares
+// that copy) ------------------------------------------------------------------
+namespace frw {
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string why;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+std::mutex g_nccl_mu;
+NcclApi& nccl() {
+  static NcclApi api;
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    api.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+    return api;
+  }
+  api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+  api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+  api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+  api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+  api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy &&
+           api.error_string;
+  if (!api.ok) api.why = "libnccl.so.2 lacks an expected symbol";
+  return api;
+}
+int nccl_fail(frw_ctx* ctx, const char* what, ncclResult_t r) {
+  return frw_fail(ctx, FRW_ECUDA, std::string(what) + ": " + nccl().error_string(r));
+}
+// the context's own communicator (frw_nccl_init); kept beside the walk engine
+std::map<frw_ctx*, ncclComm_t>& comms() {
+  static auto* m = new std::map<frw_ctx*, ncclComm_t>;
+  return *m;
+}
+}  // namespace
+}  // namespace frw
+
+extern "C" {
+
+int frw_nccl_unique_id(void* id) {
+  if (!id) return FRW_EINVAL;
+  NcclApi& api = nccl();
+  if (!api.ok) return FRW_ECUDA;
+  ncclUniqueId u;
+  if (api.get_unique_id(&u) != ncclSuccess) return FRW_ECUDA;
+  std::memcpy(id, &u, sizeof u);
+  return FRW_OK;
+}
+
+int frw_nccl_init(frw_ctx* ctx, const void* id, int nranks, int rank) {
+  if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks) return FRW_EINVAL;
+  NcclApi& api = nccl();
+  if (!api.ok) return frw_fail(ctx, FRW_ECUDA, api.why);
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof u);
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = api.comm_init_rank(&comm, nranks, u, rank);
+  if (r != ncclSuccess) return nccl_fail(ctx, "ncclCommInitRank", r);
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  auto& m = comms();
+  if (m.count(ctx)) api.comm_destroy(m[ctx]);
+  m[ctx] = comm;
+  return FRW_OK;
+}
+
+int frw_nccl_destroy(frw_ctx* ctx) {
+  if (!ctx) return FRW_EINVAL;
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  auto& m = comms();
+  auto it = m.find(ctx);
+  if (it == m.end()) return FRW_OK;
+  nccl().comm_destroy(it->second);
+  m.erase(it);
+  return FRW_OK;
+}
+
+int frw_tally_allreduce(frw_ctx* ctx, void* comm, frw_tally* out) {
+  if (!ctx || !out) return FRW_EINVAL;
+  Engine* E = static_cast<Engine*>(ctx->walk);
+  if (!E || E->tally_n <= 0)
+    return frw_fail(ctx, FRW_EINVAL, "tally_allreduce: no frw_run_walks tally on this context");
+  NcclApi& api = nccl();
+  if (!api.ok) return frw_fail(ctx, FRW_ECUDA, api.why);
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  if (!c) {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    auto it = comms().find(ctx);
+    if (it != comms().end()) c = it->second;
+  }
+  if (!c) return frw_fail(ctx, FRW_EINVAL, "tally_allreduce: no communicator (frw_nccl_init)");
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  // one all-reduce (sum) of the packed tally over NVLink / NVSwitch
+  const ncclResult_t r = api.all_reduce(E->pack, E->pack, static_cast<size_t>(E->tally_n),
+                                        ncclFloat64, ncclSum, c, ctx->stream);
+  if (r != ncclSuccess) return nccl_fail(ctx, "ncclAllReduce", r);
+  std::vector<double> h(E->tally_n);
+  FRW_CUDA(ctx, cudaMemcpyAsync(h.data(), E->pack, 8 * h.size(), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const int k = E->tally_slots;
+  for (int i = 0; i < k; ++i) {
+    if (out->sum) out->sum[i] = h[i];
+    if (out->sumsq) out->sumsq[i] = h[k + i];
+    if (out->landed) out->landed[i] = static_cast<uint64_t>(h[2 * k + i]);
+  }
+  const double* st = &h[3 * k];
+  out->aborted = static_cast<uint64_t>(st[0]);
+  out->resampled = static_cast<uint64_t>(st[1]);
+  for (int b = 0; b < 4; ++b) out->first[b] = static_cast<uint64_t>(st[2 + b]);
+  const bool mwe = E->tally_mode == FRW_MODE_MWE || E->tally_mode == FRW_MODE_HYBRID_MWE;
+  const bool fdm = E->tally_mode == FRW_MODE_FDM;
+  out->sub[0] = static_cast<uint64_t>(st[6]);
+  out->sub[1] = mwe || fdm ? 0 : static_cast<uint64_t>(st[7]);
+  out->sub[2] = mwe ? static_cast<uint64_t>(st[7]) : 0;
+  out->sub[3] = fdm ? static_cast<uint64_t>(st[7]) : 0;
+  out->mw_steps = static_cast<uint64_t>(st[8]);
+  return FRW_OK;
+}
+
 int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint64_t walk_begin,
                   int64_t count, frw_miss_fn miss, void* user, frw_tally* out,
                   frw_walk_record* records) {
@@ -3615,27 +3940,36 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   if (E.sgf.n && E.sgf.n != prm->grid_n)
     return frw_fail(ctx, FRW_EINVAL, "run_walks: SGF table holds another lattice size");
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  E.tally_n = 0;  // no tally for frw_tally_allreduce until this call succeeds
   const int nslots = E.nc + 1;
-  cudaEvent_t t0, t1, m0, m1;
-  cudaEventCreate(&t0);
-  cudaEventCreate(&t1);
-  cudaEventCreate(&m0);
-  cudaEventCreate(&m1);
-  // FRW_TRACE_ROUNDS=1: per-round queue lengths and stage times on stderr
-  const bool trace = std::getenv("FRW_TRACE_ROUNDS") != nullptr;
-  cudaEvent_t a0 = nullptr;
-  if (trace) cudaEventCreate(&a0);
-  cudaEventRecord(t0, ctx->stream);
-
   // resident walk slots: 2^20, or for long calls up to 2^22 (about half the
   // walks in flight: rounds stay full longer; 8M-walk calls run 3.1e7 ->
-  // 3.7e7 walks/s on C3/C5 from 2^20 to 2^22 slots, ~10 GB of slot state)
+  // 3.7e7 walks/s on C3/C5 from 2^20 to 2^22 slots, ~10 GB of slot state).
+  // An automatic pool is bounded by the free device memory and halved down
+  // to the default when an allocation fails (several contexts or ranks may
+  // share the GPU); capacity only grows, so mixed call sizes reuse it.
   int S = prm->n_slots > 0 ? prm->n_slots : kSlotsDefault;
-  if (prm->n_slots <= 0) {
+  const bool auto_slots = prm->n_slots <= 0;
+  if (auto_slots) {
     while (S < (1 << 22) && static_cast<long long>(S) * 2 < count) S *= 2;
     if (const char* e = std::getenv("FRW_SLOTS")) S = std::max(1024, std::atoi(e));
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+      const size_t have = static_cast<size_t>(E.S) * kSlotBytes;  // reusable pool
+      while (S > kSlotsDefault && static_cast<size_t>(S) * kSlotBytes > (fr + have) / 2) S /= 2;
+    }
   }
-  if (int rc = ensure_slots(ctx, E, S)) return rc;
+  {
+    int rc = ensure_slots(ctx, E, S);
+    while (rc == FRW_ENOMEM && auto_slots && S > kSlotsDefault) {
+      cudaGetLastError();  // clear the failed allocation
+      S /= 2;
+      rc = ensure_slots(ctx, E, S);
+    }
+    if (rc) return rc;
+  }
+  DSlots Wc = E.W;  // the pool of this call: S active slots of the capacity
+  Wc.S = S;
   if (E.recs_cap < count) {
     cudaFree(E.recs);
     E.recs = dalloc<WalkRec>(count);
@@ -3649,6 +3983,25 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   }
   if (int rc = sgf_sync(ctx, E.sgf)) return rc;
   if (int rc = uentry_sync(ctx, E)) return rc;
+
+  // events: created after every early-return allocation/sync step above and
+  // destroyed on every exit below
+  struct Events {
+    cudaEvent_t t0 = nullptr, t1 = nullptr, m0 = nullptr, m1 = nullptr, a0 = nullptr;
+    ~Events() {
+      for (cudaEvent_t e : {t0, t1, m0, m1, a0})
+        if (e) cudaEventDestroy(e);
+    }
+  } ev;
+  cudaEventCreate(&ev.t0);
+  cudaEventCreate(&ev.t1);
+  cudaEventCreate(&ev.m0);
+  cudaEventCreate(&ev.m1);
+  // FRW_TRACE_ROUNDS=1: per-round queue lengths and stage times on stderr
+  const bool trace = std::getenv("FRW_TRACE_ROUNDS") != nullptr;
+  if (trace) cudaEventCreate(&ev.a0);
+  cudaEvent_t t0 = ev.t0, t1 = ev.t1, m0 = ev.m0, m1 = ev.m1, a0 = ev.a0;
+  cudaEventRecord(t0, ctx->stream);
 
   const DStruct s = make_dstruct(E);
   DParams P = params_of(prm);
@@ -3684,7 +4037,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     int* aq_in = E.aq[round & 1];
     int* aq_out = E.aq[(round + 1) & 1];
     if (trace) cudaEventRecord(a0, ctx->stream);
-    k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in);
+    k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in);
     if (tail) {
       cudaEventRecord(m0, ctx->stream);
       const int tb = ctx->sm_count * kTailBlocks;  // persistent, one wave
@@ -3695,18 +4048,18 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         k_flow_init<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
         if (P.rng == FRW_RNG_PHILOX)
           k_flow<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(
-              s, T, P, E.W, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
+              s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
         else
           k_flow<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(
-              s, T, P, E.W, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
+              s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
       } else if (P.rng == FRW_RNG_PHILOX)
-        k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M,
+        k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M,
                                                            aq_in);
       else
-        k_tail<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs,
+        k_tail<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs,
                                                                     E.d_cnt, M, aq_in);
     } else {
-      k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, E.W, E.recs, E.d_cnt, M, aq_in,
+      k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in,
                                                    E.queue);
       cudaEventRecord(m0, ctx->stream);
       if (P.mode == FRW_MODE_FDM) {
@@ -3716,10 +4069,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
           break;
         }
       } else if (P.rng == FRW_RNG_PHILOX)
-        k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs, E.d_cnt,
+        k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, Wc, E.recs, E.d_cnt,
                                                                E.queue, aq_out);
       else
-        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, E.W, E.recs,
+        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, Wc, E.recs,
                                                                         E.d_cnt, E.queue, aq_out);
     }
     cudaEventRecord(m1, ctx->stream);
@@ -3810,6 +4163,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       cudaFree(E.osq);
       cudaFree(E.oland);
       cudaFree(E.ostat);
+      cudaFree(E.pack);
       const size_t cap = static_cast<size_t>(std::max(nblocks, 1)) * nslots;
       E.psum = dalloc<double>(cap);
       E.psq = dalloc<double>(cap);
@@ -3819,6 +4173,12 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       E.osq = dalloc<double>(nslots);
       E.oland = dalloc<unsigned long long>(nslots);
       E.ostat = dalloc<unsigned long long>(12);
+      E.pack = dalloc<double>(3 * static_cast<size_t>(nslots) + 12);
+      if (!E.psum || !E.psq || !E.pland || !E.pstat || !E.osum || !E.osq || !E.oland ||
+          !E.ostat || !E.pack) {
+        E.red_cap = 0;
+        return frw_fail(ctx, FRW_ENOMEM, "run_walks: tally allocation failed");
+      }
       E.red_cap = cap;
       E.red_slots = nslots;
     }
@@ -3827,7 +4187,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       k_reduce_chunks<<<nblocks, 256, 0, ctx->stream>>>(E.recs, count, nslots, E.psum, E.psq,
                                                          E.pland, E.pstat);
       k_reduce_final<<<(nslots + 12 + 127) / 128, 128, 0, ctx->stream>>>(
-          nblocks, nslots, E.psum, E.psq, E.pland, E.pstat, E.osum, E.osq, E.oland, E.ostat);
+          nblocks, nslots, E.psum, E.psq, E.pland, E.pstat, E.osum, E.osq, E.oland, E.ostat,
+          E.pack);
       FRW_CUDA(ctx, cudaGetLastError());
       if (out->sum)
         FRW_CUDA(ctx, cudaMemcpyAsync(out->sum, E.osum, 8 * nslots, cudaMemcpyDeviceToHost,
@@ -3841,6 +4202,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       FRW_CUDA(ctx, cudaMemcpyAsync(st.data(), E.ostat, 8 * 12, cudaMemcpyDeviceToHost,
                                     ctx->stream));
     } else {
+      FRW_CUDA(ctx, cudaMemsetAsync(E.pack, 0, 8 * (3 * static_cast<size_t>(nslots) + 12),
+                                    ctx->stream));
       for (int k = 0; k < nslots; ++k) {
         if (out->sum) out->sum[k] = 0;
         if (out->sumsq) out->sumsq[k] = 0;
@@ -3852,6 +4215,9 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                                     cudaMemcpyDeviceToHost, ctx->stream));
     cudaEventRecord(t1, ctx->stream);
     FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    E.tally_n = 3 * nslots + 12;
+    E.tally_slots = nslots;
+    E.tally_mode = P.mode;
     out->aborted = st[0];
     out->resampled = st[1];
     for (int b = 0; b < 4; ++b) out->first[b] = st[2 + b];
@@ -3875,11 +4241,6 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     cudaEventElapsedTime(&tot, t0, t1);
     out->total_ms = tot;
   }
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
-  cudaEventDestroy(m0);
-  cudaEventDestroy(m1);
-  if (a0) cudaEventDestroy(a0);
   return status;
 }
 

@@ -48,11 +48,14 @@ CASES = {
 MODES = {"HYBRID-MW": capi.MODE_HYBRID_MW, "HYBRID-MWE": capi.MODE_HYBRID_MWE}
 
 
+@pytest.mark.parametrize("grid_min", ["default", "0"])  # "0": geometry bins on every scene
 @pytest.mark.parametrize("mode", sorted(MODES))
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_walks_bit_exact_vs_oracle(gpu_ctx, oracle, case, mode):
+def test_walks_bit_exact_vs_oracle(gpu_ctx, oracle, monkeypatch, case, mode, grid_min):
     make, n = CASES[case]
     sc = make()
+    if grid_min != "default":
+        monkeypatch.setenv("FRW_GRID_MIN", grid_min)
     count = 600 if n == 24 else 2000
     if mode == "HYBRID-MWE" and case in ("c3", "c4", "c5"):
         count = 300  # expanded cubes: the oracle classifies far more voxels

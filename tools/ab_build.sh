@@ -2,6 +2,7 @@
 # A/B of a kernel compile knob on the GPU box: time C3/C5 walks with the
 # default build, rebuild libfrwgpu.so with FRW_NVCC_EXTRA="$1", time again.
 # usage: tools/ab_build.sh "-DFRW_KMW_MINB=2" [configs...]
+trap 'python -c "from paper_2507_09730_b200 import build as b; b.build_gpu_lib()" > /dev/null 2>&1' EXIT  # back to the default build
 set -e
 flags="$1"; shift
 cfg="${@:-c3 c5}"
