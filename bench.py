@@ -1,20 +1,29 @@
 """Benchmark of the B200 MicroWalk / FRW hot path (bench contract).
 
-Default workload: BASELINE.json configs[1] (C2) -- the 41^3 high-contrast
-block cube, 1e7 MicroWalk transitions per step from the centre node, Philox
-streams keyed by (seed, transit, step).  One step = one pass over the 1e7
-transits; under torchrun every rank runs its own 1e7 (weak scaling, disjoint
-stream ranges) and the per-rank histograms/moments are combined by one NCCL
-all-reduce per step.
+One JSON line.  The headline (top-level keys) is BASELINE.json configs[1]
+(C2): the 41^3 high-contrast block cube, 1e7 MicroWalk transitions per step
+from the centre node, Philox streams keyed by (seed, transit, step).  Under
+torchrun every rank runs its own 1e7 (weak scaling, disjoint stream ranges)
+and the per-rank histograms/moments are combined by one NCCL all-reduce per
+step.  `configs` carries every BASELINE config at its stated size, each with
+`value` (device time), `e2e` (the public call with host buffers), `roofline`
+and `cpu_baseline`:
+
+  C1  21^3 single cube, 1e6 transitions per step          (transitions/s)
+  C2  the headline                                         (transitions/s)
+  C3  two wires over a plane, 1e6 walks, HYBRID-MW         (walks/s)
+  C4  3-layer crossing bus, until every coupling has 1% relative SE (walks/s)
+  C5  200-conductor structure, 10 masters x 1e7 = 1e8 walks (walks/s; the
+      1/2/4/8-GPU scaling workload: one walk sequence per master, contiguous
+      ranges per rank, one frw_tally_allreduce per master)
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-`value` is device-timed (CUDA events on the launch stream, L2 flushed between
-timed steps, max over ranks); `e2e` goes through the C ABI with host buffers
-(upload of the cube + copy-back of histogram and moments inside the timed
-region); `roofline` is for the dominant kernel (mw_grid_fast) against the
-measured on-chip shared-memory bandwidth; `cpu_baseline` times the
-reference's own microwalk_transit (oracle/_ref) on the host cores.
+Device values are timed with CUDA events on the launch stream (max over
+ranks); the C1/C2 steps flush L2 between timed steps; the walk configs'
+working set (the resident walk-slot pool, GBs) exceeds L2.  cpu_baseline
+runs the reference's own code (oracle/_ref: microwalk_transit for C1/C2,
+Engine::extract for C3-C5) on all host threads over a bounded sample.
 """
 from __future__ import annotations
 
@@ -24,6 +33,7 @@ import os
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -39,6 +49,25 @@ COUNT = 10_000_000
 WORKLOAD = ("C2 (BASELINE configs[1]): 41^3-node cube, eps piecewise constant on 4x4x4-node "
             "blocks drawn from {2.5,3.9,7.5,25.0} (SplitMix64 seed 1), 1e7 MicroWalk transitions "
             "per step from the centre node")
+WL = {
+    "C1": "C1 (BASELINE configs[0]): 21^3-node unit-pitch cube, eps 3.9 with one seeded eps 7.0 "
+          "inclusion box, 1e6 MicroWalk transitions per step from the centre node",
+    "C2": WORKLOAD,
+    "C3": "C3 (BASELINE configs[2]): two 100x100x5000 nm wires, 100 nm apart, 200 nm over a "
+          "2x2 um plane, 3 z layers, 20 nm eps 7.0 coatings; HYBRID-MW, N=24, Gaussian gap 0.5; "
+          "1e6 walks from wire 1",
+    "C4": "C4 (BASELINE configs[3]): 3-layer crossing bus (5 wires per layer), ILD 2.7/3.0/3.9, "
+          "10 nm eps 7.5 liners, 10 seeded LDE blocks; HYBRID-MW, N=24; master = middle wire of "
+          "the middle layer; walks until every coupling has relative SE < 1% (all-couplings rule)",
+    "C5": "C5 (BASELINE configs[4]): 200 box conductors in a 10x10x2 um world, 4 z layers, "
+          "20 nm coatings, 50 eps 25 blocks; HYBRID-MW, N=24; 10 masters x 1e7 walks = 1e8 walks",
+}
+# algorithmic on-chip bytes of one walk: 56 B per lattice
+# step actually taken (the 7-point f64 stencil read), 24 B per lattice jump
+# (a guide entry and two thresholds of its face law), 96 B per CDF
+# inversion (12 probes of 8 B: cached hops and the first transition) and
+# 32 B for the first transition's kernel/prob/eps reads
+B_STEP, B_JUMP, B_INV, B_FIRST = 56.0, 24.0, 96.0, 32.0
 
 
 def _clock_sampler(stop, out, index):
@@ -81,22 +110,31 @@ def _summarise_clocks(lines):
             "samples": len(sm)}
 
 
-def _profile_c2():
-    """the newest committed ncu --set full summary of the C2 MicroWalk kernel
-    (profiles/*ncu_full*.json): DRAM bytes per launch and shared-memory
-    wavefront-pipe utilisation, else {}"""
+def _profiles():
+    """committed ncu --set full summaries (profiles/*ncu_full*.json), newest
+    per (workload, kernel family)"""
     import glob
-    best = {}
+    out = {}
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json"))):
         try:
             d = json.load(open(p))
-            if d.get("kernel", "").startswith("mw_grid") and d.get("workload") == "C2":
-                best = d
         except Exception:
-            pass
-    return best
+            continue
+        out[(d.get("workload", "")[:2], d.get("kernel", "").split("<")[0])] = dict(d, file=p)
+    return out
 
 
+def _lscpu_model():
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# ----------------------------------------------------------------- CPU arms
 def _cpu_impl():
     from oracle.oracle import LIB_REF, Oracle, Ref
     if os.path.exists(LIB_REF):
@@ -104,10 +142,14 @@ def _cpu_impl():
     return Oracle(), "port"
 
 
-def cpu_calibrate(seconds):
+def _grid(name):
+    from paper_2507_09730_b200.workloads import c1_grid, c2_grid
+    return (c1_grid if name == "C1" else c2_grid)(1)
+
+
+def cpu_calibrate(name, seconds):
     """transits that take about `seconds` on all host threads"""
-    from paper_2507_09730_b200.workloads import c2_grid
-    eps, c, h, _ = c2_grid(1)
+    eps, c, h, _ = _grid(name)
     impl, _ = _cpu_impl()
     threads = os.cpu_count() or 1
     cal = 4000 * threads
@@ -118,24 +160,61 @@ def cpu_calibrate(seconds):
     return max(cal, int(cal * seconds / max(dt, 1e-3)))
 
 
-def cpu_baseline(seconds=12.0, sample=None):
+def cpu_baseline(name="C2", seconds=12.0, sample=None):
     """The reference's own microwalk_transit (oracle/_ref, verbatim sources)
     on all host threads over a bounded sample of the same workload."""
-    from paper_2507_09730_b200.workloads import c2_grid
-    eps, c, h, _ = c2_grid(1)
+    eps, c, h, _ = _grid(name)
     threads = os.cpu_count() or 1
     impl, kind = _cpu_impl()
     cal = 4000 * threads
     if sample is None:
-        sample = cpu_calibrate(seconds)
+        sample = cpu_calibrate(name, seconds)
     t0 = time.perf_counter()
     r = impl.microwalk_grid(eps, c, h, seed=1, stream0=cal, count=sample, threads=threads,
                             per_transit=False)
     dt = time.perf_counter() - t0
-    return dict(value=sample / dt, unit=UNIT, cores=threads, kind=kind,
-                sample=f"{sample} C2 transitions (SplitMix64(1, t) streams) on {threads} threads "
-                       f"in {dt:.1f} s; mean steps {r['step_sum'] / sample:.1f}",
+    return dict(value=sample / dt, unit=UNIT, cores=threads, kind=kind, cpu=_lscpu_model(),
+                sample=f"{sample} {name} transitions (SplitMix64(1, t) streams) on {threads} "
+                       f"threads in {dt:.1f} s; mean steps {r['step_sum'] / sample:.1f}",
                 steps_per_s=r["step_sum"] / dt)
+
+
+def walk_cpu_baseline(name, docs, cache_path, seconds=12.0, max_per_master=None, tol=None):
+    """The reference's own Engine::extract (oracle/_ref: engine.cpp,
+    microwalk.cpp, geometry.cpp, sgf_cache.cpp built from the reference
+    sources) on all host threads, HYBRID-MW, N=24, its StratifiedSgfCache
+    loaded from the device run's SGF1 file (the CLI's --cache): a warm table,
+    the reference's own solver fills any key the sample still misses.  A
+    bounded sample: walks per master sized to ~`seconds` in total."""
+    from oracle.oracle import LIB_REF, Ref
+    from tests.scenes import scene_from_doc
+    if not os.path.exists(LIB_REF):
+        return None
+    threads = os.cpu_count() or 1
+    R = Ref()
+    loaded = R.warm_cache_load(cache_path)  # untimed, like the CLI's --cache
+    hs = [R.structure(scene_from_doc(json.loads(d))) for d in docs]
+    kw = dict(mode="HYBRID-MW", grid_n=24, warm_cache=True)
+    hs[0].extract(threads=threads, min_walks=1024, max_walks=1024, seed=97, **kw)  # warm-up
+    probe = 4096
+    t0 = time.perf_counter()
+    hs[0].extract(threads=threads, min_walks=probe, max_walks=probe, seed=98, **kw)
+    dt = time.perf_counter() - t0
+    per = int(probe * seconds / max(dt, 1e-3) / len(hs)) // 1024 * 1024
+    per = max(1024, per if max_per_master is None else min(per, max_per_master))
+    walks = hits = misses = 0
+    t0 = time.perf_counter()
+    for h in hs:
+        r = h.extract(threads=threads, min_walks=per, max_walks=per, seed=1, **kw)
+        walks += r["walks"]
+        hits += r["cache_hits"]
+        misses += r["cache_misses"]
+    dt = time.perf_counter() - t0
+    return dict(value=walks / dt, unit="walks/s", cores=threads, kind="reference",
+                cpu=_lscpu_model(), cache_hits=hits, cache_misses=misses,
+                sample=f"{walks} {name} walks ({len(hs)} master(s) x {per}, HYBRID-MW, N=24, "
+                       f"the device run's {loaded} SGF entries preloaded) on {threads} threads in "
+                       f"{dt:.1f} s")
 
 
 def run_reference(args):
@@ -145,9 +224,9 @@ def run_reference(args):
     vals = []
     last = None
     per_step_s = min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps))
-    sample = cpu_calibrate(per_step_s)
+    sample = cpu_calibrate("C2", per_step_s)
     for i in range(args.warmup + args.steps):
-        b = cpu_baseline(sample=sample)
+        b = cpu_baseline("C2", sample=sample)
         if i >= args.warmup:
             vals.append(b["value"])
             last = b
@@ -163,199 +242,15 @@ def run_reference(args):
     return 0
 
 
-def walk_cpu_baseline(doc, seconds=12.0):
-    """The reference's own Engine::extract (oracle/_ref: engine.cpp,
-    microwalk.cpp, geometry.cpp, sgf_cache.cpp built from the reference
-    sources) on all host threads, C3, HYBRID-MW, warm SGF cache."""
-    from oracle.oracle import LIB_REF, Oracle, Ref
-    from tests.scenes import scene_from_doc
-    threads = os.cpu_count() or 1
-    sc = scene_from_doc(json.loads(doc))
-    kw = dict(mode="HYBRID-MW", grid_n=24)
-    if os.path.exists(LIB_REF):
-        h, kind = Ref().structure(sc), "reference"
-        run = lambda n, seed: h.extract(threads=threads, warm_cache=True, min_walks=n,  # noqa
-                                        max_walks=n, seed=seed, **kw)
-    else:
-        O, kind = Oracle(), "port"
-        run = lambda n, seed: O.extract(sc, threads=threads, min_walks=n, max_walks=n,  # noqa
-                                        seed=seed, **kw)
-    run(2048, 99)  # warm the SGF cache
-    t0 = time.perf_counter()
-    run(1024, 98)
-    dt = time.perf_counter() - t0
-    n = max(1024, int(1024 * seconds / max(dt, 1e-3)) // 1024 * 1024)
-    t0 = time.perf_counter()
-    run(n, 1)
-    dt = time.perf_counter() - t0
-    return dict(value=n / dt, unit="walks/s", cores=threads, kind=kind,
-                sample=f"{n} C3 walks (HYBRID-MW, N=24, warm SGF cache) on {threads} threads "
-                       f"in {dt:.1f} s")
-
-
-def walk_engine_bench(args, rank, world, dist, torch):
-    """FRW walks/s (the metric's first half) on C3 through the drop-in API
-    extract_json: a warm-up call fills the stratified-SGF table, then each
-    timed call runs `walks` fresh walks (seed = step + rank: independent
-    streams per rank); per-rank tallies are combined with one NCCL
-    all-reduce.  `value` is device time of the walk launches (CUDA events
-    inside frw_run_walks), `e2e` the wall time of the public call (its
-    inputs: the structure JSON; its outputs: 32-B per-walk records, folded
-    on the host)."""
-    import paper_2507_09730_b200.frwcap as frwcap
-    from paper_2507_09730_b200.workloads import c3_structure
-    doc = json.dumps(c3_structure())
-    W = args.walks
-    kw = dict(mode="HYBRID-MW", min_walks=W, max_walks=W, device=torch.cuda.current_device())
-    frwcap.extract_json(doc, seed=10_000 + rank, **kw)  # warm the SGF table
-    dev_s, wall_s, res = 0.0, 0.0, None
-    for i in range(args.walk_steps):
-        t0 = time.perf_counter()
-        res = frwcap.extract_json(doc, seed=1 + i * 1000 + rank, **kw)
-        wall_s += time.perf_counter() - t0
-        dev_s += res["t_device_seconds"]
-    sums = torch.tensor([t["capacitance_farads"] * res["walks"] for t in res["terminals"]] +
-                        [dev_s, wall_s], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        mx = sums[-2:].clone()
-        dist.all_reduce(sums)
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sums[-2:] = mx
-    dev_s, wall_s = float(sums[-2]), float(sums[-1])
-    total = world * W * args.walk_steps
-    ids = [t["conductor_id"] for t in res["terminals"]]
-    return {"metric": "frw_walks_per_s", "unit": "walks/s",
-            "value": total / dev_s, "e2e": {"value": total / wall_s, "unit": "walks/s",
-                                            "h2d_bytes_per_step": len(doc),
-                                            "d2h_bytes_per_step": 32 * W},
-            "config": {"workload": "C3 (BASELINE configs[2]): two 100x100x5000 nm wires, 100 nm "
-                                   "apart, 200 nm over a 2x2 um plane, 3 z layers, 20 nm coatings; "
-                                   "HYBRID-MW, N=24, Gaussian gap 0.5", "walks_per_rank_per_step": W,
-                       "steps": args.walk_steps, "sgf_table": "warm (filled by a warm-up call)"},
-            "capacitance_aF_rank0_last": dict(zip(map(str, ids),
-                                                  [round(t["capacitance_farads"] * 1e18, 3)
-                                                   for t in res["terminals"]])),
-            "cpu_baseline": walk_cpu_baseline(doc) if (world == 1 and not args.no_cpu_baseline)
-            else None,
-            "dispatch_rank0_last": res["dispatch_stats"], "mw_steps_per_walk":
-                res["mw_steps"] / res["walks"], "t_mw_fraction": res["t_mw_seconds"] /
-                max(res["t_device_seconds"], 1e-12)}
-
-
-def walk_engine_c5(args, rank, world, dist, torch):
-    """FRW walks/s on C5 (BASELINE configs[4], the 1/2/4/8-GPU scaling
-    workload): 10 masters x 1e7 walks = 1e8 walks in total, split evenly over
-    the ranks (strong scaling); each rank runs its share of every master with
-    its own seed through extract_json, and the per-master rows are combined
-    with one all-reduce of (sum, sum of squares, walks).  Timed: the wall
-    time of the public calls (and the device time inside them), max over
-    ranks.  A warm-up pass of 2^18 walks per master fills the SGF table."""
-    import paper_2507_09730_b200.frwcap as frwcap
-    from paper_2507_09730_b200.workloads import c5_structure
-    c5 = c5_structure()
-    masters = [c["id"] for c in c5["conductors"]][:10]
-    per = args.c5_walks // len(masters) // world
-    kw = dict(mode="HYBRID-MW", device=torch.cuda.current_device())
-    docs = {}
-    for mid in masters:
-        c5["master"] = mid
-        docs[mid] = json.dumps(c5)
-        frwcap.extract_json(docs[mid], min_walks=1 << 18, max_walks=1 << 18,
-                            seed=50_000 + 100 * rank + mid, **kw)
-    if dist is not None:
-        dist.barrier()
-    dev_s = wall_s = 0.0
-    rows = {}
-    for mid in masters:
-        t0 = time.perf_counter()
-        r = frwcap.extract_json(docs[mid], min_walks=per, max_walks=per,
-                                seed=1 + 1000 * rank + mid, **kw)
-        wall_s += time.perf_counter() - t0
-        dev_s += r["t_device_seconds"]
-        rows[mid] = r
-    nt = len(rows[masters[0]]["terminals"])
-    # per master: sum (= mean * walks) and sum of squares rebuilt from the SE
-    acc = []
-    for mid in masters:
-        w = rows[mid]["walks"]
-        for t in rows[mid]["terminals"]:
-            m, se = t["capacitance_farads"], t["std_err_farads"]
-            acc += [m * w, (se * se * w * (w - 1)) + m * m * w]
-        acc.append(w)
-    red = torch.tensor(acc, dtype=torch.float64, device="cuda")
-    tm = torch.tensor([dev_s, wall_s], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(red)
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    red = red.cpu().numpy()
-    dev_s, wall_s = float(tm[0]), float(tm[1])
-    out_rows = {}
-    k = 0
-    for mid in masters:
-        sums = red[k:k + 2 * nt].reshape(nt, 2)
-        w = red[k + 2 * nt]
-        k += 2 * nt + 1
-        ids = [t["conductor_id"] for t in rows[mid]["terminals"]]
-        mean = sums[:, 0] / w
-        se = np.sqrt(np.maximum(0.0, (sums[:, 1] - sums[:, 0] ** 2 / w) / (w - 1)) / w)
-        i_self = ids.index(mid)
-        out_rows[str(mid)] = {"self_aF": round(mean[i_self] * 1e18, 4),
-                              "self_rel_se": float(se[i_self] / mean[i_self]),
-                              "ground_aF": round(mean[ids.index(-1)] * 1e18, 4),
-                              "sum_abs_couplings_aF": round(float(np.sum(np.abs(
-                                  [mean[j] for j, c in enumerate(ids) if c not in (mid, -1)])))
-                                  * 1e18, 4)}
-    total = per * world * len(masters)
-    return {"metric": "frw_walks_per_s", "unit": "walks/s", "value": total / dev_s,
-            "e2e": {"value": total / wall_s, "unit": "walks/s",
-                    "h2d_bytes_per_step": sum(len(d) for d in docs.values()),
-                    "d2h_bytes_per_step": 32 * per * len(masters)},
-            "scaling": "strong",
-            "config": {"workload": "C5 (BASELINE configs[4]): 200 box conductors in a 10x10x2 um "
-                                   "world, 4 z layers, 20 nm coatings, 50 high-k blocks; "
-                                   "HYBRID-MW, N=24; 10 masters x 1e7 walks = 1e8 walks in total",
-                       "walks_total": total, "walks_per_rank_per_master": per,
-                       "parallelism": f"dp{world} (walk ranges per rank, one all-reduce of the "
-                                      "per-master tallies)",
-                       "sgf_table": "warm (2^18 walks per master first)"},
-            "rows": out_rows}
-
-
-def _profile_walk():
-    """the committed ncu --set full summary of the walk engine's largest
-    kernel on C3 (profiles/r01_ncu_full_c3_ktail.json), else {}"""
-    try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full_c3_ktail.json")))
-    except Exception:
-        return {}
-
-
-def run_gpu(args):
-    import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    # FRW_DIST_BACKEND=gloo (with ranks folded onto the visible devices) is a
-    # smoke test of the launch/reduction path on a one-GPU box; the bench
-    # itself is one rank per GPU over NCCL
-    backend = os.environ.get("FRW_DIST_BACKEND", "nccl")
-    if backend != "nccl":
-        local = local % torch.cuda.device_count()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    else:
-        torch.cuda.set_device(local)
-
+# ----------------------------------------------------------- single cube (C1/C2)
+def grid_config(name, count, args, rank, world, dist, torch, local, smem_peak, prof,
+                clocks_out=None):
+    """Device-timed transits of one single-cube config: `steps` steps of
+    `count` transits per rank (Philox, disjoint stream ranges per rank), L2
+    flushed between timed steps, one all-reduce of histogram+moments per
+    step; then the e2e loop through the C ABI with host buffers."""
     from paper_2507_09730_b200 import capi
-    from paper_2507_09730_b200.workloads import c2_grid
-
-    eps, c, h, _ = c2_grid(1)
+    eps, c, h, _ = _grid(name)
     n = round(len(eps) ** (1 / 3))
     bins = 6 * n * n
     ctx = capi.Context(local)
@@ -363,19 +258,15 @@ def run_gpu(args):
     ctx.L.frw_set_stream(ctx.h, stream.cuda_stream)
     ctx.upload_grid(eps, c, h)
     info = ctx.grid_info()
-
-    # device-resident outputs: histogram + 3 moments in one tensor so a single
-    # all-reduce combines ranks
     tally = torch.zeros(bins + 4, dtype=torch.int64, device="cuda")
     hist_ptr = tally.data_ptr()
     mom_ptr = hist_ptr + bins * 8
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
-    per = args.count
 
     def step(i):
         tally.zero_()
-        ctx.microwalk_batch_dev(per, hist_ptr, mom_ptr, seed=1 + i,
-                                stream_begin=rank * per, rng=capi.RNG_PHILOX)
+        ctx.microwalk_batch_dev(count, hist_ptr, mom_ptr, seed=1 + i, stream_begin=rank * count,
+                                rng=capi.RNG_PHILOX)
         if dist is not None:
             dist.all_reduce(tally)
 
@@ -383,17 +274,17 @@ def run_gpu(args):
         step(i)
     ctx.check()
     torch.cuda.synchronize()
-
     stop = threading.Event()
     clock_lines = []
-    th = threading.Thread(target=_clock_sampler, args=(stop, clock_lines, local), daemon=True)
-    th.start()
-    time.sleep(0.3)
+    th = None
+    if clocks_out is not None:
+        th = threading.Thread(target=_clock_sampler, args=(stop, clock_lines, local), daemon=True)
+        th.start()
+        time.sleep(0.3)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     evs = []
-    steps_total = 0
     for i in range(args.steps):
         flush.fill_(i)  # evict L2 between timed steps (outside the events)
         e0 = torch.cuda.Event(enable_timing=True)
@@ -406,20 +297,18 @@ def run_gpu(args):
     if dist is not None:
         dist.barrier()
     stop.set()
+    if clocks_out is not None:
+        clocks_out.update(_summarise_clocks(clock_lines))
     ctx.check()
-    ms = [a.elapsed_time(b) for a, b in evs]
-    t_ms = float(sum(ms))
+    t_ms = float(sum(a.elapsed_time(b) for a, b in evs))
     mom = tally[bins:bins + 3].cpu().numpy()
     hist_total = int(tally[:bins].sum().item())
-    steps_total = int(mom[0])  # last step, all ranks
     if dist is not None:
         tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
-    value = world * per * args.steps / (t_ms * 1e-3)
-
-    # kernel-only launch time of the dominant kernel on this rank (no flush,
-    # no all-reduce): average over a few launches for the roofline
+    value = world * count * args.steps / (t_ms * 1e-3)
+    # kernel-only launch time (no flush, no all-reduce), for the roofline
     kms = []
     for i in range(3):
         flush.fill_(i)
@@ -427,133 +316,368 @@ def run_gpu(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ctx.microwalk_batch_dev(per, hist_ptr, mom_ptr, seed=1000 + i,
-                                stream_begin=rank * per, rng=capi.RNG_PHILOX)
+        ctx.microwalk_batch_dev(count, hist_ptr, mom_ptr, seed=1000 + i,
+                                stream_begin=rank * count, rng=capi.RNG_PHILOX)
         e1.record(stream)
         torch.cuda.synchronize()
         kms.append(e0.elapsed_time(e1))
     k_ms = float(np.mean(kms))
     k_steps = int(tally[bins].item())
-    clocks = _summarise_clocks(clock_lines)
+    # e2e through the C ABI with host buffers: compile + upload the cube and
+    # copy histogram/moments back, every step
+    ctx2 = capi.Context(local)
+    eps_pinned = torch.from_numpy(eps).pin_memory().numpy()
+    t_e = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ctx2.upload_grid(eps_pinned, c, h)
+        ctx2.microwalk_batch(count, seed=1 + i, stream_begin=rank * count, rng=capi.RNG_PHILOX)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            t_e.append(t1 - t0)
+    h2d = ctx2.grid_info()["h2d_bytes"]
+    ctx2.close()
+    e_s = float(sum(t_e))
+    if dist is not None:
+        tt = torch.tensor([e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_s = float(tt.item())
+    pr = prof.get((name, "mw_grid_fast")) or prof.get((name, "mw_grid_kernel")) or {}
+    achieved = BYTES_PER_STEP * k_steps / (k_ms * 1e-3) / 1e9
+    traffic = pr.get("dram_bytes_per_launch")
+    if traffic is not None and pr.get("transits"):
+        traffic = traffic * count / pr["transits"]
+    ctx.close()
+    return {
+        "workload": WL[name], "metric": METRIC, "unit": UNIT, "value": value,
+        "ms_per_step": t_ms / args.steps, "steps": args.steps, "warmup": args.warmup,
+        "transitions_per_rank_per_step": count, "mean_steps": k_steps / count,
+        "hist_check": hist_total == world * count, "stencil_records": info["records"],
+        "smem_bytes": info["smem_bytes"],
+        "e2e": {"value": world * count * args.steps / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": bins * 8 + 3 * 8 + 4},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak / 1e9,
+                     "unit": "GB/s", "frac": achieved * 1e9 / smem_peak, "traffic": traffic,
+                     "kernel": "mw_grid_fast<PHILOX>", "kernel_ms": k_ms,
+                     "algorithmic_bytes_per_launch": BYTES_PER_STEP * k_steps,
+                     "steps_per_s": k_steps / (k_ms * 1e-3),
+                     "peak_source": "frw_smem_bandwidth_probe (conflict-free LDS.128, all SMs), "
+                                    "measured in this run",
+                     "smem_wavefront_pipe_frac": pr.get("smem_wavefront_pipe_frac"),
+                     "ncu_profile": os.path.basename(pr["file"]) if pr else None},
+    }
 
-    # end-to-end through the C ABI with host buffers: upload the cube
-    # (compile + H2D) and copy histogram/moments back, every step
-    e2e_v = None
-    h2d = d2h = None
-    if True:  # every rank: e2e is max over ranks
-        ctx2 = capi.Context(local)
-        eps_pinned = torch.from_numpy(eps).pin_memory().numpy()
-        t_e = []
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            ctx2.upload_grid(eps_pinned, c, h)
-            ctx2.microwalk_batch(per, seed=1 + i, stream_begin=rank * per, rng=capi.RNG_PHILOX)
-            t1 = time.perf_counter()
-            if i >= args.warmup:
-                t_e.append(t1 - t0)
-        gi = ctx2.grid_info()
-        h2d = gi["h2d_bytes"]
-        d2h = bins * 8 + 3 * 8 + 4
-        e_s = float(sum(t_e))
+
+# ------------------------------------------------------------- walk engine
+def _walk_roofline(stats, walks, walks_per_s, smem_peak, prof, name):
+    """algorithmic on-chip bytes per walk (B_* above) x device walks/s
+    against the measured shared-memory bandwidth"""
+    d = stats["dispatch_stats"]
+    inv = d["subsequent"]["cached"] + sum(d["first"].values())
+    taken = stats["mw_steps"] - stats["mw_jump_steps"]
+    bpw = (B_STEP * taken + B_JUMP * stats["mw_jumps"] + B_INV * inv) / walks + B_FIRST
+    ach = bpw * walks_per_s / 1e9
+    pr = None
+    for key in ((name, "k_tail"), ("C3", "k_tail")):
+        if key in prof:
+            pr = prof[key]
+            break
+    traffic = None
+    if pr and pr.get("dram_bytes_per_walk") is not None:
+        traffic = pr["dram_bytes_per_walk"]
+    m = (pr or {}).get("metrics", {})
+
+    def _num(k):
+        try:
+            return float(str(m[k]).split()[0])
+        except Exception:
+            return None
+
+    return {"bound": "smem", "achieved": ach, "peak": smem_peak / 1e9, "unit": "GB/s",
+            "frac": ach * 1e9 / smem_peak, "traffic": traffic,
+            "traffic_unit": "DRAM bytes per walk of the dominant kernel (ncu --set full)",
+            "algorithmic_bytes_per_walk": bpw,
+            "steps_taken_per_walk": taken / walks,
+            "steps_substituted_by_jumps_per_walk": stats["mw_jump_steps"] / walks,
+            "jumps_per_walk": stats["mw_jumps"] / walks,
+            "cdf_inversions_per_walk": inv / walks,
+            "note": "whole engine (all walk kernels) over device time; bytes count the reference "
+                    "work actually done (56 B per lattice step taken, 24 B per lattice jump, "
+                    "96 B per CDF inversion, 32 B per first transition).  The engine is bound by "
+                    "instruction issue under SIMT divergence, not by bytes: issue_* are the "
+                    "committed ncu capture of its largest kernel",
+            "ncu_profile": os.path.basename(pr["file"]) if pr else None,
+            "issue_kernel": (pr or {}).get("kernel"),
+            "issue_active_frac": (_num("smsp__issue_active.avg.pct_of_peak_sustained_active") or 0)
+            / 100 if m else None,
+            "issue_active_lanes_per_inst": _num("smsp__thread_inst_executed_per_inst_executed.ratio"),
+            "issue_top_stalls": (pr or {}).get("top_stalls_per_issue")}
+
+
+def _sum_stats(rs):
+    out = {"mw_steps": 0, "mw_jump_steps": 0, "mw_jumps": 0,
+           "dispatch_stats": {"first": {}, "subsequent": {}}}
+    for r in rs:
+        for k in ("mw_steps", "mw_jump_steps", "mw_jumps"):
+            out[k] += int(r.get(k, 0))
+        for g in ("first", "subsequent"):
+            for k, v in r["dispatch_stats"][g].items():
+                out["dispatch_stats"][g][k] = out["dispatch_stats"][g].get(k, 0) + int(v)
+    return out
+
+
+def _max_over_ranks(dist, torch, vals):
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
+def walk_c3(args, rank, world, dist, torch, smem_peak, prof, cpu):
+    """C3 at its stated size: 1e6 walks per step (strong scaling over the
+    ranks through dist.extract_sharded; one rank: the drop-in extract_json),
+    `walk_steps` timed steps after one warm-up call that fills the table."""
+    import paper_2507_09730_b200.frwcap as frwcap
+    from paper_2507_09730_b200 import dist as pdist
+    from paper_2507_09730_b200.workloads import c3_structure
+    doc = json.dumps(c3_structure())
+    W = args.walks
+    dev = torch.cuda.current_device()
+    kw = dict(mode="HYBRID-MW", device=dev)
+    frwcap.sgf_cache_clear()
+
+    def run(seed):
+        if world == 1:
+            return frwcap.extract_json(doc, min_walks=W, max_walks=W, seed=seed, **kw)
+        return pdist.extract_sharded(doc, W, seed=seed, **kw)
+
+    run(10_000)  # warm the SGF table
+    cold_misses = frwcap.sgf_cache_stats()["misses"]
+    dev_s = wall_s = 0.0
+    rs = []
+    for i in range(args.walk_steps):
         if dist is not None:
-            tt = torch.tensor([e_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_s = float(tt.item())
-        e2e_v = world * per * args.steps / e_s
-        ctx2.close()
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = run(1 + i * 1000)
+        wall_s += time.perf_counter() - t0
+        dev_s += r["t_device_seconds"]
+        rs.append(r)
+    dev_s, wall_s = _max_over_ranks(dist, torch, [dev_s, wall_s])
+    total = W * args.walk_steps
+    res = rs[-1]
+    st = _sum_stats(rs)
+    out = {"workload": WL["C3"], "metric": "frw_walks_per_s", "unit": "walks/s",
+           "value": total / dev_s, "steps": args.walk_steps, "warmup": 1,
+           "scaling": "strong", "walks_per_step": W,
+           "e2e": {"value": total / wall_s, "unit": "walks/s",
+                   "h2d_bytes_per_step": len(doc),
+                   "d2h_bytes_per_step": 32 * W if world == 1 else 8 * (3 * 4 + 12)},
+           "capacitance_aF": {str(t["conductor_id"]): round(t["capacitance_farads"] * 1e18, 3)
+                              for t in res["terminals"]},
+           "rel_se_self": res["terminals"][0]["std_err_farads"] /
+           res["terminals"][0]["capacitance_farads"],
+           "dispatch_last": res["dispatch_stats"],
+           "cache_device": {"hits_last_step": res.get("cache", {}).get("hits"),
+                            "misses_last_step": res.get("cache", {}).get("misses"),
+                            "misses_warmup": cold_misses},
+           "mw_steps_per_walk": st["mw_steps"] / total,
+           "t_mw_fraction": res["t_mw_seconds"] / max(res["t_device_seconds"], 1e-12),
+           "sgf_table": "warm (filled by one warm-up call)",
+           "l2": "the walk-slot pool (GBs) exceeds L2"}
+    out["roofline"] = _walk_roofline(st, total, out["value"], smem_peak, prof, "C3")
+    if cpu:
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "c3.sgf")
+            frwcap.sgf_cache_save(path)
+            out["cpu_baseline"] = walk_cpu_baseline("C3", [doc], path, seconds=args.ref_seconds)
+    return out
 
-    walks = None if args.no_walks else walk_engine_bench(args, rank, world, dist, torch)
-    walks_c5 = None if (args.no_walks or args.c5_walks <= 0) else \
-        walk_engine_c5(args, rank, world, dist, torch)
+
+def walk_c4(args, rank, world, dist, torch, smem_peak, prof, cpu):
+    """C4 until every coupling has 1% relative SE (the all-couplings rule,
+    a Config mode: the reference stops on self + largest coupling,
+    engine.cpp:402-420).  One GPU (the rule is checked after every reference
+    batch of the walk-order fold); other ranks report nothing."""
+    if rank != 0:
+        return None
+    import paper_2507_09730_b200.frwcap as frwcap
+    from paper_2507_09730_b200.workloads import c4_structure
+    doc = json.dumps(c4_structure())
+    kw = dict(mode="HYBRID-MW", device=torch.cuda.current_device(), tol=0.01,
+              all_couplings=True, min_walks=4096, max_walks=200_000_000)
+    frwcap.sgf_cache_clear()
+    frwcap.extract_json(doc, mode="HYBRID-MW", device=torch.cuda.current_device(),
+                        min_walks=1 << 20, max_walks=1 << 20, seed=77)  # warm the table
+    t0 = time.perf_counter()
+    r = frwcap.extract_json(doc, seed=5, **kw)
+    wall = time.perf_counter() - t0
+    w = r["walks"]
+    st = _sum_stats([r])
+    ids = [t["conductor_id"] for t in r["terminals"]]
+    worst = max((t["std_err_farads"] / abs(t["capacitance_farads"]))
+                for t in r["terminals"] if t["conductor_id"] != -1 and t["capacitance_farads"])
+    out = {"workload": WL["C4"], "metric": "frw_walks_per_s", "unit": "walks/s",
+           "value": w / r["t_device_seconds"], "walks": w, "converged": r["converged"],
+           "device_seconds": r["t_device_seconds"], "wall_seconds": wall,
+           "worst_coupling_rel_se": worst, "n_gpus_used": 1,
+           "e2e": {"value": w / wall, "unit": "walks/s", "h2d_bytes_per_step": len(doc),
+                   "d2h_bytes_per_step": 32 * w},
+           "capacitance_aF": {str(i): round(t["capacitance_farads"] * 1e18, 4)
+                              for i, t in zip(ids, r["terminals"])},
+           "sgf_table": "warm (filled by a 2^20-walk warm-up call)"}
+    out["roofline"] = _walk_roofline(st, w, out["value"], smem_peak, prof, "C4")
+    if cpu:
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "c4.sgf")
+            frwcap.sgf_cache_save(path)
+            out["cpu_baseline"] = walk_cpu_baseline("C4", [doc], path, seconds=args.ref_seconds)
+            if out["cpu_baseline"]:
+                cb = out["cpu_baseline"]
+                cb["seconds_for_the_gpu_walk_count_extrapolated"] = w / cb["value"]
+    return out
+
+
+def walk_c5(args, rank, world, dist, torch, smem_peak, prof, cpu):
+    """C5, the scaling workload: 10 masters x 1e7 walks = 1e8 walks, each
+    master one walk sequence split into contiguous ranges over the ranks
+    (dist.extract_sharded: frw_run_walks per range, one frw_tally_allreduce
+    per master over NCCL).  Device and wall time max over ranks.  A warm-up
+    pass of 2^18 walks per master fills the SGF table."""
+    import paper_2507_09730_b200.frwcap as frwcap
+    from paper_2507_09730_b200 import dist as pdist
+    from paper_2507_09730_b200.workloads import c5_structure
+    c5 = c5_structure()
+    masters = [c["id"] for c in c5["conductors"]][:10]
+    per_master = args.c5_walks // len(masters)
+    dev = torch.cuda.current_device()
+    kw = dict(mode="HYBRID-MW", device=dev)
+    docs = {}
+    frwcap.sgf_cache_clear()
+    for mid in masters:
+        c5["master"] = mid
+        docs[mid] = json.dumps(c5)
+        pdist.extract_sharded(docs[mid], 1 << 18, seed=50_000 + mid, **kw)
+    if dist is not None:
+        dist.barrier()
+    dev_s = wall_s = 0.0
+    rows, rs = {}, []
+    for mid in masters:
+        t0 = time.perf_counter()
+        r = pdist.extract_sharded(docs[mid], per_master, seed=1 + mid, **kw)
+        wall_s += time.perf_counter() - t0
+        dev_s += r["t_device_seconds"]
+        rs.append(r)
+        ids = [t["conductor_id"] for t in r["terminals"]]
+        mean = {i: t["capacitance_farads"] for i, t in zip(ids, r["terminals"])}
+        se = {i: t["std_err_farads"] for i, t in zip(ids, r["terminals"])}
+        rows[str(mid)] = {"self_aF": round(mean[mid] * 1e18, 4),
+                          "self_rel_se": se[mid] / mean[mid],
+                          "ground_aF": round(mean[-1] * 1e18, 4),
+                          "sum_abs_couplings_aF": round(sum(abs(v) for i, v in mean.items()
+                                                            if i not in (mid, -1)) * 1e18, 4)}
+    dev_s, wall_s = _max_over_ranks(dist, torch, [dev_s, wall_s])
+    total = per_master * len(masters)
+    st = _sum_stats(rs)
+    out = {"workload": WL["C5"], "metric": "frw_walks_per_s", "unit": "walks/s",
+           "value": total / dev_s, "scaling": "strong", "walks_total": total,
+           "walks_per_master": per_master,
+           "parallelism": f"dp{world}: contiguous walk ranges of one sequence per master, one "
+                          "frw_tally_allreduce (ncclAllReduce) per master" if world > 1 else
+                          "one GPU",
+           "e2e": {"value": total / wall_s, "unit": "walks/s",
+                   "h2d_bytes_per_step": sum(len(d) for d in docs.values()),
+                   "d2h_bytes_per_step": 8 * len(masters) * (3 * 201 + 12)},
+           "sgf_table": "warm (2^18 walks per master first)", "rows": rows}
+    out["roofline"] = _walk_roofline(st, total, out["value"], smem_peak, prof, "C5")
+    if cpu:
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "c5.sgf")
+            frwcap.sgf_cache_save(path)
+            out["cpu_baseline"] = walk_cpu_baseline(
+                "C5", [docs[m] for m in masters], path, seconds=args.ref_seconds,
+                max_per_master=10_000)
+    return out
+
+
+# -------------------------------------------------------------------- main
+def run_gpu(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    # FRW_DIST_BACKEND=gloo (ranks folded onto the visible devices) is a smoke
+    # test of the launch/reduction path on a one-GPU box; the bench itself is
+    # one rank per GPU over NCCL
+    backend = os.environ.get("FRW_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    from paper_2507_09730_b200 import capi
+    probe = capi.Context(local)
+    smem_peak = probe.smem_bandwidth()
+    name = probe.name
+    probe.close()
+    prof = _profiles()
+    cpu = world == 1 and rank == 0 and not args.no_cpu_baseline
+
+    clocks = {}
+    c2 = grid_config("C2", args.count, args, rank, world, dist, torch, local, smem_peak, prof,
+                     clocks_out=clocks)
+    configs = {"C2": c2}
+    if not args.headline_only:
+        configs["C1"] = grid_config("C1", args.c1_count, args, rank, world, dist, torch, local,
+                                    smem_peak, prof)
+        configs["C3"] = walk_c3(args, rank, world, dist, torch, smem_peak, prof, cpu)
+        configs["C4"] = walk_c4(args, rank, world, dist, torch, smem_peak, prof, cpu)
+        if args.c5_walks > 0:
+            configs["C5"] = walk_c5(args, rank, world, dist, torch, smem_peak, prof, cpu)
+    if cpu:
+        configs["C2"]["cpu_baseline"] = cpu_baseline("C2", seconds=args.ref_seconds)
+        if "C1" in configs:
+            configs["C1"]["cpu_baseline"] = cpu_baseline("C1", seconds=args.ref_seconds)
 
     if rank != 0:
         if dist is not None:
             dist.barrier()
             dist.destroy_process_group()
         return 0
-
-    smem_peak = ctx.smem_bandwidth()
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    achieved = BYTES_PER_STEP * k_steps / (k_ms * 1e-3) / 1e9
-    prof = _profile_c2()
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "transitions_per_rank_per_step": per,
+        "metric": METRIC, "value": c2["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": c2["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "transitions_per_rank_per_step": args.count,
                    "rng": "philox4x32-10 keyed (seed, transit, step)",
                    "l2": "flushed between timed steps (256 MiB write outside the events); the "
                          "stencil table is re-staged into shared memory by every launch",
                    "parallelism": f"dp{world} (disjoint transit streams, NCCL all-reduce of "
                                   "histogram+moments per step)",
-                   "stencil_records": info["records"], "smem_bytes": info["smem_bytes"],
-                   "mean_steps": k_steps / per, "hist_check": hist_total == world * per},
-        "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
-        "gpu_launches": args.steps,
-        "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak / 1e9,
-                     "unit": "GB/s", "frac": achieved * 1e9 / smem_peak,
-                     "traffic": prof.get("dram_bytes_per_launch"),
-                     "kernel": "mw_grid_fast<PHILOX>", "kernel_ms": k_ms,
-                     "algorithmic_bytes_per_launch": BYTES_PER_STEP * k_steps,
-                     "peak_source": "frw_smem_bandwidth_probe (conflict-free LDS.128, all SMs), "
-                                    "measured in this run",
-                     "hbm_equiv_frac": achieved / hbm,
-                     "hbm_peak_gbs": hbm, "steps_per_s": k_steps / (k_ms * 1e-3),
-                     "note": "achieved counts the reference's f64 7-point stencil read (56 B "
-                             "per step, SURVEY.md §8(d)); the kernel instead gathers one 2-B "
-                             "map entry and one 8-B record per step, so frac can pass 1.  The "
-                             "binding resource is the shared-memory data pipe: random gathers "
-                             "cost ~10 wavefronts per warp-step (bank conflicts); "
-                             "smem_wavefront_pipe_frac is its utilisation (1 wavefront/clk/SM) "
-                             "in the committed ncu capture",
-                     "smem_wavefront_pipe_frac": prof.get("smem_wavefront_pipe_frac")},
+                   "stencil_records": c2["stencil_records"], "smem_bytes": c2["smem_bytes"],
+                   "mean_steps": c2["mean_steps"], "hist_check": c2["hist_check"]},
+        "e2e": c2["e2e"],
+        "gpu_launches": c2["gpu_launches"],
+        "roofline": dict(c2["roofline"], note=(
+            "achieved counts the reference's f64 7-point stencil read (56 B per step, "
+            "SURVEY.md §8(d)); the kernel instead gathers one 2-B map entry and one 8-B record "
+            "per step, so frac can pass 1.  The binding resource is the shared-memory data pipe "
+            "(random gathers, bank conflicts): smem_wavefront_pipe_frac is its utilisation in "
+            "the committed ncu capture")),
         "clocks": clocks,
-        "device": ctx.name,
+        "device": name,
+        "configs": configs,
     }
-    if walks is not None:
-        # SURVEY.md §8(d) algorithmic bytes per walk: 56 B per MicroWalk step,
-        # 8 B x 12 per CDF inversion (cached hops and the first transition),
-        # 4 x 8 B for the first-transition kernel/prob/eps reads
-        d = walks["dispatch_rank0_last"]
-        inversions = (d["subsequent"]["cached"] + sum(d["first"].values())) / args.walks
-        bpw = 56.0 * walks["mw_steps_per_walk"] + 96.0 * inversions + 32.0
-        ach = bpw * walks["value"] / 1e9
-        pw = _profile_walk()
-        m = pw.get("metrics", {})
-
-        def _num(k):
-            try:
-                return float(str(m[k]).split()[0])
-            except Exception:
-                return None
-
-        walks["roofline"] = {"bound": "smem", "achieved": ach, "peak": smem_peak / 1e9,
-                             "unit": "GB/s", "frac": ach * 1e9 / smem_peak,
-                             "algorithmic_bytes_per_walk": bpw,
-                             "note": "whole engine (all walk kernels) over device time; the "
-                                     "geometry queries, table lookups and divergence are the "
-                                     "gap to the on-chip roofline.  The engine is bound by "
-                                     "instruction issue under SIMT divergence, not by bytes: "
-                                     "issue_* are the committed ncu capture of its largest "
-                                     "kernel (the run-to-completion tail)",
-                             "issue_kernel": pw.get("kernel"),
-                             "issue_active_frac": (_num("smsp__issue_active.avg."
-                                                        "pct_of_peak_sustained_active") or 0) / 100
-                             if m else None,
-                             "issue_active_lanes_per_inst": _num(
-                                 "smsp__thread_inst_executed_per_inst_executed.ratio"),
-                             "issue_top_stalls": pw.get("top_stalls_per_issue")}
-        out["walk_engine"] = walks
-    if walks_c5 is not None:
-        out["walk_engine_c5"] = walks_c5
-    if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(seconds=args.ref_seconds)
+    if cpu:
+        out["cpu_baseline"] = configs["C2"]["cpu_baseline"]
     print(json.dumps(out))
     if dist is not None:
         dist.barrier()
@@ -568,9 +692,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--count", type=int, default=COUNT)
+    ap.add_argument("--c1-count", type=int, default=1_000_000)
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-walks", action="store_true")
+    ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--walks", type=int, default=1_000_000)
     ap.add_argument("--walk-steps", type=int, default=3)
     ap.add_argument("--c5-walks", type=int, default=100_000_000)

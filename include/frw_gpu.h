@@ -221,6 +221,11 @@ typedef struct {
   double mw_ms;           /* device time of the MicroWalk kernel          */
   double total_ms;        /* device time of the whole call                */
   uint64_t mw_jumps;      /* MicroWalk lattice jumps (Philox mode)        */
+  uint64_t mw_jump_steps; /* lattice steps the jumps stand for (counted in
+                             mw_steps as E[tau]); steps actually taken =
+                             mw_steps - mw_jump_steps                      */
+  uint64_t mw_dense_hops; /* MicroWalk hops whose cube held more than 64
+                             boxes, run on a dense voxel grid             */
 } frw_tally;
 
 /* Per-walk outcome (Engine::WalkOut, engine.hpp:157-161, plus the walk's

@@ -390,10 +390,19 @@ class Ref:
         L.ref_run_walks_cache.argtypes = [C.c_void_p, _dp, _lp, C.c_uint64, C.c_int64, C.c_int,
                                           C.c_char_p, C.c_char_p, _ip, _dp, _bp]
         L.ref_cache_save.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_char_p]
+        L.ref_warm_cache_load.restype = C.c_int64
+        L.ref_warm_cache_load.argtypes = [C.c_char_p]
         L.ref_cache_load_probs.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, _dp, _lp]
 
     def err(self):
         return self.lib.ref_last_error().decode()
+
+    def warm_cache_load(self, path):
+        """SGF1 file into the process-wide cache of extract(warm_cache=True)"""
+        n = self.lib.ref_warm_cache_load(path.encode())
+        if n < 0:
+            raise RuntimeError(self.err())
+        return n
 
     def cache_save(self, n, axes, layers, path):
         """SGF1 file written by the reference's StratifiedSgfCache"""

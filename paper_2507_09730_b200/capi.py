@@ -79,7 +79,8 @@ class Tally(C.Structure):
                 ("mw_steps", C.c_uint64), ("restarts", C.c_uint64),
                 ("mw_general_steps", C.c_uint64), ("mw_cell_changes", C.c_uint64),
                 ("mw_ms", C.c_double),
-                ("total_ms", C.c_double), ("mw_jumps", C.c_uint64)]
+                ("total_ms", C.c_double), ("mw_jumps", C.c_uint64),
+                ("mw_jump_steps", C.c_uint64), ("mw_dense_hops", C.c_uint64)]
 
 
 WALK_RECORD = np.dtype([("weight", "<f8"), ("mw_steps", "<u8"), ("slot", "<i4"),
@@ -453,7 +454,8 @@ class Context:
                      first=list(t.first), sub=list(t.sub), misses=t.cache_misses,
                      mw_steps=t.mw_steps, restarts=t.restarts, mw_ms=t.mw_ms,
                      mw_general_steps=t.mw_general_steps, mw_cell_changes=t.mw_cell_changes,
-                     total_ms=t.total_ms, mw_jumps=t.mw_jumps)
+                     total_ms=t.total_ms, mw_jumps=t.mw_jumps,
+                     mw_jump_steps=t.mw_jump_steps, mw_dense_hops=t.mw_dense_hops)
         return tally, rec
 
     def smem_bandwidth(self, iters=4096):

@@ -351,8 +351,10 @@ WalkTally Engine::run_tally(uint64_t begin, int64_t count, bool allreduce) {
   w.walks = static_cast<uint64_t>(count);
   w.mw_ms = t.mw_ms;
   w.total_ms = t.total_ms;
-  w.mw_jumps = t.mw_jumps;
   if (allreduce) throw_status(ctx_, frw_tally_allreduce(ctx_, nullptr, &t));
+  w.mw_jumps = t.mw_jumps;
+  w.mw_jump_steps = t.mw_jump_steps;
+  w.mw_dense_hops = t.mw_dense_hops;
   w.aborted = t.aborted;
   w.resampled = t.resampled;
   w.mw_steps = t.mw_steps;
@@ -523,6 +525,8 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
       throw_status(L.ctx, L.rc);
       mw_ms += L.t.mw_ms;
       res.mw_jumps += L.t.mw_jumps;
+      res.mw_jump_steps += L.t.mw_jump_steps;
+      res.mw_dense_hops += L.t.mw_dense_hops;
     }
     {
       // device time of the wave: its slowest lane

@@ -376,6 +376,8 @@ struct CapacitanceResult {
   double t_total_seconds = 0;
   uint64_t mw_steps = 0;       // B200 extra: total lattice steps
   uint64_t mw_jumps = 0;       // B200 extra: lattice jumps (Philox mode)
+  uint64_t mw_jump_steps = 0;  // B200 extra: steps the jumps stand for (E[tau], in mw_steps)
+  uint64_t mw_dense_hops = 0;  // B200 extra: hops on a dense grid (> 64 boxes in the cube)
   double t_device_seconds = 0; // B200 extra: device time of the walk launches
   const TerminalEstimate* find_terminal(int conductor_id) const;
   const TerminalEstimate& self() const;
@@ -387,7 +389,8 @@ struct CapacitanceResult {
 struct WalkTally {
   std::vector<double> sum, sumsq;
   std::vector<uint64_t> landed;
-  uint64_t walks = 0, aborted = 0, resampled = 0, mw_steps = 0, mw_jumps = 0;
+  uint64_t walks = 0, aborted = 0, resampled = 0, mw_steps = 0, mw_jumps = 0, mw_jump_steps = 0,
+           mw_dense_hops = 0;
   uint64_t first[4] = {0, 0, 0, 0};  // DispatchStats order
   uint64_t sub[4] = {0, 0, 0, 0};    // cached, microwalk, microwalk_e, fdm
   double mw_ms = 0, total_ms = 0;

@@ -122,6 +122,8 @@ py::dict result_to_dict(const CapacitanceResult& r) {
   d["t_total_seconds"] = r.t_total_seconds;
   d["mw_steps"] = r.mw_steps;                   // B200 extra
   d["mw_jumps"] = r.mw_jumps;                   // B200 extra
+  d["mw_jump_steps"] = r.mw_jump_steps;         // B200 extra: steps the jumps stand for
+  d["mw_dense_hops"] = r.mw_dense_hops;         // B200 extra: hops with > 64 boxes in the cube
   d["t_device_seconds"] = r.t_device_seconds;   // B200 extra
   return d;
 }
@@ -312,6 +314,8 @@ PYBIND11_MODULE(_core, m) {
         d["sub"] = std::vector<uint64_t>(t.sub, t.sub + 4);
         d["mw_steps"] = t.mw_steps;
         d["mw_jumps"] = t.mw_jumps;
+        d["mw_jump_steps"] = t.mw_jump_steps;
+        d["mw_dense_hops"] = t.mw_dense_hops;
         d["t_mw_seconds"] = t.mw_ms * 1e-3;
         d["t_device_seconds"] = t.total_ms * 1e-3;
         py::list ids;

@@ -52,6 +52,8 @@ constexpr int NMAX = 64;    // lattice size cap (layers per key)
 constexpr int PMAX = 64;    // palettes up to PMAX classes keep the alpha table in shared memory
 constexpr int kClassMax = 0x7FFF;  // distinct permittivities (15-bit class ids)
 constexpr int kSlotsDefault = 1 << 20;
+constexpr int kMwSlice = 64;   // MicroWalk super-steps per hop and k_mw visit
+constexpr int kAdvSlice = 16;  // transitions per walk and k_advance visit
 constexpr int kGridMinConductors = 24;  // conductor bins above this count
 // Cell atlas of a MicroWalk job (u64 words per slot).  Along each axis the
 // clipped boxes' faces cut [0, n) into segments; bm[a] holds one bit per
@@ -68,7 +70,7 @@ constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
 
 
-enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3 };
+enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3, S_MW_CARRY = 4 };
 
 
 // ---------------------------------------------------------------------------
@@ -136,6 +138,7 @@ struct JumpMeta {
 struct DJump {
   int mmax;  // largest radius tabulated; < 2: jumps off
   int twice; // a second jump from words 2-3 of the block when it fits
+  int hom;   // jumps across homogeneous balls beyond the walker's cell (mw_hom_radius)
   const JumpMeta* meta;   // [mmax + 1]
   const uint64_t* thr;    // per radius: side^2 thresholds, last = UINT64_MAX
   const uint16_t* guide;  // per radius: 2^gbits first candidates
@@ -152,6 +155,9 @@ struct DParams {
   uint64_t walk_begin;
   long long count;
   int master;
+  // time slices of the wavefront rounds (0: unlimited): super-steps of one
+  // MicroWalk hop per k_mw visit, transitions of one walk per k_advance visit
+  int mw_slice, adv_slice;
 };
 
 struct WalkRec {  // per walk id, written once when the walk terminates
@@ -165,6 +171,9 @@ struct WalkRec {  // per walk id, written once when the walk terminates
 
 struct DSlots {
   int S;
+  int jtail;             // first job entry of the k_tail lanes (one per lane,
+                         // after the capacity's slots: compiled, walked and
+                         // re-compiled by the same lane, so they stay in L2)
   uint8_t* state;
   long long* wid;        // walk index relative to walk_begin
   double* p;             // [S][3]
@@ -178,10 +187,14 @@ struct DSlots {
   uint8_t* resampled;
   // MicroWalk job compiled by k_advance
   double* cube;          // [S][4] center, half width
-  uint8_t* nbox;         // [S] conductor boxes among the clipped boxes
+  uint16_t* nbox;        // [J] conductor boxes among the clipped boxes | boxes << 8
   uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class / conductor index
   uint64_t* atlas;       // [S][kAtlasWords] cell atlas of the job (see cell_info)
   uint8_t* mwkind;       // [S] 0 plain MicroWalk job, 1 expanded (MicroWalk-E), 2 FDM
+  // a MicroWalk hop carried to the next round (S_MW_CARRY): node, steps so far
+  uint32_t* mwnode;
+  int* mwhsteps;
+  uint64_t* mwhj;        // its homogeneous-radius bound: hom | hnode << 32
 };
 
 // Work queues of one round: k_spawn and the previous round's k_mw fill the
@@ -207,15 +220,21 @@ struct DCounters {
   // k_flow: ring heads/tails (ACTIVE, MicroWalk) and walks still in the flow
   unsigned long long fah, fat, fmh, fmt, flive;
   unsigned long long jumps;      // MicroWalk lattice jumps (Philox mode)
+  unsigned long long jsteps;     // lattice steps the jumps stand for (their E[tau])
+  unsigned long long q2len;      // MicroWalk queue of the next round (carried hops)
+  unsigned long long dqlen, dqhead;  // dense MicroWalk hops of this round (k_mw_dense)
+  unsigned long long dense_hops;     // dense hops run (all rounds)
 };
 
 constexpr int kMissMax = 4096;
+constexpr uint8_t kDense = 4, kDenseCond = 8;  // mwkind flags of a dense hop (k_mw_dense)
 struct DMiss {
   int* axis;        // [kMissMax]
   double* layers;   // [kMissMax][NMAX]
   long long* retry; // [2S] walk ids whose first transition missed (restart)
   long long* pend;  // [2S] walk ids to restart
   int* park;        // [2S] slots of walks parked mid-walk by a miss (resume)
+  int* dense;       // [S] slots whose MicroWalk hop needs the dense grid (k_mw_dense)
 };
 
 // ---------------------------------------------------------------------------
@@ -510,108 +529,238 @@ __device__ __forceinline__ double uniform(const DParams& P, long long wid, Rng& 
 // -2 (error: slice centre outside the world)
 __device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih);
 
-#ifndef FRW_UKEY
-#define FRW_UKEY 1  // uniform-key index for single-class cubes (advance_once)
-#endif
-// ucls (optional): when every slice has one palette class the key is that
-// class's uniform key; *ucls gets the class and `layers` is left unwritten
-// (the caller looks the key up through DSgf::uentry), else *ucls = -1
-__device__ int stratified_key(const DStruct& s, const double c[3], double h, int n,
-                              double* layers, int* ucls = nullptr) {
-  if (ucls) *ucls = -1;
+// The stratification probe of a transition cube, held in registers (no
+// per-slice arrays: the walk kernels keep no local memory on this path).
+// stratified_profile (geometry.cpp:357-396): the dielectric boxes meeting
+// the OPEN cube; the first axis whose cross-section every one of them
+// covers; the permittivity of slice t is that of the last-declared box whose
+// closed extent contains the slice centre c - h + (t + 0.5) pitch along the
+// axis (permittivity_at, geometry.cpp:47-55), else the background.  Along
+// the axis each box covers an interval of slices (clip_axis), so the profile
+// is a few (class, slice-bitmask) pairs: painting box q (in declaration
+// order) clears its slices from every pair and adds them to its class's
+// pair.  Structures whose stratified cubes meet more than kProfHits boxes or
+// kProfCls classes fall back to classifying slice centres one by one.
+constexpr int kProfHits = 6;
+constexpr int kProfCls = 4;
+struct Prof {
+  int axis;      // key axis (profile_key: uniform profiles -> 0); -1 general cube, -2 error
+  int raxis;     // the probe's axis (slice centres lie along it)
+  int ucls;      // >= 0: every slice has this palette class
+  int ovf;       // 1: slices classified one by one (eps_class_at)
+  int cls[kProfCls];
+  uint64_t msk[kProfCls];
+};
+
+__device__ __forceinline__ uint64_t slice_bits(int lo, int hi) {  // bits lo..hi (lo <= hi < 64)
+  return (hi >= 63 ? ~0ull : (2ull << hi) - 1) & ~((1ull << lo) - 1);
+}
+
+// palette class of slice t
+__device__ __forceinline__ int prof_class(const DStruct& s, const Prof& P, const double c[3],
+                                          double h, int n, int t) {
+  if (P.ucls >= 0) return P.ucls;
+  if (!P.ovf) {
+    int k = s.bg;
+#pragma unroll
+    for (int e = 0; e < kProfCls; ++e)
+      if ((P.msk[e] >> t) & 1) k = P.cls[e];
+    return k;
+  }
+  double p[3] = {c[0], c[1], c[2]};
+  p[P.raxis] = c[P.raxis] - h + (t + 0.5) * (2.0 * h / n);
+  return eps_class_at(s, p);
+}
+
+// the key's layer t: round_sig(layer, 6) (sgf_cache.cpp:29-51; host-rounded palette)
+__device__ __forceinline__ double prof_layer(const DStruct& s, const Prof& P, const double c[3],
+                                             double h, int n, int t) {
+  return __ldg(s.rpal + prof_class(s, P, c, h, n, t));
+}
+
+// visits the dielectric boxes that can meet the closed region cb: the bins it
+// overlaps plus the large boxes (duplicates possible), or every box
+template <class F>
+__device__ __forceinline__ void for_dielectrics_near(const DStruct& s, const double cb[6], F f) {
+  const DGrid& g = s.g;
+  if (g.dims[0]) {
+    int b0[3], b1[3], nb = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      b0[a] = bin_of(g, a, cb[a]);
+      b1[a] = bin_of(g, a, cb[3 + a]);
+      nb *= b1[a] - b0[a] + 1;
+    }
+    if (nb <= kCandBins) {
+#pragma unroll 1
+      for (int q = 0; q < g.ndlarge; ++q)
+        if (!f(__ldg(g.dlarge + q))) return;
+#pragma unroll 1
+      for (int z = b0[2]; z <= b1[2]; ++z)
+#pragma unroll 1
+        for (int y = b0[1]; y <= b1[1]; ++y)
+#pragma unroll 1
+          for (int x = b0[0]; x <= b1[0]; ++x) {
+            const int bin = (z * g.dims[1] + y) * g.dims[0] + x;
+#pragma unroll 1
+            for (int q = __ldg(g.dstart + bin), e = __ldg(g.dstart + bin + 1); q < e; ++q)
+              if (!f(__ldg(g.ditem + q))) return;
+          }
+      return;
+    }
+  }
+#pragma unroll 1
+  for (int d = 0; d < s.nd; ++d)
+    if (!f(d)) return;
+}
+
+__device__ Prof strat_probe(const DStruct& s, const double c[3], double h, int n) {
+  Prof P;
+  P.axis = -1;
+  P.raxis = 0;
+  P.ucls = -1;
+  P.ovf = 0;
+#pragma unroll
+  for (int e = 0; e < kProfCls; ++e) {
+    P.cls[e] = -1;
+    P.msk[e] = 0;
+  }
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
-  int hits[KMAX];
+  // pass 1: the boxes meeting the open cube, their coverage, and up to
+  // kProfHits of them in ascending declaration order (no duplicates)
+  int hit[kProfHits];
+#pragma unroll
+  for (int i = 0; i < kProfHits; ++i) hit[i] = 0x7FFFFFFF;
   int nh = 0;
-  bool overflow = false;
-  bool cov[3] = {true, true, true};
-  int cand[kCandMax];
-  const int ncand = grid_candidates(s, true, cb, cand);
-  for (int i = 0, ni = ncand < 0 ? s.nd : ncand; i < ni; ++i) {
-    const int d = ncand < 0 ? i : cand[i];
+  bool cov0 = true, cov1 = true, cov2 = true, many = false;
+  for_dielectrics_near(s, cb, [&](int d) {
     const double* b = s.dbox + 6 * d;
     double bb[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) bb[q] = __ldg(b + q);
     // Box::intersects_open (geometry.hpp:49-52)
-    if (bb[0] < cb[3] && cb[0] < bb[3] && bb[1] < cb[4] && cb[1] < bb[4] && bb[2] < cb[5] &&
-        cb[2] < bb[5]) {
-      if (nh < KMAX)
-        hits[nh] = d;
-      else
-        overflow = true;
+    if (!(bb[0] < cb[3] && cb[0] < bb[3] && bb[1] < cb[4] && cb[1] < bb[4] && bb[2] < cb[5] &&
+          cb[2] < bb[5]))
+      return true;
+    // covers the cross-section perpendicular to axis a (geometry.cpp:372-380)
+    const bool fx = bb[0] <= cb[0] && bb[3] >= cb[3], fy = bb[1] <= cb[1] && bb[4] >= cb[4],
+               fz = bb[2] <= cb[2] && bb[5] >= cb[5];
+    cov0 &= fy && fz;
+    cov1 &= fx && fz;
+    cov2 &= fx && fy;
+    if (!(cov0 || cov1 || cov2)) return false;  // a general cube: stop scanning
+    bool dup = false;
+#pragma unroll
+    for (int i = 0; i < kProfHits; ++i) dup |= hit[i] == d;
+    if (!dup) {
       ++nh;
+      int x = d;  // sorted insert (unrolled min/max bubble: stays in registers)
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int q = 1; q <= 2; ++q) {
-          const int o = (a + q) % 3;
-          if (bb[o] > cb[o] || bb[3 + o] < cb[3 + o]) cov[a] = false;
-        }
+      for (int i = 0; i < kProfHits; ++i) {
+        const int lo = min(hit[i], x), hi = max(hit[i], x);
+        hit[i] = lo;
+        x = hi;
+      }
+      many |= x != 0x7FFFFFFF;
     }
+    return true;
+  });
+  // (the scan stops at the first box that breaks every axis' coverage,
+  // before counting it: test coverage first)
+  if (!(cov0 || cov1 || cov2)) return P;  // general cube
+  if (nh == 0) {  // background only (geometry.cpp:367-368)
+    P.axis = 0;
+    P.ucls = s.bg;
+    return P;
   }
-  int axis = -1;
-  if (nh == 0)
-    axis = 0;
-  else
-    for (int a = 0; a < 3 && axis < 0; ++a)
-      if (cov[a]) axis = a;
-  if (axis < 0) return -1;
-  if (ucls && nh == 0) {  // background only: the uniform background key
-    *ucls = s.bg;
-    return 0;
-  }
-  const double pitch = 2.0 * h / n;
-  int cls0 = -1;
-  bool uniform = true;
-  // Every hit box covers the cube's cross-section, so it contains the slice
-  // centre's other two coordinates (the cube centre) and, the cube lying in
-  // the world, so does the world box: only the axis coordinate decides.
-  // slice classes: paint each hit's slice range in declaration order (later
-  // boxes win); clip_axis finds exactly the slices whose centre
-  // c - h + (t + 0.5) pitch lies in [lo, hi], the reference's inclusion test
-  int scls[NMAX];
-  if (!overflow) {
-#pragma unroll 1
-    for (int t = 0; t < n; ++t) scls[t] = s.bg;
-    for (int q = 0; q < nh; ++q) {
+  P.raxis = cov0 ? 0 : (cov1 ? 1 : 2);
+  const int ax = P.raxis;
+  if (!many) {
+    // pass 2: paint the hits' slice intervals in declaration order
+    P.cls[0] = s.bg;
+    P.msk[0] = n >= 64 ? ~0ull : (1ull << n) - 1;
+#pragma unroll
+    for (int i = 0; i < kProfHits; ++i) {
+      if (hit[i] == 0x7FFFFFFF) continue;
+      const int d = hit[i];
       int lo, hi;
-      clip_axis(c[axis], h, n, __ldg(s.dbox + 6 * hits[q] + axis),
-                __ldg(s.dbox + 6 * hits[q] + 3 + axis), &lo, &hi);
-      const int cq = __ldg(s.dcls + hits[q]);
-#pragma unroll 1
-      for (int t = lo; t <= hi; ++t) scls[t] = cq;
-    }
-    if (ucls) {
-      bool one = true;
-      for (int t = 1; t < n && one; ++t) one = scls[t] == scls[0];
-      if (one) {
-        *ucls = scls[0];
-        return 0;
+      clip_axis(c[ax], h, n, __ldg(s.dbox + 6 * d + ax), __ldg(s.dbox + 6 * d + 3 + ax), &lo, &hi);
+      if (lo > hi) continue;
+      const uint64_t m = slice_bits(lo, hi);
+      const int k = __ldg(s.dcls + d);
+      bool placed = false;
+#pragma unroll
+      for (int e = 0; e < kProfCls; ++e) {
+        P.msk[e] &= ~m;
+        if (P.cls[e] == k) {
+          P.msk[e] |= m;
+          placed = true;
+        }
+      }
+      if (!placed) {  // a new class takes the first free pair
+        bool put = false;
+#pragma unroll
+        for (int e = 0; e < kProfCls; ++e)
+          if (!put && P.msk[e] == 0) {
+            P.cls[e] = k;
+            P.msk[e] = m;
+            put = true;
+          }
+        if (!put) P.ovf = 1;
       }
     }
+  } else {
+    P.ovf = 1;
   }
-  for (int t = 0; t < n; ++t) {
-    int cls;
-    if (__builtin_expect(!overflow, 1)) {
-      cls = scls[t];
-    } else {
-      double p[3] = {c[0], c[1], c[2]};
-      p[axis] = c[axis] - h + (t + 0.5) * pitch;
-      cls = eps_class_at(s, p);
-      if (cls < 0) return -2;
+  // uniform?  (StratifiedProfile::uniform compares raw permittivities with
+  // eps_equal, geometry.cpp:351-355; profile_key normalises equal rounded
+  // layers to axis 0, sgf_cache.cpp:40-42)
+  if (!P.ovf) {
+    int k0 = s.bg, present = 0, only = -1;
+#pragma unroll
+    for (int e = 0; e < kProfCls; ++e)
+      if (P.msk[e]) {
+        ++present;
+        only = P.cls[e];
+        if (P.msk[e] & 1) k0 = P.cls[e];
+      }
+    if (present == 1) {
+      P.axis = 0;
+      P.ucls = only;
+      return P;
     }
-    if (t == 0) cls0 = cls;
-    // StratifiedProfile::uniform() compares raw permittivities
-    if (cls != cls0 && !eps_equal(__ldg(s.pal + cls), __ldg(s.pal + cls0))) uniform = false;
-    layers[t] = __ldg(s.rpal + cls);  // round_sig(layer, 6), host-exact
+    const double e0 = __ldg(s.pal + k0), r0 = __ldg(s.rpal + k0);
+    bool raw = true, rounded = true;
+#pragma unroll
+    for (int e = 0; e < kProfCls; ++e)
+      if (P.msk[e]) {
+        raw &= P.cls[e] == k0 || eps_equal(__ldg(s.pal + P.cls[e]), e0);
+        rounded &= __ldg(s.rpal + P.cls[e]) == r0;
+      }
+    P.axis = raw || rounded ? 0 : ax;
+    return P;
   }
-  if (uniform) axis = 0;
-  // profile_key: uniform rounded layers normalise to axis 0
-  bool same = true;
+  // slice by slice (rare): the classes of the slice centres
+  const int k0 = prof_class(s, P, c, h, n, 0);
+  if (k0 < 0) {
+    P.axis = -2;
+    return P;
+  }
+  bool one = true, raw = true, rounded = true;
 #pragma unroll 1
-  for (int t = 1; t < n; ++t) same &= layers[t] == layers[0];
-  if (same) axis = 0;
-  return axis;
+  for (int t = 1; t < n; ++t) {
+    const int k = prof_class(s, P, c, h, n, t);
+    if (k < 0) {
+      P.axis = -2;
+      return P;
+    }
+    one &= k == k0;
+    raw &= k == k0 || eps_equal(__ldg(s.pal + k), __ldg(s.pal + k0));
+    rounded &= __ldg(s.rpal + k) == __ldg(s.rpal + k0);
+  }
+  if (one) P.ucls = k0;
+  P.axis = raw || rounded ? 0 : ax;
+  return P;
 }
 
 // multiply-xorshift over the layer bit patterns, one full mix at the end
@@ -619,18 +768,14 @@ __host__ __device__ __forceinline__ uint64_t key_step(uint64_t h, uint64_t w) {
   h = (h ^ w) * 0x9E3779B97F4A7C15ull;
   return h ^ (h >> 29);
 }
-__device__ __forceinline__ uint64_t key_hash(int n, int axis, const double* layers) {
-  uint64_t h = (static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis);
-#pragma unroll 1
-  for (int t = 0; t < n; ++t)
-    h = key_step(h, static_cast<uint64_t>(__double_as_longlong(layers[t])));
-  return sm64_mix(h);
-}
-
-// table lookup; entry index or -1
-__device__ int sgf_find(const DSgf& T, int n, int axis, const double* layers) {
+// table lookup of key (n, axis, layer(t)); entry index or -1
+template <class L>
+__device__ int sgf_find(const DSgf& T, int n, int axis, L layer) {
   if (T.cap == 0) return -1;
-  const uint64_t h = key_hash(n, axis, layers);
+  uint64_t h = (static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis);  // key_hash
+#pragma unroll 1
+  for (int t = 0; t < n; ++t) h = key_step(h, static_cast<uint64_t>(__double_as_longlong(layer(t))));
+  h = sm64_mix(h);
   for (int i = static_cast<int>(h & (T.cap - 1));; i = (i + 1) & (T.cap - 1)) {
     const int e = __ldg(T.entry + i);
     if (e < 0) return -1;
@@ -638,7 +783,7 @@ __device__ int sgf_find(const DSgf& T, int n, int axis, const double* layers) {
     const double* k = T.keys + static_cast<size_t>(e) * NMAX;
     bool eq = true;
 #pragma unroll 1
-    for (int t = 0; t < n && eq; ++t) eq = __ldg(k + t) == layers[t];
+    for (int t = 0; t < n && eq; ++t) eq = __ldg(k + t) == layer(t);
     if (eq) return e;
   }
 }
@@ -656,20 +801,22 @@ __device__ int sample_panel(const double* cdf, const int* guide, int count, doub
   return i == count ? count - 1 : i;
 }
 
-__device__ void record_key(DCounters* C, const DMiss& M, int n, int axis, const double* layers) {
+template <class L>
+__device__ void record_key(DCounters* C, const DMiss& M, int n, int axis, L layer) {
   const unsigned long long m = atomicAdd(&C->nmiss, 1ull);
   if (m < kMissMax) {
     M.axis[m] = axis;
 #pragma unroll 1
-    for (int t = 0; t < n; ++t) M.layers[m * NMAX + t] = layers[t];
+    for (int t = 0; t < n; ++t) M.layers[m * NMAX + t] = layer(t);
   }
 }
 
 // a first transition missed: the walk restarts from scratch once the key is
 // in the table (nothing of it was committed)
-__device__ void record_miss(DCounters* C, const DMiss& M, int n, int axis, const double* layers,
+template <class L>
+__device__ void record_miss(DCounters* C, const DMiss& M, int n, int axis, L layer,
                             long long wid) {
-  record_key(C, M, n, axis, layers);
+  record_key(C, M, n, axis, layer);
   const unsigned long long r = atomicAdd(&C->nretry, 1ull);
   M.retry[r] = wid;
 }
@@ -854,13 +1001,13 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
   }
 }
 
-// compile the MicroWalk job of a general cube into the slot
-// Compiles the MicroWalk job of a cube into the slot: the boxes that reach
-// into the cube clipped to voxel-index ranges (with the reference's
-// voxel-centre arithmetic, microwalk.cpp:25-30), the start node's cell
-// extents and face-neighbour classes.  With `conductors` (MicroWalk-E,
-// microwalk.cpp:206-228) conductor boxes are clipped too.  Returns 1 ok,
-// 0 when the start voxel is conductor (EngulfedStart), -1 on overflow.
+// Compiles the MicroWalk job of a cube into job entry `slot`: the boxes that
+// reach into the cube clipped to voxel-index ranges (with the reference's
+// voxel-centre arithmetic, microwalk.cpp:25-30) and their cell atlas.  With
+// `conductors` (MicroWalk-E, microwalk.cpp:206-228) conductor boxes are
+// clipped too.  Returns 1 ok, 0 when the start voxel is conductor
+// (EngulfedStart), 3 when more than KMAX boxes reach into the cube (only
+// the cube is stored: the hop runs on a dense grid, k_mw_dense).
 __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
                               double h, int n, bool conductors, DCounters* C) {
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
@@ -902,8 +1049,21 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
       }
       if (empty) continue;
       if (K == KMAX) {
-        set_err(C, FRW_EINVAL);  // more than KMAX boxes reach into one cube
-        return -1;
+        // more than KMAX boxes reach into the cube: the hop runs on a dense
+        // voxel-class grid (k_mw_dense); EngulfedStart from the start
+        // voxel's centre (microwalk.cpp:83-86: a conductor holds it)
+        if (conductors) {
+          const int m = (n - 1) / 2;
+          const double pitch = 2.0 * h / n;
+          const double p0[3] = {vcenter(c[0], h, pitch, m), vcenter(c[1], h, pitch, m),
+                                vcenter(c[2], h, pitch, m)};
+          if (conductor_at(s, p0, 0.0) >= 0) return 0;
+        }
+        W.cube[4 * slot + 0] = c[0];
+        W.cube[4 * slot + 1] = c[1];
+        W.cube[4 * slot + 2] = c[2];
+        W.cube[4 * slot + 3] = h;
+        return 3;
       }
       if (cph) {
         boxes[K++] = pk | (0x8000ull | static_cast<uint64_t>(q)) << 48;
@@ -921,7 +1081,7 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
   // EngulfedStart (microwalk.cpp:83-86): a conductor box holds the start
   // voxel.  The start cell itself is looked up by the first super-step.
   if (voxel_mask(A, bm, v0) & cond_mask(ncond)) return 0;
-  W.nbox[slot] = static_cast<uint8_t>(ncond);
+  W.nbox[slot] = static_cast<uint16_t>(ncond | K << 8);
   W.cube[4 * slot + 0] = c[0];
   W.cube[4 * slot + 1] = c[1];
   W.cube[4 * slot + 2] = c[2];
@@ -950,14 +1110,17 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
   double c[3], h;
   transit_cube(g, fh, n, c, &h);
   double layers[NMAX];
+  bool own_layers = false;  // ladder branches 2-3 build the layers themselves
   int branch = 0;
-  int axis = stratified_key(s, c, h, n, layers);
+  Prof pr = strat_probe(s, c, h, n);
+  int axis = pr.axis;
   if (axis == -2) return -1;
   if (axis < 0) {
     for (int i = 19; i >= 6; --i) {  // concentric shrink, engine.cpp:218-226
       double c2[3], h2;
       transit_cube(g, 0.05 * i * fh, n, c2, &h2);
-      axis = stratified_key(s, c2, h2, n, layers);
+      pr = strat_probe(s, c2, h2, n);
+      axis = pr.axis;
       if (axis == -2) return -1;
       if (axis >= 0) {
         c[0] = c2[0];
@@ -989,20 +1152,32 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
         empty |= lo[a] > hi[a];
       }
       if (empty) continue;
-      if (K == KMAX) return -1;
+      if (K == KMAX) {  // more boxes than the list holds: classify voxel centres
+        K = -1;
+        break;
+      }
       boxes[K++] = pack_box(lo, hi, static_cast<uint64_t>(__ldg(s.dcls + d)));
     }
     double sl[3][NMAX];
     for (int a = 0; a < 3; ++a)
       for (int t = 0; t < n; ++t) sl[a][t] = 0.0;
+    const double pitch = 2.0 * h / n;
     for (int k = 0; k < n; ++k)
       for (int j = 0; j < n; ++j) {
         // the class is constant between x-breakpoints: walk the row by cells
         int i = 0;
         while (i < n) {
           int lo, hi;
-          cell_extent(boxes, K, n, 0, i, &lo, &hi);
-          const double e = __ldg(s.pal + cell_class(boxes, K, s.bg, i, j, k));
+          double e;
+          if (K >= 0) {
+            cell_extent(boxes, K, n, 0, i, &lo, &hi);
+            e = __ldg(s.pal + cell_class(boxes, K, s.bg, i, j, k));
+          } else {  // permittivity_at(voxel_center) (geometry.cpp:320-349)
+            const double pv[3] = {vcenter(c[0], h, pitch, i), vcenter(c[1], h, pitch, j),
+                                  vcenter(c[2], h, pitch, k)};
+            lo = hi = i;
+            e = __ldg(s.pal + eps_class_at(s, pv));
+          }
           for (; i <= hi; ++i) {
             sl[0][i] += e;
             sl[1][j] += e;
@@ -1037,10 +1212,13 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
       branch = 3;
       axis = 0;
     }
+    own_layers = true;
   }
-  const int e = sgf_find(T, n, axis, layers);
+  auto layer = [&](int t) { return own_layers ? layers[t] : prof_layer(s, pr, c, h, n, t); };
+  int e = !own_layers && pr.ucls >= 0 ? __ldg(T.uentry + pr.ucls) : -1;
+  if (e < 0) e = sgf_find(T, n, axis, layer);
   if (e < 0) {
-    record_miss(C, M, n, axis, layers, wid);
+    record_miss(C, M, n, axis, layer, wid);
     return 2;
   }
   const double* data = T.data[e];
@@ -1156,6 +1334,8 @@ __global__ void k_spawn(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, D
 // Lane-held state of a walk in the advance stage.
 struct AdvLane {
   int slot;
+  int jslot;     // job entry a compiled MicroWalk hop goes to (the slot, or
+                 // in k_tail the lane's own L2-resident entry)
   long long wid;
   double p[3];
   Rng rng;
@@ -1165,6 +1345,7 @@ struct AdvLane {
 
 __device__ __forceinline__ void adv_load(const DSlots& W, int slot, AdvLane& L) {
   L.slot = slot;
+  L.jslot = slot;
   L.wid = W.wid[slot];
   L.p[0] = W.p[3 * slot];
   L.p[1] = W.p[3 * slot + 1];
@@ -1202,9 +1383,8 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   }
   double c[3], h;
   transit_cube(L.p, fh, n, c, &h);
-  double layers[NMAX];
-  int ucls = -1;
-  const int axis = stratified_key(s, c, h, n, layers, FRW_UKEY ? &ucls : nullptr);
+  const Prof pr = strat_probe(s, c, h, n);
+  const int axis = pr.axis;
   if (axis == -2) {
     set_err(C, FRW_EINVAL);
     W.state[slot] = S_FREE;
@@ -1214,19 +1394,13 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     // a single-class cube (2/3 of the cached hops on C3/C5) finds its entry
     // through the per-class uniform index; otherwise (or when that key is
     // not in the table yet) the full key is hashed and compared
-    int e = ucls >= 0 ? __ldg(T.uentry + ucls) : -1;
-    if (e < 0) {
-      if (ucls >= 0) {
-        const double v = __ldg(s.rpal + ucls);
-#pragma unroll 1
-        for (int t = 0; t < n; ++t) layers[t] = v;
-      }
-      e = sgf_find(T, n, axis, layers);
-    }
+    auto layer = [&](int t) { return prof_layer(s, pr, c, h, n, t); };
+    int e = pr.ucls >= 0 ? __ldg(T.uentry + pr.ucls) : -1;
+    if (e < 0) e = sgf_find(T, n, axis, layer);
     if (e < 0) {
       // parked mid-walk: the key is looked up before any draw, so the walk
       // resumes from this state, bit-identical to an uninterrupted run
-      record_key(C, M, n, axis, layers);
+      record_key(C, M, n, axis, layer);
       W.p[3 * slot] = L.p[0];
       W.p[3 * slot + 1] = L.p[1];
       W.p[3 * slot + 2] = L.p[2];
@@ -1268,7 +1442,7 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   // bound): the expanded cube first, the transit cube on EngulfedStart
 #pragma unroll 1
   for (;;) {
-    rc = compile_mw_job(s, W, slot, jc, jh, n, expanded, C);
+    rc = compile_mw_job(s, W, L.jslot, jc, jh, n, expanded, C);
     if (rc != 0 || !expanded) break;
     expanded = false;
     jc[0] = c[0];
@@ -1280,7 +1454,28 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     W.state[slot] = S_FREE;
     return 1;
   }
-  W.mwkind[slot] = kind;
+  if (rc == 3) {
+    // more than KMAX boxes reach into the cube: the hop goes to k_mw_dense
+    // (its job in the walk's own entry: the dense kernel runs after this one)
+    if (kind == 2) {  // FDM builds its system from the atlas
+      set_err(C, FRW_EINVAL);
+      W.state[slot] = S_FREE;
+      return 1;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) W.cube[4 * slot + q] = W.cube[4 * L.jslot + q];
+    W.mwkind[slot] = static_cast<uint8_t>(kind | kDense | (expanded ? kDenseCond : 0));
+    W.p[3 * slot + 0] = L.p[0];
+    W.p[3 * slot + 1] = L.p[1];
+    W.p[3 * slot + 2] = L.p[2];
+    W.rng[slot] = L.rng.s;
+    W.hops[slot] = L.hops + 1;
+    W.cached[slot] = L.cached;
+    W.state[slot] = S_NEED_MW;
+    M.dense[atomicAdd(&C->dqlen, 1ull)] = slot;
+    return 1;
+  }
+  W.mwkind[L.jslot] = kind;
   W.p[3 * slot + 0] = L.p[0];
   W.p[3 * slot + 1] = L.p[1];
   W.p[3 * slot + 2] = L.p[2];
@@ -1292,6 +1487,11 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   return 2;
 }
 
+// the walk goes back to the next round's ACTIVE queue
+__device__ __forceinline__ void mw_requeue(DCounters* C, int* aq_out, int slot) {
+  aq_out[atomicAdd(&C->a2len, 1ull)] = slot;
+}
+
 // persistent: each thread takes ACTIVE walks from the queue and advances
 // them one transition per iteration, re-armed as soon as its walk leaves.
 // The grid is 4 x 256 threads per SM, so registers must allow 4 CTAs
@@ -1300,14 +1500,30 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
 #endif
 __global__ void __launch_bounds__(256, FRW_ADV_MINB)
     k_advance(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
-              const int* aq, int* mq) {
+              const int* aq, int* mq, int* aq_out) {
   const unsigned long long alen = C->alen;
+  const int slice = P.adv_slice > 0 ? P.adv_slice : 0x7FFFFFFF;
   unsigned long long item = atomicAdd(&C->ahead, 1ull);
   bool live = item < alen;
   AdvLane L;
   if (live) adv_load(W, aq[item], L);
+  int left = slice;  // transitions left in this visit of the walk
   while (__any_sync(0xFFFFFFFFu, live)) {
-    if (live && advance_once(s, T, P, W, recs, C, M, mq, L) != 0) {
+    if (!live) continue;
+    int r = advance_once(s, T, P, W, recs, C, M, mq, L);
+    if (r == 0 && --left == 0) {
+      // a long chain of cached hops: the walk continues next round
+      W.p[3 * L.slot] = L.p[0];
+      W.p[3 * L.slot + 1] = L.p[1];
+      W.p[3 * L.slot + 2] = L.p[2];
+      W.rng[L.slot] = L.rng.s;
+      W.hops[L.slot] = L.hops;
+      W.cached[L.slot] = L.cached;
+      mw_requeue(C, aq_out, L.slot);
+      r = 1;
+    }
+    if (r != 0) {
+      left = slice;
       item = atomicAdd(&C->ahead, 1ull);
       live = item < alen;
       if (live) adv_load(W, aq[item], L);
@@ -1315,13 +1531,17 @@ __global__ void __launch_bounds__(256, FRW_ADV_MINB)
   }
 }
 
-// between rounds: the next round's ACTIVE queue becomes current
+// between rounds: the next round's ACTIVE queue becomes current, and the
+// MicroWalk hops carried over open the next round's MicroWalk queue
 __global__ void k_round(DCounters* C) {
   C->alen = C->a2len;
   C->ahead = 0;
   C->a2len = 0;
-  C->qlen = 0;
+  C->qlen = C->q2len;
   C->qhead = 0;
+  C->q2len = 0;
+  C->dqlen = 0;
+  C->dqhead = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -1329,6 +1549,7 @@ __global__ void k_round(DCounters* C) {
 
 struct MwLane {
   int slot;
+  int jslot;      // the hop's job entry (compile_mw_job)
   long long wid;
   uint32_t node;
   uint64_t room;  // distance to the cell faces, one byte per direction
@@ -1336,11 +1557,15 @@ struct MwLane {
   uint64_t rng;   // SplitMix64 state or Philox block counter
   int steps;
   int ncond;      // conductor boxes of the job (atlas bits [0, ncond))
+  int nbx;        // clipped boxes of the job
+  int hom;        // homogeneous radius known at node hnode (0: none)
+  uint32_t hnode;
   uint64_t bm[3]; // segment-start bitmaps of the job's atlas
   double al[6];   // alpha of the neighbour across each face of the cell
   uint32_t gsteps;  // diagnostics, accumulated across the lane's hops
   uint32_t cchg;
   uint32_t jumps;
+  uint32_t jsteps;  // steps the lane's jumps stand for
 };
 
 // Tables of the MicroWalk kernels: the palette-pair alphas (Pn <= PMAX: in
@@ -1378,25 +1603,51 @@ __device__ __forceinline__ const uint64_t* lane_atlas(const DSlots& W, int slot)
   return W.atlas + static_cast<size_t>(slot) * kAtlasWords;
 }
 
-__device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int n, MwLane& L) {
+__device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int n, MwLane& L) {
   const int m = (n - 1) / 2;
-  const uint64_t* A = lane_atlas(W, slot);
+  const uint64_t* A = lane_atlas(W, jslot);
   L.slot = slot;
+  L.jslot = jslot;
   L.wid = W.wid[slot];
   L.node = m | (m << 8) | (m << 16);
   L.room = 0;  // cell pending: the first super-step looks it up
   L.rng = W.rng[slot];
-  L.ncond = W.nbox[slot];
+  {
+    const int nb = W.nbox[jslot];
+    L.ncond = nb & 0xFF;
+    L.nbx = nb >> 8;
+  }
+  L.hom = 0;
   L.bm[0] = A[kAtBm];
   L.bm[1] = A[kAtBm + 1];
   L.bm[2] = A[kAtBm + 2];
   L.steps = 0;
+  L.hnode = L.node;
+  if (W.state[slot] == S_MW_CARRY) {  // a hop carried over from the last round
+    L.node = W.mwnode[slot];
+    L.steps = W.mwhsteps[slot];
+    const uint64_t hj = W.mwhj[slot];  // the jump decisions continue exactly
+    L.hom = static_cast<int>(static_cast<uint32_t>(hj));
+    L.hnode = static_cast<uint32_t>(hj >> 32);
+  }
+}
+
+// the hop's time slice ran out: its state goes to the slot and the job to
+// the next round's MicroWalk queue (the stream position is saved, so the
+// hop continues bit-identically)
+__device__ __forceinline__ void mw_carry(const DSlots& W, DCounters* C, int* mq_next, MwLane& L) {
+  W.mwnode[L.slot] = L.node;
+  W.mwhsteps[L.slot] = L.steps;
+  W.mwhj[L.slot] = static_cast<uint32_t>(L.hom) | static_cast<uint64_t>(L.hnode) << 32;
+  W.rng[L.slot] = L.rng;
+  W.state[L.slot] = S_MW_CARRY;
+  mq_next[atomicAdd(&C->q2len, 1ull)] = L.slot;
 }
 
 // a move left the current cell: look the new cell up in the atlas
 __device__ __forceinline__ void mw_cell_change(const DSlots& W, const AlphaTab& T, int n,
                                                MwLane& L) {
-  const uint64_t* A = lane_atlas(W, L.slot);
+  const uint64_t* A = lane_atlas(W, L.jslot);
   L.fc = cell_info(A, L.bm, L.ncond, n, L.node, &L.room);
   lane_alphas(T, A, L);
 }
@@ -1408,8 +1659,8 @@ __device__ void mw_exit(const DSlots& W, int n, MwLane& L, int dir) {
   const int u = a == 0 ? j : i;
   const int v = a == 2 ? j : k;
   const int panel = (dir * n + v) * n + u;  // surface_panel_of (sgf.cpp:13-30)
-  const double c[3] = {W.cube[4 * L.slot], W.cube[4 * L.slot + 1], W.cube[4 * L.slot + 2]};
-  const double h = W.cube[4 * L.slot + 3];
+  const double c[3] = {W.cube[4 * L.jslot], W.cube[4 * L.jslot + 1], W.cube[4 * L.jslot + 2]};
+  const double h = W.cube[4 * L.jslot + 3];
   double p[3];
   panel_center(c, h, n, panel, p);
   W.p[3 * L.slot + 0] = p[0];
@@ -1421,10 +1672,6 @@ __device__ void mw_exit(const DSlots& W, int n, MwLane& L, int dir) {
   W.state[L.slot] = S_ACTIVE;
 }
 
-// the walk goes back to the next round's ACTIVE queue
-__device__ __forceinline__ void mw_requeue(DCounters* C, int* aq_out, int slot) {
-  aq_out[atomicAdd(&C->a2len, 1ull)] = slot;
-}
 
 struct DirDelta {
   uint64_t room;
@@ -1530,7 +1777,10 @@ enum : int { MW_GO = 0, MW_SURFACE = 1, MW_COND = 3, MW_CAP = 4 };
 // the walker moves to that node of the radius-m sphere (still in its cell),
 // the face distances follow, and the hop's step count takes E[tau_m]
 // (stochastically rounded).  Returns false (nothing consumed) otherwise.
-// the jump of radius m (2 <= m <= mmax) from 64 random bits
+// the jump of radius m (2 <= m <= mmax) from 64 random bits.  CHECK: the
+// ball may reach beyond the lane's cell (a homogeneous-ball jump); a landing
+// outside it leaves the cell pending (room 0, looked up next super-step)
+template <bool CHECK = false>
 __device__ __forceinline__ void mw_jump_r(const DJump& J, MwLane& L, int m, uint32_t w0,
                                           uint32_t w1) {
   const JumpMeta jm = J.meta[m];
@@ -1555,10 +1805,59 @@ __device__ __forceinline__ void mw_jump_r(const DJump& J, MwLane& L, int m, uint
 #pragma unroll
   for (int q = 0; q < 3; ++q)
     dr += static_cast<long long>(dl[q]) * ((1ll << (16 * q)) - (1ll << (16 * q + 8)));
-  L.room += static_cast<uint64_t>(dr);
+  bool in_cell = true;
+  if (CHECK) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int lo = static_cast<int>((L.room >> (16 * q)) & 0xFF);
+      const int hi = static_cast<int>((L.room >> (16 * q + 8)) & 0xFF);
+      in_cell &= dl[q] >= -lo && dl[q] <= hi;
+    }
+  }
+  if (in_cell)
+    L.room += static_cast<uint64_t>(dr);
+  else
+    L.room = 0;
   ++L.jumps;
-  L.steps += static_cast<int>(jm.esteps >> 32) +
-             (static_cast<uint32_t>(jm.esteps) > static_cast<uint32_t>(y >> 8) ? 1 : 0);
+  const int js = static_cast<int>(jm.esteps >> 32) +
+                 (static_cast<uint32_t>(jm.esteps) > static_cast<uint32_t>(y >> 8) ? 1 : 0);
+  L.steps += js;
+  L.jsteps += js;
+}
+
+// The largest m such that every node within L-inf distance m of the lane's
+// node lies in the lattice and in exactly the same clipped boxes (so has the
+// same permittivity): each box either contains the whole ball or misses it.
+// Inside that ball every alpha is 1/2 (microwalk.cpp:97-104), so the jump
+// law of radius m holds there whatever cells the box faces cut (the cells are
+// a tensor grid of every face, finer than the material boundaries).
+__device__ int mw_hom_radius(const DSlots& W, const MwLane& L, int n) {
+  const int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+  int m = 31;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) m = min(m, min(v[a], n - 1 - v[a]));
+  const uint64_t* B = W.boxes + static_cast<size_t>(L.jslot) * KMAX;
+#pragma unroll 1
+  for (int q = 0; q < L.nbx && m >= 2; ++q) {
+    const uint64_t b = B[q];
+    bool in = true;
+    int gin = 64, gout = -1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int lo = box_lo(b, a), hi = box_hi(b, a);
+      if (v[a] < lo) {
+        in = false;
+        gout = max(gout, lo - v[a] - 1);
+      } else if (v[a] > hi) {
+        in = false;
+        gout = max(gout, v[a] - hi - 1);
+      } else {
+        gin = min(gin, min(v[a] - lo, hi - v[a]));
+      }
+    }
+    m = min(m, in ? gin : gout);
+  }
+  return m;
 }
 
 __device__ __forceinline__ bool mw_jump(const DJump& J, MwLane& L, uint32_t w0, uint32_t w1) {
@@ -1598,10 +1897,30 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W, c
   if ((L.room >> 48) == 0) mw_cell_change(W, AT, n, L);
   int code = 0;
   int u0 = 0;  // words taken by jumps (two per jump)
-  if (RNG == FRW_RNG_PHILOX && P.jump.mmax >= 2 && L.steps < cap &&
-      mw_jump(P.jump, L, w4[0], w4[1])) {
-    u0 = 2;
-    if (P.jump.twice && L.steps < cap && mw_jump(P.jump, L, w4[2], w4[3])) u0 = 4;
+  if (RNG == FRW_RNG_PHILOX && P.jump.mmax >= 2 && L.steps < cap) {
+    if (mw_jump(P.jump, L, w4[0], w4[1])) {
+      u0 = 2;
+      if (P.jump.twice && L.steps < cap && mw_jump(P.jump, L, w4[2], w4[3])) u0 = 4;
+    } else if (P.jump.hom) {
+      // no room for a jump inside the cell: the homogeneous ball around the
+      // node (a bound carried from the node it was computed at, recomputed
+      // once it drops below 2)
+      const int d = max(max(abs(coord(L.node, 0) - coord(L.hnode, 0)),
+                            abs(coord(L.node, 1) - coord(L.hnode, 1))),
+                        abs(coord(L.node, 2) - coord(L.hnode, 2)));
+      // the radius is 1-Lipschitz in the node: within [hom - d, hom + d];
+      // recompute only when that range straddles 2
+      int eff = L.hom - d;
+      if (eff < 2 && L.hom + d >= 2) {
+        eff = mw_hom_radius(W, L, n);
+        L.hom = eff;
+        L.hnode = L.node;
+      }
+      if (eff >= 2) {
+        mw_jump_r<true>(P.jump, L, min(eff, P.jump.mmax), w4[0], w4[1]);
+        u0 = (L.room >> 48) == 0 ? 4 : 2;  // left the cell: no steps before its lookup
+      }
+    }
   }
 #if FRW_STEP_UNROLL
 #pragma unroll
@@ -1640,24 +1959,31 @@ __device__ void mw_conductor_exit(const DSlots& W, WalkRec* recs, DCounters* C, 
                                   int xdir) {
   int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
   v[xdir >> 1] += (xdir & 1) ? 1 : -1;
-  const uint64_t cm = voxel_mask(lane_atlas(W, L.slot), L.bm, v) & cond_mask(L.ncond);
-  const int ci = box_cond(W.boxes[static_cast<size_t>(L.slot) * KMAX + __ffsll(cm) - 1]);
+  const uint64_t cm = voxel_mask(lane_atlas(W, L.jslot), L.bm, v) & cond_mask(L.ncond);
+  const int ci = box_cond(W.boxes[static_cast<size_t>(L.jslot) * KMAX + __ffsll(cm) - 1]);
   W.mw[L.slot] += 1;
   W.mwsteps[L.slot] += L.steps;
   finish_walk(W, recs, C, L.slot, ci, false);
 }
 
+__device__ __forceinline__ void flush_mw_stats_one(DCounters* C, const MwLane& L) {
+  atomicAdd(&C->gen_steps, static_cast<unsigned long long>(L.gsteps));
+  atomicAdd(&C->cell_chg, static_cast<unsigned long long>(L.cchg));
+}
+
 __device__ __forceinline__ void flush_mw_stats(DCounters* C, const MwLane& L) {
-  unsigned long long g = L.gsteps, cc = L.cchg, jp = L.jumps;
+  unsigned long long g = L.gsteps, cc = L.cchg, jp = L.jumps, js = L.jsteps;
   for (int o = 16; o > 0; o >>= 1) {
     g += __shfl_xor_sync(0xFFFFFFFFu, g, o);
     cc += __shfl_xor_sync(0xFFFFFFFFu, cc, o);
     jp += __shfl_xor_sync(0xFFFFFFFFu, jp, o);
+    js += __shfl_xor_sync(0xFFFFFFFFu, js, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&C->gen_steps, g);
     atomicAdd(&C->cell_chg, cc);
     atomicAdd(&C->jumps, jp);
+    atomicAdd(&C->jsteps, js);
   }
 }
 
@@ -1668,38 +1994,159 @@ __device__ __forceinline__ void flush_mw_stats(DCounters* C, const MwLane& L) {
 template <int RNG>
 __global__ void __launch_bounds__(512, FRW_KMW_MINB)
     k_mw(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* queue,
-         int* aq_out) {
+         int* aq_out, int* mq_next) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
   const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
   const int cap = 1000 * n * n;  // microwalk.cpp:81
+  const int slice = P.mw_slice > 0 ? P.mw_slice : 0x7FFFFFFF;
   const unsigned long long qlen = C->qlen;
   MwLane L;
   L.gsteps = 0;
   L.jumps = 0;
+  L.jsteps = 0;
   L.cchg = 0;
+  int left = slice;  // super-steps left in this visit of the hop
   unsigned long long item = atomicAdd(&C->qhead, 1ull);
   bool live = item < qlen;
-  if (live) mw_arm(W, queue[item], n, L);
+  if (live) {
+    const int q = queue[item];
+    mw_arm(W, q, q, n, L);
+  }
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
     if (live) code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+    if (live && code == MW_GO && --left == 0) {
+      mw_carry(W, C, mq_next, L);
+      code = -1;
+    }
     if (live && code != MW_GO) {
       if (code == MW_SURFACE) {
         mw_exit(W, n, L, xdir);
         mw_requeue(C, aq_out, L.slot);
       } else if (code == MW_COND) {
         mw_conductor_exit(W, recs, C, L, xdir);
-      } else {
+      } else if (code != -1) {
         set_err(C, FRW_ESTEPCAP);
       }
+      left = slice;
       item = atomicAdd(&C->qhead, 1ull);
       live = item < qlen;
-      if (live) mw_arm(W, queue[item], n, L);
+      if (live) {
+        const int q = queue[item];
+        mw_arm(W, q, q, n, L);
+      }
     }
   }
   flush_mw_stats(C, L);
+}
+
+// ---- dense MicroWalk hops (more than KMAX boxes reach into the cube) -------
+// The cell atlas holds at most KMAX boxes per cube.  Such a hop runs here:
+// one CTA classifies every voxel centre of the cube against the structure
+// (LazyField::classify, microwalk.cpp:44-71: conductor_at(p, 0) for the
+// MicroWalk-E lattice, else permittivity_at -- the same closed-box tests
+// the clipped boxes encode) into a u16 grid, and one lane walks the hop on
+// it, every node a cell of its own (its six alphas from the palette pair,
+// microwalk.cpp:97-104), with the walk's own random stream.  Rare by
+// construction; the walk then rejoins the next round's ACTIVE queue.
+constexpr uint16_t kDenseCondBit = 0x8000;
+__device__ void dense_cell(const uint16_t* grid, const AlphaTab& T, int n, MwLane& L) {
+  const int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+  const int g0 = grid[(v[2] * n + v[1]) * n + v[0]];
+  uint64_t fc = 0;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    int w[3] = {v[0], v[1], v[2]};
+    w[d >> 1] += (d & 1) ? 1 : -1;
+    const bool out = w[d >> 1] < 0 || w[d >> 1] >= n;
+    const int gn = out ? 0 : grid[(w[2] * n + w[1]) * n + w[0]];
+    const bool cond = !out && (gn & kDenseCondBit);
+    fc |= static_cast<uint64_t>(out ? kFace : (cond ? kCond : 0)) << (8 * d);
+    if (out || cond)
+      L.al[d] = 1.0;
+    else if (T.tab)
+      L.al[d] = T.tab[gn * T.Pn + g0];
+    else {
+      const double en = __ldg(T.pal + gn), e0 = __ldg(T.pal + g0);
+      L.al[d] = en / (en + e0);
+    }
+  }
+  L.fc = fc;
+  L.room = 0x0101ull << 48;  // every node is a cell of its own: on all six faces
+}
+
+template <int RNG>
+__global__ void __launch_bounds__(256)
+    k_mw_dense(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* dense,
+               int* aq_out, uint16_t* scratch) {
+  __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
+  __shared__ DirDelta dd[6];
+  __shared__ int job_sh;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
+  const int n = P.n, nn = n * n, m3 = nn * n;
+  const int cap = 1000 * n * n;
+  uint16_t* grid = scratch + static_cast<size_t>(blockIdx.x) * m3;
+  DParams Pd = P;
+  Pd.jump.mmax = 0;  // no lattice jumps: a node's ball is not known to be homogeneous
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long j = atomicAdd(&C->dqhead, 1ull);
+      job_sh = j < C->dqlen ? dense[j] : -1;
+    }
+    __syncthreads();
+    const int slot = job_sh;
+    if (slot < 0) break;
+    if (threadIdx.x == 0) atomicAdd(&C->dense_hops, 1ull);
+    const double c[3] = {W.cube[4 * slot], W.cube[4 * slot + 1], W.cube[4 * slot + 2]};
+    const double h = W.cube[4 * slot + 3];
+    const double pitch = 2.0 * h / n;
+    const bool with_cond = (W.mwkind[slot] & kDenseCond) != 0;
+    for (int v = threadIdx.x; v < m3; v += blockDim.x) {
+      const int i = v % n, j = (v / n) % n, k = v / nn;
+      const double p[3] = {vcenter(c[0], h, pitch, i), vcenter(c[1], h, pitch, j),
+                           vcenter(c[2], h, pitch, k)};
+      const int ci = with_cond ? conductor_at(s, p, 0.0) : -1;
+      grid[v] = ci >= 0 ? static_cast<uint16_t>(kDenseCondBit | ci)
+                        : static_cast<uint16_t>(eps_class_at(s, p));
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) continue;
+    MwLane L;
+    L.gsteps = L.cchg = L.jumps = L.jsteps = 0;
+    L.slot = L.jslot = slot;
+    L.wid = W.wid[slot];
+    const int mid = (n - 1) / 2;
+    L.node = mid | (mid << 8) | (mid << 16);
+    L.hnode = L.node;
+    L.hom = 0;
+    L.rng = W.rng[slot];
+    L.ncond = L.nbx = 0;
+    L.steps = 0;
+    L.room = 0;
+    int code = MW_GO, xdir = 0;
+    while (code == MW_GO) {
+      if ((L.room >> 48) == 0) dense_cell(grid, AT, n, L);
+      code = mw_superstep<RNG>(Pd, W, AT, dd, n, cap, L, &xdir);
+    }
+    if (code == MW_SURFACE) {
+      mw_exit(W, n, L, xdir);
+      mw_requeue(C, aq_out, slot);
+    } else if (code == MW_COND) {
+      int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+      v[xdir >> 1] += (xdir & 1) ? 1 : -1;
+      const int ci = grid[(v[2] * n + v[1]) * n + v[0]] & ~kDenseCondBit;
+      W.mw[slot] += 1;
+      W.mwsteps[slot] += L.steps;
+      finish_walk(W, recs, C, slot, ci, false);
+    } else {
+      set_err(C, FRW_ESTEPCAP);
+      W.state[slot] = S_FREE;
+    }
+    flush_mw_stats_one(C, L);
+  }
 }
 
 // Run-to-completion kernel for the tail of a run: once few walks remain,
@@ -1707,9 +2154,6 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
 // takes an ACTIVE walk and runs it to its end, alternating transitions and
 // MicroWalk super-steps in-thread.  A table miss parks its walk as in
 // k_advance (the host resolves misses once the other walks are done).
-#ifndef FRW_TAIL_POLICY
-#define FRW_TAIL_POLICY 0
-#endif
 #ifndef FRW_TAIL_BLOCKS
 #define FRW_TAIL_BLOCKS 2
 #endif
@@ -1723,22 +2167,40 @@ constexpr int kTailBlocks = FRW_TAIL_BLOCKS;  // resident 256-thread CTAs per SM
 template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
-           const int* aq) {
+           const int* aq, const int* mq) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
   const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
   const int n = P.n;
   const int cap = 1000 * n * n;
-  const unsigned long long alen = C->alen;
+  // items: first the MicroWalk hops carried over from the last round (their
+  // jobs in their slots' entries), then the ACTIVE walks
+  const unsigned long long qc = C->qlen;
+  const unsigned long long total = qc + C->alen;
   AdvLane A;
   MwLane L;
   L.gsteps = 0;
   L.jumps = 0;
+  L.jsteps = 0;
   L.cchg = 0;
   bool in_mw = false;
-  unsigned long long item = atomicAdd(&C->ahead, 1ull);
-  bool live = item < alen;
-  if (live) adv_load(W, aq[item], A);
+  const int jlane = W.jtail + blockIdx.x * blockDim.x + threadIdx.x;
+  bool live = false;
+  auto fetch = [&]() {
+    const unsigned long long item = atomicAdd(&C->ahead, 1ull);
+    live = item < total;
+    if (!live) return;
+    if (item < qc) {
+      const int q = mq[item];
+      mw_arm(W, q, q, n, L);
+      in_mw = true;
+    } else {
+      adv_load(W, aq[item - qc], A);
+      A.jslot = jlane;
+      in_mw = false;
+    }
+  };
+  fetch();
   while (__any_sync(0xFFFFFFFFu, live)) {
     if (live && !in_mw) {
       // up to FRW_TAIL_CHAIN transitions back to back while they are cached
@@ -1749,11 +2211,9 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
       if (r == 2) {
         in_mw = true;
-        mw_arm(W, A.slot, n, L);
+        mw_arm(W, A.slot, A.jslot, n, L);
       } else if (r == 1) {
-        item = atomicAdd(&C->ahead, 1ull);
-        live = item < alen;
-        if (live) adv_load(W, aq[item], A);
+        fetch();
       }
     }
     // up to 32 super-steps per transition (a hop is ~50 super-steps): the
@@ -1763,13 +2223,6 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     for (int rep = 0; rep < FRW_TAIL_REPS; ++rep) {
       const unsigned mwm = __ballot_sync(0xFFFFFFFFu, live && in_mw);
       if (!mwm) break;
-#if FRW_TAIL_POLICY
-      // leave early once the lanes waiting for a transition outnumber the
-      // walking ones by FRW_TAIL_POLICY (they would idle a whole stretch)
-      if (rep >= 2 && __popc(__ballot_sync(0xFFFFFFFFu, live && !in_mw)) >
-                          FRW_TAIL_POLICY * __popc(mwm))
-        break;
-#endif
       if (!(live && in_mw)) continue;
       int xdir = 0;
       const int code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
@@ -1778,6 +2231,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       if (code == MW_SURFACE) {
         mw_exit(W, n, L, xdir);
         adv_load(W, L.slot, A);
+        A.jslot = jlane;
         continue;
       }
       if (code == MW_COND)
@@ -1786,9 +2240,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         set_err(C, FRW_ESTEPCAP);
         W.state[L.slot] = S_FREE;
       }
-      item = atomicAdd(&C->ahead, 1ull);
-      live = item < alen;
-      if (live) adv_load(W, aq[item], A);
+      fetch();
     }
   }
   flush_mw_stats(C, L);
@@ -1892,7 +2344,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     MwLane L;
     L.gsteps = 0;
     L.jumps = 0;
-  L.jumps = 0;
+    L.jsteps = 0;
     L.cchg = 0;
     bool have = false;
     long long res = -1;
@@ -1903,7 +2355,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         if (v >= 0) {
           ring_m[res & mask] = -1;
           __threadfence();
-          mw_arm(W, v, n, L);
+          mw_arm(W, v, v, n, L);
           have = true;
           res = -1;
         }
@@ -1967,7 +2419,8 @@ __global__ void __launch_bounds__(128)
   e.conductor = -1;
   e.panel = -1;
   const int rc = compile_mw_job(s, W, t, c, h, n, with_cond != 0, C);
-  if (rc <= 0) {
+  if (rc != 1) {
+    if (rc == 3) set_err(C, FRW_EINVAL);  // the single-transit API keeps the KMAX cap
     e.kind = rc == 0 ? -1 : -2;  // EngulfedStart / too many boxes (error set)
     out[t] = e;
     return;
@@ -1979,8 +2432,9 @@ __global__ void __launch_bounds__(128)
   MwLane L;
   L.gsteps = 0;
   L.jumps = 0;
+  L.jsteps = 0;
   L.cchg = 0;
-  mw_arm(W, t, n, L);
+  mw_arm(W, t, t, n, L);
   int code = MW_GO, xdir = 0;
   while (code == MW_GO)
     code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
@@ -2095,6 +2549,11 @@ __global__ void __launch_bounds__(128)
     e.point[2] = L.p[2];
     states[t] = L.rng.s;
   } else if (r == 1) {
+    if (W.state[slot] == S_NEED_MW && (W.mwkind[slot] & kDense)) {
+      set_err(C, FRW_EINVAL);  // the single-transition API keeps the KMAX cap
+      rc_out[q] = 2;
+      return;
+    }
     if (!recs[t].done) {  // table miss (or geometry error, flagged in C->err)
       rc_out[q] = 2;
       return;
@@ -2112,8 +2571,9 @@ __global__ void __launch_bounds__(128)
     MwLane ml;
     ml.gsteps = 0;
     ml.jumps = 0;
+    ml.jsteps = 0;
     ml.cchg = 0;
-    mw_arm(W, slot, n, ml);
+    mw_arm(W, slot, slot, n, ml);
     ml.wid = t;
     int code = MW_GO, xdir = 0;
     while (code == MW_GO)
@@ -2268,7 +2728,7 @@ __global__ void __launch_bounds__(kFdmThreads)
     // voxel classes of the cube from the job's atlas
     const uint64_t* A = lane_atlas(W, slot);
     const uint64_t bm[3] = {A[kAtBm], A[kAtBm + 1], A[kAtBm + 2]};
-    const uint64_t cm = cond_mask(W.nbox[slot]);
+    const uint64_t cm = cond_mask(W.nbox[slot] & 0xFF);
     for (int v = threadIdx.x; v < m; v += blockDim.x) {
       const int vv[3] = {v % n, (v / n) % n, v / nn};
       cls[v] = static_cast<uint8_t>(class_of(voxel_mask(A, bm, vv), cm));
@@ -2445,10 +2905,11 @@ __global__ void k_strat_keys(DStruct s, const double* cubes, int count, int n, i
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
   const double c[3] = {cubes[4 * t], cubes[4 * t + 1], cubes[4 * t + 2]};
-  double lay[NMAX];
-  const int a = stratified_key(s, c, cubes[4 * t + 3], n, lay);
-  axis[t] = a;
-  for (int q = 0; q < n; ++q) layers[static_cast<size_t>(t) * n + q] = a >= 0 ? lay[q] : 0.0;
+  const double h = cubes[4 * t + 3];
+  const Prof P = strat_probe(s, c, h, n);
+  axis[t] = P.axis;
+  for (int q = 0; q < n; ++q)
+    layers[static_cast<size_t>(t) * n + q] = P.axis >= 0 ? prof_layer(s, P, c, h, n, q) : 0.0;
 }
 
 // ---- deterministic tallies -------------------------------------------------
@@ -2594,7 +3055,7 @@ struct Engine {
   long long recs_cap = 0;
   DCounters* d_cnt = nullptr;
   DMiss M{};
-  int* queue = nullptr;   // MicroWalk queue
+  int* mq[2] = {nullptr, nullptr};  // MicroWalk queues (current / next round)
   int* aq[2] = {nullptr, nullptr};  // ACTIVE queues (current / next round)
   int* ring_a = nullptr;  // k_flow rings of walk slots (-1 = empty entry)
   int* ring_m = nullptr;
@@ -2607,6 +3068,9 @@ struct Engine {
   unsigned long long *pland = nullptr, *pstat = nullptr, *oland = nullptr, *ostat = nullptr;
   size_t red_cap = 0;
   int red_slots = 0;
+  // dense-hop voxel grids (k_mw_dense): one n^3 u16 grid per CTA
+  uint16_t* dense_scratch = nullptr;
+  size_t dense_cap = 0;
   // FDM solve scratch (5 Krylov vectors per persistent CTA)
   double* fdm_slab = nullptr;
   size_t fdm_cap = 0;
@@ -2635,7 +3099,12 @@ void free_slots(Engine& E) {
   cudaFree(E.W.boxes);
   cudaFree(E.W.mwkind);
   cudaFree(E.W.atlas);
-  cudaFree(E.queue);
+  cudaFree(E.mq[0]);
+  cudaFree(E.mq[1]);
+  E.mq[0] = E.mq[1] = nullptr;
+  cudaFree(E.W.mwnode);
+  cudaFree(E.W.mwhsteps);
+  cudaFree(E.W.mwhj);
   cudaFree(E.aq[0]);
   cudaFree(E.aq[1]);
   E.aq[0] = E.aq[1] = nullptr;
@@ -2646,6 +3115,8 @@ void free_slots(Engine& E) {
   cudaFree(E.M.retry);
   cudaFree(E.M.pend);
   cudaFree(E.M.park);
+  cudaFree(E.M.dense);
+  E.M.dense = nullptr;
   E.W = DSlots{};
   E.S = 0;
 }
@@ -2689,6 +3160,7 @@ void engine_free(frw_ctx* ctx) {
   cudaFree(E->ostat);
   cudaFree(E->pack);
   cudaFree(E->fdm_slab);
+  cudaFree(E->dense_scratch);
   cudaFree(E->d_jmeta);
   cudaFree(E->d_jthr);
   cudaFree(E->d_jguide);
@@ -2704,7 +3176,7 @@ Engine* engine_of(frw_ctx* ctx) {
   return static_cast<Engine*>(ctx->walk);
 }
 
-uint64_t host_key_hash(int n, int axis, const double* layers) {  // == key_hash
+uint64_t host_key_hash(int n, int axis, const double* layers) {  // == sgf_find's hash
   uint64_t h = (static_cast<uint64_t>(n) << 8) ^ static_cast<uint64_t>(axis);
   for (int t = 0; t < n; ++t) {
     uint64_t b;
@@ -2939,6 +3411,8 @@ int ensure_jumps(frw_ctx* ctx, Engine& E, int n, DJump* out) {
   // more divergence between jumping and stepping lanes
   out->twice = 0;
   if (const char* e = std::getenv("FRW_MW_JUMP_TWICE")) out->twice = std::atoi(e);
+  out->hom = 1;  // homogeneous-ball jumps (mw_hom_radius); FRW_MW_HOMJUMP=0 turns them off
+  if (const char* e = std::getenv("FRW_MW_HOMJUMP")) out->hom = std::atoi(e);
   out->meta = E.d_jmeta;
   out->thr = E.d_jthr;
   out->guide = E.d_jguide;
@@ -3023,8 +3497,8 @@ int resolve_misses(frw_ctx* ctx, Engine& E, int n, unsigned long long nmiss, frw
 
 // device bytes of one resident walk slot (slot arrays, job, queues, rings,
 // restart lists; ensure_slots)
-constexpr size_t kSlotBytes = 1 + 8 + 24 + 8 + 8 + 4 + 4 + 4 + 8 + 1 + 1 + 32 + 1 + 8 * KMAX + 1 +
-                              8 * kAtlasWords + 4 + 8 + 16 + 16 + 16 + 8;
+constexpr size_t kSlotBytes = 1 + 8 + 24 + 8 + 8 + 4 + 4 + 4 + 8 + 1 + 1 + 32 + 2 + 8 * KMAX + 1 +
+                              8 * kAtlasWords + 8 + 8 + 8 + 8 + 16 + 16 + 16 + 8 + 4;
 
 // Slot capacity only grows: calls of different sizes (the short last chunk
 // of a stopping rule, the single-transition API) reuse the pool, and the
@@ -3034,6 +3508,9 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   free_slots(E);
   DSlots& W = E.W;
   W.S = S;
+  W.jtail = S;
+  // job entries: one per slot, then one per resident k_tail lane
+  const size_t J = static_cast<size_t>(S) + static_cast<size_t>(ctx->sm_count) * kTailBlocks * 256;
   W.state = dalloc<uint8_t>(S);
   W.wid = dalloc<long long>(S);
   W.p = dalloc<double>(3 * size_t(S));
@@ -3045,12 +3522,16 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   W.mwsteps = dalloc<uint64_t>(S);
   W.branch = dalloc<uint8_t>(S);
   W.resampled = dalloc<uint8_t>(S);
-  W.cube = dalloc<double>(4 * size_t(S));
-  W.nbox = dalloc<uint8_t>(S);
-  W.boxes = dalloc<uint64_t>(size_t(S) * KMAX);
-  W.mwkind = dalloc<uint8_t>(S);
-  W.atlas = dalloc<uint64_t>(size_t(S) * kAtlasWords);
-  E.queue = dalloc<int>(S);
+  W.cube = dalloc<double>(4 * J);
+  W.nbox = dalloc<uint16_t>(J);
+  W.boxes = dalloc<uint64_t>(J * KMAX);
+  W.mwkind = dalloc<uint8_t>(J);
+  W.atlas = dalloc<uint64_t>(J * kAtlasWords);
+  E.mq[0] = dalloc<int>(S);
+  E.mq[1] = dalloc<int>(S);
+  W.mwnode = dalloc<uint32_t>(S);
+  W.mwhsteps = dalloc<int>(S);
+  W.mwhj = dalloc<uint64_t>(S);
   E.aq[0] = dalloc<int>(S);
   E.aq[1] = dalloc<int>(S);
   {
@@ -3065,9 +3546,11 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   E.M.retry = dalloc<long long>(2 * size_t(S));  // parks accumulate up to S/2 + S
   E.M.pend = dalloc<long long>(2 * size_t(S));
   E.M.park = dalloc<int>(2 * size_t(S));
+  E.M.dense = dalloc<int>(S);
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
       !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes ||
-      !W.atlas || !W.mwkind || !E.queue || !E.aq[0] || !E.aq[1] || !E.ring_a ||
+      !W.atlas || !W.mwkind || !E.mq[0] || !E.mq[1] || !W.mwnode || !W.mwhsteps || !W.mwhj || !E.aq[0] ||
+      !E.aq[1] || !E.ring_a || !E.M.dense ||
       !E.ring_m || !E.M.retry || !E.M.pend || !E.M.park) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
@@ -3919,6 +4402,8 @@ int frw_tally_allreduce(frw_ctx* ctx, void* comm, frw_tally* out) {
   out->sub[2] = mwe ? static_cast<uint64_t>(st[7]) : 0;
   out->sub[3] = fdm ? static_cast<uint64_t>(st[7]) : 0;
   out->mw_steps = static_cast<uint64_t>(st[8]);
+  out->mw_jumps = static_cast<uint64_t>(st[9]);
+  out->mw_jump_steps = static_cast<uint64_t>(st[10]);
   return FRW_OK;
 }
 
@@ -4011,9 +4496,20 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   DMiss M = E.M;
   // lattice jumps in plain MicroWalk hops only: MicroWalk-E cubes (with
   // their conductor faces) leave few jumps and lose 1-4% to the test
-  if (P.rng == FRW_RNG_PHILOX && P.mode != FRW_MODE_MWE && P.mode != FRW_MODE_HYBRID_MWE)
+  bool jumps = P.mode != FRW_MODE_MWE && P.mode != FRW_MODE_HYBRID_MWE;
+  if (const char* e = std::getenv("FRW_MWE_JUMPS")) jumps = jumps || std::atoi(e) != 0;
+  if (P.rng == FRW_RNG_PHILOX && jumps)
     if (int rc = ensure_jumps(ctx, E, P.n, &P.jump)) return rc;
 
+  {  // dense-hop grids (k_mw_dense), one per persistent CTA
+    const size_t need = static_cast<size_t>(ctx->sm_count) * P.n * P.n * P.n;
+    if (E.dense_cap < need) {
+      cudaFree(E.dense_scratch);
+      E.dense_scratch = dalloc<uint16_t>(need);
+      E.dense_cap = E.dense_scratch ? need : 0;
+      if (!E.dense_scratch) return frw_fail(ctx, FRW_ENOMEM, "run_walks: dense scratch allocation failed");
+    }
+  }
   FRW_CUDA(ctx, cudaMemsetAsync(E.W.state, 0, S, ctx->stream));
   FRW_CUDA(ctx, cudaMemsetAsync(E.recs, 0, sizeof(WalkRec) * count, ctx->stream));
   FRW_CUDA(ctx, cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), ctx->stream));
@@ -4027,6 +4523,15 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   // warp-specialised k_flow (C3/C5 within a few % either way)
   const char* tk = std::getenv("FRW_TAIL_KERNEL");
   const bool use_flow = tk && std::strcmp(tk, "flow") == 0;
+  // time slices of the wavefront rounds: a MicroWalk hop
+  // gets kMwSlice super-steps per k_mw visit and a walk kAdvSlice
+  // transitions per k_advance visit, then continues next round, so a round
+  // costs its throughput, not its longest hop; FRW_MW_SLICE /
+  // FRW_ADV_SLICE override (0: unlimited).  k_flow takes no carried hops.
+  P.mw_slice = use_flow || P.mode == FRW_MODE_FDM ? 0 : kMwSlice;
+  P.adv_slice = kAdvSlice;
+  if (const char* e = std::getenv("FRW_MW_SLICE")) P.mw_slice = use_flow ? 0 : std::atoi(e);
+  if (const char* e = std::getenv("FRW_ADV_SLICE")) P.adv_slice = std::atoi(e);
   bool tail = false;
   float mw_ms = 0;
   uint64_t misses_total = 0, restarts = 0, resumes = 0;
@@ -4036,6 +4541,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
            E.sgf.d_data, E.sgf.d_uentry};
     int* aq_in = E.aq[round & 1];
     int* aq_out = E.aq[(round + 1) & 1];
+    int* mq_in = E.mq[round & 1];
+    int* mq_next = E.mq[(round + 1) & 1];
     if (trace) cudaEventRecord(a0, ctx->stream);
     k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in);
     if (tail) {
@@ -4054,26 +4561,35 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
               s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
       } else if (P.rng == FRW_RNG_PHILOX)
         k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M,
-                                                           aq_in);
+                                                           aq_in, mq_in);
       else
         k_tail<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs,
-                                                                    E.d_cnt, M, aq_in);
+                                                                    E.d_cnt, M, aq_in, mq_in);
     } else {
       k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in,
-                                                   E.queue);
+                                                   mq_in, aq_out);
       cudaEventRecord(m0, ctx->stream);
       if (P.mode == FRW_MODE_FDM) {
-        const FdmQueue Q{E.queue, &E.d_cnt->qlen, &E.d_cnt->qhead, aq_out, &E.d_cnt->a2len};
+        const FdmQueue Q{mq_in, &E.d_cnt->qlen, &E.d_cnt->qhead, aq_out, &E.d_cnt->a2len};
         if (int rc = launch_fdm(ctx, E, s, P, E.d_cnt, Q)) {
           status = rc;
           break;
         }
       } else if (P.rng == FRW_RNG_PHILOX)
         k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, Wc, E.recs, E.d_cnt,
-                                                               E.queue, aq_out);
+                                                               mq_in, aq_out, mq_next);
       else
-        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(s, P, Wc, E.recs,
-                                                                        E.d_cnt, E.queue, aq_out);
+        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(
+            s, P, Wc, E.recs, E.d_cnt, mq_in, aq_out, mq_next);
+    }
+    // hops with more than KMAX boxes in their cube (exits 0 at once if none)
+    if (P.mode != FRW_MODE_FDM) {
+      if (P.rng == FRW_RNG_PHILOX)
+        k_mw_dense<FRW_RNG_PHILOX><<<ctx->sm_count, 256, 0, ctx->stream>>>(
+            s, P, Wc, E.recs, E.d_cnt, M.dense, aq_out, E.dense_scratch);
+      else
+        k_mw_dense<FRW_RNG_SPLITMIX_PARITY><<<ctx->sm_count, 256, 0, ctx->stream>>>(
+            s, P, Wc, E.recs, E.d_cnt, M.dense, aq_out, E.dense_scratch);
     }
     cudaEventRecord(m1, ctx->stream);
     FRW_CUDA(ctx, cudaGetLastError());
@@ -4088,9 +4604,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         float ams = 0;
         cudaEventElapsedTime(&ams, a0, m0);
         std::fprintf(stderr,
-                     "round %d: active %llu mw %llu next-active %llu done %llu misses %llu "
-                     "spawn+advance %.3f ms %s %.3f ms\n",
-                     round, c.alen, c.qlen, c.a2len, c.done, c.nmiss, ams, tail ? "tail" : "mw", ms);
+                     "round %d: active %llu mw %llu next-active %llu carried %llu dense %llu "
+                     "done %llu misses %llu spawn+advance %.3f ms %s %.3f ms\n",
+                     round, c.alen, c.qlen, c.a2len, c.q2len, c.dqlen, c.done, c.nmiss, ams,
+                     tail ? "tail" : "mw", ms);
       }
     }
     if (c.err) {
@@ -4099,12 +4616,12 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                status == FRW_ESTEPCAP
                    ? "microwalk transit exceeded the step cap; the lattice is malformed"
                    : "walk engine: geometry error (point outside the world or inside a "
-                     "conductor, or more than 32 dielectric boxes in one cube)");
+                     "conductor, or FDM mode on a cube with more than 64 boxes)");
       break;
     }
     const bool all_spawned = c.next >= static_cast<unsigned long long>(count) &&
                              c.pend_head >= c.npend;
-    const bool idle = all_spawned && c.a2len == 0;
+    const bool idle = all_spawned && c.a2len == 0 && c.q2len == 0;
     // Table misses are resolved lazily: parked walks wait while the others
     // run on, so the keys of a whole run are solved in a few batches instead
     // of one host round trip per discovering round.  Resolve when nothing
@@ -4131,8 +4648,11 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       upd.alen = c.a2len + c.npark;
       upd.ahead = 0;
       upd.a2len = 0;
-      upd.qlen = 0;
+      upd.qlen = c.q2len;  // the carried MicroWalk hops open the next round's queue
       upd.qhead = 0;
+      upd.q2len = 0;
+      upd.dqlen = 0;
+      upd.dqhead = 0;
       FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cnt, &upd, sizeof upd, cudaMemcpyHostToDevice,
                                     ctx->stream));
       restarts += c.nretry;
@@ -4148,7 +4668,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       break;
     }
     // few walks left: run them to completion in one launch
-    if (all_spawned && c.a2len <= tail_threshold && P.mode != FRW_MODE_FDM) tail = true;
+    if (all_spawned && c.a2len + c.q2len <= tail_threshold && P.mode != FRW_MODE_FDM)
+      tail = true;
     k_round<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
   }
   if (status == FRW_OK) {
@@ -4237,6 +4758,11 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     out->mw_general_steps = cfin.gen_steps;
     out->mw_cell_changes = cfin.cell_chg;
     out->mw_jumps = cfin.jumps;
+    out->mw_jump_steps = cfin.jsteps;
+    out->mw_dense_hops = cfin.dense_hops;
+    // the jump counters join the packed tally (stats slots 9, 10)
+    const double js[2] = {static_cast<double>(cfin.jumps), static_cast<double>(cfin.jsteps)};
+    FRW_CUDA(ctx, cudaMemcpy(E.pack + 3 * nslots + 9, js, sizeof js, cudaMemcpyHostToDevice));
     float tot = 0;
     cudaEventElapsedTime(&tot, t0, t1);
     out->total_ms = tot;

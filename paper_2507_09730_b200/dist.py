@@ -68,7 +68,8 @@ def pack(t: dict) -> np.ndarray:
     return np.concatenate([np.asarray(t["sum"], np.float64), np.asarray(t["sumsq"], np.float64),
                            np.asarray(t["landed"], np.float64),
                            np.array([t["aborted"], t["resampled"], *t["first"], *t["sub"],
-                                     t["mw_steps"], t["walks"]], np.float64)])
+                                     t["mw_steps"], t["walks"], t.get("mw_jumps", 0),
+                                     t.get("mw_jump_steps", 0)], np.float64)])
 
 
 def unpack(v: np.ndarray, like: dict) -> dict:
@@ -79,7 +80,8 @@ def unpack(v: np.ndarray, like: dict) -> dict:
                landed=np.rint(v[2 * k:3 * k]).astype(np.uint64),
                aborted=int(st[0]), resampled=int(st[1]),
                first=[int(x) for x in st[2:6]], sub=[int(x) for x in st[6:10]],
-               mw_steps=int(st[10]), walks=int(st[11]))
+               mw_steps=int(st[10]), walks=int(st[11]), mw_jumps=int(st[12]),
+               mw_jump_steps=int(st[13]))
     return out
 
 
@@ -137,7 +139,8 @@ def result_from_tally(t: dict, ids: list[int], master: int) -> dict:
                 dispatch_stats=dict(
                     first=dict(stratified=f[0], shrunk=f[1], layered=f[2], homogenized=f[3]),
                     subsequent=dict(cached=s[0], microwalk=s[1], microwalk_e=s[2], fdm=s[3])),
-                mw_steps=int(t["mw_steps"]))
+                mw_steps=int(t["mw_steps"]), mw_jumps=int(t.get("mw_jumps", 0)),
+                mw_jump_steps=int(t.get("mw_jump_steps", 0)))
 
 
 def extract_sharded(text: str, walks: int, group=None, runner=None, device: int | None = None,

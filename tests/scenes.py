@@ -61,3 +61,26 @@ def scene_from_doc(doc):
     w = doc["world"]
     return Scene(ids, cb, db, de, float(doc.get("background_eps", 1.0)),
                  np.array(w["lo"] + w["hi"], float), int(doc["master"]))
+
+
+def block_array_scene(nx=10, edge=30.0, pitch=70.0, seed=9, distinct=True):
+    """Two plates 800 nm apart with an nx^3 array of small dielectric blocks
+    between them (edge 30 nm, pitch 70 nm), each block its own permittivity
+    (distinct=True: nx^3 distinct values, far more than 63): a transition
+    cube in the gap holds far more than 64 boxes, so its MicroWalk hop runs
+    on the dense grid and the palette exceeds the shared-memory pair table."""
+    from paper_2507_09730_b200.workloads import SplitMix64
+    r = SplitMix64(seed, 0)
+    span = (nx - 1) * pitch + edge
+    lo0 = -span / 2
+    boxes, eps = [], []
+    for k in range(nx):
+        for j in range(nx):
+            for i in range(nx):
+                lo = [lo0 + i * pitch, lo0 + j * pitch, lo0 + k * pitch]
+                boxes.append(lo + [v + edge for v in lo])
+                eps.append(2.0 + 20.0 * r.uniform() if distinct else 7.0)
+    cond = np.array([[-600, -600, -600, -400, 600, 600], [400, -600, -600, 600, 600, 600]],
+                    float)
+    return Scene(np.array([1, 2], np.int32), cond, np.array(boxes), np.array(eps), 1.0,
+                 np.array([-3000, -3000, -3000, 3000, 3000, 3000.0]), 1)
