@@ -106,6 +106,40 @@ def build_cpp_lib(force=False):
     return out
 
 
+REF_TESTS = ("test_geometry", "test_cache", "test_engine")
+
+
+def build_ref_unit_tests(force=False):
+    """The reference's own doctest suites (proj/tests/test_{geometry,cache,
+    engine}.cpp, compiled in place and unchanged) against the C++ frwcap
+    mirror (csrc/host, forwarding headers csrc/host/frwcap/*.hpp), with the
+    doctest stand-in tests/cpp/doctest_shim: the C++ source-level drop-in
+    check.  Binaries go to tests/cpp/_bin (git-ignored; they travel to the
+    GPU box).  Needs /root/reference (present in the build container only)."""
+    ref = "/root/reference/proj/tests"
+    if not os.path.isdir(ref):
+        return []
+    out_dir = os.path.join(ROOT, "tests", "cpp", "_bin")
+    os.makedirs(out_dir, exist_ok=True)
+    json_inc = os.path.join(sysconfig.get_paths()["purelib"],
+                            "include/cudnn_frontend/thirdparty/nlohmann")
+    shim = os.path.join(ROOT, "tests", "cpp", "doctest_shim")
+    lib = os.path.join(LIB, "libfrwcap.so")
+    inc = ["-I", shim, "-I", os.path.join(CSRC, "host"), "-I", os.path.join(ROOT, "include"),
+           "-I", json_inc]
+    built = []
+    for t in REF_TESTS:
+        exe = os.path.join(out_dir, t)
+        srcs = [os.path.join(ref, "doctest_main.cpp"), os.path.join(ref, t + ".cpp")]
+        deps = srcs + [lib, os.path.join(shim, "doctest.h")] + \
+            glob.glob(os.path.join(CSRC, "host", "*.hpp"))
+        if force or _stale(exe, deps):
+            _run(["g++", "-O2", "-std=c++20", "-ffp-contract=off", *inc, "-o", exe, *srcs,
+                  "-L", LIB, "-lfrwcap", "-lfrwgpu", "-Wl,-rpath," + LIB, "-lpthread"])
+        built.append(exe)
+    return built
+
+
 def build_oracle(with_ref=None):
     tgts = ["all"]
     if with_ref is None:
@@ -120,6 +154,7 @@ def build_all(force=False):
     build_core(force)
     build_cpp_lib(force)
     build_oracle()
+    build_ref_unit_tests(force)
 
 
 if __name__ == "__main__":

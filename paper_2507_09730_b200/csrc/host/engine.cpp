@@ -232,7 +232,7 @@ void Engine::upload(frw_ctx* ctx) const {
     T.n = cfg_.grid_n;
   }
   for (const auto& [k, g] : cache_->entries())
-    if (k.n == cfg_.grid_n) put_entry(ctx, k, *g);
+    if (k.n == cfg_.grid_n && !k.expanded && !k.conductor_sig) put_entry(ctx, k, *g);
 }
 
 frw_walk_params Engine::params() const {

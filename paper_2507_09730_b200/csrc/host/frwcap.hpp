@@ -145,6 +145,15 @@ void classify_grid(DielectricGrid& g);
 DielectricGrid build_grid(const Structure& s, const Cube& cube, int n,
                           bool allow_conductors = false);
 
+// stratification probe of a cube (geometry.hpp:184-196): the permittivity
+// depends on `axis` only; layers[t] at the centre of slice t
+struct StratifiedProfile {
+  int axis = 0;
+  std::vector<double> layers;
+  bool uniform() const;  // every layer eps_equal to the first
+};
+std::optional<StratifiedProfile> stratified_profile(const Structure& s, const Cube& cube, int n);
+
 // ---- lattice and panel algebra (sgf.hpp:24-61, sgf.cpp:13-55) ---------------
 inline constexpr int kDirAxis[6] = {0, 0, 1, 1, 2, 2};
 inline constexpr int kDirSign[6] = {-1, +1, -1, +1, -1, +1};
@@ -214,6 +223,7 @@ struct DiscreteSGF {
   double pitch = 1.0;
   std::vector<double> probs, cdf;
   std::array<std::vector<double>, 3> grad_kernels;
+  bool has_kernels() const { return !grad_kernels[0].empty(); }
 };
 
 class SolveError : public std::runtime_error {
@@ -225,17 +235,30 @@ class SolveError : public std::runtime_error {
 
 double round_sig(double x, int digits);
 
+// sgf_cache.hpp:20-48: the identity of a solved canonical SGF.  `expanded`
+// and `conductor_sig` key MicroWalk-E / masked-grid solves; the walk engine's
+// device table holds the plain stratified keys only.
 struct ProfileKey {
   int n = 0;
   int axis = 0;
   std::vector<double> layers;  // rounded to 6 significant digits
+  bool expanded = false;
+  std::optional<uint64_t> conductor_sig;
   bool operator==(const ProfileKey&) const = default;
 };
 struct ProfileKeyHash {
   size_t operator()(const ProfileKey& k) const;
 };
-ProfileKey profile_key(int n, int axis, const std::vector<double>& layers);
+ProfileKey profile_key(int n, int axis, const std::vector<double>& layers, bool expanded = false,
+                       std::optional<uint64_t> conductor_sig = {});
+ProfileKey profile_key(const StratifiedProfile& profile, int n);
+// from a materialised Uniform or Stratified grid; throws on General
+ProfileKey profile_key(const DielectricGrid& grid);
+// order-sensitive hash of a grid's conductor mask, for keys of masked grids
+uint64_t conductor_signature(const DielectricGrid& grid);
 
+// unit-pitch grid of a key's layers; throws for conductor-signature keys
+DielectricGrid canonical_grid(const ProfileKey& key);
 // canonical unit-pitch solve of a key (sgf_cache.cpp:78-131 + sgf.cpp:231-290)
 DiscreteSGF solve_canonical(const ProfileKey& key, bool with_kernels = true, int device = 0);
 
@@ -244,6 +267,9 @@ class StratifiedSgfCache {
   explicit StratifiedSgfCache(size_t capacity = 0) : capacity_(capacity) {}
   void set_device(int device) { device_ = device; }
   std::shared_ptr<const DiscreteSGF> get(const ProfileKey& key);
+  // a miss solves the caller's (Uniform or Stratified) grid instead
+  std::shared_ptr<const DiscreteSGF> get(const ProfileKey& key,
+                                         const std::function<DielectricGrid()>& provider);
   std::shared_ptr<const DiscreteSGF> find(const ProfileKey& key) const;
   // solves the missing keys (one device batch per lattice size)
   void solve_many(const std::vector<ProfileKey>& keys, int threads = 0);
@@ -466,6 +492,34 @@ CapacitanceResult extract(const Structure& s, const Config& cfg, int threads = 0
 // (assemble_system + solve_sgf + expected_steps, sgf.cpp:57-299)
 DiscreteSGF solve_sgf(const DielectricGrid& g, bool with_kernels = true, int device = 0);
 double expected_steps(const DielectricGrid& g, int device = 0);
+// FD system of a materialised grid (sgf.hpp:75-101).  The B200 build
+// assembles s_ii matrix-free on the device, so the system is the grid it is
+// built from; solve_sgf / expected_steps of it run the device solver.
+struct FDSystem {
+  DielectricGrid grid;
+  int n = 0;
+};
+FDSystem assemble_system(const DielectricGrid& g);
+DiscreteSGF solve_sgf(const FDSystem& sys, bool with_kernels = true);
+double expected_steps(const FDSystem& sys);
+
+// Empirical-vs-exact comparison (oracle.hpp:38-52; validation machinery on
+// the host): total variation plus a chi-square statistic over bins pooled to
+// an expected count >= 5 (an undersized tail joins the previous group),
+// against the Wilson-Hilferty critical value at p = 1e-3.
+struct DistributionReport {
+  std::vector<double> exact;
+  std::vector<double> empirical;
+  double tv_distance = 0;
+  double gof_statistic = 0;
+  double gof_critical = 0;
+  int pooled_bins = 0;
+  long samples = 0;
+  bool gof_pass() const { return gof_statistic <= gof_critical; }
+};
+DistributionReport compare_distribution(const std::vector<double>& exact,
+                                        const std::function<int(SplitMix64&)>& sampler,
+                                        long n_samples, SplitMix64& rng);
 // oracle.cpp:300-339 test lattices: exponential(mean 10) permittivities
 DielectricGrid random_voxel_grid(int n, SplitMix64& rng);
 DielectricGrid random_block_grid(int n, int blocks, SplitMix64& rng);

@@ -1,0 +1,6 @@
+// frwcap/sgf_cache.hpp -- source-level drop-in for the reference header
+// proj/include/frwcap/sgf_cache.hpp: the B200 build declares the whole frwcap API in
+// one header (../frwcap.hpp), so callers of the reference that include
+// "frwcap/sgf_cache.hpp" compile unchanged against it.
+#pragma once
+#include "../frwcap.hpp"

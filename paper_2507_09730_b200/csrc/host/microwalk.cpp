@@ -10,6 +10,7 @@
 // exactly (its raw state goes in, state + steps * gamma comes out), so
 // results are bit-identical to the reference for the same stream.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -200,6 +201,44 @@ void classify_grid(DielectricGrid& g) {
   }
   g.tag = GridTag::General;
   g.strat_axis = -1;
+}
+
+bool StratifiedProfile::uniform() const {
+  return std::all_of(layers.begin(), layers.end(),
+                     [&](double e) { return eps_equal(e, layers.front()); });
+}
+
+// geometry.cpp:357-396: the field inside the cube depends on one axis only
+// when every dielectric meeting the OPEN cube spans the cube's cross-section
+// perpendicular to it; the first such axis is read at the slice centres
+std::optional<StratifiedProfile> stratified_profile(const Structure& s, const Cube& cube, int n) {
+  const Box cb = cube.box();
+  std::array<bool, 3> spans{true, true, true};
+  bool met = false;
+  for (const Dielectric& d : s.dielectrics) {
+    if (!d.box.intersects_open(cb)) continue;
+    met = true;
+    for (int a = 0; a < 3; ++a)
+      for (int b : {(a + 1) % 3, (a + 2) % 3})
+        spans[a] = spans[a] && d.box.lo[b] <= cb.lo[b] && d.box.hi[b] >= cb.hi[b];
+  }
+  int axis = 0;  // the background alone: uniform
+  if (met) {
+    const auto it = std::find(spans.begin(), spans.end(), true);
+    if (it == spans.end()) return std::nullopt;
+    axis = static_cast<int>(it - spans.begin());
+  }
+  StratifiedProfile prof;
+  prof.axis = axis;
+  prof.layers.resize(n);
+  const double pitch = 2.0 * cube.half_width / n;
+  for (int t = 0; t < n; ++t) {
+    Vec3 p = cube.center;
+    p[axis] = cube.center[axis] - cube.half_width + (t + 0.5) * pitch;
+    prof.layers[t] = s.permittivity_at(p);
+  }
+  if (prof.uniform()) prof.axis = 0;
+  return prof;
 }
 
 DielectricGrid build_grid(const Structure& s, const Cube& cube, int n, bool allow_conductors) {
@@ -482,15 +521,108 @@ DiscreteSGF solve_sgf(const DielectricGrid& g, bool with_kernels, int device) {
   out.pitch = g.pitch();
   out.probs.resize(P);
   std::vector<double> ker(with_kernels ? 3 * P : 0);
-  throw_status(ctx, frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width,
-                                       out.probs.data(), with_kernels ? ker.data() : nullptr,
-                                       nullptr));
+  DielectricGrid cls;  // the grid's own classification (callers may not have run it)
+  cls.n = g.n;
+  cls.cube = g.cube;
+  cls.eps = g.eps;
+  classify_grid(cls);
+  bool exact = cls.tag != GridTag::General;  // (classify_grid compares at rel-tol 1e-9)
+  if (exact) {
+    const int ax = cls.tag == GridTag::Stratified ? cls.strat_axis : 0;
+    for (int k = 0; k < g.n && exact; ++k)
+      for (int j = 0; j < g.n && exact; ++j)
+        for (int i = 0; i < g.n && exact; ++i) {
+          const int t = ax == 0 ? i : (ax == 1 ? j : k);
+          exact = g.eps_at(i, j, k) ==
+                  g.eps_at(ax == 0 ? t : 0, ax == 1 ? t : 0, ax == 2 ? t : 0);
+        }
+  }
+  if (exact) {
+    // a stratified (or uniform) grid is the separable system the stratified
+    // cache solves: the same exact direct solver (frw_sgf_solve), so a
+    // cached key and the solve of its canonical grid agree bit for bit;
+    // its unit-pitch kernels scale with 1 / pitch
+    const int axis = cls.tag == GridTag::Stratified ? cls.strat_axis : 0;
+    std::vector<double> layers(g.n);
+    for (int t = 0; t < g.n; ++t)
+      layers[t] = g.eps_at(axis == 0 ? t : 0, axis == 1 ? t : 0, axis == 2 ? t : 0);
+    throw_status(ctx, frw_sgf_solve(ctx, g.n, 1, &axis, layers.data(), out.probs.data(),
+                                    with_kernels ? ker.data() : nullptr));
+    if (with_kernels && out.pitch != 1.0)
+      for (double& k : ker) k /= out.pitch;
+  } else {
+    throw_status(ctx, frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width,
+                                         out.probs.data(), with_kernels ? ker.data() : nullptr,
+                                         nullptr));
+  }
   out.cdf.resize(P);
   double run = 0;
   for (size_t b = 0; b < P; ++b) out.cdf[b] = run += out.probs[b];
   if (with_kernels)
     for (int a = 0; a < 3; ++a) out.grad_kernels[a].assign(ker.begin() + a * P, ker.begin() + (a + 1) * P);
   return out;
+}
+
+FDSystem assemble_system(const DielectricGrid& g) {
+  if (g.n < 1 || g.eps.size() != static_cast<size_t>(g.n) * g.n * g.n)
+    throw std::invalid_argument("assemble_system: malformed grid");
+  FDSystem s;
+  s.grid = g;
+  s.n = g.n;
+  return s;
+}
+
+DiscreteSGF solve_sgf(const FDSystem& sys, bool with_kernels) {
+  return solve_sgf(sys.grid, with_kernels);
+}
+
+double expected_steps(const FDSystem& sys) { return expected_steps(sys.grid); }
+
+DistributionReport compare_distribution(const std::vector<double>& exact,
+                                        const std::function<int(SplitMix64&)>& sampler,
+                                        long n_samples, SplitMix64& rng) {
+  if (n_samples < 10000) throw std::invalid_argument("compare_distribution: too few samples");
+  DistributionReport r;
+  r.exact = exact;
+  r.samples = n_samples;
+  std::vector<long> hist(exact.size(), 0);
+  for (long i = 0; i < n_samples; ++i) ++hist.at(static_cast<size_t>(sampler(rng)));
+  r.empirical.resize(exact.size());
+  for (size_t b = 0; b < exact.size(); ++b) {
+    r.empirical[b] = static_cast<double>(hist[b]) / n_samples;
+    r.tv_distance += std::fabs(r.empirical[b] - exact[b]);
+  }
+  r.tv_distance *= 0.5;
+  // consecutive bins pooled to an expected count >= 5; the tail joins the
+  // last group (or forms one when there is none)
+  std::vector<double> obs, expct;
+  double o = 0, e = 0;
+  for (size_t b = 0; b < exact.size(); ++b) {
+    e += exact[b] * n_samples;
+    o += static_cast<double>(hist[b]);
+    if (e >= 5.0) {
+      obs.push_back(o);
+      expct.push_back(e);
+      o = e = 0;
+    }
+  }
+  if (o > 0 || e > 0) {
+    if (obs.empty()) {
+      obs.push_back(o);
+      expct.push_back(std::max(e, 1e-12));
+    } else {
+      obs.back() += o;
+      expct.back() += e;
+    }
+  }
+  for (size_t k = 0; k < obs.size(); ++k)
+    r.gof_statistic += (obs[k] - expct[k]) * (obs[k] - expct[k]) / expct[k];
+  r.pooled_bins = static_cast<int>(obs.size());
+  // Wilson-Hilferty: chi2_{1-p}(d) ~ d (1 - 2/(9d) + z sqrt(2/(9d)))^3, z = 3.0902
+  const double d = std::max(r.pooled_bins - 1, 1);
+  const double w = 1.0 - 2.0 / (9.0 * d) + 3.090232306167813 * std::sqrt(2.0 / (9.0 * d));
+  r.gof_critical = d * w * w * w;
+  return r;
 }
 
 double expected_steps(const DielectricGrid& g, int device) {

@@ -42,12 +42,15 @@ uint64_t mix64(uint64_t z) {
 }  // namespace
 
 size_t ProfileKeyHash::operator()(const ProfileKey& k) const {
-  uint64_t h = mix64((static_cast<uint64_t>(k.n) << 8) ^ static_cast<uint64_t>(k.axis));
+  uint64_t h = mix64((static_cast<uint64_t>(k.n) << 8) ^ static_cast<uint64_t>(k.axis) ^
+                     (static_cast<uint64_t>(k.expanded) << 40));
   for (double v : k.layers) h = mix64(h ^ std::bit_cast<uint64_t>(v));
+  if (k.conductor_sig) h = mix64(h ^ *k.conductor_sig ^ 0x5bd1e995ull);
   return static_cast<size_t>(h);
 }
 
-ProfileKey profile_key(int n, int axis, const std::vector<double>& layers) {
+ProfileKey profile_key(int n, int axis, const std::vector<double>& layers, bool expanded,
+                       std::optional<uint64_t> conductor_sig) {
   if (static_cast<int>(layers.size()) != n)
     throw std::invalid_argument("profile_key: expected one layer per slice");
   if (axis < 0 || axis > 2) throw std::invalid_argument("profile_key: axis out of range");
@@ -57,8 +60,34 @@ ProfileKey profile_key(int n, int axis, const std::vector<double>& layers) {
   for (double v : layers) k.layers.push_back(round_sig(v, 6));
   bool uniform = true;
   for (double v : k.layers) uniform = uniform && v == k.layers[0];
-  if (uniform) k.axis = 0;
+  if (uniform) k.axis = 0;  // sgf_cache.cpp:40-42
+  k.expanded = expanded;
+  k.conductor_sig = conductor_sig;
   return k;
+}
+
+ProfileKey profile_key(const StratifiedProfile& profile, int n) {
+  return profile_key(n, profile.axis, profile.layers);
+}
+
+ProfileKey profile_key(const DielectricGrid& grid) {
+  if (grid.tag == GridTag::General)
+    throw std::invalid_argument("profile_key: grid is not stratified");
+  const int axis = grid.tag == GridTag::Stratified ? grid.strat_axis : 0;
+  std::vector<double> layers(grid.n);
+  for (int t = 0; t < grid.n; ++t)  // the layer along the axis, at (0, 0) across
+    layers[t] = grid.eps_at(axis == 0 ? t : 0, axis == 1 ? t : 0, axis == 2 ? t : 0);
+  return profile_key(grid.n, axis, layers);
+}
+
+uint64_t conductor_signature(const DielectricGrid& grid) {
+  uint64_t h = mix64(static_cast<uint64_t>(grid.n));
+  if (!grid.has_mask()) return h;
+  for (size_t i = 0; i < grid.conductor_mask.size(); ++i)
+    if (grid.conductor_mask[i] >= 0)
+      h = mix64(h ^ (static_cast<uint64_t>(i) << 32 ^
+                     static_cast<uint32_t>(grid.conductor_mask[i])));
+  return h;
 }
 
 
@@ -147,9 +176,48 @@ std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::get(const ProfileKey& key
     }
     ++misses_;
   }
+  if (key.conductor_sig)
+    throw std::invalid_argument("canonical_grid: a conductor signature cannot be reconstructed");
   auto sgf = solve_keys({key}, true, device_)[0];
   std::lock_guard<std::mutex> lk(mu_);
   return store_locked(key, std::move(sgf));
+}
+
+std::shared_ptr<const DiscreteSGF> StratifiedSgfCache::get(
+    const ProfileKey& key, const std::function<DielectricGrid()>& provider) {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = map_.find(key);
+    if (it != map_.end()) {
+      ++hits_;
+      touch(it->second);
+      return it->second.sgf;
+    }
+    ++misses_;
+  }
+  const DielectricGrid g = provider();
+  if (g.tag == GridTag::General)
+    throw std::invalid_argument("StratifiedSgfCache::get: the provided grid is General");
+  auto sgf = std::make_shared<DiscreteSGF>(solve_sgf(g, true, device_));
+  std::lock_guard<std::mutex> lk(mu_);
+  return store_locked(key, std::move(sgf));
+}
+
+DielectricGrid canonical_grid(const ProfileKey& key) {
+  if (key.conductor_sig)
+    throw std::invalid_argument("canonical_grid: a conductor signature cannot be reconstructed");
+  if (key.n < 1 || static_cast<int>(key.layers.size()) != key.n || key.axis < 0 || key.axis > 2)
+    throw std::invalid_argument("canonical_grid: malformed key");
+  DielectricGrid g;
+  g.n = key.n;
+  g.cube = {{0, 0, 0}, key.n / 2.0};  // unit pitch (sgf_cache.cpp:78-96)
+  g.eps.resize(static_cast<size_t>(key.n) * key.n * key.n);
+  for (int k = 0; k < key.n; ++k)
+    for (int j = 0; j < key.n; ++j)
+      for (int i = 0; i < key.n; ++i)
+        g.eps[g.index(i, j, k)] = key.layers[key.axis == 0 ? i : (key.axis == 1 ? j : k)];
+  classify_grid(g);
+  return g;
 }
 
 void StratifiedSgfCache::solve_many(const std::vector<ProfileKey>& keys, int /*threads*/) {
@@ -249,9 +317,9 @@ void StratifiedSgfCache::save(const std::string& path, int only_n) const {
   for (const auto& [k, v] : all) {
     if (only_n > 0 && k.n != only_n) continue;
     put_u32(o, static_cast<uint32_t>(k.axis));
-    o.push_back(0);
-    o.push_back(0);
-    put_u64(o, 0);
+    o.push_back(k.expanded ? 1 : 0);
+    o.push_back(k.conductor_sig ? 1 : 0);
+    put_u64(o, k.conductor_sig.value_or(0));
     put_u32(o, static_cast<uint32_t>(k.layers.size()));
     for (double x : k.layers) put_f64(o, x);
     put_f64(o, v->pitch);
@@ -287,9 +355,10 @@ size_t StratifiedSgfCache::load(const std::string& path) {
     key.n = n;
     key.axis = static_cast<int>(r.uint(4));
     if (key.axis < 0 || key.axis > 2) throw std::runtime_error("SGF cache: bad axis");
-    const bool expanded = r.uint(1) != 0;
+    key.expanded = r.uint(1) != 0;
     const bool has_sig = r.uint(1) != 0;
-    r.uint(8);
+    const uint64_t sig = r.uint(8);
+    if (has_sig) key.conductor_sig = sig;
     if (static_cast<int>(r.uint(4)) != n) throw std::runtime_error("SGF cache: layer count mismatch");
     key.layers.resize(n);
     for (double& v : key.layers) v = r.f64();
@@ -317,9 +386,9 @@ size_t StratifiedSgfCache::load(const std::string& path) {
         for (double& v : g) ks += v = r.f64();
         if (std::fabs(ks) > 1e-9) throw std::runtime_error("SGF cache: kernel fails zero-sum check");
       }
-    // expanded / conductor-signature keys belong to the MicroWalk-E cache,
-    // which this build does not serve from the table; keep them out
-    if (!expanded && !has_sig) {
+    // (expanded / conductor-signature keys are kept and saved back; the
+    // walk engine's device table takes the plain stratified keys only)
+    {
       std::lock_guard<std::mutex> lk(mu_);
       store_locked(key, std::move(sgf));
       ++loaded;

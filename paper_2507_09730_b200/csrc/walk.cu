@@ -224,6 +224,9 @@ struct DCounters {
   unsigned long long q2len;      // MicroWalk queue of the next round (carried hops)
   unsigned long long dqlen, dqhead;  // dense MicroWalk hops of this round (k_mw_dense)
   unsigned long long dense_hops;     // dense hops run (all rounds)
+  // k_tail: warp cycles in MicroWalk super-steps / in the whole loop, for
+  // the MicroWalk share of the tail's device time (T_MW, engine.cpp:322-345)
+  unsigned long long tail_mw_cyc, tail_all_cyc;
 };
 
 constexpr int kMissMax = 4096;
@@ -2201,7 +2204,9 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     }
   };
   fetch();
+  long long cyc_mw = 0, cyc_all = 0;  // warp-uniform clock64 spans
   while (__any_sync(0xFFFFFFFFu, live)) {
+    const long long c0 = clock64();
     if (live && !in_mw) {
       // up to FRW_TAIL_CHAIN transitions back to back while they are cached
       // hops (each would otherwise wait out a whole MicroWalk stretch)
@@ -2219,6 +2224,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     // up to 32 super-steps per transition (a hop is ~50 super-steps): the
     // MicroWalk lanes run long stretches between the divergent transitions
     // (8: 1.64e7, 16: 1.76e7, 32: 1.76e7 C3 walks/s; C5 MWE best at 32)
+    const long long c1 = clock64();
 #pragma unroll 1
     for (int rep = 0; rep < FRW_TAIL_REPS; ++rep) {
       const unsigned mwm = __ballot_sync(0xFFFFFFFFu, live && in_mw);
@@ -2242,7 +2248,15 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       }
       fetch();
     }
+    const long long c2 = clock64();
+    cyc_mw += c2 - c1;
+    cyc_all += c2 - c0;
   }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&C->tail_mw_cyc, static_cast<unsigned long long>(cyc_mw));
+    atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_all));
+  }
+
   flush_mw_stats(C, L);
 }
 
@@ -4533,7 +4547,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   if (const char* e = std::getenv("FRW_MW_SLICE")) P.mw_slice = use_flow ? 0 : std::atoi(e);
   if (const char* e = std::getenv("FRW_ADV_SLICE")) P.adv_slice = std::atoi(e);
   bool tail = false;
-  float mw_ms = 0;
+  double mw_ms = 0;
+  unsigned long long tail_cyc_mw0 = 0, tail_cyc_all0 = 0;
   uint64_t misses_total = 0, restarts = 0, resumes = 0;
   int status = FRW_OK;
   for (int round = 0;; ++round) {
@@ -4599,7 +4614,19 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     {
       float ms = 0;
       cudaEventElapsedTime(&ms, m0, m1);
-      mw_ms += ms;
+      // T_MW: k_mw (and the dense hops) are MicroWalk only; of a k_tail
+      // launch only its warps' share of cycles in MicroWalk super-steps
+      if (tail) {
+        const double f = c.tail_all_cyc > tail_cyc_all0
+                             ? static_cast<double>(c.tail_mw_cyc - tail_cyc_mw0) /
+                                   static_cast<double>(c.tail_all_cyc - tail_cyc_all0)
+                             : 0.0;
+        tail_cyc_mw0 = c.tail_mw_cyc;
+        tail_cyc_all0 = c.tail_all_cyc;
+        mw_ms += f * ms;
+      } else {
+        mw_ms += ms;
+      }
       if (trace) {
         float ams = 0;
         cudaEventElapsedTime(&ams, a0, m0);
