@@ -342,7 +342,9 @@ def grid_config(name, count, args, rank, world, dist, torch, local, smem_peak, p
         tt = torch.tensor([e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_s = float(tt.item())
-    pr = prof.get((name, "mw_grid_fast")) or prof.get((name, "mw_grid_kernel")) or {}
+    two = os.environ.get("FRW_GRID_WPT", "2") != "1"
+    kname = "mw_grid_fast2" if two else "mw_grid_fast"
+    pr = prof.get((name, kname)) or prof.get((name, "mw_grid_fast")) or {}
     achieved = BYTES_PER_STEP * k_steps / (k_ms * 1e-3) / 1e9
     traffic = pr.get("dram_bytes_per_launch")
     if traffic is not None and pr.get("transits"):
@@ -359,7 +361,7 @@ def grid_config(name, count, args, rank, world, dist, torch, local, smem_peak, p
         "gpu_launches": args.steps,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak / 1e9,
                      "unit": "GB/s", "frac": achieved * 1e9 / smem_peak, "traffic": traffic,
-                     "kernel": "mw_grid_fast<PHILOX>", "kernel_ms": k_ms,
+                     "kernel": kname + "<PHILOX>", "kernel_ms": k_ms,
                      "algorithmic_bytes_per_launch": BYTES_PER_STEP * k_steps,
                      "steps_per_s": k_steps / (k_ms * 1e-3),
                      "peak_source": "frw_smem_bandwidth_probe (conflict-free LDS.128, all SMs), "

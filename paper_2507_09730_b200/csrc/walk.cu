@@ -70,6 +70,23 @@ constexpr double kMPerNm = 1e-9;            // constants.hpp:6
 
 
 
+// Device bounds checks (compute-sanitizer is unavailable on the GPU pool):
+// a build with -DFRW_DEBUG_CHECKS tests every queue push and pop, slot and
+// job index, walk record index, lattice node and table index below; the
+// first failure records its source line and fails the call (FRW_ECUDA,
+// "device check failed at walk.cu:LINE").  Compiled out by default.
+#ifdef FRW_DEBUG_CHECKS
+#define FRW_DCHECK(C, cond)                                                               \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      atomicCAS(&(C)->chk_line, 0ull, static_cast<unsigned long long>(__LINE__));         \
+      atomicCAS(&(C)->err, 0ull, static_cast<unsigned long long>(-FRW_ECUDA));                                                            \
+    }                                                                                     \
+  } while (0)
+#else
+#define FRW_DCHECK(C, cond) static_cast<void>(0)
+#endif
+
 enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3, S_MW_CARRY = 4 };
 
 
@@ -171,6 +188,8 @@ struct WalkRec {  // per walk id, written once when the walk terminates
 
 struct DSlots {
   int S;
+  int J;                 // job entries (slot capacity + tail lanes)
+  long long count;       // walk records of the call (FRW_DEBUG_CHECKS)
   int jtail;             // first job entry of the k_tail lanes (one per lane,
                          // after the capacity's slots: compiled, walked and
                          // re-compiled by the same lane, so they stay in L2)
@@ -227,6 +246,7 @@ struct DCounters {
   // k_tail: warp cycles in MicroWalk super-steps / in the whole loop, for
   // the MicroWalk share of the tail's device time (T_MW, engine.cpp:322-345)
   unsigned long long tail_mw_cyc, tail_all_cyc;
+  unsigned long long chk_line;   // FRW_DEBUG_CHECKS: line of the first failed device check
 };
 
 constexpr int kMissMax = 4096;
@@ -238,6 +258,7 @@ struct DMiss {
   long long* pend;  // [2S] walk ids to restart
   int* park;        // [2S] slots of walks parked mid-walk by a miss (resume)
   int* dense;       // [S] slots whose MicroWalk hop needs the dense grid (k_mw_dense)
+  long long cap;    // slot capacity (retry/pend/park hold 2 cap)
 };
 
 // ---------------------------------------------------------------------------
@@ -821,12 +842,15 @@ __device__ void record_miss(DCounters* C, const DMiss& M, int n, int axis, L lay
                             long long wid) {
   record_key(C, M, n, axis, layer);
   const unsigned long long r = atomicAdd(&C->nretry, 1ull);
+  FRW_DCHECK(C, r < 2ull * M.cap);
   M.retry[r] = wid;
 }
 
 __device__ __forceinline__ void set_err(DCounters* C, int code) {
   atomicCAS(&C->err, 0ull, static_cast<unsigned long long>(static_cast<unsigned>(-code)));
 }
+
+
 
 // ---------------------------------------------------------------------------
 // voxel-index clipping of the dielectric boxes for a lazy MicroWalk cube
@@ -1013,6 +1037,7 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
 // the cube is stored: the hop runs on a dense grid, k_mw_dense).
 __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
                               double h, int n, bool conductors, DCounters* C) {
+  FRW_DCHECK(C, slot >= 0 && slot < W.J);
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
   uint64_t* A = W.atlas + static_cast<size_t>(slot) * kAtlasWords;
   int K = 0, ncond = 0;
@@ -1257,6 +1282,7 @@ __device__ void finish_walk(const DSlots& W, WalkRec* recs, DCounters* C, int sl
   r.branch = W.branch[slot];
   r.resampled = W.resampled[slot];
   r.done = 1;
+  FRW_DCHECK(C, wid >= 0 && wid < W.count);
   recs[wid] = r;
   W.state[slot] = S_FREE;
   atomicAdd(&C->done, 1ull);
@@ -1330,7 +1356,9 @@ __global__ void k_spawn(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, D
     W.branch[slot] = static_cast<uint8_t>(fo.branch);
     W.rng[slot] = rng.s;
     W.state[slot] = S_ACTIVE;
-    aq[atomicAdd(&C->alen, 1ull)] = slot;
+    const unsigned long long qa = atomicAdd(&C->alen, 1ull);
+    FRW_DCHECK(C, qa < static_cast<unsigned long long>(W.S));
+    aq[qa] = slot;
   }
 }
 
@@ -1411,7 +1439,9 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
       W.hops[slot] = L.hops;
       W.cached[slot] = L.cached;
       W.state[slot] = S_PARKED;
-      M.park[atomicAdd(&C->npark, 1ull)] = slot;
+      const unsigned long long qp = atomicAdd(&C->npark, 1ull);
+      FRW_DCHECK(C, qp < 2ull * M.cap);
+      M.park[qp] = slot;
       return 1;
     }
     const double* data = T.data[e];
@@ -1475,7 +1505,9 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     W.hops[slot] = L.hops + 1;
     W.cached[slot] = L.cached;
     W.state[slot] = S_NEED_MW;
-    M.dense[atomicAdd(&C->dqlen, 1ull)] = slot;
+    const unsigned long long qd = atomicAdd(&C->dqlen, 1ull);
+    FRW_DCHECK(C, qd < static_cast<unsigned long long>(W.S));
+    M.dense[qd] = slot;
     return 1;
   }
   W.mwkind[L.jslot] = kind;
@@ -1486,13 +1518,22 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   W.hops[slot] = L.hops + 1;
   W.cached[slot] = L.cached;
   W.state[slot] = S_NEED_MW;
-  if (mq) mq[atomicAdd(&C->qlen, 1ull)] = slot;
+  if (mq) {
+    const unsigned long long qm = atomicAdd(&C->qlen, 1ull);
+    FRW_DCHECK(C, qm < static_cast<unsigned long long>(W.S));
+    mq[qm] = slot;
+  }
   return 2;
+}
+
+// (FRW_DEBUG_CHECKS) the lane's node lies in the lattice
+__device__ __forceinline__ bool node_ok(uint32_t node, int n) {
+  return coord(node, 0) < n && coord(node, 1) < n && coord(node, 2) < n;
 }
 
 // the walk goes back to the next round's ACTIVE queue
 __device__ __forceinline__ void mw_requeue(DCounters* C, int* aq_out, int slot) {
-  aq_out[atomicAdd(&C->a2len, 1ull)] = slot;
+  aq_out[atomicAdd(&C->a2len, 1ull)] = slot;  // (checked by the host: a2len <= S)
 }
 
 // persistent: each thread takes ACTIVE walks from the queue and advances
@@ -1509,7 +1550,10 @@ __global__ void __launch_bounds__(256, FRW_ADV_MINB)
   unsigned long long item = atomicAdd(&C->ahead, 1ull);
   bool live = item < alen;
   AdvLane L;
-  if (live) adv_load(W, aq[item], L);
+  if (live) {
+    FRW_DCHECK(C, aq[item] >= 0 && aq[item] < W.S);
+    adv_load(W, aq[item], L);
+  }
   int left = slice;  // transitions left in this visit of the walk
   while (__any_sync(0xFFFFFFFFu, live)) {
     if (!live) continue;
@@ -1644,7 +1688,9 @@ __device__ __forceinline__ void mw_carry(const DSlots& W, DCounters* C, int* mq_
   W.mwhj[L.slot] = static_cast<uint32_t>(L.hom) | static_cast<uint64_t>(L.hnode) << 32;
   W.rng[L.slot] = L.rng;
   W.state[L.slot] = S_MW_CARRY;
-  mq_next[atomicAdd(&C->q2len, 1ull)] = L.slot;
+  const unsigned long long qn = atomicAdd(&C->q2len, 1ull);
+  FRW_DCHECK(C, qn < static_cast<unsigned long long>(W.S));
+  mq_next[qn] = L.slot;
 }
 
 // a move left the current cell: look the new cell up in the atlas
@@ -2015,11 +2061,15 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
   bool live = item < qlen;
   if (live) {
     const int q = queue[item];
+    FRW_DCHECK(C, q >= 0 && q < W.S);
     mw_arm(W, q, q, n, L);
   }
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
-    if (live) code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+    if (live) {
+      code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+      FRW_DCHECK(C, node_ok(L.node, n));
+    }
     if (live && code == MW_GO && --left == 0) {
       mw_carry(W, C, mq_next, L);
       code = -1;
@@ -2038,6 +2088,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
       live = item < qlen;
       if (live) {
         const int q = queue[item];
+        FRW_DCHECK(C, q >= 0 && q < W.S);
         mw_arm(W, q, q, n, L);
       }
     }
@@ -2133,6 +2184,7 @@ __global__ void __launch_bounds__(256)
     while (code == MW_GO) {
       if ((L.room >> 48) == 0) dense_cell(grid, AT, n, L);
       code = mw_superstep<RNG>(Pd, W, AT, dd, n, cap, L, &xdir);
+      FRW_DCHECK(C, node_ok(L.node, n));
     }
     if (code == MW_SURFACE) {
       mw_exit(W, n, L, xdir);
@@ -2195,10 +2247,13 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     if (!live) return;
     if (item < qc) {
       const int q = mq[item];
+      FRW_DCHECK(C, q >= 0 && q < W.S);
       mw_arm(W, q, q, n, L);
       in_mw = true;
     } else {
-      adv_load(W, aq[item - qc], A);
+      const int q = aq[item - qc];
+      FRW_DCHECK(C, q >= 0 && q < W.S && jlane < W.J);
+      adv_load(W, q, A);
       A.jslot = jlane;
       in_mw = false;
     }
@@ -2232,6 +2287,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       if (!(live && in_mw)) continue;
       int xdir = 0;
       const int code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+      FRW_DCHECK(C, node_ok(L.node, n));
       if (code == MW_GO) continue;
       in_mw = false;
       if (code == MW_SURFACE) {
@@ -3525,6 +3581,8 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   W.jtail = S;
   // job entries: one per slot, then one per resident k_tail lane
   const size_t J = static_cast<size_t>(S) + static_cast<size_t>(ctx->sm_count) * kTailBlocks * 256;
+  W.J = static_cast<int>(J);
+  E.M.cap = S;
   W.state = dalloc<uint8_t>(S);
   W.wid = dalloc<long long>(S);
   W.p = dalloc<double>(3 * size_t(S));
@@ -3607,6 +3665,7 @@ int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double
     if (!E.recs) return frw_fail(ctx, FRW_ENOMEM, "transitions: record allocation failed");
     E.recs_cap = count;
   }
+  E.W.count = count;
   if (!E.d_cnt) {
     E.d_cnt = dalloc<DCounters>(1);
     E.M.axis = dalloc<int>(kMissMax);
@@ -4469,6 +4528,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   }
   DSlots Wc = E.W;  // the pool of this call: S active slots of the capacity
   Wc.S = S;
+  Wc.count = count;
   if (E.recs_cap < count) {
     cudaFree(E.recs);
     E.recs = dalloc<WalkRec>(count);
@@ -4636,6 +4696,11 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                      round, c.alen, c.qlen, c.a2len, c.q2len, c.dqlen, c.done, c.nmiss, ams,
                      tail ? "tail" : "mw", ms);
       }
+    }
+    if (c.chk_line) {
+      status = frw_fail(ctx, FRW_ECUDA, "device check failed at walk.cu:" +
+                                            std::to_string(c.chk_line));
+      break;
     }
     if (c.err) {
       status = -static_cast<int>(c.err);
