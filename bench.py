@@ -342,9 +342,8 @@ def grid_config(name, count, args, rank, world, dist, torch, local, smem_peak, p
         tt = torch.tensor([e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_s = float(tt.item())
-    two = os.environ.get("FRW_GRID_WPT", "2") != "1"
-    kname = "mw_grid_fast2" if two else "mw_grid_fast"
-    pr = prof.get((name, kname)) or prof.get((name, "mw_grid_fast")) or {}
+    kname = "mw_grid_fast"
+    pr = prof.get((name, kname)) or {}
     achieved = BYTES_PER_STEP * k_steps / (k_ms * 1e-3) / 1e9
     traffic = pr.get("dram_bytes_per_launch")
     if traffic is not None and pr.get("transits"):

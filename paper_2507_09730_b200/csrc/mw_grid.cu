@@ -827,177 +827,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Two walkers per thread (Philox, no per-transit exit records): the same
-// steps as mw_grid_fast, interleaved for two independent transits, so each
-// warp carries two dependency chains through the shared-memory gathers.
-// 768 threads x 2 walkers = 1536 chains per SM (mw_grid_fast: 1024; the
-// 183 KB table admits one CTA per SM, and 2048 threads would leave 32
-// registers each).  Transit t draws from Philox (seed, t, block) whichever
-// thread and walker run it, so results equal mw_grid_fast's bit for bit.
-#ifndef FRW_GRID_T2
-#define FRW_GRID_T2 768
-#endif
-constexpr int kThreads2 = FRW_GRID_T2;
-template <int RNG>
-__global__ void __launch_bounds__(kThreads2, 1)
-    mw_grid_fast2(DevGrid g, DevParams p, unsigned long long* ctr, int* err,
-                  int32_t* out_panel, int32_t* out_steps, int32_t* out_cond,
-                  unsigned long long* hist, unsigned long long* m_sum,
-                  unsigned long long* m_sq, unsigned long long* m_cx) {
-  static_assert(RNG == FRW_RNG_PHILOX, "the two-walker kernel serves Philox streams");
-  constexpr int SS = 8;
-  constexpr int WPT = 2;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* rec_p = smem;
-  uint8_t* map_p = smem + g.rec_bytes;
-  int* str_p = reinterpret_cast<int*>(map_p + g.map_bytes);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(str_p + 8);
-  bulk_stage2(rec_p, g.rec, g.rec_bytes, map_p, g.map, g.map_bytes, bar);
-  const uint32_t s_rec = smem_base(rec_p);
-  if (s_rec + g.rec_bytes > 65536u) {
-    if (threadIdx.x == 0) atomicExch(err, FRW_EINVAL);
-    return;
-  }
-  for (uint32_t i = threadIdx.x; i < g.map_bytes / 4; i += blockDim.x) {
-    uint32_t* w = reinterpret_cast<uint32_t*>(map_p) + i;
-    const uint32_t v = *w;
-    *w = (s_rec + 8u * (v & 0xFFFFu)) | ((s_rec + 8u * (v >> 16)) << 16);
-  }
-  if (threadIdx.x < 8) {
-    const int d = threadIdx.x, ax = d >> 1;
-    str_p[d] = d >= 6 ? 0 : ((d & 1) ? 2 : -2) * (ax == 0 ? 1 : ax == 1 ? g.np : g.npp);
-  }
-  __syncthreads();
-  const uint32_t s_map = smem_base(map_p);
-  const int lane_stride = str_p[threadIdx.x & 7];
-  const uint32_t s_exit = s_rec + 8u * g.exit_rec;
-  const uint32_t a_start = s_map + 2u * g.start_idx;
-  const uint32_t ra_start = lds_u16(a_start);
-  const uint32_t a_dead = s_map;
-  const int cap = p.step_cap;
-  unsigned long long ssum = 0, ssq = 0, cexit = 0;
-  const uint32_t k0 = static_cast<uint32_t>(p.seed);
-  const uint32_t k1 = static_cast<uint32_t>(p.seed >> 32);
-
-  long long t[WPT];
-  bool live[WPT];
-  uint32_t a[WPT], ra[WPT];
-  int dwell[WPT], blk[WPT];
-#pragma unroll
-  for (int i = 0; i < WPT; ++i) {
-    t[i] = static_cast<long long>(atomicAdd(ctr, 1ull));
-    live[i] = t[i] < p.count;
-    a[i] = live[i] ? a_start : a_dead;
-    ra[i] = live[i] ? ra_start : s_exit;
-    dwell[i] = 0;
-    blk[i] = 0;
-  }
-  while (__any_sync(0xFFFFFFFFu, live[0] || live[1])) {
-    uint32_t w[WPT][4];
-#pragma unroll
-    for (int i = 0; i < WPT; ++i) {
-      const uint64_t id = static_cast<uint64_t>(p.stream_begin + t[i]);
-      const U32x4 o = philox4x32_10({static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
-                                     static_cast<uint32_t>(blk[i]), 0u},
-                                    k0, k1);
-      w[i][0] = o.x;
-      w[i][1] = o.y;
-      w[i][2] = o.z;
-      w[i][3] = o.w;
-    }
-#pragma unroll
-    for (int u = 0; u < SS; ++u) {
-#pragma unroll
-      for (int i = 0; i < WPT; ++i) {
-        const uint64_t rc = lds_u64(ra[i]);
-        const uint32_t x11 = (u & 1) ? (w[i][u >> 1] & 0x7FFu) : (w[i][u >> 1] >> 21);
-        const uint64_t d1 = static_cast<uint64_t>(x11) * kOnes + rc;
-        const uint32_t d1h = static_cast<uint32_t>(d1 >> 32);
-        int dir = __popc((static_cast<uint32_t>(d1) & kGuardLo) | (d1h & kGuardHi));
-        const bool tie = (~shr64_lo(d1, 12u * dir) & 0x7FFu) == 0;
-        if (__builtin_expect(__any_sync(0xFFFFFFFFu, tie), 0)) {
-          const uint64_t* f = g.full + 5 * ((ra[i] - s_rec) >> 3);
-          uint64_t th[5];
-#pragma unroll
-          for (int d = 0; d < 5; ++d) th[d] = tie ? __ldg(f + d) : 0;
-          const uint32_t wu = w[i][u >> 1];
-          const uint32_t h16 =
-              (u & 1) ? (((wu & 0x7FFu) << 5) | ((wu >> 11) & 0x1Fu)) : (wu >> 16);
-          int dx = 0;
-          bool tie16 = false;
-#pragma unroll
-          for (int d = 0; d < 5; ++d) {
-            const uint32_t t16 = static_cast<uint32_t>(th[d] >> 37);
-            dx += h16 > t16;
-            tie16 |= h16 == t16;
-          }
-          tie16 = tie16 && tie;
-          if (__any_sync(0xFFFFFFFFu, tie16)) {
-            const uint64_t id = static_cast<uint64_t>(p.stream_begin + t[i]);
-            const U32x4 o = philox4x32_10(
-                {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
-                 static_cast<uint32_t>(blk[i] * SS + u), 1u},
-                k0, k1);
-            const uint64_t low37 = ((static_cast<uint64_t>(o.x) << 32) | o.y) >> 27;
-            const uint64_t x53 = (static_cast<uint64_t>(h16) << 37) | low37;
-            int de = 0;
-#pragma unroll
-            for (int d = 0; d < 5; ++d) de += x53 >= th[d];
-            dx = tie16 ? de : dx;
-          }
-          dir = tie ? dx : dir;
-        }
-        a[i] += static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, lane_stride, dir));
-        ra[i] = lds_u16(a[i]);
-        dwell[i] += d1h >> 31;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < WPT; ++i) {
-      const bool exited = ra[i] == s_exit;
-      const int steps = SS * (blk[i] + 1) - dwell[i];
-      ++blk[i];
-      if (live[i] && (exited || steps >= cap)) {
-        int32_t panel = -1, cid = -1;
-        if (exited && steps <= cap) {
-          const int info = __ldg(g.exit_info + static_cast<int>((a[i] - s_map) >> 1));
-          if (info >= 0) {
-            panel = info;
-            atomicAdd(hist + panel, 1ull);
-          } else {
-            cid = -2 - info;
-            ++cexit;
-          }
-        } else {
-          atomicExch(err, FRW_ESTEPCAP);  // microwalk.cpp:153-155
-        }
-        if (out_panel) out_panel[t[i]] = panel;
-        if (out_steps) out_steps[t[i]] = steps;
-        if (out_cond) out_cond[t[i]] = cid;
-        ssum += steps;
-        ssq += static_cast<unsigned long long>(steps) * steps;
-        t[i] = static_cast<long long>(atomicAdd(ctr, 1ull));
-        live[i] = t[i] < p.count;
-        blk[i] = 0;
-        dwell[i] = 0;
-        a[i] = live[i] ? a_start : a_dead;
-        ra[i] = live[i] ? ra_start : s_exit;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ssum += __shfl_xor_sync(0xFFFFFFFFu, ssum, o);
-    ssq += __shfl_xor_sync(0xFFFFFFFFu, ssq, o);
-    cexit += __shfl_xor_sync(0xFFFFFFFFu, cexit, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(m_sum, ssum);
-    atomicAdd(m_sq, ssq);
-    atomicAdd(m_cx, cexit);
-  }
-}
-
 template <int RNG, bool SMEM>
 int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned long long* ms,
            unsigned long long* mq, unsigned long long* mc) {
@@ -1013,34 +842,17 @@ int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned l
   // base is at most a few KB; the kernel checks the exact bound)
   const bool fast = SMEM && G.rec_bytes + 4096 <= 65536;
   const size_t smem = !SMEM ? 0 : fast ? G.map_bytes + G.rec_bytes + 48 : G.map_bytes + G.rec_bytes;
+  auto kern = !fast ? mw_grid_kernel<RNG, SMEM>
+              : o->exit_nd ? mw_grid_fast<RNG, true> : mw_grid_fast<RNG, false>;
+  if (SMEM)
+    FRW_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
   FRW_CUDA(ctx, cudaMemsetAsync(ctx->d_ctr, 0, sizeof(unsigned long long), ctx->stream));
   const int blocks = p->blocks > 0 ? p->blocks : ctx->sm_count;
-  // Philox without per-transit exit records: two walkers per thread
-  // (FRW_GRID_WPT=1 keeps one)
-  bool two = false;
-  if constexpr (RNG == FRW_RNG_PHILOX) {
-    two = fast && !o->exit_nd;
-    if (const char* e = std::getenv("FRW_GRID_WPT")) two = two && std::atoi(e) != 1;
-    if (two) {
-      auto k2 = mw_grid_fast2<FRW_RNG_PHILOX>;
-      FRW_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-      k2<<<blocks, kThreads2, smem, ctx->stream>>>(
-          g, dp, ctx->d_ctr, ctx->d_err, o->panels, o->steps, o->cond,
-          reinterpret_cast<unsigned long long*>(o->hist), ms, mq, mc);
-    }
-  }
-  if (!two) {
-    auto kern = !fast ? mw_grid_kernel<RNG, SMEM>
-                : o->exit_nd ? mw_grid_fast<RNG, true> : mw_grid_fast<RNG, false>;
-    if (SMEM)
-      FRW_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-    kern<<<blocks, kThreads, smem, ctx->stream>>>(
-        g, dp, ctx->d_ctr, ctx->d_err, o->panels, o->steps, o->cond,
-        reinterpret_cast<long long*>(o->exit_nd), reinterpret_cast<unsigned long long*>(o->hist),
-        ms, mq, mc);
-  }
+  kern<<<blocks, kThreads, smem, ctx->stream>>>(
+      g, dp, ctx->d_ctr, ctx->d_err, o->panels, o->steps, o->cond,
+      reinterpret_cast<long long*>(o->exit_nd), reinterpret_cast<unsigned long long*>(o->hist),
+      ms, mq, mc);
   FRW_CUDA(ctx, cudaGetLastError());
   return FRW_OK;
 }

@@ -160,6 +160,7 @@ def extract_sharded(text: str, walks: int, group=None, runner=None, device: int 
     nccl = runner is None and d is not None and world > 1 and d.get_backend(group) == "nccl"
     if runner is None:
         runner = device_runner
+    reducer = "frw_tally_allreduce" if nccl else ("torch.distributed" if world > 1 else "none")
     if nccl:
         init_nccl(device if device is not None else kw.get("device", 0), group)
     if device is not None:
@@ -176,6 +177,7 @@ def extract_sharded(text: str, walks: int, group=None, runner=None, device: int 
     res["t_device_seconds"] = t.get("t_device_seconds", 0.0)
     res["t_mw_seconds"] = t.get("t_mw_seconds", 0.0)
     res["walks_this_rank"] = e - b
+    res["allreduce"] = reducer
     return res
 
 

@@ -201,17 +201,3 @@ def test_n1_one_step(gpu_ctx):
     rep = compare_counts(np.full(6, 1 / 6), g["hist"])
     assert rep["tv"] <= 0.01 and rep["p"] > 0.01
 
-
-def test_two_walker_kernel_equals_one_walker(gpu_ctx, monkeypatch):
-    """mw_grid_fast2 (two transits per thread) and mw_grid_fast run the same
-    Philox transits: identical histograms and step moments"""
-    eps, c, h, _ = c2_grid(1)
-    gpu_ctx.upload_grid(eps, c, h)
-    out = {}
-    for wpt in ("1", "2"):
-        monkeypatch.setenv("FRW_GRID_WPT", wpt)
-        r = gpu_ctx.microwalk_batch(300_000, seed=17, stream_begin=5, rng=capi.RNG_PHILOX)
-        out[wpt] = r
-    assert np.array_equal(out["1"]["hist"], out["2"]["hist"])
-    assert out["1"]["step_sum"] == out["2"]["step_sum"]
-    assert out["1"]["step_sumsq"] == out["2"]["step_sumsq"]
