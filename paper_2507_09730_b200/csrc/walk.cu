@@ -49,7 +49,8 @@ namespace {
 
 constexpr int KMAX = 64;    // clipped boxes (conductors + dielectrics) per MicroWalk cube
 constexpr int NMAX = 64;    // lattice size cap (layers per key)
-constexpr int PMAX = 64;    // palettes up to PMAX classes keep the alpha table in shared memory
+constexpr int PMAX = 40;    // palettes up to PMAX classes keep the alpha table in shared memory
+                            // (12.8 KB; larger ones divide, the same IEEE quotient)
 constexpr int kClassMax = 0x7FFF;  // distinct permittivities (15-bit class ids)
 constexpr int kSlotsDefault = 1 << 20;
 constexpr int kMwSlice = 64;   // MicroWalk super-steps per hop and k_mw visit
@@ -85,6 +86,33 @@ constexpr double kMPerNm = 1e-9;            // constants.hpp:6
   } while (0)
 #else
 #define FRW_DCHECK(C, cond) static_cast<void>(0)
+#endif
+
+// Phase clocks (experiment builds, -DFRW_PHASE_CLOCKS): clock64 spans of the
+// walk kernels' phases summed per phase (g_ph[i]) with event counts
+// (g_ph[16 + i]); frw_run_walks prints them to stderr after the call.
+#ifdef FRW_PHASE_CLOCKS
+__device__ unsigned long long g_ph[256 * 32];  // 256 rows (spread by thread): no hot address
+#define PH_ROW (((blockIdx.x * blockDim.x + threadIdx.x) & 255) * 32)
+// completion times of the walks k_tail finishes, 0.25 ms buckets from the
+// launch (g_tail_t0: globaltimer of the launch's first lane)
+__device__ unsigned long long g_tail_hist[256];
+__device__ unsigned long long g_tail_t0;
+__device__ int g_in_tail;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PH_T0(v) const long long v = clock64()
+#define PH_ADD(i, v)                                                              \
+  do {                                                                            \
+    atomicAdd(&g_ph[PH_ROW + (i)], static_cast<unsigned long long>(clock64() - (v))); \
+    atomicAdd(&g_ph[PH_ROW + 16 + (i)], 1ull);                                    \
+  } while (0)
+#else
+#define PH_T0(v) static_cast<void>(0)
+#define PH_ADD(i, v) static_cast<void>(0)
 #endif
 
 enum : uint8_t { S_FREE = 0, S_ACTIVE = 1, S_NEED_MW = 2, S_PARKED = 3, S_MW_CARRY = 4 };
@@ -142,23 +170,36 @@ struct DSgf {
 // surface Green's function of the uniform cube with n' = 2m-1 nodes (the
 // device solve of sgf_solve.cu).  By the strong Markov property replacing
 // those steps by one draw from it leaves the law of the hop's exit (and the
-// expected step count) unchanged.  Per radius m: the face law as u64
-// thresholds over (2m-1)^2 positions (face chosen uniformly: the cube is
-// octahedrally symmetric), a guide table, and E[tau] in 32.32 fixed point.
+// expected step count) unchanged.  Per radius m: the face law over the
+// (2m-1)^2 positions of a face (face chosen uniformly: the cube is
+// octahedrally symmetric) as a Walker alias table -- u64 acceptance
+// thresholds and u16 aliases, one lookup and no scan -- and E[tau] in 32.32
+// fixed point.  The kernels stage the tables of the radii that fit
+// (kJumpSm entries, all of them for n <= 24) in shared memory.
 struct JumpMeta {
-  uint32_t thr_off;    // into DJump::thr
-  uint32_t guide_off;  // into DJump::guide
-  uint32_t gbits;      // log2 of the guide-table size
+  uint32_t off;        // into DJump::prob / alias
+  uint32_t K;          // side^2 positions
+  uint32_t magic;      // ceil(2^32 / side): idx / side = umulhi(idx, magic)
   uint32_t side;       // 2m - 1
   uint64_t esteps;     // E[tau] * 2^32
 };
+constexpr int kJumpMetaMax = 32;   // radii 0..31
+constexpr int kJumpSm = 2048;      // alias entries staged in shared memory
 struct DJump {
   int mmax;  // largest radius tabulated; < 2: jumps off
   int twice; // a second jump from words 2-3 of the block when it fits
   int hom;   // jumps across homogeneous balls beyond the walker's cell (mw_hom_radius)
+  int msm;   // radii <= msm read prob_s / alias_s (shared memory)
   const JumpMeta* meta;   // [mmax + 1]
-  const uint64_t* thr;    // per radius: side^2 thresholds, last = UINT64_MAX
-  const uint16_t* guide;  // per radius: 2^gbits first candidates
+  const uint64_t* prob;   // per radius: K acceptance thresholds (u64 fractions)
+  const uint16_t* alias;  // per radius: K aliases
+  const uint64_t* prob_s; // shared-memory copies of the first radii's tables
+  const uint16_t* alias_s;
+};
+struct JumpSmem {
+  JumpMeta meta[kJumpMetaMax];
+  uint64_t prob[kJumpSm];
+  uint16_t alias[kJumpSm];
 };
 
 struct DParams {
@@ -213,7 +254,7 @@ struct DSlots {
   // a MicroWalk hop carried to the next round (S_MW_CARRY): node, steps so far
   uint32_t* mwnode;
   int* mwhsteps;
-  uint64_t* mwhj;        // its homogeneous-radius bound: hom | hnode << 32
+  uint64_t* mwhj;        // its homogeneous-radius bound: hom | (hq + 1) << 8 | hnode << 32
 };
 
 // Work queues of one round: k_spawn and the previous round's k_mw fill the
@@ -242,6 +283,7 @@ struct DCounters {
   unsigned long long jsteps;     // lattice steps the jumps stand for (their E[tau])
   unsigned long long q2len;      // MicroWalk queue of the next round (carried hops)
   unsigned long long dqlen, dqhead;  // dense MicroWalk hops of this round (k_mw_dense)
+  unsigned long long cqlen;          // walks queued for k_compile this round
   unsigned long long dense_hops;     // dense hops run (all rounds)
   // k_tail: warp cycles in MicroWalk super-steps / in the whole loop, for
   // the MicroWalk share of the tail's device time (T_MW, engine.cpp:322-345)
@@ -862,19 +904,25 @@ __device__ __forceinline__ double vcenter(double c, double h, double p, int i) {
 }
 
 // first i in [0, n] with centre(i) >= lo; last i in [-1, n-1] with centre(i) <= hi
-__device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih) {
-  const double p = 2.0 * h / n;
+// p = 2h/n (the reference's pitch), ip ~ 1/p: the reciprocal only seeds the
+// index guesses, which the exact voxel-centre comparisons then correct
+__device__ void clip_axis(double c, double h, double p, double ip, int n, double lo, double hi,
+                          int* il, int* ih) {
   const double base = c - h;
-  int a = static_cast<int>(floor((lo - base) / p - 0.5));
+  int a = static_cast<int>(floor((lo - base) * ip - 0.5));
   a = max(0, min(n, a));
   while (a > 0 && vcenter(c, h, p, a - 1) >= lo) --a;
   while (a < n && vcenter(c, h, p, a) < lo) ++a;
-  int b = static_cast<int>(floor((hi - base) / p - 0.5));
+  int b = static_cast<int>(floor((hi - base) * ip - 0.5));
   b = max(-1, min(n - 1, b));
   while (b < n - 1 && vcenter(c, h, p, b + 1) <= hi) ++b;
   while (b >= 0 && vcenter(c, h, p, b) > hi) --b;
   *il = a;
   *ih = b;
+}
+__device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih) {
+  const double p = 2.0 * h / n;
+  clip_axis(c, h, p, 1.0 / p, n, lo, hi, il, ih);
 }
 
 __device__ __forceinline__ int box_lo(uint64_t b, int a) { return static_cast<int>((b >> (8 * a)) & 0xFF); }
@@ -1042,6 +1090,7 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
   uint64_t* A = W.atlas + static_cast<size_t>(slot) * kAtlasWords;
   int K = 0, ncond = 0;
   const double cb[6] = {c[0] - h, c[1] - h, c[2] - h, c[0] + h, c[1] + h, c[2] + h};
+  const double pitch = 2.0 * h / n, ipitch = 1.0 / pitch;
   int cand[kCandMax];
   uint16_t* cls = reinterpret_cast<uint16_t*>(A + kAtCls);
   // phase 0: conductor boxes (MicroWalk-E only), phase 1: dielectric boxes,
@@ -1070,7 +1119,7 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
       for (int ax = 0; ax < 3; ++ax) {
         const double ca = ax == 0 ? c[0] : (ax == 1 ? c[1] : c[2]);
         int l, hh;
-        clip_axis(ca, h, n, __ldg(bx + ax), __ldg(bx + 3 + ax), &l, &hh);
+        clip_axis(ca, h, pitch, ipitch, n, __ldg(bx + ax), __ldg(bx + 3 + ax), &l, &hh);
         empty |= l > hh;
         pk |= static_cast<uint64_t>(l & 0xFF) << (8 * ax) |
               static_cast<uint64_t>(hh & 0xFF) << (24 + 8 * ax);
@@ -1286,6 +1335,12 @@ __device__ void finish_walk(const DSlots& W, WalkRec* recs, DCounters* C, int sl
   recs[wid] = r;
   W.state[slot] = S_FREE;
   atomicAdd(&C->done, 1ull);
+#ifdef FRW_PHASE_CLOCKS
+  if (g_in_tail) {
+    const unsigned long long dt = (gtimer() - g_tail_t0) / 250000ull;
+    atomicAdd(&g_tail_hist[dt < 255 ? dt : 255], 1ull);
+  }
+#endif
 }
 
 // Gaussian sample + first transition for every free slot
@@ -1333,8 +1388,10 @@ __global__ void k_spawn(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, D
       g[a] = sign < 0 ? P.gbox[a] : P.gbox[3 + a];
       g[b1] = P.gbox[b1] + uniform(P, wid, rng) * (P.gbox[3 + b1] - P.gbox[b1]);
       g[b2] = P.gbox[b2] + uniform(P, wid, rng) * (P.gbox[3 + b2] - P.gbox[b2]);
+      PH_T0(ph8);
       rc = first_transition(s, T, P, wid, rng, g, a, sign,
                             W.boxes + static_cast<size_t>(slot) * KMAX, C, M, &fo);
+      PH_ADD(8, ph8);
       if (rc == 0) ++resampled;
     }
     W.resampled[slot] = static_cast<uint8_t>(resampled);
@@ -1386,13 +1443,80 @@ __device__ __forceinline__ void adv_load(const DSlots& W, int slot, AdvLane& L) 
   L.cached = W.cached[slot];
 }
 
+// The MicroWalk job of a general cube (engine.cpp:311-347) at point p with
+// free-cube half width fh: MicroWalk on the transit cube, or MicroWalk-E on
+// the expanded cube, falling back to the transit cube when the expanded
+// lattice swallows the start voxel (EngulfedStart).  Compiled into job entry
+// jslot.  Returns 2 (job ready, its kind in W.mwkind[jslot]) or 1 (the walk
+// left the stage: queued for a dense hop, or dropped on an error).
+__device__ __forceinline__ int hop_compile(const DStruct& s, const DParams& P, const DSlots& W,
+                                           DCounters* C, const DMiss& M, int slot, int jslot,
+                                           const double p[3], double fh) {
+  const int n = P.n;
+  double c[3], h;
+  transit_cube(p, fh, n, c, &h);
+  uint8_t kind = P.mode == FRW_MODE_FDM ? 2 : 0;  // 2: FDM solve (engine.cpp:311-318)
+  double jc[3] = {c[0], c[1], c[2]}, jh = h;
+  bool expanded = false;
+  if (P.mode == FRW_MODE_MWE || P.mode == FRW_MODE_HYBRID_MWE) {
+    kind = 1;
+    expanded = true;
+    const double wall = cheb_wall(s.world, p);
+    const double half = mn(P.expansion * fh, wall);  // microwalk.cpp:213-214
+    if (!(half > 0)) {
+      set_err(C, FRW_EINVAL);
+      W.state[slot] = S_FREE;
+      return 1;
+    }
+    transit_cube(p, half, n, jc, &jh);
+  }
+  // one inlined copy of the job compiler (the kernels are instruction-fetch
+  // bound): the expanded cube first, the transit cube on EngulfedStart
+  int rc = -1;
+#pragma unroll 1
+  for (;;) {
+    rc = compile_mw_job(s, W, jslot, jc, jh, n, expanded, C);
+    if (rc != 0 || !expanded) break;
+    expanded = false;
+    jc[0] = c[0];
+    jc[1] = c[1];
+    jc[2] = c[2];
+    jh = h;
+  }
+  if (rc < 0) {
+    W.state[slot] = S_FREE;
+    return 1;
+  }
+  if (rc == 3) {
+    // more than KMAX boxes reach into the cube: the hop goes to k_mw_dense
+    // (its job in the walk's own entry: the dense kernel runs after this one)
+    if (kind == 2) {  // FDM builds its system from the atlas
+      set_err(C, FRW_EINVAL);
+      W.state[slot] = S_FREE;
+      return 1;
+    }
+    if (jslot != slot) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) W.cube[4 * slot + q] = W.cube[4 * jslot + q];
+    }
+    W.mwkind[slot] = static_cast<uint8_t>(kind | kDense | (expanded ? kDenseCond : 0));
+    const unsigned long long qd = atomicAdd(&C->dqlen, 1ull);
+    FRW_DCHECK(C, qd < static_cast<unsigned long long>(W.S));
+    M.dense[qd] = slot;
+    return 1;
+  }
+  W.mwkind[jslot] = kind;
+  return 2;
+}
+
 // One transition (engine.cpp:290-350; hop cap engine.cpp:367-375) of the
 // lane's walk.  Returns 0 when a cached hop was taken (the walk stays with
 // the lane), 1 when the walk left the stage (terminated or parked by a
-// table miss), 2 when its MicroWalk job is compiled (pushed to `mq` unless
-// null).
+// table miss), 2 when its walk needs a MicroWalk hop: with a compile queue
+// `cq` (wavefront rounds) the walk is queued for k_compile, else its job is
+// compiled here into the lane's job entry.
 __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, const DSlots& W,
-                            WalkRec* recs, DCounters* C, const DMiss& M, int* mq, AdvLane& L) {
+                            WalkRec* recs, DCounters* C, const DMiss& M, int* cq, AdvLane& L) {
   const int slot = L.slot;
   const int n = P.n;
   if (L.hops >= P.hop_cap) {
@@ -1401,7 +1525,9 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     return 1;
   }
   double fh;
+  PH_T0(ph0);
   const int g = hop_scan(s, L.p, P.snap, &fh);
+  PH_ADD(0, ph0);
   if (g >= 0 || g == -1) {  // snapped to a conductor / to the grounded wall
     W.cached[slot] = L.cached;
     finish_walk(W, recs, C, slot, g >= 0 ? g : s.nc, false);
@@ -1414,7 +1540,9 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   }
   double c[3], h;
   transit_cube(L.p, fh, n, c, &h);
+  PH_T0(ph1);
   const Prof pr = strat_probe(s, c, h, n);
+  PH_ADD(1, ph1);
   const int axis = pr.axis;
   if (axis == -2) {
     set_err(C, FRW_EINVAL);
@@ -1426,6 +1554,7 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     // through the per-class uniform index; otherwise (or when that key is
     // not in the table yet) the full key is hashed and compared
     auto layer = [&](int t) { return prof_layer(s, pr, c, h, n, t); };
+    PH_T0(ph2);
     int e = pr.ucls >= 0 ? __ldg(T.uentry + pr.ucls) : -1;
     if (e < 0) e = sgf_find(T, n, axis, layer);
     if (e < 0) {
@@ -1448,69 +1577,12 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     const int panel = sample_panel(data, reinterpret_cast<const int*>(data + 5 * P.panels),
                                    P.panels, uniform(P, L.wid, L.rng));
     panel_center(c, h, n, panel, L.p);
+    PH_ADD(2, ph2);
     ++L.cached;
     ++L.hops;
     return 0;
   }
-  // general cube (engine.cpp:311-347): MicroWalk on the transit cube, or
-  // MicroWalk-E on the expanded cube, falling back to the transit cube when
-  // the expanded lattice swallows the start voxel (EngulfedStart)
-  int rc = -1;
-  uint8_t kind = P.mode == FRW_MODE_FDM ? 2 : 0;  // 2: FDM solve (engine.cpp:311-318)
-  double jc[3] = {c[0], c[1], c[2]}, jh = h;
-  bool expanded = false;
-  if (P.mode == FRW_MODE_MWE || P.mode == FRW_MODE_HYBRID_MWE) {
-    kind = 1;
-    expanded = true;
-    const double wall = cheb_wall(s.world, L.p);
-    const double half = mn(P.expansion * fh, wall);  // microwalk.cpp:213-214
-    if (!(half > 0)) {
-      set_err(C, FRW_EINVAL);
-      W.state[slot] = S_FREE;
-      return 1;
-    }
-    transit_cube(L.p, half, n, jc, &jh);
-  }
-  // one inlined copy of the job compiler (the kernels are instruction-fetch
-  // bound): the expanded cube first, the transit cube on EngulfedStart
-#pragma unroll 1
-  for (;;) {
-    rc = compile_mw_job(s, W, L.jslot, jc, jh, n, expanded, C);
-    if (rc != 0 || !expanded) break;
-    expanded = false;
-    jc[0] = c[0];
-    jc[1] = c[1];
-    jc[2] = c[2];
-    jh = h;
-  }
-  if (rc < 0) {
-    W.state[slot] = S_FREE;
-    return 1;
-  }
-  if (rc == 3) {
-    // more than KMAX boxes reach into the cube: the hop goes to k_mw_dense
-    // (its job in the walk's own entry: the dense kernel runs after this one)
-    if (kind == 2) {  // FDM builds its system from the atlas
-      set_err(C, FRW_EINVAL);
-      W.state[slot] = S_FREE;
-      return 1;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) W.cube[4 * slot + q] = W.cube[4 * L.jslot + q];
-    W.mwkind[slot] = static_cast<uint8_t>(kind | kDense | (expanded ? kDenseCond : 0));
-    W.p[3 * slot + 0] = L.p[0];
-    W.p[3 * slot + 1] = L.p[1];
-    W.p[3 * slot + 2] = L.p[2];
-    W.rng[slot] = L.rng.s;
-    W.hops[slot] = L.hops + 1;
-    W.cached[slot] = L.cached;
-    W.state[slot] = S_NEED_MW;
-    const unsigned long long qd = atomicAdd(&C->dqlen, 1ull);
-    FRW_DCHECK(C, qd < static_cast<unsigned long long>(W.S));
-    M.dense[qd] = slot;
-    return 1;
-  }
-  W.mwkind[L.jslot] = kind;
+  // general cube (engine.cpp:311-347): the walk waits for its MicroWalk hop
   W.p[3 * slot + 0] = L.p[0];
   W.p[3 * slot + 1] = L.p[1];
   W.p[3 * slot + 2] = L.p[2];
@@ -1518,12 +1590,21 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   W.hops[slot] = L.hops + 1;
   W.cached[slot] = L.cached;
   W.state[slot] = S_NEED_MW;
-  if (mq) {
-    const unsigned long long qm = atomicAdd(&C->qlen, 1ull);
-    FRW_DCHECK(C, qm < static_cast<unsigned long long>(W.S));
-    mq[qm] = slot;
+  if (cq) {
+    // wavefront rounds: k_compile builds the job, every lane of a warp
+    // compiling one (in k_advance only a few lanes of a warp would, the rest
+    // waiting: the job compiler was over half of k_advance's issue slots at
+    // 2.6 active lanes)
+    W.cube[4 * slot + 3] = fh;
+    const unsigned long long qc = atomicAdd(&C->cqlen, 1ull);
+    FRW_DCHECK(C, qc < static_cast<unsigned long long>(W.S));
+    cq[qc] = slot;
+    return 2;
   }
-  return 2;
+  PH_T0(ph3);
+  const int rc = hop_compile(s, P, W, C, M, slot, L.jslot, L.p, fh);
+  PH_ADD(3, ph3);
+  return rc;
 }
 
 // (FRW_DEBUG_CHECKS) the lane's node lies in the lattice
@@ -1544,7 +1625,7 @@ __device__ __forceinline__ void mw_requeue(DCounters* C, int* aq_out, int slot) 
 #endif
 __global__ void __launch_bounds__(256, FRW_ADV_MINB)
     k_advance(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
-              const int* aq, int* mq, int* aq_out) {
+              const int* aq, int* cq, int* aq_out) {
   const unsigned long long alen = C->alen;
   const int slice = P.adv_slice > 0 ? P.adv_slice : 0x7FFFFFFF;
   unsigned long long item = atomicAdd(&C->ahead, 1ull);
@@ -1557,7 +1638,7 @@ __global__ void __launch_bounds__(256, FRW_ADV_MINB)
   int left = slice;  // transitions left in this visit of the walk
   while (__any_sync(0xFFFFFFFFu, live)) {
     if (!live) continue;
-    int r = advance_once(s, T, P, W, recs, C, M, mq, L);
+    int r = advance_once(s, T, P, W, recs, C, M, cq, L);
     if (r == 0 && --left == 0) {
       // a long chain of cached hops: the walk continues next round
       W.p[3 * L.slot] = L.p[0];
@@ -1578,6 +1659,26 @@ __global__ void __launch_bounds__(256, FRW_ADV_MINB)
   }
 }
 
+// the MicroWalk jobs of the walks k_advance queued, one per thread (each
+// warp compiles 32 jobs side by side), appended to the round's MicroWalk
+// queue (or the dense-hop queue)
+__global__ void __launch_bounds__(256, 2)
+    k_compile(DStruct s, DParams P, DSlots W, DCounters* C, DMiss M, const int* cq, int* mq) {
+  const unsigned long long len = C->cqlen;
+  for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const int slot = cq[i];
+    FRW_DCHECK(C, slot >= 0 && slot < W.S);
+    const double p[3] = {W.p[3 * slot], W.p[3 * slot + 1], W.p[3 * slot + 2]};
+    const double fh = W.cube[4 * slot + 3];
+    if (hop_compile(s, P, W, C, M, slot, slot, p, fh) == 2) {
+      const unsigned long long qm = atomicAdd(&C->qlen, 1ull);
+      FRW_DCHECK(C, qm < static_cast<unsigned long long>(W.S));
+      mq[qm] = slot;
+    }
+  }
+}
+
 // between rounds: the next round's ACTIVE queue becomes current, and the
 // MicroWalk hops carried over open the next round's MicroWalk queue
 __global__ void k_round(DCounters* C) {
@@ -1589,6 +1690,7 @@ __global__ void k_round(DCounters* C) {
   C->q2len = 0;
   C->dqlen = 0;
   C->dqhead = 0;
+  C->cqlen = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -1607,6 +1709,7 @@ struct MwLane {
   int nbx;        // clipped boxes of the job
   int hom;        // homogeneous radius known at node hnode (0: none)
   uint32_t hnode;
+  int hq;         // the clipped box that limited it (-1: the lattice), see mw_superstep
   uint64_t bm[3]; // segment-start bitmaps of the job's atlas
   double al[6];   // alpha of the neighbour across each face of the cell
   uint32_t gsteps;  // diagnostics, accumulated across the lane's hops
@@ -1665,6 +1768,7 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int
     L.nbx = nb >> 8;
   }
   L.hom = 0;
+  L.hq = -1;
   L.bm[0] = A[kAtBm];
   L.bm[1] = A[kAtBm + 1];
   L.bm[2] = A[kAtBm + 2];
@@ -1674,7 +1778,8 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int
     L.node = W.mwnode[slot];
     L.steps = W.mwhsteps[slot];
     const uint64_t hj = W.mwhj[slot];  // the jump decisions continue exactly
-    L.hom = static_cast<int>(static_cast<uint32_t>(hj));
+    L.hom = static_cast<int>(hj & 0xFF);
+    L.hq = static_cast<int>((hj >> 8) & 0xFF) - 1;
     L.hnode = static_cast<uint32_t>(hj >> 32);
   }
 }
@@ -1685,7 +1790,8 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int
 __device__ __forceinline__ void mw_carry(const DSlots& W, DCounters* C, int* mq_next, MwLane& L) {
   W.mwnode[L.slot] = L.node;
   W.mwhsteps[L.slot] = L.steps;
-  W.mwhj[L.slot] = static_cast<uint32_t>(L.hom) | static_cast<uint64_t>(L.hnode) << 32;
+  W.mwhj[L.slot] = static_cast<uint32_t>(L.hom & 0xFF) | static_cast<uint64_t>(L.hq + 1) << 8 |
+                   static_cast<uint64_t>(L.hnode) << 32;
   W.rng[L.slot] = L.rng;
   W.state[L.slot] = S_MW_CARRY;
   const unsigned long long qn = atomicAdd(&C->q2len, 1ull);
@@ -1728,6 +1834,10 @@ struct DirDelta {
   uint32_t pad;
 };
 
+// interior steps (mw_step): words w with (w * 6 mod 2^32) >= kInteriorTie
+// may straddle an f64 threshold and take the exact scan
+constexpr uint32_t kInteriorTie = 0xFFFFFFFAu;
+
 // One lattice step (microwalk.cpp:88-152) for lane L.  Every node takes the
 // same code path: a neighbour inside the current cell has the node's own
 // permittivity, so its alpha is e/(e+e) = 1/2 exactly; a neighbour across a
@@ -1744,6 +1854,22 @@ __device__ __forceinline__ int mw_step(const DParams& P, const DirDelta* dd, MwL
   const uint64_t r = L.room & 0x0000FFFFFFFFFFFFull;
   const uint64_t t = (r & 0x00007F7F7F7F7F7Full) + 0x00007F7F7F7F7F7Full;
   const uint64_t onface = ~(t | r | 0x00007F7F7F7F7F7Full) & 0x0000808080808080ull;
+  if (RNG == FRW_RNG_PHILOX && onface == 0 && w * 6u < kInteriorTie) {
+    // interior node: all six alphas are 1/2, so the scan below computes
+    // sum = 3, acc_d = (d+1)/2 exactly and dir = #{d : (d+1)/2 <= fl(3x/2^53)}
+    // for the 53-bit uniform x = w*2^21 + low21.  That count is floor(6w/2^32)
+    // for every word w whose 2^21-wide interval contains none of the five
+    // exact f64 thresholds; the words that can contain one have 6w within 6
+    // of a multiple of 2^32 (the low word of w*6 >= kInteriorTie) and take
+    // the scan (tests/test_step_law.py checks the equivalence exhaustively
+    // around every threshold).
+    const int dir = static_cast<int>(__umulhi(w, 6u));
+    const DirDelta del = dd[dir];
+    *xdir = dir;
+    L.node += del.node;
+    L.room += del.room;
+    return 0;
+  }
   double acc[6];
   double sum = 0;
 #pragma unroll
@@ -1793,7 +1919,26 @@ __device__ __forceinline__ int mw_step(const DParams& P, const DirDelta* dd, MwL
 
 // alpha_sm: the palette-pair alphas, then alpha 1 (absorbing faces) at
 // index P*P so a face alpha is one unconditional shared load (P <= PMAX)
-__device__ AlphaTab setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* dd) {
+__device__ AlphaTab setup_smem_tables(const DStruct& s, double* alpha_sm, DirDelta* dd,
+                                      const DJump& Jg, JumpSmem& jsm, DJump* J) {
+  // lattice-jump tables: every radius's meta, the alias tables of the radii
+  // whose cumulative size fits kJumpSm
+  *J = Jg;
+  J->msm = 0;
+  if (Jg.mmax >= 2) {
+    int msm = 1;
+    while (msm < Jg.mmax && Jg.meta[msm + 1].off + Jg.meta[msm + 1].K <= kJumpSm) ++msm;
+    const int ne = msm >= 2 ? static_cast<int>(Jg.meta[msm].off + Jg.meta[msm].K) : 0;
+    for (int i = threadIdx.x; i <= Jg.mmax; i += blockDim.x) jsm.meta[i] = Jg.meta[i];
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+      jsm.prob[i] = __ldg(Jg.prob + i);
+      jsm.alias[i] = __ldg(Jg.alias + i);
+    }
+    J->msm = msm;
+    J->meta = jsm.meta;
+    J->prob_s = jsm.prob;
+    J->alias_s = jsm.alias;
+  }
   const bool small = s.P <= PMAX;
   if (small) {
     for (int i = threadIdx.x; i < s.P * s.P; i += blockDim.x) alpha_sm[i] = __ldg(s.alpha + i);
@@ -1836,11 +1981,15 @@ __device__ __forceinline__ void mw_jump_r(const DJump& J, MwLane& L, int m, uint
   const uint64_t x = (static_cast<uint64_t>(w0) << 32) | w1;
   const int face = static_cast<int>(__umul64hi(x, 6ull));
   const uint64_t y = x * 6ull;  // uniform given the face
-  const uint64_t* T = J.thr + jm.thr_off;
-  uint32_t idx = __ldg(J.guide + jm.guide_off + (y >> (64 - jm.gbits)));
-  while (y >= __ldg(T + idx)) ++idx;  // T[last] = UINT64_MAX ends the scan
+  // alias draw: column i uniform in [0, K), its fraction f uniform given i
+  const uint32_t i = static_cast<uint32_t>(__umul64hi(y, jm.K));
+  const uint64_t f = y * jm.K;
+  const bool shared = m <= J.msm;
+  const uint64_t thr = shared ? J.prob_s[jm.off + i] : __ldg(J.prob + jm.off + i);
+  const uint32_t al = shared ? J.alias_s[jm.off + i] : __ldg(J.alias + jm.off + i);
+  const uint32_t idx = f < thr ? i : al;
   const int side = static_cast<int>(jm.side);
-  const int v = static_cast<int>(idx) / side;
+  const int v = static_cast<int>(__umulhi(idx, jm.magic));
   const int u = static_cast<int>(idx) - v * side;
   const int a = face >> 1;
   // displacement: +-m along the face axis a, the panel's (u, v) across it in
@@ -1880,32 +2029,47 @@ __device__ __forceinline__ void mw_jump_r(const DJump& J, MwLane& L, int m, uint
 // Inside that ball every alpha is 1/2 (microwalk.cpp:97-104), so the jump
 // law of radius m holds there whatever cells the box faces cut (the cells are
 // a tensor grid of every face, finer than the material boundaries).
-__device__ int mw_hom_radius(const DSlots& W, const MwLane& L, int n) {
-  const int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+// the largest m for which box b contains or misses the whole L-inf ball of
+// radius m around node v
+__device__ __forceinline__ int box_ball(uint64_t b, const int v[3]) {
+  bool in = true;
+  int gin = 64, gout = -1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int lo = box_lo(b, a), hi = box_hi(b, a);
+    if (v[a] < lo) {
+      in = false;
+      gout = max(gout, lo - v[a] - 1);
+    } else if (v[a] > hi) {
+      in = false;
+      gout = max(gout, v[a] - hi - 1);
+    } else {
+      gin = min(gin, min(v[a] - lo, hi - v[a]));
+    }
+  }
+  return in ? gin : gout;
+}
+__device__ __forceinline__ int lattice_ball(const int v[3], int n) {
   int m = 31;
 #pragma unroll
   for (int a = 0; a < 3; ++a) m = min(m, min(v[a], n - 1 - v[a]));
+  return m;
+}
+// *hq: the box that brought the radius below 2 or set it (-1: the lattice)
+__device__ int mw_hom_radius(const DSlots& W, const MwLane& L, int n, int* hq) {
+  const int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+  int m = lattice_ball(v, n);
+  int arg = -1;
   const uint64_t* B = W.boxes + static_cast<size_t>(L.jslot) * KMAX;
 #pragma unroll 1
   for (int q = 0; q < L.nbx && m >= 2; ++q) {
-    const uint64_t b = B[q];
-    bool in = true;
-    int gin = 64, gout = -1;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const int lo = box_lo(b, a), hi = box_hi(b, a);
-      if (v[a] < lo) {
-        in = false;
-        gout = max(gout, lo - v[a] - 1);
-      } else if (v[a] > hi) {
-        in = false;
-        gout = max(gout, v[a] - hi - 1);
-      } else {
-        gin = min(gin, min(v[a] - lo, hi - v[a]));
-      }
+    const int mb = box_ball(B[q], v);
+    if (mb < m) {
+      m = mb;
+      arg = q;
     }
-    m = min(m, in ? gin : gout);
   }
+  *hq = arg;
   return m;
 }
 
@@ -1926,10 +2090,11 @@ __device__ __forceinline__ bool mw_jump(const DJump& J, MwLane& L, uint32_t w0, 
 // SplitMix64 draws in parity mode); a move into another cell ends the
 // super-step and refreshes the cell from the atlas.  Returns an MW_* event.
 template <int RNG>
-__device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W, const AlphaTab& AT,
-                                            const DirDelta* dd, int n, int cap, MwLane& L,
-                                            int* xdir) {
+__device__ __forceinline__ int mw_superstep(const DParams& P, const DJump& J, const DSlots& W,
+                                            const AlphaTab& AT, const DirDelta* dd, int n, int cap,
+                                            MwLane& L, int* xdir) {
   uint32_t w4[4] = {0, 0, 0, 0};
+  PH_T0(ph11);
   if (RNG == FRW_RNG_PHILOX) {
     const uint64_t id = P.walk_begin + L.wid;
     const U32x4 o = philox4x32_10(
@@ -1941,16 +2106,26 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W, c
     w4[2] = o.z;
     w4[3] = o.w;
   }
+#ifdef FRW_PHASE_CLOCKS
+  if (w4[0] == 0x12345678u) w4[1] ^= 1;  // keep the draw before the clock read
+#endif
+  PH_ADD(11, ph11);
   // a pending cell (new hop, or a move into another cell last super-step):
   // one inlined copy of the atlas lookup serves both
-  if ((L.room >> 48) == 0) mw_cell_change(W, AT, n, L);
+  PH_T0(ph5);
+  if ((L.room >> 48) == 0) {
+    PH_T0(ph4);
+    mw_cell_change(W, AT, n, L);
+    PH_ADD(4, ph4);
+  }
   int code = 0;
   int u0 = 0;  // words taken by jumps (two per jump)
-  if (RNG == FRW_RNG_PHILOX && P.jump.mmax >= 2 && L.steps < cap) {
-    if (mw_jump(P.jump, L, w4[0], w4[1])) {
+  PH_T0(ph12);
+  if (RNG == FRW_RNG_PHILOX && J.mmax >= 2 && L.steps < cap) {
+    if (mw_jump(J, L, w4[0], w4[1])) {
       u0 = 2;
-      if (P.jump.twice && L.steps < cap && mw_jump(P.jump, L, w4[2], w4[3])) u0 = 4;
-    } else if (P.jump.hom) {
+      if (J.twice && L.steps < cap && mw_jump(J, L, w4[2], w4[3])) u0 = 4;
+    } else if (J.hom) {
       // no room for a jump inside the cell: the homogeneous ball around the
       // node (a bound carried from the node it was computed at, recomputed
       // once it drops below 2)
@@ -1961,16 +2136,30 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W, c
       // recompute only when that range straddles 2
       int eff = L.hom - d;
       if (eff < 2 && L.hom + d >= 2) {
-        eff = mw_hom_radius(W, L, n);
-        L.hom = eff;
-        L.hnode = L.node;
+        // the radius is at most what the box (or lattice) that limited it
+        // last time allows here: the full O(boxes) scan only when that is >= 2
+        const int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
+        int lim = lattice_ball(v, n);
+        if (L.hq >= 0)
+          lim = min(lim, box_ball(W.boxes[static_cast<size_t>(L.jslot) * KMAX + L.hq], v));
+        if (lim >= 2) {
+          PH_T0(ph14);
+          int hq;
+          eff = mw_hom_radius(W, L, n, &hq);
+          L.hq = hq;
+          PH_ADD(14, ph14);
+          L.hom = eff;
+          L.hnode = L.node;
+        }
       }
       if (eff >= 2) {
-        mw_jump_r<true>(P.jump, L, min(eff, P.jump.mmax), w4[0], w4[1]);
+        mw_jump_r<true>(J, L, min(eff, J.mmax), w4[0], w4[1]);
         u0 = (L.room >> 48) == 0 ? 4 : 2;  // left the cell: no steps before its lookup
       }
     }
   }
+  PH_ADD(12, ph12);
+  PH_T0(ph13);
 #if FRW_STEP_UNROLL
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -1991,12 +2180,14 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DSlots& W, c
     code = mw_step<RNG>(P, dd, L, w, z, static_cast<uint32_t>(L.rng * 4 + u), xdir);
   }
 #endif
+  PH_ADD(13, ph13);
   if (RNG == FRW_RNG_PHILOX) ++L.rng;  // next 4-word block
   if (code == 2) {  // moved into another cell: looked up next super-step
     ++L.cchg;
     L.room = 0;
     code = 0;
   }
+  PH_ADD(5, ph5);
   if (code == 0 && L.steps >= cap) return MW_CAP;
   return code;
 }
@@ -2046,7 +2237,9 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
          int* aq_out, int* mq_next) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
+  __shared__ JumpSmem jsm;
+  DJump J;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
   const int n = P.n;
   const int cap = 1000 * n * n;  // microwalk.cpp:81
   const int slice = P.mw_slice > 0 ? P.mw_slice : 0x7FFFFFFF;
@@ -2067,7 +2260,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
     if (live) {
-      code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+      code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
       FRW_DCHECK(C, node_ok(L.node, n));
     }
     if (live && code == MW_GO && --left == 0) {
@@ -2138,12 +2331,16 @@ __global__ void __launch_bounds__(256)
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
   __shared__ int job_sh;
-  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
+  __shared__ JumpSmem jsm;
+  DJump J;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
   const int n = P.n, nn = n * n, m3 = nn * n;
   const int cap = 1000 * n * n;
   uint16_t* grid = scratch + static_cast<size_t>(blockIdx.x) * m3;
   DParams Pd = P;
   Pd.jump.mmax = 0;  // no lattice jumps: a node's ball is not known to be homogeneous
+  DJump Jd = J;
+  Jd.mmax = 0;
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2176,6 +2373,7 @@ __global__ void __launch_bounds__(256)
     L.node = mid | (mid << 8) | (mid << 16);
     L.hnode = L.node;
     L.hom = 0;
+    L.hq = -1;
     L.rng = W.rng[slot];
     L.ncond = L.nbx = 0;
     L.steps = 0;
@@ -2183,7 +2381,7 @@ __global__ void __launch_bounds__(256)
     int code = MW_GO, xdir = 0;
     while (code == MW_GO) {
       if ((L.room >> 48) == 0) dense_cell(grid, AT, n, L);
-      code = mw_superstep<RNG>(Pd, W, AT, dd, n, cap, L, &xdir);
+      code = mw_superstep<RNG>(Pd, Jd, W, AT, dd, n, cap, L, &xdir);
       FRW_DCHECK(C, node_ok(L.node, n));
     }
     if (code == MW_SURFACE) {
@@ -2225,7 +2423,9 @@ __global__ void __launch_bounds__(256, kTailBlocks)
            const int* aq, const int* mq) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
+  __shared__ JumpSmem jsm;
+  DJump J;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
   const int n = P.n;
   const int cap = 1000 * n * n;
   // items: first the MicroWalk hops carried over from the last round (their
@@ -2242,6 +2442,12 @@ __global__ void __launch_bounds__(256, kTailBlocks)
   const int jlane = W.jtail + blockIdx.x * blockDim.x + threadIdx.x;
   bool live = false;
   auto fetch = [&]() {
+#ifdef FRW_TAIL_SOLO
+    if (threadIdx.x & 31) {  // latency experiment: one walk per warp
+      live = false;
+      return;
+    }
+#endif
     const unsigned long long item = atomicAdd(&C->ahead, 1ull);
     live = item < total;
     if (!live) return;
@@ -2258,6 +2464,12 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       in_mw = false;
     }
   };
+#ifdef FRW_PHASE_CLOCKS
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicCAS(&g_tail_t0, 0ull, gtimer());
+    g_in_tail = 1;
+  }
+#endif
   fetch();
   long long cyc_mw = 0, cyc_all = 0;  // warp-uniform clock64 spans
   while (__any_sync(0xFFFFFFFFu, live)) {
@@ -2286,14 +2498,16 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       if (!mwm) break;
       if (!(live && in_mw)) continue;
       int xdir = 0;
-      const int code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+      const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
       FRW_DCHECK(C, node_ok(L.node, n));
       if (code == MW_GO) continue;
       in_mw = false;
       if (code == MW_SURFACE) {
+        PH_T0(ph6);
         mw_exit(W, n, L, xdir);
         adv_load(W, L.slot, A);
         A.jslot = jlane;
+        PH_ADD(6, ph6);
         continue;
       }
       if (code == MW_COND)
@@ -2307,6 +2521,13 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     const long long c2 = clock64();
     cyc_mw += c2 - c1;
     cyc_all += c2 - c0;
+#ifdef FRW_PHASE_CLOCKS
+    if (live || in_mw) {
+      atomicAdd(&g_ph[PH_ROW + 9], static_cast<unsigned long long>(c1 - c0));
+      atomicAdd(&g_ph[PH_ROW + 10], static_cast<unsigned long long>(c2 - c1));
+      atomicAdd(&g_ph[PH_ROW + 25], 1ull);
+    }
+#endif
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&C->tail_mw_cyc, static_cast<unsigned long long>(cyc_mw));
@@ -2361,7 +2582,9 @@ __global__ void __launch_bounds__(256, kTailBlocks)
            const int* aq, int* ring_a, int* ring_m, unsigned mask) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
+  __shared__ JumpSmem jsm;
+  DJump J;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
   const int n = P.n;
   const unsigned long long alen = C->alen;
   if ((threadIdx.x >> 5) < kFlowAdvWarps) {
@@ -2437,7 +2660,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
       }
       if (have) {
         int xdir = 0;
-        const int code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+        const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
         if (code != MW_GO) {
           have = false;
           if (code == MW_SURFACE) {
@@ -2479,7 +2702,9 @@ __global__ void __launch_bounds__(128)
                const uint64_t* states, int count, int with_cond, int cap, DevExit* out) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
+  __shared__ JumpSmem jsm;
+  DJump J;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
   const int n = P.n;
@@ -2507,7 +2732,7 @@ __global__ void __launch_bounds__(128)
   mw_arm(W, t, t, n, L);
   int code = MW_GO, xdir = 0;
   while (code == MW_GO)
-    code = mw_superstep<RNG>(P, W, AT, dd, n, cap, L, &xdir);
+    code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
   const int a = xdir >> 1;
   e.kind = code == MW_SURFACE ? 0 : 1;
   e.dir = xdir;
@@ -2588,7 +2813,9 @@ __global__ void __launch_bounds__(128)
                         int* rc_out, DevEvent* out) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
-  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd);
+  __shared__ JumpSmem jsm;
+  DJump J;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= count) return;
   const int t = idx[q];
@@ -2647,7 +2874,7 @@ __global__ void __launch_bounds__(128)
     ml.wid = t;
     int code = MW_GO, xdir = 0;
     while (code == MW_GO)
-      code = mw_superstep<FRW_RNG_SPLITMIX_PARITY>(P, W, AT, dd, n, cap, ml, &xdir);
+      code = mw_superstep<FRW_RNG_SPLITMIX_PARITY>(P, J, W, AT, dd, n, cap, ml, &xdir);
     e.dispatch = W.mwkind[slot] ? 2 : 1;
     e.mw_steps = ml.steps;
     if (code == MW_SURFACE) {
@@ -3126,6 +3353,7 @@ struct Engine {
   DCounters* d_cnt = nullptr;
   DMiss M{};
   int* mq[2] = {nullptr, nullptr};  // MicroWalk queues (current / next round)
+  int* cq = nullptr;                // walks waiting for k_compile (this round)
   int* aq[2] = {nullptr, nullptr};  // ACTIVE queues (current / next round)
   int* ring_a = nullptr;  // k_flow rings of walk slots (-1 = empty entry)
   int* ring_m = nullptr;
@@ -3148,8 +3376,8 @@ struct Engine {
   // lattice-jump tables (DJump) for lattice size jump_n, radii 2..jump_mmax
   int jump_n = 0, jump_mmax = 0;
   JumpMeta* d_jmeta = nullptr;
-  uint64_t* d_jthr = nullptr;
-  uint16_t* d_jguide = nullptr;
+  uint64_t* d_jthr = nullptr;    // alias acceptance thresholds
+  uint16_t* d_jguide = nullptr;  // aliases
 };
 
 void free_slots(Engine& E) {
@@ -3172,6 +3400,8 @@ void free_slots(Engine& E) {
   cudaFree(E.mq[0]);
   cudaFree(E.mq[1]);
   E.mq[0] = E.mq[1] = nullptr;
+  cudaFree(E.cq);
+  E.cq = nullptr;
   cudaFree(E.W.mwnode);
   cudaFree(E.W.mwhsteps);
   cudaFree(E.W.mwhj);
@@ -3426,8 +3656,9 @@ int ensure_jumps(frw_ctx* ctx, Engine& E, int n, DJump* out) {
   if (mmax < 2) return FRW_OK;
   if (E.jump_n != n || E.jump_mmax != mmax) {
     std::vector<JumpMeta> meta(mmax + 1, JumpMeta{});
-    std::vector<uint64_t> thr;
-    std::vector<uint16_t> guide;
+    std::vector<uint64_t> prob;
+    std::vector<uint16_t> alias;
+    const long double two64 = 18446744073709551616.0L;
     for (int m = 2; m <= mmax; ++m) {
       const int side = 2 * m - 1;
       const size_t K = static_cast<size_t>(side) * side;
@@ -3436,43 +3667,50 @@ int ensure_jumps(frw_ctx* ctx, Engine& E, int n, DJump* out) {
       jump_law(m, f, tot, et);
       if (std::fabs(static_cast<double>(6.0L * tot) - 1.0) > 1e-9)
         return frw_fail(ctx, FRW_ESOLVE, "run_walks: lattice-jump law failed its normalisation");
-      const double st = static_cast<double>(et);
       JumpMeta& jm = meta[m];
-      jm.thr_off = static_cast<uint32_t>(thr.size());
+      jm.off = static_cast<uint32_t>(prob.size());
+      jm.K = static_cast<uint32_t>(K);
       jm.side = static_cast<uint32_t>(side);
-      const long double two64 = 18446744073709551616.0L;
-      long double cum = 0;
+      jm.magic = static_cast<uint32_t>((4294967296ull + side - 1) / side);
+      jm.esteps = static_cast<uint64_t>(static_cast<double>(et) * 4294967296.0 + 0.5);
+      // Walker/Vose alias table of the face law: column i is kept with
+      // probability q_i (scaled so the mean is 1), else its alias
+      std::vector<long double> q(K);
+      std::vector<size_t> small, large;
       for (size_t k = 0; k < K; ++k) {
-        cum += f[k];
-        const long double q = cum / tot * two64;
-        thr.push_back(q >= two64 ? UINT64_MAX : static_cast<uint64_t>(q));
+        q[k] = f[k] / tot * static_cast<long double>(K);
+        (q[k] < 1.0L ? small : large).push_back(k);
       }
-      thr.back() = UINT64_MAX;
-      uint32_t gb = 0;
-      while ((size_t{1} << gb) < K) ++gb;
-      jm.gbits = gb;
-      jm.guide_off = static_cast<uint32_t>(guide.size());
-      size_t i = 0;
-      for (size_t g = 0; g < (size_t{1} << gb); ++g) {
-        const uint64_t lo = static_cast<uint64_t>(g) << (64 - gb);
-        while (thr[jm.thr_off + i] <= lo) ++i;  // first i with T[i] > lo
-        guide.push_back(static_cast<uint16_t>(i));
+      std::vector<uint64_t> pr(K, UINT64_MAX);
+      std::vector<uint16_t> al(K);
+      for (size_t k = 0; k < K; ++k) al[k] = static_cast<uint16_t>(k);
+      while (!small.empty() && !large.empty()) {
+        const size_t a = small.back(), b = large.back();
+        small.pop_back();
+        large.pop_back();
+        const long double t = q[a] * two64;
+        pr[a] = t >= two64 ? UINT64_MAX : static_cast<uint64_t>(t);
+        al[a] = static_cast<uint16_t>(b);
+        q[b] = (q[b] + q[a]) - 1.0L;
+        (q[b] < 1.0L ? small : large).push_back(b);
       }
-      jm.esteps = static_cast<uint64_t>(st * 4294967296.0 + 0.5);
+      // leftovers (rounding) keep their own column
+      prob.insert(prob.end(), pr.begin(), pr.end());
+      alias.insert(alias.end(), al.begin(), al.end());
     }
     cudaFree(E.d_jmeta);
     cudaFree(E.d_jthr);
     cudaFree(E.d_jguide);
     E.jump_n = 0;
     E.d_jmeta = dalloc<JumpMeta>(meta.size());
-    E.d_jthr = dalloc<uint64_t>(thr.size());
-    E.d_jguide = dalloc<uint16_t>(guide.size());
+    E.d_jthr = dalloc<uint64_t>(prob.size());
+    E.d_jguide = dalloc<uint16_t>(alias.size());
     if (!E.d_jmeta || !E.d_jthr || !E.d_jguide)
       return frw_fail(ctx, FRW_ENOMEM, "run_walks: jump table allocation failed");
     FRW_CUDA(ctx, cudaMemcpy(E.d_jmeta, meta.data(), sizeof(JumpMeta) * meta.size(),
                              cudaMemcpyHostToDevice));
-    FRW_CUDA(ctx, cudaMemcpy(E.d_jthr, thr.data(), 8 * thr.size(), cudaMemcpyHostToDevice));
-    FRW_CUDA(ctx, cudaMemcpy(E.d_jguide, guide.data(), 2 * guide.size(), cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(E.d_jthr, prob.data(), 8 * prob.size(), cudaMemcpyHostToDevice));
+    FRW_CUDA(ctx, cudaMemcpy(E.d_jguide, alias.data(), 2 * alias.size(), cudaMemcpyHostToDevice));
     E.jump_n = n;
     E.jump_mmax = mmax;
   }
@@ -3484,8 +3722,8 @@ int ensure_jumps(frw_ctx* ctx, Engine& E, int n, DJump* out) {
   out->hom = 1;  // homogeneous-ball jumps (mw_hom_radius); FRW_MW_HOMJUMP=0 turns them off
   if (const char* e = std::getenv("FRW_MW_HOMJUMP")) out->hom = std::atoi(e);
   out->meta = E.d_jmeta;
-  out->thr = E.d_jthr;
-  out->guide = E.d_jguide;
+  out->prob = E.d_jthr;  // (alias tables)
+  out->alias = E.d_jguide;
   return FRW_OK;
 }
 
@@ -3567,7 +3805,7 @@ int resolve_misses(frw_ctx* ctx, Engine& E, int n, unsigned long long nmiss, frw
 
 // device bytes of one resident walk slot (slot arrays, job, queues, rings,
 // restart lists; ensure_slots)
-constexpr size_t kSlotBytes = 1 + 8 + 24 + 8 + 8 + 4 + 4 + 4 + 8 + 1 + 1 + 32 + 2 + 8 * KMAX + 1 +
+constexpr size_t kSlotBytes = 4 + 1 + 8 + 24 + 8 + 8 + 4 + 4 + 4 + 8 + 1 + 1 + 32 + 2 + 8 * KMAX + 1 +
                               8 * kAtlasWords + 8 + 8 + 8 + 8 + 16 + 16 + 16 + 8 + 4;
 
 // Slot capacity only grows: calls of different sizes (the short last chunk
@@ -3601,6 +3839,7 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   W.atlas = dalloc<uint64_t>(J * kAtlasWords);
   E.mq[0] = dalloc<int>(S);
   E.mq[1] = dalloc<int>(S);
+  E.cq = dalloc<int>(S);
   W.mwnode = dalloc<uint32_t>(S);
   W.mwhsteps = dalloc<int>(S);
   W.mwhj = dalloc<uint64_t>(S);
@@ -3621,7 +3860,7 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
   E.M.dense = dalloc<int>(S);
   if (!W.state || !W.wid || !W.p || !W.weight || !W.rng || !W.hops || !W.cached || !W.mw ||
       !W.mwsteps || !W.branch || !W.resampled || !W.cube || !W.nbox || !W.boxes ||
-      !W.atlas || !W.mwkind || !E.mq[0] || !E.mq[1] || !W.mwnode || !W.mwhsteps || !W.mwhj || !E.aq[0] ||
+      !W.atlas || !W.mwkind || !E.mq[0] || !E.mq[1] || !E.cq || !W.mwnode || !W.mwhsteps || !W.mwhj || !E.aq[0] ||
       !E.aq[1] || !E.ring_a || !E.M.dense ||
       !E.ring_m || !E.M.retry || !E.M.pend || !E.M.park) {
     free_slots(E);
@@ -4642,8 +4881,11 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                                                                     E.d_cnt, M, aq_in, mq_in);
     } else {
       k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in,
-                                                   mq_in, aq_out);
+                                                   E.cq, aq_out);
+      // T_MW includes building the lazy field (engine.cpp:322-324 brackets
+      // microwalk_transit_lazy)
       cudaEventRecord(m0, ctx->stream);
+      k_compile<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(s, P, Wc, E.d_cnt, M, E.cq, mq_in);
       if (P.mode == FRW_MODE_FDM) {
         const FdmQueue Q{mq_in, &E.d_cnt->qlen, &E.d_cnt->qhead, aq_out, &E.d_cnt->a2len};
         if (int rc = launch_fdm(ctx, E, s, P, E.d_cnt, Q)) {
@@ -4745,6 +4987,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       upd.q2len = 0;
       upd.dqlen = 0;
       upd.dqhead = 0;
+      upd.cqlen = 0;
       FRW_CUDA(ctx, cudaMemcpyAsync(E.d_cnt, &upd, sizeof upd, cudaMemcpyHostToDevice,
                                     ctx->stream));
       restarts += c.nretry;
@@ -4858,6 +5101,40 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     float tot = 0;
     cudaEventElapsedTime(&tot, t0, t1);
     out->total_ms = tot;
+#ifdef FRW_PHASE_CLOCKS
+    {
+      std::vector<unsigned long long> rows(256 * 32);
+      cudaMemcpyFromSymbol(rows.data(), g_ph, 8 * rows.size());
+      unsigned long long ph[32] = {};
+      for (int r = 0; r < 256; ++r)
+        for (int i = 0; i < 32; ++i) ph[i] += rows[32 * r + i];
+      static const char* nm[16] = {"hop_scan", "strat_probe", "cached_lookup_sample", "compile_job",
+                                   "cell_change", "superstep", "tail_exit_reload", "-",
+                                   "first_transition", "tail_adv_part", "tail_mw_part",
+                                   "ss_philox", "ss_jump", "ss_steps", "ss_hom_radius", "-"};
+      std::fprintf(stderr, "phase clocks (walks %lld, total %.3f ms):\n", static_cast<long long>(count), tot);
+      for (int i = 0; i < 15; ++i) {
+        const unsigned long long cnt = i == 9 || i == 10 ? ph[25] : ph[16 + i];
+        if (cnt)
+          std::fprintf(stderr, "  %-22s events %12llu  cycles/event %10.1f  total Gcyc %8.3f\n", nm[i],
+                       cnt, static_cast<double>(ph[i]) / cnt, ph[i] * 1e-9);
+      }
+      std::fill(rows.begin(), rows.end(), 0ull);
+      cudaMemcpyToSymbol(g_ph, rows.data(), 8 * rows.size());
+      unsigned long long hist[256];
+      cudaMemcpyFromSymbol(hist, g_tail_hist, sizeof hist);
+      std::fprintf(stderr, "  k_tail completions per 0.25 ms (first launch from its start):");
+      for (int i = 0; i < 256; ++i)
+        if (hist[i]) std::fprintf(stderr, " %d:%llu", i, hist[i]);
+      std::fprintf(stderr, "\n");
+      std::memset(hist, 0, sizeof hist);
+      cudaMemcpyToSymbol(g_tail_hist, hist, sizeof hist);
+      const unsigned long long z = 0;
+      const int zi = 0;
+      cudaMemcpyToSymbol(g_tail_t0, &z, sizeof z);
+      cudaMemcpyToSymbol(g_in_tail, &zi, sizeof zi);
+    }
+#endif
   }
   return status;
 }
