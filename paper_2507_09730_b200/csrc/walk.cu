@@ -249,7 +249,7 @@ struct DSlots {
   double* cube;          // [S][4] center, half width
   uint16_t* nbox;        // [J] conductor boxes among the clipped boxes | boxes << 8
   uint64_t* boxes;       // [S][KMAX] lo.xyz, hi.xyz, class / conductor index
-  uint64_t* atlas;       // [S][kAtlasWords] cell atlas of the job (see cell_info)
+  uint64_t* atlas;       // [S][kAtlasWords] cell atlas of an FDM job (build_atlas; k_fdm)
   uint8_t* mwkind;       // [S] 0 plain MicroWalk job, 1 expanded (MicroWalk-E), 2 FDM
   // a MicroWalk hop carried to the next round (S_MW_CARRY): node, steps so far
   uint32_t* mwnode;
@@ -1008,42 +1008,93 @@ __device__ __forceinline__ uint64_t voxel_mask(const uint64_t* A, const uint64_t
   return M;
 }
 
-// The cell (maximal box of voxels with one box set) containing `node`: its
-// face distances (room, one byte per direction 2a+side) and the classes of
-// the six face-neighbour cells (kFace on a lattice face) with its own class
-// in byte 6.  O(1): three bit scans per axis and nine mask loads.
-__device__ uint64_t cell_info(const uint64_t* A, const uint64_t bm[3], int ncond, int n,
-                              uint32_t node, uint64_t* room_out) {
+// ---- cell lookup by a scan of the job's clipped boxes ----------------------
+// A lane's clipped boxes are read through a strided view: a shared-memory
+// slice (box q of lane t at [q * blockDim + t], conflict-free) when the job
+// has at most kBoxSm boxes, else the job entry in global memory.
+constexpr int kBoxSm = 16;
+constexpr int kBoxSmem512 = 512 * kBoxSm * 8;  // dynamic shared memory of 512- / 256-thread CTAs
+constexpr int kBoxSmem256 = 256 * kBoxSm * 8;
+struct BoxView {
+  const uint64_t* p;
+  int stride;
+  __device__ __forceinline__ uint64_t operator[](int q) const { return p[q * stride]; }
+};
+
+// The cell (maximal box of voxels with one box set) holding `node`, its face
+// distances (room, one byte per direction 2a+side) and the classes of the six
+// face-neighbour cells (kFace on a lattice face) with its own in byte 6, from
+// the boxes themselves (no atlas): along each axis the
+// cell is cut by every box face (lo and hi + 1), so its extent is bounded by
+// the nearest cut at or below the node and the nearest above; the classes of
+// the cell and of the six face-neighbour cells are those of one voxel each
+// (the node, and the voxel just across each face), i.e. of the boxes holding
+// it: any conductor box -> conductor, else the last declared dielectric box
+// (local class q + 1), else background (geometry.cpp:42-62).  Two passes of
+// O(K) register work; no atlas, no global memory when the boxes are staged.
+__device__ uint64_t cell_scan(const BoxView B, int K, int ncond, int n, uint32_t node,
+                              uint64_t* room_out) {
+  const int v0 = coord(node, 0), v1 = coord(node, 1), v2 = coord(node, 2);
+  int lo0 = 0, lo1 = 0, lo2 = 0, hi0 = n - 1, hi1 = n - 1, hi2 = n - 1;
+#pragma unroll 1
+  for (int q = 0; q < K; ++q) {
+    const uint64_t b = B[q];
+#define FRW_CUT(a, v, lo, hi)                              \
+  {                                                        \
+    const int bl = box_lo(b, a), bh = box_hi(b, a) + 1;    \
+    if (bl <= v) lo = max(lo, bl); else hi = min(hi, bl - 1); \
+    if (bh <= v) lo = max(lo, bh); else hi = min(hi, bh - 1); \
+  }
+    FRW_CUT(0, v0, lo0, hi0)
+    FRW_CUT(1, v1, lo1, hi1)
+    FRW_CUT(2, v2, lo2, hi2)
+#undef FRW_CUT
+  }
+  // box sets of the node and of the voxels across the six faces
+  uint64_t M = 0, Ml0 = 0, Mh0 = 0, Ml1 = 0, Mh1 = 0, Ml2 = 0, Mh2 = 0;
+#pragma unroll 1
+  for (int q = 0; q < K; ++q) {
+    const uint64_t b = B[q], bit = 1ull << q;
+    const int bl0 = box_lo(b, 0), bh0 = box_hi(b, 0), bl1 = box_lo(b, 1), bh1 = box_hi(b, 1),
+              bl2 = box_lo(b, 2), bh2 = box_hi(b, 2);
+    const bool i0 = bl0 <= v0 && v0 <= bh0, i1 = bl1 <= v1 && v1 <= bh1,
+               i2 = bl2 <= v2 && v2 <= bh2;
+    if (i0 && i1 && i2) M |= bit;
+    if (i1 && i2) {
+      if (bl0 <= lo0 - 1 && lo0 - 1 <= bh0) Ml0 |= bit;
+      if (bl0 <= hi0 + 1 && hi0 + 1 <= bh0) Mh0 |= bit;
+    }
+    if (i0 && i2) {
+      if (bl1 <= lo1 - 1 && lo1 - 1 <= bh1) Ml1 |= bit;
+      if (bl1 <= hi1 + 1 && hi1 + 1 <= bh1) Mh1 |= bit;
+    }
+    if (i0 && i1) {
+      if (bl2 <= lo2 - 1 && lo2 - 1 <= bh2) Ml2 |= bit;
+      if (bl2 <= hi2 + 1 && hi2 + 1 <= bh2) Mh2 |= bit;
+    }
+  }
   const uint64_t cmask = cond_mask(ncond);
-  uint64_t M[3], Ml[3], Mh[3];
-  bool hl[3], hh[3];
   uint64_t room = 0x0101ull << 48;  // two unused bytes kept non-zero
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const int v = coord(node, a);
-    const uint64_t below = bm[a] & upto(v), above = bm[a] & ~upto(v);
-    const int sg = __popcll(below) - 1;
-    const int lo = 63 - __clzll(below);
-    const int hi = above ? __ffsll(above) - 2 : n - 1;
-    room |= static_cast<uint64_t>(v - lo) << (16 * a);
-    room |= static_cast<uint64_t>(hi - v) << (16 * a + 8);
-    const uint64_t* mk = A + kAtMask + 64 * a;
-    hl[a] = lo > 0;
-    hh[a] = hi < n - 1;
-    M[a] = mk[sg];
-    Ml[a] = hl[a] ? mk[sg - 1] : 0;
-    Mh[a] = hh[a] ? mk[sg + 1] : 0;
-  }
-  uint64_t fc = static_cast<uint64_t>(class_of(M[0] & M[1] & M[2], cmask)) << 48;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const uint64_t rest = M[(a + 1) % 3] & M[(a + 2) % 3];
-    const uint64_t cl = hl[a] ? class_of(Ml[a] & rest, cmask) : kFace;
-    const uint64_t ch = hh[a] ? class_of(Mh[a] & rest, cmask) : kFace;
-    fc |= cl << (16 * a) | ch << (16 * a + 8);
-  }
+  room |= static_cast<uint64_t>(v0 - lo0) | static_cast<uint64_t>(hi0 - v0) << 8 |
+          static_cast<uint64_t>(v1 - lo1) << 16 | static_cast<uint64_t>(hi1 - v1) << 24 |
+          static_cast<uint64_t>(v2 - lo2) << 32 | static_cast<uint64_t>(hi2 - v2) << 40;
   *room_out = room;
+  uint64_t fc = static_cast<uint64_t>(class_of(M, cmask)) << 48;
+  fc |= static_cast<uint64_t>(lo0 > 0 ? class_of(Ml0, cmask) : kFace);
+  fc |= static_cast<uint64_t>(hi0 < n - 1 ? class_of(Mh0, cmask) : kFace) << 8;
+  fc |= static_cast<uint64_t>(lo1 > 0 ? class_of(Ml1, cmask) : kFace) << 16;
+  fc |= static_cast<uint64_t>(hi1 < n - 1 ? class_of(Mh1, cmask) : kFace) << 24;
+  fc |= static_cast<uint64_t>(lo2 > 0 ? class_of(Ml2, cmask) : kFace) << 32;
+  fc |= static_cast<uint64_t>(hi2 < n - 1 ? class_of(Mh2, cmask) : kFace) << 40;
   return fc;
+}
+
+// the first declared conductor box holding voxel v (-1: none)
+__device__ __forceinline__ int cond_box_at(const BoxView B, int ncond, const int v[3]) {
+#pragma unroll 1
+  for (int q = 0; q < ncond; ++q)
+    if (box_has(B[q], v[0], v[1], v[2])) return q;
+  return -1;
 }
 
 // builds the atlas of the K clipped boxes of a job (compile_mw_job)
@@ -1084,7 +1135,7 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
 // (EngulfedStart), 3 when more than KMAX boxes reach into the cube (only
 // the cube is stored: the hop runs on a dense grid, k_mw_dense).
 __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
-                              double h, int n, bool conductors, DCounters* C) {
+                              double h, int n, bool conductors, bool atlas, DCounters* C) {
   FRW_DCHECK(C, slot >= 0 && slot < W.J);
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
   uint64_t* A = W.atlas + static_cast<size_t>(slot) * kAtlasWords;
@@ -1146,18 +1197,22 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
         boxes[K++] = pk | (0x8000ull | static_cast<uint64_t>(q)) << 48;
       } else {
         const int dc = __ldg(s.dcls + q);
-        cls[K] = static_cast<uint16_t>(dc);
+        if (atlas) cls[K] = static_cast<uint16_t>(dc);
         boxes[K++] = pk | static_cast<uint64_t>(dc) << 48;
       }
     }
   }
-  uint64_t bm[3];
-  build_atlas(boxes, K, n, A, bm);
+  // the cell atlas only for FDM jobs (k_fdm classifies voxels from it); the
+  // MicroWalk kernels look cells up by scanning the boxes (cell_scan)
+  if (atlas) {
+    uint64_t bm[3];
+    build_atlas(boxes, K, n, A, bm);
+  }
   const int m = (n - 1) / 2;  // start_node (sgf.hpp:58-61)
   const int v0[3] = {m, m, m};
   // EngulfedStart (microwalk.cpp:83-86): a conductor box holds the start
   // voxel.  The start cell itself is looked up by the first super-step.
-  if (voxel_mask(A, bm, v0) & cond_mask(ncond)) return 0;
+  if (ncond && cond_box_at(BoxView{boxes, 1}, ncond, v0) >= 0) return 0;
   W.nbox[slot] = static_cast<uint16_t>(ncond | K << 8);
   W.cube[4 * slot + 0] = c[0];
   W.cube[4 * slot + 1] = c[1];
@@ -1475,7 +1530,7 @@ __device__ __forceinline__ int hop_compile(const DStruct& s, const DParams& P, c
   int rc = -1;
 #pragma unroll 1
   for (;;) {
-    rc = compile_mw_job(s, W, jslot, jc, jh, n, expanded, C);
+    rc = compile_mw_job(s, W, jslot, jc, jh, n, expanded, kind == 2, C);
     if (rc != 0 || !expanded) break;
     expanded = false;
     jc[0] = c[0];
@@ -1705,12 +1760,12 @@ struct MwLane {
   uint64_t fc;    // face-neighbour classes (byte per dir), current class in byte 6
   uint64_t rng;   // SplitMix64 state or Philox block counter
   int steps;
-  int ncond;      // conductor boxes of the job (atlas bits [0, ncond))
+  int ncond;      // conductor boxes of the job (boxes [0, ncond))
   int nbx;        // clipped boxes of the job
   int hom;        // homogeneous radius known at node hnode (0: none)
   uint32_t hnode;
   int hq;         // the clipped box that limited it (-1: the lattice), see mw_superstep
-  uint64_t bm[3]; // segment-start bitmaps of the job's atlas
+  BoxView bx;     // the job's clipped boxes (shared-memory slice or job entry)
   double al[6];   // alpha of the neighbour across each face of the cell
   uint32_t gsteps;  // diagnostics, accumulated across the lane's hops
   uint32_t cchg;
@@ -1730,20 +1785,24 @@ struct AlphaTab {
 
 // the per-face alphas of the lane's cell: palette pair (face class, own
 // class), 1 for lattice and conductor faces (both absorb the step)
-__device__ __forceinline__ void lane_alphas(const AlphaTab& T, const uint64_t* A, MwLane& L) {
-  const int g0 = global_class(A, static_cast<int>((L.fc >> 48) & 0xFF), T.bg);
+// palette class of a job-local class (0: background, q + 1: dielectric box q)
+__device__ __forceinline__ int lane_class(const MwLane& L, int lc, int bg) {
+  return lc ? box_cls(L.bx[lc - 1]) : bg;
+}
+__device__ __forceinline__ void lane_alphas(const AlphaTab& T, MwLane& L) {
+  const int g0 = lane_class(L, static_cast<int>((L.fc >> 48) & 0xFF), T.bg);
   if (T.tab) {
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
       const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-      L.al[d] = T.tab[cn >= kCond ? T.Pn * T.Pn : global_class(A, cn, T.bg) * T.Pn + g0];
+      L.al[d] = T.tab[cn >= kCond ? T.Pn * T.Pn : lane_class(L, cn, T.bg) * T.Pn + g0];
     }
   } else {
     const double e0 = __ldg(T.pal + g0);
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
       const int cn = static_cast<int>((L.fc >> (8 * d)) & 0xFF);
-      const double en = cn >= kCond ? 0.0 : __ldg(T.pal + global_class(A, cn, T.bg));
+      const double en = cn >= kCond ? 0.0 : __ldg(T.pal + lane_class(L, cn, T.bg));
       L.al[d] = cn >= kCond ? 1.0 : en / (en + e0);
     }
   }
@@ -1753,9 +1812,11 @@ __device__ __forceinline__ const uint64_t* lane_atlas(const DSlots& W, int slot)
   return W.atlas + static_cast<size_t>(slot) * kAtlasWords;
 }
 
-__device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int n, MwLane& L) {
+// bsm: the kernel's shared-memory box slices (kBoxSm per thread, strided by
+// blockDim), or null: jobs with at most kBoxSm boxes are staged there
+__device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int n, MwLane& L,
+                                       uint64_t* bsm) {
   const int m = (n - 1) / 2;
-  const uint64_t* A = lane_atlas(W, jslot);
   L.slot = slot;
   L.jslot = jslot;
   L.wid = W.wid[slot];
@@ -1769,9 +1830,17 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int
   }
   L.hom = 0;
   L.hq = -1;
-  L.bm[0] = A[kAtBm];
-  L.bm[1] = A[kAtBm + 1];
-  L.bm[2] = A[kAtBm + 2];
+  {
+    const uint64_t* G = W.boxes + static_cast<size_t>(jslot) * KMAX;
+    if (bsm && L.nbx <= kBoxSm) {
+      uint64_t* d = bsm + threadIdx.x;
+#pragma unroll 4
+      for (int q = 0; q < L.nbx; ++q) d[q * blockDim.x] = G[q];
+      L.bx = BoxView{d, static_cast<int>(blockDim.x)};
+    } else {
+      L.bx = BoxView{G, 1};
+    }
+  }
   L.steps = 0;
   L.hnode = L.node;
   if (W.state[slot] == S_MW_CARRY) {  // a hop carried over from the last round
@@ -1799,12 +1868,10 @@ __device__ __forceinline__ void mw_carry(const DSlots& W, DCounters* C, int* mq_
   mq_next[qn] = L.slot;
 }
 
-// a move left the current cell: look the new cell up in the atlas
-__device__ __forceinline__ void mw_cell_change(const DSlots& W, const AlphaTab& T, int n,
-                                               MwLane& L) {
-  const uint64_t* A = lane_atlas(W, L.jslot);
-  L.fc = cell_info(A, L.bm, L.ncond, n, L.node, &L.room);
-  lane_alphas(T, A, L);
+// a move left the current cell: look the new cell up from the job's boxes
+__device__ __forceinline__ void mw_cell_change(const AlphaTab& T, int n, MwLane& L) {
+  L.fc = cell_scan(L.bx, L.nbx, L.ncond, n, L.node, &L.room);
+  lane_alphas(T, L);
 }
 
 // surface exit: continuation point, counters, slot back to ACTIVE
@@ -2056,14 +2123,13 @@ __device__ __forceinline__ int lattice_ball(const int v[3], int n) {
   return m;
 }
 // *hq: the box that brought the radius below 2 or set it (-1: the lattice)
-__device__ int mw_hom_radius(const DSlots& W, const MwLane& L, int n, int* hq) {
+__device__ int mw_hom_radius(const MwLane& L, int n, int* hq) {
   const int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
   int m = lattice_ball(v, n);
   int arg = -1;
-  const uint64_t* B = W.boxes + static_cast<size_t>(L.jslot) * KMAX;
 #pragma unroll 1
   for (int q = 0; q < L.nbx && m >= 2; ++q) {
-    const int mb = box_ball(B[q], v);
+    const int mb = box_ball(L.bx[q], v);
     if (mb < m) {
       m = mb;
       arg = q;
@@ -2115,7 +2181,7 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DJump& J, co
   PH_T0(ph5);
   if ((L.room >> 48) == 0) {
     PH_T0(ph4);
-    mw_cell_change(W, AT, n, L);
+    mw_cell_change(AT, n, L);
     PH_ADD(4, ph4);
   }
   int code = 0;
@@ -2140,12 +2206,11 @@ __device__ __forceinline__ int mw_superstep(const DParams& P, const DJump& J, co
         // last time allows here: the full O(boxes) scan only when that is >= 2
         const int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
         int lim = lattice_ball(v, n);
-        if (L.hq >= 0)
-          lim = min(lim, box_ball(W.boxes[static_cast<size_t>(L.jslot) * KMAX + L.hq], v));
+        if (L.hq >= 0) lim = min(lim, box_ball(L.bx[L.hq], v));
         if (lim >= 2) {
           PH_T0(ph14);
           int hq;
-          eff = mw_hom_radius(W, L, n, &hq);
+          eff = mw_hom_radius(L, n, &hq);
           L.hq = hq;
           PH_ADD(14, ph14);
           L.hom = eff;
@@ -2199,8 +2264,7 @@ __device__ void mw_conductor_exit(const DSlots& W, WalkRec* recs, DCounters* C, 
                                   int xdir) {
   int v[3] = {coord(L.node, 0), coord(L.node, 1), coord(L.node, 2)};
   v[xdir >> 1] += (xdir & 1) ? 1 : -1;
-  const uint64_t cm = voxel_mask(lane_atlas(W, L.jslot), L.bm, v) & cond_mask(L.ncond);
-  const int ci = box_cond(W.boxes[static_cast<size_t>(L.jslot) * KMAX + __ffsll(cm) - 1]);
+  const int ci = box_cond(L.bx[cond_box_at(L.bx, L.ncond, v)]);
   W.mw[L.slot] += 1;
   W.mwsteps[L.slot] += L.steps;
   finish_walk(W, recs, C, L.slot, ci, false);
@@ -2237,6 +2301,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
          int* aq_out, int* mq_next) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
+  extern __shared__ uint64_t frw_dsm[];  // kBoxSm box slices per thread (mw_arm)
   __shared__ JumpSmem jsm;
   DJump J;
   const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
@@ -2255,7 +2320,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
   if (live) {
     const int q = queue[item];
     FRW_DCHECK(C, q >= 0 && q < W.S);
-    mw_arm(W, q, q, n, L);
+    mw_arm(W, q, q, n, L, frw_dsm);
   }
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
@@ -2282,7 +2347,7 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
       if (live) {
         const int q = queue[item];
         FRW_DCHECK(C, q >= 0 && q < W.S);
-        mw_arm(W, q, q, n, L);
+        mw_arm(W, q, q, n, L, frw_dsm);
       }
     }
   }
@@ -2423,6 +2488,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
            const int* aq, const int* mq) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
+  extern __shared__ uint64_t frw_dsm[];  // kBoxSm box slices per thread (mw_arm)
   __shared__ JumpSmem jsm;
   DJump J;
   const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
@@ -2454,7 +2520,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     if (item < qc) {
       const int q = mq[item];
       FRW_DCHECK(C, q >= 0 && q < W.S);
-      mw_arm(W, q, q, n, L);
+      mw_arm(W, q, q, n, L, frw_dsm);
       in_mw = true;
     } else {
       const int q = aq[item - qc];
@@ -2483,7 +2549,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
       if (r == 2) {
         in_mw = true;
-        mw_arm(W, A.slot, A.jslot, n, L);
+        mw_arm(W, A.slot, A.jslot, n, L, frw_dsm);
       } else if (r == 1) {
         fetch();
       }
@@ -2582,6 +2648,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
            const int* aq, int* ring_a, int* ring_m, unsigned mask) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
+  extern __shared__ uint64_t frw_dsm[];  // kBoxSm box slices per thread (mw_arm)
   __shared__ JumpSmem jsm;
   DJump J;
   const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
@@ -2648,7 +2715,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         if (v >= 0) {
           ring_m[res & mask] = -1;
           __threadfence();
-          mw_arm(W, v, v, n, L);
+          mw_arm(W, v, v, n, L, frw_dsm);
           have = true;
           res = -1;
         }
@@ -2713,7 +2780,7 @@ __global__ void __launch_bounds__(128)
   DevExit e{};
   e.conductor = -1;
   e.panel = -1;
-  const int rc = compile_mw_job(s, W, t, c, h, n, with_cond != 0, C);
+  const int rc = compile_mw_job(s, W, t, c, h, n, with_cond != 0, false, C);
   if (rc != 1) {
     if (rc == 3) set_err(C, FRW_EINVAL);  // the single-transit API keeps the KMAX cap
     e.kind = rc == 0 ? -1 : -2;  // EngulfedStart / too many boxes (error set)
@@ -2729,7 +2796,7 @@ __global__ void __launch_bounds__(128)
   L.jumps = 0;
   L.jsteps = 0;
   L.cchg = 0;
-  mw_arm(W, t, t, n, L);
+  mw_arm(W, t, t, n, L, nullptr);
   int code = MW_GO, xdir = 0;
   while (code == MW_GO)
     code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
@@ -2748,8 +2815,7 @@ __global__ void __launch_bounds__(128)
   } else if (code == MW_COND) {
     int v[3] = {e.voxel[0], e.voxel[1], e.voxel[2]};
     v[a] += (xdir & 1) ? 1 : -1;
-    const uint64_t cm = voxel_mask(lane_atlas(W, t), L.bm, v) & cond_mask(L.ncond);
-    e.conductor = box_cond(W.boxes[static_cast<size_t>(t) * KMAX + __ffsll(cm) - 1]);
+    e.conductor = box_cond(L.bx[cond_box_at(L.bx, L.ncond, v)]);
     // lattice_voxel_center + half a pitch towards the conductor
     // (microwalk.cpp:24-30, :141-143)
     const double pitch = 2.0 * h / n;
@@ -2870,7 +2936,7 @@ __global__ void __launch_bounds__(128)
     ml.jumps = 0;
     ml.jsteps = 0;
     ml.cchg = 0;
-    mw_arm(W, slot, slot, n, ml);
+    mw_arm(W, slot, slot, n, ml, nullptr);
     ml.wid = t;
     int code = MW_GO, xdir = 0;
     while (code == MW_GO)
@@ -2886,9 +2952,8 @@ __global__ void __launch_bounds__(128)
     } else if (code == MW_COND) {
       int v[3] = {coord(ml.node, 0), coord(ml.node, 1), coord(ml.node, 2)};
       v[xdir >> 1] += (xdir & 1) ? 1 : -1;
-      const uint64_t cm = voxel_mask(lane_atlas(W, slot), ml.bm, v) & cond_mask(ml.ncond);
       e.kind = 1;
-      e.conductor = box_cond(W.boxes[static_cast<size_t>(slot) * KMAX + __ffsll(cm) - 1]);
+      e.conductor = box_cond(ml.bx[cond_box_at(ml.bx, ml.ncond, v)]);
     } else {
       set_err(C, FRW_ESTEPCAP);
     }
@@ -4845,6 +4910,17 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   P.adv_slice = kAdvSlice;
   if (const char* e = std::getenv("FRW_MW_SLICE")) P.mw_slice = use_flow ? 0 : std::atoi(e);
   if (const char* e = std::getenv("FRW_ADV_SLICE")) P.adv_slice = std::atoi(e);
+  {  // the box slices are dynamic shared memory beyond the 48 KB default
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(k_mw<FRW_RNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem512);
+      cudaFuncSetAttribute(k_mw<FRW_RNG_SPLITMIX_PARITY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem512);
+      cudaFuncSetAttribute(k_tail<FRW_RNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem256);
+      cudaFuncSetAttribute(k_tail<FRW_RNG_SPLITMIX_PARITY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem256);
+      cudaFuncSetAttribute(k_flow<FRW_RNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem256);
+      cudaFuncSetAttribute(k_flow<FRW_RNG_SPLITMIX_PARITY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem256);
+    });
+  }
   bool tail = false;
   double mw_ms = 0;
   unsigned long long tail_cyc_mw0 = 0, tail_cyc_all0 = 0;
@@ -4868,16 +4944,16 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         FRW_CUDA(ctx, cudaMemsetAsync(E.ring_m, 0xFF, 4ull * (E.ring_mask + 1), ctx->stream));
         k_flow_init<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
         if (P.rng == FRW_RNG_PHILOX)
-          k_flow<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(
+          k_flow<FRW_RNG_PHILOX><<<tb, 256, kBoxSmem256, ctx->stream>>>(
               s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
         else
-          k_flow<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(
+          k_flow<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, kBoxSmem256, ctx->stream>>>(
               s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
       } else if (P.rng == FRW_RNG_PHILOX)
-        k_tail<FRW_RNG_PHILOX><<<tb, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M,
+        k_tail<FRW_RNG_PHILOX><<<tb, 256, kBoxSmem256, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M,
                                                            aq_in, mq_in);
       else
-        k_tail<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs,
+        k_tail<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, kBoxSmem256, ctx->stream>>>(s, T, P, Wc, E.recs,
                                                                     E.d_cnt, M, aq_in, mq_in);
     } else {
       k_advance<<<adv_grid, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in,
@@ -4893,10 +4969,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
           break;
         }
       } else if (P.rng == FRW_RNG_PHILOX)
-        k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, 0, ctx->stream>>>(s, P, Wc, E.recs, E.d_cnt,
+        k_mw<FRW_RNG_PHILOX><<<mw_grid, 512, kBoxSmem512, ctx->stream>>>(s, P, Wc, E.recs, E.d_cnt,
                                                                mq_in, aq_out, mq_next);
       else
-        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, 0, ctx->stream>>>(
+        k_mw<FRW_RNG_SPLITMIX_PARITY><<<mw_grid, 512, kBoxSmem512, ctx->stream>>>(
             s, P, Wc, E.recs, E.d_cnt, mq_in, aq_out, mq_next);
     }
     // hops with more than KMAX boxes in their cube (exits 0 at once if none)
