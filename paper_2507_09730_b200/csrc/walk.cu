@@ -594,6 +594,8 @@ __device__ __forceinline__ double uniform(const DParams& P, long long wid, Rng& 
 // returns the key axis (0..2) and rounded layers, or -1 (general cube),
 // -2 (error: slice centre outside the world)
 __device__ void clip_axis(double c, double h, int n, double lo, double hi, int* il, int* ih);
+__device__ void clip_axis(double c, double h, double p, double ip, int n, double lo, double hi,
+                          int* il, int* ih);
 
 // The stratification probe of a transition cube, held in registers (no
 // per-slice arrays: the walk kernels keep no local memory on this path).
@@ -745,12 +747,17 @@ __device__ Prof strat_probe(const DStruct& s, const double c[3], double h, int n
     // pass 2: paint the hits' slice intervals in declaration order
     P.cls[0] = s.bg;
     P.msk[0] = n >= 64 ? ~0ull : (1ull << n) - 1;
+    const double pitch = 2.0 * h / n, ipitch = 1.0 / pitch;
+    // one rolled copy of the paint step: the hits leave the front of the
+    // sorted register list one by one (static indices, no local memory)
+#pragma unroll 1
+    for (int i = 0; i < nh; ++i) {
+      const int d = hit[0];
 #pragma unroll
-    for (int i = 0; i < kProfHits; ++i) {
-      if (hit[i] == 0x7FFFFFFF) continue;
-      const int d = hit[i];
+      for (int j = 0; j + 1 < kProfHits; ++j) hit[j] = hit[j + 1];
       int lo, hi;
-      clip_axis(c[ax], h, n, __ldg(s.dbox + 6 * d + ax), __ldg(s.dbox + 6 * d + 3 + ax), &lo, &hi);
+      clip_axis(c[ax], h, pitch, ipitch, n, __ldg(s.dbox + 6 * d + ax),
+                __ldg(s.dbox + 6 * d + 3 + ax), &lo, &hi);
       if (lo > hi) continue;
       const uint64_t m = slice_bits(lo, hi);
       const int k = __ldg(s.dcls + d);
@@ -1570,6 +1577,9 @@ __device__ __forceinline__ int hop_compile(const DStruct& s, const DParams& P, c
 // table miss), 2 when its walk needs a MicroWalk hop: with a compile queue
 // `cq` (wavefront rounds) the walk is queued for k_compile, else its job is
 // compiled here into the lane's job entry.
+// QUEUE: the compile queue is always given (k_advance), so the inline job
+// compiler is not instantiated there
+template <bool QUEUE = false>
 __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, const DSlots& W,
                             WalkRec* recs, DCounters* C, const DMiss& M, int* cq, AdvLane& L) {
   const int slot = L.slot;
@@ -1645,7 +1655,7 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   W.hops[slot] = L.hops + 1;
   W.cached[slot] = L.cached;
   W.state[slot] = S_NEED_MW;
-  if (cq) {
+  if (QUEUE || cq) {
     // wavefront rounds: k_compile builds the job, every lane of a warp
     // compiling one (in k_advance only a few lanes of a warp would, the rest
     // waiting: the job compiler was over half of k_advance's issue slots at
@@ -1693,7 +1703,7 @@ __global__ void __launch_bounds__(256, FRW_ADV_MINB)
   int left = slice;  // transitions left in this visit of the walk
   while (__any_sync(0xFFFFFFFFu, live)) {
     if (!live) continue;
-    int r = advance_once(s, T, P, W, recs, C, M, cq, L);
+    int r = advance_once<true>(s, T, P, W, recs, C, M, cq, L);
     if (r == 0 && --left == 0) {
       // a long chain of cached hops: the walk continues next round
       W.p[3 * L.slot] = L.p[0];
@@ -1785,6 +1795,15 @@ struct AlphaTab {
 
 // the per-face alphas of the lane's cell: palette pair (face class, own
 // class), 1 for lattice and conductor faces (both absorb the step)
+// global -> shared 8-byte asynchronous copy (cp.async, sm_80+)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // palette class of a job-local class (0: background, q + 1: dielectric box q)
 __device__ __forceinline__ int lane_class(const MwLane& L, int lc, int bg) {
   return lc ? box_cls(L.bx[lc - 1]) : bg;
@@ -1834,8 +1853,11 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int
     const uint64_t* G = W.boxes + static_cast<size_t>(jslot) * KMAX;
     if (bsm && L.nbx <= kBoxSm) {
       uint64_t* d = bsm + threadIdx.x;
-#pragma unroll 4
-      for (int q = 0; q < L.nbx; ++q) d[q * blockDim.x] = G[q];
+      // asynchronous copies (LDGSTS): the loads go out back to back and no
+      // register waits on them until the one wait below
+#pragma unroll 1
+      for (int q = 0; q < L.nbx; ++q) cp_async8(d + q * blockDim.x, G + q);
+      cp_async_wait_all();
       L.bx = BoxView{d, static_cast<int>(blockDim.x)};
     } else {
       L.bx = BoxView{G, 1};
@@ -2315,12 +2337,17 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
   L.jsteps = 0;
   L.cchg = 0;
   int left = slice;  // super-steps left in this visit of the hop
-  unsigned long long item = atomicAdd(&C->qhead, 1ull);
-  bool live = item < qlen;
+  // (popping one job ahead to take the queue read off the re-arm path lost
+  // 3-8%: lanes holding a reserved job lengthen the round's last hops)
+  auto pop = [&]() -> int {
+    const unsigned long long it = atomicAdd(&C->qhead, 1ull);
+    return it < qlen ? queue[it] : -1;
+  };
+  const int q0 = pop();
+  bool live = q0 >= 0;
   if (live) {
-    const int q = queue[item];
-    FRW_DCHECK(C, q >= 0 && q < W.S);
-    mw_arm(W, q, q, n, L, frw_dsm);
+    FRW_DCHECK(C, q0 >= 0 && q0 < W.S);
+    mw_arm(W, q0, q0, n, L, frw_dsm);
   }
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
@@ -2342,10 +2369,9 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
         set_err(C, FRW_ESTEPCAP);
       }
       left = slice;
-      item = atomicAdd(&C->qhead, 1ull);
-      live = item < qlen;
+      const int q = pop();
+      live = q >= 0;
       if (live) {
-        const int q = queue[item];
         FRW_DCHECK(C, q >= 0 && q < W.S);
         mw_arm(W, q, q, n, L, frw_dsm);
       }
@@ -4895,7 +4921,9 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   const int adv_grid = ctx->sm_count * 4;  // persistent: 4 x 256 threads per SM
   const int mw_grid = ctx->sm_count * 2;   // persistent: 2 x 512 threads per SM
   // run-to-completion threshold (active walks); FRW_TAIL_WALKS overrides
-  unsigned long long tail_threshold = static_cast<unsigned long long>(ctx->sm_count) * 2048;
+  // (148 * 1024 after the box-scan cells: C3/C5 +7-8% over 148 * 2048; 100K-200K
+  // within 1%, tools/tail_sweep2.sh)
+  unsigned long long tail_threshold = static_cast<unsigned long long>(ctx->sm_count) * 1024;
   if (const char* e = std::getenv("FRW_TAIL_WALKS")) tail_threshold = std::strtoull(e, nullptr, 10);
   // tail kernel: k_tail by default; FRW_TAIL_KERNEL=flow selects the
   // warp-specialised k_flow (C3/C5 within a few % either way)
