@@ -60,7 +60,7 @@ void Config::validate() const {
   if (hop_cap < 1) throw std::invalid_argument("hop_cap must be >= 1");
   if (!(gaussian_gap_fraction > 0.0 && gaussian_gap_fraction < 1.0))
     throw std::invalid_argument("gaussian_gap_fraction must lie in (0,1)");
-  if (grid_n > 64) throw std::invalid_argument("grid_n must be <= 64 on the device");
+  if (grid_n > 128) throw std::invalid_argument("grid_n must be <= 128 on the device");
   if (device_batch < 0) throw std::invalid_argument("device_batch must be >= 0 (0 = auto)");
   for (int d : devices)
     if (d < 0) throw std::invalid_argument("devices: device indices must be >= 0");

@@ -24,7 +24,8 @@ namespace frw {
 namespace {
 
 constexpr int kSolveThreads = 1024;
-constexpr int kMaxN = 64;
+constexpr int kMaxN = 128;     // stratified keys (direct solve): the walk engine's grid_n cap
+constexpr int kGridMaxN = 64;  // general grids (Jacobi-PCG, FDM / validate-sgf)
 
 __device__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -65,7 +66,7 @@ __device__ __forceinline__ double dst2(int n, int k, int i) {  // q_k[i], k = 1.
 __global__ void __launch_bounds__(kDirectThreads)
     k_sgf_direct(int n, const int* axes, const double* layers, double* scratch, double* out) {
   __shared__ double e[kMaxN], adiag[kMaxN], aoff[kMaxN], lam[kMaxN];
-  __shared__ double q[kMaxN * kMaxN];  // q[k * n + i], k = 0..n-1 for modes 1..n
+  extern __shared__ double q[];  // [n * n]: q[k * n + i], k = 0..n-1 for modes 1..n
   const int key = blockIdx.x;
   const int axis = axes[key];
   const int nn = n * n, m = nn * n, P = 6 * nn;
@@ -338,14 +339,16 @@ extern "C" int frw_sgf_solve(frw_ctx* ctx, int n, int count, const int* axes,
                              const double* layers, double* probs, double* kernels) {
   if (!ctx || !axes || !layers || !probs) return FRW_EINVAL;
   if (n < 1 || n > kMaxN || count < 0)
-    return frw_fail(ctx, FRW_EINVAL, "sgf_solve: need 1 <= n <= 64");
+    return frw_fail(ctx, FRW_EINVAL, "sgf_solve: need 1 <= n <= 128");
   if (count == 0) return FRW_OK;
   for (int q = 0; q < count; ++q)
     if (axes[q] < 0 || axes[q] > 2) return frw_fail(ctx, FRW_EINVAL, "sgf_solve: bad axis");
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   const size_t m = static_cast<size_t>(n) * n * n, P = 6ull * n * n;
-  // bounded scratch (kept in the context): solve in chunks of keys
-  const int chunk = std::min(count, 128);
+  // bounded scratch (kept in the context): solve in chunks of keys, at most
+  // 128 keys or ~2 GB of slabs (8 n^3 doubles per key: 134 MB at n = 128)
+  const int chunk = static_cast<int>(std::max<size_t>(
+      1, std::min<size_t>(std::min(count, 128), (size_t{2} << 30) / (64 * m))));
   const size_t b_lay = (8 * static_cast<size_t>(chunk) * n + 255) / 256 * 256;
   const size_t b_ax = (4 * static_cast<size_t>(chunk) + 255) / 256 * 256;
   const size_t b_slab = 8 * 8 * m * static_cast<size_t>(chunk);
@@ -370,7 +373,10 @@ extern "C" int frw_sgf_solve(frw_ctx* ctx, int n, int count, const int* axes,
                     cudaMemcpyHostToDevice, ctx->stream);
     cudaMemcpyAsync(d_ax, axes + k0, 4 * static_cast<size_t>(kc), cudaMemcpyHostToDevice,
                     ctx->stream);
-    k_sgf_direct<<<kc, kDirectThreads, 0, ctx->stream>>>(n, d_ax, d_lay, slab, out);
+    const int qbytes = 8 * n * n;  // the DST-II basis (128 KB at n = 128)
+    if (qbytes > 48 * 1024)
+      cudaFuncSetAttribute(k_sgf_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, qbytes);
+    k_sgf_direct<<<kc, kDirectThreads, qbytes, ctx->stream>>>(n, d_ax, d_lay, slab, out);
     cudaMemcpyAsync(h.data(), out, 8 * P * 4 * static_cast<size_t>(kc), cudaMemcpyDeviceToHost,
                     ctx->stream);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
@@ -401,7 +407,7 @@ extern "C" int frw_grid_sgf_solve(frw_ctx* ctx, int n, int count, const double* 
                                   double half_width, double* probs, double* kernels,
                                   double* steps) {
   if (!ctx || !eps || (!probs && !kernels && !steps)) return FRW_EINVAL;
-  if (n < 1 || n > kMaxN || count < 0 || !(half_width > 0))
+  if (n < 1 || n > kGridMaxN || count < 0 || !(half_width > 0))
     return frw_fail(ctx, FRW_EINVAL, "grid_sgf_solve: need 1 <= n <= 64, half_width > 0");
   if (count == 0) return FRW_OK;
   const size_t m = static_cast<size_t>(n) * n * n, P = 6ull * n * n;

@@ -48,7 +48,8 @@ namespace frw {
 namespace {
 
 constexpr int KMAX = 64;    // clipped boxes (conductors + dielectrics) per MicroWalk cube
-constexpr int NMAX = 64;    // lattice size cap (layers per key)
+constexpr int NMAX = 128;   // lattice size cap (layers per key; face distances stay < 128,
+                            // the byte tricks of mw_step / mw_jump need that)
 constexpr int PMAX = 40;    // palettes up to PMAX classes keep the alpha table in shared memory
                             // (12.8 KB; larger ones divide, the same IEEE quotient)
 constexpr int kClassMax = 0x7FFF;  // distinct permittivities (15-bit class ids)
@@ -60,7 +61,7 @@ constexpr int kGridMinConductors = 24;  // conductor bins above this count
 // clipped boxes' faces cut [0, n) into segments; bm[a] holds one bit per
 // segment start.  mask[a][s] is the set of clipped boxes (bit q = box q)
 // spanning segment s, so the boxes containing a cell are the AND of its
-// three segment masks and its class is a bit scan.  n <= NMAX = 64 keeps
+// three segment masks and its class is a bit scan.  FDM jobs (n <= 32) keep
 // every bitmap in one word.
 constexpr int kAtMask = 0;    // [3][64] segment masks
 constexpr int kAtBm = 192;    // [3] segment-start bitmaps
@@ -743,7 +744,9 @@ __device__ Prof strat_probe(const DStruct& s, const double c[3], double h, int n
   }
   P.raxis = cov0 ? 0 : (cov1 ? 1 : 2);
   const int ax = P.raxis;
-  if (!many) {
+  // (the (class, slice-mask) pairs hold 64 slices: larger lattices classify
+  // slice centres one by one)
+  if (!many && n <= 64) {
     // pass 2: paint the hits' slice intervals in declaration order
     P.cls[0] = s.bg;
     P.msk[0] = n >= 64 ? ~0ull : (1ull << n) - 1;
@@ -3978,7 +3981,7 @@ int run_single(frw_ctx* ctx, const frw_walk_params* prm, int count, const double
   Engine& E = *engine_of(ctx);
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "transitions: no structure uploaded");
   if (!prm || prm->grid_n < 2 || prm->grid_n > NMAX)
-    return frw_fail(ctx, FRW_EINVAL, "transitions: grid_n must lie in [2, 64]");
+    return frw_fail(ctx, FRW_EINVAL, "transitions: grid_n must lie in [2, 128]");
   if (prm->mode == FRW_MODE_FDM && prm->grid_n > kFdmMaxN)
     return frw_fail(ctx, FRW_EINVAL, "transitions: FDM mode supports grid_n <= 32");
   if (count < 0 || (count > 0 && (!pts || !states || !out)))
@@ -4344,7 +4347,7 @@ int frw_sgf_put(frw_ctx* ctx, int n, int axis, const double* layers, double pitc
                 const double* probs, const double* cdf, const double* kernels) {
   if (!ctx || !layers || !probs || !cdf) return FRW_EINVAL;
   if (n < 1 || n > NMAX || axis < 0 || axis > 2)
-    return frw_fail(ctx, FRW_EINVAL, "sgf_put: need 1 <= n <= 64 and 0 <= axis <= 2");
+    return frw_fail(ctx, FRW_EINVAL, "sgf_put: need 1 <= n <= 128 and 0 <= axis <= 2");
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   Engine& E = *engine_of(ctx);
   SgfHost& T = E.sgf;
@@ -4433,7 +4436,7 @@ static int structure_transits(frw_ctx* ctx, int n, int count, const double* cube
   if (!ctx) return FRW_EINVAL;
   Engine& E = *engine_of(ctx);
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "transits: no structure uploaded");
-  if (n < 1 || n > NMAX) return frw_fail(ctx, FRW_EINVAL, "transits: n must lie in [1, 64]");
+  if (n < 1 || n > NMAX) return frw_fail(ctx, FRW_EINVAL, "transits: n must lie in [1, 128]");
   if (count < 0 || (count > 0 && (!cubes || (!states && rng != FRW_RNG_PHILOX) || !out)))
     return frw_fail(ctx, FRW_EINVAL, "transits: bad arguments");
   if (count == 0) return FRW_OK;
@@ -4573,7 +4576,7 @@ int frw_stratified_keys(frw_ctx* ctx, int n, int count, const double* cubes, int
   if (!ctx) return FRW_EINVAL;
   Engine& E = *engine_of(ctx);
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "strat keys: no structure uploaded");
-  if (n < 1 || n > NMAX) return frw_fail(ctx, FRW_EINVAL, "strat keys: n must lie in [1, 64]");
+  if (n < 1 || n > NMAX) return frw_fail(ctx, FRW_EINVAL, "strat keys: n must lie in [1, 128]");
   if (count < 0 || (count > 0 && (!cubes || !axis || !layers)))
     return frw_fail(ctx, FRW_EINVAL, "strat keys: bad arguments");
   if (count == 0) return FRW_OK;
@@ -4817,7 +4820,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   Engine& E = *engine_of(ctx);
   if (!E.have_structure) return frw_fail(ctx, FRW_EINVAL, "run_walks: no structure uploaded");
   if (prm->grid_n < 2 || prm->grid_n > NMAX)
-    return frw_fail(ctx, FRW_EINVAL, "run_walks: grid_n must lie in [2, 64]");
+    return frw_fail(ctx, FRW_EINVAL, "run_walks: grid_n must lie in [2, 128]");
   if (prm->mode == FRW_MODE_FDM && prm->grid_n > kFdmMaxN)
     return frw_fail(ctx, FRW_EINVAL, "run_walks: FDM mode supports grid_n <= 32");
   if (prm->mode < FRW_MODE_FDM || prm->mode > FRW_MODE_HYBRID_MWE)

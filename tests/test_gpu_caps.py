@@ -66,3 +66,41 @@ def test_dense_cubes_production_vs_reference_extract(ref, tmp_path, mode):
         se = math.hypot(tg["std_err_farads"], r["std_err"][k])
         z = abs(tg["capacitance_farads"] - r["value"][k]) / se
         assert z < 3.0, (k, tg, r["value"][k], z)
+
+
+@pytest.mark.parametrize("n,count", [(80, 160), (128, 48)])
+@pytest.mark.parametrize("mode", sorted(MODES))
+def test_large_lattice_bit_exact_vs_reference_engine(gpu_ctx, ref, tmp_path, mode, n, count):
+    """grid_n past 64 (the reference takes any lattice size,
+    engine.cpp:69-82): stratification probes classify slice centres one by
+    one, the stratified-SGF direct solve stages its DST basis in dynamic
+    shared memory, and the walks equal the reference Engine's bit for bit
+    on the device-solved tables (the same SGF1 file on both sides)."""
+    import paper_2507_09730_b200.frwcap as frwcap
+    from paper_2507_09730_b200.workloads import c3_structure
+    from tests.scenes import scene_from_doc
+    sc = scene_from_doc(c3_structure())
+    cache = frwcap.SgfCache()
+
+    def solve(nn, axis, layers):
+        probs = np.asarray(cache.get(nn, axis, list(layers)))
+        kern = np.asarray(cache.kernels(nn, axis, list(layers)))
+        return 1.0, probs, np.cumsum(probs), kern
+
+    upload_scene(gpu_ctx, sc)
+    gpu_ctx.sgf_clear()
+    p = walk_params(sc, grid_n=n, seed=41, rng=capi.RNG_SPLITMIX_PARITY, n_slots=4096,
+                    mode=MODES[mode])
+    tally, rec = gpu_ctx.run_walks(p, sc.master_slot(), 0, count, solve)
+    assert tally["misses"] > 0 and (rec["done"] == 1).all()
+    path = tmp_path / "dev.sgf"
+    cache.save(str(path))
+    slot, w, ab = ref.structure(sc).run_walks(0, count, threads=THREADS, cache_in=str(path),
+                                              grid_n=n, mode=mode, seed=41)
+    assert np.array_equal(rec["slot"], slot), np.nonzero(rec["slot"] != slot)[0][:10]
+    assert np.array_equal(rec["aborted"], ab)
+    assert np.array_equal(rec["weight"], w)
+    # production mode (Philox, lattice jumps up to radius 31) runs at this size
+    p = walk_params(sc, grid_n=n, seed=42, rng=capi.RNG_PHILOX, mode=MODES[mode])
+    tally, rec = gpu_ctx.run_walks(p, sc.master_slot(), 0, 4096, None)
+    assert (rec["done"] == 1).all() and tally["landed"].sum() == 4096
