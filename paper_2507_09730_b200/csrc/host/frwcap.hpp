@@ -490,8 +490,20 @@ CapacitanceResult extract(const Structure& s, const Config& cfg, int threads = 0
 
 // ---- surface Green's function of a materialised (unmasked) grid, on the device
 // (assemble_system + solve_sgf + expected_steps, sgf.cpp:57-299)
+// general grids solve on the device (Jacobi-PCG); masked grids, and grids
+// whose PCG does not converge, take the host direct solve below (sgf.cpp:162-211)
 DiscreteSGF solve_sgf(const DielectricGrid& g, bool with_kernels = true, int device = 0);
 double expected_steps(const DielectricGrid& g, int device = 0);
+
+// host direct solve of the transition-cube system (band L D L^T of s_ii,
+// direct.cpp): the SGF (surface then conductor panels) and E[steps]; n <= 32
+struct DirectSgf {
+  DiscreteSGF sgf;
+  double expected_steps = 0;
+};
+DirectSgf direct_sgf(const DielectricGrid& g, bool with_kernels = true);
+// oracle.hpp:14-19: the start node's row of a_ii^-1 a_ib by a dense LU
+std::vector<double> exact_absorption_row(const DielectricGrid& grid, int cap = 12);
 // FD system of a materialised grid (sgf.hpp:75-101).  The B200 build
 // assembles s_ii matrix-free on the device, so the system is the grid it is
 // built from; solve_sgf / expected_steps of it run the device solver.

@@ -512,8 +512,7 @@ ReferenceSolution reference_capacitance(const Structure& s, int resolution, int 
 }
 
 DiscreteSGF solve_sgf(const DielectricGrid& g, bool with_kernels, int device) {
-  if (g.has_mask())
-    throw std::invalid_argument("solve_sgf: masked grids are not supported on the device");
+  if (g.has_mask()) return direct_sgf(g, with_kernels).sgf;  // conductor voxels: host direct
   frw_ctx* ctx = Device::get(device).ctx();
   const size_t P = 6ull * g.n * g.n;
   DiscreteSGF out;
@@ -551,9 +550,13 @@ DiscreteSGF solve_sgf(const DielectricGrid& g, bool with_kernels, int device) {
     if (with_kernels && out.pitch != 1.0)
       for (double& k : ker) k /= out.pitch;
   } else {
-    throw_status(ctx, frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width,
-                                         out.probs.data(), with_kernels ? ker.data() : nullptr,
-                                         nullptr));
+    const int rc = frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width,
+                                      out.probs.data(), with_kernels ? ker.data() : nullptr,
+                                      nullptr);
+    // the PCG stalled: the direct factorisation, as the reference falls back
+    // to SimplicialLDLT (sgf.cpp:170-176)
+    if (rc == FRW_ESOLVE && g.n <= 32) return direct_sgf(g, with_kernels).sgf;
+    throw_status(ctx, rc);
   }
   out.cdf.resize(P);
   double run = 0;
@@ -626,12 +629,13 @@ DistributionReport compare_distribution(const std::vector<double>& exact,
 }
 
 double expected_steps(const DielectricGrid& g, int device) {
-  if (g.has_mask())
-    throw std::invalid_argument("expected_steps: masked grids are not supported on the device");
+  if (g.has_mask()) return direct_sgf(g, false).expected_steps;
   frw_ctx* ctx = Device::get(device).ctx();
   double st = 0;
-  throw_status(ctx, frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width, nullptr,
-                                       nullptr, &st));
+  const int rc = frw_grid_sgf_solve(ctx, g.n, 1, g.eps.data(), g.cube.half_width, nullptr,
+                                    nullptr, &st);
+  if (rc == FRW_ESOLVE && g.n <= 32) return direct_sgf(g, false).expected_steps;
+  throw_status(ctx, rc);
   return st;
 }
 

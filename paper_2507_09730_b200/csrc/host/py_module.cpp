@@ -604,6 +604,50 @@ PYBIND11_MODULE(_core, m) {
       py::arg("structure_json"), py::arg("center"), py::arg("half_width"), py::arg("n"),
       py::arg("allow_conductors") = false);
 
+  // host direct solves (direct.cpp): the band L D L^T fallback of solve_sgf
+  // and oracle.hpp's dense exact_absorption_row -- B200 extras for tests
+  auto grid_of = [](py::array_t<double, py::array::c_style | py::array::forcecast> eps,
+                    double hw, py::object mask) {
+    DielectricGrid g;
+    g.n = static_cast<int>(std::lround(std::cbrt(static_cast<double>(eps.size()))));
+    g.cube = {{0, 0, 0}, hw > 0 ? hw : g.n / 2.0};
+    g.eps.assign(eps.data(), eps.data() + eps.size());
+    if (!mask.is_none()) {
+      auto mk = py::cast<py::array_t<int32_t, py::array::c_style | py::array::forcecast>>(mask);
+      g.conductor_mask.assign(mk.data(), mk.data() + mk.size());
+    }
+    return g;
+  };
+  m.def(
+      "direct_sgf",
+      [grid_of](py::array_t<double, py::array::c_style | py::array::forcecast> eps, double hw,
+                py::object mask) {
+        const DirectSgf d = direct_sgf(grid_of(eps, hw, mask), true);
+        const size_t P = d.sgf.probs.size();
+        py::array_t<double> probs(P), ker({static_cast<size_t>(3), P});
+        std::copy(d.sgf.probs.begin(), d.sgf.probs.end(), probs.mutable_data());
+        for (int a = 0; a < 3; ++a)
+          std::copy(d.sgf.grad_kernels[a].begin(), d.sgf.grad_kernels[a].end(),
+                    ker.mutable_data() + a * P);
+        py::dict o;
+        o["probs"] = probs;
+        o["kernels"] = ker;
+        o["pitch"] = d.sgf.pitch;
+        o["expected_steps"] = d.expected_steps;
+        return o;
+      },
+      py::arg("eps"), py::arg("half_width") = 0.0, py::arg("mask") = py::none());
+  m.def(
+      "exact_absorption_row",
+      [grid_of](py::array_t<double, py::array::c_style | py::array::forcecast> eps,
+                py::object mask, int cap) {
+        const std::vector<double> r = exact_absorption_row(grid_of(eps, 0.0, mask), cap);
+        py::array_t<double> out(r.size());
+        std::copy(r.begin(), r.end(), out.mutable_data());
+        return out;
+      },
+      py::arg("eps"), py::arg("mask") = py::none(), py::arg("cap") = 12);
+
   // StratifiedSgfCache (sgf_cache.hpp:47-101) -- B200 extra for tests and tools
   py::class_<StratifiedSgfCache>(m, "SgfCache")
       .def(py::init<size_t>(), py::arg("capacity") = 0)

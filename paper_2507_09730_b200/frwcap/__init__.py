@@ -20,6 +20,7 @@ from .._core import sgf_cache_stats  # noqa: F401
 from .._core import build_grid, neighbor_weights, transits_grid, transits_structure  # noqa: F401
 from .._core import transitions_json, walks_by_transitions  # noqa: F401
 from .._core import SgfCache  # noqa: F401
+from .._core import direct_sgf, exact_absorption_row  # noqa: F401  (host direct solves)
 
 __all__ = [
     "analytic_plate_capacitance",

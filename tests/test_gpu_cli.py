@@ -21,6 +21,8 @@ def test_validate_sgf_passes():
     assert rep["results"]["uniform_face_symmetry"]["max_abs_err"] <= 1e-9
     for c in rep["results"]["checks"]:
         assert c["sgf_properties_ok"] and abs(c["steps_z"]) <= 4.0
+        # n <= 6: the dense-LU cross-check of the device PCG (cli.cpp:271-279)
+        assert c["dense_max_abs_diff"] <= 1e-8
 
 
 def test_bench_scaling_reports_slopes():
