@@ -78,6 +78,7 @@ void frw_ctx_destroy(frw_ctx* ctx) {
   cudaFree(g.d_map);  // also releases d_rec (same allocation)
   cudaFree(g.d_full);
   cudaFree(g.d_exit);
+  cudaFree(g.d_dc);
   cudaFree(g.d_mask);
   cudaFree(ctx->d_ctr);
   cudaFree(ctx->d_err);

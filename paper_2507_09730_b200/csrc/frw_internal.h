@@ -29,6 +29,12 @@ struct GridTable {
   size_t map_bytes = 0, rec_bytes = 0;  // padded to 16 B
   // allocation capacities (re-uploads of a same-sized grid reuse them)
   size_t blob_cap = 0, full_cap = 0, mask_cap = 0, exit_cap = 0;
+  // on-device compile (mw_grid.cu, compile_grid_device): eps staging, the
+  // palette / stencil hash tables and counters, one allocation
+  char* d_dc = nullptr;
+  size_t dc_cap = 0;
+  int exit_n = 0;  // exit_info cached for this n (unmasked grids)
+  bool host_compiled = false;  // FRW_GRID_HOST_COMPILE / fallback: the last upload compiled on the host
 };
 
 }  // namespace frw

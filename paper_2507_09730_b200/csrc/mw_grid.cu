@@ -80,8 +80,8 @@ struct Key {
 // smallest x in [0, 2^53] with fl(x * sum) >= acc * 2^53 (2^53 if none);
 // fl(x*sum) is monotone in x, so "x >= X" <=> "not (target < acc)".  The
 // quotient lands within a few units of X; the two walks settle it exactly.
-uint64_t threshold_of(double acc, double sum) {
-  const double target = std::ldexp(acc, 53);
+__host__ __device__ uint64_t threshold_of(double acc, double sum) {
+  const double target = acc * 9007199254740992.0;  // ldexp(acc, 53): exact
   constexpr uint64_t kTop = 1ull << 53;
   const auto ok = [&](uint64_t x) { return static_cast<double>(x) * sum >= target; };
   const double g = target / sum;
@@ -857,6 +857,284 @@ int launch(frw_ctx* ctx, const frw_mw_params* p, const frw_mw_out* o, unsigned l
   return FRW_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// On-device compile of the cube (the e2e path: only the permittivities cross
+// PCIe).  The same records as compile_grid -- alphas en / (en + ev), their
+// in-order partial sums and the exact thresholds of threshold_of, all plain
+// IEEE f64 -- numbered in whatever order the hash inserts land (the record
+// numbering is invisible to the walk: a node's record content is what it
+// steps with, and the exact thresholds follow the record).  A stencil key is
+// the node's palette id and its six neighbour codes at 9 bits each, so
+// palettes of up to kDcPal permittivities compile here; larger ones (and
+// FRW_GRID_HOST_COMPILE=1) take compile_grid.
+constexpr uint32_t kDcPal = 510;           // palette ids; 510 = conductor, 511 = surface
+constexpr uint32_t kDcCond = 510, kDcSurf = 511;
+
+struct DcBufs {
+  double* eps;          // [n^3] staged permittivities
+  int32_t* mask;        // [n^3] or null
+  uint64_t* pal_key;    // [pcap] eps bits (0: empty)
+  uint32_t* pal_val;    // [pcap]
+  double* pal_eps;      // [kDcPal]
+  uint64_t* rec_key;    // [rcap] stencil keys (0: empty)
+  uint32_t* rec_val;    // [rcap]
+  uint64_t* rec_of;     // [kRecMax] key of record r
+  uint32_t* node_pal;   // [n^3]
+  uint32_t* cnt;        // [0] palette size, [1] records, [2] error
+  uint32_t pmask, rmask;
+};
+constexpr uint32_t kRecMax = 65535;
+
+__device__ __forceinline__ uint32_t dc_hash(uint64_t k) { return static_cast<uint32_t>(sm64_mix(k)); }
+
+__global__ void k_dc_palette(int nodes, DcBufs B) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += gridDim.x * blockDim.x) {
+    const double e = B.eps[v];
+    if (!(e > 0) || !isfinite(e)) {
+      atomicMax(&B.cnt[2], 1u);
+      continue;
+    }
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(e));
+    for (uint32_t h = dc_hash(bits) & B.pmask;; h = (h + 1) & B.pmask) {
+      const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(B.pal_key + h), 0ull,
+                                                static_cast<unsigned long long>(bits));
+      if (prev == 0) {
+        const uint32_t id = atomicAdd(&B.cnt[0], 1u);
+        B.pal_val[h] = id;
+        if (id < kDcPal) B.pal_eps[id] = e;
+        break;
+      }
+      if (prev == bits) break;
+    }
+  }
+}
+
+__global__ void k_dc_node_pal(int nodes, DcBufs B) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += gridDim.x * blockDim.x) {
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(B.eps[v]));
+    uint32_t h = dc_hash(bits) & B.pmask;
+    while (B.pal_key[h] != bits) h = (h + 1) & B.pmask;
+    B.node_pal[v] = B.pal_val[h];
+  }
+}
+
+// the stencil key of lattice node (i, j, k): its palette id and the six
+// neighbour codes (surface / conductor / palette id), 9 bits each; bit 63 set
+__device__ __forceinline__ uint64_t dc_key(const DcBufs& B, int n, int i, int j, int k) {
+  const int v = (k * n + j) * n + i;
+  uint64_t key = (1ull << 63) | B.node_pal[v];
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    int nb[3] = {i, j, k};
+    nb[d >> 1] += (d & 1) ? 1 : -1;
+    uint32_t code;
+    if (nb[d >> 1] < 0 || nb[d >> 1] >= n) {
+      code = kDcSurf;
+    } else {
+      const int nv = (nb[2] * n + nb[1]) * n + nb[0];
+      code = (B.mask && B.mask[nv] >= 0) ? kDcCond : B.node_pal[nv];
+    }
+    key |= static_cast<uint64_t>(code) << (9 * (d + 1));
+  }
+  return key;
+}
+
+__global__ void k_dc_records(int n, DcBufs B) {
+  const int nodes = n * n * n;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nodes; v += gridDim.x * blockDim.x) {
+    if (B.mask && B.mask[v] >= 0) continue;  // conductor voxel: the exit record
+    const uint64_t key = dc_key(B, n, v % n, (v / n) % n, v / (n * n));
+    for (uint32_t h = dc_hash(key) & B.rmask;; h = (h + 1) & B.rmask) {
+      const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(B.rec_key + h), 0ull,
+                                                static_cast<unsigned long long>(key));
+      if (prev == 0) {
+        const uint32_t r = atomicAdd(&B.cnt[1], 1u);
+        B.rec_val[h] = r;
+        if (r < kRecMax) B.rec_of[r] = key;
+        break;
+      }
+      if (prev == key) break;
+    }
+  }
+}
+
+// padded map: record id of each lattice node, the exit record (id R) on the
+// halo and on conductor voxels
+__global__ void k_dc_map(int n, DcBufs B, uint16_t* map) {
+  const int np = n + 2, total = np * np * np;
+  const uint32_t R = B.cnt[1];
+  for (int pv = blockIdx.x * blockDim.x + threadIdx.x; pv < total; pv += gridDim.x * blockDim.x) {
+    const int i = pv % np - 1, j = (pv / np) % np - 1, k = pv / (np * np) - 1;
+    uint32_t r = R;
+    if (i >= 0 && i < n && j >= 0 && j < n && k >= 0 && k < n &&
+        !(B.mask && B.mask[(k * n + j) * n + i] >= 0)) {
+      const uint64_t key = dc_key(B, n, i, j, k);
+      uint32_t h = dc_hash(key) & B.rmask;
+      while (B.rec_key[h] != key) h = (h + 1) & B.rmask;
+      r = B.rec_val[h];
+    }
+    map[pv] = static_cast<uint16_t>(r);
+  }
+}
+
+// record contents (microwalk.cpp:91-109 alphas, exact thresholds), then the exit record
+__global__ void k_dc_contents(DcBufs B, uint64_t* rec, uint64_t* full) {
+  const uint32_t R = B.cnt[1];
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= R; r += gridDim.x * blockDim.x) {
+    if (r == R) {
+      rec[R] = kExitRec;
+      for (int d = 0; d < 5; ++d) full[5ull * R + d] = 1ull << 53;
+      continue;
+    }
+    const uint64_t key = B.rec_of[r];
+    const double ev = B.pal_eps[key & 0x1FF];
+    double acc[6], sum = 0;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+      const uint32_t code = static_cast<uint32_t>(key >> (9 * (d + 1))) & 0x1FF;
+      double a = 1.0;
+      if (code < kDcCond) {
+        const double en = B.pal_eps[code];
+        a = en / (en + ev);
+      }
+      sum += a;
+      acc[d] = sum;
+    }
+    uint64_t packed = 0;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+      const uint64_t X = threshold_of(acc[d], sum);
+      full[5ull * r + d] = X;
+      const uint64_t t11 = X >> 42 < static_cast<uint64_t>(kTop) ? X >> 42 : kTop;
+      packed |= (kTop - t11) << (kLane * d);
+    }
+    rec[r] = packed;
+  }
+}
+
+// exit_info_of on the device (see there)
+__global__ void k_dc_exit(int n, const int32_t* mask, int32_t* info) {
+  const int np = n + 2, total = np * np * np;
+  for (int pv = blockIdx.x * blockDim.x + threadIdx.x; pv < total; pv += gridDim.x * blockDim.x) {
+    const int h[3] = {pv % np, (pv / np) % np, pv / (np * np)};
+    int out = 0, ax = -1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (h[a] == 0 || h[a] == n + 1) ++out, ax = a;
+    int r = -1;
+    if (out == 0) {
+      if (mask) {
+        const int m = mask[((h[2] - 1) * n + (h[1] - 1)) * n + (h[0] - 1)];
+        if (m >= 0) r = -2 - m;
+      }
+    } else if (out == 1) {
+      const int dir = 2 * ax + (h[ax] == n + 1 ? 1 : 0);
+      int c[3] = {h[0] - 1, h[1] - 1, h[2] - 1};
+      c[ax] = h[ax] == 0 ? 0 : n - 1;
+      const int uu = ax == 0 ? c[1] : c[0];
+      const int vv = ax == 2 ? c[1] : c[2];
+      r = (dir * n + vv) * n + uu;
+    }
+    info[pv] = r;
+  }
+}
+
+
+inline size_t pow2_at_least(size_t v) {
+  size_t c = 1024;
+  while (c < v) c <<= 1;
+  return c;
+}
+
+// The device compile driver (see k_dc_*): stages eps (and the mask), builds
+// palette and stencil tables, then map, records, exact thresholds and the
+// exit table straight into the GridTable buffers.  Returns 1 when the grid
+// needs the host compile (palette past kDcPal), FRW_OK, or an error.
+int compile_grid_device(frw_ctx* ctx, int n, const double* eps, const int32_t* mask) {
+  GridTable& G = ctx->grid;
+  const size_t nodes = static_cast<size_t>(n) * n * n;
+  const int np = n + 2;
+  const size_t pnodes = static_cast<size_t>(np) * np * np;
+  const size_t pcap = pow2_at_least(2 * nodes), rcap = pow2_at_least(2 * std::min<size_t>(nodes, kRecMax));
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t o_eps = 0, o_mask = o_eps + al(8 * nodes), o_pk = o_mask + (mask ? al(4 * nodes) : 0),
+               o_pv = o_pk + al(8 * pcap), o_pe = o_pv + al(4 * pcap), o_rk = o_pe + al(8 * 512),
+               o_rv = o_rk + al(8 * rcap), o_ro = o_rv + al(4 * rcap), o_np = o_ro + al(8 * kRecMax),
+               o_cnt = o_np + al(4 * nodes), need = o_cnt + 256;
+  if (G.dc_cap < need) {
+    cudaFree(G.d_dc);
+    G.d_dc = nullptr;
+    G.dc_cap = 0;
+    FRW_CUDA(ctx, cudaMalloc(&G.d_dc, need));
+    G.dc_cap = need;
+  }
+  char* b = G.d_dc;
+  DcBufs B{reinterpret_cast<double*>(b + o_eps),
+           mask ? reinterpret_cast<int32_t*>(b + o_mask) : nullptr,
+           reinterpret_cast<uint64_t*>(b + o_pk), reinterpret_cast<uint32_t*>(b + o_pv),
+           reinterpret_cast<double*>(b + o_pe), reinterpret_cast<uint64_t*>(b + o_rk),
+           reinterpret_cast<uint32_t*>(b + o_rv), reinterpret_cast<uint64_t*>(b + o_ro),
+           reinterpret_cast<uint32_t*>(b + o_np), reinterpret_cast<uint32_t*>(b + o_cnt),
+           static_cast<uint32_t>(pcap - 1), static_cast<uint32_t>(rcap - 1)};
+  cudaStream_t st = ctx->stream;
+  FRW_CUDA(ctx, cudaMemcpyAsync(B.eps, eps, 8 * nodes, cudaMemcpyHostToDevice, st));
+  if (mask) FRW_CUDA(ctx, cudaMemcpyAsync(B.mask, mask, 4 * nodes, cudaMemcpyHostToDevice, st));
+  FRW_CUDA(ctx, cudaMemsetAsync(B.pal_key, 0, 8 * pcap, st));
+  FRW_CUDA(ctx, cudaMemsetAsync(B.rec_key, 0, 8 * rcap, st));
+  FRW_CUDA(ctx, cudaMemsetAsync(B.cnt, 0, 16, st));
+  const int grid = ctx->sm_count * 4;
+  k_dc_palette<<<grid, 256, 0, st>>>(static_cast<int>(nodes), B);
+  k_dc_node_pal<<<grid, 256, 0, st>>>(static_cast<int>(nodes), B);
+  k_dc_records<<<grid, 256, 0, st>>>(n, B);
+  uint32_t cnt[3] = {0, 0, 0};
+  FRW_CUDA(ctx, cudaMemcpyAsync(cnt, B.cnt, 12, cudaMemcpyDeviceToHost, st));
+  FRW_CUDA(ctx, cudaStreamSynchronize(st));
+  if (cnt[2]) return frw_fail(ctx, FRW_EINVAL, "grid permittivities must be finite and > 0");
+  if (cnt[0] > kDcPal) return 1;  // palette past the 9-bit key fields: host compile
+  if (cnt[1] >= kRecMax)
+    return frw_fail(ctx, FRW_EINVAL, "more than 65535 distinct stencil records");
+  const uint32_t R = cnt[1];
+  G.n = n;
+  G.records = static_cast<int>(R);
+  G.map_bytes = (pnodes * 2 + 15) / 16 * 16;
+  G.rec_bytes = ((R + 1) * 8 + 15) / 16 * 16;
+  const size_t blob = G.map_bytes + G.rec_bytes, full = (R + 1) * 5 * 8;
+  if (G.blob_cap < blob) {
+    cudaFree(G.d_map);
+    G.d_map = nullptr;
+    G.blob_cap = 0;
+    char* p = nullptr;
+    FRW_CUDA(ctx, cudaMalloc(&p, blob));
+    G.d_map = reinterpret_cast<uint16_t*>(p);
+    G.blob_cap = blob;
+  }
+  G.d_rec = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(G.d_map) + G.map_bytes);
+  if (G.full_cap < full) {
+    cudaFree(G.d_full);
+    G.d_full = nullptr;
+    G.full_cap = 0;
+    FRW_CUDA(ctx, cudaMalloc(&G.d_full, full));
+    G.full_cap = full;
+  }
+  k_dc_map<<<grid, 256, 0, st>>>(n, B, G.d_map);
+  k_dc_contents<<<(R + 256) / 256, 256, 0, st>>>(B, G.d_rec, G.d_full);
+  if (mask || G.exit_n != n) {  // the exit table of an unmasked lattice depends on n only
+    if (G.exit_cap < 4 * pnodes) {
+      cudaFree(G.d_exit);
+      G.d_exit = nullptr;
+      G.exit_cap = 0;
+      FRW_CUDA(ctx, cudaMalloc(&G.d_exit, 4 * pnodes));
+      G.exit_cap = 4 * pnodes;
+    }
+    k_dc_exit<<<grid, 256, 0, st>>>(n, B.mask, G.d_exit);
+    G.exit_n = mask ? 0 : n;
+  }
+  FRW_CUDA(ctx, cudaGetLastError());
+  G.h2d_bytes = 8 * nodes + (mask ? 4 * nodes : 0);
+  return FRW_OK;
+}
+
 }  // namespace
 }  // namespace frw
 
@@ -870,12 +1148,8 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   if (n < 1 || n > 253 || !eps)
     return frw_fail(ctx, FRW_EINVAL, "upload_grid: need 1 <= n <= 253 and eps");
   if (!(half_width > 0)) return frw_fail(ctx, FRW_EINVAL, "upload_grid: half_width <= 0");
-  Compiled cg;
-  if (int rc = compile_grid(ctx, n, eps, mask, cg)) return rc;
   FRW_CUDA(ctx, cudaSetDevice(ctx->device));
   GridTable& G = ctx->grid;
-  G.n = n;
-  G.records = static_cast<int>(cg.rec.size()) - 1;  // step records; [R] is the exit record
   const int c = (n - 1) / 2;  // start_node, sgf.hpp:58-61
   const int np = n + 2;
   G.start_idx = ((c + 1) * np + (c + 1)) * np + (c + 1);  // padded
@@ -884,6 +1158,39 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   G.center[1] = cy;
   G.center[2] = cz;
   G.half_width = half_width;
+  G.has_mask = mask != nullptr;
+  if (mask) {  // the walk kernels read the mask of a masked lattice
+    const size_t bytes = static_cast<size_t>(n) * n * n * 4;
+    if (G.mask_cap < bytes) {
+      cudaFree(G.d_mask);
+      G.d_mask = nullptr;
+      G.mask_cap = 0;
+      FRW_CUDA(ctx, cudaMalloc(&G.d_mask, bytes));
+      G.mask_cap = bytes;
+    }
+    FRW_CUDA(ctx, cudaMemcpyAsync(G.d_mask, mask, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  // compile on the device (only eps crosses PCIe); FRW_GRID_HOST_COMPILE=1
+  // or a palette past 510 permittivities compiles on the host
+  static const bool host_only = [] {
+    const char* e = std::getenv("FRW_GRID_HOST_COMPILE");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!host_only) {
+    const int rc = compile_grid_device(ctx, n, eps, mask);
+    if (rc == FRW_OK) {
+      G.host_compiled = false;
+      FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      return FRW_OK;
+    }
+    if (rc != 1) return rc;
+  }
+  G.host_compiled = true;
+  G.exit_n = 0;
+  Compiled cg;
+  if (int rc = compile_grid(ctx, n, eps, mask, cg)) return rc;
+  G.n = n;
+  G.records = static_cast<int>(cg.rec.size()) - 1;  // step records; [R] is the exit record
   G.map_bytes = (cg.map.size() * 2 + 15) / 16 * 16;
   G.rec_bytes = (cg.rec.size() * 8 + 15) / 16 * 16;
   // one allocation: map then packed records, so one bulk stage covers both;
@@ -922,20 +1229,8 @@ int frw_upload_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
   }
   FRW_CUDA(ctx, cudaMemcpyAsync(G.d_exit, cg.exit_info.data(), ebytes, cudaMemcpyHostToDevice,
                                 ctx->stream));
-  G.h2d_bytes = cg.map.size() * 2 + cg.rec.size() * 8 + full + ebytes;
-  G.has_mask = mask != nullptr;
-  if (mask) {
-    const size_t bytes = static_cast<size_t>(n) * n * n * 4;
-    if (G.mask_cap < bytes) {
-      cudaFree(G.d_mask);
-      G.d_mask = nullptr;
-      G.mask_cap = 0;
-      FRW_CUDA(ctx, cudaMalloc(&G.d_mask, bytes));
-      G.mask_cap = bytes;
-    }
-    FRW_CUDA(ctx, cudaMemcpyAsync(G.d_mask, mask, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    G.h2d_bytes += bytes;
-  }
+  G.h2d_bytes = cg.map.size() * 2 + cg.rec.size() * 8 + full + ebytes +
+                (mask ? static_cast<size_t>(n) * n * n * 4 : 0);
   FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FRW_OK;
 }

@@ -3960,6 +3960,7 @@ int ensure_slots(frw_ctx* ctx, Engine& E, int S) {
     free_slots(E);
     return frw_fail(ctx, FRW_ENOMEM, "walk slots: device allocation failed");
   }
+  cudaMemset(W.state, 0, S);  // fresh slots are free (never a stale carried hop)
   E.S = S;
   return FRW_OK;
 }
@@ -4482,7 +4483,9 @@ static int structure_transits(frw_ctx* ctx, int n, int count, const double* cube
                         ctx->stream) != cudaSuccess ||
         (states && cudaMemcpyAsync(d_states, states, 8 * size_t(count), cudaMemcpyHostToDevice,
                                    ctx->stream) != cudaSuccess) ||
-        cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), ctx->stream) != cudaSuccess) {
+        cudaMemsetAsync(E.d_cnt, 0, sizeof(DCounters), ctx->stream) != cudaSuccess ||
+        // job t arms from slot t: no stale S_MW_CARRY state may resume it
+        cudaMemsetAsync(E.W.state, 0, static_cast<size_t>(count), ctx->stream) != cudaSuccess) {
       status = frw_fail(ctx, FRW_ECUDA, "transits: copy failed");
       break;
     }
