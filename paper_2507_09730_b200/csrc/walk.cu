@@ -1621,7 +1621,20 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     // a single-class cube (2/3 of the cached hops on C3/C5) finds its entry
     // through the per-class uniform index; otherwise (or when that key is
     // not in the table yet) the full key is hashed and compared
-    auto layer = [&](int t) { return prof_layer(s, pr, c, h, n, t); };
+    // the rounded layer values of the profile's (class, slice-mask) pairs
+    // in registers: a layer is four mask tests, no palette load per slice
+    double lv[kProfCls];
+#pragma unroll
+    for (int q = 0; q < kProfCls; ++q) lv[q] = pr.msk[q] ? __ldg(s.rpal + pr.cls[q]) : 0.0;
+    const bool fast = pr.ucls < 0 && !pr.ovf;
+    auto layer = [&](int t) {
+      if (!fast) return prof_layer(s, pr, c, h, n, t);
+      double x = 0.0;
+#pragma unroll
+      for (int q = 0; q < kProfCls; ++q)
+        if ((pr.msk[q] >> t) & 1) x = lv[q];
+      return x;
+    };
     PH_T0(ph2);
     int e = pr.ucls >= 0 ? __ldg(T.uentry + pr.ucls) : -1;
     if (e < 0) e = sgf_find(T, n, axis, layer);
