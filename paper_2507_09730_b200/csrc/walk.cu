@@ -325,6 +325,9 @@ __device__ __forceinline__ double cheb_wall(const double* b, const double p[3]) 
   return d;
 }
 // Box::contains (geometry.hpp:37-40); `b` may live in any address space
+// (short-circuit on purpose: the long scans of permittivity_at -- dense hop
+// grids classify every voxel centre -- mostly stop at the first compare; a
+// branch-free six-load version cost C5 a third of its large-call throughput)
 __device__ __forceinline__ bool box_contains(const double* b, const double p[3]) {
   return p[0] >= b[0] && p[0] <= b[3] && p[1] >= b[1] && p[1] <= b[4] && p[2] >= b[2] &&
          p[2] <= b[5];
@@ -707,9 +710,9 @@ __device__ Prof strat_probe(const DStruct& s, const double c[3], double h, int n
     double bb[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) bb[q] = __ldg(b + q);
-    // Box::intersects_open (geometry.hpp:49-52)
-    if (!(bb[0] < cb[3] && cb[0] < bb[3] && bb[1] < cb[4] && cb[1] < bb[4] && bb[2] < cb[5] &&
-          cb[2] < bb[5]))
+    // Box::intersects_open (geometry.hpp:49-52), without short-circuit branches
+    if (!((bb[0] < cb[3]) & (cb[0] < bb[3]) & (bb[1] < cb[4]) & (cb[1] < bb[4]) &
+          (bb[2] < cb[5]) & (cb[2] < bb[5])))
       return true;
     // covers the cross-section perpendicular to axis a (geometry.cpp:372-380)
     const bool fx = bb[0] <= cb[0] && bb[3] >= cb[3], fy = bb[1] <= cb[1] && bb[4] >= cb[4],
@@ -1170,9 +1173,14 @@ __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const
       const int q = nca < 0 ? i : cand[i];
       const double* bx = base + 6 * q;
       // voxel centres lie inside the closed cube: a box that misses the
-      // cube cannot contain one (cheap reject before the exact clip)
-      if (__ldg(bx + 0) > cb[3] || __ldg(bx + 3) < cb[0] || __ldg(bx + 1) > cb[4] ||
-          __ldg(bx + 4) < cb[1] || __ldg(bx + 2) > cb[5] || __ldg(bx + 5) < cb[2])
+      // cube cannot contain one (cheap reject before the exact clip).  All
+      // six compares, no short-circuit: lanes scanning different boxes stay
+      // on one path (the || chain split warps six ways, 2.5 active lanes on C4)
+      double b6[6];
+#pragma unroll
+      for (int e = 0; e < 6; ++e) b6[e] = __ldg(bx + e);
+      if ((b6[0] > cb[3]) | (b6[3] < cb[0]) | (b6[1] > cb[4]) | (b6[4] < cb[1]) |
+          (b6[2] > cb[5]) | (b6[5] < cb[2]))
         continue;
       uint64_t pk = 0;  // pack_box layout: lo bytes 0-2, hi bytes 3-5
       bool empty = false;
@@ -1284,8 +1292,8 @@ __device__ int first_transition(const DStruct& s, const DSgf& T, const DParams& 
     for (int i = 0, ni = dcand < 0 ? s.nd : dcand; i < ni; ++i) {
       const int d = dcand < 0 ? i : cand[i];
       const double* b = s.dbox + 6 * d;
-      if (__ldg(b) > c[0] + h || __ldg(b + 3) < c[0] - h || __ldg(b + 1) > c[1] + h ||
-          __ldg(b + 4) < c[1] - h || __ldg(b + 2) > c[2] + h || __ldg(b + 5) < c[2] - h)
+      if ((__ldg(b) > c[0] + h) | (__ldg(b + 3) < c[0] - h) | (__ldg(b + 1) > c[1] + h) |
+          (__ldg(b + 4) < c[1] - h) | (__ldg(b + 2) > c[2] + h) | (__ldg(b + 5) < c[2] - h))
         continue;
       int lo[3], hi[3];
       bool empty = false;
