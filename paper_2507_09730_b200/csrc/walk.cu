@@ -1147,8 +1147,10 @@ __device__ void build_atlas(const uint64_t* boxes, int K, int n, uint64_t* A, ui
 // clipped too.  Returns 1 ok, 0 when the start voxel is conductor
 // (EngulfedStart), 3 when more than KMAX boxes reach into the cube (only
 // the cube is stored: the hop runs on a dense grid, k_mw_dense).
+template <bool ATLAS_OK = true>
 __device__ int compile_mw_job(const DStruct& s, const DSlots& W, int slot, const double c[3],
-                              double h, int n, bool conductors, bool atlas, DCounters* C) {
+                              double h, int n, bool conductors, bool atlas_arg, DCounters* C) {
+  const bool atlas = ATLAS_OK && atlas_arg;  // (instantiated without the atlas in k_tail)
   FRW_DCHECK(C, slot >= 0 && slot < W.J);
   uint64_t* boxes = W.boxes + static_cast<size_t>(slot) * KMAX;
   uint64_t* A = W.atlas + static_cast<size_t>(slot) * kAtlasWords;
@@ -1522,6 +1524,7 @@ __device__ __forceinline__ void adv_load(const DSlots& W, int slot, AdvLane& L) 
 // lattice swallows the start voxel (EngulfedStart).  Compiled into job entry
 // jslot.  Returns 2 (job ready, its kind in W.mwkind[jslot]) or 1 (the walk
 // left the stage: queued for a dense hop, or dropped on an error).
+template <bool ATLAS = true>  // false: never an FDM job (the atlas code is not instantiated)
 __device__ __forceinline__ int hop_compile(const DStruct& s, const DParams& P, const DSlots& W,
                                            DCounters* C, const DMiss& M, int slot, int jslot,
                                            const double p[3], double fh) {
@@ -1548,7 +1551,7 @@ __device__ __forceinline__ int hop_compile(const DStruct& s, const DParams& P, c
   int rc = -1;
 #pragma unroll 1
   for (;;) {
-    rc = compile_mw_job(s, W, jslot, jc, jh, n, expanded, kind == 2, C);
+    rc = compile_mw_job<ATLAS>(s, W, jslot, jc, jh, n, expanded, kind == 2, C);
     if (rc != 0 || !expanded) break;
     expanded = false;
     jc[0] = c[0];
@@ -1590,7 +1593,7 @@ __device__ __forceinline__ int hop_compile(const DStruct& s, const DParams& P, c
 // compiled here into the lane's job entry.
 // QUEUE: the compile queue is always given (k_advance), so the inline job
 // compiler is not instantiated there
-template <bool QUEUE = false>
+template <bool QUEUE = false, bool ATLAS = true>
 __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, const DSlots& W,
                             WalkRec* recs, DCounters* C, const DMiss& M, int* cq, AdvLane& L) {
   const int slot = L.slot;
@@ -1691,7 +1694,7 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     return 2;
   }
   PH_T0(ph3);
-  const int rc = hop_compile(s, P, W, C, M, slot, L.jslot, L.p, fh);
+  const int rc = hop_compile<ATLAS>(s, P, W, C, M, slot, L.jslot, L.p, fh);
   PH_ADD(3, ph3);
   return rc;
 }
@@ -2593,10 +2596,10 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     if (live && !in_mw) {
       // up to FRW_TAIL_CHAIN transitions back to back while they are cached
       // hops (each would otherwise wait out a whole MicroWalk stretch)
-      int r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
+      int r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
 #pragma unroll 1
       for (int k = 1; k < FRW_TAIL_CHAIN && r == 0; ++k)
-        r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
+        r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
       if (r == 2) {
         in_mw = true;
         mw_arm(W, A.slot, A.jslot, n, L, frw_dsm);
@@ -2738,7 +2741,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         continue;
       }
       if (have) {
-        const int r = advance_once(s, T, P, W, recs, C, M, nullptr, A);
+        const int r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
         if (r == 2) {
           ring_push(ring_m, &C->fmt, mask, A.slot);
           have = false;
