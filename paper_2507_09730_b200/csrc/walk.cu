@@ -350,10 +350,16 @@ __device__ int grid_conductor_within(const DStruct& s, const double p[3], double
     b1[a] = bin_of(g, a, p[a] + tol);
   }
   int best = 0x7FFFFFFF;
+  // (rolled loops: one copy of the distance test -- the walk kernels are
+  // instruction-fetch bound)
+#pragma unroll 1
   for (int z = b0[2]; z <= b1[2]; ++z)
+#pragma unroll 1
     for (int y = b0[1]; y <= b1[1]; ++y)
+#pragma unroll 1
       for (int x = b0[0]; x <= b1[0]; ++x) {
         const int bin = (z * g.dims[1] + y) * g.dims[0] + x;
+#pragma unroll 1
         for (int q = __ldg(g.cstart + bin), e = __ldg(g.cstart + bin + 1); q < e; ++q) {
           const int c = __ldg(g.citem + q);
           if (c < best && cheb_to(s.cbox + 6 * c, p) <= tol) best = c;
@@ -371,6 +377,7 @@ __device__ double grid_min_cheb(const DStruct& s, const double p[3], double r, b
   const DGrid& g = s.g;
   const int bin = (bin_of(g, 2, p[2]) * g.dims[1] + bin_of(g, 1, p[1])) * g.dims[0] +
                   bin_of(g, 0, p[0]);
+#pragma unroll 1
   for (int q = __ldg(g.nstart + bin), e = __ldg(g.nstart + bin + 1); q < e; ++q) {
     const double d = cheb_to(s.cbox + 6 * __ldg(g.nitem + q), p);
     if (d <= 0) *inside = true;
@@ -469,6 +476,7 @@ __device__ int hop_scan(const DStruct& s, const double p[3], double snap, double
     return -3;
   }
   double r = wall;
+#pragma unroll 1
   for (int c = 0; c < s.nc; ++c) {
     const double d = cheb_to(s.cbox + 6 * c, p);
     if (d <= snap) return c;
