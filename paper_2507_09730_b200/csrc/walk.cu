@@ -694,7 +694,10 @@ __device__ __forceinline__ void for_dielectrics_near(const DStruct& s, const dou
     if (!f(d)) return;
 }
 
-__device__ Prof strat_probe(const DStruct& s, const double c[3], double h, int n) {
+// scls (optional): the palette class of every slice when the probe classifies
+// slice centres one by one (P.ovf), so lookups need no second classification
+__device__ Prof strat_probe(const DStruct& s, const double c[3], double h, int n,
+                            uint16_t* scls = nullptr) {
   Prof P;
   P.axis = -1;
   P.raxis = 0;
@@ -827,19 +830,21 @@ __device__ Prof strat_probe(const DStruct& s, const double c[3], double h, int n
     P.axis = raw || rounded ? 0 : ax;
     return P;
   }
-  // slice by slice (rare): the classes of the slice centres
-  const int k0 = prof_class(s, P, c, h, n, 0);
-  if (k0 < 0) {
-    P.axis = -2;
-    return P;
-  }
+  // slice by slice (rare): the classes of the slice centres (one call site
+  // of the classification: code size)
+  int k0 = -1;
   bool one = true, raw = true, rounded = true;
 #pragma unroll 1
-  for (int t = 1; t < n; ++t) {
+  for (int t = 0; t < n; ++t) {
     const int k = prof_class(s, P, c, h, n, t);
     if (k < 0) {
       P.axis = -2;
       return P;
+    }
+    if (scls) scls[t] = static_cast<uint16_t>(k);
+    if (t == 0) {
+      k0 = k;
+      continue;
     }
     one &= k == k0;
     raw &= k == k0 || eps_equal(__ldg(s.pal + k), __ldg(s.pal + k0));
@@ -1628,7 +1633,8 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
   double c[3], h;
   transit_cube(L.p, fh, n, c, &h);
   PH_T0(ph1);
-  const Prof pr = strat_probe(s, c, h, n);
+  uint16_t scls[NMAX];  // slice classes of an overflowing profile (rare; local memory)
+  const Prof pr = strat_probe(s, c, h, n, scls);
   PH_ADD(1, ph1);
   const int axis = pr.axis;
   if (axis == -2) {
@@ -1645,9 +1651,9 @@ __device__ int advance_once(const DStruct& s, const DSgf& T, const DParams& P, c
     double lv[kProfCls];
 #pragma unroll
     for (int q = 0; q < kProfCls; ++q) lv[q] = pr.msk[q] ? __ldg(s.rpal + pr.cls[q]) : 0.0;
-    const bool fast = pr.ucls < 0 && !pr.ovf;
     auto layer = [&](int t) {
-      if (!fast) return prof_layer(s, pr, c, h, n, t);
+      if (pr.ucls >= 0) return __ldg(s.rpal + pr.ucls);
+      if (pr.ovf) return __ldg(s.rpal + scls[t]);
       double x = 0.0;
 #pragma unroll
       for (int q = 0; q < kProfCls; ++q)
@@ -2566,6 +2572,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
   L.jsteps = 0;
   L.cchg = 0;
   bool in_mw = false;
+  int arm_s = -1, arm_j = -1;  // a MicroWalk hop to arm (one inlined mw_arm: code size)
   const int jlane = W.jtail + blockIdx.x * blockDim.x + threadIdx.x;
   bool live = false;
   auto fetch = [&]() {
@@ -2581,7 +2588,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     if (item < qc) {
       const int q = mq[item];
       FRW_DCHECK(C, q >= 0 && q < W.S);
-      mw_arm(W, q, q, n, L, frw_dsm);
+      arm_s = arm_j = q;  // armed at the one mw_arm site below
       in_mw = true;
     } else {
       const int q = aq[item - qc];
@@ -2610,10 +2617,15 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
       if (r == 2) {
         in_mw = true;
-        mw_arm(W, A.slot, A.jslot, n, L, frw_dsm);
+        arm_s = A.slot;
+        arm_j = A.jslot;
       } else if (r == 1) {
         fetch();
       }
+    }
+    if (arm_s >= 0) {
+      mw_arm(W, arm_s, arm_j, n, L, frw_dsm);
+      arm_s = -1;
     }
     // up to 32 super-steps per transition (a hop is ~50 super-steps): the
     // MicroWalk lanes run long stretches between the divergent transitions
@@ -2621,9 +2633,9 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     const long long c1 = clock64();
 #pragma unroll 1
     for (int rep = 0; rep < FRW_TAIL_REPS; ++rep) {
-      const unsigned mwm = __ballot_sync(0xFFFFFFFFu, live && in_mw);
+      const unsigned mwm = __ballot_sync(0xFFFFFFFFu, live && in_mw && arm_s < 0);
       if (!mwm) break;
-      if (!(live && in_mw)) continue;
+      if (!(live && in_mw) || arm_s >= 0) continue;  // (a hop fetched here is armed next iteration)
       int xdir = 0;
       const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
       FRW_DCHECK(C, node_ok(L.node, n));
