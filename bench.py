@@ -474,7 +474,9 @@ def walk_c3(args, rank, world, dist, torch, smem_peak, prof, cpu):
            "scaling": "strong", "walks_per_step": W,
            "e2e": {"value": total / wall_s, "unit": "walks/s",
                    "h2d_bytes_per_step": len(doc),
-                   "d2h_bytes_per_step": 32 * W if world == 1 else 8 * (3 * 4 + 12)},
+                   # per-1024-walk partial tallies (frw_walk_chunk_tallies): 4 slots
+                   "d2h_bytes_per_step": (-(-W // 1024) * 8 * (3 * 4 + 12)) if world == 1
+                   else 8 * (3 * 4 + 12)},
            "capacitance_aF": {str(t["conductor_id"]): round(t["capacitance_farads"] * 1e18, 3)
                               for t in res["terminals"]},
            "rel_se_self": res["terminals"][0]["std_err_farads"] /
@@ -524,7 +526,7 @@ def walk_c4(args, rank, world, dist, torch, smem_peak, prof, cpu):
            "device_seconds": r["t_device_seconds"], "wall_seconds": wall,
            "worst_coupling_rel_se": worst, "n_gpus_used": 1,
            "e2e": {"value": w / wall, "unit": "walks/s", "h2d_bytes_per_step": len(doc),
-                   "d2h_bytes_per_step": 32 * w},
+                   "d2h_bytes_per_step": -(-w // 1024) * 8 * (3 * len(ids) + 12)},
            "capacitance_aF": {str(i): round(t["capacitance_farads"] * 1e18, 4)
                               for i, t in zip(ids, r["terminals"])},
            "sgf_table": "warm (filled by a 2^20-walk warm-up call)"}

@@ -249,6 +249,18 @@ int frw_run_walks(frw_ctx *ctx, const frw_walk_params *p, int32_t master,
                   uint64_t walk_begin, int64_t count, frw_miss_fn miss,
                   void *user, frw_tally *out, frw_walk_record *records);
 
+/* Per-chunk tallies of the last successful frw_run_walks on this context: the
+ * call's walks in chunks of *chunk (1024) consecutive walk indices from its
+ * walk_begin, per chunk sum[nslots], sumsq[nslots], landed[nslots] (each sum
+ * taken in walk order) and stats[12] (aborted, resampled, first-transition
+ * branches 0-3, cached hops, MicroWalk hops, MicroWalk steps).  The host fold
+ * of engine.cpp:461-468 over reference batches that are multiples of the
+ * chunk reads these instead of the per-walk records (192 B per 1024 walks and
+ * conductor slot against 32 KB of records).  Any pointer may be NULL; arrays
+ * hold *nchunks * nslots (stats: *nchunks * 12) entries. */
+int frw_walk_chunk_tallies(frw_ctx *ctx, int64_t *nchunks, int32_t *chunk, double *sum,
+                           double *sumsq, uint64_t *landed, uint64_t *stats);
+
 /* ---- multi-GPU: the per-conductor tallies across ranks ---
  * Walks shard as contiguous walk-index ranges of ONE seed (rank g of G runs
  * [g*W/G, (g+1)*W/G), the reference's per-thread chunking, engine.cpp:437-458);

@@ -139,6 +139,8 @@ std::map<std::pair<int, int>, Device*>& devices() {
   return *m;                                                    // no teardown after CUDA exits
 }
 std::mutex g_tab_mu;  // guards the tables() map (lanes of a multi-device extract)
+constexpr int64_t kTallyChunk = 1024;  // walks per device partial tally (frw_walk_chunk_tallies)
+
 struct DeviceTable {
   int n = 0;  // lattice size of the keys currently on the device
   std::unordered_set<ProfileKey, ProfileKeyHash> keys;  // keys already put
@@ -146,6 +148,10 @@ struct DeviceTable {
   // one chunk while the device fills the other), kept across extract calls
   frw_walk_record* rec[2] = {nullptr, nullptr};
   size_t rec_cap[2] = {0, 0};
+  // per-1024-walk partial tallies (frw_walk_chunk_tallies), same two buffers
+  std::vector<double> csum[2], csq[2];
+  std::vector<uint64_t> cland[2], cstat[2];
+  int64_t nchunks[2] = {0, 0};
 };
 std::map<frw_ctx*, DeviceTable>& tables() {
   static auto* m = new std::map<frw_ctx*, DeviceTable>;
@@ -471,6 +477,45 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
       }
     }
   };
+  // The same fold from the device's per-chunk tallies (1024 consecutive walks
+  // each, summed in walk order): when reference batches are whole chunks,
+  // only ~200 bytes per 1024 walks and slot cross PCIe instead of the
+  // records; a batch adds its chunks in order, so the result is the same for
+  // every device chunking and device count
+  const bool use_chunks = batch % kTallyChunk == 0;
+  auto fold_chunks = [&](const DeviceTable& DT, int buf, int64_t chunk) {
+    const size_t ns = nslots;
+    for (int64_t off = 0; off < chunk; off += batch) {
+      const int64_t end = std::min<int64_t>(chunk, off + batch);
+      for (int64_t c = off / kTallyChunk; c < (end + kTallyChunk - 1) / kTallyChunk; ++c) {
+        for (size_t k = 0; k < ns; ++k) {
+          sum[k] += DT.csum[buf][c * ns + k];
+          sumsq[k] += DT.csq[buf][c * ns + k];
+          landed[k] += DT.cland[buf][c * ns + k];
+        }
+        const uint64_t* st = &DT.cstat[buf][c * 12];
+        res.aborted += st[0];
+        res.resampled += st[1];
+        res.dispatch.first_stratified += st[2];
+        res.dispatch.first_shrunk += st[3];
+        res.dispatch.first_layered += st[4];
+        res.dispatch.first_homogenized += st[5];
+        res.dispatch.cached += st[6];
+        if (cfg_.mode == Mode::MWE || cfg_.mode == Mode::HybridMWE)
+          res.dispatch.microwalk_e += st[7];
+        else if (cfg_.mode == Mode::FDM)
+          res.dispatch.fdm += st[7];
+        else
+          res.dispatch.microwalk += st[7];
+        res.mw_steps += st[8];
+      }
+      walks += end - off;
+      if (walks >= static_cast<uint64_t>(cfg_.min_walks) && converged_now()) {
+        converged = true;
+        break;
+      }
+    }
+  };
   // Device chunks of dev_batch walks (each drains its slot pool through the
   // run-to-completion tail once, so large chunks amortise it), G at a time
   // (one per lane / device, in walk order).  While the devices run wave k+1 a
@@ -486,6 +531,24 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
     L.rc = FRW_OK;
     if (L.count <= 0) return;
     DeviceTable& DT = *L.dt;
+    L.t.sum = L.ts.data();
+    L.t.sumsq = L.tq.data();
+    L.t.landed = L.tl.data();
+    if (use_chunks) {
+      L.rc = frw_run_walks(L.ctx, &p, master, L.begin, L.count, miss_cb, &L.mc, &L.t, nullptr);
+      if (L.rc != FRW_OK) return;
+      const size_t nc = (L.count + kTallyChunk - 1) / kTallyChunk;
+      DT.csum[buf].resize(nc * nslots);
+      DT.csq[buf].resize(nc * nslots);
+      DT.cland[buf].resize(nc * nslots);
+      DT.cstat[buf].resize(nc * 12);
+      int32_t ch = 0;
+      L.rc = frw_walk_chunk_tallies(L.ctx, &DT.nchunks[buf], &ch, DT.csum[buf].data(),
+                                    DT.csq[buf].data(), DT.cland[buf].data(), DT.cstat[buf].data());
+      if (L.rc == FRW_OK && (ch != kTallyChunk || DT.nchunks[buf] != static_cast<int64_t>(nc)))
+        L.rc = FRW_ECUDA;
+      return;
+    }
     if (DT.rec_cap[buf] < static_cast<size_t>(L.count)) {
       if (DT.rec[buf]) frw_host_free(L.ctx, DT.rec[buf]);
       DT.rec[buf] = nullptr;
@@ -535,11 +598,19 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
       dev_ms += wave_ms;
     }
     std::vector<std::pair<const frw_walk_record*, int64_t>> parts;
+    std::vector<std::pair<const DeviceTable*, int64_t>> cparts;
     for (const Lane& L : lanes)
-      if (L.count > 0) parts.emplace_back(L.dt->rec[cur], L.count);
-    worker = std::thread([&fold, &converged, parts] {
-      for (const auto& [rec, n] : parts) {
-        fold(rec, n);
+      if (L.count > 0) {
+        parts.emplace_back(L.dt->rec[cur], L.count);
+        cparts.emplace_back(L.dt, L.count);
+      }
+    const int fb = cur;
+    worker = std::thread([&fold, &fold_chunks, &converged, use_chunks, parts, cparts, fb] {
+      for (size_t i = 0; i < parts.size(); ++i) {
+        if (use_chunks)
+          fold_chunks(*cparts[i].first, fb, cparts[i].second);
+        else
+          fold(parts[i].first, parts[i].second);
         if (converged) break;
       }
     });

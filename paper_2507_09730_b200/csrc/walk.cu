@@ -3500,6 +3500,7 @@ struct Engine {
   // for frw_tally_allreduce
   double* pack = nullptr;
   int tally_n = 0, tally_slots = 0, tally_mode = 0;
+  long long tally_chunks = 0;  // kChunk-walk partial tallies of the last call (k_reduce_chunks)
   double *psum = nullptr, *psq = nullptr, *osum = nullptr, *osq = nullptr;
   unsigned long long *pland = nullptr, *pstat = nullptr, *oland = nullptr, *ostat = nullptr;
   size_t red_cap = 0;
@@ -4815,6 +4816,26 @@ int frw_nccl_destroy(frw_ctx* ctx) {
   return FRW_OK;
 }
 
+int frw_walk_chunk_tallies(frw_ctx* ctx, int64_t* nchunks, int32_t* chunk, double* sum,
+                           double* sumsq, uint64_t* landed, uint64_t* stats) {
+  if (!ctx || !nchunks) return FRW_EINVAL;
+  Engine& E = *engine_of(ctx);
+  if (E.tally_n == 0) return frw_fail(ctx, FRW_EINVAL, "chunk tallies: no successful run_walks");
+  *nchunks = E.tally_chunks;
+  if (chunk) *chunk = kChunk;
+  const size_t ns = static_cast<size_t>(E.tally_chunks) * E.tally_slots;
+  FRW_CUDA(ctx, cudaSetDevice(ctx->device));
+  if (sum) FRW_CUDA(ctx, cudaMemcpyAsync(sum, E.psum, 8 * ns, cudaMemcpyDeviceToHost, ctx->stream));
+  if (sumsq) FRW_CUDA(ctx, cudaMemcpyAsync(sumsq, E.psq, 8 * ns, cudaMemcpyDeviceToHost, ctx->stream));
+  if (landed)
+    FRW_CUDA(ctx, cudaMemcpyAsync(landed, E.pland, 8 * ns, cudaMemcpyDeviceToHost, ctx->stream));
+  if (stats)
+    FRW_CUDA(ctx, cudaMemcpyAsync(stats, E.pstat, 8 * 12 * static_cast<size_t>(E.tally_chunks),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  FRW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FRW_OK;
+}
+
 int frw_tally_allreduce(frw_ctx* ctx, void* comm, frw_tally* out) {
   if (!ctx || !out) return FRW_EINVAL;
   Engine* E = static_cast<Engine*>(ctx->walk);
@@ -5228,6 +5249,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     E.tally_n = 3 * nslots + 12;
     E.tally_slots = nslots;
     E.tally_mode = P.mode;
+    E.tally_chunks = count > 0 ? (count + kChunk - 1) / kChunk : 0;
     out->aborted = st[0];
     out->resampled = st[1];
     for (int b = 0; b < 4; ++b) out->first[b] = st[2 + b];
