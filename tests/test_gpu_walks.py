@@ -243,3 +243,21 @@ def test_default_mode_is_hybrid_mwe_and_dispatch_counts():
     sub = res["dispatch_stats"]["subsequent"]
     assert sub["microwalk"] == 0 and sub["microwalk_e"] > 0 and sub["fdm"] == 0
     assert sum(res["dispatch_stats"]["first"].values()) == res["walks"]
+
+
+def test_chunk_tally_fold_equals_record_fold():
+    """extract folds per-1024-walk device tallies (frw_walk_chunk_tallies) when
+    reference batches are whole chunks, and per-walk records otherwise: the
+    same walks land in the same slots, the sums agree to rounding, and the
+    stopping rule stops on the same batch boundary class"""
+    import paper_2507_09730_b200.frwcap as frwcap
+    doc = json.dumps(c3_structure())
+    kw = dict(mode="HYBRID-MW", min_walks=200_000, max_walks=200_000, seed=9)
+    a = frwcap.extract_json(doc, batch=1024, **kw)   # chunk tallies
+    b = frwcap.extract_json(doc, batch=1000, **kw)   # per-walk records
+    assert a["walks"] == b["walks"] == 200_000
+    assert a["dispatch_stats"] == b["dispatch_stats"] and a["mw_steps"] == b["mw_steps"]
+    for ta, tb in zip(a["terminals"], b["terminals"]):
+        assert ta["walks_landed"] == tb["walks_landed"]
+        assert ta["capacitance_farads"] == pytest.approx(tb["capacitance_farads"], rel=1e-12,
+                                                         abs=1e-30)
