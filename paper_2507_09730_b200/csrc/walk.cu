@@ -1898,6 +1898,13 @@ __device__ __forceinline__ void mw_arm(const DSlots& W, int slot, int jslot, int
       // register waits on them until the one wait below
 #pragma unroll 1
       for (int q = 0; q < L.nbx; ++q) cp_async8(d + q * blockDim.x, G + q);
+      // the job's cube (centre, half width) in the slice's top words when it
+      // has room: the surface exit then reads no global memory
+      if (L.nbx <= kBoxSm - 4) {
+        const uint64_t* cube = reinterpret_cast<const uint64_t*>(W.cube) + 4 * static_cast<size_t>(jslot);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cp_async8(d + (kBoxSm - 4 + q) * blockDim.x, cube + q);
+      }
       cp_async_wait_all();
       L.bx = BoxView{d, static_cast<int>(blockDim.x)};
     } else {
@@ -1944,16 +1951,22 @@ __device__ void mw_exit(const DSlots& W, int n, MwLane& L, int dir) {
   const int u = a == 0 ? j : i;
   const int v = a == 2 ? j : k;
   const int panel = (dir * n + v) * n + u;  // surface_panel_of (sgf.cpp:13-30)
-  const double c[3] = {W.cube[4 * L.jslot], W.cube[4 * L.jslot + 1], W.cube[4 * L.jslot + 2]};
-  const double h = W.cube[4 * L.jslot + 3];
+  // the cube from the lane's shared-memory slice when mw_arm staged it there
+  const bool staged = L.bx.stride != 1 && L.nbx <= kBoxSm - 4;
+  const double* cs = staged ? reinterpret_cast<const double*>(L.bx.p) : W.cube + 4 * L.jslot;
+  const int cst = staged ? L.bx.stride : 1, c0 = staged ? kBoxSm - 4 : 0;
+  const double c[3] = {cs[c0 * cst], cs[(c0 + 1) * cst], cs[(c0 + 2) * cst]};
+  const double h = cs[(c0 + 3) * cst];
   double p[3];
   panel_center(c, h, n, panel, p);
   W.p[3 * L.slot + 0] = p[0];
   W.p[3 * L.slot + 1] = p[1];
   W.p[3 * L.slot + 2] = p[2];
   W.rng[L.slot] = L.rng;
-  W.mw[L.slot] += 1;
-  W.mwsteps[L.slot] += L.steps;
+  // reductions, not load-add-store: nothing waits for the slot's counters
+  atomicAdd(&W.mw[L.slot], 1u);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&W.mwsteps[L.slot]),
+            static_cast<unsigned long long>(L.steps));
   W.state[L.slot] = S_ACTIVE;
 }
 
