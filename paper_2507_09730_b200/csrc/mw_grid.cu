@@ -54,6 +54,11 @@ namespace {
 #ifndef FRW_STRIDE_SHFL
 #define FRW_STRIDE_SHFL 1
 #endif
+// Philox 8-step blocks per super-step of mw_grid_fast (exit bookkeeping and
+// the step cap test run once per super-step)
+#ifndef FRW_GRID_PB
+#define FRW_GRID_PB 1
+#endif
 constexpr int kThreads = 1024;
 constexpr int kDirAxis[6] = {0, 0, 1, 1, 2, 2};
 constexpr int kDirSign[6] = {-1, +1, -1, +1, -1, +1};
@@ -301,8 +306,8 @@ __device__ __forceinline__ uint32_t smem_base(const void* p) {
   return a;
 }
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
-  uint16_t v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  uint32_t v;  // zero-extended into a 32-bit register (no 16-bit merges)
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
@@ -619,7 +624,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the step count comes from a dwell counter and the exit panel from the
   // absorbing node alone (exit_info)
   constexpr bool SM = RNG != FRW_RNG_PHILOX;
-  constexpr int SS = SM ? 4 : 8;
+  // Philox: FRW_GRID_PB blocks of 8 steps per super-step (the stream is the
+  // same: block b of a transit is counter (id, b))
+  constexpr int PB = SM ? 1 : FRW_GRID_PB;
+  constexpr int SS = SM ? 4 : 8 * PB;
   // shared: records | node map | stride table (8 x s32) | mbarrier
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* rec_p = smem;
@@ -644,11 +652,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   const uint32_t s_map = smem_base(map_p);
-#if FRW_STRIDE_SHFL
+#if FRW_STRIDE_SHFL == 2
+  // stride magnitudes as 16-bit fields {2, 2np, 2npp, 0}, selected by PRMT
+  const uint32_t mag_lo = 2u | (static_cast<uint32_t>(2 * g.np) << 16);
+  const uint32_t mag_hi = static_cast<uint32_t>(2 * g.npp);
+#elif FRW_STRIDE_SHFL
   const int lane_stride = str_p[threadIdx.x & 7];
 #else
   const uint32_t s_str = smem_base(str_p);
 #endif
+  // byte stride of direction d in the padded map (d = 6: the exit record's
+  // stand-still)
+  auto stride_of = [&](int d) -> uint32_t {
+#if FRW_STRIDE_SHFL == 2
+    // field d>>1 (upper bytes from the zero field 3), negated for even d: no
+    // MIO op on the step's critical path
+    uint32_t mag;
+    asm("prmt.b32 %0, %1, %2, %3;"
+        : "=r"(mag)
+        : "r"(mag_lo), "r"(mag_hi), "r"(static_cast<uint32_t>(d & 6) * 0x11u + 0x7710u));
+    return mag * static_cast<uint32_t>(2 * (d & 1) - 1);
+#elif FRW_STRIDE_SHFL
+    return static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, lane_stride, d));
+#else
+    return static_cast<uint32_t>(lds_s32(s_str + 4u * d));
+#endif
+  };
   const uint32_t s_exit = s_rec + 8u * g.exit_rec;
   const uint32_t a_start = s_map + 2u * g.start_idx;
   const uint32_t ra_start = lds_u16(a_start);
@@ -674,21 +703,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t k1 = static_cast<uint32_t>(p.seed >> 32);
 
   while (__any_sync(0xFFFFFFFFu, live)) {
-    uint32_t w[4];
+    uint32_t w[4 * PB];
     if (RNG == FRW_RNG_PHILOX) {
       // one 4x32-10 call per 8 steps: word k gives step 2k its x11 from bits
       // 31..21 (16-bit prefix 31..16) and step 2k+1 from bits 10..0 (prefix
       // continues with bits 15..11); the low 37 bits of x come from the
       // (id, step slot, 1) counter only on a 16-bit tie
       const uint64_t id = static_cast<uint64_t>(p.stream_begin + t);
-      const U32x4 o = philox4x32_10(
-          {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
-           static_cast<uint32_t>(blk), 0u},
-          k0, k1);
-      w[0] = o.x;
-      w[1] = o.y;
-      w[2] = o.z;
-      w[3] = o.w;
+#pragma unroll
+      for (int c = 0; c < PB; ++c) {
+        const U32x4 o = philox4x32_10(
+            {static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32),
+             static_cast<uint32_t>(blk * PB + c), 0u},
+            k0, k1);
+        w[4 * c] = o.x;
+        w[4 * c + 1] = o.y;
+        w[4 * c + 2] = o.z;
+        w[4 * c + 3] = o.w;
+      }
     }
 #pragma unroll
     for (int u = 0; u < SS; ++u) {
@@ -709,11 +741,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       int dir = __popc((static_cast<uint32_t>(d1) & kGuardLo) | (d1h & kGuardHi));
       // (absorbed lanes never tie: their shift is 72, which PTX clamps to 0)
       const bool tie = (~shr64_lo(d1, 12u * dir) & 0x7FFu) == 0;
+      // move first (the common case) so the next map load is in flight while
+      // the tie test resolves; a tied lane redoes its move in the tie block
+      const uint32_t a0 = a, ra0 = ra;
+      a = a0 + stride_of(dir);
+      ra = lds_u16(a);
       if (__builtin_expect(__any_sync(0xFFFFFFFFu, tie), 0)) {
         // 11-bit tie: exact comparison against the 53-bit thresholds.  The
         // block is warp-uniform (predicated per lane), so the common path
         // carries no reconvergence barrier.
-        const uint64_t* f = g.full + 5 * ((ra - s_rec) >> 3);
+        const uint64_t* f = g.full + 5 * ((ra0 - s_rec) >> 3);
         uint64_t th[5];
 #pragma unroll
         for (int d = 0; d < 5; ++d) th[d] = tie ? __ldg(f + d) : 0;
@@ -749,13 +786,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         dir = tie ? dx : dir;
+        const uint32_t a1 = a0 + stride_of(dir);  // (all lanes: the shuffle)
+        if (tie) {
+          a = a1;
+          ra = lds_u16(a1);
+        }
       }
-#if FRW_STRIDE_SHFL
-      a += static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, lane_stride, dir));
-#else
-      a += static_cast<uint32_t>(lds_s32(s_str + 4u * dir));
-#endif
-      ra = lds_u16(a);
       if (TRACK) {
         if (act) xinfo = (u << 3) | dir;
       } else {
