@@ -99,6 +99,9 @@ __host__ __device__ uint64_t threshold_of(double acc, double sum) {
   return x;
 }
 
+// e / (e + e) is exactly 1/2 unless e + e overflows
+__host__ __device__ inline bool same_eps_halves(double e) { return e <= 0x1.0p1022; }
+
 // open-addressing map from a 112-bit stencil key to its record index
 struct KeyTable {
   std::vector<Key> key;
@@ -219,7 +222,22 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
           const int nv = (nb[2] * n + nb[1]) * n + nb[0];
           code[d] = (mask && mask[nv] >= 0) ? kCond : node_pal[nv];
         }
-        const uint32_t self = node_pal[v];
+        uint32_t self = node_pal[v];
+        // A node whose non-absorbing neighbours all share its permittivity e
+        // steps with alphas e / (e + e) = 1/2 whatever e is: one record for
+        // all of them (palette id 0 stands for e), so the walkers inside
+        // uniform regions gather one shared-memory address (a broadcast)
+        // instead of one per permittivity.
+        if (same_eps_halves(pal[self]) && same_eps_halves(pal[0])) {
+          bool uniform = true;
+          for (int d = 0; d < 6; ++d)
+            uniform = uniform && (code[d] == self || code[d] == kSurface || code[d] == kCond);
+          if (uniform) {
+            for (int d = 0; d < 6; ++d)
+              if (code[d] == self) code[d] = 0;
+            self = 0;
+          }
+        }
         Key key{(uint64_t(self) << 48) | (uint64_t(code[0]) << 32) |
                     (uint64_t(code[1]) << 16) | code[2],
                 (uint64_t(code[3]) << 32) | (uint64_t(code[4]) << 16) | code[5]};
@@ -232,7 +250,7 @@ int compile_grid(frw_ctx* ctx, int n, const double* eps, const int32_t* mask,
           // in-order partial sums
           double acc[6], sum = 0;
           uint64_t packed = 0;
-          const double ev = pal[node_pal[v]];
+          const double ev = pal[self];
           for (int d = 0; d < 6; ++d) {
             double a = 1.0;
             if (code[d] != kSurface && code[d] != kCond) {
@@ -959,7 +977,9 @@ __global__ void k_dc_node_pal(int nodes, DcBufs B) {
 // neighbour codes (surface / conductor / palette id), 9 bits each; bit 63 set
 __device__ __forceinline__ uint64_t dc_key(const DcBufs& B, int n, int i, int j, int k) {
   const int v = (k * n + j) * n + i;
-  uint64_t key = (1ull << 63) | B.node_pal[v];
+  const uint32_t self = B.node_pal[v];
+  uint64_t key = (1ull << 63) | self;
+  bool uniform = true;  // every non-absorbing neighbour has the node's permittivity
 #pragma unroll
   for (int d = 0; d < 6; ++d) {
     int nb[3] = {i, j, k};
@@ -971,7 +991,19 @@ __device__ __forceinline__ uint64_t dc_key(const DcBufs& B, int n, int i, int j,
       const int nv = (nb[2] * n + nb[1]) * n + nb[0];
       code = (B.mask && B.mask[nv] >= 0) ? kDcCond : B.node_pal[nv];
     }
+    uniform = uniform && (code == self || code >= kDcCond);
     key |= static_cast<uint64_t>(code) << (9 * (d + 1));
+  }
+  // all alphas 1/2 or 1 whatever the permittivity: palette id 0 stands for it
+  // (see compile_grid), one record for every uniform neighbourhood
+  if (uniform && self < kDcPal && same_eps_halves(B.pal_eps[self]) && same_eps_halves(B.pal_eps[0])) {
+    uint64_t canon = 1ull << 63;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+      const uint64_t code = (key >> (9 * (d + 1))) & 0x1FF;
+      canon |= (code >= kDcCond ? code : 0ull) << (9 * (d + 1));
+    }
+    key = canon;
   }
   return key;
 }

@@ -2367,6 +2367,38 @@ __device__ __forceinline__ void flush_mw_stats(DCounters* C, const MwLane& L) {
   }
 }
 
+// Cell-change batching: a lane whose hop moved into another cell looks the
+// cell up at the start of its next super-step (cell_scan, O(boxes), ~1/5 of
+// the lanes per pass).  With FRW_CC_NUM/FRW_CC_DEN > 0 such a lane sits out
+// passes until that share of the warp's stepping lanes is waiting too (or one
+// has waited FRW_CC_WAIT passes), so the lookup's instructions serve several
+// lanes at once.  A waiting lane draws nothing: its stream position and
+// hence its walk are unchanged.
+#ifndef FRW_CC_NUM
+#define FRW_CC_NUM 0
+#endif
+#ifndef FRW_CC_DEN
+#define FRW_CC_DEN 1
+#endif
+#ifndef FRW_CC_WAIT
+#define FRW_CC_WAIT 4
+#endif
+// stepping: the lane would run a super-step this pass; returns whether it
+// should sit this pass out (all 32 lanes call)
+__device__ __forceinline__ bool cc_hold(bool stepping, const MwLane& L, int& waited) {
+#if FRW_CC_NUM > 0
+  const bool pend = stepping && (L.room >> 48) == 0;
+  const int np = __popc(__ballot_sync(0xFFFFFFFFu, pend));
+  const int ns = __popc(__ballot_sync(0xFFFFFFFFu, stepping));
+  const bool late = __any_sync(0xFFFFFFFFu, pend && waited >= FRW_CC_WAIT);
+  const bool hold = pend && !late && np * FRW_CC_DEN < ns * FRW_CC_NUM;
+  waited = hold ? waited + 1 : 0;
+  return hold;
+#else
+  return false;
+#endif
+}
+
 // persistent MicroWalk kernel: each thread runs queued hops back to back
 #ifndef FRW_KMW_MINB
 #define FRW_KMW_MINB 2  // 64 registers: two 512-thread CTAs per SM (+1-2% over one)
@@ -2403,13 +2435,15 @@ __global__ void __launch_bounds__(512, FRW_KMW_MINB)
     FRW_DCHECK(C, q0 >= 0 && q0 < W.S);
     mw_arm(W, q0, q0, n, L, frw_dsm);
   }
+  int cc_waited = 0;
   while (__any_sync(0xFFFFFFFFu, live)) {
     int code = MW_GO, xdir = 0;
-    if (live) {
+    const bool hold = cc_hold(live, L, cc_waited);
+    if (live && !hold) {
       code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
       FRW_DCHECK(C, node_ok(L.node, n));
     }
-    if (live && code == MW_GO && --left == 0) {
+    if (live && !hold && code == MW_GO && --left == 0) {
       mw_carry(W, C, mq_next, L);
       code = -1;
     }
@@ -2562,6 +2596,15 @@ constexpr int kTailBlocks = FRW_TAIL_BLOCKS;  // resident 256-thread CTAs per SM
 #ifndef FRW_TAIL_REPS
 #define FRW_TAIL_REPS 32  // MicroWalk super-steps per transition in k_tail
 #endif
+#ifndef FRW_TAIL_VOTE
+#define FRW_TAIL_VOTE 1  // phase vote (0: the fixed transition / MicroWalk alternation)
+#endif
+#ifndef FRW_TAIL_VOTE_T
+#define FRW_TAIL_VOTE_T 1  // weights of the lanes waiting for a transition / inside a hop
+#endif
+#ifndef FRW_TAIL_VOTE_M
+#define FRW_TAIL_VOTE_M 2  // (1:1 and 2:1 measured 1-2% behind 1:2 on C3-C5)
+#endif
 template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_tail(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
@@ -2619,6 +2662,70 @@ __global__ void __launch_bounds__(256, kTailBlocks)
 #endif
   fetch();
   long long cyc_mw = 0, cyc_all = 0;  // warp-uniform clock64 spans
+#if FRW_TAIL_VOTE
+  // Phase vote: each pass the warp runs the phase more of its live lanes wait
+  // for -- one transition each for the lanes between hops, or MicroWalk
+  // super-steps for the lanes inside a hop, until the waiting lanes outnumber
+  // them (ties alternate) -- instead of a fixed alternation, so either
+  // phase's instructions run with at least half of the live lanes.
+  bool last_adv = false;
+  int cc_waited = 0;
+  while (__any_sync(0xFFFFFFFFu, live)) {
+    const long long c0 = clock64();
+    if (arm_s >= 0) {
+      mw_arm(W, arm_s, arm_j, n, L, frw_dsm);
+      arm_s = -1;
+    }
+    const int nt = __popc(__ballot_sync(0xFFFFFFFFu, live && !in_mw));
+    const int nm = __popc(__ballot_sync(0xFFFFFFFFu, live && in_mw));
+    if (nt * FRW_TAIL_VOTE_T > nm * FRW_TAIL_VOTE_M || (nt * FRW_TAIL_VOTE_T == nm * FRW_TAIL_VOTE_M && !last_adv)) {
+      last_adv = true;
+      if (live && !in_mw) {
+        const int r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
+        if (r == 2) {
+          in_mw = true;
+          arm_s = A.slot;
+          arm_j = A.jslot;
+        } else if (r == 1) {
+          fetch();
+        }
+      }
+      cyc_all += clock64() - c0;
+      continue;
+    }
+    last_adv = false;
+    const long long c1 = clock64();
+#pragma unroll 1
+    for (int rep = 0; rep < FRW_TAIL_REPS; ++rep) {
+      const int km = __popc(__ballot_sync(0xFFFFFFFFu, live && in_mw && arm_s < 0));
+      const int kt = __popc(__ballot_sync(0xFFFFFFFFu, live && (!in_mw || arm_s >= 0)));
+      if (km == 0 || km * FRW_TAIL_VOTE_M < kt * FRW_TAIL_VOTE_T) break;
+      if (cc_hold(live && in_mw && arm_s < 0, L, cc_waited)) continue;
+      if (!(live && in_mw) || arm_s >= 0) continue;
+      int xdir = 0;
+      const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
+      FRW_DCHECK(C, node_ok(L.node, n));
+      if (code == MW_GO) continue;
+      in_mw = false;
+      if (code == MW_SURFACE) {
+        mw_exit(W, n, L, xdir);
+        adv_load(W, L.slot, A);
+        A.jslot = jlane;
+        continue;
+      }
+      if (code == MW_COND)
+        mw_conductor_exit(W, recs, C, L, xdir);
+      else {
+        set_err(C, FRW_ESTEPCAP);
+        W.state[L.slot] = S_FREE;
+      }
+      fetch();
+    }
+    const long long c2 = clock64();
+    cyc_mw += c2 - c1;
+    cyc_all += c2 - c0;
+  }
+#else
   while (__any_sync(0xFFFFFFFFu, live)) {
     const long long c0 = clock64();
     if (live && !in_mw) {
@@ -2681,6 +2788,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     }
 #endif
   }
+#endif  // FRW_TAIL_VOTE
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&C->tail_mw_cyc, static_cast<unsigned long long>(cyc_mw));
     atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_all));
