@@ -217,6 +217,8 @@ struct DParams {
   // time slices of the wavefront rounds (0: unlimited): super-steps of one
   // MicroWalk hop per k_mw visit, transitions of one walk per k_advance visit
   int mw_slice, adv_slice;
+  // k_flow: SM pairs (of flow_sms) that run transitions; the others run MicroWalk hops
+  int flow_adv, flow_sms;
 };
 
 struct WalkRec {  // per walk id, written once when the walk terminates
@@ -2833,13 +2835,18 @@ __device__ __forceinline__ unsigned long long flow_live(const DCounters* C) {
 
 __global__ void k_flow_init(DCounters* C) {
   C->fah = C->fat = C->fmh = C->fmt = 0;
-  C->flive = C->alen;
+  C->flive = C->alen + C->qlen;  // ACTIVE walks and the hops carried over from the last round
 }
+
+// Roles by SM instead of by warp (DParams::flow_adv of the flow_sms SMs run
+// transitions, the others MicroWalk hops): an SM then fetches only its
+// role's code -- k_tail's top stall is instruction fetch, its transition and
+// MicroWalk paths together are three times the 32 KB L1.5 instruction cache.
 
 template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_flow(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
-           const int* aq, int* ring_a, int* ring_m, unsigned mask) {
+           const int* aq, const int* mq, int* ring_a, int* ring_m, unsigned mask) {
   __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
   __shared__ DirDelta dd[6];
   extern __shared__ uint64_t frw_dsm[];  // kBoxSm box slices per thread (mw_arm)
@@ -2848,7 +2855,19 @@ __global__ void __launch_bounds__(256, kTailBlocks)
   const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
   const int n = P.n;
   const unsigned long long alen = C->alen;
-  if ((threadIdx.x >> 5) < kFlowAdvWarps) {
+  const unsigned long long qlen = C->qlen;
+  long long cyc_busy = 0;  // warp-uniform clock64 spans with work in hand
+  // role by SM pair (SM ids 2t and 2t+1, one TPC: measured, mixed pairs lose the
+  // instruction-cache benefit): flow_adv of the flow_sms pairs, evenly spread
+  // (flow_sms = 0: roles by warp, kFlowAdvWarps of the CTA's 8)
+  bool adv_role = (threadIdx.x >> 5) < kFlowAdvWarps;
+  if (P.flow_sms > 0) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned m = (smid >> 1) % static_cast<unsigned>(P.flow_sms);
+    adv_role = (m + 1) * P.flow_adv / P.flow_sms != m * P.flow_adv / P.flow_sms;
+  }
+  if (adv_role) {
     // ---- advance warp ----
     AdvLane A;
     bool have = false, first = true;
@@ -2881,6 +2900,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         __nanosleep(256);
         continue;
       }
+      const long long c0 = clock64();
       if (have) {
         const int r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
         if (r == 2) {
@@ -2891,7 +2911,11 @@ __global__ void __launch_bounds__(256, kTailBlocks)
           have = false;
         }
       }
+      cyc_busy += clock64() - c0;
     }
+    // T_MW: the busy cycles of the MicroWalk warps over those of all warps
+    if ((threadIdx.x & 31) == 0)
+      atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_busy));
   } else {
     // ---- MicroWalk warp ----
     const int cap = 1000 * n * n;  // microwalk.cpp:81
@@ -2900,10 +2924,20 @@ __global__ void __launch_bounds__(256, kTailBlocks)
     L.jumps = 0;
     L.jsteps = 0;
     L.cchg = 0;
-    bool have = false;
+    bool have = false, firstm = qlen > 0;
     long long res = -1;
     for (;;) {
-      if (!have) {
+      if (!have && firstm) {  // the hops carried over from the last round first
+        const unsigned long long item = atomicAdd(&C->qhead, 1ull);
+        if (item < qlen) {
+          const int q = mq[item];
+          mw_arm(W, q, q, n, L, frw_dsm);
+          have = true;
+        } else {
+          firstm = false;
+        }
+      }
+      if (!have && !firstm) {
         if (res < 0) res = static_cast<long long>(atomicAdd(&C->fmh, 1ull));
         const int v = ring_poll(ring_m, res, mask);
         if (v >= 0) {
@@ -2919,6 +2953,7 @@ __global__ void __launch_bounds__(256, kTailBlocks)
         __nanosleep(256);
         continue;
       }
+      const long long c0 = clock64();
       if (have) {
         int xdir = 0;
         const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
@@ -2938,6 +2973,11 @@ __global__ void __launch_bounds__(256, kTailBlocks)
           }
         }
       }
+      cyc_busy += clock64() - c0;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&C->tail_mw_cyc, static_cast<unsigned long long>(cyc_busy));
+      atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_busy));
     }
     flush_mw_stats(C, L);
   }
@@ -5068,9 +5108,9 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   // events: created after every early-return allocation/sync step above and
   // destroyed on every exit below
   struct Events {
-    cudaEvent_t t0 = nullptr, t1 = nullptr, m0 = nullptr, m1 = nullptr, a0 = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr, m0 = nullptr, m1 = nullptr, a0 = nullptr, c0 = nullptr;
     ~Events() {
-      for (cudaEvent_t e : {t0, t1, m0, m1, a0})
+      for (cudaEvent_t e : {t0, t1, m0, m1, a0, c0})
         if (e) cudaEventDestroy(e);
     }
   } ev;
@@ -5080,8 +5120,9 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   cudaEventCreate(&ev.m1);
   // FRW_TRACE_ROUNDS=1: per-round queue lengths and stage times on stderr
   const bool trace = std::getenv("FRW_TRACE_ROUNDS") != nullptr;
-  if (trace) cudaEventCreate(&ev.a0);
-  cudaEvent_t t0 = ev.t0, t1 = ev.t1, m0 = ev.m0, m1 = ev.m1, a0 = ev.a0;
+  cudaEventCreate(&ev.a0);
+  cudaEventCreate(&ev.c0);
+  cudaEvent_t t0 = ev.t0, t1 = ev.t1, m0 = ev.m0, m1 = ev.m1, a0 = ev.a0, c0 = ev.c0;
   cudaEventRecord(t0, ctx->stream);
 
   const DStruct s = make_dstruct(E);
@@ -5115,20 +5156,32 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   // run-to-completion threshold (active walks); FRW_TAIL_WALKS overrides
   // (148 * 1024 after the box-scan cells: C3/C5 +7-8% over 148 * 2048; 100K-200K
   // within 1%, tools/tail_sweep2.sh)
-  unsigned long long tail_threshold = static_cast<unsigned long long>(ctx->sm_count) * 1024;
-  if (const char* e = std::getenv("FRW_TAIL_WALKS")) tail_threshold = std::strtoull(e, nullptr, 10);
-  // tail kernel: k_tail by default; FRW_TAIL_KERNEL=flow selects the
-  // warp-specialised k_flow (C3/C5 within a few % either way)
+  // tail kernel: k_flow with its roles split by SM (C3 +16%, C5 +25%
+  // over k_tail); FRW_TAIL_KERNEL=tail selects k_tail, =flowwarp k_flow with roles by warp
   const char* tk = std::getenv("FRW_TAIL_KERNEL");
-  const bool use_flow = tk && std::strcmp(tk, "flow") == 0;
+  const bool use_flow = !tk || std::strncmp(tk, "flow", 4) == 0;
+  const bool flow_by_sm = use_flow && !(tk && std::strcmp(tk, "flowwarp") == 0);
+  // threshold: k_flow runs hops about as efficiently as the rounds, so it takes over once
+  // the rounds' slices stop filling the device (148 * 3072; 300K-700K within 2%,
+  // tools/ab_flow3.sh); k_tail 148 * 1024 (100K-200K within 1%, tools/tail_sweep2.sh)
+  unsigned long long tail_threshold =
+      static_cast<unsigned long long>(ctx->sm_count) * (use_flow ? 3072 : 1024);
+  if (const char* e = std::getenv("FRW_TAIL_WALKS")) tail_threshold = std::strtoull(e, nullptr, 10);
+  // k_flow's share of transition SMs: the share of the rounds' time spent in k_spawn,
+  // k_advance and k_compile (what its transition role does), measured on this run's own
+  // rounds, times kFlowAdvBias; FRW_FLOW_ADV_PCT overrides (percent of the SMs)
+  double adv_ms_acc = 0, mwk_ms_acc = 0;
+  constexpr double kFlowAdvBias = 1.05;
+  P.flow_adv = 0;
+  P.flow_sms = 0;
   // time slices of the wavefront rounds: a MicroWalk hop
   // gets kMwSlice super-steps per k_mw visit and a walk kAdvSlice
   // transitions per k_advance visit, then continues next round, so a round
   // costs its throughput, not its longest hop; FRW_MW_SLICE /
-  // FRW_ADV_SLICE override (0: unlimited).  k_flow takes no carried hops.
-  P.mw_slice = use_flow || P.mode == FRW_MODE_FDM ? 0 : kMwSlice;
+  // FRW_ADV_SLICE override (0: unlimited).
+  P.mw_slice = P.mode == FRW_MODE_FDM ? 0 : kMwSlice;
   P.adv_slice = kAdvSlice;
-  if (const char* e = std::getenv("FRW_MW_SLICE")) P.mw_slice = use_flow ? 0 : std::atoi(e);
+  if (const char* e = std::getenv("FRW_MW_SLICE")) P.mw_slice = std::atoi(e);
   if (const char* e = std::getenv("FRW_ADV_SLICE")) P.adv_slice = std::atoi(e);
   {  // the box slices are dynamic shared memory beyond the 48 KB default
     static std::once_flag once;
@@ -5153,22 +5206,33 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     int* aq_out = E.aq[(round + 1) & 1];
     int* mq_in = E.mq[round & 1];
     int* mq_next = E.mq[(round + 1) & 1];
-    if (trace) cudaEventRecord(a0, ctx->stream);
+    cudaEventRecord(a0, ctx->stream);
     k_spawn<<<grid, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in);
     if (tail) {
       cudaEventRecord(m0, ctx->stream);
       const int tb = ctx->sm_count * kTailBlocks;  // persistent, one wave
       if (use_flow) {
+        if (flow_by_sm) {
+          double f = adv_ms_acc + mwk_ms_acc > 0
+                         ? kFlowAdvBias * adv_ms_acc / (adv_ms_acc + mwk_ms_acc)
+                         : 0.4;
+          if (const char* e = std::getenv("FRW_FLOW_ADV_PCT")) f = std::atof(e) / 100.0;
+          f = std::min(0.75, std::max(0.15, f));
+          P.flow_sms = std::max(1, ctx->sm_count / 2);  // SM pairs
+          P.flow_adv = std::max(1, static_cast<int>(f * P.flow_sms + 0.5));
+          if (trace)
+            std::fprintf(stderr, "  k_flow: %d of %d SM pairs run transitions\n", P.flow_adv, P.flow_sms);
+        }
         // rings start empty (a run that stopped on an error may leave entries)
         FRW_CUDA(ctx, cudaMemsetAsync(E.ring_a, 0xFF, 4ull * (E.ring_mask + 1), ctx->stream));
         FRW_CUDA(ctx, cudaMemsetAsync(E.ring_m, 0xFF, 4ull * (E.ring_mask + 1), ctx->stream));
         k_flow_init<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
         if (P.rng == FRW_RNG_PHILOX)
           k_flow<FRW_RNG_PHILOX><<<tb, 256, kBoxSmem256, ctx->stream>>>(
-              s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
+              s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, mq_in, E.ring_a, E.ring_m, E.ring_mask);
         else
           k_flow<FRW_RNG_SPLITMIX_PARITY><<<tb, 256, kBoxSmem256, ctx->stream>>>(
-              s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, E.ring_a, E.ring_m, E.ring_mask);
+              s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, mq_in, E.ring_a, E.ring_m, E.ring_mask);
       } else if (P.rng == FRW_RNG_PHILOX)
         k_tail<FRW_RNG_PHILOX><<<tb, 256, kBoxSmem256, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M,
                                                            aq_in, mq_in);
@@ -5182,6 +5246,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       // microwalk_transit_lazy)
       cudaEventRecord(m0, ctx->stream);
       k_compile<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(s, P, Wc, E.d_cnt, M, E.cq, mq_in);
+      cudaEventRecord(c0, ctx->stream);
       if (P.mode == FRW_MODE_FDM) {
         const FdmQueue Q{mq_in, &E.d_cnt->qlen, &E.d_cnt->qhead, aq_out, &E.d_cnt->a2len};
         if (int rc = launch_fdm(ctx, E, s, P, E.d_cnt, Q)) {
@@ -5224,6 +5289,13 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         mw_ms += f * ms;
       } else {
         mw_ms += ms;
+      }
+      if (!tail) {  // the rounds' time split, for k_flow's role shares
+        float ams = 0, cms = 0;
+        cudaEventElapsedTime(&ams, a0, m0);
+        cudaEventElapsedTime(&cms, m0, c0);
+        adv_ms_acc += ams + cms;
+        mwk_ms_acc += ms - cms;
       }
       if (trace) {
         float ams = 0;
