@@ -2838,11 +2838,156 @@ __global__ void k_flow_init(DCounters* C) {
   C->flive = C->alen + C->qlen;  // ACTIVE walks and the hops carried over from the last round
 }
 
-// Roles by SM instead of by warp (DParams::flow_adv of the flow_sms SMs run
-// transitions, the others MicroWalk hops): an SM then fetches only its
+// Roles by SM instead of by warp (DParams::flow_adv of the flow_sms SM pairs
+// run transitions, the others MicroWalk hops): an SM then fetches only its
 // role's code -- k_tail's top stall is instruction fetch, its transition and
 // MicroWalk paths together are three times the 32 KB L1.5 instruction cache.
 
+// this SM's role: flow_adv of the flow_sms SM pairs run transitions, evenly
+// spread (SM ids 2t and 2t+1, one TPC, share a role: measured, mixed pairs
+// lose the instruction-cache benefit)
+__device__ __forceinline__ bool flow_sm_adv(const DParams& P) {
+  unsigned smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  const unsigned m = (smid >> 1) % static_cast<unsigned>(P.flow_sms);
+  return (m + 1) * P.flow_adv / P.flow_sms != m * P.flow_adv / P.flow_sms;
+}
+
+// the transition role: walks from the round's ACTIVE list, then from the
+// ACTIVE ring; one transition per pass until the walk needs a MicroWalk hop
+// (compiled here, pushed to the MicroWalk ring) or ends
+__device__ __forceinline__ void flow_adv_loop(const DStruct& s, const DSgf& T, const DParams& P,
+                                              const DSlots& W, WalkRec* recs, DCounters* C,
+                                              const DMiss& M, const int* aq, int* ring_a,
+                                              int* ring_m, unsigned mask) {
+  const unsigned long long alen = C->alen;
+  long long cyc_busy = 0;  // warp-uniform clock64 spans with work in hand
+  AdvLane A;
+  bool have = false, first = true;
+  long long res = -1;  // reserved ACTIVE-ring index
+  for (;;) {
+    if (!have) {
+      if (first) {
+        const unsigned long long item = atomicAdd(&C->ahead, 1ull);
+        if (item < alen) {
+          adv_load(W, aq[item], A);
+          have = true;
+        } else {
+          first = false;
+        }
+      }
+      if (!have && !first) {
+        if (res < 0) res = static_cast<long long>(atomicAdd(&C->fah, 1ull));
+        const int v = ring_poll(ring_a, res, mask);
+        if (v >= 0) {
+          ring_a[res & mask] = -1;
+          __threadfence();
+          adv_load(W, v, A);
+          have = true;
+          res = -1;
+        }
+      }
+    }
+    if (!__any_sync(0xFFFFFFFFu, have)) {
+      if (flow_live(C) == 0) break;
+      __nanosleep(256);
+      continue;
+    }
+    const long long c0 = clock64();
+    if (have) {
+      const int r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
+      if (r == 2) {
+        ring_push(ring_m, &C->fmt, mask, A.slot);
+        have = false;
+      } else if (r == 1) {
+        atomicAdd(&C->flive, ~0ull);  // -1
+        have = false;
+      }
+    }
+    cyc_busy += clock64() - c0;
+  }
+  // T_MW: the busy cycles of the MicroWalk warps over those of all warps
+  if ((threadIdx.x & 31) == 0)
+    atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_busy));
+}
+
+// the MicroWalk role: the hops carried over from the last round, then jobs
+// from the MicroWalk ring, back to back (lanes refilled independently, as in
+// k_mw); surface exits go to the ACTIVE ring
+template <int RNG>
+__device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, const DSlots& W,
+                                             const AlphaTab& AT, const DirDelta* dd,
+                                             WalkRec* recs, DCounters* C, const int* mq,
+                                             int* ring_a, int* ring_m, unsigned mask,
+                                             uint64_t* bsm) {
+  const int n = P.n;
+  const unsigned long long qlen = C->qlen;
+  long long cyc_busy = 0;
+  const int cap = 1000 * n * n;  // microwalk.cpp:81
+  MwLane L;
+  L.gsteps = 0;
+  L.jumps = 0;
+  L.jsteps = 0;
+  L.cchg = 0;
+  bool have = false, firstm = qlen > 0;
+  long long res = -1;
+  for (;;) {
+    if (!have && firstm) {  // the hops carried over from the last round first
+      const unsigned long long item = atomicAdd(&C->qhead, 1ull);
+      if (item < qlen) {
+        const int q = mq[item];
+        mw_arm(W, q, q, n, L, bsm);
+        have = true;
+      } else {
+        firstm = false;
+      }
+    }
+    if (!have && !firstm) {
+      if (res < 0) res = static_cast<long long>(atomicAdd(&C->fmh, 1ull));
+      const int v = ring_poll(ring_m, res, mask);
+      if (v >= 0) {
+        ring_m[res & mask] = -1;
+        __threadfence();
+        mw_arm(W, v, v, n, L, bsm);
+        have = true;
+        res = -1;
+      }
+    }
+    if (!__any_sync(0xFFFFFFFFu, have)) {
+      if (flow_live(C) == 0) break;
+      __nanosleep(256);
+      continue;
+    }
+    const long long c0 = clock64();
+    if (have) {
+      int xdir = 0;
+      const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
+      if (code != MW_GO) {
+        have = false;
+        if (code == MW_SURFACE) {
+          mw_exit(W, n, L, xdir);
+          ring_push(ring_a, &C->fat, mask, L.slot);
+        } else {
+          if (code == MW_COND)
+            mw_conductor_exit(W, recs, C, L, xdir);
+          else {
+            set_err(C, FRW_ESTEPCAP);
+            W.state[L.slot] = S_FREE;
+          }
+          atomicAdd(&C->flive, ~0ull);  // -1
+        }
+      }
+    }
+    cyc_busy += clock64() - c0;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&C->tail_mw_cyc, static_cast<unsigned long long>(cyc_busy));
+    atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_busy));
+  }
+  flush_mw_stats(C, L);
+}
+
+// one kernel, both roles: by SM pair (P.flow_sms > 0) or by warp
 template <int RNG>
 __global__ void __launch_bounds__(256, kTailBlocks)
     k_flow(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
@@ -2853,134 +2998,42 @@ __global__ void __launch_bounds__(256, kTailBlocks)
   __shared__ JumpSmem jsm;
   DJump J;
   const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
-  const int n = P.n;
-  const unsigned long long alen = C->alen;
-  const unsigned long long qlen = C->qlen;
-  long long cyc_busy = 0;  // warp-uniform clock64 spans with work in hand
-  // role by SM pair (SM ids 2t and 2t+1, one TPC: measured, mixed pairs lose the
-  // instruction-cache benefit): flow_adv of the flow_sms pairs, evenly spread
-  // (flow_sms = 0: roles by warp, kFlowAdvWarps of the CTA's 8)
-  bool adv_role = (threadIdx.x >> 5) < kFlowAdvWarps;
-  if (P.flow_sms > 0) {
-    unsigned smid;
-    asm("mov.u32 %0, %%smid;" : "=r"(smid));
-    const unsigned m = (smid >> 1) % static_cast<unsigned>(P.flow_sms);
-    adv_role = (m + 1) * P.flow_adv / P.flow_sms != m * P.flow_adv / P.flow_sms;
-  }
-  if (adv_role) {
-    // ---- advance warp ----
-    AdvLane A;
-    bool have = false, first = true;
-    long long res = -1;  // reserved ACTIVE-ring index
-    for (;;) {
-      if (!have) {
-        if (first) {
-          const unsigned long long item = atomicAdd(&C->ahead, 1ull);
-          if (item < alen) {
-            adv_load(W, aq[item], A);
-            have = true;
-          } else {
-            first = false;
-          }
-        }
-        if (!have && !first) {
-          if (res < 0) res = static_cast<long long>(atomicAdd(&C->fah, 1ull));
-          const int v = ring_poll(ring_a, res, mask);
-          if (v >= 0) {
-            ring_a[res & mask] = -1;
-            __threadfence();
-            adv_load(W, v, A);
-            have = true;
-            res = -1;
-          }
-        }
-      }
-      if (!__any_sync(0xFFFFFFFFu, have)) {
-        if (flow_live(C) == 0) break;
-        __nanosleep(256);
-        continue;
-      }
-      const long long c0 = clock64();
-      if (have) {
-        const int r = advance_once<false, false>(s, T, P, W, recs, C, M, nullptr, A);
-        if (r == 2) {
-          ring_push(ring_m, &C->fmt, mask, A.slot);
-          have = false;
-        } else if (r == 1) {
-          atomicAdd(&C->flive, ~0ull);  // -1
-          have = false;
-        }
-      }
-      cyc_busy += clock64() - c0;
-    }
-    // T_MW: the busy cycles of the MicroWalk warps over those of all warps
-    if ((threadIdx.x & 31) == 0)
-      atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_busy));
-  } else {
-    // ---- MicroWalk warp ----
-    const int cap = 1000 * n * n;  // microwalk.cpp:81
-    MwLane L;
-    L.gsteps = 0;
-    L.jumps = 0;
-    L.jsteps = 0;
-    L.cchg = 0;
-    bool have = false, firstm = qlen > 0;
-    long long res = -1;
-    for (;;) {
-      if (!have && firstm) {  // the hops carried over from the last round first
-        const unsigned long long item = atomicAdd(&C->qhead, 1ull);
-        if (item < qlen) {
-          const int q = mq[item];
-          mw_arm(W, q, q, n, L, frw_dsm);
-          have = true;
-        } else {
-          firstm = false;
-        }
-      }
-      if (!have && !firstm) {
-        if (res < 0) res = static_cast<long long>(atomicAdd(&C->fmh, 1ull));
-        const int v = ring_poll(ring_m, res, mask);
-        if (v >= 0) {
-          ring_m[res & mask] = -1;
-          __threadfence();
-          mw_arm(W, v, v, n, L, frw_dsm);
-          have = true;
-          res = -1;
-        }
-      }
-      if (!__any_sync(0xFFFFFFFFu, have)) {
-        if (flow_live(C) == 0) break;
-        __nanosleep(256);
-        continue;
-      }
-      const long long c0 = clock64();
-      if (have) {
-        int xdir = 0;
-        const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
-        if (code != MW_GO) {
-          have = false;
-          if (code == MW_SURFACE) {
-            mw_exit(W, n, L, xdir);
-            ring_push(ring_a, &C->fat, mask, L.slot);
-          } else {
-            if (code == MW_COND)
-              mw_conductor_exit(W, recs, C, L, xdir);
-            else {
-              set_err(C, FRW_ESTEPCAP);
-              W.state[L.slot] = S_FREE;
-            }
-            atomicAdd(&C->flive, ~0ull);  // -1
-          }
-        }
-      }
-      cyc_busy += clock64() - c0;
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd(&C->tail_mw_cyc, static_cast<unsigned long long>(cyc_busy));
-      atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_busy));
-    }
-    flush_mw_stats(C, L);
-  }
+  const bool adv_role = P.flow_sms > 0 ? flow_sm_adv(P) : (threadIdx.x >> 5) < kFlowAdvWarps;
+  if (adv_role)
+    flow_adv_loop(s, T, P, W, recs, C, M, aq, ring_a, ring_m, mask);
+  else
+    flow_mw_loop<RNG>(P, J, W, AT, dd, recs, C, mq, ring_a, ring_m, mask, frw_dsm);
+}
+
+// The two roles as two kernels, launched side by side on two streams, each
+// with the registers and shared memory of its role (the transition kernel as
+// k_advance: 4 x 256 threads per SM and no tables; the MicroWalk kernel as
+// k_mw: 2 x 512 threads per SM at 64 registers with the jump tables and box
+// slices).  A CTA that lands on an SM of the other role exits at once, so each
+// SM fills up with CTAs of its own role; CTAs left over once their SMs are
+// full run (and exit) when the flow has ended.
+#ifndef FRW_FLOWADV_MINB
+#define FRW_FLOWADV_MINB 4
+#endif
+__global__ void __launch_bounds__(256, FRW_FLOWADV_MINB)
+    k_flow_adv(DStruct s, DSgf T, DParams P, DSlots W, WalkRec* recs, DCounters* C, DMiss M,
+               const int* aq, int* ring_a, int* ring_m, unsigned mask) {
+  if (!flow_sm_adv(P) || flow_live(C) == 0) return;
+  flow_adv_loop(s, T, P, W, recs, C, M, aq, ring_a, ring_m, mask);
+}
+
+template <int RNG>
+__global__ void __launch_bounds__(512, 2)
+    k_flow_mw(DStruct s, DParams P, DSlots W, WalkRec* recs, DCounters* C, const int* mq,
+              int* ring_a, int* ring_m, unsigned mask) {
+  if (flow_sm_adv(P) || flow_live(C) == 0) return;
+  __shared__ double alpha_sm[PMAX * PMAX + 1];  // used when P <= PMAX
+  __shared__ DirDelta dd[6];
+  extern __shared__ uint64_t frw_dsm[];  // kBoxSm box slices per thread (mw_arm)
+  __shared__ JumpSmem jsm;
+  DJump J;
+  const AlphaTab AT = setup_smem_tables(s, alpha_sm, dd, P.jump, jsm, &J);
+  flow_mw_loop<RNG>(P, J, W, AT, dd, recs, C, mq, ring_a, ring_m, mask, frw_dsm);
 }
 
 // ---- single transits over structure cubes (the single-transit API) --------
@@ -3657,6 +3710,8 @@ struct Engine {
   int* ring_a = nullptr;  // k_flow rings of walk slots (-1 = empty entry)
   int* ring_m = nullptr;
   unsigned ring_mask = 0;
+  cudaStream_t flow_stream = nullptr;  // the MicroWalk kernel of a two-kernel flow
+  cudaEvent_t flow_fork = nullptr, flow_join = nullptr;
   // reduction scratch; `pack` holds the last call's tally (tally_n doubles)
   // for frw_tally_allreduce
   double* pack = nullptr;
@@ -3712,6 +3767,11 @@ void free_slots(Engine& E) {
   cudaFree(E.ring_m);
   E.ring_a = E.ring_m = nullptr;
   E.ring_mask = 0;
+  if (E.flow_stream) cudaStreamDestroy(E.flow_stream);
+  if (E.flow_fork) cudaEventDestroy(E.flow_fork);
+  if (E.flow_join) cudaEventDestroy(E.flow_join);
+  E.flow_stream = nullptr;
+  E.flow_fork = E.flow_join = nullptr;
   cudaFree(E.M.retry);
   cudaFree(E.M.pend);
   cudaFree(E.M.park);
@@ -5161,6 +5221,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   const char* tk = std::getenv("FRW_TAIL_KERNEL");
   const bool use_flow = !tk || std::strncmp(tk, "flow", 4) == 0;
   const bool flow_by_sm = use_flow && !(tk && std::strcmp(tk, "flowwarp") == 0);
+  // =flow2: the two roles as two kernels on two streams (k_flow_adv, k_flow_mw)
+  const bool flow_split = flow_by_sm && tk && std::strcmp(tk, "flow2") == 0;
   // threshold: k_flow runs hops about as efficiently as the rounds, so it takes over once
   // the rounds' slices stop filling the device (148 * 3072; 300K-700K within 2%,
   // tools/ab_flow3.sh); k_tail 148 * 1024 (100K-200K within 1%, tools/tail_sweep2.sh)
@@ -5192,6 +5254,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       cudaFuncSetAttribute(k_tail<FRW_RNG_SPLITMIX_PARITY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem256);
       cudaFuncSetAttribute(k_flow<FRW_RNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem256);
       cudaFuncSetAttribute(k_flow<FRW_RNG_SPLITMIX_PARITY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem256);
+      cudaFuncSetAttribute(k_flow_mw<FRW_RNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem512);
+      cudaFuncSetAttribute(k_flow_mw<FRW_RNG_SPLITMIX_PARITY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSmem512);
     });
   }
   bool tail = false;
@@ -5227,7 +5291,27 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
         FRW_CUDA(ctx, cudaMemsetAsync(E.ring_a, 0xFF, 4ull * (E.ring_mask + 1), ctx->stream));
         FRW_CUDA(ctx, cudaMemsetAsync(E.ring_m, 0xFF, 4ull * (E.ring_mask + 1), ctx->stream));
         k_flow_init<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
-        if (P.rng == FRW_RNG_PHILOX)
+        if (flow_split) {
+          if (!E.flow_stream) {
+            FRW_CUDA(ctx, cudaStreamCreateWithFlags(&E.flow_stream, cudaStreamNonBlocking));
+            FRW_CUDA(ctx, cudaEventCreateWithFlags(&E.flow_fork, cudaEventDisableTiming));
+            FRW_CUDA(ctx, cudaEventCreateWithFlags(&E.flow_join, cudaEventDisableTiming));
+          }
+          FRW_CUDA(ctx, cudaEventRecord(E.flow_fork, ctx->stream));
+          FRW_CUDA(ctx, cudaStreamWaitEvent(E.flow_stream, E.flow_fork, 0));
+          // more CTAs than fit: those landing on SMs of the other role exit at once
+          const int ga = ctx->sm_count * FRW_FLOWADV_MINB * 2, gm = ctx->sm_count * 2 * 2;
+          k_flow_adv<<<ga, 256, 0, ctx->stream>>>(s, T, P, Wc, E.recs, E.d_cnt, M, aq_in,
+                                                  E.ring_a, E.ring_m, E.ring_mask);
+          if (P.rng == FRW_RNG_PHILOX)
+            k_flow_mw<FRW_RNG_PHILOX><<<gm, 512, kBoxSmem512, E.flow_stream>>>(
+                s, P, Wc, E.recs, E.d_cnt, mq_in, E.ring_a, E.ring_m, E.ring_mask);
+          else
+            k_flow_mw<FRW_RNG_SPLITMIX_PARITY><<<gm, 512, kBoxSmem512, E.flow_stream>>>(
+                s, P, Wc, E.recs, E.d_cnt, mq_in, E.ring_a, E.ring_m, E.ring_mask);
+          FRW_CUDA(ctx, cudaEventRecord(E.flow_join, E.flow_stream));
+          FRW_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, E.flow_join, 0));
+        } else if (P.rng == FRW_RNG_PHILOX)
           k_flow<FRW_RNG_PHILOX><<<tb, 256, kBoxSmem256, ctx->stream>>>(
               s, T, P, Wc, E.recs, E.d_cnt, M, aq_in, mq_in, E.ring_a, E.ring_m, E.ring_mask);
         else
@@ -5305,6 +5389,10 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
                      "done %llu misses %llu spawn+advance %.3f ms %s %.3f ms\n",
                      round, c.alen, c.qlen, c.a2len, c.q2len, c.dqlen, c.done, c.nmiss, ams,
                      tail ? "tail" : "mw", ms);
+        if (tail)  // busy warp-cycles (work in hand) by role, in ms of one warp at the SM clock
+          std::fprintf(stderr, "  tail busy warp-ms: transitions %.1f MicroWalk %.1f\n",
+                       (c.tail_all_cyc - c.tail_mw_cyc) / (ctx->sm_clock_khz * 1.0),
+                       c.tail_mw_cyc / (ctx->sm_clock_khz * 1.0));
       }
     }
     if (c.chk_line) {
