@@ -94,8 +94,10 @@ def test_walk_offsets_and_slots_are_irrelevant(gpu_ctx, oracle):
 
 @pytest.mark.parametrize("mode", sorted(MODES))
 def test_tail_kernels_agree_bitwise(gpu_ctx, oracle, monkeypatch, mode):
-    """k_tail (one lane per walk) and k_flow (warp-specialised, ring
-    handoffs) run the same walks to the same records, whatever the order"""
+    """k_tail (one lane per walk) and k_flow (transition and MicroWalk roles
+    with ring handoffs: roles by SM pair -- the default --, by warp, or as two
+    kernels on two streams) run the same walks to the same records, whatever
+    the order"""
     sc = _scene(c3_structure())
     upload_scene(gpu_ctx, sc)
     gpu_ctx.sgf_clear()
@@ -103,13 +105,15 @@ def test_tail_kernels_agree_bitwise(gpu_ctx, oracle, monkeypatch, mode):
     p = walk_params(sc, grid_n=24, seed=9, rng=PHILOX, mode=MODES[mode])
     monkeypatch.setenv("FRW_TAIL_WALKS", str(1 << 30))  # everything after round 0
     out = {}
-    for k in ("tail", "flow"):
+    for k in ("tail", "flow", "flowwarp", "flow2"):
         monkeypatch.setenv("FRW_TAIL_KERNEL", k)
         out[k] = gpu_ctx.run_walks(p, sc.master_slot(), 0, 50_000, solve)
-    (ta, a), (tb, b) = out["tail"], out["flow"]
-    for f in ("slot", "weight", "aborted", "mw_steps", "cached", "microwalk"):
-        assert np.array_equal(a[f], b[f]), f
-    assert np.array_equal(ta["sum"], tb["sum"]) and np.array_equal(ta["landed"], tb["landed"])
+    ta, a = out["tail"]
+    for k in ("flow", "flowwarp", "flow2"):
+        tb, b = out[k]
+        for f in ("slot", "weight", "aborted", "mw_steps", "cached", "microwalk"):
+            assert np.array_equal(a[f], b[f]), (k, f)
+        assert np.array_equal(ta["sum"], tb["sum"]) and np.array_equal(ta["landed"], tb["landed"]), k
 
 
 def test_hop_cap_aborts_into_ground(gpu_ctx, oracle):
