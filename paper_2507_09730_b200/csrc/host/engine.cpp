@@ -522,6 +522,44 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   // host thread folds wave k in walk order; chunks launched after the
   // stopping rule fired inside an earlier one are discarded, so the result
   // equals the sequential fold for any number of devices.
+  //
+  // Under a stopping rule with chunk tallies (a fold of ~1 ms per wave) the
+  // fold runs before the next wave is sized instead: no speculative wave is
+  // thrown away, and once the walk count the rule needs is in sight
+  // (SE ~ 1/sqrt(walks): walks * (se / (tol |C|))^2 for the entries the rule
+  // tests) the wave is cut to reach it with a 3% margin, in whole reference
+  // batches and not below kMinWave.  Only the partition of the one walk
+  // sequence into device calls changes: the walks, the fold order and the
+  // batch at which the rule fires are the same.
+  const bool seq_fold = use_chunks && cfg_.min_walks < cfg_.max_walks;
+  constexpr int64_t kMinWave = 1 << 19;
+  auto walks_needed = [&]() -> double {
+    const double inf = std::numeric_limits<double>::infinity();
+    if (walks < 2) return inf;
+    auto need = [&](size_t k) {
+      const auto [v, se] = estimate(k);
+      if (!(std::fabs(v) > 0)) return inf;
+      const double r = se / (cfg_.rel_std_tol * std::fabs(v));
+      return static_cast<double>(walks) * r * r;
+    };
+    double n = need(master);
+    if (cfg_.all_couplings_rule) {
+      for (size_t k = 0; k + 1 < nslots; ++k)
+        if (static_cast<int>(k) != master) n = std::max(n, need(k));
+      return n;
+    }
+    size_t big = nslots;
+    double big_abs = 0;
+    for (size_t k = 0; k < nslots; ++k) {
+      if (static_cast<int>(k) == master) continue;
+      const double a = std::fabs(sum[k] / static_cast<double>(walks));
+      if (a > big_abs) {
+        big_abs = a;
+        big = k;
+      }
+    }
+    return big == nslots ? n : std::max(n, need(big));
+  };
   const int64_t max_walks = cfg_.max_walks;
   int64_t launched = 0;
   int cur = 0;
@@ -566,9 +604,23 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
   };
   for (;;) {
     int64_t wave = 0;
+    int64_t lane_batch = dev_batch;
+    if (seq_fold && launched == 0) {
+      // a short first wave gives the estimate the later waves are sized from
+      const int64_t first = std::max<int64_t>(kMinWave, cfg_.min_walks);
+      lane_batch = std::min<int64_t>(dev_batch, (first + batch - 1) / batch * batch);
+    } else if (seq_fold && walks >= static_cast<uint64_t>(std::max<long>(cfg_.min_walks, 1))) {
+      // (the fold of every earlier wave is complete here)
+      const double need = walks_needed() * 1.03 - static_cast<double>(launched);
+      const double per_lane = need / static_cast<double>(lanes.size());
+      if (per_lane < static_cast<double>(dev_batch)) {
+        const int64_t want = std::max<int64_t>(kMinWave, static_cast<int64_t>(std::ceil(std::max(per_lane, 0.0))));
+        lane_batch = std::min<int64_t>(dev_batch, (want + batch - 1) / batch * batch);
+      }
+    }
     for (Lane& L : lanes) {
       L.begin = launched;
-      L.count = launched < max_walks ? std::min<int64_t>(dev_batch, max_walks - launched) : 0;
+      L.count = launched < max_walks ? std::min<int64_t>(lane_batch, max_walks - launched) : 0;
       launched += L.count;
       wave += L.count;
     }
@@ -605,6 +657,13 @@ CapacitanceResult Engine::extract(int /*threads: walks run on the device*/) {
         cparts.emplace_back(L.dt, L.count);
       }
     const int fb = cur;
+    if (seq_fold) {
+      for (size_t i = 0; i < cparts.size() && !converged; ++i)
+        fold_chunks(*cparts[i].first, fb, cparts[i].second);
+      if (converged) break;
+      cur ^= 1;
+      continue;
+    }
     worker = std::thread([&fold, &fold_chunks, &converged, use_chunks, parts, cparts, fb] {
       for (size_t i = 0; i < parts.size(); ++i) {
         if (use_chunks)
