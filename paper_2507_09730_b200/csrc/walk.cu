@@ -2911,6 +2911,9 @@ __device__ __forceinline__ void flow_adv_loop(const DStruct& s, const DSgf& T, c
     atomicAdd(&C->tail_all_cyc, static_cast<unsigned long long>(cyc_busy));
 }
 
+#ifndef FRW_FLOW_POLL
+#define FRW_FLOW_POLL 4
+#endif
 // the MicroWalk role: the hops carried over from the last round, then jobs
 // from the MicroWalk ring, back to back (lanes refilled independently, as in
 // k_mw); surface exits go to the ACTIVE ring
@@ -2931,8 +2934,14 @@ __device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, c
   L.cchg = 0;
   bool have = false, firstm = qlen > 0;
   long long res = -1;
+  // a warp with hops in hand lets its idle lanes look for a job only every
+  // FRW_FLOW_POLL-th pass: the ring poll is a dependent L2 round trip that the
+  // stepping lanes of the warp would wait out on every super-step
+  unsigned pass = 0;
+  bool busy = false;
   for (;;) {
-    if (!have && firstm) {  // the hops carried over from the last round first
+    const bool look = !busy || (pass++ % FRW_FLOW_POLL) == 0;
+    if (!have && firstm && look) {  // the hops carried over from the last round first
       const unsigned long long item = atomicAdd(&C->qhead, 1ull);
       if (item < qlen) {
         const int q = mq[item];
@@ -2942,7 +2951,7 @@ __device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, c
         firstm = false;
       }
     }
-    if (!have && !firstm) {
+    if (!have && !firstm && look) {
       if (res < 0) res = static_cast<long long>(atomicAdd(&C->fmh, 1ull));
       const int v = ring_poll(ring_m, res, mask);
       if (v >= 0) {
@@ -2953,7 +2962,8 @@ __device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, c
         res = -1;
       }
     }
-    if (!__any_sync(0xFFFFFFFFu, have)) {
+    busy = __any_sync(0xFFFFFFFFu, have);
+    if (!busy) {
       if (flow_live(C) == 0) break;
       __nanosleep(256);
       continue;
