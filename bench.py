@@ -380,7 +380,7 @@ def _walk_roofline(stats, walks, walks_per_s, smem_peak, prof, name):
     bpw = (B_STEP * taken + B_JUMP * stats["mw_jumps"] + B_INV * inv) / walks + B_FIRST
     ach = bpw * walks_per_s / 1e9
     pr = None
-    for key in ((name, "k_tail"), ("C3", "k_tail")):
+    for key in ((name, "k_flow"), ("C3", "k_flow"), (name, "k_tail"), ("C3", "k_tail")):
         if key in prof:
             pr = prof[key]
             break
