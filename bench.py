@@ -514,14 +514,16 @@ def walk_c4(args, rank, world, dist, torch, smem_peak, prof, cpu):
     kw = dict(mode="HYBRID-MW", device=torch.cuda.current_device(), tol=0.01,
               all_couplings=True, min_walks=4096, max_walks=200_000_000)
     frwcap.sgf_cache_clear()
-    frwcap.extract_json(doc, mode="HYBRID-MW", device=torch.cuda.current_device(),
-                        min_walks=1 << 20, max_walks=1 << 20, seed=77)  # warm the table
-    for sd in (78, 79):  # two more warm-up calls on the steady-state path
+    # three warm-up calls: the first (2^22 walks, the timed run's wave size) fills the SGF
+    # table and grows the slot pool to its steady-state size
+    for sd, w in ((77, 1 << 22), (78, 1 << 20), (79, 1 << 20)):
         frwcap.extract_json(doc, mode="HYBRID-MW", device=torch.cuda.current_device(),
-                            min_walks=1 << 20, max_walks=1 << 20, seed=sd)
+                            min_walks=w, max_walks=w, seed=sd)
+    miss0 = frwcap.sgf_cache_stats()["misses"]
     t0 = time.perf_counter()
     r = frwcap.extract_json(doc, seed=5, **kw)
     wall = time.perf_counter() - t0
+    misses_timed = frwcap.sgf_cache_stats()["misses"] - miss0
     w = r["walks"]
     st = _sum_stats([r])
     ids = [t["conductor_id"] for t in r["terminals"]]
@@ -535,7 +537,8 @@ def walk_c4(args, rank, world, dist, torch, smem_peak, prof, cpu):
                    "d2h_bytes_per_step": -(-w // 1024) * 8 * (3 * len(ids) + 12)},
            "capacitance_aF": {str(i): round(t["capacitance_farads"] * 1e18, 4)
                               for i, t in zip(ids, r["terminals"])},
-           "warmup": 3, "sgf_table": "warm (three 2^20-walk warm-up calls, the first fills it)"}
+           "warmup": 3, "sgf_table": "warm (three warm-up calls of 2^22, 2^20, 2^20 walks)",
+           "sgf_misses_in_timed_run": misses_timed}
     out["roofline"] = _walk_roofline(st, w, out["value"], smem_peak, prof, "C4")
     if cpu:
         with tempfile.TemporaryDirectory() as td:
@@ -553,7 +556,7 @@ def walk_c5(args, rank, world, dist, torch, smem_peak, prof, cpu):
     master one walk sequence split into contiguous ranges over the ranks
     (dist.extract_sharded: frw_run_walks per range, one frw_tally_allreduce
     per master over NCCL).  Device and wall time max over ranks.  A warm-up
-    pass of 2^18 walks per master fills the SGF table."""
+    pass of 2^20 walks per master fills the SGF table."""
     import paper_2507_09730_b200.frwcap as frwcap
     from paper_2507_09730_b200 import dist as pdist
     from paper_2507_09730_b200.workloads import c5_structure
@@ -567,7 +570,10 @@ def walk_c5(args, rank, world, dist, torch, smem_peak, prof, cpu):
     for mid in masters:
         c5["master"] = mid
         docs[mid] = json.dumps(c5)
-        pdist.extract_sharded(docs[mid], 1 << 18, seed=50_000 + mid, **kw)
+        pdist.extract_sharded(docs[mid], 1 << 20, seed=50_000 + mid, **kw)
+    # (one call at the timed size: the slot pool grows to its steady-state size)
+    pdist.extract_sharded(docs[masters[0]], per_master, seed=60_000, **kw)
+    miss0 = frwcap.sgf_cache_stats()["misses"]
     if dist is not None:
         dist.barrier()
     dev_s = wall_s = 0.0
@@ -598,7 +604,8 @@ def walk_c5(args, rank, world, dist, torch, smem_peak, prof, cpu):
            "e2e": {"value": total / wall_s, "unit": "walks/s",
                    "h2d_bytes_per_step": sum(len(d) for d in docs.values()),
                    "d2h_bytes_per_step": 8 * len(masters) * (3 * 201 + 12)},
-           "sgf_table": "warm (2^18 walks per master first)", "rows": rows}
+           "sgf_table": "warm (2^20 walks per master first, and one call at the timed size)",
+           "sgf_misses_in_timed_run": frwcap.sgf_cache_stats()["misses"] - miss0, "rows": rows}
     out["roofline"] = _walk_roofline(st, total, out["value"], smem_peak, prof, "C5")
     if cpu:
         with tempfile.TemporaryDirectory() as td:

@@ -5243,6 +5243,8 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
   // k_advance and k_compile (what its transition role does), measured on this run's own
   // rounds, times kFlowAdvBias; FRW_FLOW_ADV_PCT overrides (percent of the SMs)
   double adv_ms_acc = 0, mwk_ms_acc = 0;
+  constexpr unsigned long long kFlowMinWalks = 8192;
+  unsigned long long next_live = 0;  // walks entering the next pass of the loop
   constexpr double kFlowAdvBias = 1.05;
   P.flow_adv = 0;
   P.flow_sms = 0;
@@ -5285,7 +5287,11 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     if (tail) {
       cudaEventRecord(m0, ctx->stream);
       const int tb = ctx->sm_count * kTailBlocks;  // persistent, one wave
-      if (use_flow) {
+      // a small batch (the parked walks of a miss cycle, a short call) is latency-bound:
+      // k_tail's one lane per walk has no handoffs (2048 walks: 5.9 ms against 8.4 ms;
+      // equal at 16K; the flow wins from there: 131K walks 10.2 against 13.0 ms,
+      // tools/small_calls.py)
+      if (use_flow && next_live > kFlowMinWalks) {
         if (flow_by_sm) {
           double f = adv_ms_acc + mwk_ms_acc > 0
                          ? kFlowAdvBias * adv_ms_acc / (adv_ms_acc + mwk_ms_acc)
@@ -5446,6 +5452,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
       upd.nmiss = 0;
       upd.npark = 0;
       upd.alen = c.a2len + c.npark;
+      next_live = upd.alen + c.q2len;
       upd.ahead = 0;
       upd.a2len = 0;
       upd.qlen = c.q2len;  // the carried MicroWalk hops open the next round's queue
@@ -5471,6 +5478,7 @@ int frw_run_walks(frw_ctx* ctx, const frw_walk_params* prm, int32_t master, uint
     // few walks left: run them to completion in one launch
     if (all_spawned && c.a2len + c.q2len <= tail_threshold && P.mode != FRW_MODE_FDM)
       tail = true;
+    next_live = c.a2len + c.q2len;
     k_round<<<1, 1, 0, ctx->stream>>>(E.d_cnt);
   }
   if (status == FRW_OK) {
