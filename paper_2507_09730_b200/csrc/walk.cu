@@ -2816,6 +2816,9 @@ __global__ void __launch_bounds__(256, kTailBlocks)
 #ifndef FRW_FLOW_ADV_WARPS
 #define FRW_FLOW_ADV_WARPS 3
 #endif
+#ifndef FRW_FLOW_SLEEP
+#define FRW_FLOW_SLEEP 256  // ns between the ring polls of a warp with nothing in hand
+#endif
 constexpr int kFlowAdvWarps = FRW_FLOW_ADV_WARPS;  // of the 8 warps of a CTA
 
 __device__ __forceinline__ int ring_poll(const int* ring, unsigned long long h, unsigned mask) {
@@ -2890,7 +2893,7 @@ __device__ __forceinline__ void flow_adv_loop(const DStruct& s, const DSgf& T, c
     }
     if (!__any_sync(0xFFFFFFFFu, have)) {
       if (flow_live(C) == 0) break;
-      __nanosleep(256);
+      __nanosleep(FRW_FLOW_SLEEP);
       continue;
     }
     const long long c0 = clock64();
@@ -2965,7 +2968,7 @@ __device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, c
     busy = __any_sync(0xFFFFFFFFu, have);
     if (!busy) {
       if (flow_live(C) == 0) break;
-      __nanosleep(256);
+      __nanosleep(FRW_FLOW_SLEEP);
       continue;
     }
     const long long c0 = clock64();
