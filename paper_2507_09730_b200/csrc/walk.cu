@@ -2873,6 +2873,7 @@ __device__ __forceinline__ void flow_adv_loop(const DStruct& s, const DSgf& T, c
       if (first) {
         const unsigned long long item = atomicAdd(&C->ahead, 1ull);
         if (item < alen) {
+          FRW_DCHECK(C, aq[item] >= 0 && aq[item] < W.S);
           adv_load(W, aq[item], A);
           have = true;
         } else {
@@ -2883,8 +2884,10 @@ __device__ __forceinline__ void flow_adv_loop(const DStruct& s, const DSgf& T, c
         if (res < 0) res = static_cast<long long>(atomicAdd(&C->fah, 1ull));
         const int v = ring_poll(ring_a, res, mask);
         if (v >= 0) {
+          FRW_DCHECK(C, v < W.S);
           ring_a[res & mask] = -1;
           __threadfence();
+          FRW_DCHECK(C, W.state[v] == S_ACTIVE);  // (after the fence: the producer's writes are visible)
           adv_load(W, v, A);
           have = true;
           res = -1;
@@ -2948,6 +2951,7 @@ __device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, c
       const unsigned long long item = atomicAdd(&C->qhead, 1ull);
       if (item < qlen) {
         const int q = mq[item];
+        FRW_DCHECK(C, q >= 0 && q < W.S);
         mw_arm(W, q, q, n, L, bsm);
         have = true;
       } else {
@@ -2958,6 +2962,7 @@ __device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, c
       if (res < 0) res = static_cast<long long>(atomicAdd(&C->fmh, 1ull));
       const int v = ring_poll(ring_m, res, mask);
       if (v >= 0) {
+        FRW_DCHECK(C, v < W.S);
         ring_m[res & mask] = -1;
         __threadfence();
         mw_arm(W, v, v, n, L, bsm);
@@ -2975,6 +2980,7 @@ __device__ __forceinline__ void flow_mw_loop(const DParams& P, const DJump& J, c
     if (have) {
       int xdir = 0;
       const int code = mw_superstep<RNG>(P, J, W, AT, dd, n, cap, L, &xdir);
+      FRW_DCHECK(C, node_ok(L.node, n));
       if (code != MW_GO) {
         have = false;
         if (code == MW_SURFACE) {
